@@ -1,0 +1,278 @@
+"""Python (ctypes) front end of the FP64 CPU oracle in ptucker_oracle.c.
+
+TEST INFRASTRUCTURE ONLY: only tests/, __graft_entry__.smoke() and bench.py
+(cpu_baseline / --impl reference) may import this module.  The product path
+(paper_1710_02261_b200/) never imports it, and it imports nothing from there.
+
+All arithmetic lives in ptucker_oracle.c (plain C, FP64, the paper's algorithm
+step by step; see that file's header for the P:<line> citations).  This module
+only marshals numpy arrays.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import subprocess
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SRC = os.path.join(_HERE, "ptucker_oracle.c")
+_LIB = os.path.join(_HERE, "liboracle.so")
+
+
+def build(force: bool = False) -> str:
+    """Compile the oracle with gcc (OpenMP for the paper's dynamic row loop)."""
+    if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
+        tmp = _LIB + f".tmp{os.getpid()}"
+        subprocess.check_call(["gcc", "-O2", "-fopenmp", "-fPIC", "-shared", "-o", tmp, _SRC, "-lm"])
+        os.replace(tmp, _LIB)
+    return _LIB
+
+
+_lib = None
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        _lib = C.CDLL(build())
+        P = C.c_void_p
+        i64, i32, f64, u64 = C.c_int64, C.c_int32, C.c_double, C.c_uint64
+        sig = {
+            "or_mix64": (u64, [u64]),
+            "or_rng_word": (u64, [u64, u64, u64]),
+            "or_uniform": (f64, [u64, u64, u64, C.c_int]),
+            "or_init": (None, [C.c_int, P, P, u64, C.c_int, P, P]),
+            "or_mode_index": (C.c_int, [C.c_int, i64, P, P, C.c_int, P, P]),
+            "or_partition": (None, [P, i64, C.c_int, P]),
+            "or_delta": (None, [C.c_int, P, P, P, P, P, C.c_int, P]),
+            "or_predict": (f64, [C.c_int, P, P, P, P, P]),
+            "or_row_system": (None, [C.c_int, P, P, P, P, P, P, C.c_int, P, P, i64, P, P, P]),
+            "or_solve": (C.c_int, [C.c_int, P, P, f64, P]),
+            "or_update_row": (C.c_int, [C.c_int, P, P, P, P, P, P, C.c_int, P, P, i64, f64]),
+            "or_update_mode": (C.c_int, [C.c_int, P, P, P, P, P, P, C.c_int, P, P, f64, C.c_int]),
+            "or_sse": (f64, [C.c_int, P, P, P, P, P, P, i64, C.c_int]),
+            "or_loss": (f64, [C.c_int, P, P, P, P, P, P, i64, f64, C.c_int]),
+            "or_thin_qr": (C.c_int, [i64, C.c_int, P, P]),
+            "or_core_mode_product": (None, [C.c_int, P, P, C.c_int, P]),
+            "or_orthogonalize": (C.c_int, [C.c_int, P, P, P, P, P]),
+        }
+        for name, (res, args) in sig.items():
+            fn = getattr(_lib, name)
+            fn.restype = res
+            fn.argtypes = args
+    return _lib
+
+
+def _p(a: np.ndarray):
+    assert a.flags["C_CONTIGUOUS"], "oracle arrays must be C-contiguous"
+    return a.ctypes.data_as(C.c_void_p)
+
+
+class Tensor:
+    """Observed entries Omega (Table 2): 0-based int32 coords (nnz x N),
+    FP64 values (FP32 inputs are widened exactly), dims I_1..I_N."""
+
+    def __init__(self, coords, vals, dims):
+        self.coords = np.ascontiguousarray(coords, dtype=np.int32)
+        self.vals = np.ascontiguousarray(vals, dtype=np.float64)
+        self.dims = np.ascontiguousarray(dims, dtype=np.int64)
+        self.N = int(self.dims.size)
+        self.nnz = int(self.vals.size)
+        assert self.coords.shape == (self.nnz, self.N)
+        self._index = {}
+
+    def mode_index(self, n: int):
+        """Stable per-mode CSR of Omega^(n)_{i_n}: (row_ptr[I_n+1], perm[nnz]), int64."""
+        if n not in self._index:
+            I = int(self.dims[n])
+            row_ptr = np.zeros(I + 1, np.int64)
+            perm = np.zeros(max(self.nnz, 1), np.int64)
+            rc = lib().or_mode_index(self.N, self.nnz, _p(self.coords), _p(self.dims), n, _p(row_ptr), _p(perm))
+            if rc:
+                raise ValueError("coordinate out of range")
+            self._index[n] = (row_ptr, perm[: self.nnz])
+        return self._index[n]
+
+
+class Model:
+    """Core G (C-order, J_1 x ... x J_N) and factors A^(n) (I_n x J_n row-major), FP64."""
+
+    def __init__(self, G, A):
+        self.J = np.ascontiguousarray([a.shape[1] for a in A], dtype=np.int32)
+        self.G = np.ascontiguousarray(G, dtype=np.float64).reshape(tuple(int(j) for j in self.J))
+        self.A_all = np.ascontiguousarray(np.concatenate([np.asarray(a, np.float64).ravel() for a in A]))
+        self.dims = np.ascontiguousarray([a.shape[0] for a in A], dtype=np.int64)
+        self._off = np.concatenate([[0], np.cumsum(self.dims * self.J.astype(np.int64))])
+
+    @property
+    def N(self):
+        return int(self.J.size)
+
+    def A(self, n: int) -> np.ndarray:
+        """View of A^(n) inside the flat buffer (writes go through)."""
+        return self.A_all[self._off[n]: self._off[n + 1]].reshape(int(self.dims[n]), int(self.J[n]))
+
+    @property
+    def factors(self):
+        return [self.A(n).copy() for n in range(self.N)]
+
+    def copy(self) -> "Model":
+        return Model(self.G.copy(), self.factors)
+
+
+def init_model(dims, J, seed: int, prec: int) -> Model:
+    """Alg. 2 line 1: G, A^(n) ~ U[0,1) from the counter RNG.
+    prec=0 gives the values an FP32 library stores (exact in f32), prec=1 FP64."""
+    dims = np.ascontiguousarray(dims, np.int64)
+    J = np.ascontiguousarray(J, np.int32)
+    G = np.zeros(int(np.prod(J)), np.float64)
+    A_all = np.zeros(int(np.sum(dims * J)), np.float64)
+    lib().or_init(len(dims), _p(dims), _p(J), seed, prec, _p(G), _p(A_all))
+    A, off = [], 0
+    for I, j in zip(dims, J):
+        A.append(A_all[off: off + I * j].reshape(I, j))
+        off += I * j
+    return Model(G, A)
+
+
+def rng_word(seed, stream, idx) -> int:
+    return int(lib().or_rng_word(seed, stream, idx))
+
+
+def mix64(z) -> int:
+    return int(lib().or_mix64(z))
+
+
+def uniform(seed, stream, idx, prec) -> float:
+    return float(lib().or_uniform(seed, stream, idx, prec))
+
+
+def delta(t: Tensor, m: Model, entry: int, n: int) -> np.ndarray:
+    """Eq. 12 for entry `entry` (index into t) and mode n."""
+    out = np.zeros(int(m.J[n]), np.float64)
+    coord = np.ascontiguousarray(t.coords[entry])
+    lib().or_delta(m.N, _p(m.J), _p(m.G), _p(m.A_all), _p(m.dims), _p(coord), n, _p(out))
+    return out
+
+
+def predict(m: Model, coord) -> float:
+    """Eq. 4."""
+    coord = np.ascontiguousarray(coord, np.int32)
+    return float(lib().or_predict(m.N, _p(m.J), _p(m.G), _p(m.A_all), _p(m.dims), _p(coord)))
+
+
+def row_system(t: Tensor, m: Model, n: int, row: int):
+    """Eq. 10-11: B (J x J), c (J), sum x^2 over Omega^(n)_row."""
+    row_ptr, perm = t.mode_index(n)
+    Jn = int(m.J[n])
+    B = np.zeros((Jn, Jn), np.float64)
+    c = np.zeros(Jn, np.float64)
+    s2 = np.zeros(1, np.float64)
+    lib().or_row_system(m.N, _p(m.J), _p(m.G), _p(m.A_all), _p(m.dims), _p(t.coords), _p(t.vals), n,
+                        _p(row_ptr), _p(perm), row, _p(B), _p(c), _p(s2))
+    return B, c, float(s2[0])
+
+
+def solve(B, c, lam: float) -> np.ndarray:
+    """Eq. 9: a = c [B + lambda I]^-1 (Cholesky)."""
+    B = np.ascontiguousarray(B, np.float64)
+    c = np.ascontiguousarray(c, np.float64)
+    a = np.zeros(c.size, np.float64)
+    rc = lib().or_solve(int(c.size), _p(B), _p(c), float(lam), _p(a))
+    if rc:
+        raise FloatingPointError("non-positive pivot")
+    return a
+
+
+def update_row(t: Tensor, m: Model, n: int, row: int, lam: float) -> None:
+    row_ptr, perm = t.mode_index(n)
+    rc = lib().or_update_row(m.N, _p(m.J), _p(m.G), _p(m.A_all), _p(m.dims), _p(t.coords), _p(t.vals), n,
+                             _p(row_ptr), _p(perm), row, float(lam))
+    if rc:
+        raise FloatingPointError("non-positive pivot")
+
+
+def update_mode(t: Tensor, m: Model, n: int, lam: float, threads: int = 0) -> None:
+    """Alg. 3 lines 6-15 for every row of A^(n), in place."""
+    row_ptr, perm = t.mode_index(n)
+    rc = lib().or_update_mode(m.N, _p(m.J), _p(m.G), _p(m.A_all), _p(m.dims), _p(t.coords), _p(t.vals), n,
+                              _p(row_ptr), _p(perm), float(lam), int(threads))
+    if rc:
+        raise FloatingPointError("non-positive pivot")
+
+
+def sse(t: Tensor, m: Model, threads: int = 0) -> float:
+    """Squared Eq. 5."""
+    return float(lib().or_sse(m.N, _p(m.J), _p(m.G), _p(m.A_all), _p(m.dims), _p(t.coords), _p(t.vals),
+                              t.nnz, int(threads)))
+
+
+def error(t: Tensor, m: Model, threads: int = 0) -> float:
+    """Eq. 5: sqrt of the SSE over Omega."""
+    return float(np.sqrt(sse(t, m, threads)))
+
+
+def loss(t: Tensor, m: Model, lam: float, threads: int = 0) -> float:
+    """Eq. 6."""
+    return float(lib().or_loss(m.N, _p(m.J), _p(m.G), _p(m.A_all), _p(m.dims), _p(t.coords), _p(t.vals),
+                               t.nnz, float(lam), int(threads)))
+
+
+def thin_qr(A):
+    """Eq. 7: Householder thin QR with diag(R) > 0."""
+    Q = np.ascontiguousarray(A, np.float64).copy()
+    I, Jn = Q.shape
+    R = np.zeros((Jn, Jn), np.float64)
+    rc = lib().or_thin_qr(I, Jn, _p(Q), _p(R))
+    if rc == 1:
+        raise ValueError("I < J")
+    if rc == 2:
+        raise FloatingPointError("rank deficient")
+    return Q, R
+
+
+def core_mode_product(G, n: int, R) -> np.ndarray:
+    """Eq. 2 with U = R, as in Eq. 8."""
+    G = np.ascontiguousarray(G, np.float64).copy()
+    J = np.ascontiguousarray(G.shape, np.int32)
+    R = np.ascontiguousarray(R, np.float64)
+    lib().or_core_mode_product(len(J), _p(J), _p(G), n, _p(R))
+    return G
+
+
+def orthogonalize(m: Model):
+    """Alg. 2 lines 8-11, in place; returns the R^(n)."""
+    R_all = np.zeros(int(np.sum(m.J.astype(np.int64) ** 2)), np.float64)
+    rc = lib().or_orthogonalize(m.N, _p(m.J), _p(m.G), _p(m.A_all), _p(m.dims), _p(R_all))
+    if rc == 1:
+        raise ValueError("I < J")
+    if rc == 2:
+        raise FloatingPointError("rank deficient")
+    Rs, off = [], 0
+    for j in m.J:
+        Rs.append(R_all[off: off + j * j].reshape(j, j))
+        off += j * j
+    return Rs
+
+
+def partition(row_ptr, world: int) -> np.ndarray:
+    row_ptr = np.ascontiguousarray(row_ptr, np.int64)
+    b = np.zeros(world + 1, np.int64)
+    lib().or_partition(_p(row_ptr), row_ptr.size - 1, int(world), _p(b))
+    return b
+
+
+def als(t: Tensor, m: Model, lam: float, iters: int, threads: int = 0):
+    """Alg. 2 lines 2-4: `iters` sweeps of Alg. 3 over n = 1..N
+    (ascending), error Eq. 5 after each sweep.  Returns (errors, losses)
+    with index 0 = the state before the first sweep (reading R10)."""
+    errs = [error(t, m, threads)]
+    losses = [loss(t, m, lam, threads)]
+    for _ in range(iters):
+        for n in range(m.N):
+            update_mode(t, m, n, lam, threads)
+        errs.append(error(t, m, threads))
+        losses.append(loss(t, m, lam, threads))
+    return np.array(errs), np.array(losses)

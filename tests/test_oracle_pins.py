@@ -1,0 +1,416 @@
+"""Pins of the FP64 CPU oracle (oracle/ptucker_oracle.c) to what the paper and the
+mathematics fix -- never to the oracle itself.
+
+Each test names the passage it pins (P:<line> = /root/reference/PAPER.md,
+S:<line> = SPEC.md worked examples) and the independent route it uses:
+closed forms, SPEC's printed examples, textbook special cases solved with a
+library routine (numpy.linalg), brute force on tiny inputs, Theorem 1/2
+invariants with the loss re-evaluated by numpy einsum (not by the oracle).
+"""
+import json
+import os
+
+import numpy as np
+import pytest
+
+GOLD = os.path.join(os.path.dirname(__file__), "golden")
+
+
+# ---------------------------------------------------------------- helpers (independent of the oracle)
+def np_predict(G, A, coords):
+    """Eq. 4 via numpy einsum over the dense core."""
+    coords = np.asarray(coords)
+    T = np.einsum("ej,j...->e...", A[0][coords[:, 0]], G)
+    for k in range(1, len(A)):
+        T = np.einsum("ej,ej...->e...", A[k][coords[:, k]], T)
+    return T
+
+
+def np_loss(G, A, coords, vals, lam):
+    """Eq. 6 via numpy."""
+    r = vals - np_predict(G, A, coords)
+    return float(r @ r + lam * sum(float((a * a).sum()) for a in A))
+
+
+def rand_problem(rng, dims, J, nnz, distinct=True):
+    from oracle import oracle as o
+    N = len(dims)
+    if distinct:
+        tot = int(np.prod(dims))
+        flat = rng.choice(tot, size=min(nnz, tot), replace=False)
+        coords = np.stack(np.unravel_index(flat, dims), axis=1).astype(np.int32)
+    else:
+        coords = np.stack([rng.integers(0, d, nnz) for d in dims], axis=1).astype(np.int32)
+    vals = rng.random(coords.shape[0])
+    G = rng.random((J,) * N)
+    A = [rng.random((d, J)) for d in dims]
+    return o.Tensor(coords, vals, dims), o.Model(G, A)
+
+
+# ---------------------------------------------------------------- RNG (reading R2; parity unpinned vs paper)
+def test_splitmix64_published_vector(orc):
+    # SplitMix64 reference generator seeded with 1234567: first two outputs
+    # (public test vector of the SplitMix64 algorithm; the finaliser is or_mix64).
+    phi = 0x9E3779B97F4A7C15
+    assert orc.mix64((1234567 + phi) % 2**64) == 6457827717110365317
+    assert orc.mix64((1234567 + 2 * phi) % 2**64) == 3203168211198807973
+
+
+def test_rng_known_answers(orc):
+    for line in open(os.path.join(GOLD, "rng_kat.txt")):
+        if line.startswith("#") or not line.strip():
+            continue
+        s, i, z, f64, f32 = line.split()
+        assert orc.rng_word(0, int(s), int(i)) == int(z, 16)
+        assert orc.uniform(0, int(s), int(i), 1) == float(f64)
+        assert abs(orc.uniform(0, int(s), int(i), 0) - float(f32)) < 5e-9
+        assert orc.uniform(0, int(s), int(i), 0) == float(np.float32(orc.uniform(0, int(s), int(i), 0)))
+
+
+def test_init_layout_and_range(orc):
+    """Alg. 2 line 1 / P:466: G and A^(n) in [0,1); core C-order idx, A idx = i*J+j."""
+    m = orc.init_model([3, 4, 2], [2, 3, 2], seed=7, prec=1)
+    assert m.G.shape == (2, 3, 2)
+    assert m.G.ravel()[5] == orc.uniform(7, 0, 5, 1)
+    assert m.A(1)[2, 1] == orc.uniform(7, 2, 2 * 3 + 1, 1)
+    for x in [m.G.ravel(), m.A_all]:
+        assert (x >= 0).all() and (x < 1).all()
+    m2 = orc.init_model([3, 4, 2], [2, 3, 2], seed=8, prec=1)
+    assert not np.array_equal(m.A_all, m2.A_all)
+    m3 = orc.init_model([3, 4, 2], [2, 3, 2], seed=7, prec=0)
+    assert np.array_equal(m3.A_all.astype(np.float32).astype(np.float64), m3.A_all)
+
+
+# ---------------------------------------------------------------- mode slices
+def test_mode_index_bruteforce(orc):
+    rng = np.random.default_rng(1)
+    dims = (7, 5, 9, 3)
+    coords = np.stack([rng.integers(0, d, 300) for d in dims], 1).astype(np.int32)
+    t = orc.Tensor(coords, rng.random(300), dims)
+    for n in range(4):
+        row_ptr, perm = t.mode_index(n)
+        # brute force: re-partition by coordinate, keeping input order in each slice
+        for i in range(dims[n]):
+            want = [e for e in range(300) if coords[e, n] == i]
+            assert list(perm[row_ptr[i]:row_ptr[i + 1]]) == want
+        assert row_ptr[-1] == 300 and sorted(perm) == list(range(300))
+
+
+def test_mode_index_spec_example(orc):
+    # 2x2 tensor, entries (1,1),(1,2),(2,1) -> mode-1 slices {0,1}, {2}
+    t = orc.Tensor([[0, 0], [0, 1], [1, 0]], [1.0, 2.0, 3.0], (2, 2))
+    row_ptr, perm = t.mode_index(0)
+    assert list(row_ptr) == [0, 2, 3] and list(perm) == [0, 1, 2]
+
+
+def test_partition_property(orc):
+    """Contiguous nnz-balanced blocks: b_g is the first row whose prefix count
+    reaches ceil(g*nnz/W) (checked by scanning every candidate row)."""
+    rng = np.random.default_rng(2)
+    for trial in range(20):
+        I = int(rng.integers(1, 40))
+        lens = rng.integers(0, 30, I) * (rng.random(I) < 0.8)
+        row_ptr = np.concatenate([[0], np.cumsum(lens)]).astype(np.int64)
+        nnz = int(row_ptr[-1])
+        for W in (1, 2, 3, 8):
+            b = orc.partition(row_ptr, W)
+            assert b[0] == 0 and b[-1] == I and (np.diff(b) >= 0).all()
+            for g in range(1, W):
+                target = -(-g * nnz // W)
+                cands = [r for r in range(I + 1) if row_ptr[r] >= target]
+                assert b[g] == (cands[0] if cands else I)
+
+
+# ---------------------------------------------------------------- delta (Eq. 12)
+def test_delta_spec_example(orc):
+    # N=2, 2x2 identity core, mode 1, alpha=(1,1), a^(2)_{1:}=[4,5] -> delta=[4,5]
+    m = orc.Model(np.eye(2), [np.array([[1.0, 1.0]]), np.array([[4.0, 5.0]])])
+    t = orc.Tensor([[0, 0]], [23.0], (1, 1))
+    assert np.array_equal(orc.delta(t, m, 0, 0), [4.0, 5.0])
+    # zero core -> 0
+    m0 = orc.Model(np.zeros((2, 2)), [np.array([[1.0, 1.0]]), np.array([[4.0, 5.0]])])
+    assert np.array_equal(orc.delta(t, m0, 0, 0), [0.0, 0.0])
+    # reconstruct_entry = 2*4 + 3*5 = 23
+    m1 = orc.Model(np.eye(2), [np.array([[2.0, 3.0]]), np.array([[4.0, 5.0]])])
+    assert orc.predict(m1, [0, 0]) == 23.0
+
+
+@pytest.mark.parametrize("dims,J", [((4, 5, 3), 3), ((3, 4, 2, 3), 2), ((2, 3, 2, 2, 3), 2), ((6, 5, 4), 5)])
+def test_delta_linearity_bruteforce(orc, dims, J):
+    """x_hat is linear in row a^(n)_{i_n}: delta(j) = x_hat with that row := e_j (Eq. 4 vs Eq. 12)."""
+    rng = np.random.default_rng(3)
+    t, m = rand_problem(rng, dims, J, 12)
+    A = m.factors
+    for e in range(t.nnz):
+        for n in range(len(dims)):
+            d = orc.delta(t, m, e, n)
+            want = np.empty(J)
+            for j in range(J):
+                A2 = [a.copy() for a in A]
+                A2[n][t.coords[e, n]] = np.eye(J)[j]
+                want[j] = np_predict(m.G, A2, t.coords[e:e + 1])[0]
+            np.testing.assert_allclose(d, want, rtol=1e-13, atol=1e-15)
+            assert abs(orc.predict(m, t.coords[e]) - np_predict(m.G, A, t.coords[e:e + 1])[0]) < 1e-13 * max(1, abs(d).sum())
+
+
+# ---------------------------------------------------------------- B, c (Eq. 10-11)
+def test_row_system_spec_example(orc):
+    # one observation, delta=[4,5], X=23 -> B=[[16,20],[20,25]], c=[92,115]
+    m = orc.Model(np.eye(2), [np.array([[1.0, 1.0]]), np.array([[4.0, 5.0]])])
+    t = orc.Tensor([[0, 0]], [23.0], (1, 1))
+    B, c, s2 = orc.row_system(t, m, 0, 0)
+    assert np.array_equal(B, [[16, 20], [20, 25]]) and np.array_equal(c, [92, 115]) and s2 == 529.0
+
+
+def test_row_system_dense_normal_equations(orc):
+    """B = D^T D, c = D^T x with D the design matrix of the row's observations,
+    D[e, j] = x_hat_e with a_{i_n} := e_j (brute force through numpy)."""
+    rng = np.random.default_rng(4)
+    dims, J = (3, 6, 5), 3
+    t, m = rand_problem(rng, dims, J, 60)
+    A = m.factors
+    for n in range(3):
+        row_ptr, perm = t.mode_index(n)
+        for i in range(dims[n]):
+            ent = [e for e in range(t.nnz) if t.coords[e, n] == i]
+            D = np.zeros((len(ent), J))
+            for j in range(J):
+                A2 = [a.copy() for a in A]
+                A2[n][i] = np.eye(J)[j]
+                if ent:
+                    D[:, j] = np_predict(m.G, A2, t.coords[ent])
+            B, c, s2 = orc.row_system(t, m, n, i)
+            np.testing.assert_allclose(B, D.T @ D, rtol=1e-12, atol=1e-13)
+            np.testing.assert_allclose(c, D.T @ t.vals[ent], rtol=1e-12, atol=1e-13)
+            assert abs(s2 - float(t.vals[ent] @ t.vals[ent])) < 1e-12
+
+
+# ---------------------------------------------------------------- row solve (Eq. 9, Theorem 1)
+def test_solve_spec_examples(orc):
+    assert np.array_equal(orc.solve(np.zeros((2, 2)), [0.0, 0.0], 0.01), [0.0, 0.0])
+    np.testing.assert_allclose(orc.solve(np.eye(2), [1.0, 2.0], 1.0), [0.5, 1.0], rtol=1e-15)
+    # S:136 one observation: a = x delta / (||delta||^2 + lambda) (Sherman-Morrison closed form)
+    a = orc.solve(np.array([[16.0, 20.0], [20.0, 25.0]]), [92.0, 115.0], 0.01)
+    np.testing.assert_allclose(a, [2.2433552792, 2.8041940990], rtol=0, atol=5e-11)
+    np.testing.assert_allclose(a, 23 * np.array([4.0, 5.0]) / 41.01, rtol=1e-12)  # cond(B+lambda I) ~ 4e3
+
+
+def test_solve_vs_library(orc):
+    rng = np.random.default_rng(5)
+    for J in (1, 2, 5, 10, 16):
+        M = rng.standard_normal((3 * J, J))
+        B = M.T @ M
+        c = rng.standard_normal(J)
+        a = orc.solve(B, c, 0.01)
+        np.testing.assert_allclose(a, np.linalg.solve(B + 0.01 * np.eye(J), c), rtol=1e-10, atol=1e-12)
+
+
+def test_ridge_special_case(orc):
+    """N=2 with an identity core: the row rule reduces to ridge regression
+    (M^T M + lambda I)^-1 M^T x with M the paired rows of A^(2)."""
+    rng = np.random.default_rng(6)
+    I0, I1, J, lam = 8, 11, 4, 0.3
+    coords = np.stack(np.unravel_index(rng.choice(I0 * I1, 50, replace=False), (I0, I1)), 1).astype(np.int32)
+    x = rng.standard_normal(50)
+    t = orc.Tensor(coords, x, (I0, I1))
+    m = orc.Model(np.eye(J), [rng.random((I0, J)), rng.random((I1, J))])
+    A1 = m.A(1).copy()
+    orc.update_mode(t, m, 0, lam)
+    for i in range(I0):
+        sel = coords[:, 0] == i
+        M = A1[coords[sel, 1]]
+        want = np.linalg.solve(M.T @ M + lam * np.eye(J), M.T @ x[sel])
+        np.testing.assert_allclose(m.A(0)[i], want, rtol=1e-10, atol=1e-12)
+
+
+def test_theorem1_stationarity(orc):
+    """Theorem 1: the updated row zeroes dL/da_{i_n} (Eq. 6).
+    Checked with central differences of a numpy-evaluated loss (h=1e-6), and
+    the normal-equation residual ||a(B+lambda I) - c|| <= 1e-9 (1 + ||c||)."""
+    rng = np.random.default_rng(7)
+    dims, J, lam = (5, 4, 6), 3, 0.05
+    t, m = rand_problem(rng, dims, J, 70)
+    for n in range(3):
+        orc.update_mode(t, m, n, lam)
+        A = m.factors
+        for i in range(dims[n]):
+            B, c, _ = orc.row_system(t, m, n, i)
+            a = m.A(n)[i]
+            assert np.linalg.norm(a @ (B + lam * np.eye(J)) - c) <= 1e-9 * (1 + np.linalg.norm(c))
+            h = 1e-6
+            for j in range(J):
+                Ap = [x.copy() for x in A]
+                Am = [x.copy() for x in A]
+                Ap[n][i, j] += h
+                Am[n][i, j] -= h
+                g = (np_loss(m.G, Ap, t.coords, t.vals, lam) - np_loss(m.G, Am, t.coords, t.vals, lam)) / (2 * h)
+                assert abs(g) <= 1e-4
+
+
+def test_theorem2_monotone_loss_per_row(orc):
+    """Theorem 2: Eq. 6 never increases across single-row updates
+    (loss re-evaluated by numpy); the order of rows inside a mode does not
+    change the result (rows are independent)."""
+    rng = np.random.default_rng(8)
+    dims, J, lam = (6, 5, 7), 3, 0.01
+    t, m = rand_problem(rng, dims, J, 90)
+    m_rev = m.copy()
+    prev = np_loss(m.G, m.factors, t.coords, t.vals, lam)
+    for it in range(3):
+        for n in range(3):
+            for i in rng.permutation(dims[n]):
+                orc.update_row(t, m, n, int(i), lam)
+                cur = np_loss(m.G, m.factors, t.coords, t.vals, lam)
+                assert cur <= prev + 1e-12 * prev
+                prev = cur
+            for i in reversed(range(dims[n])):
+                orc.update_row(t, m_rev, n, i, lam)
+            assert np.array_equal(m.A(n), m_rev.A(n))
+
+
+def test_empty_rows_are_zero(orc):
+    t = orc.Tensor([[0, 0, 0], [0, 1, 1], [2, 1, 0]], [1.0, 2.0, 3.0], (4, 2, 2))
+    m = orc.init_model([4, 2, 2], [2, 2, 2], seed=0, prec=1)
+    orc.update_mode(t, m, 0, 0.01)
+    assert np.array_equal(m.A(0)[1], [0, 0]) and np.array_equal(m.A(0)[3], [0, 0])
+
+
+# ---------------------------------------------------------------- error (Eq. 5) and the SSE identity
+def test_error_special_cases(orc):
+    rng = np.random.default_rng(9)
+    t, m = rand_problem(rng, (5, 6, 7), 3, 80)
+    np.testing.assert_allclose(orc.sse(t, m), float(((t.vals - np_predict(m.G, m.factors, t.coords)) ** 2).sum()),
+                               rtol=1e-12)
+    z = orc.Model(m.G, [np.zeros_like(a) for a in m.factors])
+    assert abs(orc.error(t, z) - np.linalg.norm(t.vals)) <= 1e-14 * np.linalg.norm(t.vals)
+    perfect = orc.Tensor(t.coords, np_predict(m.G, m.factors, t.coords), t.dims)
+    assert orc.error(perfect, m) <= 1e-12 * np.linalg.norm(perfect.vals)
+    lam = 0.2
+    assert abs(orc.loss(t, m, lam) - np_loss(m.G, m.factors, t.coords, t.vals, lam)) < 1e-11
+
+
+def test_sse_identity(orc):
+    """For a solved row a = c (B+lambda I)^-1: sum_row (x - a.delta)^2 = sum x^2 - a.c - lambda ||a||^2
+    (exact algebra; the fused error of the CUDA path relies on it)."""
+    rng = np.random.default_rng(10)
+    t, m = rand_problem(rng, (4, 9, 8), 4, 200)
+    lam = 0.01
+    orc.update_mode(t, m, 2, lam)
+    row_ptr, perm = t.mode_index(2)
+    for i in range(8):
+        B, c, s2 = orc.row_system(t, m, 2, i)
+        a = m.A(2)[i]
+        ent = perm[row_ptr[i]:row_ptr[i + 1]]
+        lit = float(((t.vals[ent] - np_predict(m.G, m.factors, t.coords[ent])) ** 2).sum())
+        assert abs(lit - (s2 - a @ c - lam * a @ a)) <= 1e-12 * s2
+
+
+@pytest.mark.parametrize("init_seed,iters", [(2, 200), (1, 1000)])
+def test_planted_recovery(orc, init_seed, iters):
+    """North-star oracle check: a noise-free planted Tucker tensor is recovered
+    to near-zero error.  The core is never fitted during ALS (Alg. 2),
+    so the plant shares the solver's own init core (survey F2) and has fresh
+    U[0,1) factors; N=3, I=30, J=2, 30% observed, lambda=1e-6.  Row-wise ALS
+    converges linearly and its rate depends on the start (init_seed 1 needs
+    ~1000 sweeps, init_seed 2 ~100), so both are run to their own budget."""
+    rng = np.random.default_rng(11)
+    dims, J = (30, 30, 30), 2
+    m = orc.init_model(dims, [J] * 3, seed=init_seed, prec=1)
+    Astar = [rng.random((d, J)) for d in dims]
+    flat = rng.choice(27000, 8100, replace=False)
+    coords = np.stack(np.unravel_index(flat, dims), 1).astype(np.int32)
+    x = np_predict(m.G, Astar, coords)
+    t = orc.Tensor(coords, x, dims)
+    errs, losses = orc.als(t, m, 1e-6, iters)
+    assert errs[-1] / np.linalg.norm(x) <= 1e-6
+    assert (np.diff(losses) <= 1e-12 * losses[:-1]).all()
+
+
+def test_fixed_point(orc):
+    """Data = the init model's own reconstruction: e_0 = 0, and one sweep with
+    lambda ~ 0 stays at (near) zero error."""
+    rng = np.random.default_rng(12)
+    dims = (12, 10, 9)
+    m = orc.init_model(dims, [3, 3, 3], seed=3, prec=1)
+    flat = rng.choice(int(np.prod(dims)), 400, replace=False)
+    coords = np.stack(np.unravel_index(flat, dims), 1).astype(np.int32)
+    x = np_predict(m.G, m.factors, coords)
+    t = orc.Tensor(coords, x, dims)
+    errs, _ = orc.als(t, m, 1e-12, 1)
+    assert errs[0] <= 1e-13 * np.linalg.norm(x)
+    assert errs[1] <= 1e-6 * np.linalg.norm(x)
+
+
+# ---------------------------------------------------------------- QR + core update (Eq. 7-8)
+def test_qr_spec_examples(orc):
+    Q, R = orc.thin_qr(np.array([[3.0, 0], [4, 0], [0, 1]]))
+    np.testing.assert_allclose(Q, [[0.6, 0], [0.8, 0], [0, 1]], atol=1e-15)
+    np.testing.assert_allclose(R, [[5, 0], [0, 1]], atol=1e-14)
+    rng = np.random.default_rng(13)
+    O = np.linalg.qr(rng.standard_normal((20, 4)))[0]
+    O = O * np.sign(np.diag(np.linalg.qr(O)[1]))  # any orthonormal matrix
+    Q, R = orc.thin_qr(O)
+    np.testing.assert_allclose(np.abs(R), np.eye(4), atol=1e-12)
+
+
+def test_qr_vs_library(orc):
+    rng = np.random.default_rng(14)
+    for I, J in [(5, 5), (50, 5), (300, 10), (7, 1)]:
+        A = rng.random((I, J))
+        Q, R = orc.thin_qr(A)
+        Ql, Rl = np.linalg.qr(A)
+        s = np.sign(np.diag(Rl))
+        np.testing.assert_allclose(Q, Ql * s, atol=1e-12)
+        np.testing.assert_allclose(R, Rl * s[:, None], atol=1e-12)
+        assert np.abs(Q.T @ Q - np.eye(J)).max() <= 1e-12
+        assert (np.diag(R) > 0).all() and np.allclose(np.tril(R, -1), 0)
+    with pytest.raises(ValueError):
+        orc.thin_qr(np.ones((2, 3)))
+
+
+def test_core_mode_product(orc):
+    # 2x2 identity core x_1 diag(5,1) -> (1,1)->5, (2,2)->1
+    np.testing.assert_array_equal(orc.core_mode_product(np.eye(2), 0, np.diag([5.0, 1.0])), np.diag([5.0, 1.0]))
+    rng = np.random.default_rng(15)
+    G = rng.standard_normal((3, 4, 2))
+    for n in range(3):
+        np.testing.assert_array_equal(orc.core_mode_product(G, n, np.eye(G.shape[n])), G)
+        R = rng.standard_normal((G.shape[n], G.shape[n]))
+        want = np.moveaxis(np.tensordot(R, G, axes=([1], [n])), 0, n)   # Eq. 2 with U = R
+        np.testing.assert_allclose(orc.core_mode_product(G, n, R), want, rtol=1e-13, atol=1e-14)
+
+
+def test_orthogonalize_invariance(orc):
+    """Eq. 7-8: 'to maintain the same reconstruction error' -- every
+    prediction is unchanged, and every A^(n) becomes column-orthonormal."""
+    rng = np.random.default_rng(16)
+    t, m = rand_problem(rng, (20, 15, 12, 10), 3, 150)
+    before = np_predict(m.G, m.factors, t.coords)
+    orc.orthogonalize(m)
+    after = np_predict(m.G, m.factors, t.coords)
+    assert np.abs(after - before).max() <= 1e-10 * np.abs(before).max()
+    for n in range(4):
+        assert np.abs(m.A(n).T @ m.A(n) - np.eye(3)).max() <= 1e-12
+
+
+# ---------------------------------------------------------------- advisory worked example (SURVEY [E10])
+def test_worked_example_advisory(orc):
+    ex = json.load(open(os.path.join(GOLD, "worked_example_e10.json")))
+    t = orc.Tensor(ex["coords"], ex["vals"], ex["dims"])
+    m = orc.init_model(ex["dims"], ex["J"], seed=ex["seed"], prec=1)
+    np.testing.assert_allclose(m.G.ravel(), ex["G_init"], rtol=1e-13)
+    np.testing.assert_allclose(m.A(0), ex["A0_init"], rtol=1e-13)
+    lam = ex["lambda"]
+    assert abs(orc.error(t, m) - ex["e0"]) < 1e-12 and abs(orc.loss(t, m, lam) - ex["L0"]) < 1e-12
+    orc.update_mode(t, m, 0, lam)
+    np.testing.assert_allclose(m.A(0), ex["A0_after_first_mode_update"], rtol=1e-12)
+    orc.update_mode(t, m, 1, lam)
+    orc.update_mode(t, m, 2, lam)
+    assert abs(orc.error(t, m) - ex["e1"]) < 1e-12 and abs(orc.loss(t, m, lam) - ex["L1"]) < 1e-12
+    for n in range(3):
+        orc.update_mode(t, m, n, lam)
+    assert abs(orc.error(t, m) - ex["e2"]) < 1e-12 and abs(orc.loss(t, m, lam) - ex["L2"]) < 1e-12
+    before = np_predict(m.G, m.factors, t.coords)
+    Rs = orc.orthogonalize(m)
+    np.testing.assert_allclose(Rs[0], ex["R0_after_orthogonalize"], rtol=1e-10, atol=1e-13)
+    assert np.abs(np_predict(m.G, m.factors, t.coords) - before).max() < 1e-14
