@@ -1,0 +1,153 @@
+/*
+ * ptucker.h -- C-ABI of the B200-native P-Tucker row-wise ALS hot path.
+ *
+ * Method: Oh, Park, Sael, Kang, "Scalable Tucker Factorization for Sparse
+ * Tensors - Algorithms and Discoveries" (arXiv 1710.02261).  P:<line> cites
+ * /root/reference/PAPER.md.  Readings of the paper (R#) are listed in DESIGN.md.
+ *
+ * Conventions
+ *  - Indices are 0-based (the paper's 1-based notation, stops here).
+ *  - "host" pointers are plain CPU memory owned by the caller; every call that
+ *    takes one copies synchronously before returning, so the caller may free it.
+ *  - The library owns all device memory (one context per process, one GPU per
+ *    process: the device current at ptucker_init).  Not thread-safe.
+ *  - Precision: PTUCKER_F32 stores values, factors and core in fp32 (the
+ *    per-entry contraction runs in fp32, the normal equations B, c and the
+ *    solve in fp64); PTUCKER_F64 is fp64 throughout.
+ *  - Factor A^(n) host layout: I_n x J_n row-major.  Core host layout: C order
+ *    J_1 x ... x J_N (last mode fastest).  Both in the context precision.
+ *  - Every function returns PTUCKER_OK (0) or an error code; the message of the
+ *    last failure is ptucker_last_error().  Kernel launches are stream-ordered:
+ *    a numeric failure inside a kernel (non-positive Cholesky pivot) is
+ *    reported by the next synchronising call (ptucker_error, ptucker_get_*,
+ *    ptucker_orthogonalize, ptucker_synchronize, ptucker_finalize) as
+ *    PTUCKER_ENUMERIC with the (mode, row) in the message.
+ */
+#ifndef PTUCKER_H
+#define PTUCKER_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum {
+    PTUCKER_OK = 0,
+    PTUCKER_EINVAL = 1,    /* bad argument (shape, range, non-finite value, lambda <= 0, unsupported (N, J)) */
+    PTUCKER_ENUMERIC = 2,  /* non-positive pivot in a row solve, rank-deficient factor in QR */
+    PTUCKER_ERESOURCE = 3, /* device allocation failed */
+    PTUCKER_ECUDA = 4,     /* CUDA runtime error (message has the driver text) */
+    PTUCKER_ENCCL = 5,     /* NCCL error */
+    PTUCKER_ESTATE = 6     /* call out of order (e.g. update before init) */
+};
+enum { PTUCKER_F32 = 0, PTUCKER_F64 = 1 };
+
+/* Library version (major*10000 + minor*100 + patch). */
+int32_t ptucker_version(void);
+
+/* Message of the last failing call in this thread ("" if none). */
+const char* ptucker_last_error(void);
+
+/* ---------------- multi-GPU bootstrap (skip both when world == 1) --------
+ * ptucker_get_unique_id: rank 0 creates an NCCL unique id (128 bytes, host);
+ * the caller broadcasts the bytes (e.g. torch.distributed) and every rank then
+ * calls ptucker_comm_init(rank, world, id) before ptucker_init.  Rows of each
+ * mode are then split into nnz-balanced contiguous blocks (see
+ * ptucker_partition_rows); each rank updates its block and the blocks are
+ * all-gathered over NVLink after each mode (the paper aggregates "all updated
+ * rows from all threads", Fig. 3 caption P:517-518). */
+int ptucker_get_unique_id(uint8_t out[128]);
+int ptucker_comm_init(int32_t rank, int32_t world, const uint8_t id[128]);
+
+/* Pure host helper (no GPU needed): nnz-balanced contiguous row blocks.
+ * row_ptr: host, I+1 int64 prefix counts of a mode's slices.  bounds: host,
+ * world+1 int64 output; bounds[0] = 0, bounds[world] = I and bounds[g] is the
+ * first row r with row_ptr[r] >= ceil(g*nnz/world).  Rows are never split. */
+int ptucker_partition_rows(const int64_t* row_ptr, int64_t I, int32_t world, int64_t* bounds);
+
+/* Use this CUDA stream (a cudaStream_t passed as void*, e.g.
+ * torch.cuda.current_stream().cuda_stream) for all later work.  NULL selects
+ * the library's own non-blocking stream (the default). */
+int ptucker_set_stream(void* cuda_stream);
+
+/* Alg. 2 line 1: set up the problem of Def. "Sparse Tucker
+ * Factorization".
+ *  coords    host, nnz x order int32, row-major, 0-based; coords[e*order+n] in [0, dims[n])
+ *  vals      host, nnz values; vals_dtype selects the context precision
+ *  vals_dtype PTUCKER_F32 | PTUCKER_F64
+ *  nnz       >= 1 (duplicate coordinates are accepted: multiset, reading R14)
+ *  order     N >= 2
+ *  dims      host, N int64, each >= 1
+ *  core_dims host, N int32; this version requires all J_n equal and the pair
+ *            (N, J) in the compiled set (N in 2..5, J in {2,3,4,5,8,10}, J^N <= 10^4)
+ *  lambda    > 0 (makes B + lambda I positive definite)
+ *  seed      init RNG seed: G and every A^(n) ~ U[0,1) (reading R2)
+ * Copies the COO to the device, draws the init, builds every mode's slice
+ * index Omega^(n)_{i_n} on the device (stable radix sort -> CSR ->
+ * length-sorted segments) and this rank's row blocks.  Replaces any previous
+ * context's data (the communicator is kept). */
+int ptucker_init(const int32_t* coords, const void* vals, int32_t vals_dtype, int64_t nnz, int32_t order,
+                 const int64_t* dims, const int32_t* core_dims, double lambda, uint64_t seed);
+
+/* Alg. 3 lines 6-15 for mode n (0-based): every row i of A^(n)
+ * owned by this rank becomes a_i = c_i [B_i + lambda I]^-1 (Eq. 9-12,
+ * P:536-552), with empty rows set to 0; then, when world > 1, the row blocks
+ * are all-gathered so every rank holds the whole A^(n).  Stream-ordered:
+ * returns after enqueueing. */
+int ptucker_update_mode(int32_t n);
+
+/* One full ALS iteration (Alg. 2 line 3: update A^(1..N) by Alg. 3):
+ * ptucker_update_mode(0..N-1) in ascending order. */
+int ptucker_sweep(void);
+
+/* Eq. 5: sqrt of sum over Omega of (x - x_hat)^2 for the current
+ * state, summed over ranks (host *out, synchronises).  After an update_mode it
+ * uses the per-row identity sum x^2 - 2 a.c + a B a^T of the rows just solved
+ * (fused); otherwise it runs the literal per-entry pass. */
+int ptucker_error(double* out);
+/* Same quantity, always by the literal per-entry pass (Eq. 4-5). */
+int ptucker_error_literal(double* out);
+
+/* Alg. 2 lines 8-11: for n = 1..N, A^(n) = Q^(n) R^(n) with
+ * diag(R) > 0, A^(n) <- Q^(n), G <- G x_n R^(n) (Eq. 7-8).
+ * Requires I_n >= J_n; a rank-deficient A^(n) gives PTUCKER_ENUMERIC. */
+int ptucker_orthogonalize(void);
+
+/* State access (host buffers of exactly I_n*J_n or prod J elements, context precision). */
+int ptucker_get_factor(int32_t n, void* out);
+int ptucker_set_factor(int32_t n, const void* in);
+int ptucker_get_core(void* out);
+int ptucker_set_core(const void* in);
+
+/* Test hook: mode n's slice index.  row_ptr: host, I_n+1 int64; perm: host,
+ * nnz int64 (entry ids sorted by coordinate n, ties in input order). */
+int ptucker_get_mode_index(int32_t n, int64_t* row_ptr, int64_t* perm);
+/* This context's row blocks of mode n: host, world+1 int64. */
+int ptucker_get_partition(int32_t n, int64_t* bounds);
+
+/* Options (set after init unless noted):
+ *  "policy"       0 = F32-A (contraction all fp32), 1 = F32-B (last contraction stage fp64; default)
+ *  "seg_len"      max entries per row segment (>= 1, default 256; set BEFORE init)
+ *  "time_kernels" 1 = bracket every kernel launch with CUDA events (ptucker_kernel_stats) */
+int ptucker_set_option(const char* key, int64_t value);
+
+/* Device time (CUDA events on the library stream) accumulated for kernel
+ * `name` ("update", "finalize", "sse_reduce", "allgather", ...) since the last
+ * reset, with the launch count; synchronises. */
+int ptucker_kernel_stats(const char* name, double* total_ms, int64_t* launches);
+int ptucker_reset_kernel_stats(void);
+
+/* JSON description of the context (sizes, segments, kernel variant); host buffer. */
+int ptucker_info(char* buf, int32_t len);
+
+/* Wait for all enqueued work; reports deferred numeric failures. */
+int ptucker_synchronize(void);
+
+/* Free all device memory and the communicator. */
+int ptucker_finalize(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PTUCKER_H */

@@ -1,0 +1,707 @@
+// abi.cu -- the C-ABI (include/ptucker.h): context, validation, orchestration of
+// the kernels per call, NCCL exchange between ranks, state access.
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <string>
+#include <vector>
+
+#include "../../include/ptucker.h"
+#include "index.cuh"
+#include "internal.cuh"
+#include "kernels.cuh"
+
+namespace pt {
+
+const UpdateKernel* find_update_kernel(int prec, int last64, int N, int J) {
+    int cnt = 0;
+    const UpdateKernel* t = prec == PTUCKER_F64 ? update_kernels_f64(&cnt)
+                            : (last64 ? update_kernels_f32b(&cnt) : update_kernels_f32a(&cnt));
+    for (int i = 0; i < cnt; ++i)
+        if (t[i].N == N && t[i].J == J) return &t[i];
+    return nullptr;
+}
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const char* fmt, ...) {
+    char buf[1024];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof(buf), fmt, ap);
+    va_end(ap);
+    g_err = buf;
+    return code;
+}
+
+#define CK(x)                                                                                       \
+    do {                                                                                            \
+        cudaError_t e_ = (x);                                                                       \
+        if (e_ != cudaSuccess) {                                                                    \
+            return fail(e_ == cudaErrorMemoryAllocation ? PTUCKER_ERESOURCE : PTUCKER_ECUDA,        \
+                        "%s:%d %s: %s", __FILE__, __LINE__, #x, cudaGetErrorString(e_));           \
+        }                                                                                           \
+    } while (0)
+
+#define NK(x)                                                                                    \
+    do {                                                                                         \
+        ncclResult_t r_ = (x);                                                                   \
+        if (r_ != ncclSuccess)                                                                   \
+            return fail(PTUCKER_ENCCL, "%s:%d %s: %s", __FILE__, __LINE__, #x, ncclGetErrorString(r_)); \
+    } while (0)
+
+struct Pending {
+    std::string name;
+    cudaEvent_t a, b;
+};
+
+struct Ctx {
+    bool inited = false;
+    int device = -1;
+    cudaStream_t stream = nullptr;
+    bool own_stream = false;
+    int rank = 0, world = 1;
+    ncclComm_t comm = nullptr;
+    // problem
+    int N = 0, J = 0, prec = 0, esz = 4;
+    int64_t nnz = 0;
+    int64_t dims[kMaxN] = {0};
+    double lambda = 0.0;
+    uint64_t seed = 0;
+    int lda = 0, gp_elems = 0;
+    int policy = 1;     // F32-B by default
+    int seg_len = 256;  // S
+    DeviceArena arena, scratch;
+    void* A[kMaxN] = {nullptr};
+    void* G = nullptr;
+    void* Gtmp = nullptr;
+    void* Gp[kMaxN] = {nullptr};
+    ModeIndex mi[kMaxN];
+    double* sse_row[kMaxN] = {nullptr};
+    double* lit_part = nullptr;
+    double* red_part = nullptr;  // 256
+    double* red_out = nullptr;   // 4
+    double* qr = nullptr;        // W, W2, R1, R2, R (J*J each) + gram partials (256*NB)
+    double* qd = nullptr;        // I_max x J fp64 scratch for CholeskyQR2 (lazy)
+    int* d_fail = nullptr;       // row + 1 of a failed solve
+    int* d_qrfail = nullptr;     // mode + 1 of a failed QR
+    unsigned int* d_work = nullptr;
+    int sse_mode = -1;           // mode whose per-row SSE describes the current state
+    int last_fail_mode = -1;
+    const UpdateKernel* kern = nullptr;
+    int grid_upd = 0, grid_lit = 0;
+    // timing
+    bool time_kernels = false;
+    std::vector<Pending> pending;
+    std::map<std::string, std::pair<double, int64_t>> stats;
+};
+
+Ctx g;
+
+cudaStream_t S() { return g.stream; }
+
+template <class F>
+int timed(const char* name, F&& f) {
+    if (!g.time_kernels) return f();
+    Pending p;
+    p.name = name;
+    CK(cudaEventCreate(&p.a));
+    CK(cudaEventCreate(&p.b));
+    CK(cudaEventRecord(p.a, S()));
+    const int rc = f();
+    CK(cudaEventRecord(p.b, S()));
+    g.pending.push_back(p);
+    return rc;
+}
+
+int fold_stats() {
+    for (auto& p : g.pending) {
+        CK(cudaEventSynchronize(p.b));
+        float ms = 0.f;
+        CK(cudaEventElapsedTime(&ms, p.a, p.b));
+        auto& s = g.stats[p.name];
+        s.first += ms;
+        s.second += 1;
+        cudaEventDestroy(p.a);
+        cudaEventDestroy(p.b);
+    }
+    g.pending.clear();
+    return PTUCKER_OK;
+}
+
+int check_fail_flags() {
+    int h[2] = {0, 0};
+    CK(cudaMemcpyAsync(&h[0], g.d_fail, sizeof(int), cudaMemcpyDeviceToHost, S()));
+    CK(cudaMemcpyAsync(&h[1], g.d_qrfail, sizeof(int), cudaMemcpyDeviceToHost, S()));
+    CK(cudaStreamSynchronize(S()));
+    if (h[0] != 0) {
+        CK(cudaMemsetAsync(g.d_fail, 0, sizeof(int), S()));
+        CK(cudaStreamSynchronize(S()));
+        return fail(PTUCKER_ENUMERIC, "non-positive pivot in the row solve of mode %d, row %d", g.last_fail_mode,
+                    h[0] - 1);
+    }
+    if (h[1] != 0) {
+        CK(cudaMemsetAsync(g.d_qrfail, 0, sizeof(int), S()));
+        CK(cudaStreamSynchronize(S()));
+        return fail(PTUCKER_ENUMERIC, "rank-deficient factor A^(%d) in QR", h[1] - 1);
+    }
+    return PTUCKER_OK;
+}
+
+int sync_and_check() {
+    CK(cudaStreamSynchronize(S()));
+    CK(cudaGetLastError());
+    return check_fail_flags();
+}
+
+int require_init() {
+    if (!g.inited) return fail(PTUCKER_ESTATE, "ptucker_init has not been called");
+    int dev = -1;
+    CK(cudaGetDevice(&dev));
+    if (dev != g.device) CK(cudaSetDevice(g.device));
+    return PTUCKER_OK;
+}
+
+template <typename TS>
+UpdateParams<TS> make_params(int n, bool literal) {
+    UpdateParams<TS> p;
+    memset(&p, 0, sizeof(p));
+    const ModeIndex& m = g.mi[n];
+    p.n = n;
+    p.nslices = m.nslices;
+    p.slice_off = m.slice_off;
+    p.slice_len = m.slice_len;
+    p.lane_row = m.lane_row;
+    p.lane_len = m.lane_len;
+    p.lane_pidx = m.lane_pidx;
+    p.lane_pstride = m.lane_pstride;
+    int l = 0;
+    for (int k = 0; k < g.N; ++k) {
+        if (k == n) continue;
+        p.sc[l] = m.sc[l];
+        p.A[l] = (const TS*)g.A[k];
+        ++l;
+    }
+    p.sv = (const TS*)m.sv;
+    p.An = (TS*)g.A[n];
+    p.lda = g.lda;
+    p.Gp = (const TS*)g.Gp[n];
+    p.gp_elems = g.gp_elems;
+    p.lambda = g.lambda;
+    p.partials = m.partials;
+    p.sse_row = g.sse_row[n];
+    p.lit_part = literal ? g.lit_part : nullptr;
+    p.fail = g.d_fail;
+    p.work = g.d_work;
+    p.policy = g.policy;
+    return p;
+}
+
+int launch_update_kernel(int n, bool literal) {
+    const int grid = literal ? g.grid_lit : g.grid_upd;
+    if (g.mi[n].nslices == 0) return PTUCKER_OK;
+    CK(cudaMemsetAsync(g.d_work, 0, sizeof(unsigned int), S()));
+    if (g.prec == PTUCKER_F64) {
+        UpdateParams<double> p = make_params<double>(n, literal);
+        g.kern->launch(&p, literal, grid, S());
+    } else {
+        UpdateParams<float> p = make_params<float>(n, literal);
+        g.kern->launch(&p, literal, grid, S());
+    }
+    CK(cudaGetLastError());
+    return PTUCKER_OK;
+}
+
+int rebuild_gp() {
+    for (int n = 0; n < g.N; ++n) launch_permute_core(g.G, g.Gp[n], g.esz, g.N, g.J, n, S());
+    CK(cudaGetLastError());
+    return PTUCKER_OK;
+}
+
+int choose_kernel() {
+    const int last64 = (g.prec == PTUCKER_F64) ? 1 : (g.policy ? 1 : 0);
+    g.kern = find_update_kernel(g.prec, last64, g.N, g.J);
+    if (!g.kern) return fail(PTUCKER_EINVAL, "no compiled kernel for N=%d J=%d", g.N, g.J);
+    int nsm = 148;
+    CK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, g.device));
+    const size_t smem = (size_t)g.gp_elems * g.esz;
+    int occ = g.kern->occupancy(false, smem);
+    int occl = g.kern->occupancy(true, smem);
+    CK(cudaGetLastError());
+    if (occ < 1 || occl < 1) return fail(PTUCKER_ERESOURCE, "update kernel does not fit on an SM (smem %zu B)", smem);
+    g.grid_upd = nsm * occ;
+    g.grid_lit = nsm * occl;
+    return PTUCKER_OK;
+}
+
+void free_all() {
+    g.arena.release_all();
+    g.scratch.release_all();
+    for (int n = 0; n < kMaxN; ++n) {
+        g.mi[n] = ModeIndex();
+        g.A[n] = nullptr;
+        g.Gp[n] = nullptr;
+        g.sse_row[n] = nullptr;
+    }
+    g.G = g.Gtmp = nullptr;
+    g.lit_part = g.red_part = g.red_out = g.qr = g.qd = nullptr;
+    g.d_fail = g.d_qrfail = nullptr;
+    g.d_work = nullptr;
+    g.inited = false;
+    g.sse_mode = -1;
+}
+
+void partition_rows(const int64_t* row_ptr, int64_t I, int world, int64_t* bounds) {
+    const int64_t nnz = row_ptr[I];
+    bounds[0] = 0;
+    for (int w = 1; w < world; ++w) {
+        const int64_t target = (w * nnz + world - 1) / world;
+        bounds[w] = std::lower_bound(row_ptr, row_ptr + I + 1, target) - row_ptr;
+        if (bounds[w] > I) bounds[w] = I;
+    }
+    bounds[world] = I;
+}
+
+}  // namespace
+}  // namespace pt
+
+using namespace pt;
+
+extern "C" {
+
+int32_t ptucker_version(void) { return 100; }
+
+const char* ptucker_last_error(void) { return g_err.c_str(); }
+
+int ptucker_get_unique_id(uint8_t out[128]) {
+    if (!out) return fail(PTUCKER_EINVAL, "null id buffer");
+    ncclUniqueId id;
+    NK(ncclGetUniqueId(&id));
+    static_assert(sizeof(id) == 128, "ncclUniqueId size");
+    memcpy(out, &id, 128);
+    return PTUCKER_OK;
+}
+
+int ptucker_comm_init(int32_t rank, int32_t world, const uint8_t id[128]) {
+    if (world < 1 || rank < 0 || rank >= world) return fail(PTUCKER_EINVAL, "bad rank/world %d/%d", rank, world);
+    if (g.comm) {
+        ncclCommDestroy(g.comm);
+        g.comm = nullptr;
+    }
+    g.rank = rank;
+    g.world = world;
+    if (world > 1) {
+        if (!id) return fail(PTUCKER_EINVAL, "null id");
+        ncclUniqueId uid;
+        memcpy(&uid, id, 128);
+        NK(ncclCommInitRank(&g.comm, world, uid, rank));
+    }
+    return PTUCKER_OK;
+}
+
+int ptucker_partition_rows(const int64_t* row_ptr, int64_t I, int32_t world, int64_t* bounds) {
+    if (!row_ptr || !bounds || I < 0 || world < 1) return fail(PTUCKER_EINVAL, "bad partition arguments");
+    partition_rows(row_ptr, I, world, bounds);
+    return PTUCKER_OK;
+}
+
+int ptucker_set_stream(void* cuda_stream) {
+    if (g.own_stream && g.stream) cudaStreamDestroy(g.stream);
+    g.own_stream = false;
+    g.stream = (cudaStream_t)cuda_stream;
+    if (!g.stream) {
+        CK(cudaStreamCreateWithFlags(&g.stream, cudaStreamNonBlocking));
+        g.own_stream = true;
+    }
+    return PTUCKER_OK;
+}
+
+int ptucker_set_option(const char* key, int64_t value) {
+    if (!key) return fail(PTUCKER_EINVAL, "null key");
+    const std::string k = key;
+    if (k == "policy") {
+        if (value != 0 && value != 1) return fail(PTUCKER_EINVAL, "policy must be 0 or 1");
+        g.policy = (int)value;
+        if (g.inited) return choose_kernel();
+        return PTUCKER_OK;
+    }
+    if (k == "seg_len") {
+        if (value < 1 || value > (1 << 20)) return fail(PTUCKER_EINVAL, "seg_len out of range");
+        if (g.inited) return fail(PTUCKER_ESTATE, "seg_len must be set before ptucker_init");
+        g.seg_len = (int)value;
+        return PTUCKER_OK;
+    }
+    if (k == "time_kernels") {
+        g.time_kernels = value != 0;
+        return PTUCKER_OK;
+    }
+    return fail(PTUCKER_EINVAL, "unknown option '%s'", key);
+}
+
+int ptucker_init(const int32_t* coords, const void* vals, int32_t vals_dtype, int64_t nnz, int32_t order,
+                 const int64_t* dims, const int32_t* core_dims, double lambda, uint64_t seed) {
+    // ---- validation (synchronous, EINVAL) ----
+    if (!coords || !vals || !dims || !core_dims) return fail(PTUCKER_EINVAL, "null argument");
+    if (vals_dtype != PTUCKER_F32 && vals_dtype != PTUCKER_F64) return fail(PTUCKER_EINVAL, "bad vals_dtype");
+    if (order < 2 || order > kMaxN) return fail(PTUCKER_EINVAL, "order %d not in 2..%d", order, kMaxN);
+    if (nnz < 1 || nnz > INT32_MAX) return fail(PTUCKER_EINVAL, "nnz %lld out of range", (long long)nnz);
+    if (!(lambda > 0.0) || !std::isfinite(lambda)) return fail(PTUCKER_EINVAL, "lambda must be > 0");
+    for (int n = 0; n < order; ++n) {
+        if (dims[n] < 1 || dims[n] > INT32_MAX) return fail(PTUCKER_EINVAL, "dims[%d] out of range", n);
+        if (core_dims[n] != core_dims[0]) return fail(PTUCKER_EINVAL, "unequal core dims are not supported");
+    }
+    const int J = core_dims[0];
+    if (J < 1) return fail(PTUCKER_EINVAL, "core dim must be >= 1");
+    for (int64_t e = 0; e < nnz; ++e)
+        for (int n = 0; n < order; ++n) {
+            const int32_t c = coords[e * order + n];
+            if (c < 0 || c >= dims[n])
+                return fail(PTUCKER_EINVAL, "coordinate %d of entry %lld out of range", n, (long long)e);
+        }
+    const int esz = vals_dtype == PTUCKER_F64 ? 8 : 4;
+    for (int64_t e = 0; e < nnz; ++e) {
+        const double v = esz == 8 ? ((const double*)vals)[e] : ((const float*)vals)[e];
+        if (!std::isfinite(v)) return fail(PTUCKER_EINVAL, "value of entry %lld is not finite", (long long)e);
+    }
+    {
+        const int last64 = (vals_dtype == PTUCKER_F64) ? 1 : (g.policy ? 1 : 0);
+        if (!find_update_kernel(vals_dtype, last64, order, J))
+            return fail(PTUCKER_EINVAL, "(N=%d, J=%d) is not a compiled kernel shape", order, J);
+    }
+    // ---- fresh context ----
+    free_all();
+    CK(cudaGetDevice(&g.device));
+    if (!g.stream) {
+        CK(cudaStreamCreateWithFlags(&g.stream, cudaStreamNonBlocking));
+        g.own_stream = true;
+    }
+    g.N = order;
+    g.J = J;
+    g.prec = vals_dtype;
+    g.esz = esz;
+    g.nnz = nnz;
+    g.lambda = lambda;
+    g.seed = seed;
+    for (int n = 0; n < order; ++n) g.dims[n] = dims[n];
+    g.lda = factor_ld(J, esz);
+    int64_t nblk = 1;
+    for (int l = 0; l < order - 2; ++l) nblk *= J;
+    g.gp_elems = (int)(nblk * gblk(J, esz));
+    DeviceArena& A = g.arena;
+    CK(A.alloc((void**)&g.d_fail, sizeof(int)));
+    CK(A.alloc((void**)&g.d_qrfail, sizeof(int)));
+    CK(A.alloc((void**)&g.d_work, sizeof(unsigned int)));
+    CK(A.alloc((void**)&g.red_part, 256 * sizeof(double)));
+    CK(A.alloc((void**)&g.red_out, 4 * sizeof(double)));
+    CK(A.alloc((void**)&g.qr, (5 * 256 + 256 * 256) * sizeof(double)));
+    CK(cudaMemsetAsync(g.d_fail, 0, sizeof(int), S()));
+    CK(cudaMemsetAsync(g.d_qrfail, 0, sizeof(int), S()));
+    // ---- init (Alg. 2 line 1) ----
+    int64_t gsize = 1;
+    for (int n = 0; n < order; ++n) gsize *= J;
+    CK(A.alloc(&g.G, gsize * esz));
+    CK(A.alloc(&g.Gtmp, gsize * esz));
+    launch_init_uniform(g.G, esz, 1, (int)gsize, (int)gsize, seed, 0, S());
+    for (int n = 0; n < order; ++n) {
+        CK(A.alloc(&g.A[n], dims[n] * g.lda * esz));
+        CK(cudaMemsetAsync(g.A[n], 0, dims[n] * g.lda * esz, S()));
+        launch_init_uniform(g.A[n], esz, dims[n], J, g.lda, seed, (uint64_t)(1 + n), S());
+        CK(A.alloc(&g.Gp[n], (size_t)g.gp_elems * esz));
+        CK(A.alloc((void**)&g.sse_row[n], dims[n] * sizeof(double)));
+        CK(cudaMemsetAsync(g.sse_row[n], 0, dims[n] * sizeof(double), S()));
+    }
+    int rc = rebuild_gp();
+    if (rc) return rc;
+    // ---- device index of every mode ----
+    DeviceArena input;
+    int32_t* d_coords = nullptr;
+    void* d_vals = nullptr;
+    CK(input.alloc((void**)&d_coords, (size_t)nnz * order * sizeof(int32_t)));
+    CK(input.alloc(&d_vals, (size_t)nnz * esz));
+    CK(cudaMemcpyAsync(d_coords, coords, (size_t)nnz * order * sizeof(int32_t), cudaMemcpyHostToDevice, S()));
+    CK(cudaMemcpyAsync(d_vals, vals, (size_t)nnz * esz, cudaMemcpyHostToDevice, S()));
+    for (int n = 0; n < order; ++n) {
+        ModeIndex& m = g.mi[n];
+        CK(build_mode_csr(d_coords, nnz, order, n, dims[n], m, g.arena, g.scratch, S()));
+        m.bounds.assign((size_t)g.world + 1, 0);
+        partition_rows(m.h_row_ptr.data(), dims[n], g.world, m.bounds.data());
+        CK(build_mode_sell(d_coords, d_vals, esz, nnz, order, n, J, g.seg_len, m.bounds[g.rank],
+                           m.bounds[g.rank + 1], m, g.arena, g.scratch, S()));
+    }
+    CK(A.alloc((void**)&g.lit_part, std::max<int64_t>(g.mi[0].nslices * 32, 1) * sizeof(double)));
+    CK(cudaStreamSynchronize(S()));
+    input.release_all();
+    g.inited = true;
+    rc = choose_kernel();
+    if (rc) {
+        g.inited = false;
+        return rc;
+    }
+    g.sse_mode = -1;
+    return PTUCKER_OK;
+}
+
+int ptucker_update_mode(int32_t n) {
+    int rc = require_init();
+    if (rc) return rc;
+    if (n < 0 || n >= g.N) return fail(PTUCKER_EINVAL, "mode %d out of range", n);
+    g.last_fail_mode = n;
+    rc = timed("update", [&]() -> int { return launch_update_kernel(n, false); });
+    if (rc) return rc;
+    ModeIndex& m = g.mi[n];
+    if (m.nheavy > 0) {
+        rc = timed("finalize", [&]() -> int {
+            launch_heavy_finalize(m.nheavy, m.hrow, m.hnseg, m.hpbase, m.partials, g.J, g.lambda, g.A[n], g.esz,
+                                  g.lda, g.sse_row[n], g.d_fail, S());
+            CK(cudaGetLastError());
+            return PTUCKER_OK;
+        });
+        if (rc) return rc;
+    }
+    if (g.world > 1) {
+        rc = timed("allgather", [&]() -> int {
+            // all-gather-v of the row blocks (grouped broadcasts, in place)
+            const ncclDataType_t dt = g.prec == PTUCKER_F64 ? ncclDouble : ncclFloat;
+            NK(ncclGroupStart());
+            for (int r = 0; r < g.world; ++r) {
+                const int64_t b0 = m.bounds[r], b1 = m.bounds[r + 1];
+                if (b1 <= b0) continue;
+                char* p = (char*)g.A[n] + (size_t)b0 * g.lda * g.esz;
+                NK(ncclBroadcast(p, p, (size_t)(b1 - b0) * g.lda, dt, r, g.comm, S()));
+            }
+            NK(ncclGroupEnd());
+            return PTUCKER_OK;
+        });
+        if (rc) return rc;
+    }
+    g.sse_mode = n;
+    return PTUCKER_OK;
+}
+
+int ptucker_sweep(void) {
+    int rc = require_init();
+    if (rc) return rc;
+    for (int n = 0; n < g.N; ++n) {
+        rc = ptucker_update_mode(n);
+        if (rc) return rc;
+    }
+    return PTUCKER_OK;
+}
+
+static int finish_error(double* out) {
+    if (g.world > 1) NK(ncclAllReduce(g.red_out, g.red_out, 1, ncclDouble, ncclSum, g.comm, S()));
+    double h = 0.0;
+    CK(cudaMemcpyAsync(&h, g.red_out, sizeof(double), cudaMemcpyDeviceToHost, S()));
+    int rc = sync_and_check();
+    if (rc) return rc;
+    *out = std::sqrt(std::max(h, 0.0));
+    return PTUCKER_OK;
+}
+
+int ptucker_error_literal(double* out) {
+    int rc = require_init();
+    if (rc) return rc;
+    if (!out) return fail(PTUCKER_EINVAL, "null out");
+    rc = timed("literal", [&]() -> int { return launch_update_kernel(0, true); });
+    if (rc) return rc;
+    rc = timed("error_reduce", [&]() -> int {
+        launch_sum(g.lit_part, g.mi[0].nslices * 32, g.red_part, g.red_out, S());
+        CK(cudaGetLastError());
+        return PTUCKER_OK;
+    });
+    if (rc) return rc;
+    return finish_error(out);
+}
+
+int ptucker_error(double* out) {
+    int rc = require_init();
+    if (rc) return rc;
+    if (!out) return fail(PTUCKER_EINVAL, "null out");
+    if (g.sse_mode < 0) return ptucker_error_literal(out);
+    const ModeIndex& m = g.mi[g.sse_mode];
+    rc = timed("error_reduce", [&]() -> int {
+        launch_sum(g.sse_row[g.sse_mode] + m.r0, m.r1 - m.r0, g.red_part, g.red_out, S());
+        CK(cudaGetLastError());
+        return PTUCKER_OK;
+    });
+    if (rc) return rc;
+    return finish_error(out);
+}
+
+int ptucker_orthogonalize(void) {
+    int rc = require_init();
+    if (rc) return rc;
+    const int J = g.J;
+    for (int n = 0; n < g.N; ++n)
+        if (g.dims[n] < J) return fail(PTUCKER_EINVAL, "orthogonalize needs I_%d >= J", n);
+    if (!g.qd) {
+        int64_t imax = 0;
+        for (int n = 0; n < g.N; ++n) imax = std::max(imax, g.dims[n]);
+        CK(g.arena.alloc((void**)&g.qd, (size_t)imax * J * sizeof(double)));
+    }
+    double* W = g.qr;
+    double* R1 = W + 256;
+    double* R2 = R1 + 256;
+    double* R = R2 + 256;
+    double* part = g.qr + 5 * 256;
+    rc = timed("qr", [&]() -> int {
+        for (int n = 0; n < g.N; ++n) {
+            const int64_t I = g.dims[n];
+            launch_gram(g.A[n], g.esz, false, I, J, g.lda, part, W, S());
+            launch_chol_upper(W, J, R1, g.d_qrfail, n + 1, S());
+            launch_apply_rinv(g.A[n], g.esz, g.lda, g.qd, 8, J, I, J, R1, S());
+            launch_gram(g.qd, 8, true, I, J, J, part, W, S());
+            launch_chol_upper(W, J, R2, g.d_qrfail, n + 1, S());
+            launch_apply_rinv(g.qd, 8, J, g.A[n], g.esz, g.lda, I, J, R2, S());
+            launch_mat_upper_mul(R2, R1, R, J, S());
+            launch_core_mode_product(g.G, g.Gtmp, g.esz, g.N, J, n, R, S());
+            std::swap(g.G, g.Gtmp);
+        }
+        CK(cudaGetLastError());
+        return rebuild_gp();
+    });
+    if (rc) return rc;
+    g.sse_mode = -1;
+    return sync_and_check();
+}
+
+int ptucker_get_factor(int32_t n, void* out) {
+    int rc = require_init();
+    if (rc) return rc;
+    if (n < 0 || n >= g.N || !out) return fail(PTUCKER_EINVAL, "bad mode or buffer");
+    CK(cudaMemcpy2DAsync(out, (size_t)g.J * g.esz, g.A[n], (size_t)g.lda * g.esz, (size_t)g.J * g.esz, g.dims[n],
+                         cudaMemcpyDeviceToHost, S()));
+    return sync_and_check();
+}
+
+int ptucker_set_factor(int32_t n, const void* in) {
+    int rc = require_init();
+    if (rc) return rc;
+    if (n < 0 || n >= g.N || !in) return fail(PTUCKER_EINVAL, "bad mode or buffer");
+    CK(cudaMemcpy2DAsync(g.A[n], (size_t)g.lda * g.esz, in, (size_t)g.J * g.esz, (size_t)g.J * g.esz, g.dims[n],
+                         cudaMemcpyHostToDevice, S()));
+    g.sse_mode = -1;
+    CK(cudaStreamSynchronize(S()));
+    return PTUCKER_OK;
+}
+
+int ptucker_get_core(void* out) {
+    int rc = require_init();
+    if (rc) return rc;
+    if (!out) return fail(PTUCKER_EINVAL, "null buffer");
+    int64_t gsize = 1;
+    for (int n = 0; n < g.N; ++n) gsize *= g.J;
+    CK(cudaMemcpyAsync(out, g.G, gsize * g.esz, cudaMemcpyDeviceToHost, S()));
+    return sync_and_check();
+}
+
+int ptucker_set_core(const void* in) {
+    int rc = require_init();
+    if (rc) return rc;
+    if (!in) return fail(PTUCKER_EINVAL, "null buffer");
+    int64_t gsize = 1;
+    for (int n = 0; n < g.N; ++n) gsize *= g.J;
+    CK(cudaMemcpyAsync(g.G, in, gsize * g.esz, cudaMemcpyHostToDevice, S()));
+    rc = rebuild_gp();
+    if (rc) return rc;
+    g.sse_mode = -1;
+    CK(cudaStreamSynchronize(S()));
+    return PTUCKER_OK;
+}
+
+int ptucker_get_mode_index(int32_t n, int64_t* row_ptr, int64_t* perm) {
+    int rc = require_init();
+    if (rc) return rc;
+    if (n < 0 || n >= g.N || !row_ptr || !perm) return fail(PTUCKER_EINVAL, "bad mode or buffer");
+    const ModeIndex& m = g.mi[n];
+    memcpy(row_ptr, m.h_row_ptr.data(), sizeof(int64_t) * (size_t)(m.I + 1));
+    std::vector<int32_t> p32((size_t)g.nnz);
+    CK(cudaMemcpyAsync(p32.data(), m.perm, sizeof(int32_t) * (size_t)g.nnz, cudaMemcpyDeviceToHost, S()));
+    CK(cudaStreamSynchronize(S()));
+    for (int64_t e = 0; e < g.nnz; ++e) perm[e] = p32[(size_t)e];
+    return PTUCKER_OK;
+}
+
+int ptucker_get_partition(int32_t n, int64_t* bounds) {
+    int rc = require_init();
+    if (rc) return rc;
+    if (n < 0 || n >= g.N || !bounds) return fail(PTUCKER_EINVAL, "bad mode or buffer");
+    memcpy(bounds, g.mi[n].bounds.data(), sizeof(int64_t) * g.mi[n].bounds.size());
+    return PTUCKER_OK;
+}
+
+int ptucker_kernel_stats(const char* name, double* total_ms, int64_t* launches) {
+    if (!name || !total_ms || !launches) return fail(PTUCKER_EINVAL, "null argument");
+    int rc = fold_stats();
+    if (rc) return rc;
+    auto it = g.stats.find(name);
+    *total_ms = it == g.stats.end() ? 0.0 : it->second.first;
+    *launches = it == g.stats.end() ? 0 : it->second.second;
+    return PTUCKER_OK;
+}
+
+int ptucker_reset_kernel_stats(void) {
+    int rc = fold_stats();
+    g.stats.clear();
+    return rc;
+}
+
+int ptucker_info(char* buf, int32_t len) {
+    if (!buf || len <= 0) return fail(PTUCKER_EINVAL, "bad buffer");
+    std::string s = "{";
+    char tmp[512];
+    snprintf(tmp, sizeof(tmp),
+             "\"inited\": %s, \"N\": %d, \"J\": %d, \"prec\": \"%s\", \"policy\": \"%s\", \"nnz\": %lld, "
+             "\"lambda\": %.17g, \"seg_len\": %d, \"rank\": %d, \"world\": %d, \"grid_update\": %d, "
+             "\"threads_per_cta\": %d, \"smem_core_bytes\": %d, \"modes\": [",
+             g.inited ? "true" : "false", g.N, g.J, g.prec == PTUCKER_F64 ? "f64" : "f32",
+             g.prec == PTUCKER_F64 ? "F64" : (g.policy ? "F32-B" : "F32-A"), (long long)g.nnz, g.lambda, g.seg_len,
+             g.rank, g.world, g.grid_upd, kUpdThreads, g.gp_elems * g.esz);
+    s += tmp;
+    for (int n = 0; n < g.N; ++n) {
+        const ModeIndex& m = g.mi[n];
+        snprintf(tmp, sizeof(tmp),
+                 "%s{\"I\": %lld, \"rows\": [%lld, %lld], \"segments\": %lld, \"slices\": %lld, \"slots\": %lld, "
+                 "\"heavy_rows\": %lld}",
+                 n ? ", " : "", (long long)m.I, (long long)m.r0, (long long)m.r1, (long long)m.nsegments,
+                 (long long)m.nslices, (long long)m.nslots, (long long)m.nheavy);
+        s += tmp;
+    }
+    s += "]}";
+    snprintf(buf, (size_t)len, "%s", s.c_str());
+    return (int)s.size() < len ? PTUCKER_OK : fail(PTUCKER_EINVAL, "buffer too small (%zu)", s.size() + 1);
+}
+
+int ptucker_synchronize(void) {
+    int rc = require_init();
+    if (rc) return rc;
+    return sync_and_check();
+}
+
+int ptucker_finalize(void) {
+    if (g.inited) {
+        cudaStreamSynchronize(S());
+        fold_stats();
+    }
+    free_all();
+    if (g.comm) {
+        ncclCommDestroy(g.comm);
+        g.comm = nullptr;
+    }
+    g.world = 1;
+    g.rank = 0;
+    if (g.own_stream && g.stream) cudaStreamDestroy(g.stream);
+    g.stream = nullptr;
+    g.own_stream = false;
+    return PTUCKER_OK;
+}
+
+}  // extern "C"

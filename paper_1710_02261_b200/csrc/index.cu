@@ -1,0 +1,324 @@
+// index.cu -- device-side build of the mode-slice index Omega^(n)_{i_n} (P:257,
+// P:566) and of the SELL-32 segment layout the update kernel streams.
+//
+//   1. keys = coords[:, n]; stable LSD radix sort of (key, entry id) -> perm
+//      (ties keep input order, reading R25); row_ptr by boundary scan.
+//   2. This rank's row block [r0, r1) (nnz-balanced, see ptucker_partition_rows).
+//   3. Every row becomes ceil(len/S) segments of <= S entries (S = seg_len;
+//      an empty row is one segment of length 0, which solves to a = 0).  Rows
+//      with more than one segment are "heavy": their segments write partial
+//      (B, c, sum x^2) records that k_heavy_finalize reduces in a fixed order.
+//   4. Segments are stably sorted by length (descending) and cut into slices
+//      of 32 -- one warp per slice, one lane per segment, so lanes of a warp
+//      do near-equal work (the paper's load balancing concern).
+//   5. Entries are scattered into SELL-32 order: entry e of lane l of slice s
+//      at slot slice_off[s] + e*32 + l, so a warp's loads are coalesced.
+#include <cub/cub.cuh>
+
+#include <cstdint>
+
+#include "index.cuh"
+#include "internal.cuh"
+#include "kernels.cuh"
+
+namespace pt {
+
+__global__ void k_extract_col(const int32_t* coords, int64_t nnz, int N, int n, int32_t* keys, int32_t* iota) {
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < nnz; e += (int64_t)gridDim.x * blockDim.x) {
+        keys[e] = coords[e * N + n];
+        iota[e] = (int32_t)e;
+    }
+}
+
+void launch_extract_col(const int32_t* coords, int64_t nnz, int N, int n, int32_t* keys, int32_t* iota,
+                        cudaStream_t st) {
+    int grid = (int)((nnz + 255) / 256);
+    if (grid > 148 * 16) grid = 148 * 16;
+    k_extract_col<<<grid, 256, 0, st>>>(coords, nnz, N, n, keys, iota);
+}
+
+__global__ void k_iota(int32_t* out, int64_t n) {
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x)
+        out[e] = (int32_t)e;
+}
+
+static int grid_for(int64_t n);
+
+// row_ptr[i] = first position whose key >= i (sorted keys); row_ptr[I] = nnz.
+__global__ void k_row_ptr(const int32_t* sk, int64_t nnz, int64_t I, int64_t* row_ptr) {
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e <= nnz; e += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t prev = (e == 0) ? -1 : sk[e - 1];
+        const int64_t cur = (e == nnz) ? I : sk[e];
+        for (int64_t r = prev + 1; r <= cur; ++r) row_ptr[r] = e;
+    }
+}
+
+void launch_row_ptr(const int32_t* sorted_keys, int64_t nnz, int64_t I, int64_t* row_ptr, cudaStream_t st) {
+    int grid = (int)((nnz + 256) / 256);
+    if (grid > 148 * 16) grid = 148 * 16;
+    k_row_ptr<<<grid, 256, 0, st>>>(sorted_keys, nnz, I, row_ptr);
+}
+
+// Per row of the block: number of segments, heavy flag, heavy segment count.
+__global__ void k_seg_count(const int64_t* row_ptr, int64_t r0, int64_t nrows, int S, int64_t* nseg, int64_t* hflag,
+                            int64_t* hseg) {
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < nrows; t += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t len = row_ptr[r0 + t + 1] - row_ptr[r0 + t];
+        const int64_t ns = len == 0 ? 1 : (len + S - 1) / S;
+        nseg[t] = ns;
+        hflag[t] = ns > 1 ? 1 : 0;
+        hseg[t] = ns > 1 ? ns : 0;
+    }
+}
+
+__global__ void k_seg_fill(const int64_t* row_ptr, int64_t r0, int64_t nrows, int S, int PW, const int64_t* seg_start,
+                           const int64_t* hidx, const int64_t* hbase, int32_t* seg_row, int32_t* seg_sidx,
+                           int32_t* seg_len, uint32_t* seg_key, int64_t* seg_pidx, int32_t* seg_pstride,
+                           int32_t* hrow, int32_t* hnseg, int64_t* hpbase) {
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < nrows; t += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t row = r0 + t;
+        const int64_t len = row_ptr[row + 1] - row_ptr[row];
+        const int64_t ns = len == 0 ? 1 : (len + S - 1) / S;
+        const bool heavy = ns > 1;
+        if (heavy) {
+            hrow[hidx[t]] = (int32_t)row;
+            hnseg[hidx[t]] = (int32_t)ns;
+            hpbase[hidx[t]] = hbase[t] * PW;
+        }
+        for (int64_t s = 0; s < ns; ++s) {
+            const int64_t sid = seg_start[t] + s;
+            const int64_t l = len - s * S < S ? len - s * S : S;
+            seg_row[sid] = (int32_t)row;
+            seg_sidx[sid] = (int32_t)s;
+            seg_len[sid] = (int32_t)l;
+            seg_key[sid] = (uint32_t)(S - l);  // ascending key = descending length
+            seg_pidx[sid] = heavy ? hbase[t] * PW + s : -1;
+            seg_pstride[sid] = heavy ? (int32_t)ns : 0;
+        }
+    }
+}
+
+__global__ void k_slices(const int32_t* order, int64_t nseg, int64_t nslices, const int32_t* seg_row,
+                         const int32_t* seg_sidx, const int32_t* seg_len, const int64_t* seg_pidx,
+                         const int32_t* seg_pstride, int32_t* slice_len, int64_t* slice_slots, int32_t* lane_row,
+                         int32_t* lane_len, int64_t* lane_pidx, int32_t* lane_pstride, int32_t* lane_sidx) {
+    const int64_t total = nslices * 32;
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
+        if (t < nseg) {
+            const int32_t sid = order[t];
+            lane_row[t] = seg_row[sid];
+            lane_len[t] = seg_len[sid];
+            lane_pidx[t] = seg_pidx[sid];
+            lane_pstride[t] = seg_pstride[sid];
+            lane_sidx[t] = seg_sidx[sid];
+        } else {
+            lane_row[t] = -1;
+            lane_len[t] = 0;
+            lane_pidx[t] = -1;
+            lane_pstride[t] = 0;
+            lane_sidx[t] = 0;
+        }
+        if ((t & 31) == 0) {
+            const int32_t l = (t < nseg) ? seg_len[order[t]] : 0;
+            slice_len[t >> 5] = l;
+            slice_slots[t >> 5] = (int64_t)l * 32;
+        }
+    }
+}
+
+template <typename TS>
+__global__ void k_sell_fill(int64_t nslices, const int64_t* slice_off, const int32_t* lane_row,
+                            const int32_t* lane_len, const int32_t* lane_sidx, const int64_t* row_ptr,
+                            const int32_t* perm, int S, const int32_t* coords, const TS* vals, int N, int n,
+                            int32_t* const* sc, TS* sv) {
+    const int64_t total = nslices * 32;
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
+        const int32_t row = lane_row[t];
+        if (row < 0) continue;
+        const int32_t len = lane_len[t];
+        const int64_t src0 = row_ptr[row] + (int64_t)lane_sidx[t] * S;
+        const int64_t dst0 = slice_off[t >> 5] + (t & 31);
+        for (int32_t e = 0; e < len; ++e) {
+            const int64_t src = perm[src0 + e];
+            const int64_t dst = dst0 + (int64_t)e * 32;
+            int l = 0;
+            for (int m = 0; m < N; ++m) {
+                if (m == n) continue;
+                sc[l][dst] = coords[src * N + m];
+                ++l;
+            }
+            sv[dst] = vals[src];
+        }
+    }
+}
+
+static int grid_for(int64_t n) {
+    int64_t g = (n + 255) / 256;
+    if (g > 148 * 16) g = 148 * 16;
+    if (g < 1) g = 1;
+    return (int)g;
+}
+
+#define IB_CHECK(x)                                  \
+    do {                                             \
+        cudaError_t e_ = (x);                        \
+        if (e_ != cudaSuccess) return e_;            \
+    } while (0)
+
+template <typename T>
+static cudaError_t dalloc(T** p, int64_t n, DeviceArena& arena) {
+    return arena.alloc((void**)p, (size_t)(n > 0 ? n : 1) * sizeof(T));
+}
+
+cudaError_t build_mode_csr(const int32_t* d_coords, int64_t nnz, int N, int n, int64_t I, ModeIndex& mi,
+                           DeviceArena& arena, DeviceArena& scratch, cudaStream_t st) {
+    int32_t *keys = nullptr, *keys_sorted = nullptr, *iota = nullptr;
+    IB_CHECK(dalloc(&keys, nnz, scratch));
+    IB_CHECK(dalloc(&keys_sorted, nnz, scratch));
+    IB_CHECK(dalloc(&iota, nnz, scratch));
+    IB_CHECK(dalloc(&mi.perm, nnz, arena));
+    IB_CHECK(dalloc(&mi.row_ptr, I + 1, arena));
+    launch_extract_col(d_coords, nnz, N, n, keys, iota, st);
+    int bits = 1;
+    while ((int64_t(1) << bits) < I) ++bits;
+    size_t tb = 0;
+    IB_CHECK(cub::DeviceRadixSort::SortPairs(nullptr, tb, keys, keys_sorted, iota, mi.perm, (int)nnz, 0, bits, st));
+    void* tmp = nullptr;
+    IB_CHECK(scratch.alloc(&tmp, tb));
+    IB_CHECK(cub::DeviceRadixSort::SortPairs(tmp, tb, keys, keys_sorted, iota, mi.perm, (int)nnz, 0, bits, st));
+    launch_row_ptr(keys_sorted, nnz, I, mi.row_ptr, st);
+    mi.I = I;
+    mi.h_row_ptr.resize((size_t)I + 1);
+    IB_CHECK(cudaMemcpyAsync(mi.h_row_ptr.data(), mi.row_ptr, sizeof(int64_t) * (size_t)(I + 1),
+                             cudaMemcpyDeviceToHost, st));
+    IB_CHECK(cudaStreamSynchronize(st));
+    scratch.release_all();
+    return cudaSuccess;
+}
+
+template <typename T>
+static cudaError_t exclusive_sum(const T* in, T* out, int64_t n, DeviceArena& scratch, cudaStream_t st) {
+    size_t tb = 0;
+    IB_CHECK(cub::DeviceScan::ExclusiveSum(nullptr, tb, in, out, (int)n, st));
+    void* tmp = nullptr;
+    IB_CHECK(scratch.alloc(&tmp, tb));
+    IB_CHECK(cub::DeviceScan::ExclusiveSum(tmp, tb, in, out, (int)n, st));
+    return cudaSuccess;
+}
+
+cudaError_t build_mode_sell(const int32_t* d_coords, const void* d_vals, int elem_bytes, int64_t nnz, int N, int n,
+                            int J, int S, int64_t r0, int64_t r1, ModeIndex& mi, DeviceArena& arena,
+                            DeviceArena& scratch, cudaStream_t st) {
+    (void)nnz;
+    const int PW = rec_width(J);
+    const int64_t nrows = r1 - r0;
+    mi.r0 = r0;
+    mi.r1 = r1;
+    // ---- 3. segments ----
+    int64_t *nseg = nullptr, *hflag = nullptr, *hseg = nullptr, *seg_start = nullptr, *hidx = nullptr,
+            *hbase = nullptr;
+    const int64_t nr1 = nrows + 1;  // trailing zero gives the totals from the exclusive scans
+    IB_CHECK(dalloc(&nseg, nr1, scratch));
+    IB_CHECK(dalloc(&hflag, nr1, scratch));
+    IB_CHECK(dalloc(&hseg, nr1, scratch));
+    IB_CHECK(dalloc(&seg_start, nr1, scratch));
+    IB_CHECK(dalloc(&hidx, nr1, scratch));
+    IB_CHECK(dalloc(&hbase, nr1, scratch));
+    IB_CHECK(cudaMemsetAsync(nseg, 0, sizeof(int64_t) * nr1, st));
+    IB_CHECK(cudaMemsetAsync(hflag, 0, sizeof(int64_t) * nr1, st));
+    IB_CHECK(cudaMemsetAsync(hseg, 0, sizeof(int64_t) * nr1, st));
+    if (nrows > 0) k_seg_count<<<grid_for(nrows), 256, 0, st>>>(mi.row_ptr, r0, nrows, S, nseg, hflag, hseg);
+    IB_CHECK(exclusive_sum(nseg, seg_start, nr1, scratch, st));
+    IB_CHECK(exclusive_sum(hflag, hidx, nr1, scratch, st));
+    IB_CHECK(exclusive_sum(hseg, hbase, nr1, scratch, st));
+    int64_t tot[3];
+    IB_CHECK(cudaMemcpyAsync(&tot[0], seg_start + nrows, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+    IB_CHECK(cudaMemcpyAsync(&tot[1], hidx + nrows, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+    IB_CHECK(cudaMemcpyAsync(&tot[2], hbase + nrows, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+    IB_CHECK(cudaStreamSynchronize(st));
+    const int64_t nS = tot[0];
+    mi.nheavy = tot[1];
+    mi.npartial_doubles = tot[2] * PW;
+    mi.nsegments = nS;
+
+    int32_t *seg_row, *seg_sidx, *seg_len, *seg_pstride;
+    uint32_t *seg_key, *seg_key_sorted;
+    int64_t* seg_pidx;
+    int32_t *seg_iota, *order;
+    IB_CHECK(dalloc(&seg_row, nS, scratch));
+    IB_CHECK(dalloc(&seg_sidx, nS, scratch));
+    IB_CHECK(dalloc(&seg_len, nS, scratch));
+    IB_CHECK(dalloc(&seg_pstride, nS, scratch));
+    IB_CHECK(dalloc(&seg_key, nS, scratch));
+    IB_CHECK(dalloc(&seg_key_sorted, nS, scratch));
+    IB_CHECK(dalloc(&seg_pidx, nS, scratch));
+    IB_CHECK(dalloc(&seg_iota, nS, scratch));
+    IB_CHECK(dalloc(&order, nS, scratch));
+    IB_CHECK(dalloc(&mi.hrow, mi.nheavy, arena));
+    IB_CHECK(dalloc(&mi.hnseg, mi.nheavy, arena));
+    IB_CHECK(dalloc(&mi.hpbase, mi.nheavy, arena));
+    IB_CHECK(dalloc(&mi.partials, mi.npartial_doubles, arena));
+    if (nrows > 0)
+        k_seg_fill<<<grid_for(nrows), 256, 0, st>>>(mi.row_ptr, r0, nrows, S, PW, seg_start, hidx, hbase, seg_row,
+                                                    seg_sidx, seg_len, seg_key, seg_pidx, seg_pstride, mi.hrow,
+                                                    mi.hnseg, mi.hpbase);
+    // ---- 4. stable sort of segments by length (descending) ----
+    {
+        if (nS > 0) k_iota<<<grid_for(nS), 256, 0, st>>>(seg_iota, nS);
+        int bits = 1;
+        while ((int64_t(1) << bits) <= S) ++bits;
+        size_t tb = 0;
+        IB_CHECK(cub::DeviceRadixSort::SortPairs(nullptr, tb, seg_key, seg_key_sorted, seg_iota, order, (int)nS, 0,
+                                                 bits, st));
+        void* tmp = nullptr;
+        IB_CHECK(scratch.alloc(&tmp, tb));
+        IB_CHECK(cub::DeviceRadixSort::SortPairs(tmp, tb, seg_key, seg_key_sorted, seg_iota, order, (int)nS, 0, bits,
+                                                 st));
+    }
+    mi.nslices = (nS + 31) / 32;
+    const int64_t nlanes = mi.nslices * 32;
+    int64_t* slice_slots = nullptr;
+    int32_t* lane_sidx = nullptr;
+    IB_CHECK(dalloc(&slice_slots, mi.nslices + 1, scratch));
+    IB_CHECK(dalloc(&lane_sidx, nlanes, scratch));
+    IB_CHECK(dalloc(&mi.slice_len, mi.nslices, arena));
+    IB_CHECK(dalloc(&mi.slice_off, mi.nslices + 1, arena));
+    IB_CHECK(dalloc(&mi.lane_row, nlanes, arena));
+    IB_CHECK(dalloc(&mi.lane_len, nlanes, arena));
+    IB_CHECK(dalloc(&mi.lane_pidx, nlanes, arena));
+    IB_CHECK(dalloc(&mi.lane_pstride, nlanes, arena));
+    IB_CHECK(cudaMemsetAsync(slice_slots, 0, sizeof(int64_t) * (mi.nslices + 1), st));
+    if (nlanes > 0)
+        k_slices<<<grid_for(nlanes), 256, 0, st>>>(order, nS, mi.nslices, seg_row, seg_sidx, seg_len, seg_pidx,
+                                                   seg_pstride, mi.slice_len, slice_slots, mi.lane_row, mi.lane_len,
+                                                   mi.lane_pidx, mi.lane_pstride, lane_sidx);
+    IB_CHECK(exclusive_sum(slice_slots, mi.slice_off, mi.nslices + 1, scratch, st));
+    IB_CHECK(cudaMemcpyAsync(&mi.nslots, mi.slice_off + mi.nslices, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+    IB_CHECK(cudaStreamSynchronize(st));
+    // ---- 5. SELL scatter ----
+    for (int k = 0; k < N - 1; ++k) {
+        IB_CHECK(dalloc(&mi.sc[k], mi.nslots, arena));
+        IB_CHECK(cudaMemsetAsync(mi.sc[k], 0, sizeof(int32_t) * (size_t)(mi.nslots > 0 ? mi.nslots : 1), st));
+    }
+    IB_CHECK(arena.alloc(&mi.sv, (size_t)(mi.nslots > 0 ? mi.nslots : 1) * elem_bytes));
+    IB_CHECK(cudaMemsetAsync(mi.sv, 0, (size_t)(mi.nslots > 0 ? mi.nslots : 1) * elem_bytes, st));
+    int32_t** d_sc = nullptr;
+    IB_CHECK(dalloc(&d_sc, kMaxN, scratch));
+    IB_CHECK(cudaMemcpyAsync(d_sc, mi.sc, sizeof(int32_t*) * kMaxN, cudaMemcpyHostToDevice, st));
+    if (nlanes > 0) {
+        if (elem_bytes == 8)
+            k_sell_fill<double><<<grid_for(nlanes), 256, 0, st>>>(mi.nslices, mi.slice_off, mi.lane_row, mi.lane_len,
+                                                                  lane_sidx, mi.row_ptr, mi.perm, S, d_coords,
+                                                                  (const double*)d_vals, N, n, d_sc, (double*)mi.sv);
+        else
+            k_sell_fill<float><<<grid_for(nlanes), 256, 0, st>>>(mi.nslices, mi.slice_off, mi.lane_row, mi.lane_len,
+                                                                 lane_sidx, mi.row_ptr, mi.perm, S, d_coords,
+                                                                 (const float*)d_vals, N, n, d_sc, (float*)mi.sv);
+    }
+    IB_CHECK(cudaGetLastError());
+    IB_CHECK(cudaStreamSynchronize(st));
+    scratch.release_all();
+    return cudaSuccess;
+}
+
+}  // namespace pt

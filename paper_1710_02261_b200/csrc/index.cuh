@@ -1,0 +1,60 @@
+// index.cuh -- device index of one mode (CSR + SELL-32 segments) and a tiny arena.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <vector>
+
+#include "internal.cuh"
+
+namespace pt {
+
+// Device allocations owned by a context (freed together).
+struct DeviceArena {
+    std::vector<void*> ptrs;
+    cudaError_t alloc(void** p, size_t bytes) {
+        cudaError_t e = cudaMalloc(p, bytes > 0 ? bytes : 1);
+        if (e == cudaSuccess) ptrs.push_back(*p);
+        else *p = nullptr;
+        return e;
+    }
+    void release_all() {
+        for (void* p : ptrs) cudaFree(p);
+        ptrs.clear();
+    }
+    ~DeviceArena() { release_all(); }
+};
+
+struct ModeIndex {
+    int64_t I = 0;
+    // CSR of Omega^(n) over all rows
+    int32_t* perm = nullptr;       // [nnz] entry ids sorted by coordinate n (stable)
+    int64_t* row_ptr = nullptr;    // [I+1]
+    std::vector<int64_t> h_row_ptr;
+    // this rank's row block and its SELL-32 segments
+    int64_t r0 = 0, r1 = 0;
+    int64_t nsegments = 0, nslices = 0, nslots = 0;
+    int32_t* slice_len = nullptr;
+    int64_t* slice_off = nullptr;
+    int32_t* lane_row = nullptr;
+    int32_t* lane_len = nullptr;
+    int64_t* lane_pidx = nullptr;
+    int32_t* lane_pstride = nullptr;
+    int32_t* sc[kMaxN] = {nullptr};  // coordinates of the other modes, SELL order
+    void* sv = nullptr;              // values, SELL order
+    // heavy rows (more than one segment)
+    int64_t nheavy = 0, npartial_doubles = 0;
+    int32_t* hrow = nullptr;
+    int32_t* hnseg = nullptr;
+    int64_t* hpbase = nullptr;
+    double* partials = nullptr;
+    std::vector<int64_t> bounds;     // world+1 row-block bounds
+};
+
+cudaError_t build_mode_csr(const int32_t* d_coords, int64_t nnz, int N, int n, int64_t I, ModeIndex& mi,
+                           DeviceArena& arena, DeviceArena& scratch, cudaStream_t st);
+cudaError_t build_mode_sell(const int32_t* d_coords, const void* d_vals, int elem_bytes, int64_t nnz, int N, int n,
+                            int J, int S, int64_t r0, int64_t r1, ModeIndex& mi, DeviceArena& arena,
+                            DeviceArena& scratch, cudaStream_t st);
+
+}  // namespace pt

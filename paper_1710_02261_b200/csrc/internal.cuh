@@ -1,0 +1,79 @@
+// internal.cuh -- shared declarations of the B200 P-Tucker library (not part of the ABI).
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <string>
+#include <vector>
+
+namespace pt {
+
+constexpr int kMaxN = 5;      // compiled orders N = 2..5
+constexpr int kWarp = 32;
+constexpr int kUpdThreads = 256;  // update kernel CTA size (8 warps, one slice per warp at a time)
+
+// Packed normal-equation record of one row (segment): upper triangle of B
+// (J(J+1)/2), c (J), sum x^2 (1) -- all fp64 (Eq. 10-11).
+__host__ __device__ constexpr int rec_width(int J) { return J * (J + 1) / 2 + J + 1; }
+// Padded row stride of a factor in elements (16-byte rows for vector loads).
+__host__ __device__ constexpr int factor_ld(int J, int elem_bytes) {
+    return elem_bytes == 4 ? (J + 3) / 4 * 4 : (J + 1) / 2 * 2;
+}
+// Permuted core block: the innermost (k_{N-2}, j) J x J block, padded to 16 bytes.
+__host__ __device__ constexpr int gblk(int J, int elem_bytes) {
+    return elem_bytes == 4 ? (J * J + 3) / 4 * 4 : (J * J + 1) / 2 * 2;
+}
+__host__ __device__ constexpr int ipow(int b, int e) { return e == 0 ? 1 : b * ipow(b, e - 1); }
+
+// Arguments of the fused row-update kernel for mode n over this rank's
+// length-sorted segments (SELL-32 layout).
+template <typename TS>
+struct UpdateParams {
+    int n;                        // mode being updated
+    int64_t nslices;              // slices of 32 segments
+    const int64_t* slice_off;     // [nslices] first slot of slice s; entry e of lane l at slice_off + e*32 + l
+    const int32_t* slice_len;     // [nslices] iterations of slice s (= longest segment, lane 0)
+    const int32_t* lane_row;      // [nslices*32] row of the segment in that lane (-1: pad lane)
+    const int32_t* lane_len;      // [nslices*32] entries of that segment
+    const int64_t* lane_pidx;     // [nslices*32] heavy rows: first partial slot (-1: segment is the whole row)
+    const int32_t* lane_pstride;  // [nslices*32] heavy rows: stride between partial components (= #segments of the row)
+    const int32_t* sc[kMaxN - 1]; // SELL coordinates of the other modes (ascending mode order)
+    const TS* sv;                 // SELL values
+    const TS* A[kMaxN - 1];       // the other factors, same order, row stride lda
+    TS* An;                       // A^(n), written
+    int lda;
+    const TS* Gp;                 // core permuted for mode n: [outer J^(N-2)][gblk] with block = [k_{N-2}][j]
+    int gp_elems;                 // elements of Gp (smem copy)
+    double lambda;
+    double* partials;             // heavy-row partial records, component-major per row
+    double* sse_row;              // [I_n] per-row SSE by the identity (fused error, Eq. 5)
+    double* lit_part;             // literal error mode: [nslices*32] per-lane SSE (else null)
+    int* fail;                    // numeric failure flag (row+1)
+    unsigned int* work;           // dynamic slice counter (reset to 0 before launch)
+    int policy;                   // runtime copy of the precision policy (info only)
+};
+
+using UpdateLauncher = void (*)(const void* params, bool literal, int grid, cudaStream_t st);
+using UpdateOccupancy = int (*)(bool literal, size_t smem);
+
+struct UpdateKernel {
+    int prec, last64, N, J;
+    UpdateLauncher launch;
+    UpdateOccupancy occupancy;
+};
+
+// Registries filled by the instantiation units (update_f32a.cu, update_f32b.cu, update_f64.cu).
+const UpdateKernel* update_kernels_f32a(int* count);
+const UpdateKernel* update_kernels_f32b(int* count);
+const UpdateKernel* update_kernels_f64(int* count);
+// Returns nullptr when (prec, last64, N, J) was not compiled.
+const UpdateKernel* find_update_kernel(int prec, int last64, int N, int J);
+
+// (N, J) pairs compiled: N = 2..5, J in {2,3,4,5,8,10}, J^N <= 10^4.
+#define PT_NJ_LIST(X) \
+    X(2, 2) X(2, 3) X(2, 4) X(2, 5) X(2, 8) X(2, 10) \
+    X(3, 2) X(3, 3) X(3, 4) X(3, 5) X(3, 8) X(3, 10) \
+    X(4, 2) X(4, 3) X(4, 4) X(4, 5) X(4, 8) X(4, 10) \
+    X(5, 2) X(5, 3) X(5, 4) X(5, 5)
+
+}  // namespace pt

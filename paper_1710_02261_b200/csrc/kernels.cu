@@ -1,0 +1,371 @@
+// kernels.cu -- small kernels around the hot path: init RNG, core permutation,
+// heavy-row finalize, deterministic sums, CholeskyQR2 and the core update.
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "internal.cuh"
+#include "kernels.cuh"
+
+namespace pt {
+
+// ---------------------------------------------------------------------------
+// Init (Alg. 2 line 1; "random real values between 0 and 1").
+// Reading R2: z = mix64(seed*0x9E3779B97F4A7C15 + (stream+1)*0xD1B54A32D192ED03 + idx),
+// mix64 = SplitMix64 finaliser; f64 = (z>>11)*2^-53, f32 = (z>>40)*2^-24.
+// stream 0 = core (idx = C-order index), stream 1+n = A^(n) (idx = i*J + j).
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint64_t splitmix_finalize(uint64_t z) {
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    return z ^ (z >> 31);
+}
+
+template <typename T>
+__global__ void k_init_uniform(T* out, int64_t rows, int J, int ld, uint64_t seed, uint64_t stream) {
+    const int64_t total = rows * J;
+    const uint64_t base = seed * 0x9E3779B97F4A7C15ull + (stream + 1) * 0xD1B54A32D192ED03ull;
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
+        const uint64_t z = splitmix_finalize(base + (uint64_t)t);
+        const int64_t i = t / J, j = t % J;
+        T v;
+        if constexpr (sizeof(T) == 8) v = (T)((double)(z >> 11) * 0x1.0p-53);
+        else v = (T)((float)(z >> 40) * 0x1.0p-24f);
+        out[i * ld + j] = v;
+    }
+}
+
+void launch_init_uniform(void* out, int elem_bytes, int64_t rows, int J, int ld, uint64_t seed, uint64_t stream,
+                         cudaStream_t st) {
+    const int64_t total = rows * J;
+    int grid = (int)((total + 255) / 256);
+    if (grid > 148 * 32) grid = 148 * 32;
+    if (grid < 1) grid = 1;
+    if (elem_bytes == 8) k_init_uniform<double><<<grid, 256, 0, st>>>((double*)out, rows, J, ld, seed, stream);
+    else k_init_uniform<float><<<grid, 256, 0, st>>>((float*)out, rows, J, ld, seed, stream);
+}
+
+// ---------------------------------------------------------------------------
+// Core permuted for mode n (Eq. 12 groups beta by beta_n = j): the other modes
+// m_0 < ... < m_{N-2} become k_0..k_{N-2}; Gp[o][k_{N-2}][j] with o the
+// row-major index of (k_0..k_{N-3}); each J x J block padded to gblk.
+// ---------------------------------------------------------------------------
+template <typename T>
+__global__ void k_permute_core(const T* G, T* Gp, int N, int J, int n, int GB, int64_t nblocks) {
+    const int64_t total = nblocks * GB;
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t o = t / GB;
+        const int w = (int)(t % GB);
+        if (w >= J * J) { Gp[t] = T(0); continue; }
+        int k[kMaxN];
+        k[N - 2] = w / J;
+        const int j = w % J;
+        int64_t rem = o;
+        for (int l = N - 3; l >= 0; --l) { k[l] = (int)(rem % J); rem /= J; }
+        // assemble beta in C order
+        int64_t beta = 0;
+        int l = 0;
+        for (int m = 0; m < N; ++m) {
+            const int bm = (m == n) ? j : k[l++];
+            beta = beta * J + bm;
+        }
+        Gp[t] = G[beta];
+    }
+}
+
+void launch_permute_core(const void* G, void* Gp, int elem_bytes, int N, int J, int n, cudaStream_t st) {
+    int64_t nblocks = 1;
+    for (int l = 0; l < N - 2; ++l) nblocks *= J;
+    const int GB = gblk(J, elem_bytes);
+    const int64_t total = nblocks * GB;
+    const int grid = (int)((total + 255) / 256);
+    if (elem_bytes == 8) k_permute_core<double><<<grid, 256, 0, st>>>((const double*)G, (double*)Gp, N, J, n, GB, nblocks);
+    else k_permute_core<float><<<grid, 256, 0, st>>>((const float*)G, (float*)Gp, N, J, n, GB, nblocks);
+}
+
+// ---------------------------------------------------------------------------
+// Generic small fp64 Cholesky solve (runtime J <= 16), used once per heavy row.
+// ---------------------------------------------------------------------------
+__device__ bool chol_solve_rt(const double* rec, int J, double lam, double* a) {
+    double L[16][16];
+    double y[16];
+    int q = 0;
+    for (int i = 0; i < J; ++i)
+        for (int j = i; j < J; ++j) { L[j][i] = rec[q]; ++q; }  // lower part holds M[j][i] = B[i][j]
+    const double* c = rec + q;
+    bool ok = true;
+    for (int j = 0; j < J; ++j) {
+        double d = L[j][j] + lam;
+        for (int k = 0; k < j; ++k) d = fma(-L[j][k], L[j][k], d);
+        ok = ok && (d > 0.0);
+        const double l = sqrt(fmax(d, 1e-300));
+        L[j][j] = l;
+        const double il = 1.0 / l;
+        for (int i = j + 1; i < J; ++i) {
+            double s = L[i][j];
+            for (int k = 0; k < j; ++k) s = fma(-L[i][k], L[j][k], s);
+            L[i][j] = s * il;
+        }
+    }
+    for (int i = 0; i < J; ++i) {
+        double s = c[i];
+        for (int k = 0; k < i; ++k) s = fma(-L[i][k], y[k], s);
+        y[i] = s / L[i][i];
+    }
+    for (int i = J - 1; i >= 0; --i) {
+        double s = y[i];
+        for (int k = i + 1; k < J; ++k) s = fma(-L[k][i], a[k], s);
+        a[i] = s / L[i][i];
+    }
+    return ok;
+}
+
+// Heavy rows: the partial records of a row's segments are stored
+// component-major (partials[pbase + p*nseg + s]).  Warp w sums components
+// p = w, w+8, ...: lane l adds segments l, l+32, ... in order, then a fixed
+// xor-butterfly -- the result depends only on the row's own segments (F9).
+template <typename T>
+__global__ void __launch_bounds__(256) k_heavy_finalize(const int32_t* hrow, const int32_t* hnseg,
+                                                        const int64_t* hpbase, const double* partials, int J,
+                                                        double lambda, T* An, int lda, double* sse_row, int* fail) {
+    __shared__ double rec[16 * 17 / 2 + 16 + 1];
+    const int h = blockIdx.x;
+    const int PW = J * (J + 1) / 2 + J + 1;
+    const int nseg = hnseg[h];
+    const int64_t pb = hpbase[h];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    for (int p = warp; p < PW; p += 8) {
+        double acc = 0.0;
+        const double* src = partials + pb + (int64_t)p * nseg;
+        for (int s = lane; s < nseg; s += 32) acc += src[s];
+        for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+        if (lane == 0) rec[p] = acc;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        const int row = hrow[h];
+        double a[16];
+        const bool ok = chol_solve_rt(rec, J, lambda, a);
+        if (!ok) {
+            atomicCAS(fail, 0, row + 1);
+            for (int j = 0; j < J; ++j) a[j] = 0.0;
+        }
+        const int NB = J * (J + 1) / 2;
+        const double* c = rec + NB;
+        double sse = rec[NB + J], ac = 0.0, aa = 0.0, ec = 0.0;
+        T* out = An + (int64_t)row * lda;
+        for (int j = 0; j < J; ++j) {
+            const T st = T(a[j]);
+            out[j] = st;
+            const double at = double(st);
+            sse = fma(-2.0 * at, c[j], sse);
+            ac = fma(a[j], c[j], ac);
+            aa = fma(a[j], a[j], aa);
+            ec = fma(at - a[j], c[j] - lambda * a[j], ec);
+        }
+        sse_row[row] = sse + ac - lambda * aa + 2.0 * ec;
+    }
+}
+
+void launch_heavy_finalize(int64_t nheavy, const int32_t* hrow, const int32_t* hnseg, const int64_t* hpbase,
+                           const double* partials, int J, double lambda, void* An, int elem_bytes, int lda,
+                           double* sse_row, int* fail, cudaStream_t st) {
+    if (nheavy <= 0) return;
+    if (elem_bytes == 8)
+        k_heavy_finalize<double><<<(unsigned)nheavy, 256, 0, st>>>(hrow, hnseg, hpbase, partials, J, lambda,
+                                                                   (double*)An, lda, sse_row, fail);
+    else
+        k_heavy_finalize<float><<<(unsigned)nheavy, 256, 0, st>>>(hrow, hnseg, hpbase, partials, J, lambda,
+                                                                  (float*)An, lda, sse_row, fail);
+}
+
+// ---------------------------------------------------------------------------
+// Deterministic sum: 256 fixed blocks over contiguous chunks, fixed smem tree,
+// then one block over the 256 partials.  Independent of the device and run.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ double block_tree_sum(double v, double* sm) {
+    sm[threadIdx.x] = v;
+    __syncthreads();
+    for (int o = 128; o > 0; o >>= 1) {
+        if ((int)threadIdx.x < o) sm[threadIdx.x] += sm[threadIdx.x + o];
+        __syncthreads();
+    }
+    return sm[0];
+}
+
+__global__ void __launch_bounds__(256) k_sum_stage1(const double* x, int64_t n, double* part) {
+    __shared__ double sm[256];
+    const int64_t chunk = (n + 255) / 256;
+    const int64_t b0 = blockIdx.x * chunk;
+    const int64_t b1 = b0 + chunk < n ? b0 + chunk : n;
+    double acc = 0.0;
+    for (int64_t i = b0 + threadIdx.x; i < b1; i += 256) acc += x[i];
+    const double s = block_tree_sum(acc, sm);
+    if (threadIdx.x == 0) part[blockIdx.x] = s;
+}
+
+__global__ void __launch_bounds__(256) k_sum_stage2(const double* part, double* out) {
+    __shared__ double sm[256];
+    const double s = block_tree_sum(part[threadIdx.x], sm);
+    if (threadIdx.x == 0) *out = s;
+}
+
+void launch_sum(const double* x, int64_t n, double* part256, double* out, cudaStream_t st) {
+    k_sum_stage1<<<256, 256, 0, st>>>(x, n, part256);
+    k_sum_stage2<<<1, 256, 0, st>>>(part256, out);
+}
+
+// ---------------------------------------------------------------------------
+// QR (Eq. 7) by CholeskyQR2 in fp64:
+//   W = A^T A, R1 = chol(W)^T, Q1 = A R1^-1; W2 = Q1^T Q1, R2 = chol(W2)^T,
+//   Q = Q1 R2^-1, R = R2 R1 (diag > 0 by construction).
+// ---------------------------------------------------------------------------
+template <typename T>
+__global__ void __launch_bounds__(256) k_gram_stage1(const T* A, int64_t I, int J, int lda, double* part) {
+    // block b covers rows [b*chunk, (b+1)*chunk); rows staged in smem tiles of 64
+    __shared__ double tile[64][17];
+    const int NB = J * (J + 1) / 2;
+    const int64_t chunk = (I + 255) / 256;
+    const int64_t r0 = blockIdx.x * chunk;
+    const int64_t r1 = r0 + chunk < I ? r0 + chunk : I;
+    int pi = 0, pj = 0;
+    {
+        int q = threadIdx.x, i = 0;
+        while (i < J && q >= J - i) { q -= J - i; ++i; }
+        pi = i;
+        pj = i + q;
+    }
+    double acc = 0.0;
+    for (int64_t t0 = r0; t0 < r1; t0 += 64) {
+        const int nt = (int)((r1 - t0) < 64 ? (r1 - t0) : 64);
+        __syncthreads();
+        for (int w = threadIdx.x; w < nt * J; w += 256) {
+            const int r = w / J, j = w % J;
+            tile[r][j] = double(A[(t0 + r) * lda + j]);
+        }
+        __syncthreads();
+        if ((int)threadIdx.x < NB)
+            for (int r = 0; r < nt; ++r) acc = fma(tile[r][pi], tile[r][pj], acc);
+    }
+    if ((int)threadIdx.x < NB) part[(int64_t)blockIdx.x * NB + threadIdx.x] = acc;
+}
+
+__global__ void k_gram_stage2(const double* part, int J, double* W) {
+    const int NB = J * (J + 1) / 2;
+    const int q = threadIdx.x;
+    if (q >= NB) return;
+    double acc = 0.0;
+    for (int b = 0; b < 256; ++b) acc += part[(int64_t)b * NB + q];
+    int i = 0, r = q;
+    while (r >= J - i) { r -= J - i; ++i; }
+    const int j = i + r;
+    W[i * J + j] = acc;
+    W[j * J + i] = acc;
+}
+
+void launch_gram(const void* A, int elem_bytes, bool /*unused*/, int64_t I, int J, int lda, double* part, double* W,
+                 cudaStream_t st) {
+    if (elem_bytes == 8) k_gram_stage1<double><<<256, 256, 0, st>>>((const double*)A, I, J, lda, part);
+    else k_gram_stage1<float><<<256, 256, 0, st>>>((const float*)A, I, J, lda, part);
+    k_gram_stage2<<<1, 256, 0, st>>>(part, J, W);
+}
+
+// R = L^T with W = L L^T (upper triangular, positive diagonal).
+__global__ void k_chol_upper(const double* W, int J, double* R, int* fail, int fail_code) {
+    if (threadIdx.x != 0) return;
+    double L[16][16];
+    double wmax = 0.0;
+    for (int i = 0; i < J; ++i) wmax = fmax(wmax, W[i * J + i]);
+    bool ok = true;
+    for (int j = 0; j < J; ++j) {
+        double d = W[j * J + j];
+        for (int k = 0; k < j; ++k) d = fma(-L[j][k], L[j][k], d);
+        if (!(d > 1e-24 * wmax)) ok = false;  // |R_kk| <= 1e-12 max|A| : rank deficient
+        const double l = sqrt(fmax(d, 1e-300));
+        L[j][j] = l;
+        for (int i = j + 1; i < J; ++i) {
+            double s = W[i * J + j];
+            for (int k = 0; k < j; ++k) s = fma(-L[i][k], L[j][k], s);
+            L[i][j] = s / l;
+        }
+    }
+    for (int i = 0; i < J; ++i)
+        for (int j = 0; j < J; ++j) R[i * J + j] = (j >= i) ? L[j][i] : 0.0;
+    if (!ok) atomicCAS(fail, 0, fail_code);
+}
+
+void launch_chol_upper(const double* W, int J, double* R, int* fail, int fail_code, cudaStream_t st) {
+    k_chol_upper<<<1, 32, 0, st>>>(W, J, R, fail, fail_code);
+}
+
+// Q = A R^-1 row by row: x R = a  =>  x_j = (a_j - sum_{k<j} x_k R[k][j]) / R[j][j]
+template <typename TA, typename TQ>
+__global__ void k_apply_rinv(const TA* A, int lda_a, TQ* Q, int lda_q, int64_t I, int J, const double* R) {
+    __shared__ double Rs[16 * 16];
+    for (int t = threadIdx.x; t < J * J; t += blockDim.x) Rs[t] = R[t];
+    __syncthreads();
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < I; i += (int64_t)gridDim.x * blockDim.x) {
+        double x[16];
+        for (int j = 0; j < J; ++j) {
+            double s = double(A[i * lda_a + j]);
+            for (int k = 0; k < j; ++k) s = fma(-x[k], Rs[k * J + j], s);
+            x[j] = s / Rs[j * J + j];
+        }
+        for (int j = 0; j < J; ++j) Q[i * lda_q + j] = TQ(x[j]);
+    }
+}
+
+void launch_apply_rinv(const void* A, int a_bytes, int lda_a, void* Q, int q_bytes, int lda_q, int64_t I, int J,
+                       const double* R, cudaStream_t st) {
+    int grid = (int)((I + 255) / 256);
+    if (grid > 148 * 8) grid = 148 * 8;
+    if (grid < 1) grid = 1;
+    if (a_bytes == 8 && q_bytes == 8)
+        k_apply_rinv<double, double><<<grid, 256, 0, st>>>((const double*)A, lda_a, (double*)Q, lda_q, I, J, R);
+    else if (a_bytes == 4 && q_bytes == 8)
+        k_apply_rinv<float, double><<<grid, 256, 0, st>>>((const float*)A, lda_a, (double*)Q, lda_q, I, J, R);
+    else if (a_bytes == 8 && q_bytes == 4)
+        k_apply_rinv<double, float><<<grid, 256, 0, st>>>((const double*)A, lda_a, (float*)Q, lda_q, I, J, R);
+    else
+        k_apply_rinv<float, float><<<grid, 256, 0, st>>>((const float*)A, lda_a, (float*)Q, lda_q, I, J, R);
+}
+
+__global__ void k_mat_upper_mul(const double* R2, const double* R1, double* R, int J) {
+    const int t = threadIdx.x;
+    if (t >= J * J) return;
+    const int i = t / J, j = t % J;
+    double s = 0.0;
+    for (int k = 0; k < J; ++k) s = fma(R2[i * J + k], R1[k * J + j], s);
+    R[t] = s;
+}
+
+void launch_mat_upper_mul(const double* R2, const double* R1, double* R, int J, cudaStream_t st) {
+    k_mat_upper_mul<<<1, 256, 0, st>>>(R2, R1, R, J);
+}
+
+// Eq. 2 with U = R (Eq. 8): G'[..k..] = sum_j R[k][j] G[..j..]   (fp64 accumulation)
+template <typename T>
+__global__ void k_core_mode_product(const T* G, T* Gout, int N, int J, int n, const double* R) {
+    int64_t inner = 1, total = 1;
+    for (int m = n + 1; m < N; ++m) inner *= J;
+    for (int m = 0; m < N; ++m) total *= J;
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t in = t % inner;
+        const int k = (int)((t / inner) % J);
+        const int64_t o = t / (inner * J);
+        double s = 0.0;
+        for (int j = 0; j < J; ++j) s = fma(R[k * J + j], double(G[(o * J + j) * inner + in]), s);
+        Gout[t] = T(s);
+    }
+}
+
+void launch_core_mode_product(const void* G, void* Gout, int elem_bytes, int N, int J, int n, const double* R,
+                              cudaStream_t st) {
+    int64_t total = 1;
+    for (int m = 0; m < N; ++m) total *= J;
+    const int grid = (int)((total + 255) / 256);
+    if (elem_bytes == 8) k_core_mode_product<double><<<grid, 256, 0, st>>>((const double*)G, (double*)Gout, N, J, n, R);
+    else k_core_mode_product<float><<<grid, 256, 0, st>>>((const float*)G, (float*)Gout, N, J, n, R);
+}
+
+}  // namespace pt

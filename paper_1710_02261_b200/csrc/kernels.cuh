@@ -1,0 +1,34 @@
+// kernels.cuh -- host-side launch wrappers of the small kernels (kernels.cu, index.cu).
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+namespace pt {
+
+// ---- init (Alg. 2 line 1; reading R2: counter-based SplitMix64) ----
+void launch_init_uniform(void* out, int elem_bytes, int64_t rows, int J, int ld, uint64_t seed, uint64_t stream,
+                         cudaStream_t st);
+// ---- core permuted for mode n: Gp[(k_0..k_{N-3})][gblk] with block [k_{N-2}][j] ----
+void launch_permute_core(const void* G, void* Gp, int elem_bytes, int N, int J, int n, cudaStream_t st);
+// ---- heavy rows: reduce the segment partials in a fixed order and solve (Eq. 9) ----
+void launch_heavy_finalize(int64_t nheavy, const int32_t* hrow, const int32_t* hnseg, const int64_t* hpbase,
+                           const double* partials, int J, double lambda, void* An, int elem_bytes, int lda,
+                           double* sse_row, int* fail, cudaStream_t st);
+// ---- deterministic sum of x[0..n) (fixed 256-block tree) into *out (device) ----
+void launch_sum(const double* x, int64_t n, double* part256, double* out, cudaStream_t st);
+// ---- QR (Eq. 7) by CholeskyQR2 in fp64, and G <- G x_n R (Eq. 8) ----
+void launch_gram(const void* A, int elem_bytes, bool a_is_f64_scratch, int64_t I, int J, int lda, double* part,
+                 double* W, cudaStream_t st);
+void launch_chol_upper(const double* W, int J, double* R, int* fail, int fail_code, cudaStream_t st);
+void launch_apply_rinv(const void* A, int a_bytes, int lda_a, void* Q, int q_bytes, int lda_q, int64_t I, int J,
+                       const double* R, cudaStream_t st);
+void launch_mat_upper_mul(const double* R2, const double* R1, double* R, int J, cudaStream_t st);
+void launch_core_mode_product(const void* G, void* Gout, int elem_bytes, int N, int J, int n, const double* R,
+                              cudaStream_t st);
+// ---- index build helpers (index.cu) ----
+void launch_extract_col(const int32_t* coords, int64_t nnz, int N, int n, int32_t* keys, int32_t* iota,
+                        cudaStream_t st);
+void launch_row_ptr(const int32_t* sorted_keys, int64_t nnz, int64_t I, int64_t* row_ptr, cudaStream_t st);
+
+}  // namespace pt

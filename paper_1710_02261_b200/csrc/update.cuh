@@ -1,0 +1,346 @@
+// update.cuh -- the fused row-update kernel of P-Tucker (Alg. 3 lines 6-15).
+//
+// One warp owns a slice of 32 row segments (rows sorted by length, SELL-32
+// layout); each LANE streams the entries of its own segment and, per entry,
+//   (1) gathers the N-1 other factor rows a^(k)_{i_k}                  (Eq. 12)
+//   (2) contracts the core with them as a depth-first TTV chain,
+//       delta(j) = sum_{k_0} a0[k_0] ( ... sum_{k_{N-2}} G'[k..][j] a_{N-2}[k_{N-2}] )
+//       -- exactly Eq. 12's sum over beta with beta_n = j, regrouped so every
+//       core element is used once per entry (J^N + ... + J^2 FMAs instead of
+//       the paper's N*J^N); the core sits in shared memory and every
+//       lane reads the same element at the same time (broadcast LDS.128);
+//   (3) accumulates B += delta delta^T (upper triangle), c += x delta and
+//       sum x^2 in fp64 registers                                 (Eq. 10-11)
+// and at the end of the segment either solves a = c [B + lambda I]^-1 by an
+// in-register fp64 Cholesky (Eq. 9) and stores the row plus its SSE by the
+// identity sum x^2 - 2 a.c + a B a^T (fused Eq. 5), or -- for segments of a
+// heavy row -- writes its partial (B, c, sum x^2) for k_heavy_finalize.
+//
+// The LITERAL variant (mode 0 only) reuses (1)-(2) and accumulates the
+// residual (x - a^(0)_{i_0} . delta)^2 per lane instead: the literal Eq. 5 pass.
+#pragma once
+#include <type_traits>
+
+#include "internal.cuh"
+
+namespace pt {
+
+template <typename T> struct Vec16;
+template <> struct Vec16<float> { using type = float4; static constexpr int n = 4; };
+template <> struct Vec16<double> { using type = double2; static constexpr int n = 2; };
+
+template <typename T>
+__device__ __forceinline__ void unpack(const typename Vec16<T>::type& v, T* e);
+template <>
+__device__ __forceinline__ void unpack<float>(const float4& v, float* e) { e[0] = v.x; e[1] = v.y; e[2] = v.z; e[3] = v.w; }
+template <>
+__device__ __forceinline__ void unpack<double>(const double2& v, double* e) { e[0] = v.x; e[1] = v.y; }
+
+// Innermost TTV stage over one padded J x J core block g = [k][j]:
+//   r[j] = sum_k g[k][j] * ak[k]   (sequential in k for each j; J independent chains)
+template <typename TS, int J, typename TAcc, typename TA>
+__device__ __forceinline__ void ttv_inner(const TS* __restrict__ g, const TA (&ak)[J], TAcc (&r)[J]) {
+    using V = typename Vec16<TS>::type;
+    constexpr int VN = Vec16<TS>::n;
+    constexpr int NV = (J * J + VN - 1) / VN;
+    const V* gv = reinterpret_cast<const V*>(g);
+#pragma unroll
+    for (int j = 0; j < J; ++j) r[j] = TAcc(0);
+#pragma unroll
+    for (int q = 0; q < NV; ++q) {
+        TS e[VN];
+        unpack<TS>(gv[q], e);
+#pragma unroll
+        for (int u = 0; u < VN; ++u) {
+            const int idx = q * VN + u;
+            if (idx < J * J) {
+                const int k = idx / J, j = idx % J;
+                r[j] = fma(TAcc(e[u]), TAcc(ak[k]), r[j]);
+            }
+        }
+    }
+}
+
+// Levels L = 1 .. N-2 of the chain (compile-time unrolled), fp type TF.
+// a[L] is the row of the L-th other mode; the child block stride is
+// J^(N-3-L) padded blocks.
+template <typename TS, typename TF, int N, int J, int L>
+__device__ __forceinline__ void ttv_level(const TS* __restrict__ g, const TF (&a)[N - 1][J], TF (&r)[J]) {
+    constexpr int GB = gblk(J, sizeof(TS));
+    if constexpr (L == N - 2) {
+        ttv_inner<TS, J, TF, TF>(g, a[N - 2], r);
+    } else {
+        constexpr int sub = ipow(J, N - 3 - L) * GB;
+#pragma unroll
+        for (int j = 0; j < J; ++j) r[j] = TF(0);
+#pragma unroll
+        for (int k = 0; k < J; ++k) {
+            TF t[J];
+            ttv_level<TS, TF, N, J, L + 1>(g + k * sub, a, t);
+#pragma unroll
+            for (int j = 0; j < J; ++j) r[j] = fma(a[L][k], t[j], r[j]);
+        }
+    }
+}
+
+// delta for one entry.  Level 0 accumulates in TD (fp64 under policy F32-B);
+// for N >= 4 level 0 is a runtime loop reading a0[k] from the (L1-cached) row.
+template <typename TS, typename TF, typename TD, int N, int J>
+__device__ __forceinline__ void compute_delta(const TS* __restrict__ g, const TF (&a)[N - 1][J],
+                                              const TS* __restrict__ a0row, TD (&d)[J]) {
+    constexpr int GB = gblk(J, sizeof(TS));
+    if constexpr (N == 2) {
+        ttv_inner<TS, J, TD, TF>(g, a[0], d);
+    } else if constexpr (N == 3) {
+#pragma unroll
+        for (int j = 0; j < J; ++j) d[j] = TD(0);
+#pragma unroll
+        for (int k = 0; k < J; ++k) {
+            TF t[J];
+            ttv_inner<TS, J, TF, TF>(g + k * GB, a[1], t);
+#pragma unroll
+            for (int j = 0; j < J; ++j) d[j] = fma(TD(a[0][k]), TD(t[j]), d[j]);
+        }
+    } else {
+        constexpr int sub = ipow(J, N - 3) * GB;
+#pragma unroll
+        for (int j = 0; j < J; ++j) d[j] = TD(0);
+#pragma unroll 1
+        for (int k = 0; k < J; ++k) {
+            TF t[J];
+            ttv_level<TS, TF, N, J, 1>(g + k * sub, a, t);
+            const TD ak = TD(TF(a0row[k]));
+#pragma unroll
+            for (int j = 0; j < J; ++j) d[j] = fma(ak, TD(t[j]), d[j]);
+        }
+    }
+}
+
+__host__ __device__ constexpr int up_idx(int i, int j, int J) { return i * J - i * (i - 1) / 2 + (j - i); }
+
+// In-register fp64 Cholesky solve of a (B + lam I) = c (Eq. 9).  B is the
+// packed upper triangle; it is overwritten by L^T.  Returns false on a
+// non-positive (or NaN) pivot.
+template <int J>
+__device__ __forceinline__ bool chol_solve(double (&B)[J * (J + 1) / 2], const double (&c)[J], double lam,
+                                           double (&a)[J]) {
+    bool ok = true;
+    double inv[J];
+#pragma unroll
+    for (int j = 0; j < J; ++j) {
+        double dj = B[up_idx(j, j, J)] + lam;
+#pragma unroll
+        for (int k = 0; k < j; ++k) dj = fma(-B[up_idx(k, j, J)], B[up_idx(k, j, J)], dj);
+        ok = ok && (dj > 0.0);
+        const double l = sqrt(fmax(dj, 1e-300));
+        inv[j] = 1.0 / l;
+#pragma unroll
+        for (int i = j + 1; i < J; ++i) {
+            double s = B[up_idx(j, i, J)];
+#pragma unroll
+            for (int k = 0; k < j; ++k) s = fma(-B[up_idx(k, i, J)], B[up_idx(k, j, J)], s);
+            B[up_idx(j, i, J)] = s * inv[j];  // L[i][j]
+        }
+    }
+    double y[J];
+#pragma unroll
+    for (int i = 0; i < J; ++i) {
+        double s = c[i];
+#pragma unroll
+        for (int k = 0; k < i; ++k) s = fma(-B[up_idx(k, i, J)], y[k], s);
+        y[i] = s * inv[i];
+    }
+#pragma unroll
+    for (int i = J - 1; i >= 0; --i) {
+        double s = y[i];
+#pragma unroll
+        for (int k = i + 1; k < J; ++k) s = fma(-B[up_idx(i, k, J)], a[k], s);
+        a[i] = s * inv[i];
+    }
+    return ok;
+}
+
+template <typename TS, int J>
+__device__ __forceinline__ void load_row(const TS* __restrict__ row, TS (&out)[J]) {
+    using V = typename Vec16<TS>::type;
+    constexpr int VN = Vec16<TS>::n;
+    constexpr int NV = (J + VN - 1) / VN;
+    const V* rv = reinterpret_cast<const V*>(row);
+#pragma unroll
+    for (int q = 0; q < NV; ++q) {
+        TS e[VN];
+        unpack<TS>(__ldg(rv + q), e);
+#pragma unroll
+        for (int u = 0; u < VN; ++u)
+            if (q * VN + u < J) out[q * VN + u] = e[u];
+    }
+}
+
+template <typename TS, typename TF, int N, int J, bool LAST64, bool LITERAL>
+__global__ void __launch_bounds__(kUpdThreads, 1) k_update(const UpdateParams<TS> p) {
+    using TD = typename std::conditional<LAST64 || std::is_same<TF, double>::value, double, float>::type;
+    constexpr int NB = J * (J + 1) / 2;
+    using V = typename Vec16<TS>::type;
+    constexpr int VN = Vec16<TS>::n;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    TS* gs = reinterpret_cast<TS*>(smem_raw);
+    {
+        const V* src = reinterpret_cast<const V*>(p.Gp);
+        V* dst = reinterpret_cast<V*>(gs);
+        for (int i = threadIdx.x; i < p.gp_elems / VN; i += blockDim.x) dst[i] = src[i];
+    }
+    __syncthreads();
+    const int lane = threadIdx.x & (kWarp - 1);
+
+    for (;;) {
+        int s = 0;
+        if (lane == 0) s = (int)atomicAdd(p.work, 1u);
+        s = __shfl_sync(0xffffffffu, s, 0);
+        if (s >= p.nslices) break;
+        const int64_t slot = (int64_t)s * kWarp + lane;
+        const int row = p.lane_row[slot];
+        const int len = p.lane_len[slot];
+        const int iters = p.slice_len[s];
+        const int64_t base = p.slice_off[s] + lane;
+
+        double B[NB], c[J], s2 = 0.0;
+#pragma unroll
+        for (int q = 0; q < NB; ++q) B[q] = 0.0;
+#pragma unroll
+        for (int q = 0; q < J; ++q) c[q] = 0.0;
+        TS arow[J];
+        if constexpr (LITERAL) {
+            if (row >= 0) load_row<TS, J>(p.An + (int64_t)row * p.lda, arow);
+            else {
+#pragma unroll
+                for (int q = 0; q < J; ++q) arow[q] = TS(0);
+            }
+        }
+
+        for (int e = 0; e < iters; ++e) {
+            const int64_t idx = base + (int64_t)e * kWarp;
+            int crd[N - 1];
+#pragma unroll
+            for (int k = 0; k < N - 1; ++k) crd[k] = __ldg(p.sc[k] + idx);
+            const TS x = __ldg(p.sv + idx);
+            TF a[N - 1][J];
+#pragma unroll
+            for (int k = (N >= 4 ? 1 : 0); k < N - 1; ++k) {
+                TS tmp[J];
+                load_row<TS, J>(p.A[k] + (int64_t)crd[k] * p.lda, tmp);
+#pragma unroll
+                for (int j = 0; j < J; ++j) a[k][j] = TF(tmp[j]);
+            }
+            if constexpr (N >= 4) {
+#pragma unroll
+                for (int j = 0; j < J; ++j) a[0][j] = TF(0);
+            }
+            TD d[J];
+            compute_delta<TS, TF, TD, N, J>(gs, a, p.A[0] + (int64_t)crd[0] * p.lda, d);
+            const bool act = e < len;
+            if constexpr (!LITERAL) {
+                double dd[J];
+#pragma unroll
+                for (int j = 0; j < J; ++j) dd[j] = act ? double(d[j]) : 0.0;
+                const double xd = act ? double(x) : 0.0;
+#pragma unroll
+                for (int i = 0; i < J; ++i) {
+                    c[i] = fma(xd, dd[i], c[i]);
+#pragma unroll
+                    for (int j = i; j < J; ++j) B[up_idx(i, j, J)] = fma(dd[i], dd[j], B[up_idx(i, j, J)]);
+                }
+                s2 = fma(xd, xd, s2);
+            } else {
+                double xh = 0.0;
+#pragma unroll
+                for (int j = 0; j < J; ++j) xh = fma(double(d[j]), double(arow[j]), xh);
+                const double r = act ? double(x) - xh : 0.0;
+                s2 = fma(r, r, s2);
+            }
+        }
+
+        if constexpr (LITERAL) {
+            p.lit_part[slot] = s2;
+        } else {
+            if (row < 0) continue;
+            const int64_t pidx = p.lane_pidx[slot];
+            if (pidx < 0) {
+                double a[J];
+                const bool ok = chol_solve<J>(B, c, p.lambda, a);
+                if (!ok) {
+                    atomicCAS(p.fail, 0, row + 1);
+#pragma unroll
+                    for (int j = 0; j < J; ++j) a[j] = 0.0;
+                }
+                TS* out = p.An + (int64_t)row * p.lda;
+                double sse = s2, ac = 0.0, aa = 0.0, ec = 0.0;
+                TS st[J];
+#pragma unroll
+                for (int j = 0; j < J; ++j) {
+                    st[j] = TS(a[j]);
+                    const double at = double(st[j]);
+                    const double eps = at - a[j];
+                    sse = fma(-2.0 * at, c[j], sse);
+                    ac = fma(a[j], c[j], ac);
+                    aa = fma(a[j], a[j], aa);
+                    ec = fma(eps, c[j] - p.lambda * a[j], ec);
+                }
+                // SSE of the stored row (Eq. 5 restricted to the row):
+                // s2 - 2 a~.c + a~ B a~^T with a~ B a~^T = a.c - lam|a|^2 + 2 eps.(c - lam a) + O(eps^2)
+                sse += ac - p.lambda * aa + 2.0 * ec;
+                constexpr int LD = factor_ld(J, sizeof(TS));
+#pragma unroll
+                for (int q = 0; q < LD / VN; ++q) {
+                    TS e4[VN];
+#pragma unroll
+                    for (int u = 0; u < VN; ++u) e4[u] = (q * VN + u < J) ? st[(q * VN + u) < J ? q * VN + u : 0] : TS(0);
+                    V v;
+                    if constexpr (VN == 4) v = make_float4(e4[0], e4[1], e4[2], e4[3]);
+                    else v = make_double2(e4[0], e4[1]);
+                    reinterpret_cast<V*>(out)[q] = v;
+                }
+                p.sse_row[row] = sse;
+            } else {
+                const int st = p.lane_pstride[slot];
+                double* dst = p.partials + pidx;
+#pragma unroll
+                for (int q = 0; q < NB; ++q) dst[(int64_t)q * st] = B[q];
+#pragma unroll
+                for (int q = 0; q < J; ++q) dst[(int64_t)(NB + q) * st] = c[q];
+                dst[(int64_t)(NB + J) * st] = s2;
+            }
+        }
+    }
+}
+
+template <typename TS, typename TF, int N, int J, bool LAST64>
+void launch_update(const void* params, bool literal, int grid, cudaStream_t st) {
+    const UpdateParams<TS>& p = *reinterpret_cast<const UpdateParams<TS>*>(params);
+    const size_t smem = (size_t)p.gp_elems * sizeof(TS);
+    if (literal) {
+        auto k = k_update<TS, TF, N, J, LAST64, true>;
+        if (smem > 48 * 1024) cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        k<<<grid, kUpdThreads, smem, st>>>(p);
+    } else {
+        auto k = k_update<TS, TF, N, J, LAST64, false>;
+        if (smem > 48 * 1024) cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        k<<<grid, kUpdThreads, smem, st>>>(p);
+    }
+}
+
+template <typename TS, typename TF, int N, int J, bool LAST64>
+int occupancy_update(bool literal, size_t smem) {
+    int nb = 0;
+    if (literal) {
+        auto k = k_update<TS, TF, N, J, LAST64, true>;
+        if (smem > 48 * 1024) cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k, kUpdThreads, smem);
+    } else {
+        auto k = k_update<TS, TF, N, J, LAST64, false>;
+        if (smem > 48 * 1024) cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k, kUpdThreads, smem);
+    }
+    return nb;
+}
+
+}  // namespace pt

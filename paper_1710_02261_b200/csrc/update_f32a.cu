@@ -1,0 +1,14 @@
+// update_f32a.cu -- instantiations of the fused row-update kernel: TS=float, TF=float, LAST64=false.
+#include "update.cuh"
+
+namespace pt {
+namespace {
+#define PT_ENTRY(N, J) {0, 0, N, J, &launch_update<float, float, N, J, false>, &occupancy_update<float, float, N, J, false>},
+const UpdateKernel kTable[] = {PT_NJ_LIST(PT_ENTRY)};
+#undef PT_ENTRY
+}  // namespace
+const UpdateKernel* update_kernels_f32a(int* count) {
+    *count = (int)(sizeof(kTable) / sizeof(kTable[0]));
+    return kTable;
+}
+}  // namespace pt

@@ -1,0 +1,226 @@
+"""GPU parity: the CUDA path (through the C-ABI) against the FP64 CPU oracle on
+the same seeded inputs (north-star tolerances, BASELINE.json):
+  * init, slice index (CSR/perm) and row partition bit-exact;
+  * one mode update from an identical state within 1e-5 (FP32) / 1e-10 (FP64)
+    relative per factor row (reading R20: ||a_gpu - a_ref|| / ||a_ref||, the
+    reference computed in FP64 from the identical stored state; empty rows 0);
+  * the error trajectory over the iterations within 1e-3 relative;
+  * QR + core update against the oracle's Householder QR (Eq. 7-8).
+"""
+import numpy as np
+import pytest
+
+from gen import synth
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def pt():
+    import torch
+    assert torch.cuda.is_available(), "GPU tests need a B200"
+    torch.cuda.set_device(0)
+    from paper_1710_02261_b200 import build, ptucker
+    build.build()
+    ptucker.load()
+    yield ptucker
+    ptucker.ptucker_finalize()
+
+
+def gpu_model(pt, orc, N):
+    G = pt.ptucker_get_core().astype(np.float64)
+    A = [pt.ptucker_get_factor(n).astype(np.float64) for n in range(N)]
+    return orc.Model(G, A)
+
+
+def row_rel_err(a_gpu, a_ref):
+    a_gpu = np.asarray(a_gpu, np.float64)
+    num = np.linalg.norm(a_gpu - a_ref, axis=1)
+    den = np.linalg.norm(a_ref, axis=1)
+    zero = den == 0
+    assert np.all(num[zero] == 0), "empty rows must be exactly zero"
+    return num[~zero] / den[~zero]
+
+
+def init_cfg(pt, cfg, policy=1, seg_len=256):
+    coords, vals = synth.generate(cfg)
+    pt.ptucker_finalize()
+    pt.ptucker_set_option("seg_len", seg_len)
+    pt.ptucker_init(coords, vals, cfg.dims, [cfg.J] * len(cfg.dims), cfg.lam, 0)
+    pt.ptucker_set_option("policy", policy)
+    return coords, vals
+
+
+def mode_update_parity(pt, orc, t, N, lam, tol, modes=None):
+    worst = 0.0
+    for n in (range(N) if modes is None else modes):
+        m = gpu_model(pt, orc, N)
+        orc.update_mode(t, m, n, lam)
+        pt.ptucker_update_mode(n)
+        err = row_rel_err(pt.ptucker_get_factor(n), m.A(n))
+        worst = max(worst, float(err.max()) if err.size else 0.0)
+        assert err.size == 0 or err.max() <= tol, (n, float(err.max()), float(np.median(err)))
+    return worst
+
+
+# ---------------------------------------------------------------- init / index / partition
+@pytest.mark.parametrize("name,scale", [("c1", 1.0), ("c2", 0.01), ("c3", 0.002)])
+def test_init_and_index_bit_exact(pt, orc, name, scale):
+    cfg = synth.config("c1") if scale == 1.0 else synth.small(name, scale)
+    coords, vals = init_cfg(pt, cfg)
+    N = len(cfg.dims)
+    prec = 1 if cfg.dtype == "f64" else 0
+    ref = orc.init_model(cfg.dims, [cfg.J] * N, seed=0, prec=prec)
+    assert np.array_equal(pt.ptucker_get_core().astype(np.float64), ref.G)
+    for n in range(N):
+        assert np.array_equal(pt.ptucker_get_factor(n).astype(np.float64), ref.A(n))
+    t = orc.Tensor(coords, vals, cfg.dims)
+    for n in range(N):
+        rp, perm = pt.ptucker_get_mode_index(n)
+        orp, operm = t.mode_index(n)
+        assert np.array_equal(rp, orp) and np.array_equal(perm, operm)
+        assert np.array_equal(pt.ptucker_get_partition(n), orc.partition(orp, 1))
+
+
+# ---------------------------------------------------------------- one mode update from an identical state
+def test_mode_update_f64_c1(pt, orc):
+    cfg = synth.config("c1")
+    coords, vals = init_cfg(pt, cfg)
+    t = orc.Tensor(coords, vals, cfg.dims)
+    mode_update_parity(pt, orc, t, 3, cfg.lam, 1e-10)           # init state
+    for _ in range(2):
+        pt.ptucker_sweep()
+    mode_update_parity(pt, orc, t, 3, cfg.lam, 1e-10)           # mid-trajectory state
+
+
+@pytest.mark.parametrize("name,scale,seg", [("c2", 0.01, 256), ("c3", 0.002, 256), ("c3", 0.002, 7),
+                                            ("c4", 0.001, 256), ("c5", 0.0001, 256)])
+def test_mode_update_f32(pt, orc, name, scale, seg):
+    cfg = synth.small(name, scale)
+    coords, vals = init_cfg(pt, cfg, seg_len=seg)
+    N = len(cfg.dims)
+    t = orc.Tensor(coords, vals, cfg.dims)
+    w0 = mode_update_parity(pt, orc, t, N, cfg.lam, 1e-5)       # init state (worst case, survey E4)
+    pt.ptucker_sweep()
+    w1 = mode_update_parity(pt, orc, t, N, cfg.lam, 1e-5)       # mid-trajectory
+    info = pt.ptucker_info()
+    print(f"{name} seg={seg} worst row rel err init {w0:.2e} mid {w1:.2e}; heavy rows "
+          f"{[m['heavy_rows'] for m in info['modes']]}")
+
+
+@pytest.mark.parametrize("name,scale", [("c2", 0.01), ("c4", 0.001)])
+def test_mode_update_f64_variants(pt, orc, name, scale):
+    """Every config also runs in FP64 mode (1e-10 per row)."""
+    cfg = synth.small(name, scale)
+    cfg.dtype = "f64"
+    coords, vals = init_cfg(pt, cfg)
+    assert vals.dtype == np.float64
+    t = orc.Tensor(coords, vals, cfg.dims)
+    mode_update_parity(pt, orc, t, len(cfg.dims), cfg.lam, 1e-10)
+
+
+def test_policy_f32a_reported(pt, orc):
+    """F32-A (all-fp32 contraction) is measured, not assumed: its worst row error is printed."""
+    cfg = synth.small("c2", 0.01)
+    coords, vals = init_cfg(pt, cfg, policy=0)
+    t = orc.Tensor(coords, vals, cfg.dims)
+    w = mode_update_parity(pt, orc, t, 3, cfg.lam, 1e-4)
+    print(f"F32-A worst row rel err {w:.2e}")
+
+
+# ---------------------------------------------------------------- error (Eq. 5) and trajectory
+@pytest.mark.parametrize("name,scale,iters", [("c1", 1.0, 5), ("c2", 0.01, 10), ("c3", 0.001, 10),
+                                              ("c4", 0.001, 10)])
+def test_error_trajectory(pt, orc, name, scale, iters):
+    cfg = synth.config(name) if scale == 1.0 else synth.small(name, scale)
+    coords, vals = init_cfg(pt, cfg)
+    N = len(cfg.dims)
+    t = orc.Tensor(coords, vals, cfg.dims)
+    m = orc.init_model(cfg.dims, [cfg.J] * N, seed=0, prec=1 if cfg.dtype == "f64" else 0)
+    ref_errs, _ = orc.als(t, m, cfg.lam, iters)
+    gpu = [pt.ptucker_error()]                                   # literal pass (no update yet)
+    for _ in range(iters):
+        pt.ptucker_sweep()
+        e_fused = pt.ptucker_error()
+        e_lit = pt.ptucker_error_literal()
+        assert abs(e_fused - e_lit) <= 1e-6 * e_lit, (e_fused, e_lit)
+        gpu.append(e_fused)
+    rel = np.abs(np.array(gpu) - ref_errs) / ref_errs
+    assert rel.max() <= 1e-3, rel
+    print(f"{name}: trajectory max rel diff {rel.max():.2e}; e {ref_errs[0]:.4g} -> {ref_errs[-1]:.4g}")
+
+
+def test_error_of_identical_state(pt, orc):
+    cfg = synth.small("c4", 0.001)
+    coords, vals = init_cfg(pt, cfg)
+    pt.ptucker_sweep()
+    m = gpu_model(pt, orc, 5)
+    t = orc.Tensor(coords, vals, cfg.dims)
+    ref = orc.error(t, m)
+    assert abs(pt.ptucker_error() - ref) <= 1e-5 * ref
+    assert abs(pt.ptucker_error_literal() - ref) <= 1e-5 * ref
+
+
+# ---------------------------------------------------------------- QR + core update (Eq. 7-8)
+@pytest.mark.parametrize("name,scale,tol", [("c1", 1.0, 1e-10), ("c2", 0.01, 2e-5), ("c4", 0.001, 2e-5)])
+def test_orthogonalize(pt, orc, name, scale, tol):
+    cfg = synth.config(name) if scale == 1.0 else synth.small(name, scale)
+    coords, vals = init_cfg(pt, cfg)
+    N = len(cfg.dims)
+    for _ in range(2):
+        pt.ptucker_sweep()
+    m = gpu_model(pt, orc, N)
+    t = orc.Tensor(coords, vals, cfg.dims)
+    e_before = orc.error(t, m)
+    orc.orthogonalize(m)
+    pt.ptucker_orthogonalize()
+    g = gpu_model(pt, orc, N)
+    for n in range(N):
+        Q = g.A(n)
+        assert np.abs(Q.T @ Q - np.eye(cfg.J)).max() <= (1e-12 if tol < 1e-6 else 1e-5)
+        assert np.abs(Q - m.A(n)).max() <= tol * max(1.0, np.abs(m.A(n)).max()) * 10
+    assert np.abs(g.G - m.G).max() <= tol * np.abs(m.G).max()
+    assert abs(pt.ptucker_error() - e_before) <= tol * e_before
+
+
+# ---------------------------------------------------------------- edge cases
+def test_edge_empty_rows_and_tiny(pt, orc):
+    coords = np.array([[0, 0, 0], [0, 1, 1], [3, 1, 0]], np.int32)
+    vals = np.array([1.0, 2.0, 3.0])
+    pt.ptucker_finalize()
+    pt.ptucker_set_option("seg_len", 256)
+    pt.ptucker_init(coords, vals, [5, 2, 2], [2, 2, 2], 0.01, 0)
+    t = orc.Tensor(coords, vals, [5, 2, 2])
+    mode_update_parity(pt, orc, t, 3, 0.01, 1e-10)
+    a0 = pt.ptucker_get_factor(0)
+    assert np.all(a0[[1, 2, 4]] == 0)
+    # single entry, N = 2 (matrix case)
+    pt.ptucker_init(np.array([[1, 2]], np.int32), np.array([0.5]), [3, 4], [3, 3], 0.1, 1)
+    t = orc.Tensor([[1, 2]], [0.5], [3, 4])
+    mode_update_parity(pt, orc, t, 2, 0.1, 1e-10)
+
+
+def test_worked_example(pt, orc):
+    import json, os
+    ex = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "worked_example_e10.json")))
+    pt.ptucker_finalize()
+    pt.ptucker_init(np.array(ex["coords"], np.int32), np.array(ex["vals"]), ex["dims"], ex["J"], ex["lambda"], 0)
+    assert abs(pt.ptucker_error() - ex["e0"]) < 1e-12
+    pt.ptucker_update_mode(0)
+    np.testing.assert_allclose(pt.ptucker_get_factor(0), ex["A0_after_first_mode_update"], rtol=1e-12)
+    pt.ptucker_update_mode(1)
+    pt.ptucker_update_mode(2)
+    assert abs(pt.ptucker_error() - ex["e1"]) < 1e-12
+    pt.ptucker_sweep()
+    assert abs(pt.ptucker_error() - ex["e2"]) < 1e-12
+
+
+def test_determinism(pt):
+    cfg = synth.small("c3", 0.002)
+    init_cfg(pt, cfg, seg_len=16)
+    pt.ptucker_sweep()
+    a = [pt.ptucker_get_factor(n).copy() for n in range(4)]
+    init_cfg(pt, cfg, seg_len=16)
+    pt.ptucker_sweep()
+    for n in range(4):
+        assert np.array_equal(a[n], pt.ptucker_get_factor(n))
