@@ -1,0 +1,353 @@
+"""Benchmark of the P-Tucker row-wise ALS hot path on B200 (BASELINE.json metric:
+observed entries/s per full ALS iteration, and % of roofline).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c5] [--impl ours|reference]
+    (N > 1: python -m torch.distributed.run --nproc-per-node N ... bench.py --gpus N ...)
+
+A "step" is one full ALS iteration (Alg. 2 lines 3-4): ptucker_update_mode
+for n = 0..N-1 plus ptucker_error (Eq. 5), on synthetic data of the config's shape
+(gen/synth.py).  Timed with CUDA events on the library's stream (torch's current
+stream), barrier + synchronize on both sides, max over ranks.  Inputs are larger than
+L2 (the SELL entry stream of c5 is 1.2 GB per mode), so no L2 flush is needed.
+
+--impl reference times the FP64 CPU oracle (oracle/, test infrastructure) on a
+bounded sample of the same workload on this host's cores (rank 0 only).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+from gen import synth  # noqa: E402
+
+METRIC = "observed entries/sec per full ALS iteration"
+UNIT = "entries/s"
+
+
+# ----------------------------------------------------------------------------- helpers
+def algorithmic_work(N: int, J: int, policy: str):
+    """FMAs per observed entry per mode update of the shipped kernel (DESIGN.md
+    "Roofline"): innermost TTV stage J^N (fp32 unless F64), outer stages
+    J^(N-1)+...+J^2 (fp64 under F32-B), normal equations J(J+1)/2 + J + 1 (fp64)."""
+    inner = J ** N
+    outer = sum(J ** k for k in range(2, N))
+    bc = J * (J + 1) // 2 + J + 1
+    if policy == "F64":
+        return 0, inner + outer + bc
+    if policy == "F32-A":
+        return inner + outer, bc
+    return inner, outer + bc
+
+
+def clocks_sampler(device: int):
+    q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+    try:
+        return subprocess.Popen(["nvidia-smi", f"--query-gpu={q}", "--format=csv,noheader,nounits", "-lms", "100",
+                                 "-i", str(device)], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+    except Exception:
+        return None
+
+
+def clocks_summary(proc):
+    if proc is None:
+        return None
+    proc.terminate()
+    try:
+        out, _ = proc.communicate(timeout=5)
+    except Exception:
+        proc.kill()
+        return None
+    sm, mx, reasons = [], 0.0, set()
+    names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+    for line in out.strip().splitlines():
+        f = [x.strip() for x in line.split(",")]
+        if len(f) < 8:
+            continue
+        try:
+            sm.append(float(f[0]))
+            mx = max(mx, float(f[1]))
+        except ValueError:
+            continue
+        for nm, v in zip(names, f[4:8]):
+            if v.lower() == "active":
+                reasons.add(nm)
+    if not sm:
+        return None
+    return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def load_traffic(cfg_name: str):
+    """Per-launch DRAM bytes of the update kernel from the committed ncu capture, if any."""
+    p = os.path.join(ROOT, "profiles", "traffic.json")
+    try:
+        d = json.load(open(p))
+        return d.get(cfg_name)
+    except Exception:
+        return None
+
+
+# ----------------------------------------------------------------------------- oracle arm
+def oracle_sample_rate(cfg, coords, vals, target_s: float = 12.0):
+    """The FP64 CPU oracle (as it stands) on a bounded sample of the workload: for
+    each mode n, the rows [0, R) of mode n with all their entries (a sub-tensor with
+    I_n = R, the other dims unchanged, so rows have the workload's length mix); one
+    oracle update_mode per mode plus the literal error over the sampled entries.
+    Returns (entries/s per full iteration, cores, description)."""
+    from oracle import oracle as orc
+    import multiprocessing
+    cores = multiprocessing.cpu_count()
+    N, J = len(cfg.dims), cfg.J
+    model = orc.init_model(cfg.dims, [J] * N, seed=cfg.seed, prec=1 if cfg.dtype == "f64" else 0)
+
+    def sample(R):
+        t_total, tot_entries = 0.0, 0
+        per_entry = 0.0
+        for n in range(N):
+            sel = coords[:, n] < R
+            c = np.ascontiguousarray(coords[sel])
+            dims = list(cfg.dims)
+            dims[n] = R
+            t = orc.Tensor(c, vals[sel].astype(np.float64), dims)
+            t.mode_index(n)
+            A = [model.A(k)[:dims[k]] for k in range(N)]
+            m = orc.Model(model.G, A)
+            t0 = time.perf_counter()
+            orc.update_mode(t, m, n, cfg.lam, threads=cores)
+            dt = time.perf_counter() - t0
+            per_entry += dt / max(t.nnz, 1)
+            t_total += dt
+            tot_entries += t.nnz
+        # literal error (Eq. 5) over the mode-0 sample's entries
+        sel = coords[:, 0] < R
+        dims = list(cfg.dims)
+        dims[0] = R
+        t = orc.Tensor(np.ascontiguousarray(coords[sel]), vals[sel].astype(np.float64), dims)
+        m = orc.Model(model.G, [model.A(k)[:dims[k]] for k in range(N)])
+        t0 = time.perf_counter()
+        orc.sse(t, m, threads=cores)
+        dt = time.perf_counter() - t0
+        per_entry += dt / max(t.nnz, 1)
+        t_total += dt
+        return 1.0 / per_entry, t_total, tot_entries
+
+    R = max(8, min(cfg.dims) // 10000)
+    rate, took, ent = sample(R)
+    R2 = int(R * max(1.0, min(target_s / max(took, 1e-3), 1e4)))
+    R2 = min(R2, min(cfg.dims))
+    if R2 > R:
+        rate, took, ent = sample(R2)
+        R = R2
+    desc = (f"oracle (FP64 C, OpenMP dynamic rows) on rows [0,{R}) of each mode with all their entries "
+            f"({ent} entry-updates) + literal Eq.5 on the mode-0 sample; per-entry times summed over the "
+            f"{N} mode updates and the error pass")
+    return rate, cores, desc
+
+
+def run_reference(args, cfg):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    coords, vals = synth.generate(cfg)
+    rates = []
+    for _ in range(args.warmup + args.steps):
+        r, cores, desc = oracle_sample_rate(cfg, coords, vals, target_s=args.ref_seconds)
+        rates.append(r)
+    rates = rates[args.warmup:]
+    v = float(statistics.median(rates))
+    line = {
+        "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": 1e3 * cfg.nnz / v, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": workload_config(cfg, args),
+        "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": desc},
+        "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def workload_config(cfg, args):
+    return {
+        "workload": f"{cfg.name}: order-{len(cfg.dims)} {'x'.join(str(d) for d in cfg.dims)}, |Omega|={cfg.nnz}, "
+                    f"J={cfg.J}, lambda={cfg.lam}, values={cfg.values}, coords={cfg.coords}",
+        "dims": list(cfg.dims), "nnz": cfg.nnz, "J": cfg.J, "lambda": cfg.lam, "seed": cfg.seed,
+        "parallelism": f"rows of each mode sharded over {args.gpus} GPU(s), all-gather per mode",
+        "l2": "inputs larger than L2 (no flush)",
+    }
+
+
+# ----------------------------------------------------------------------------- our arm
+def run_ours(args, cfg):
+    import torch
+    import torch.distributed as dist
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    from paper_1710_02261_b200 import build, ptucker as pt
+    if rank == 0 or world == 1:
+        build.build()
+    if world > 1:
+        dist.barrier()
+    pt.load()
+    if world > 1:
+        obj = [pt.ptucker_get_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        pt.ptucker_comm_init(rank, world, obj[0])
+    stream = torch.cuda.current_stream()
+    pt.ptucker_set_stream(stream.cuda_stream)
+    pt.ptucker_set_option("seg_len", args.seg_len)
+
+    coords, vals = synth.generate(cfg)
+    N, J = len(cfg.dims), cfg.J
+    t0 = time.perf_counter()
+    pt.ptucker_init(coords, vals, cfg.dims, [J] * N, cfg.lam, cfg.seed)
+    pt.ptucker_set_option("policy", 0 if args.policy == "F32-A" else 1)
+    pt.ptucker_synchronize()
+    init_s = time.perf_counter() - t0
+    info = pt.ptucker_info()
+
+    def barrier_sync():
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    for _ in range(args.warmup):
+        pt.ptucker_sweep()
+        pt.ptucker_error()
+    barrier_sync()
+    pt.ptucker_set_option("time_kernels", 1)
+    pt.ptucker_reset_kernel_stats()
+    launches0 = pt.ptucker_info()["kernel_launches"]
+    clk = clocks_sampler(local)
+    time.sleep(0.3)
+    errs = []
+    barrier_sync()
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    ev0.record(stream)
+    for _ in range(args.steps):
+        pt.ptucker_sweep()
+        errs.append(pt.ptucker_error())
+    ev1.record(stream)
+    barrier_sync()
+    clocks = clocks_summary(clk)
+    ms = ev0.elapsed_time(ev1)
+    launches = pt.ptucker_info()["kernel_launches"] - launches0
+    upd_ms, upd_n = pt.ptucker_kernel_stats("update")
+    fin_ms, _ = pt.ptucker_kernel_stats("finalize")
+    pt.ptucker_set_option("time_kernels", 0)
+    if world > 1:
+        t = torch.tensor([ms, upd_ms], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms, upd_ms = float(t[0]), float(t[1])
+    ms_per_step = ms / args.steps
+    value = cfg.nnz * args.steps / (ms / 1e3)
+
+    # roofline of the dominant kernel (the fused row update), per launch
+    policy = info["policy"]
+    f32, f64 = algorithmic_work(N, J, policy)
+    nsm = torch.cuda.get_device_properties(local).multi_processor_count
+    clk_max = (clocks or {}).get("sm_max_mhz") or 1965.0
+    p32 = nsm * 128 * 2 * clk_max * 1e6 / 1e12   # TFLOP/s fp32 FMA pipe (unit counts x max clock)
+    p64 = nsm * 64 * 2 * clk_max * 1e6 / 1e12     # TFLOP/s fp64
+    entries_per_launch = cfg.nnz / world           # each rank's launch covers its row block of one mode
+    avg_launch_s = (upd_ms / max(upd_n, 1)) / 1e3
+    if f32 > 0:
+        achieved = 2 * f32 * entries_per_launch / avg_launch_s / 1e12
+        peak, bound_pipe = p32, "fp32"
+    else:
+        achieved = 2 * f64 * entries_per_launch / avg_launch_s / 1e12
+        peak, bound_pipe = p64, "fp64"
+    t_roof = max(2 * f32 * entries_per_launch / (p32 * 1e12), 2 * f64 * entries_per_launch / (p64 * 1e12))
+    roof = {
+        "bound": "alu", "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
+        "traffic": load_traffic(cfg.name),
+        "kernel": "k_update (fused TTV + fp64 normal equations + Cholesky)", "pipe": bound_pipe,
+        "peak_source": f"derived: {nsm} SMs x {'128' if bound_pipe == 'fp32' else '64'} FMA/clk x 2 x {clk_max:.0f} MHz",
+        "fp64_achieved_tflops": 2 * f64 * entries_per_launch / avg_launch_s / 1e12, "fp64_peak_tflops": p64,
+        "frac_of_pipe_roofline_time": t_roof / avg_launch_s,
+        "avg_launch_ms": avg_launch_s * 1e3, "launches": upd_n,
+        "update_share_of_step": upd_ms / ms, "finalize_ms_per_step": fin_ms / args.steps,
+    }
+
+    # e2e: the whole job through the public API from pinned host buffers
+    e2e = None
+    if not args.no_e2e:
+        pc = torch.from_numpy(coords).pin_memory().numpy()
+        pv = torch.from_numpy(vals).pin_memory().numpy()
+        barrier_sync()
+        t0 = time.perf_counter()
+        pt.ptucker_set_stream(stream.cuda_stream)
+        pt.ptucker_init(pc, pv, cfg.dims, [J] * N, cfg.lam, cfg.seed)
+        for _ in range(args.steps):
+            pt.ptucker_sweep()
+            pt.ptucker_error()
+        barrier_sync()
+        e2e_s = time.perf_counter() - t0
+        if world > 1:
+            t = torch.tensor([e2e_s], dtype=torch.float64, device="cuda")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            e2e_s = float(t[0])
+        e2e = {"value": cfg.nnz * args.steps / e2e_s, "unit": UNIT,
+               "h2d_bytes_per_step": int((coords.nbytes + vals.nbytes) / args.steps), "d2h_bytes_per_step": 8,
+               "note": f"ptucker_init from pinned host COO (H2D + validation + device index build) + {args.steps} "
+                       f"iterations with the error read back each iteration; H2D amortised over the steps"}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        r, cores, desc = oracle_sample_rate(cfg, coords, vals, target_s=args.ref_seconds)
+        cpu = {"value": r, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": desc}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "fp32 storage/contraction + fp64 normal equations" if cfg.dtype == "f32"
+            else "f64", "data": "synthetic", "config": workload_config(cfg, args) | {"policy": policy},
+            "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "clocks": clocks,
+            "init_s": init_s, "errors": errs[-1:], "info": {k: info[k] for k in ("grid_update", "seg_len", "modes")},
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="c5")
+    ap.add_argument("--scale", type=float, default=1.0, help="shrink the config (tests only)")
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--policy", default="F32-B", choices=["F32-A", "F32-B"])
+    ap.add_argument("--seg-len", type=int, default=256)
+    ap.add_argument("--ref-seconds", type=float, default=12.0)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    cfg = synth.config(args.config) if args.scale == 1.0 else synth.small(args.config, args.scale)
+    if args.impl == "reference":
+        run_reference(args, cfg)
+    else:
+        run_ours(args, cfg)
+
+
+if __name__ == "__main__":
+    main()

@@ -17,7 +17,29 @@ OBJ = os.path.join(HERE, "_obj")
 LIB = os.path.join(HERE, "libptucker.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+
+
+
+def _nccl_dir():
+    """Prefer the NCCL that torch ships (2.28.x): both libraries then share one
+    libnccl.so.2 in the process whichever is imported first."""
+    try:
+        import nvidia.nccl as nn
+        d = list(nn.__path__)[0]
+        if os.path.exists(os.path.join(d, "lib", "libnccl.so.2")):
+            return d
+    except Exception:
+        pass
+    return None
+
+
+NCCL = _nccl_dir()
 FLAGS = ["-std=c++17", "-O3", "-lineinfo", "-Xcompiler", "-fPIC", "-Xptxas", "-v", "-I", CSRC, "-I", INC]
+if NCCL:
+    FLAGS += ["-I", os.path.join(NCCL, "include")]
+    LINK_NCCL = ["-L", os.path.join(NCCL, "lib"), "-l:libnccl.so.2", "-Xlinker", "-rpath=" + os.path.join(NCCL, "lib")]
+else:
+    LINK_NCCL = ["-lnccl"]
 
 
 def _headers():
@@ -52,7 +74,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
         objs = list(ex.map(lambda s: _compile(s, force), srcs))
     if force or _stale(LIB, objs):
         tmp = LIB + f".tmp{os.getpid()}"
-        cmd = [NVCC, *ARCH, "-shared", "-o", tmp, *objs, "-lnccl", "-Xlinker", "--no-undefined"]
+        cmd = [NVCC, *ARCH, "-shared", "-o", tmp, *objs, *LINK_NCCL, "-Xlinker", "--no-undefined"]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError(f"link failed:\n{r.stderr[-4000:]}")

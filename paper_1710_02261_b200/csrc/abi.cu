@@ -98,6 +98,7 @@ struct Ctx {
     int last_fail_mode = -1;
     const UpdateKernel* kern = nullptr;
     int grid_upd = 0, grid_lit = 0;
+    int64_t launches = 0;        // kernels this library launched since init (gpu_launches evidence)
     // timing
     bool time_kernels = false;
     std::vector<Pending> pending;
@@ -209,6 +210,7 @@ int launch_update_kernel(int n, bool literal) {
     const int grid = literal ? g.grid_lit : g.grid_upd;
     if (g.mi[n].nslices == 0) return PTUCKER_OK;
     CK(cudaMemsetAsync(g.d_work, 0, sizeof(unsigned int), S()));
+    g.launches += 1;
     if (g.prec == PTUCKER_F64) {
         UpdateParams<double> p = make_params<double>(n, literal);
         g.kern->launch(&p, literal, grid, S());
@@ -222,6 +224,7 @@ int launch_update_kernel(int n, bool literal) {
 
 int rebuild_gp() {
     for (int n = 0; n < g.N; ++n) launch_permute_core(g.G, g.Gp[n], g.esz, g.N, g.J, n, S());
+    g.launches += g.N;
     CK(cudaGetLastError());
     return PTUCKER_OK;
 }
@@ -255,6 +258,7 @@ void free_all() {
     g.lit_part = g.red_part = g.red_out = g.qr = g.qd = nullptr;
     g.d_fail = g.d_qrfail = nullptr;
     g.d_work = nullptr;
+    g.launches = 0;
     g.inited = false;
     g.sse_mode = -1;
 }
@@ -461,6 +465,7 @@ int ptucker_update_mode(int32_t n) {
         rc = timed("finalize", [&]() -> int {
             launch_heavy_finalize(m.nheavy, m.hrow, m.hnseg, m.hpbase, m.partials, g.J, g.lambda, g.A[n], g.esz,
                                   g.lda, g.sse_row[n], g.d_fail, S());
+            g.launches += 1;
             CK(cudaGetLastError());
             return PTUCKER_OK;
         });
@@ -514,6 +519,7 @@ int ptucker_error_literal(double* out) {
     if (rc) return rc;
     rc = timed("error_reduce", [&]() -> int {
         launch_sum(g.lit_part, g.mi[0].nslices * 32, g.red_part, g.red_out, S());
+        g.launches += 2;
         CK(cudaGetLastError());
         return PTUCKER_OK;
     });
@@ -529,6 +535,7 @@ int ptucker_error(double* out) {
     const ModeIndex& m = g.mi[g.sse_mode];
     rc = timed("error_reduce", [&]() -> int {
         launch_sum(g.sse_row[g.sse_mode] + m.r0, m.r1 - m.r0, g.red_part, g.red_out, S());
+        g.launches += 2;
         CK(cudaGetLastError());
         return PTUCKER_OK;
     });
@@ -563,6 +570,7 @@ int ptucker_orthogonalize(void) {
             launch_apply_rinv(g.qd, 8, J, g.A[n], g.esz, g.lda, I, J, R2, S());
             launch_mat_upper_mul(R2, R1, R, J, S());
             launch_core_mode_product(g.G, g.Gtmp, g.esz, g.N, J, n, R, S());
+            g.launches += 9;
             std::swap(g.G, g.Gtmp);
         }
         CK(cudaGetLastError());
@@ -661,10 +669,10 @@ int ptucker_info(char* buf, int32_t len) {
     snprintf(tmp, sizeof(tmp),
              "\"inited\": %s, \"N\": %d, \"J\": %d, \"prec\": \"%s\", \"policy\": \"%s\", \"nnz\": %lld, "
              "\"lambda\": %.17g, \"seg_len\": %d, \"rank\": %d, \"world\": %d, \"grid_update\": %d, "
-             "\"threads_per_cta\": %d, \"smem_core_bytes\": %d, \"modes\": [",
+             "\"threads_per_cta\": %d, \"smem_core_bytes\": %d, \"kernel_launches\": %lld, \"modes\": [",
              g.inited ? "true" : "false", g.N, g.J, g.prec == PTUCKER_F64 ? "f64" : "f32",
              g.prec == PTUCKER_F64 ? "F64" : (g.policy ? "F32-B" : "F32-A"), (long long)g.nnz, g.lambda, g.seg_len,
-             g.rank, g.world, g.grid_upd, kUpdThreads, g.gp_elems * g.esz);
+             g.rank, g.world, g.grid_upd, kUpdThreads, g.gp_elems * g.esz, (long long)g.launches);
     s += tmp;
     for (int n = 0; n < g.N; ++n) {
         const ModeIndex& m = g.mi[n];

@@ -61,57 +61,65 @@ __device__ __forceinline__ void ttv_inner(const TS* __restrict__ g, const TA (&a
     }
 }
 
-// Levels L = 1 .. N-2 of the chain (compile-time unrolled), fp type TF.
-// a[L] is the row of the L-th other mode; the child block stride is
-// J^(N-3-L) padded blocks.
-template <typename TS, typename TF, int N, int J, int L>
-__device__ __forceinline__ void ttv_level(const TS* __restrict__ g, const TF (&a)[N - 1][J], TF (&r)[J]) {
+// Outer levels L = 1 .. N-3 of the chain (compile-time unrolled), accumulated in
+// TO; the innermost level N-2 runs in TF and its J outputs are widened to TO.
+// a_out[L] is the row of the L-th other mode (TO), a_in the innermost row (TF).
+// The child block stride of level L is J^(N-3-L) padded blocks.
+template <typename TS, typename TF, typename TO, int N, int J, int L>
+__device__ __forceinline__ void ttv_level(const TS* __restrict__ g, const TF (&a_in)[J],
+                                          const TO (&a_out)[N - 1][J], TO (&r)[J]) {
     constexpr int GB = gblk(J, sizeof(TS));
-    if constexpr (L == N - 2) {
-        ttv_inner<TS, J, TF, TF>(g, a[N - 2], r);
-    } else {
-        constexpr int sub = ipow(J, N - 3 - L) * GB;
+    constexpr int sub = ipow(J, N - 3 - L) * GB;
 #pragma unroll
-        for (int j = 0; j < J; ++j) r[j] = TF(0);
+    for (int j = 0; j < J; ++j) r[j] = TO(0);
 #pragma unroll
-        for (int k = 0; k < J; ++k) {
-            TF t[J];
-            ttv_level<TS, TF, N, J, L + 1>(g + k * sub, a, t);
+    for (int k = 0; k < J; ++k) {
+        TO t[J];
+        if constexpr (L + 1 == N - 2) {
+            TF ti[J];
+            ttv_inner<TS, J, TF, TF>(g + k * sub, a_in, ti);
 #pragma unroll
-            for (int j = 0; j < J; ++j) r[j] = fma(a[L][k], t[j], r[j]);
+            for (int j = 0; j < J; ++j) t[j] = TO(ti[j]);
+        } else {
+            ttv_level<TS, TF, TO, N, J, L + 1>(g + k * sub, a_in, a_out, t);
         }
+#pragma unroll
+        for (int j = 0; j < J; ++j) r[j] = fma(a_out[L][k], t[j], r[j]);
     }
 }
 
-// delta for one entry.  Level 0 accumulates in TD (fp64 under policy F32-B);
-// for N >= 4 level 0 is a runtime loop reading a0[k] from the (L1-cached) row.
-template <typename TS, typename TF, typename TD, int N, int J>
-__device__ __forceinline__ void compute_delta(const TS* __restrict__ g, const TF (&a)[N - 1][J],
-                                              const TS* __restrict__ a0row, TD (&d)[J]) {
+// delta for one entry.  Precision policy: the
+// innermost stage (J^N of the J^N + ... + J^2 FMAs) runs in TF; every outer
+// stage accumulates in TO (fp64 under F32-B, fp32 under F32-A).  For N >= 4
+// level 0 is a runtime loop reading a0[k] from the (L1-resident) factor row.
+template <typename TS, typename TF, typename TO, int N, int J>
+__device__ __forceinline__ void compute_delta(const TS* __restrict__ g, const TF (&a_in)[J],
+                                              const TO (&a_out)[N - 1][J], const TS* __restrict__ a0row,
+                                              TO (&d)[J]) {
     constexpr int GB = gblk(J, sizeof(TS));
     if constexpr (N == 2) {
-        ttv_inner<TS, J, TD, TF>(g, a[0], d);
+        ttv_inner<TS, J, TO, TF>(g, a_in, d);
     } else if constexpr (N == 3) {
 #pragma unroll
-        for (int j = 0; j < J; ++j) d[j] = TD(0);
+        for (int j = 0; j < J; ++j) d[j] = TO(0);
 #pragma unroll
         for (int k = 0; k < J; ++k) {
             TF t[J];
-            ttv_inner<TS, J, TF, TF>(g + k * GB, a[1], t);
+            ttv_inner<TS, J, TF, TF>(g + k * GB, a_in, t);
 #pragma unroll
-            for (int j = 0; j < J; ++j) d[j] = fma(TD(a[0][k]), TD(t[j]), d[j]);
+            for (int j = 0; j < J; ++j) d[j] = fma(a_out[0][k], TO(t[j]), d[j]);
         }
     } else {
         constexpr int sub = ipow(J, N - 3) * GB;
 #pragma unroll
-        for (int j = 0; j < J; ++j) d[j] = TD(0);
+        for (int j = 0; j < J; ++j) d[j] = TO(0);
 #pragma unroll 1
         for (int k = 0; k < J; ++k) {
-            TF t[J];
-            ttv_level<TS, TF, N, J, 1>(g + k * sub, a, t);
-            const TD ak = TD(TF(a0row[k]));
+            TO t[J];
+            ttv_level<TS, TF, TO, N, J, 1>(g + k * sub, a_in, a_out, t);
+            const TO ak = TO(a0row[k]);
 #pragma unroll
-            for (int j = 0; j < J; ++j) d[j] = fma(ak, TD(t[j]), d[j]);
+            for (int j = 0; j < J; ++j) d[j] = fma(ak, t[j], d[j]);
         }
     }
 }
@@ -178,7 +186,7 @@ __device__ __forceinline__ void load_row(const TS* __restrict__ row, TS (&out)[J
 
 template <typename TS, typename TF, int N, int J, bool LAST64, bool LITERAL>
 __global__ void __launch_bounds__(kUpdThreads, 1) k_update(const UpdateParams<TS> p) {
-    using TD = typename std::conditional<LAST64 || std::is_same<TF, double>::value, double, float>::type;
+    using TD = typename std::conditional<LAST64 || std::is_same<TF, double>::value, double, float>::type;  // TO
     constexpr int NB = J * (J + 1) / 2;
     using V = typename Vec16<TS>::type;
     constexpr int VN = Vec16<TS>::n;
@@ -223,20 +231,22 @@ __global__ void __launch_bounds__(kUpdThreads, 1) k_update(const UpdateParams<TS
 #pragma unroll
             for (int k = 0; k < N - 1; ++k) crd[k] = __ldg(p.sc[k] + idx);
             const TS x = __ldg(p.sv + idx);
-            TF a[N - 1][J];
+            TF a_in[J];
+            TD a_out[N - 1][J];
+            load_row<TS, J>(p.A[N - 2] + (int64_t)crd[N - 2] * p.lda, a_in);
 #pragma unroll
-            for (int k = (N >= 4 ? 1 : 0); k < N - 1; ++k) {
+            for (int k = (N >= 4 ? 1 : 0); k < N - 2; ++k) {
                 TS tmp[J];
                 load_row<TS, J>(p.A[k] + (int64_t)crd[k] * p.lda, tmp);
 #pragma unroll
-                for (int j = 0; j < J; ++j) a[k][j] = TF(tmp[j]);
+                for (int j = 0; j < J; ++j) a_out[k][j] = TD(tmp[j]);
             }
             if constexpr (N >= 4) {
 #pragma unroll
-                for (int j = 0; j < J; ++j) a[0][j] = TF(0);
+                for (int j = 0; j < J; ++j) a_out[0][j] = TD(0);
             }
             TD d[J];
-            compute_delta<TS, TF, TD, N, J>(gs, a, p.A[0] + (int64_t)crd[0] * p.lda, d);
+            compute_delta<TS, TF, TD, N, J>(gs, a_in, a_out, p.A[0] + (int64_t)crd[0] * p.lda, d);
             const bool act = e < len;
             if constexpr (!LITERAL) {
                 double dd[J];
