@@ -235,7 +235,7 @@ int choose_kernel() {
     if (!g.kern) return fail(PTUCKER_EINVAL, "no compiled kernel for N=%d J=%d", g.N, g.J);
     int nsm = 148;
     CK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, g.device));
-    const size_t smem = (size_t)g.gp_elems * g.esz;
+    const size_t smem = ((size_t)g.gp_elems * g.esz + 15) / 16 * 16;  // + staging ring (added per kernel)
     int occ = g.kern->occupancy(false, smem);
     int occl = g.kern->occupancy(true, smem);
     CK(cudaGetLastError());

@@ -25,6 +25,18 @@
 
 namespace pt {
 
+// The permuted core of the mode being updated, when it fits the 64 KB constant
+// bank: every lane of a warp reads the same element at the same time, so the
+// compiler feeds the FFMAs from uniform registers (LDCU.128 -> FFMA R,R,UR,R)
+// without spending per-thread registers or shared-memory bandwidth on it.
+// One copy per translation unit (static); filled by set_core_constant().
+static __constant__ __align__(16) unsigned char c_core[65536];
+
+template <typename TS, int N, int J>
+struct CoreInConst {
+    static constexpr bool value = (size_t)ipow(J, N - 2) * gblk(J, sizeof(TS)) * sizeof(TS) <= sizeof(c_core);
+};
+
 template <typename T> struct Vec16;
 template <> struct Vec16<float> { using type = float4; static constexpr int n = 4; };
 template <> struct Vec16<double> { using type = double2; static constexpr int n = 2; };
@@ -91,7 +103,7 @@ __device__ __forceinline__ void ttv_level(const TS* __restrict__ g, const TF (&a
 // delta for one entry.  Precision policy: the
 // innermost stage (J^N of the J^N + ... + J^2 FMAs) runs in TF; every outer
 // stage accumulates in TO (fp64 under F32-B, fp32 under F32-A).  For N >= 4
-// level 0 is a runtime loop reading a0[k] from the (L1-resident) factor row.
+// level 0 is a runtime loop reading a0[k] from the entry's staged row in smem.
 template <typename TS, typename TF, typename TO, int N, int J>
 __device__ __forceinline__ void compute_delta(const TS* __restrict__ g, const TF (&a_in)[J],
                                               const TO (&a_out)[N - 1][J], const TS* __restrict__ a0row,
@@ -117,7 +129,8 @@ __device__ __forceinline__ void compute_delta(const TS* __restrict__ g, const TF
         for (int k = 0; k < J; ++k) {
             TO t[J];
             ttv_level<TS, TF, TO, N, J, 1>(g + k * sub, a_in, a_out, t);
-            const TO ak = TO(a0row[k]);
+            constexpr int VN = Vec16<TS>::n;
+            const TO ak = TO(a0row[(k / VN) * (kWarp * VN) + (k % VN)]);  // lane-interleaved stage layout
 #pragma unroll
             for (int j = 0; j < J; ++j) d[j] = fma(ak, t[j], d[j]);
         }
@@ -168,6 +181,25 @@ __device__ __forceinline__ bool chol_solve(double (&B)[J * (J + 1) / 2], const d
     return ok;
 }
 
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+    const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int PENDING>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(PENDING) : "memory"); }
+
+// Per-warp staging ring (2 stages) of the gathered factor rows of one entry
+// per lane: 16-byte chunk (stage, k, q) of lane l at ((stage*NR + k)*NQ + q)*32 + l,
+// so both the cp.async writes and the LDS.128 reads of a warp are conflict-free.
+template <typename TS, int N, int J>
+struct Stage {
+    static constexpr int NR = N - 1;
+    static constexpr int NQ = factor_ld(J, sizeof(TS)) * (int)sizeof(TS) / 16;
+    static constexpr int CHUNKS_PER_WARP = 2 * NR * NQ * kWarp;
+    static constexpr size_t BYTES_PER_WARP = (size_t)CHUNKS_PER_WARP * 16;
+};
+
 template <typename TS, int J>
 __device__ __forceinline__ void load_row(const TS* __restrict__ row, TS (&out)[J]) {
     using V = typename Vec16<TS>::type;
@@ -184,6 +216,24 @@ __device__ __forceinline__ void load_row(const TS* __restrict__ row, TS (&out)[J
     }
 }
 
+template <typename TS, int J, typename TR>
+__device__ __forceinline__ void stage_row(const uint4* __restrict__ chunk0, TR (&out)[J]) {
+    using V = typename Vec16<TS>::type;
+    constexpr int VN = Vec16<TS>::n;
+    constexpr int NV = (J + VN - 1) / VN;
+#pragma unroll
+    for (int q = 0; q < NV; ++q) {
+        const V v = *reinterpret_cast<const V*>(chunk0 + q * kWarp);
+        TS e[VN];
+        unpack<TS>(v, e);
+#pragma unroll
+        for (int u = 0; u < VN; ++u)
+            if (q * VN + u < J) out[q * VN + u] = TR(e[u]);
+    }
+}
+
+__host__ __device__ inline size_t gp_smem_bytes(int gp_elems, int esz) { return ((size_t)gp_elems * esz + 15) / 16 * 16; }
+
 template <typename TS, typename TF, int N, int J, bool LAST64, bool LITERAL>
 __global__ void __launch_bounds__(kUpdThreads, 1) k_update(const UpdateParams<TS> p) {
     using TD = typename std::conditional<LAST64 || std::is_same<TF, double>::value, double, float>::type;  // TO
@@ -191,14 +241,33 @@ __global__ void __launch_bounds__(kUpdThreads, 1) k_update(const UpdateParams<TS
     using V = typename Vec16<TS>::type;
     constexpr int VN = Vec16<TS>::n;
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    TS* gs = reinterpret_cast<TS*>(smem_raw);
-    {
+    constexpr bool GC = CoreInConst<TS, N, J>::value;
+    const TS* gs;
+    if constexpr (GC) {
+        gs = reinterpret_cast<const TS*>(c_core);
+    } else {
+        TS* gsm = reinterpret_cast<TS*>(smem_raw);
         const V* src = reinterpret_cast<const V*>(p.Gp);
-        V* dst = reinterpret_cast<V*>(gs);
+        V* dst = reinterpret_cast<V*>(gsm);
         for (int i = threadIdx.x; i < p.gp_elems / VN; i += blockDim.x) dst[i] = src[i];
+        __syncthreads();
+        gs = gsm;
     }
-    __syncthreads();
     const int lane = threadIdx.x & (kWarp - 1);
+    using ST = Stage<TS, N, J>;
+    constexpr int NR = ST::NR, NQ = ST::NQ;
+    uint4* stg = reinterpret_cast<uint4*>(smem_raw + (GC ? 0 : gp_smem_bytes(p.gp_elems, sizeof(TS)))) +
+                 (threadIdx.x / kWarp) * ST::CHUNKS_PER_WARP + lane;
+    // cp.async the N-1 gathered rows of an entry into stage st
+    auto issue_rows = [&](int st, const int (&crd)[NR]) {
+#pragma unroll
+        for (int k = 0; k < NR; ++k) {
+            const char* src = reinterpret_cast<const char*>(p.A[k] + (int64_t)crd[k] * p.lda);
+#pragma unroll
+            for (int q = 0; q < NQ; ++q) cp_async16(stg + ((st * NR + k) * NQ + q) * kWarp, src + 16 * q);
+        }
+        cp_async_commit();
+    };
 
     for (;;) {
         int s = 0;
@@ -225,28 +294,59 @@ __global__ void __launch_bounds__(kUpdThreads, 1) k_update(const UpdateParams<TS
             }
         }
 
-        for (int e = 0; e < iters; ++e) {
-            const int64_t idx = base + (int64_t)e * kWarp;
-            int crd[N - 1];
+        // software pipeline: coordinates two entries ahead (registers), gathered
+        // rows one entry ahead (cp.async into the 2-stage smem ring)
+        int crd0[NR], crd1[NR];
+        TS x0 = TS(0), x1 = TS(0);
 #pragma unroll
-            for (int k = 0; k < N - 1; ++k) crd[k] = __ldg(p.sc[k] + idx);
-            const TS x = __ldg(p.sv + idx);
+        for (int k = 0; k < NR; ++k) crd0[k] = crd1[k] = 0;
+        if (iters > 0) {
+#pragma unroll
+            for (int k = 0; k < NR; ++k) crd0[k] = __ldg(p.sc[k] + base);
+            x0 = __ldg(p.sv + base);
+            issue_rows(0, crd0);
+        }
+        if (iters > 1) {
+#pragma unroll
+            for (int k = 0; k < NR; ++k) crd1[k] = __ldg(p.sc[k] + base + kWarp);
+            x1 = __ldg(p.sv + base + kWarp);
+        }
+        for (int e = 0; e < iters; ++e) {
+            const int st = e & 1;
+            if (e + 1 < iters) issue_rows(st ^ 1, crd1);
+            int crd2[NR];
+            TS x2 = TS(0);
+            if (e + 2 < iters) {
+                const int64_t idx2 = base + (int64_t)(e + 2) * kWarp;
+#pragma unroll
+                for (int k = 0; k < NR; ++k) crd2[k] = __ldg(p.sc[k] + idx2);
+                x2 = __ldg(p.sv + idx2);
+            } else {
+#pragma unroll
+                for (int k = 0; k < NR; ++k) crd2[k] = 0;
+            }
+            if (e + 1 < iters) cp_async_wait<1>();
+            else cp_async_wait<0>();
+            const TS x = x0;
             TF a_in[J];
             TD a_out[N - 1][J];
-            load_row<TS, J>(p.A[N - 2] + (int64_t)crd[N - 2] * p.lda, a_in);
+            stage_row<TS, J>(stg + ((st * NR + (NR - 1)) * NQ) * kWarp, a_in);
 #pragma unroll
-            for (int k = (N >= 4 ? 1 : 0); k < N - 2; ++k) {
-                TS tmp[J];
-                load_row<TS, J>(p.A[k] + (int64_t)crd[k] * p.lda, tmp);
-#pragma unroll
-                for (int j = 0; j < J; ++j) a_out[k][j] = TD(tmp[j]);
-            }
+            for (int k = (N >= 4 ? 1 : 0); k < N - 2; ++k) stage_row<TS, J>(stg + ((st * NR + k) * NQ) * kWarp, a_out[k]);
             if constexpr (N >= 4) {
 #pragma unroll
                 for (int j = 0; j < J; ++j) a_out[0][j] = TD(0);
             }
             TD d[J];
-            compute_delta<TS, TF, TD, N, J>(gs, a_in, a_out, p.A[0] + (int64_t)crd[0] * p.lda, d);
+            compute_delta<TS, TF, TD, N, J>(gs, a_in, a_out,
+                                            reinterpret_cast<const TS*>(stg + (st * NR) * NQ * kWarp), d);
+#pragma unroll
+            for (int k = 0; k < NR; ++k) {
+                crd0[k] = crd1[k];
+                crd1[k] = crd2[k];
+            }
+            x0 = x1;
+            x1 = x2;
             const bool act = e < len;
             if constexpr (!LITERAL) {
                 double dd[J];
@@ -326,7 +426,10 @@ __global__ void __launch_bounds__(kUpdThreads, 1) k_update(const UpdateParams<TS
 template <typename TS, typename TF, int N, int J, bool LAST64>
 void launch_update(const void* params, bool literal, int grid, cudaStream_t st) {
     const UpdateParams<TS>& p = *reinterpret_cast<const UpdateParams<TS>*>(params);
-    const size_t smem = (size_t)p.gp_elems * sizeof(TS);
+    const size_t smem = (CoreInConst<TS, N, J>::value ? 0 : gp_smem_bytes(p.gp_elems, sizeof(TS))) +
+                        (kUpdThreads / kWarp) * Stage<TS, N, J>::BYTES_PER_WARP;
+    if (CoreInConst<TS, N, J>::value)
+        cudaMemcpyToSymbolAsync(c_core, p.Gp, (size_t)p.gp_elems * sizeof(TS), 0, cudaMemcpyDeviceToDevice, st);
     if (literal) {
         auto k = k_update<TS, TF, N, J, LAST64, true>;
         if (smem > 48 * 1024) cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -339,7 +442,8 @@ void launch_update(const void* params, bool literal, int grid, cudaStream_t st) 
 }
 
 template <typename TS, typename TF, int N, int J, bool LAST64>
-int occupancy_update(bool literal, size_t smem) {
+int occupancy_update(bool literal, size_t gp_bytes) {
+    const size_t smem = (CoreInConst<TS, N, J>::value ? 0 : gp_bytes) + (kUpdThreads / kWarp) * Stage<TS, N, J>::BYTES_PER_WARP;
     int nb = 0;
     if (literal) {
         auto k = k_update<TS, TF, N, J, LAST64, true>;
