@@ -217,6 +217,7 @@ def run_ours(args, cfg):
     t0 = time.perf_counter()
     pt.ptucker_init(coords, vals, cfg.dims, [J] * N, cfg.lam, cfg.seed)
     pt.ptucker_set_option("policy", 0 if args.policy == "F32-A" else 1)
+    pt.ptucker_set_option("tc", args.tc)
     pt.ptucker_synchronize()
     init_s = time.perf_counter() - t0
     info = pt.ptucker_info()
@@ -295,6 +296,8 @@ def run_ours(args, cfg):
         t0 = time.perf_counter()
         pt.ptucker_set_stream(stream.cuda_stream)
         pt.ptucker_init(pc, pv, cfg.dims, [J] * N, cfg.lam, cfg.seed)
+        pt.ptucker_set_option("policy", 0 if args.policy == "F32-A" else 1)
+        pt.ptucker_set_option("tc", args.tc)
         for _ in range(args.steps):
             pt.ptucker_sweep()
             pt.ptucker_error()
@@ -321,7 +324,7 @@ def run_ours(args, cfg):
             "vs_baseline": None, "dtype": "fp32 storage/contraction + fp64 normal equations" if cfg.dtype == "f32"
             else "f64", "data": "synthetic", "config": workload_config(cfg, args) | {"policy": policy},
             "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "clocks": clocks,
-            "init_s": init_s, "errors": errs[-1:], "info": {k: info[k] for k in ("grid_update", "seg_len", "modes")},
+            "init_s": init_s, "errors": errs[-1:], "info": {k: info[k] for k in ("grid_update", "seg_len", "tensor_cores", "modes")},
         }
         print(json.dumps(line), flush=True)
     if world > 1:
@@ -338,6 +341,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--policy", default="F32-B", choices=["F32-A", "F32-B"])
     ap.add_argument("--seg-len", type=int, default=256)
+    ap.add_argument("--tc", type=int, default=1, choices=[0, 1], help="tensor-core inner stage for order-3 fp32")
     ap.add_argument("--ref-seconds", type=float, default=12.0)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")

@@ -96,7 +96,9 @@ struct Ctx {
     unsigned int* d_work = nullptr;
     int sse_mode = -1;           // mode whose per-row SSE describes the current state
     int last_fail_mode = -1;
-    const UpdateKernel* kern = nullptr;
+    const UpdateKernel* kern = nullptr;      // row update (tensor-core variant when available)
+    const UpdateKernel* kern_alu = nullptr;  // ALU kernel (literal error pass, and updates when tc = 0)
+    int use_tc = 1;                          // option "tc"
     int grid_upd = 0, grid_lit = 0;
     int64_t launches = 0;        // kernels this library launched since init (gpu_launches evidence)
     // timing
@@ -211,12 +213,13 @@ int launch_update_kernel(int n, bool literal) {
     if (g.mi[n].nslices == 0) return PTUCKER_OK;
     CK(cudaMemsetAsync(g.d_work, 0, sizeof(unsigned int), S()));
     g.launches += 1;
+    const UpdateKernel* k = literal ? g.kern_alu : g.kern;
     if (g.prec == PTUCKER_F64) {
         UpdateParams<double> p = make_params<double>(n, literal);
-        g.kern->launch(&p, literal, grid, S());
+        k->launch(&p, literal, grid, S());
     } else {
         UpdateParams<float> p = make_params<float>(n, literal);
-        g.kern->launch(&p, literal, grid, S());
+        k->launch(&p, literal, grid, S());
     }
     CK(cudaGetLastError());
     return PTUCKER_OK;
@@ -231,13 +234,18 @@ int rebuild_gp() {
 
 int choose_kernel() {
     const int last64 = (g.prec == PTUCKER_F64) ? 1 : (g.policy ? 1 : 0);
-    g.kern = find_update_kernel(g.prec, last64, g.N, g.J);
-    if (!g.kern) return fail(PTUCKER_EINVAL, "no compiled kernel for N=%d J=%d", g.N, g.J);
+    g.kern_alu = find_update_kernel(g.prec, last64, g.N, g.J);
+    if (!g.kern_alu) return fail(PTUCKER_EINVAL, "no compiled kernel for N=%d J=%d", g.N, g.J);
+    g.kern = g.kern_alu;
+    if (g.use_tc && g.prec == PTUCKER_F32 && g.N == 3) {
+        const UpdateKernel* k = find_update_kernel_tc(last64, g.J);
+        if (k) g.kern = k;
+    }
     int nsm = 148;
     CK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, g.device));
     const size_t smem = ((size_t)g.gp_elems * g.esz + 15) / 16 * 16;  // + staging ring (added per kernel)
     int occ = g.kern->occupancy(false, smem);
-    int occl = g.kern->occupancy(true, smem);
+    int occl = g.kern_alu->occupancy(true, smem);
     CK(cudaGetLastError());
     if (occ < 1 || occl < 1) return fail(PTUCKER_ERESOURCE, "update kernel does not fit on an SM (smem %zu B)", smem);
     g.grid_upd = nsm * occ;
@@ -341,6 +349,12 @@ int ptucker_set_option(const char* key, int64_t value) {
         if (value < 1 || value > (1 << 20)) return fail(PTUCKER_EINVAL, "seg_len out of range");
         if (g.inited) return fail(PTUCKER_ESTATE, "seg_len must be set before ptucker_init");
         g.seg_len = (int)value;
+        return PTUCKER_OK;
+    }
+    if (k == "tc") {
+        if (value != 0 && value != 1) return fail(PTUCKER_EINVAL, "tc must be 0 or 1");
+        g.use_tc = (int)value;
+        if (g.inited) return choose_kernel();
         return PTUCKER_OK;
     }
     if (k == "time_kernels") {
@@ -669,10 +683,11 @@ int ptucker_info(char* buf, int32_t len) {
     snprintf(tmp, sizeof(tmp),
              "\"inited\": %s, \"N\": %d, \"J\": %d, \"prec\": \"%s\", \"policy\": \"%s\", \"nnz\": %lld, "
              "\"lambda\": %.17g, \"seg_len\": %d, \"rank\": %d, \"world\": %d, \"grid_update\": %d, "
-             "\"threads_per_cta\": %d, \"smem_core_bytes\": %d, \"kernel_launches\": %lld, \"modes\": [",
+             "\"threads_per_cta\": %d, \"smem_core_bytes\": %d, \"kernel_launches\": %lld, \"tensor_cores\": %s, \"modes\": [",
              g.inited ? "true" : "false", g.N, g.J, g.prec == PTUCKER_F64 ? "f64" : "f32",
              g.prec == PTUCKER_F64 ? "F64" : (g.policy ? "F32-B" : "F32-A"), (long long)g.nnz, g.lambda, g.seg_len,
-             g.rank, g.world, g.grid_upd, kUpdThreads, g.gp_elems * g.esz, (long long)g.launches);
+             g.rank, g.world, g.grid_upd, kUpdThreads, g.gp_elems * g.esz, (long long)g.launches,
+             (g.kern && g.kern != g.kern_alu) ? "true" : "false");
     s += tmp;
     for (int n = 0; n < g.N; ++n) {
         const ModeIndex& m = g.mi[n];

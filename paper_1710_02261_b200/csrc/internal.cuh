@@ -68,6 +68,8 @@ const UpdateKernel* update_kernels_f32b(int* count);
 const UpdateKernel* update_kernels_f64(int* count);
 // Returns nullptr when (prec, last64, N, J) was not compiled.
 const UpdateKernel* find_update_kernel(int prec, int last64, int N, int J);
+// Tensor-core variant (fp32, N = 3): innermost TTV stage on tcgen05 (update_tc.cu).
+const UpdateKernel* find_update_kernel_tc(int last64, int J);
 
 // (N, J) pairs compiled: N = 2..5, J in {2,3,4,5,8,10}, J^N <= 10^4.
 #define PT_NJ_LIST(X) \

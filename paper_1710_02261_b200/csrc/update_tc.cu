@@ -1,0 +1,420 @@
+// update_tc.cu -- row update for order-3 fp32 tensors with the innermost TTV
+// stage on the 5th-generation tensor cores (tcgen05, kind::tf32, TMEM
+// accumulators).
+//
+// For mode n with other modes m0 < m1, Eq. 12 regrouped as a TTV
+// chain is   delta(j) = sum_k0 a0[k0] * t[k0][j],   t[k0][j] = sum_k1 a1[k1] G'[k0][k1][j].
+// The inner stage, over the 128 entries a CTA holds at a time, is a dense GEMM
+//     T (128 x J^2) = A1 (128 x J) * Bt^T,   Bt[(k0,j)][k1] = G'[k0][k1][j],
+// with B = the core, shared by every entry.  It runs as 3xTF32 (a = a_hi + a_lo,
+// small products first: lo*hi, hi*lo, hi*hi) so its accuracy matches an fp32
+// FMA chain (tools/tc_probe.cu), accumulating in TMEM.  Each thread owns one
+// TMEM lane = one entry of its own row segment (the SELL-32 layout of the ALU
+// kernel, 4 slices per CTA), reads its J^2 outputs back with tcgen05.ld and
+// finishes level 0 (fp64 under F32-B), B += delta delta^T, c += x delta (fp64,
+// Eq. 10-11) and the Cholesky solve (Eq. 9) in registers.  The MMA for the next
+// entry is issued before the epilogue of the current one (double-buffered A
+// tiles and TMEM accumulators); the next rows are gathered by cp.async two
+// entries ahead.
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <cstdio>
+#include <cstdlib>
+
+#include "internal.cuh"
+#include "update.cuh"
+
+namespace pt {
+namespace tc {
+
+constexpr int kThreads = 128;  // one TMEM lane per thread; 4 warps = 4 SELL slices
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+// K-major SWIZZLE_NONE canonical layout (8-row x 16-byte core matrices): 32-bit
+// element (r, k) of a [rows x KP] tile, in floats.
+template <int KP>
+__device__ __forceinline__ int kmaj(int r, int k) {
+    return (((r >> 3) * (KP / 4) + (k >> 2)) * 128 + (r & 7) * 16 + (k & 3) * 4) / 4;
+}
+
+__device__ __forceinline__ uint64_t umma_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+    uint64_t d = (uint64_t)((saddr >> 4) & 0x3FFF);
+    d |= (uint64_t)((lbo >> 4) & 0x3FFF) << 16;
+    d |= (uint64_t)((sbo >> 4) & 0x3FFF) << 32;
+    d |= (uint64_t)1 << 46;  // sm100 descriptor version; base offset 0; SWIZZLE_NONE
+    return d;
+}
+
+__device__ __forceinline__ float tf32_rna(float x) {
+    uint32_t r;
+    asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
+    return __uint_as_float(r);
+}
+
+__device__ __forceinline__ void mma_tf32(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t idesc, uint32_t acc) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(tmem_d),
+        "l"(da), "l"(db), "r"(idesc), "r"(acc));
+}
+
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+    uint32_t done = 0;
+    while (!done) {
+        asm volatile(
+            "{\n\t.reg .pred P1;\n\tmbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2;\n\tselp.b32 %0, 1, 0, P1;\n\t}\n"
+            : "=r"(done)
+            : "r"(bar), "r"(parity)
+            : "memory");
+    }
+}
+
+
+__device__ __forceinline__ void tmem_ld16(uint32_t addr, float (&v)[16]) {
+    uint32_t r[16];
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
+          "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+        : "r"(addr));
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+    for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+template <int J>
+struct Shape {
+    static constexpr int KP = (J + 7) / 8 * 8;             // K padded to the tf32 MMA K-step (8)
+    static constexpr int KSTEPS = KP / 8;
+    static constexpr int NP = (J * J + 15) / 16 * 16;      // N padded to 16 (M = 128)
+    static constexpr int TCOLS = 2 * NP <= 32 ? 32 : (2 * NP <= 64 ? 64 : (2 * NP <= 128 ? 128 : (2 * NP <= 256 ? 256 : 512)));
+    static constexpr int LD = factor_ld(J, 4);             // padded factor row (floats)
+    static constexpr int NQ = LD / 4;                       // 16-byte chunks per row
+    // shared memory map (bytes)
+    static constexpr int B_BYTES = NP * KP * 4;                     // one of B_hi / B_lo
+    static constexpr int A_BYTES = kThreads * KP * 4;               // one of A_hi / A_lo (per stage)
+    static constexpr int RING_CHUNKS = 3 * 2 * NQ * kThreads;       // 3 stages x 2 rows
+    static constexpr int OFF_BHI = 0;
+    static constexpr int OFF_BLO = OFF_BHI + B_BYTES;
+    static constexpr int OFF_A = OFF_BLO + B_BYTES;                 // [stage][hi,lo]
+    static constexpr int OFF_RING = OFF_A + 4 * A_BYTES;
+    static constexpr int OFF_BAR = OFF_RING + RING_CHUNKS * 16;     // mbarriers: acc_full[2], a_full[2]
+    static constexpr int OFF_MISC = OFF_BAR + 32;                   // tmem base, group id
+    static constexpr int SMEM = OFF_MISC + 16;
+};
+
+template <int J, bool LAST64>
+__global__ void __launch_bounds__(kThreads, 2) k_update_tc(const UpdateParams<float> p) {
+    using SH = Shape<J>;
+    constexpr int KP = SH::KP, NP = SH::NP, NQ = SH::NQ;
+    constexpr int NB = J * (J + 1) / 2;
+    constexpr int GB = gblk(J, 4);
+    using TD = typename std::conditional<LAST64, double, float>::type;
+    extern __shared__ __align__(1024) unsigned char sm[];
+    float* sBhi = reinterpret_cast<float*>(sm + SH::OFF_BHI);
+    float* sBlo = reinterpret_cast<float*>(sm + SH::OFF_BLO);
+    uint4* ring = reinterpret_cast<uint4*>(sm + SH::OFF_RING);
+    uint64_t* mbar = reinterpret_cast<uint64_t*>(sm + SH::OFF_BAR);
+    uint32_t* misc = reinterpret_cast<uint32_t*>(sm + SH::OFF_MISC);
+    const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
+
+    // ---- B = core (hi/lo tf32 split), K-major: Bt[(k0, j)][k1] = G'[k0][k1][j] ----
+    for (int i = t; i < NP * KP; i += kThreads) {
+        const int c = i / KP, k1 = i % KP;
+        float v = 0.f;
+        if (c < J * J && k1 < J) v = p.Gp[(c / J) * GB + k1 * J + (c % J)];
+        const float h = tf32_rna(v);
+        sBhi[kmaj<KP>(c, k1)] = h;
+        sBlo[kmaj<KP>(c, k1)] = tf32_rna(v - h);
+    }
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&misc[0])),
+                     "n"(SH::TCOLS));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    if (t == 0) {
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(&mbar[0])), "r"(1));
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(&mbar[1])), "r"(1));
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(&mbar[2])), "r"(kThreads));
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(&mbar[3])), "r"(kThreads));
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    const uint32_t tmem = misc[0];
+    const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(NP >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
+    const uint32_t bhi = smem_u32(sBhi), blo = smem_u32(sBlo);
+    const uint32_t a_base = smem_u32(sm + SH::OFF_A);
+    uint32_t ntile = 0;  // tiles issued so far by this CTA (mbarrier phases, buffer parity)
+
+    // ring chunk (stage, row k, q) of this thread
+    auto ring_at = [&](int st, int k, int q) -> uint4* { return ring + ((st * 2 + k) * NQ + q) * kThreads + t; };
+    auto issue_rows = [&](int st, int c0, int c1) {
+        const char* s0 = reinterpret_cast<const char*>(p.A[0] + (int64_t)c0 * p.lda);
+        const char* s1 = reinterpret_cast<const char*>(p.A[1] + (int64_t)c1 * p.lda);
+#pragma unroll
+        for (int q = 0; q < NQ; ++q) {
+            cp_async16(ring_at(st, 0, q), s0 + 16 * q);
+            cp_async16(ring_at(st, 1, q), s1 + 16 * q);
+        }
+    };
+    // A tile of stage `st` (hi, lo), row t = this thread's a1 row, zero-padded to KP
+    auto arrive_a = [&](int st) {
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+        asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&mbar[2 + st])) : "memory");
+    };
+    auto build_a = [&](int rst, int st) {
+        float a1[NQ * 4];
+#pragma unroll
+        for (int q = 0; q < NQ; ++q) {
+            const float4 v = *reinterpret_cast<const float4*>(ring_at(rst, 1, q));
+            a1[4 * q] = v.x; a1[4 * q + 1] = v.y; a1[4 * q + 2] = v.z; a1[4 * q + 3] = v.w;
+        }
+        float* Ahi = reinterpret_cast<float*>(sm + SH::OFF_A + (st * 2 + 0) * SH::A_BYTES);
+        float* Alo = reinterpret_cast<float*>(sm + SH::OFF_A + (st * 2 + 1) * SH::A_BYTES);
+#pragma unroll
+        for (int q = 0; q < KP / 4; ++q) {
+            float h[4], l[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const int k = 4 * q + u;
+                const float v = (k < J) ? a1[k] : 0.f;
+                h[u] = tf32_rna(v);
+                l[u] = tf32_rna(v - h[u]);
+            }
+            *reinterpret_cast<float4*>(Ahi + kmaj<KP>(t, 4 * q)) = make_float4(h[0], h[1], h[2], h[3]);
+            *reinterpret_cast<float4*>(Alo + kmaj<KP>(t, 4 * q)) = make_float4(l[0], l[1], l[2], l[3]);
+        }
+    };
+    // 3xTF32 into TMEM buffer `buf` from A stage `st`: lo*hi, hi*lo, hi*hi (small terms first)
+    // A tile of stage `st` complete (all 128 rows arrived): the a_full barrier
+    // of that stage completes once per use, so its phase is (tile >> 1) & 1.
+    auto issue_mma = [&](int st, int buf, uint32_t tile) {
+        mbar_wait(smem_u32(&mbar[2 + st]), (tile >> 1) & 1);
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        const uint32_t ahi = a_base + (st * 2 + 0) * SH::A_BYTES, alo = a_base + (st * 2 + 1) * SH::A_BYTES;
+        const uint32_t d = tmem + buf * NP;
+        const uint32_t as[3] = {alo, ahi, ahi}, bs[3] = {bhi, blo, bhi};
+        uint32_t acc = 0;
+#pragma unroll
+        for (int pr = 0; pr < 3; ++pr)
+#pragma unroll
+            for (int ks = 0; ks < SH::KSTEPS; ++ks) {
+                // LBO: next 16-byte K chunk = next core matrix (128 B); SBO: next 8 rows
+                mma_tf32(d, umma_desc(as[pr] + ks * 256, 128, KP * 32), umma_desc(bs[pr] + ks * 256, 128, KP * 32),
+                         idesc, acc);
+                acc = 1;
+            }
+        asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                         smem_u32(&mbar[buf])) : "memory");
+    };
+
+    for (;;) {
+        __syncthreads();
+        if (t == 0) misc[1] = atomicAdd(p.work, 1u);
+        __syncthreads();
+        const int64_t s0 = (int64_t)misc[1] * 4;
+        if (s0 >= p.nslices) break;
+        const int64_t s = s0 + warp;
+        const bool vs = s < p.nslices;
+        const int64_t slot = s * kWarp + lane;
+        const int row = vs ? p.lane_row[slot] : -1;
+        const int len = vs ? p.lane_len[slot] : 0;
+        const int iters = p.slice_len[s0];
+        const int mylen = vs ? p.slice_len[s] : 0;
+        const int64_t base = vs ? p.slice_off[s] + lane : 0;
+
+        double B[NB], c[J], s2 = 0.0;
+#pragma unroll
+        for (int q = 0; q < NB; ++q) B[q] = 0.0;
+#pragma unroll
+        for (int q = 0; q < J; ++q) c[q] = 0.0;
+
+        if (iters > 0) {
+            // coordinates/values run 3 entries ahead of use (register queue q0 -> q1 -> q2),
+            // rows 2 ahead (cp.async ring of 3 stages, stage = entry % 3)
+            int ca0 = 0, cb0 = 0, ca1 = 0, cb1 = 0, ca2 = 0, cb2 = 0;
+            float x0 = 0.f, x1 = 0.f, x2 = 0.f;
+            auto load_crd = [&](int e, int& a, int& b, float& x) {
+                const bool v = e < mylen;
+                const int64_t idx = base + (int64_t)e * kWarp;
+                a = v ? __ldg(p.sc[0] + idx) : 0;
+                b = v ? __ldg(p.sc[1] + idx) : 0;
+                x = v ? __ldg(p.sv + idx) : 0.f;
+            };
+            load_crd(0, ca0, cb0, x0);
+            load_crd(1, ca1, cb1, x1);
+            load_crd(2, ca2, cb2, x2);
+            issue_rows(0, ca0, cb0);
+            cp_async_commit();
+            if (iters > 1) issue_rows(1, ca1, cb1);
+            cp_async_commit();
+            cp_async_wait<1>();
+            build_a(0, ntile & 1);
+            arrive_a(ntile & 1);
+            if (t == 0) issue_mma(ntile & 1, ntile & 1, ntile);
+            int rs = 0;  // ring stage of entry e
+            for (int e = 0; e < iters; ++e) {
+                const uint32_t tile = ntile + e;
+                const int rs1 = rs == 2 ? 0 : rs + 1, rs2 = rs1 == 2 ? 0 : rs1 + 1;
+                if (e + 2 < iters) issue_rows(rs2, ca2, cb2);
+                cp_async_commit();
+                const float x = x0;
+                // advance the coordinate queue: entry e+1 -> q0, e+2 -> q1, load e+3 -> q2
+                ca0 = ca1; cb0 = cb1; x0 = x1;
+                ca1 = ca2; cb1 = cb2; x1 = x2;
+                load_crd(e + 3, ca2, cb2, x2);
+                if (e + 1 < iters) {
+                    cp_async_wait<1>();
+                    build_a(rs1, (tile + 1) & 1);
+                    arrive_a((tile + 1) & 1);
+                    if (t == 0) issue_mma((tile + 1) & 1, (tile + 1) & 1, tile + 1);
+                }
+                // ---- epilogue of entry e ----
+                TD a0[J];
+#pragma unroll
+                for (int q = 0; q < NQ; ++q) {
+                    const float4 v = *reinterpret_cast<const float4*>(ring_at(rs, 0, q));
+                    const float w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+                    for (int u = 0; u < 4; ++u)
+                        if (4 * q + u < J) a0[4 * q + u] = TD(w[u]);
+                }
+                rs = rs1;
+                mbar_wait(smem_u32(&mbar[tile & 1]), (tile >> 1) & 1);
+                asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+                TD d[J];
+#pragma unroll
+                for (int j = 0; j < J; ++j) d[j] = TD(0);
+                const uint32_t taddr = tmem + ((uint32_t)(warp * 32) << 16) + (tile & 1) * NP;
+#pragma unroll
+                for (int c0 = 0; c0 < J * J; c0 += 16) {
+                    float v[16];
+                    tmem_ld16(taddr + c0, v);
+#pragma unroll
+                    for (int i = 0; i < 16; ++i) {
+                        const int cc = c0 + i;
+                        if (cc < J * J) d[cc % J] = fma(a0[cc / J], TD(v[i]), d[cc % J]);
+                    }
+                }
+                asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+                const bool act = e < len;
+                double dd[J];
+#pragma unroll
+                for (int j = 0; j < J; ++j) dd[j] = act ? double(d[j]) : 0.0;
+                const double xd = act ? double(x) : 0.0;
+#pragma unroll
+                for (int i = 0; i < J; ++i) {
+                    c[i] = fma(xd, dd[i], c[i]);
+#pragma unroll
+                    for (int j = i; j < J; ++j) B[up_idx(i, j, J)] = fma(dd[i], dd[j], B[up_idx(i, j, J)]);
+                }
+                s2 = fma(xd, xd, s2);
+            }
+            cp_async_wait<0>();
+            ntile += iters;
+        }
+
+        if (row < 0) continue;
+        const int64_t pidx = p.lane_pidx[slot];
+        if (pidx < 0) {
+            double a[J];
+            const bool ok = chol_solve<J>(B, c, p.lambda, a);
+            if (!ok) {
+                atomicCAS(p.fail, 0, row + 1);
+#pragma unroll
+                for (int j = 0; j < J; ++j) a[j] = 0.0;
+            }
+            float* out = p.An + (int64_t)row * p.lda;
+            double sse = s2, ac = 0.0, aa = 0.0, ec = 0.0;
+            float st[SH::LD];
+#pragma unroll
+            for (int j = 0; j < SH::LD; ++j) st[j] = 0.f;
+#pragma unroll
+            for (int j = 0; j < J; ++j) {
+                st[j] = float(a[j]);
+                const double at = double(st[j]);
+                sse = fma(-2.0 * at, c[j], sse);
+                ac = fma(a[j], c[j], ac);
+                aa = fma(a[j], a[j], aa);
+                ec = fma(at - a[j], c[j] - p.lambda * a[j], ec);
+            }
+            sse += ac - p.lambda * aa + 2.0 * ec;  // SSE of the stored row (see update.cuh)
+#pragma unroll
+            for (int q = 0; q < SH::NQ; ++q)
+                reinterpret_cast<float4*>(out)[q] = make_float4(st[4 * q], st[4 * q + 1], st[4 * q + 2], st[4 * q + 3]);
+            p.sse_row[row] = sse;
+        } else {
+            const int stp = p.lane_pstride[slot];
+            double* dst = p.partials + pidx;
+#pragma unroll
+            for (int q = 0; q < NB; ++q) dst[(int64_t)q * stp] = B[q];
+#pragma unroll
+            for (int q = 0; q < J; ++q) dst[(int64_t)(NB + q) * stp] = c[q];
+            dst[(int64_t)(NB + J) * stp] = s2;
+        }
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(SH::TCOLS));
+}
+
+template <int J, bool LAST64>
+void launch_tc(const void* params, bool literal, int grid, cudaStream_t st) {
+    (void)literal;
+    const UpdateParams<float>& p = *reinterpret_cast<const UpdateParams<float>*>(params);
+    auto k = k_update_tc<J, LAST64>;
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, Shape<J>::SMEM);
+    cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    k<<<grid, kThreads, Shape<J>::SMEM, st>>>(p);
+}
+
+template <int J, bool LAST64>
+int occupancy_tc(bool literal, size_t gp_bytes) {
+    (void)literal;
+    (void)gp_bytes;
+    auto k = k_update_tc<J, LAST64>;
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, Shape<J>::SMEM);
+    cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    // Resident CTAs per SM from the kernel's own resource use (the occupancy API
+    // under-reports this kernel on sm_100a): registers, shared memory, TMEM.
+    cudaFuncAttributes fa;
+    cudaFuncGetAttributes(&fa, k);
+    int dev = 0, smem_sm = 0, regs_sm = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&smem_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev);
+    cudaDeviceGetAttribute(&regs_sm, cudaDevAttrMaxRegistersPerMultiprocessor, dev);
+    const int regs = (fa.numRegs + 7) / 8 * 8;
+    const int by_regs = regs_sm / (regs * kThreads);
+    const int by_smem = smem_sm / (Shape<J>::SMEM + 1024);
+    int nb = by_regs < by_smem ? by_regs : by_smem;
+    const int tm = 512 / Shape<J>::TCOLS;  // TMEM: every resident CTA allocates TCOLS of the 512 columns
+    if (getenv("PTUCKER_DEBUG"))
+        fprintf(stderr, "[ptucker] tc occupancy J=%d smem=%d regs=%d: by_regs=%d by_smem=%d tmem=%d\n", J,
+                Shape<J>::SMEM, fa.numRegs, by_regs, by_smem, tm);
+    return nb < tm ? nb : tm;
+}
+
+}  // namespace tc
+
+#define PT_TC_J_LIST(X) X(2) X(3) X(4) X(5) X(8) X(10)
+
+namespace {
+#define PT_TC_ENTRY(J) {0, 0, 3, J, &tc::launch_tc<J, false>, &tc::occupancy_tc<J, false>}, \
+                       {0, 1, 3, J, &tc::launch_tc<J, true>, &tc::occupancy_tc<J, true>},
+const UpdateKernel kTcTable[] = {PT_TC_J_LIST(PT_TC_ENTRY)};
+#undef PT_TC_ENTRY
+}  // namespace
+
+const UpdateKernel* find_update_kernel_tc(int last64, int J) {
+    for (const auto& k : kTcTable)
+        if (k.J == J && k.last64 == last64) return &k;
+    return nullptr;
+}
+
+}  // namespace pt
