@@ -72,6 +72,21 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
 }
 
 
+__device__ __forceinline__ void tmem_ld32(uint32_t addr, float (&v)[32]) {
+    uint32_t r[32];
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+        "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
+          "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), "=r"(r[16]),
+          "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]),
+          "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+        : "r"(addr));
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+    for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+}
+
 __device__ __forceinline__ void tmem_ld16(uint32_t addr, float (&v)[16]) {
     uint32_t r[16];
     asm volatile(
@@ -100,7 +115,7 @@ struct Shape {
     static constexpr int OFF_BLO = OFF_BHI + B_BYTES;
     static constexpr int OFF_A = OFF_BLO + B_BYTES;                 // [stage][hi,lo]
     static constexpr int OFF_RING = OFF_A + 4 * A_BYTES;
-    static constexpr int OFF_BAR = OFF_RING + RING_CHUNKS * 16;     // mbarriers: acc_full[2], a_full[2]
+    static constexpr int OFF_BAR = OFF_RING + RING_CHUNKS * 16;     // mbarriers: acc_full[2]
     static constexpr int OFF_MISC = OFF_BAR + 32;                   // tmem base, group id
     static constexpr int SMEM = OFF_MISC + 16;
 };
@@ -137,8 +152,8 @@ __global__ void __launch_bounds__(kThreads, 2) k_update_tc(const UpdateParams<fl
     if (t == 0) {
         asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(&mbar[0])), "r"(1));
         asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(&mbar[1])), "r"(1));
-        asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(&mbar[2])), "r"(kThreads));
-        asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(&mbar[3])), "r"(kThreads));
+        misc[2] = 0;  // arrival counters of the two A stages
+        misc[3] = 0;
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -163,11 +178,6 @@ __global__ void __launch_bounds__(kThreads, 2) k_update_tc(const UpdateParams<fl
         }
     };
     // A tile of stage `st` (hi, lo), row t = this thread's a1 row, zero-padded to KP
-    auto arrive_a = [&](int st) {
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-        asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&mbar[2 + st])) : "memory");
-    };
     auto build_a = [&](int rst, int st) {
         float a1[NQ * 4];
 #pragma unroll
@@ -194,8 +204,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_update_tc(const UpdateParams<fl
     // 3xTF32 into TMEM buffer `buf` from A stage `st`: lo*hi, hi*lo, hi*hi (small terms first)
     // A tile of stage `st` complete (all 128 rows arrived): the a_full barrier
     // of that stage completes once per use, so its phase is (tile >> 1) & 1.
-    auto issue_mma = [&](int st, int buf, uint32_t tile) {
-        mbar_wait(smem_u32(&mbar[2 + st]), (tile >> 1) & 1);
+    auto issue_mma = [&](int st, int buf) {
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
         const uint32_t ahi = a_base + (st * 2 + 0) * SH::A_BYTES, alo = a_base + (st * 2 + 1) * SH::A_BYTES;
         const uint32_t d = tmem + buf * NP;
@@ -212,6 +221,21 @@ __global__ void __launch_bounds__(kThreads, 2) k_update_tc(const UpdateParams<fl
             }
         asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
                          smem_u32(&mbar[buf])) : "memory");
+    };
+
+    // A row written: make it visible to the tensor core's async proxy, then count
+    // the arrival; the LAST of the 128 threads issues the MMAs for that stage, so
+    // no thread ever blocks on the others here.  (acq_rel atomic: the issuer
+    // observes every writer's row and its completed tcgen05.ld of the buffer.)
+    auto arrive_a = [&](int st, int buf) {
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+        uint32_t old;
+        asm volatile("atom.acq_rel.cta.shared::cta.add.u32 %0, [%1], 1;" : "=r"(old) : "r"(smem_u32(&misc[2 + st])) : "memory");
+        if (old == kThreads - 1) {
+            misc[2 + st] = 0;
+            issue_mma(st, buf);
+        }
     };
 
     for (;;) {
@@ -256,8 +280,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_update_tc(const UpdateParams<fl
             cp_async_commit();
             cp_async_wait<1>();
             build_a(0, ntile & 1);
-            arrive_a(ntile & 1);
-            if (t == 0) issue_mma(ntile & 1, ntile & 1, ntile);
+            arrive_a(ntile & 1, ntile & 1);
             int rs = 0;  // ring stage of entry e
             for (int e = 0; e < iters; ++e) {
                 const uint32_t tile = ntile + e;
@@ -272,8 +295,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_update_tc(const UpdateParams<fl
                 if (e + 1 < iters) {
                     cp_async_wait<1>();
                     build_a(rs1, (tile + 1) & 1);
-                    arrive_a((tile + 1) & 1);
-                    if (t == 0) issue_mma((tile + 1) & 1, (tile + 1) & 1, tile + 1);
+                    arrive_a((tile + 1) & 1, (tile + 1) & 1);
                 }
                 // ---- epilogue of entry e ----
                 TD a0[J];
@@ -293,13 +315,23 @@ __global__ void __launch_bounds__(kThreads, 2) k_update_tc(const UpdateParams<fl
                 for (int j = 0; j < J; ++j) d[j] = TD(0);
                 const uint32_t taddr = tmem + ((uint32_t)(warp * 32) << 16) + (tile & 1) * NP;
 #pragma unroll
-                for (int c0 = 0; c0 < J * J; c0 += 16) {
-                    float v[16];
-                    tmem_ld16(taddr + c0, v);
+                for (int c0 = 0; c0 < J * J; c0 += 32) {
+                    if (c0 + 16 >= J * J) {
+                        float v[16];
+                        tmem_ld16(taddr + c0, v);
 #pragma unroll
-                    for (int i = 0; i < 16; ++i) {
-                        const int cc = c0 + i;
-                        if (cc < J * J) d[cc % J] = fma(a0[cc / J], TD(v[i]), d[cc % J]);
+                        for (int i = 0; i < 16; ++i) {
+                            const int cc = c0 + i;
+                            if (cc < J * J) d[cc % J] = fma(a0[cc / J], TD(v[i]), d[cc % J]);
+                        }
+                    } else {
+                        float v[32];
+                        tmem_ld32(taddr + c0, v);
+#pragma unroll
+                        for (int i = 0; i < 32; ++i) {
+                            const int cc = c0 + i;
+                            if (cc < J * J) d[cc % J] = fma(a0[cc / J], TD(v[i]), d[cc % J]);
+                        }
                     }
                 }
                 asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");

@@ -1,0 +1,76 @@
+"""Parity at BASELINE.json's full sizes, in the launch configuration bench.py times
+(default options: tensor cores for order-3 fp32, seg_len 256, F32-B): one mode
+update from the init state, checked on sampled rows that the FP64 oracle can
+compute one by one, plus size-independent properties (fused vs literal error).
+
+The oracle builds its own slice index (oracle.mode_index) and its own init
+(oracle.init_model, bit-identical to the library's by test_gpu_parity); nothing
+the oracle consumes comes from the CUDA path.
+"""
+import numpy as np
+import pytest
+
+from gen import synth
+
+pytestmark = pytest.mark.gpu
+
+# max entries of a sampled row the oracle recomputes (N*J^N literal ops per entry)
+ROW_BUDGET = {"c2": 10**9, "c3": 12_000, "c4": 10**9, "c5": 10**9}
+
+
+@pytest.fixture(scope="module")
+def pt():
+    import torch
+    assert torch.cuda.is_available()
+    torch.cuda.set_device(0)
+    from paper_1710_02261_b200 import build, ptucker
+    build.build()
+    ptucker.load()
+    yield ptucker
+    ptucker.ptucker_finalize()
+
+
+@pytest.mark.parametrize("name", ["c2", "c3", "c4", "c5"])
+def test_fullsize_sampled_rows(pt, orc, name):
+    cfg = synth.config(name)
+    coords, vals = synth.generate(cfg)
+    N, J = len(cfg.dims), cfg.J
+    pt.ptucker_finalize()
+    pt.ptucker_set_option("seg_len", 256)
+    pt.ptucker_init(coords, vals, cfg.dims, [J] * N, cfg.lam, cfg.seed)
+    info = pt.ptucker_info()
+    t = orc.Tensor(coords, vals, cfg.dims)
+    m = orc.init_model(cfg.dims, [J] * N, seed=cfg.seed, prec=0)   # == the library's init (bit-exact)
+    rng = np.random.default_rng(123)
+    worst = 0.0
+    for n in range(N):
+        if n:   # back to the init state (identical on both sides) for the next mode
+            pt.ptucker_set_factor(n - 1, m.A(n - 1).astype(np.float32))
+        pt.ptucker_update_mode(n)
+        gpu_n = pt.ptucker_get_factor(n).astype(np.float64)
+        row_ptr, perm = t.mode_index(n)
+        lens = np.diff(row_ptr)
+        cand = np.flatnonzero(lens <= ROW_BUDGET[name])
+        pick = rng.choice(cand, size=min(24, cand.size), replace=False).tolist()
+        heavy = np.flatnonzero((lens > 256) & (lens <= ROW_BUDGET[name]))
+        if heavy.size:
+            pick.append(int(heavy[np.argmax(lens[heavy])]))   # the longest checkable multi-segment row
+        empty = np.flatnonzero(lens == 0)
+        if empty.size:
+            pick.append(int(empty[0]))
+        for i in pick:
+            B, c, _ = orc.row_system(t, m, n, i)
+            a = orc.solve(B, c, cfg.lam)
+            den = np.linalg.norm(a)
+            if den == 0:
+                assert np.all(gpu_n[i] == 0)
+                continue
+            err = np.linalg.norm(gpu_n[i] - a) / den
+            worst = max(worst, err)
+            assert err <= 1e-5, (name, n, i, int(lens[i]), err)
+    pt.ptucker_sweep()
+    e_fused = pt.ptucker_error()
+    e_lit = pt.ptucker_error_literal()
+    assert abs(e_fused - e_lit) <= 1e-6 * e_lit
+    print(f"{name}: worst sampled row rel err {worst:.2e}; heavy rows per mode "
+          f"{[md['heavy_rows'] for md in info['modes']]}; error {e_fused:.6g}")

@@ -28,9 +28,23 @@ def pt():
 
 
 def gpu_model(pt, orc, N):
+    """The GPU's current state, read back (used only for checks of the GPU's own
+    output, never as an oracle input)."""
     G = pt.ptucker_get_core().astype(np.float64)
     A = [pt.ptucker_get_factor(n).astype(np.float64) for n in range(N)]
     return orc.Model(G, A)
+
+
+def push_state(pt, m, dtype):
+    """Put an oracle-made state (already representable in `dtype`) into the library."""
+    pt.ptucker_set_core(m.G.astype(dtype))
+    for n in range(m.N):
+        pt.ptucker_set_factor(n, m.A(n).astype(dtype))
+
+
+def rounded(orc, m, dtype):
+    """The oracle state rounded to the library's storage precision."""
+    return orc.Model(m.G.astype(dtype).astype(np.float64), [a.astype(dtype).astype(np.float64) for a in m.factors])
 
 
 def row_rel_err(a_gpu, a_ref):
@@ -51,11 +65,30 @@ def init_cfg(pt, cfg, policy=1, seg_len=256):
     return coords, vals
 
 
-def mode_update_parity(pt, orc, t, N, lam, tol, modes=None):
+def oracle_state(orc, t, cfg, sweeps):
+    """Identical starting state made by the ORACLE: its own init (bit-identical to the
+    library's, checked in test_init_and_index_bit_exact) plus `sweeps` FP64 sweeps,
+    rounded to the storage precision."""
+    N = len(cfg.dims)
+    prec = 1 if cfg.dtype == "f64" else 0
+    m = orc.init_model(cfg.dims, [cfg.J] * N, seed=0, prec=prec)
+    for _ in range(sweeps):
+        for n in range(N):
+            orc.update_mode(t, m, n, cfg.lam)
+    return rounded(orc, m, np.float64 if prec else np.float32)
+
+
+def mode_update_parity(pt, orc, t, cfg, tol, sweeps=0, modes=None):
+    """For each mode n: the same oracle-made state goes into both sides, both update
+    mode n once, the rows of A^(n) are compared (reading R20)."""
+    N = len(cfg.dims)
+    dtype = np.float64 if cfg.dtype == "f64" else np.float32
+    s0 = oracle_state(orc, t, cfg, sweeps)
     worst = 0.0
     for n in (range(N) if modes is None else modes):
-        m = gpu_model(pt, orc, N)
-        orc.update_mode(t, m, n, lam)
+        m = s0.copy()
+        push_state(pt, m, dtype)
+        orc.update_mode(t, m, n, cfg.lam)
         pt.ptucker_update_mode(n)
         err = row_rel_err(pt.ptucker_get_factor(n), m.A(n))
         worst = max(worst, float(err.max()) if err.size else 0.0)
@@ -87,10 +120,8 @@ def test_mode_update_f64_c1(pt, orc):
     cfg = synth.config("c1")
     coords, vals = init_cfg(pt, cfg)
     t = orc.Tensor(coords, vals, cfg.dims)
-    mode_update_parity(pt, orc, t, 3, cfg.lam, 1e-10)           # init state
-    for _ in range(2):
-        pt.ptucker_sweep()
-    mode_update_parity(pt, orc, t, 3, cfg.lam, 1e-10)           # mid-trajectory state
+    mode_update_parity(pt, orc, t, cfg, 1e-10, sweeps=0)        # init state
+    mode_update_parity(pt, orc, t, cfg, 1e-10, sweeps=2)        # mid-trajectory state
 
 
 @pytest.mark.parametrize("name,scale,seg", [("c2", 0.01, 256), ("c3", 0.002, 256), ("c3", 0.002, 7),
@@ -100,9 +131,8 @@ def test_mode_update_f32(pt, orc, name, scale, seg):
     coords, vals = init_cfg(pt, cfg, seg_len=seg)
     N = len(cfg.dims)
     t = orc.Tensor(coords, vals, cfg.dims)
-    w0 = mode_update_parity(pt, orc, t, N, cfg.lam, 1e-5)       # init state (worst case, survey E4)
-    pt.ptucker_sweep()
-    w1 = mode_update_parity(pt, orc, t, N, cfg.lam, 1e-5)       # mid-trajectory
+    w0 = mode_update_parity(pt, orc, t, cfg, 1e-5, sweeps=0)    # init state (worst case, survey E4)
+    w1 = mode_update_parity(pt, orc, t, cfg, 1e-5, sweeps=1)    # mid-trajectory
     info = pt.ptucker_info()
     print(f"{name} seg={seg} worst row rel err init {w0:.2e} mid {w1:.2e}; heavy rows "
           f"{[m['heavy_rows'] for m in info['modes']]}")
@@ -116,7 +146,7 @@ def test_mode_update_f64_variants(pt, orc, name, scale):
     coords, vals = init_cfg(pt, cfg)
     assert vals.dtype == np.float64
     t = orc.Tensor(coords, vals, cfg.dims)
-    mode_update_parity(pt, orc, t, len(cfg.dims), cfg.lam, 1e-10)
+    mode_update_parity(pt, orc, t, cfg, 1e-10)
 
 
 def test_policy_f32a_reported(pt, orc):
@@ -124,7 +154,7 @@ def test_policy_f32a_reported(pt, orc):
     cfg = synth.small("c2", 0.01)
     coords, vals = init_cfg(pt, cfg, policy=0)
     t = orc.Tensor(coords, vals, cfg.dims)
-    w = mode_update_parity(pt, orc, t, 3, cfg.lam, 1e-4)
+    w = mode_update_parity(pt, orc, t, cfg, 1e-4)
     print(f"F32-A worst row rel err {w:.2e}")
 
 
@@ -153,11 +183,11 @@ def test_error_trajectory(pt, orc, name, scale, iters):
 def test_error_of_identical_state(pt, orc):
     cfg = synth.small("c4", 0.001)
     coords, vals = init_cfg(pt, cfg)
-    pt.ptucker_sweep()
-    m = gpu_model(pt, orc, 5)
     t = orc.Tensor(coords, vals, cfg.dims)
+    m = oracle_state(orc, t, cfg, 1)
+    push_state(pt, m, np.float32)
     ref = orc.error(t, m)
-    assert abs(pt.ptucker_error() - ref) <= 1e-5 * ref
+    assert abs(pt.ptucker_error() - ref) <= 1e-5 * ref            # literal pass (state was set)
     assert abs(pt.ptucker_error_literal() - ref) <= 1e-5 * ref
 
 
@@ -167,10 +197,10 @@ def test_orthogonalize(pt, orc, name, scale, tol):
     cfg = synth.config(name) if scale == 1.0 else synth.small(name, scale)
     coords, vals = init_cfg(pt, cfg)
     N = len(cfg.dims)
-    for _ in range(2):
-        pt.ptucker_sweep()
-    m = gpu_model(pt, orc, N)
     t = orc.Tensor(coords, vals, cfg.dims)
+    m = oracle_state(orc, t, cfg, 2)
+    dtype = np.float64 if cfg.dtype == "f64" else np.float32
+    push_state(pt, m, dtype)
     e_before = orc.error(t, m)
     orc.orthogonalize(m)
     pt.ptucker_orthogonalize()
@@ -191,13 +221,15 @@ def test_edge_empty_rows_and_tiny(pt, orc):
     pt.ptucker_set_option("seg_len", 256)
     pt.ptucker_init(coords, vals, [5, 2, 2], [2, 2, 2], 0.01, 0)
     t = orc.Tensor(coords, vals, [5, 2, 2])
-    mode_update_parity(pt, orc, t, 3, 0.01, 1e-10)
+    tiny = synth.Config("tiny", (5, 2, 2), 3, 2, 0.01, 1, "f64", "uniform", "uniform", False)
+    mode_update_parity(pt, orc, t, tiny, 1e-10)
     a0 = pt.ptucker_get_factor(0)
     assert np.all(a0[[1, 2, 4]] == 0)
     # single entry, N = 2 (matrix case)
     pt.ptucker_init(np.array([[1, 2]], np.int32), np.array([0.5]), [3, 4], [3, 3], 0.1, 1)
     t = orc.Tensor([[1, 2]], [0.5], [3, 4])
-    mode_update_parity(pt, orc, t, 2, 0.1, 1e-10)
+    tiny2 = synth.Config("tiny2", (3, 4), 1, 3, 0.1, 1, "f64", "uniform", "uniform", False, seed=1)
+    mode_update_parity(pt, orc, t, tiny2, 1e-10)
 
 
 def test_worked_example(pt, orc):
