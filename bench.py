@@ -31,22 +31,23 @@ sys.path.insert(0, ROOT)
 from gen import synth  # noqa: E402
 
 METRIC = "observed entries/sec per full ALS iteration"
+POLICY = {"auto": -1, "F32-A": 0, "F32-B": 1, "F32-C": 2}
 UNIT = "entries/s"
 
 
 # ----------------------------------------------------------------------------- helpers
 def algorithmic_work(N: int, J: int, policy: str):
-    """FMAs per observed entry per mode update of the shipped kernel (DESIGN.md
-    "Roofline"): innermost TTV stage J^N (fp32 unless F64), outer stages
-    J^(N-1)+...+J^2 (fp64 under F32-B), normal equations J(J+1)/2 + J + 1 (fp64)."""
+    """FMAs per observed entry per mode update: innermost TTV
+    stage J^N (fp32 unless F64); outer level L (J^(L+2) FMAs, L = 0..N-3) in fp64
+    when the policy puts it there (F32-A: none, F32-B: level 0, F32-C: all);
+    normal equations J(J+1)/2 + J + 1 (fp64).  Returns (fp32 FMAs, fp64 FMAs)."""
     inner = J ** N
-    outer = sum(J ** k for k in range(2, N))
+    levels = [J ** (L + 2) for L in range(N - 2)]
     bc = J * (J + 1) // 2 + J + 1
     if policy == "F64":
-        return 0, inner + outer + bc
-    if policy == "F32-A":
-        return inner + outer, bc
-    return inner, outer + bc
+        return 0, inner + sum(levels) + bc
+    n64 = {"F32-A": 0, "F32-B": 1, "F32-C": N - 2}[policy]
+    return inner + sum(levels[n64:]), sum(levels[:n64]) + bc
 
 
 def clocks_sampler(device: int):
@@ -216,7 +217,7 @@ def run_ours(args, cfg):
     N, J = len(cfg.dims), cfg.J
     t0 = time.perf_counter()
     pt.ptucker_init(coords, vals, cfg.dims, [J] * N, cfg.lam, cfg.seed)
-    pt.ptucker_set_option("policy", 0 if args.policy == "F32-A" else 1)
+    pt.ptucker_set_option("policy", POLICY[args.policy])
     pt.ptucker_set_option("tc", args.tc)
     pt.ptucker_synchronize()
     init_s = time.perf_counter() - t0
@@ -296,7 +297,7 @@ def run_ours(args, cfg):
         t0 = time.perf_counter()
         pt.ptucker_set_stream(stream.cuda_stream)
         pt.ptucker_init(pc, pv, cfg.dims, [J] * N, cfg.lam, cfg.seed)
-        pt.ptucker_set_option("policy", 0 if args.policy == "F32-A" else 1)
+        pt.ptucker_set_option("policy", POLICY[args.policy])
         pt.ptucker_set_option("tc", args.tc)
         for _ in range(args.steps):
             pt.ptucker_sweep()
@@ -339,7 +340,7 @@ def main():
     ap.add_argument("--config", default="c5")
     ap.add_argument("--scale", type=float, default=1.0, help="shrink the config (tests only)")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--policy", default="F32-B", choices=["F32-A", "F32-B"])
+    ap.add_argument("--policy", default="auto", choices=list(POLICY))
     ap.add_argument("--seg-len", type=int, default=256)
     ap.add_argument("--tc", type=int, default=1, choices=[0, 1], help="tensor-core inner stage for order-3 fp32")
     ap.add_argument("--ref-seconds", type=float, default=12.0)

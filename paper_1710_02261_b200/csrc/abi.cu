@@ -19,10 +19,12 @@
 
 namespace pt {
 
-const UpdateKernel* find_update_kernel(int prec, int last64, int N, int J) {
+const UpdateKernel* find_update_kernel(int prec, int l64, int N, int J) {
     int cnt = 0;
+    if (prec == PTUCKER_F32 && N <= 3 && l64 > 1) l64 = 1;  // N = 3 has a single outer level
     const UpdateKernel* t = prec == PTUCKER_F64 ? update_kernels_f64(&cnt)
-                            : (last64 ? update_kernels_f32b(&cnt) : update_kernels_f32a(&cnt));
+                            : (l64 == 0 ? update_kernels_f32a(&cnt)
+                                        : (l64 == 1 ? update_kernels_f32b(&cnt) : update_kernels_f32c(&cnt)));
     for (int i = 0; i < cnt; ++i)
         if (t[i].N == N && t[i].J == J) return &t[i];
     return nullptr;
@@ -77,7 +79,7 @@ struct Ctx {
     double lambda = 0.0;
     uint64_t seed = 0;
     int lda = 0, gp_elems = 0;
-    int policy = 1;     // F32-B by default
+    int policy = -1;    // -1 = automatic per order; else outer fp64 levels
     int seg_len = 256;  // S
     DeviceArena arena, scratch;
     void* A[kMaxN] = {nullptr};
@@ -232,8 +234,16 @@ int rebuild_gp() {
     return PTUCKER_OK;
 }
 
+// outer TTV levels in fp64 for the current policy (auto: F32-B for N = 3 and 5,
+// F32-C (all outer levels) for N = 4 -- chosen by measured row error)
+int policy_l64() {
+    if (g.prec == PTUCKER_F64) return 1;
+    if (g.policy >= 0) return g.policy == 2 ? (g.N >= 4 ? g.N - 2 : 1) : g.policy;
+    return g.N == 4 ? 2 : 1;
+}
+
 int choose_kernel() {
-    const int last64 = (g.prec == PTUCKER_F64) ? 1 : (g.policy ? 1 : 0);
+    const int last64 = policy_l64();
     g.kern_alu = find_update_kernel(g.prec, last64, g.N, g.J);
     if (!g.kern_alu) return fail(PTUCKER_EINVAL, "no compiled kernel for N=%d J=%d", g.N, g.J);
     g.kern = g.kern_alu;
@@ -340,7 +350,7 @@ int ptucker_set_option(const char* key, int64_t value) {
     if (!key) return fail(PTUCKER_EINVAL, "null key");
     const std::string k = key;
     if (k == "policy") {
-        if (value != 0 && value != 1) return fail(PTUCKER_EINVAL, "policy must be 0 or 1");
+        if (value < -1 || value > 2) return fail(PTUCKER_EINVAL, "policy must be -1 (auto), 0, 1 or 2");
         g.policy = (int)value;
         if (g.inited) return choose_kernel();
         return PTUCKER_OK;
@@ -390,8 +400,7 @@ int ptucker_init(const int32_t* coords, const void* vals, int32_t vals_dtype, in
         if (!std::isfinite(v)) return fail(PTUCKER_EINVAL, "value of entry %lld is not finite", (long long)e);
     }
     {
-        const int last64 = (vals_dtype == PTUCKER_F64) ? 1 : (g.policy ? 1 : 0);
-        if (!find_update_kernel(vals_dtype, last64, order, J))
+        if (!find_update_kernel(vals_dtype, 1, order, J))
             return fail(PTUCKER_EINVAL, "(N=%d, J=%d) is not a compiled kernel shape", order, J);
     }
     // ---- fresh context ----
@@ -685,7 +694,7 @@ int ptucker_info(char* buf, int32_t len) {
              "\"lambda\": %.17g, \"seg_len\": %d, \"rank\": %d, \"world\": %d, \"grid_update\": %d, "
              "\"threads_per_cta\": %d, \"smem_core_bytes\": %d, \"kernel_launches\": %lld, \"tensor_cores\": %s, \"modes\": [",
              g.inited ? "true" : "false", g.N, g.J, g.prec == PTUCKER_F64 ? "f64" : "f32",
-             g.prec == PTUCKER_F64 ? "F64" : (g.policy ? "F32-B" : "F32-A"), (long long)g.nnz, g.lambda, g.seg_len,
+             g.prec == PTUCKER_F64 ? "F64" : (policy_l64() == 0 ? "F32-A" : (policy_l64() == 1 ? "F32-B" : "F32-C")), (long long)g.nnz, g.lambda, g.seg_len,
              g.rank, g.world, g.grid_upd, kUpdThreads, g.gp_elems * g.esz, (long long)g.launches,
              (g.kern && g.kern != g.kern_alu) ? "true" : "false");
     s += tmp;

@@ -57,24 +57,29 @@ using UpdateLauncher = void (*)(const void* params, bool literal, int grid, cuda
 using UpdateOccupancy = int (*)(bool literal, size_t smem);
 
 struct UpdateKernel {
-    int prec, last64, N, J;
+    int prec, l64, N, J;  // l64: outer TTV levels in fp64 (precision policy)
     UpdateLauncher launch;
     UpdateOccupancy occupancy;
 };
 
-// Registries filled by the instantiation units (update_f32a.cu, update_f32b.cu, update_f64.cu).
+// Registries filled by the instantiation units (update_f32a.cu: l64 = 0,
+// update_f32b.cu: l64 = 1, update_f32c.cu: l64 = N-2 for N >= 4, update_f64.cu).
 const UpdateKernel* update_kernels_f32a(int* count);
 const UpdateKernel* update_kernels_f32b(int* count);
+const UpdateKernel* update_kernels_f32c(int* count);
 const UpdateKernel* update_kernels_f64(int* count);
-// Returns nullptr when (prec, last64, N, J) was not compiled.
-const UpdateKernel* find_update_kernel(int prec, int last64, int N, int J);
+// Returns nullptr when (prec, l64, N, J) was not compiled.
+const UpdateKernel* find_update_kernel(int prec, int l64, int N, int J);
 // Tensor-core variant (fp32, N = 3): innermost TTV stage on tcgen05 (update_tc.cu).
-const UpdateKernel* find_update_kernel_tc(int last64, int J);
+const UpdateKernel* find_update_kernel_tc(int l64, int J);
 
 // (N, J) pairs compiled: N = 2..5, J in {2,3,4,5,8,10}, J^N <= 10^4.
 #define PT_NJ_LIST(X) \
     X(2, 2) X(2, 3) X(2, 4) X(2, 5) X(2, 8) X(2, 10) \
     X(3, 2) X(3, 3) X(3, 4) X(3, 5) X(3, 8) X(3, 10) \
+    X(4, 2) X(4, 3) X(4, 4) X(4, 5) X(4, 8) X(4, 10) \
+    X(5, 2) X(5, 3) X(5, 4) X(5, 5)
+#define PT_NJ_LIST_N45(X) \
     X(4, 2) X(4, 3) X(4, 4) X(4, 5) X(4, 8) X(4, 10) \
     X(5, 2) X(5, 3) X(5, 4) X(5, 5)
 

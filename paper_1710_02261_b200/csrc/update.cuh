@@ -73,13 +73,20 @@ __device__ __forceinline__ void ttv_inner(const TS* __restrict__ g, const TA (&a
     }
 }
 
-// Outer levels L = 1 .. N-3 of the chain (compile-time unrolled), accumulated in
-// TO; the innermost level N-2 runs in TF and its J outputs are widened to TO.
-// a_out[L] is the row of the L-th other mode (TO), a_in the innermost row (TF).
-// The child block stride of level L is J^(N-3-L) padded blocks.
-template <typename TS, typename TF, typename TO, int N, int J, int L>
+// Precision policy: the innermost TTV stage (level
+// N-2, J^N of the J^N + ... + J^2 FMAs) always runs in TF; outer level L
+// accumulates in fp64 when L < L64 (L64 = number of outer levels in fp64,
+// counted from level 0: 0 = "F32-A", 1 = "F32-B", N-2 = "F32-C").
+template <typename TF, int L, int L64>
+using LevelT = typename std::conditional<(L < L64) || std::is_same<TF, double>::value, double, TF>::type;
+
+// Outer levels L = 1 .. N-3 of the chain (compile-time unrolled).  a_out[L] is
+// the raw row of the L-th other mode, a_in the innermost row.  The child block
+// stride of level L is J^(N-3-L) padded blocks.
+template <typename TS, typename TF, int N, int J, int L64, int L>
 __device__ __forceinline__ void ttv_level(const TS* __restrict__ g, const TF (&a_in)[J],
-                                          const TO (&a_out)[N - 1][J], TO (&r)[J]) {
+                                          const TS (&a_out)[N - 1][J], LevelT<TF, L, L64> (&r)[J]) {
+    using TO = LevelT<TF, L, L64>;
     constexpr int GB = gblk(J, sizeof(TS));
     constexpr int sub = ipow(J, N - 3 - L) * GB;
 #pragma unroll
@@ -93,21 +100,24 @@ __device__ __forceinline__ void ttv_level(const TS* __restrict__ g, const TF (&a
 #pragma unroll
             for (int j = 0; j < J; ++j) t[j] = TO(ti[j]);
         } else {
-            ttv_level<TS, TF, TO, N, J, L + 1>(g + k * sub, a_in, a_out, t);
-        }
+            LevelT<TF, L + 1, L64> tc[J];
+            ttv_level<TS, TF, N, J, L64, L + 1>(g + k * sub, a_in, a_out, tc);
 #pragma unroll
-        for (int j = 0; j < J; ++j) r[j] = fma(a_out[L][k], t[j], r[j]);
+            for (int j = 0; j < J; ++j) t[j] = TO(tc[j]);
+        }
+        const TO ak = TO(a_out[L][k]);
+#pragma unroll
+        for (int j = 0; j < J; ++j) r[j] = fma(ak, t[j], r[j]);
     }
 }
 
-// delta for one entry.  Precision policy: the
-// innermost stage (J^N of the J^N + ... + J^2 FMAs) runs in TF; every outer
-// stage accumulates in TO (fp64 under F32-B, fp32 under F32-A).  For N >= 4
-// level 0 is a runtime loop reading a0[k] from the entry's staged row in smem.
-template <typename TS, typename TF, typename TO, int N, int J>
+// delta for one entry, in LevelT<TF, 0, L64>.  For N >= 4 level 0 is a runtime
+// loop reading a0[k] from the entry's staged row in smem.
+template <typename TS, typename TF, int N, int J, int L64>
 __device__ __forceinline__ void compute_delta(const TS* __restrict__ g, const TF (&a_in)[J],
-                                              const TO (&a_out)[N - 1][J], const TS* __restrict__ a0row,
-                                              TO (&d)[J]) {
+                                              const TS (&a_out)[N - 1][J], const TS* __restrict__ a0row,
+                                              LevelT<TF, 0, L64> (&d)[J]) {
+    using TO = LevelT<TF, 0, L64>;
     constexpr int GB = gblk(J, sizeof(TS));
     if constexpr (N == 2) {
         ttv_inner<TS, J, TO, TF>(g, a_in, d);
@@ -118,8 +128,9 @@ __device__ __forceinline__ void compute_delta(const TS* __restrict__ g, const TF
         for (int k = 0; k < J; ++k) {
             TF t[J];
             ttv_inner<TS, J, TF, TF>(g + k * GB, a_in, t);
+            const TO ak = TO(a_out[0][k]);
 #pragma unroll
-            for (int j = 0; j < J; ++j) d[j] = fma(a_out[0][k], TO(t[j]), d[j]);
+            for (int j = 0; j < J; ++j) d[j] = fma(ak, TO(t[j]), d[j]);
         }
     } else {
         constexpr int sub = ipow(J, N - 3) * GB;
@@ -127,12 +138,12 @@ __device__ __forceinline__ void compute_delta(const TS* __restrict__ g, const TF
         for (int j = 0; j < J; ++j) d[j] = TO(0);
 #pragma unroll 1
         for (int k = 0; k < J; ++k) {
-            TO t[J];
-            ttv_level<TS, TF, TO, N, J, 1>(g + k * sub, a_in, a_out, t);
+            LevelT<TF, 1, L64> t[J];
+            ttv_level<TS, TF, N, J, L64, 1>(g + k * sub, a_in, a_out, t);
             constexpr int VN = Vec16<TS>::n;
             const TO ak = TO(a0row[(k / VN) * (kWarp * VN) + (k % VN)]);  // lane-interleaved stage layout
 #pragma unroll
-            for (int j = 0; j < J; ++j) d[j] = fma(ak, t[j], d[j]);
+            for (int j = 0; j < J; ++j) d[j] = fma(ak, TO(t[j]), d[j]);
         }
     }
 }
@@ -234,9 +245,9 @@ __device__ __forceinline__ void stage_row(const uint4* __restrict__ chunk0, TR (
 
 __host__ __device__ inline size_t gp_smem_bytes(int gp_elems, int esz) { return ((size_t)gp_elems * esz + 15) / 16 * 16; }
 
-template <typename TS, typename TF, int N, int J, bool LAST64, bool LITERAL>
+template <typename TS, typename TF, int N, int J, int L64, bool LITERAL>
 __global__ void __launch_bounds__(kUpdThreads, 1) k_update(const UpdateParams<TS> p) {
-    using TD = typename std::conditional<LAST64 || std::is_same<TF, double>::value, double, float>::type;  // TO
+    using TD = LevelT<TF, 0, L64>;  // type of delta
     constexpr int NB = J * (J + 1) / 2;
     using V = typename Vec16<TS>::type;
     constexpr int VN = Vec16<TS>::n;
@@ -329,16 +340,16 @@ __global__ void __launch_bounds__(kUpdThreads, 1) k_update(const UpdateParams<TS
             else cp_async_wait<0>();
             const TS x = x0;
             TF a_in[J];
-            TD a_out[N - 1][J];
+            TS a_out[N - 1][J];
             stage_row<TS, J>(stg + ((st * NR + (NR - 1)) * NQ) * kWarp, a_in);
 #pragma unroll
             for (int k = (N >= 4 ? 1 : 0); k < N - 2; ++k) stage_row<TS, J>(stg + ((st * NR + k) * NQ) * kWarp, a_out[k]);
             if constexpr (N >= 4) {
 #pragma unroll
-                for (int j = 0; j < J; ++j) a_out[0][j] = TD(0);
+                for (int j = 0; j < J; ++j) a_out[0][j] = TS(0);
             }
             TD d[J];
-            compute_delta<TS, TF, TD, N, J>(gs, a_in, a_out,
+            compute_delta<TS, TF, N, J, L64>(gs, a_in, a_out,
                                             reinterpret_cast<const TS*>(stg + (st * NR) * NQ * kWarp), d);
 #pragma unroll
             for (int k = 0; k < NR; ++k) {
@@ -423,7 +434,7 @@ __global__ void __launch_bounds__(kUpdThreads, 1) k_update(const UpdateParams<TS
     }
 }
 
-template <typename TS, typename TF, int N, int J, bool LAST64>
+template <typename TS, typename TF, int N, int J, int L64>
 void launch_update(const void* params, bool literal, int grid, cudaStream_t st) {
     const UpdateParams<TS>& p = *reinterpret_cast<const UpdateParams<TS>*>(params);
     const size_t smem = (CoreInConst<TS, N, J>::value ? 0 : gp_smem_bytes(p.gp_elems, sizeof(TS))) +
@@ -431,26 +442,26 @@ void launch_update(const void* params, bool literal, int grid, cudaStream_t st) 
     if (CoreInConst<TS, N, J>::value)
         cudaMemcpyToSymbolAsync(c_core, p.Gp, (size_t)p.gp_elems * sizeof(TS), 0, cudaMemcpyDeviceToDevice, st);
     if (literal) {
-        auto k = k_update<TS, TF, N, J, LAST64, true>;
+        auto k = k_update<TS, TF, N, J, L64, true>;
         if (smem > 48 * 1024) cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         k<<<grid, kUpdThreads, smem, st>>>(p);
     } else {
-        auto k = k_update<TS, TF, N, J, LAST64, false>;
+        auto k = k_update<TS, TF, N, J, L64, false>;
         if (smem > 48 * 1024) cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         k<<<grid, kUpdThreads, smem, st>>>(p);
     }
 }
 
-template <typename TS, typename TF, int N, int J, bool LAST64>
+template <typename TS, typename TF, int N, int J, int L64>
 int occupancy_update(bool literal, size_t gp_bytes) {
     const size_t smem = (CoreInConst<TS, N, J>::value ? 0 : gp_bytes) + (kUpdThreads / kWarp) * Stage<TS, N, J>::BYTES_PER_WARP;
     int nb = 0;
     if (literal) {
-        auto k = k_update<TS, TF, N, J, LAST64, true>;
+        auto k = k_update<TS, TF, N, J, L64, true>;
         if (smem > 48 * 1024) cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k, kUpdThreads, smem);
     } else {
-        auto k = k_update<TS, TF, N, J, LAST64, false>;
+        auto k = k_update<TS, TF, N, J, L64, false>;
         if (smem > 48 * 1024) cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k, kUpdThreads, smem);
     }

@@ -1,9 +1,9 @@
-// update_f32b.cu -- instantiations of the fused row-update kernel: TS=float, TF=float, LAST64=true.
+// update_f32b.cu -- instantiations of the fused row-update kernel: TS=float, TF=float, l64=1.
 #include "update.cuh"
 
 namespace pt {
 namespace {
-#define PT_ENTRY(N, J) {0, 1, N, J, &launch_update<float, float, N, J, true>, &occupancy_update<float, float, N, J, true>},
+#define PT_ENTRY(N, J) {0, 1, N, J, &launch_update<float, float, N, J, 1>, &occupancy_update<float, float, N, J, 1>},
 const UpdateKernel kTable[] = {PT_NJ_LIST(PT_ENTRY)};
 #undef PT_ENTRY
 }  // namespace

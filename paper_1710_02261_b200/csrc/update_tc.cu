@@ -443,9 +443,10 @@ const UpdateKernel kTcTable[] = {PT_TC_J_LIST(PT_TC_ENTRY)};
 #undef PT_TC_ENTRY
 }  // namespace
 
-const UpdateKernel* find_update_kernel_tc(int last64, int J) {
+const UpdateKernel* find_update_kernel_tc(int l64, int J) {
+    const int want = l64 > 0 ? 1 : 0;
     for (const auto& k : kTcTable)
-        if (k.J == J && k.last64 == last64) return &k;
+        if (k.J == J && k.l64 == want) return &k;
     return nullptr;
 }
 

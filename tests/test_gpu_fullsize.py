@@ -30,14 +30,16 @@ def pt():
     ptucker.ptucker_finalize()
 
 
-@pytest.mark.parametrize("name", ["c2", "c3", "c4", "c5"])
-def test_fullsize_sampled_rows(pt, orc, name):
+# policy -1 = the library's automatic choice (held to 1e-5); 0 = F32-A, reported only
+@pytest.mark.parametrize("name,policy", [("c2", -1), ("c3", -1), ("c4", -1), ("c5", -1), ("c2", 0), ("c5", 0)])
+def test_fullsize_sampled_rows(pt, orc, name, policy):
     cfg = synth.config(name)
     coords, vals = synth.generate(cfg)
     N, J = len(cfg.dims), cfg.J
     pt.ptucker_finalize()
     pt.ptucker_set_option("seg_len", 256)
     pt.ptucker_init(coords, vals, cfg.dims, [J] * N, cfg.lam, cfg.seed)
+    pt.ptucker_set_option("policy", policy)
     info = pt.ptucker_info()
     t = orc.Tensor(coords, vals, cfg.dims)
     m = orc.init_model(cfg.dims, [J] * N, seed=cfg.seed, prec=0)   # == the library's init (bit-exact)
@@ -67,10 +69,10 @@ def test_fullsize_sampled_rows(pt, orc, name):
                 continue
             err = np.linalg.norm(gpu_n[i] - a) / den
             worst = max(worst, err)
-            assert err <= 1e-5, (name, n, i, int(lens[i]), err)
+            assert err <= (1e-5 if policy < 0 else 1e-4), (name, n, i, int(lens[i]), err)
     pt.ptucker_sweep()
     e_fused = pt.ptucker_error()
     e_lit = pt.ptucker_error_literal()
     assert abs(e_fused - e_lit) <= 1e-6 * e_lit
-    print(f"{name}: worst sampled row rel err {worst:.2e}; heavy rows per mode "
+    print(f"{name} policy={info['policy']}: worst sampled row rel err {worst:.2e}; heavy rows per mode "
           f"{[md['heavy_rows'] for md in info['modes']]}; error {e_fused:.6g}")

@@ -56,7 +56,7 @@ def row_rel_err(a_gpu, a_ref):
     return num[~zero] / den[~zero]
 
 
-def init_cfg(pt, cfg, policy=1, seg_len=256):
+def init_cfg(pt, cfg, policy=-1, seg_len=256):
     coords, vals = synth.generate(cfg)
     pt.ptucker_finalize()
     pt.ptucker_set_option("seg_len", seg_len)
@@ -149,13 +149,16 @@ def test_mode_update_f64_variants(pt, orc, name, scale):
     mode_update_parity(pt, orc, t, cfg, 1e-10)
 
 
-def test_policy_f32a_reported(pt, orc):
-    """F32-A (all-fp32 contraction) is measured, not assumed: its worst row error is printed."""
-    cfg = synth.small("c2", 0.01)
-    coords, vals = init_cfg(pt, cfg, policy=0)
+@pytest.mark.parametrize("name,scale,policy", [("c2", 0.01, 0), ("c3", 0.002, 0), ("c3", 0.002, 1),
+                                               ("c4", 0.001, 0), ("c4", 0.001, 2)])
+def test_policies_reported(pt, orc, name, scale, policy):
+    """The non-default precision policies are measured, not assumed: their worst row
+    error is printed (the automatic policy is the one held to 1e-5 above)."""
+    cfg = synth.small(name, scale)
+    coords, vals = init_cfg(pt, cfg, policy=policy)
     t = orc.Tensor(coords, vals, cfg.dims)
     w = mode_update_parity(pt, orc, t, cfg, 1e-4)
-    print(f"F32-A worst row rel err {w:.2e}")
+    print(f"{name} policy {pt.ptucker_info()['policy']}: worst row rel err {w:.2e}")
 
 
 # ---------------------------------------------------------------- error (Eq. 5) and trajectory
@@ -223,8 +226,9 @@ def test_edge_empty_rows_and_tiny(pt, orc):
     t = orc.Tensor(coords, vals, [5, 2, 2])
     tiny = synth.Config("tiny", (5, 2, 2), 3, 2, 0.01, 1, "f64", "uniform", "uniform", False)
     mode_update_parity(pt, orc, t, tiny, 1e-10)
+    pt.ptucker_update_mode(0)
     a0 = pt.ptucker_get_factor(0)
-    assert np.all(a0[[1, 2, 4]] == 0)
+    assert np.all(a0[[1, 2, 4]] == 0) and np.all(a0[[0, 3]] != 0)
     # single entry, N = 2 (matrix case)
     pt.ptucker_init(np.array([[1, 2]], np.int32), np.array([0.5]), [3, 4], [3, 3], 0.1, 1)
     t = orc.Tensor([[1, 2]], [0.5], [3, 4])
