@@ -127,7 +127,9 @@ int ptucker_get_mode_index(int32_t n, int64_t* row_ptr, int64_t* perm);
 int ptucker_get_partition(int32_t n, int64_t* bounds);
 
 /* Options (set after init unless noted):
- *  "policy"       0 = F32-A (contraction all fp32), 1 = F32-B (last contraction stage fp64; default)
+ *  "policy"       precision of the fp32 contraction: -1 = automatic
+ *                 (default: every outer TTV stage in fp64), 0 = F32-A (all fp32), 1 = F32-B
+ *                 (outermost stage fp64), 2 = F32-C (all outer stages fp64)
  *  "seg_len"      max entries per row segment (>= 1, default 256; set BEFORE init)
  *  "tc"           1 = order-3 fp32 updates run the innermost contraction on the tcgen05 tensor
  *                 cores (3xTF32, default); 0 = the all-ALU kernel

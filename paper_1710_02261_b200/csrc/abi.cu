@@ -234,12 +234,14 @@ int rebuild_gp() {
     return PTUCKER_OK;
 }
 
-// outer TTV levels in fp64 for the current policy (auto: F32-B for N = 3 and 5,
-// F32-C (all outer levels) for N = 4 -- chosen by measured row error)
+// outer TTV levels in fp64 for the current policy.  auto = every outer level
+// (F32-B for N = 3, F32-C for N >= 4): the one-level F32-B and the all-fp32
+// F32-A both exceed the 1e-5 row bound on measured configs.
 int policy_l64() {
     if (g.prec == PTUCKER_F64) return 1;
-    if (g.policy >= 0) return g.policy == 2 ? (g.N >= 4 ? g.N - 2 : 1) : g.policy;
-    return g.N == 4 ? 2 : 1;
+    const int all = g.N >= 4 ? g.N - 2 : 1;
+    if (g.policy >= 0) return g.policy == 2 ? all : g.policy;
+    return all;
 }
 
 int choose_kernel() {
