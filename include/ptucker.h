@@ -133,6 +133,8 @@ int ptucker_get_partition(int32_t n, int64_t* bounds);
  *  "seg_len"      max entries per row segment (>= 1, default 256; set BEFORE init)
  *  "tc"           1 = order-3 fp32 updates run the innermost contraction on the tcgen05 tensor
  *                 cores (3xTF32, default); 0 = the all-ALU kernel
+ *  "smp"          1 = small-mode precontraction where it applies (order 4, two other modes with
+ *                 <= 64 rows whose table fits on chip; default), 0 = off
  *  "time_kernels" 1 = bracket every kernel launch with CUDA events (ptucker_kernel_stats) */
 int ptucker_set_option(const char* key, int64_t value);
 

@@ -101,6 +101,15 @@ struct Ctx {
     const UpdateKernel* kern = nullptr;      // row update (tensor-core variant when available)
     const UpdateKernel* kern_alu = nullptr;  // ALU kernel (literal error pass, and updates when tc = 0)
     int use_tc = 1;                          // option "tc"
+    int use_smp = 1;                         // option "smp"
+    struct Smp {
+        int kind = 0;                        // 2: order-4 mode with two small other modes (smp.cu)
+        int r = 0, s1 = 0, s2 = 0;           // global mode ids
+        int ir = 0, is1 = 0, is2 = 0;        // ordinals among the other modes (SELL/param order)
+        int64_t elems = 0;                   // table elements
+    } smp[kMaxN];
+    void* smp_T = nullptr;                   // device table (largest over modes)
+    int nsm = 148;
     int grid_upd = 0, grid_lit = 0;
     int64_t launches = 0;        // kernels this library launched since init (gpu_launches evidence)
     // timing
@@ -214,6 +223,24 @@ int launch_update_kernel(int n, bool literal) {
     const int grid = literal ? g.grid_lit : g.grid_upd;
     if (g.mi[n].nslices == 0) return PTUCKER_OK;
     CK(cudaMemsetAsync(g.d_work, 0, sizeof(unsigned int), S()));
+    const Ctx::Smp& sp = g.smp[n];
+    if (!literal && g.use_smp && sp.kind == 2) {
+        // small-mode precontraction: T from the (unchanged) small-mode factors, then J^2 per entry
+        launch_smp_table2(g.G, g.A[sp.s1], g.A[sp.s2], g.lda, g.dims[sp.s1], g.dims[sp.s2], g.J, n, sp.r, sp.s1, sp.s2,
+                          g.smp_T, g.esz, S());
+        bool ok;
+        if (g.prec == PTUCKER_F64) {
+            UpdateParams<double> p = make_params<double>(n, false);
+            ok = launch_smp2_update(&p, 8, g.J, g.smp_T, sp.elems, sp.ir, sp.is1, sp.is2, (int)g.dims[sp.s2], g.nsm, S());
+        } else {
+            UpdateParams<float> p = make_params<float>(n, false);
+            ok = launch_smp2_update(&p, 4, g.J, g.smp_T, sp.elems, sp.ir, sp.is1, sp.is2, (int)g.dims[sp.s2], g.nsm, S());
+        }
+        if (!ok) return fail(PTUCKER_EINVAL, "no SMP kernel for J=%d", g.J);
+        g.launches += 2;
+        CK(cudaGetLastError());
+        return PTUCKER_OK;
+    }
     g.launches += 1;
     const UpdateKernel* k = literal ? g.kern_alu : g.kern;
     if (g.prec == PTUCKER_F64) {
@@ -255,6 +282,7 @@ int choose_kernel() {
     }
     int nsm = 148;
     CK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, g.device));
+    g.nsm = nsm;
     const size_t smem = ((size_t)g.gp_elems * g.esz + 15) / 16 * 16;  // + staging ring (added per kernel)
     int occ = g.kern->occupancy(false, smem);
     int occl = g.kern_alu->occupancy(true, smem);
@@ -275,6 +303,7 @@ void free_all() {
         g.sse_row[n] = nullptr;
     }
     g.G = g.Gtmp = nullptr;
+    g.smp_T = nullptr;
     g.lit_part = g.red_part = g.red_out = g.qr = g.qd = nullptr;
     g.d_fail = g.d_qrfail = nullptr;
     g.d_work = nullptr;
@@ -367,6 +396,11 @@ int ptucker_set_option(const char* key, int64_t value) {
         if (value != 0 && value != 1) return fail(PTUCKER_EINVAL, "tc must be 0 or 1");
         g.use_tc = (int)value;
         if (g.inited) return choose_kernel();
+        return PTUCKER_OK;
+    }
+    if (k == "smp") {
+        if (value != 0 && value != 1) return fail(PTUCKER_EINVAL, "smp must be 0 or 1");
+        g.use_smp = (int)value;
         return PTUCKER_OK;
     }
     if (k == "time_kernels") {
@@ -466,6 +500,34 @@ int ptucker_init(const int32_t* coords, const void* vals, int32_t vals_dtype, in
                            m.bounds[g.rank + 1], m, g.arena, g.scratch, S()));
     }
     CK(A.alloc((void**)&g.lit_part, std::max<int64_t>(g.mi[0].nslices * 32, 1) * sizeof(double)));
+    // ---- small-mode precontraction plans ----
+    {
+        int64_t tmax = 0;
+        for (int n = 0; n < order; ++n) {
+            g.smp[n] = Ctx::Smp();
+            if (order != 4) continue;
+            int oth[3], c = 0;
+            for (int m = 0; m < order; ++m)
+                if (m != n) oth[c++] = m;
+            // the two smallest other modes, if small enough that the table fits on chip
+            int a = 0, b = 1, r = 2;
+            for (int x = 0; x < 3; ++x)
+                if (dims[oth[x]] > dims[oth[r]]) r = x;
+            a = r == 0 ? 1 : 0;
+            b = 3 - r - a;
+            if (a > b) std::swap(a, b);
+            const int64_t elems = dims[oth[a]] * dims[oth[b]] * (int64_t)J * J;
+            if (dims[oth[a]] <= 64 && dims[oth[b]] <= 64 && elems * esz <= 200 * 1024 && dims[oth[r]] > 64) {
+                Ctx::Smp& sp = g.smp[n];
+                sp.kind = 2;
+                sp.r = oth[r]; sp.s1 = oth[a]; sp.s2 = oth[b];
+                sp.ir = r; sp.is1 = a; sp.is2 = b;
+                sp.elems = elems;
+                tmax = std::max(tmax, elems);
+            }
+        }
+        if (tmax > 0) CK(A.alloc(&g.smp_T, (size_t)tmax * esz));
+    }
     CK(cudaStreamSynchronize(S()));
     input.release_all();
     g.inited = true;
@@ -704,9 +766,9 @@ int ptucker_info(char* buf, int32_t len) {
         const ModeIndex& m = g.mi[n];
         snprintf(tmp, sizeof(tmp),
                  "%s{\"I\": %lld, \"rows\": [%lld, %lld], \"segments\": %lld, \"slices\": %lld, \"slots\": %lld, "
-                 "\"heavy_rows\": %lld}",
+                 "\"heavy_rows\": %lld, \"smp\": %d}",
                  n ? ", " : "", (long long)m.I, (long long)m.r0, (long long)m.r1, (long long)m.nsegments,
-                 (long long)m.nslices, (long long)m.nslots, (long long)m.nheavy);
+                 (long long)m.nslices, (long long)m.nslots, (long long)m.nheavy, g.use_smp ? g.smp[n].kind : 0);
         s += tmp;
     }
     s += "]}";

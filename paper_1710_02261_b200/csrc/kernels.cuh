@@ -26,6 +26,11 @@ void launch_apply_rinv(const void* A, int a_bytes, int lda_a, void* Q, int q_byt
 void launch_mat_upper_mul(const double* R2, const double* R1, double* R, int J, cudaStream_t st);
 void launch_core_mode_product(const void* G, void* Gout, int elem_bytes, int N, int J, int n, const double* R,
                               cudaStream_t st);
+// ---- small-mode precontraction for order-4 tensors with two small modes (smp.cu) ----
+void launch_smp_table2(const void* G, const void* As1, const void* As2, int lda, int64_t I1, int64_t I2, int J, int n,
+                       int r, int s1, int s2, void* T, int elem_bytes, cudaStream_t st);
+bool launch_smp2_update(const void* params, int elem_bytes, int J, const void* T, int64_t tab_elems, int ir, int is1,
+                        int is2, int I2, int nsm, cudaStream_t st);
 // ---- index build helpers (index.cu) ----
 void launch_extract_col(const int32_t* coords, int64_t nnz, int N, int n, int32_t* keys, int32_t* iota,
                         cudaStream_t st);

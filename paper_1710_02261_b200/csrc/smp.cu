@@ -1,0 +1,225 @@
+// smp.cu -- small-mode precontraction (SMP) for order-4 tensors with two small modes
+// (the MovieLens-shaped c3: 138,000 x 27,000 x 21 x 24).
+//
+// Eq. 12 for mode n with other modes {r, s1, s2}, where s1 < s2 have
+// few rows:
+//   delta(j) = sum_{k_r} a_r[k_r] * T[i_s1][i_s2][k_r][j],
+//   T[i1][i2][k_r][j] = sum_{k1,k2} G[..j..k_r..k1..k2..] a_s1[i1][k1] a_s2[i2][k2].
+// T depends only on the small modes' factors, which do not change while mode n
+// (a large mode) is updated, so it is built once per mode update (I_s1*I_s2*J^2
+// values, 504 x 100 for c3) and every entry then costs J^2 FMAs instead of
+// J^4 + J^3 + J^2 (the per-entry minimum WITHOUT sharing).  This
+// is the same sum regrouped; T is accumulated in fp64 and stored in the
+// context precision, the per-entry stage runs in fp64.
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <cstdio>
+#include <cstdlib>
+
+#include "internal.cuh"
+#include "update.cuh"
+
+namespace pt {
+namespace smp {
+
+// ---- table build: one thread per output T[i1][i2][k_r][j], fp64 accumulation ----
+template <typename TS>
+__global__ void k_table2(const TS* __restrict__ G, const TS* __restrict__ As1, const TS* __restrict__ As2, int lda,
+                         int64_t I1, int64_t I2, int J, int n, int r, int s1, int s2, TS* __restrict__ T) {
+    const int64_t total = I1 * I2 * J * J;
+    int strideG[4];
+    {
+        int st = 1;
+        for (int m = 3; m >= 0; --m) { strideG[m] = st; st *= J; }
+    }
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
+        const int j = (int)(t % J);
+        const int kr = (int)((t / J) % J);
+        const int64_t blk = t / (J * J);
+        const int64_t i2 = blk % I2, i1 = blk / I2;
+        const TS* a1 = As1 + i1 * lda;
+        const TS* a2 = As2 + i2 * lda;
+        const int64_t base = (int64_t)j * strideG[n] + (int64_t)kr * strideG[r];
+        double acc = 0.0;
+        for (int k1 = 0; k1 < J; ++k1) {
+            double inner = 0.0;
+            for (int k2 = 0; k2 < J; ++k2)
+                inner = fma(double(G[base + (int64_t)k1 * strideG[s1] + (int64_t)k2 * strideG[s2]]), double(a2[k2]), inner);
+            acc = fma(double(a1[k1]), inner, acc);
+        }
+        T[t] = TS(acc);
+    }
+}
+
+// ---- row update: lane per row segment (SELL-32, as k_update), per entry
+//      delta = a_r^T T[i_s1][i_s2] in fp64; B, c, solve as in k_update ----
+template <typename TS, int J>
+__global__ void __launch_bounds__(kUpdThreads, 1) k_update_smp2(const UpdateParams<TS> p, const TS* __restrict__ T,
+                                                               int64_t tab_elems, int ir, int is1, int is2, int I2) {
+    constexpr int NB = J * (J + 1) / 2;
+    using V = typename Vec16<TS>::type;
+    constexpr int VN = Vec16<TS>::n;
+    constexpr int BLK = J * J;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    TS* ts = reinterpret_cast<TS*>(smem_raw);
+    {
+        const V* src = reinterpret_cast<const V*>(T);
+        V* dst = reinterpret_cast<V*>(ts);
+        for (int64_t i = threadIdx.x; i < tab_elems / VN; i += blockDim.x) dst[i] = src[i];
+    }
+    __syncthreads();
+    const int lane = threadIdx.x & (kWarp - 1);
+    for (;;) {
+        int s = 0;
+        if (lane == 0) s = (int)atomicAdd(p.work, 1u);
+        s = __shfl_sync(0xffffffffu, s, 0);
+        if (s >= p.nslices) break;
+        const int64_t slot = (int64_t)s * kWarp + lane;
+        const int row = p.lane_row[slot];
+        const int len = p.lane_len[slot];
+        const int iters = p.slice_len[s];
+        const int64_t base = p.slice_off[s] + lane;
+        double B[NB], c[J], s2 = 0.0;
+#pragma unroll
+        for (int q = 0; q < NB; ++q) B[q] = 0.0;
+#pragma unroll
+        for (int q = 0; q < J; ++q) c[q] = 0.0;
+        // one entry ahead: coordinates, value and the gathered row a_r
+        int cr = 0, c1 = 0, c2 = 0;
+        TS x = TS(0);
+        TS ar[J];
+        auto load = [&](int e, int& r_, int& a_, int& b_, TS& x_) {
+            const int64_t idx = base + (int64_t)e * kWarp;
+            r_ = __ldg(p.sc[ir] + idx);
+            a_ = __ldg(p.sc[is1] + idx);
+            b_ = __ldg(p.sc[is2] + idx);
+            x_ = __ldg(p.sv + idx);
+        };
+        if (iters > 0) {
+            load(0, cr, c1, c2, x);
+            load_row<TS, J>(p.A[ir] + (int64_t)cr * p.lda, ar);
+        }
+        for (int e = 0; e < iters; ++e) {
+            int nr = 0, n1 = 0, n2 = 0;
+            TS nx = TS(0);
+            TS nar[J];
+            if (e + 1 < iters) {
+                load(e + 1, nr, n1, n2, nx);
+                load_row<TS, J>(p.A[ir] + (int64_t)nr * p.lda, nar);
+            }
+            const TS* tb = ts + ((int64_t)c1 * I2 + c2) * BLK;
+            double d[J];
+#pragma unroll
+            for (int j = 0; j < J; ++j) d[j] = 0.0;
+#pragma unroll
+            for (int k = 0; k < J; ++k) {
+                const double ak = double(ar[k]);
+#pragma unroll
+                for (int j = 0; j < J; ++j) d[j] = fma(ak, double(tb[k * J + j]), d[j]);
+            }
+            const bool act = e < len;
+            const double xd = act ? double(x) : 0.0;
+#pragma unroll
+            for (int j = 0; j < J; ++j) d[j] = act ? d[j] : 0.0;
+#pragma unroll
+            for (int i = 0; i < J; ++i) {
+                c[i] = fma(xd, d[i], c[i]);
+#pragma unroll
+                for (int j = i; j < J; ++j) B[up_idx(i, j, J)] = fma(d[i], d[j], B[up_idx(i, j, J)]);
+            }
+            s2 = fma(xd, xd, s2);
+            cr = nr; c1 = n1; c2 = n2; x = nx;
+#pragma unroll
+            for (int j = 0; j < J; ++j) ar[j] = nar[j];
+        }
+        if (row < 0) continue;
+        const int64_t pidx = p.lane_pidx[slot];
+        if (pidx < 0) {
+            double a[J];
+            const bool ok = chol_solve<J>(B, c, p.lambda, a);
+            if (!ok) {
+                atomicCAS(p.fail, 0, row + 1);
+#pragma unroll
+                for (int j = 0; j < J; ++j) a[j] = 0.0;
+            }
+            TS* out = p.An + (int64_t)row * p.lda;
+            double sse = s2, ac = 0.0, aa = 0.0, ec = 0.0;
+#pragma unroll
+            for (int j = 0; j < J; ++j) {
+                const TS st = TS(a[j]);
+                out[j] = st;
+                const double at = double(st);
+                sse = fma(-2.0 * at, c[j], sse);
+                ac = fma(a[j], c[j], ac);
+                aa = fma(a[j], a[j], aa);
+                ec = fma(at - a[j], c[j] - p.lambda * a[j], ec);
+            }
+            p.sse_row[row] = sse + ac - p.lambda * aa + 2.0 * ec;
+        } else {
+            const int stp = p.lane_pstride[slot];
+            double* dst = p.partials + pidx;
+#pragma unroll
+            for (int q = 0; q < NB; ++q) dst[(int64_t)q * stp] = B[q];
+#pragma unroll
+            for (int q = 0; q < J; ++q) dst[(int64_t)(NB + q) * stp] = c[q];
+            dst[(int64_t)(NB + J) * stp] = s2;
+        }
+    }
+}
+
+template <typename TS, int J>
+int launch_smp2(const UpdateParams<TS>& p, const TS* T, int64_t tab_elems, int ir, int is1, int is2, int I2,
+                int nsm, cudaStream_t st) {
+    auto k = k_update_smp2<TS, J>;
+    const size_t smem = (size_t)tab_elems * sizeof(TS);
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    int nb = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k, kUpdThreads, smem);
+    if (nb < 1) nb = 1;
+    k<<<nsm * nb, kUpdThreads, smem, st>>>(p, T, tab_elems, ir, is1, is2, I2);
+    return 0;
+}
+
+}  // namespace smp
+
+// Host entry points (declared in kernels.cuh).
+void launch_smp_table2(const void* G, const void* As1, const void* As2, int lda, int64_t I1, int64_t I2, int J, int n,
+                       int r, int s1, int s2, void* T, int elem_bytes, cudaStream_t st) {
+    const int64_t total = I1 * I2 * J * J;
+    int grid = (int)((total + 255) / 256);
+    if (elem_bytes == 8)
+        smp::k_table2<double><<<grid, 256, 0, st>>>((const double*)G, (const double*)As1, (const double*)As2, lda, I1, I2,
+                                                    J, n, r, s1, s2, (double*)T);
+    else
+        smp::k_table2<float><<<grid, 256, 0, st>>>((const float*)G, (const float*)As1, (const float*)As2, lda, I1, I2, J,
+                                                   n, r, s1, s2, (float*)T);
+}
+
+bool launch_smp2_update(const void* params, int elem_bytes, int J, const void* T, int64_t tab_elems, int ir, int is1,
+                        int is2, int I2, int nsm, cudaStream_t st) {
+    if (elem_bytes == 4) {
+        const auto& p = *reinterpret_cast<const UpdateParams<float>*>(params);
+        switch (J) {
+            case 2: smp::launch_smp2<float, 2>(p, (const float*)T, tab_elems, ir, is1, is2, I2, nsm, st); return true;
+            case 3: smp::launch_smp2<float, 3>(p, (const float*)T, tab_elems, ir, is1, is2, I2, nsm, st); return true;
+            case 4: smp::launch_smp2<float, 4>(p, (const float*)T, tab_elems, ir, is1, is2, I2, nsm, st); return true;
+            case 5: smp::launch_smp2<float, 5>(p, (const float*)T, tab_elems, ir, is1, is2, I2, nsm, st); return true;
+            case 8: smp::launch_smp2<float, 8>(p, (const float*)T, tab_elems, ir, is1, is2, I2, nsm, st); return true;
+            case 10: smp::launch_smp2<float, 10>(p, (const float*)T, tab_elems, ir, is1, is2, I2, nsm, st); return true;
+        }
+    } else {
+        const auto& p = *reinterpret_cast<const UpdateParams<double>*>(params);
+        switch (J) {
+            case 2: smp::launch_smp2<double, 2>(p, (const double*)T, tab_elems, ir, is1, is2, I2, nsm, st); return true;
+            case 3: smp::launch_smp2<double, 3>(p, (const double*)T, tab_elems, ir, is1, is2, I2, nsm, st); return true;
+            case 4: smp::launch_smp2<double, 4>(p, (const double*)T, tab_elems, ir, is1, is2, I2, nsm, st); return true;
+            case 5: smp::launch_smp2<double, 5>(p, (const double*)T, tab_elems, ir, is1, is2, I2, nsm, st); return true;
+            case 8: smp::launch_smp2<double, 8>(p, (const double*)T, tab_elems, ir, is1, is2, I2, nsm, st); return true;
+            case 10: smp::launch_smp2<double, 10>(p, (const double*)T, tab_elems, ir, is1, is2, I2, nsm, st); return true;
+        }
+    }
+    return false;
+}
+
+}  // namespace pt
