@@ -10,6 +10,7 @@
 #include <cstring>
 #include <map>
 #include <string>
+#include <type_traits>
 #include <vector>
 
 #include "../../include/ptucker.h"
@@ -197,6 +198,7 @@ UpdateParams<TS> make_params(int n, bool literal) {
     p.lane_len = m.lane_len;
     p.lane_pidx = m.lane_pidx;
     p.lane_pstride = m.lane_pstride;
+    p.lane_aux = m.lane_aux;
     int l = 0;
     for (int k = 0; k < g.N; ++k) {
         if (k == n) continue;
@@ -237,6 +239,35 @@ int launch_update_kernel(int n, bool literal) {
             ok = launch_smp2_update(&p, 4, g.J, g.smp_T, sp.elems, sp.ir, sp.is1, sp.is2, (int)g.dims[sp.s2], g.nsm, S());
         }
         if (!ok) return fail(PTUCKER_EINVAL, "no SMP kernel for J=%d", g.J);
+        g.launches += 2;
+        CK(cudaGetLastError());
+        return PTUCKER_OK;
+    }
+    if (!literal && g.use_smp && sp.kind == 1) {
+        // one small mode: table of order-3 cores T[i_s], then an order-3 TTV per entry
+        launch_smp_table1(g.G, g.A[sp.s1], g.lda, g.dims[sp.s1], g.J, n, sp.r, sp.s2, sp.s1, g.smp_T, g.esz, S());
+        const int GBk = gblk(g.J, g.esz);
+        bool ok;
+        auto fill = [&](auto& p) {
+            using TSp = typename std::remove_const<typename std::remove_pointer<decltype(p.sv)>::type>::type;
+            p.sc[0] = g.mi[n].sc[sp.ir];
+            p.sc[1] = g.mi[n].sc[sp.is2];
+            p.A[0] = (const TSp*)g.A[sp.r];
+            p.A[1] = (const TSp*)g.A[sp.s2];
+            p.Gp = (const TSp*)g.smp_T;
+            p.gp_elems = (int)sp.elems;
+            p.aux_stride = (int64_t)g.J * GBk;
+        };
+        if (g.prec == PTUCKER_F64) {
+            UpdateParams<double> p = make_params<double>(n, false);
+            fill(p);
+            ok = launch_table_update(&p, 8, g.J, g.nsm, S());
+        } else {
+            UpdateParams<float> p = make_params<float>(n, false);
+            fill(p);
+            ok = launch_table_update(&p, 4, g.J, g.nsm, S());
+        }
+        if (!ok) return fail(PTUCKER_EINVAL, "no table kernel for J=%d", g.J);
         g.launches += 2;
         CK(cudaGetLastError());
         return PTUCKER_OK;
@@ -483,6 +514,50 @@ int ptucker_init(const int32_t* coords, const void* vals, int32_t vals_dtype, in
     }
     int rc = rebuild_gp();
     if (rc) return rc;
+    // ---- small-mode precontraction plans, order 4 only ----
+    {
+        int64_t tmax = 0;
+        const int GBk = gblk(J, esz);
+        for (int n = 0; n < order; ++n) {
+            g.smp[n] = Ctx::Smp();
+            if (order != 4) continue;
+            int oth[3], c = 0;
+            for (int m = 0; m < order; ++m)
+                if (m != n) oth[c++] = m;
+            int nsmall = 0;
+            for (int x = 0; x < 3; ++x) nsmall += dims[oth[x]] <= 64;
+            Ctx::Smp& sp = g.smp[n];
+            if (nsmall == 2) {
+                // kind 2: two small other modes -> J^2 fp64 per entry against T[i_s1][i_s2]
+                int r = 0;
+                for (int x = 0; x < 3; ++x)
+                    if (dims[oth[x]] > 64) r = x;
+                const int a = r == 0 ? 1 : 0, b = 3 - r - a;
+                const int64_t elems = dims[oth[a]] * dims[oth[b]] * (int64_t)J * J;
+                if (elems * esz <= 200 * 1024) {
+                    sp.kind = 2;
+                    sp.r = oth[r]; sp.s1 = oth[a]; sp.s2 = oth[b];
+                    sp.ir = r; sp.is1 = a; sp.is2 = b;
+                    sp.elems = elems;
+                }
+            } else if (nsmall == 1) {
+                // kind 1: one small other mode -> order-3 TTV against the block T[i_s] of the segment
+                int sx = 0;
+                for (int x = 0; x < 3; ++x)
+                    if (dims[oth[x]] <= 64) sx = x;
+                const int a = sx == 0 ? 1 : 0, b = sx == 2 ? 1 : 2;
+                const int64_t elems = dims[oth[sx]] * (int64_t)J * GBk;
+                if (elems * esz <= 128 * 1024) {
+                    sp.kind = 1;
+                    sp.s1 = oth[sx]; sp.r = oth[a]; sp.s2 = oth[b];   // r, s2 = the two large modes (a < b)
+                    sp.is1 = sx; sp.ir = a; sp.is2 = b;
+                    sp.elems = elems;
+                }
+            }
+            if (sp.kind) tmax = std::max(tmax, sp.elems);
+        }
+        if (tmax > 0) CK(A.alloc(&g.smp_T, (size_t)tmax * esz));
+    }
     // ---- device index of every mode ----
     DeviceArena input;
     int32_t* d_coords = nullptr;
@@ -496,38 +571,13 @@ int ptucker_init(const int32_t* coords, const void* vals, int32_t vals_dtype, in
         CK(build_mode_csr(d_coords, nnz, order, n, dims[n], m, g.arena, g.scratch, S()));
         m.bounds.assign((size_t)g.world + 1, 0);
         partition_rows(m.h_row_ptr.data(), dims[n], g.world, m.bounds.data());
+        const int smode = g.smp[n].kind == 1 ? g.smp[n].s1 : -1;  // group each row by the small mode
+        m.Is = smode >= 0 ? dims[smode] : 1;
         CK(build_mode_sell(d_coords, d_vals, esz, nnz, order, n, J, g.seg_len, m.bounds[g.rank],
-                           m.bounds[g.rank + 1], m, g.arena, g.scratch, S()));
+                           m.bounds[g.rank + 1], smode, m, g.arena, g.scratch, S()));
     }
     CK(A.alloc((void**)&g.lit_part, std::max<int64_t>(g.mi[0].nslices * 32, 1) * sizeof(double)));
-    // ---- small-mode precontraction plans ----
-    {
-        int64_t tmax = 0;
-        for (int n = 0; n < order; ++n) {
-            g.smp[n] = Ctx::Smp();
-            if (order != 4) continue;
-            int oth[3], c = 0;
-            for (int m = 0; m < order; ++m)
-                if (m != n) oth[c++] = m;
-            // the two smallest other modes, if small enough that the table fits on chip
-            int a = 0, b = 1, r = 2;
-            for (int x = 0; x < 3; ++x)
-                if (dims[oth[x]] > dims[oth[r]]) r = x;
-            a = r == 0 ? 1 : 0;
-            b = 3 - r - a;
-            if (a > b) std::swap(a, b);
-            const int64_t elems = dims[oth[a]] * dims[oth[b]] * (int64_t)J * J;
-            if (dims[oth[a]] <= 64 && dims[oth[b]] <= 64 && elems * esz <= 200 * 1024 && dims[oth[r]] > 64) {
-                Ctx::Smp& sp = g.smp[n];
-                sp.kind = 2;
-                sp.r = oth[r]; sp.s1 = oth[a]; sp.s2 = oth[b];
-                sp.ir = r; sp.is1 = a; sp.is2 = b;
-                sp.elems = elems;
-                tmax = std::max(tmax, elems);
-            }
-        }
-        if (tmax > 0) CK(A.alloc(&g.smp_T, (size_t)tmax * esz));
-    }
+
     CK(cudaStreamSynchronize(S()));
     input.release_all();
     g.inited = true;

@@ -59,49 +59,76 @@ void launch_row_ptr(const int32_t* sorted_keys, int64_t nnz, int64_t I, int64_t*
     k_row_ptr<<<grid, 256, 0, st>>>(sorted_keys, nnz, I, row_ptr);
 }
 
-// Per row of the block: number of segments, heavy flag, heavy segment count.
-__global__ void k_seg_count(const int64_t* row_ptr, int64_t r0, int64_t nrows, int S, int64_t* nseg, int64_t* hflag,
+// Segments are cut inside "groups": a group is a row (Is = 1) or, for a mode
+// updated with a small-mode table, a (row, i_s) pair, so that
+// every segment has one i_s and a warp's lanes mostly share one table block.
+// Per group of the block: number of segments (an empty ROW keeps one empty
+// segment in its first group, which solves to a = 0).
+__global__ void k_group_count(const int64_t* group_ptr, int64_t g0, int64_t ngroups, int64_t Is, int S,
+                              int64_t* nseg_g) {
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < ngroups; t += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t G = g0 + t;
+        const int64_t len = group_ptr[G + 1] - group_ptr[G];
+        const int64_t row = G / Is;
+        const bool first = (G % Is) == 0;
+        const int64_t row_len = group_ptr[(row + 1) * Is] - group_ptr[row * Is];
+        nseg_g[t] = len > 0 ? (len + S - 1) / S : ((first && row_len == 0) ? 1 : 0);
+    }
+}
+
+// Per row of the block: segments of the row (its groups are contiguous), heavy flag.
+__global__ void k_row_count(const int64_t* seg_start_g, int64_t nrows, int64_t Is, int64_t* nseg_r, int64_t* hflag,
                             int64_t* hseg) {
     for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < nrows; t += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t len = row_ptr[r0 + t + 1] - row_ptr[r0 + t];
-        const int64_t ns = len == 0 ? 1 : (len + S - 1) / S;
-        nseg[t] = ns;
+        const int64_t ns = seg_start_g[(t + 1) * Is] - seg_start_g[t * Is];
+        nseg_r[t] = ns;
         hflag[t] = ns > 1 ? 1 : 0;
         hseg[t] = ns > 1 ? ns : 0;
     }
 }
 
-__global__ void k_seg_fill(const int64_t* row_ptr, int64_t r0, int64_t nrows, int S, int PW, const int64_t* seg_start,
-                           const int64_t* hidx, const int64_t* hbase, int32_t* seg_row, int32_t* seg_sidx,
-                           int32_t* seg_len, uint32_t* seg_key, int64_t* seg_pidx, int32_t* seg_pstride,
-                           int32_t* hrow, int32_t* hnseg, int64_t* hpbase) {
+__global__ void k_heavy_list(int64_t r0, int64_t nrows, int PW, const int64_t* nseg_r, const int64_t* hidx,
+                             const int64_t* hbase, int32_t* hrow, int32_t* hnseg, int64_t* hpbase) {
     for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < nrows; t += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t row = r0 + t;
-        const int64_t len = row_ptr[row + 1] - row_ptr[row];
-        const int64_t ns = len == 0 ? 1 : (len + S - 1) / S;
-        const bool heavy = ns > 1;
-        if (heavy) {
-            hrow[hidx[t]] = (int32_t)row;
-            hnseg[hidx[t]] = (int32_t)ns;
+        if (nseg_r[t] > 1) {
+            hrow[hidx[t]] = (int32_t)(r0 + t);
+            hnseg[hidx[t]] = (int32_t)nseg_r[t];
             hpbase[hidx[t]] = hbase[t] * PW;
         }
+    }
+}
+
+__global__ void k_group_fill(const int64_t* group_ptr, int64_t g0, int64_t ngroups, int64_t Is, int S, int PW,
+                             const int64_t* seg_start_g, const int64_t* nseg_r, const int64_t* hbase, int32_t* seg_row,
+                             int64_t* seg_src, int32_t* seg_aux, int32_t* seg_len, uint32_t* seg_key,
+                             int64_t* seg_pidx, int32_t* seg_pstride) {
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < ngroups; t += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t G = g0 + t;
+        const int64_t len = group_ptr[G + 1] - group_ptr[G];
+        const int64_t rl = t / Is;                       // row index within the block
+        const int64_t ns = seg_start_g[t + 1] - seg_start_g[t];
+        const int64_t nsr = nseg_r[rl];
+        const bool heavy = nsr > 1;
         for (int64_t s = 0; s < ns; ++s) {
-            const int64_t sid = seg_start[t] + s;
+            const int64_t sid = seg_start_g[t] + s;
+            const int64_t in_row = sid - seg_start_g[rl * Is];
             const int64_t l = len - s * S < S ? len - s * S : S;
-            seg_row[sid] = (int32_t)row;
-            seg_sidx[sid] = (int32_t)s;
-            seg_len[sid] = (int32_t)l;
-            seg_key[sid] = (uint32_t)(S - l);  // ascending key = descending length
-            seg_pidx[sid] = heavy ? hbase[t] * PW + s : -1;
-            seg_pstride[sid] = heavy ? (int32_t)ns : 0;
+            seg_row[sid] = (int32_t)(G / Is);
+            seg_src[sid] = group_ptr[G] + s * S;
+            seg_aux[sid] = (int32_t)(G % Is);
+            seg_len[sid] = (int32_t)(l > 0 ? l : 0);
+            seg_key[sid] = (uint32_t)(S - (l > 0 ? l : 0));  // ascending key = descending length
+            seg_pidx[sid] = heavy ? hbase[rl] * PW + in_row : -1;
+            seg_pstride[sid] = heavy ? (int32_t)nsr : 0;
         }
     }
 }
 
 __global__ void k_slices(const int32_t* order, int64_t nseg, int64_t nslices, const int32_t* seg_row,
-                         const int32_t* seg_sidx, const int32_t* seg_len, const int64_t* seg_pidx,
-                         const int32_t* seg_pstride, int32_t* slice_len, int64_t* slice_slots, int32_t* lane_row,
-                         int32_t* lane_len, int64_t* lane_pidx, int32_t* lane_pstride, int32_t* lane_sidx) {
+                         const int64_t* seg_src, const int32_t* seg_aux, const int32_t* seg_len,
+                         const int64_t* seg_pidx, const int32_t* seg_pstride, int32_t* slice_len,
+                         int64_t* slice_slots, int32_t* lane_row, int32_t* lane_len, int64_t* lane_pidx,
+                         int32_t* lane_pstride, int64_t* lane_src, int32_t* lane_aux) {
     const int64_t total = nslices * 32;
     for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
         if (t < nseg) {
@@ -110,13 +137,15 @@ __global__ void k_slices(const int32_t* order, int64_t nseg, int64_t nslices, co
             lane_len[t] = seg_len[sid];
             lane_pidx[t] = seg_pidx[sid];
             lane_pstride[t] = seg_pstride[sid];
-            lane_sidx[t] = seg_sidx[sid];
+            lane_src[t] = seg_src[sid];
+            lane_aux[t] = seg_aux[sid];
         } else {
             lane_row[t] = -1;
             lane_len[t] = 0;
             lane_pidx[t] = -1;
             lane_pstride[t] = 0;
-            lane_sidx[t] = 0;
+            lane_src[t] = 0;
+            lane_aux[t] = 0;
         }
         if ((t & 31) == 0) {
             const int32_t l = (t < nseg) ? seg_len[order[t]] : 0;
@@ -128,15 +157,14 @@ __global__ void k_slices(const int32_t* order, int64_t nseg, int64_t nslices, co
 
 template <typename TS>
 __global__ void k_sell_fill(int64_t nslices, const int64_t* slice_off, const int32_t* lane_row,
-                            const int32_t* lane_len, const int32_t* lane_sidx, const int64_t* row_ptr,
-                            const int32_t* perm, int S, const int32_t* coords, const TS* vals, int N, int n,
-                            int32_t* const* sc, TS* sv) {
+                            const int32_t* lane_len, const int64_t* lane_src, const int32_t* perm,
+                            const int32_t* coords, const TS* vals, int N, int n, int32_t* const* sc, TS* sv) {
     const int64_t total = nslices * 32;
     for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
         const int32_t row = lane_row[t];
         if (row < 0) continue;
         const int32_t len = lane_len[t];
-        const int64_t src0 = row_ptr[row] + (int64_t)lane_sidx[t] * S;
+        const int64_t src0 = lane_src[t];
         const int64_t dst0 = slice_off[t >> 5] + (t & 31);
         for (int32_t e = 0; e < len; ++e) {
             const int64_t src = perm[src0 + e];
@@ -149,6 +177,22 @@ __global__ void k_sell_fill(int64_t nslices, const int64_t* slice_off, const int
             }
             sv[dst] = vals[src];
         }
+    }
+}
+
+__global__ void k_composite_key(const int32_t* coords, int64_t nnz, int N, int n, int s, int64_t Is, uint32_t* keys,
+                                int32_t* iota) {
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < nnz; e += (int64_t)gridDim.x * blockDim.x) {
+        keys[e] = (uint32_t)((int64_t)coords[e * N + n] * Is + coords[e * N + s]);
+        iota[e] = (int32_t)e;
+    }
+}
+
+__global__ void k_group_ptr(const uint32_t* sk, int64_t nnz, int64_t G, int64_t* gp) {
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e <= nnz; e += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t prev = (e == 0) ? -1 : (int64_t)sk[e - 1];
+        const int64_t cur = (e == nnz) ? G : (int64_t)sk[e];
+        for (int64_t r = prev + 1; r <= cur; ++r) gp[r] = e;
     }
 }
 
@@ -207,32 +251,59 @@ static cudaError_t exclusive_sum(const T* in, T* out, int64_t n, DeviceArena& sc
 }
 
 cudaError_t build_mode_sell(const int32_t* d_coords, const void* d_vals, int elem_bytes, int64_t nnz, int N, int n,
-                            int J, int S, int64_t r0, int64_t r1, ModeIndex& mi, DeviceArena& arena,
+                            int J, int S, int64_t r0, int64_t r1, int smode, ModeIndex& mi, DeviceArena& arena,
                             DeviceArena& scratch, cudaStream_t st) {
-    (void)nnz;
     const int PW = rec_width(J);
     const int64_t nrows = r1 - r0;
     mi.r0 = r0;
     mi.r1 = r1;
+    // ---- groups: rows, or (row, i_s) pairs for a small-mode table ----
+    const int64_t Is = smode >= 0 ? mi.Is : 1;
+    const int64_t* group_ptr = mi.row_ptr;
+    const int32_t* perm = mi.perm;
+    if (smode >= 0) {
+        uint32_t *k_in = nullptr, *k_out = nullptr;
+        int32_t *iota = nullptr, *perm2 = nullptr;
+        int64_t* gptr = nullptr;
+        IB_CHECK(dalloc(&k_in, nnz, scratch));
+        IB_CHECK(dalloc(&k_out, nnz, scratch));
+        IB_CHECK(dalloc(&iota, nnz, scratch));
+        IB_CHECK(dalloc(&perm2, nnz, scratch));
+        IB_CHECK(dalloc(&gptr, mi.I * Is + 1, scratch));
+        k_composite_key<<<grid_for(nnz), 256, 0, st>>>(d_coords, nnz, N, n, smode, Is, k_in, iota);
+        int bits = 1;
+        while ((int64_t(1) << bits) < mi.I * Is) ++bits;
+        size_t tb = 0;
+        IB_CHECK(cub::DeviceRadixSort::SortPairs(nullptr, tb, k_in, k_out, iota, perm2, (int)nnz, 0, bits, st));
+        void* tmp = nullptr;
+        IB_CHECK(scratch.alloc(&tmp, tb));
+        IB_CHECK(cub::DeviceRadixSort::SortPairs(tmp, tb, k_in, k_out, iota, perm2, (int)nnz, 0, bits, st));
+        k_group_ptr<<<grid_for(nnz + 1), 256, 0, st>>>(k_out, nnz, mi.I * Is, gptr);
+        group_ptr = gptr;
+        perm = perm2;
+    }
+    const int64_t g0 = r0 * Is, ngroups = nrows * Is;
     // ---- 3. segments ----
-    int64_t *nseg = nullptr, *hflag = nullptr, *hseg = nullptr, *seg_start = nullptr, *hidx = nullptr,
-            *hbase = nullptr;
-    const int64_t nr1 = nrows + 1;  // trailing zero gives the totals from the exclusive scans
-    IB_CHECK(dalloc(&nseg, nr1, scratch));
-    IB_CHECK(dalloc(&hflag, nr1, scratch));
-    IB_CHECK(dalloc(&hseg, nr1, scratch));
-    IB_CHECK(dalloc(&seg_start, nr1, scratch));
-    IB_CHECK(dalloc(&hidx, nr1, scratch));
-    IB_CHECK(dalloc(&hbase, nr1, scratch));
-    IB_CHECK(cudaMemsetAsync(nseg, 0, sizeof(int64_t) * nr1, st));
-    IB_CHECK(cudaMemsetAsync(hflag, 0, sizeof(int64_t) * nr1, st));
-    IB_CHECK(cudaMemsetAsync(hseg, 0, sizeof(int64_t) * nr1, st));
-    if (nrows > 0) k_seg_count<<<grid_for(nrows), 256, 0, st>>>(mi.row_ptr, r0, nrows, S, nseg, hflag, hseg);
-    IB_CHECK(exclusive_sum(nseg, seg_start, nr1, scratch, st));
-    IB_CHECK(exclusive_sum(hflag, hidx, nr1, scratch, st));
-    IB_CHECK(exclusive_sum(hseg, hbase, nr1, scratch, st));
+    int64_t *nseg_g = nullptr, *seg_start_g = nullptr, *nseg_r = nullptr, *hflag = nullptr, *hseg = nullptr,
+            *hidx = nullptr, *hbase = nullptr;
+    IB_CHECK(dalloc(&nseg_g, ngroups + 1, scratch));
+    IB_CHECK(dalloc(&seg_start_g, ngroups + 1, scratch));
+    IB_CHECK(dalloc(&nseg_r, nrows + 1, scratch));
+    IB_CHECK(dalloc(&hflag, nrows + 1, scratch));
+    IB_CHECK(dalloc(&hseg, nrows + 1, scratch));
+    IB_CHECK(dalloc(&hidx, nrows + 1, scratch));
+    IB_CHECK(dalloc(&hbase, nrows + 1, scratch));
+    IB_CHECK(cudaMemsetAsync(nseg_g, 0, sizeof(int64_t) * (ngroups + 1), st));
+    IB_CHECK(cudaMemsetAsync(nseg_r, 0, sizeof(int64_t) * (nrows + 1), st));
+    IB_CHECK(cudaMemsetAsync(hflag, 0, sizeof(int64_t) * (nrows + 1), st));
+    IB_CHECK(cudaMemsetAsync(hseg, 0, sizeof(int64_t) * (nrows + 1), st));
+    if (ngroups > 0) k_group_count<<<grid_for(ngroups), 256, 0, st>>>(group_ptr, g0, ngroups, Is, S, nseg_g);
+    IB_CHECK(exclusive_sum(nseg_g, seg_start_g, ngroups + 1, scratch, st));
+    if (nrows > 0) k_row_count<<<grid_for(nrows), 256, 0, st>>>(seg_start_g, nrows, Is, nseg_r, hflag, hseg);
+    IB_CHECK(exclusive_sum(hflag, hidx, nrows + 1, scratch, st));
+    IB_CHECK(exclusive_sum(hseg, hbase, nrows + 1, scratch, st));
     int64_t tot[3];
-    IB_CHECK(cudaMemcpyAsync(&tot[0], seg_start + nrows, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+    IB_CHECK(cudaMemcpyAsync(&tot[0], seg_start_g + ngroups, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
     IB_CHECK(cudaMemcpyAsync(&tot[1], hidx + nrows, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
     IB_CHECK(cudaMemcpyAsync(&tot[2], hbase + nrows, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
     IB_CHECK(cudaStreamSynchronize(st));
@@ -241,17 +312,18 @@ cudaError_t build_mode_sell(const int32_t* d_coords, const void* d_vals, int ele
     mi.npartial_doubles = tot[2] * PW;
     mi.nsegments = nS;
 
-    int32_t *seg_row, *seg_sidx, *seg_len, *seg_pstride;
+    int32_t *seg_row, *seg_aux, *seg_len, *seg_pstride;
+    int64_t *seg_src, *seg_pidx;
     uint32_t *seg_key, *seg_key_sorted;
-    int64_t* seg_pidx;
     int32_t *seg_iota, *order;
     IB_CHECK(dalloc(&seg_row, nS, scratch));
-    IB_CHECK(dalloc(&seg_sidx, nS, scratch));
+    IB_CHECK(dalloc(&seg_aux, nS, scratch));
     IB_CHECK(dalloc(&seg_len, nS, scratch));
     IB_CHECK(dalloc(&seg_pstride, nS, scratch));
+    IB_CHECK(dalloc(&seg_src, nS, scratch));
+    IB_CHECK(dalloc(&seg_pidx, nS, scratch));
     IB_CHECK(dalloc(&seg_key, nS, scratch));
     IB_CHECK(dalloc(&seg_key_sorted, nS, scratch));
-    IB_CHECK(dalloc(&seg_pidx, nS, scratch));
     IB_CHECK(dalloc(&seg_iota, nS, scratch));
     IB_CHECK(dalloc(&order, nS, scratch));
     IB_CHECK(dalloc(&mi.hrow, mi.nheavy, arena));
@@ -259,9 +331,11 @@ cudaError_t build_mode_sell(const int32_t* d_coords, const void* d_vals, int ele
     IB_CHECK(dalloc(&mi.hpbase, mi.nheavy, arena));
     IB_CHECK(dalloc(&mi.partials, mi.npartial_doubles, arena));
     if (nrows > 0)
-        k_seg_fill<<<grid_for(nrows), 256, 0, st>>>(mi.row_ptr, r0, nrows, S, PW, seg_start, hidx, hbase, seg_row,
-                                                    seg_sidx, seg_len, seg_key, seg_pidx, seg_pstride, mi.hrow,
-                                                    mi.hnseg, mi.hpbase);
+        k_heavy_list<<<grid_for(nrows), 256, 0, st>>>(r0, nrows, PW, nseg_r, hidx, hbase, mi.hrow, mi.hnseg, mi.hpbase);
+    if (ngroups > 0)
+        k_group_fill<<<grid_for(ngroups), 256, 0, st>>>(group_ptr, g0, ngroups, Is, S, PW, seg_start_g, nseg_r, hbase,
+                                                        seg_row, seg_src, seg_aux, seg_len, seg_key, seg_pidx,
+                                                        seg_pstride);
     // ---- 4. stable sort of segments by length (descending) ----
     {
         if (nS > 0) k_iota<<<grid_for(nS), 256, 0, st>>>(seg_iota, nS);
@@ -277,21 +351,21 @@ cudaError_t build_mode_sell(const int32_t* d_coords, const void* d_vals, int ele
     }
     mi.nslices = (nS + 31) / 32;
     const int64_t nlanes = mi.nslices * 32;
-    int64_t* slice_slots = nullptr;
-    int32_t* lane_sidx = nullptr;
+    int64_t *slice_slots = nullptr, *lane_src = nullptr;
     IB_CHECK(dalloc(&slice_slots, mi.nslices + 1, scratch));
-    IB_CHECK(dalloc(&lane_sidx, nlanes, scratch));
+    IB_CHECK(dalloc(&lane_src, nlanes, scratch));
     IB_CHECK(dalloc(&mi.slice_len, mi.nslices, arena));
     IB_CHECK(dalloc(&mi.slice_off, mi.nslices + 1, arena));
     IB_CHECK(dalloc(&mi.lane_row, nlanes, arena));
     IB_CHECK(dalloc(&mi.lane_len, nlanes, arena));
     IB_CHECK(dalloc(&mi.lane_pidx, nlanes, arena));
     IB_CHECK(dalloc(&mi.lane_pstride, nlanes, arena));
+    IB_CHECK(dalloc(&mi.lane_aux, nlanes, arena));
     IB_CHECK(cudaMemsetAsync(slice_slots, 0, sizeof(int64_t) * (mi.nslices + 1), st));
     if (nlanes > 0)
-        k_slices<<<grid_for(nlanes), 256, 0, st>>>(order, nS, mi.nslices, seg_row, seg_sidx, seg_len, seg_pidx,
+        k_slices<<<grid_for(nlanes), 256, 0, st>>>(order, nS, mi.nslices, seg_row, seg_src, seg_aux, seg_len, seg_pidx,
                                                    seg_pstride, mi.slice_len, slice_slots, mi.lane_row, mi.lane_len,
-                                                   mi.lane_pidx, mi.lane_pstride, lane_sidx);
+                                                   mi.lane_pidx, mi.lane_pstride, lane_src, mi.lane_aux);
     IB_CHECK(exclusive_sum(slice_slots, mi.slice_off, mi.nslices + 1, scratch, st));
     IB_CHECK(cudaMemcpyAsync(&mi.nslots, mi.slice_off + mi.nslices, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
     IB_CHECK(cudaStreamSynchronize(st));
@@ -308,12 +382,12 @@ cudaError_t build_mode_sell(const int32_t* d_coords, const void* d_vals, int ele
     if (nlanes > 0) {
         if (elem_bytes == 8)
             k_sell_fill<double><<<grid_for(nlanes), 256, 0, st>>>(mi.nslices, mi.slice_off, mi.lane_row, mi.lane_len,
-                                                                  lane_sidx, mi.row_ptr, mi.perm, S, d_coords,
-                                                                  (const double*)d_vals, N, n, d_sc, (double*)mi.sv);
+                                                                  lane_src, perm, d_coords, (const double*)d_vals, N, n,
+                                                                  d_sc, (double*)mi.sv);
         else
             k_sell_fill<float><<<grid_for(nlanes), 256, 0, st>>>(mi.nslices, mi.slice_off, mi.lane_row, mi.lane_len,
-                                                                 lane_sidx, mi.row_ptr, mi.perm, S, d_coords,
-                                                                 (const float*)d_vals, N, n, d_sc, (float*)mi.sv);
+                                                                 lane_src, perm, d_coords, (const float*)d_vals, N, n,
+                                                                 d_sc, (float*)mi.sv);
     }
     IB_CHECK(cudaGetLastError());
     IB_CHECK(cudaStreamSynchronize(st));

@@ -37,6 +37,8 @@ struct UpdateParams {
     const int32_t* lane_len;      // [nslices*32] entries of that segment
     const int64_t* lane_pidx;     // [nslices*32] heavy rows: first partial slot (-1: segment is the whole row)
     const int32_t* lane_pstride;  // [nslices*32] heavy rows: stride between partial components (= #segments of the row)
+    const int32_t* lane_aux;      // [nslices*32] small-mode table block of the segment (TABLE kernels only)
+    int64_t aux_stride;           // elements per table block
     const int32_t* sc[kMaxN - 1]; // SELL coordinates of the other modes (ascending mode order)
     const TS* sv;                 // SELL values
     const TS* A[kMaxN - 1];       // the other factors, same order, row stride lda

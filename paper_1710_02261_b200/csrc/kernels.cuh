@@ -31,6 +31,10 @@ void launch_smp_table2(const void* G, const void* As1, const void* As2, int lda,
                        int r, int s1, int s2, void* T, int elem_bytes, cudaStream_t st);
 bool launch_smp2_update(const void* params, int elem_bytes, int J, const void* T, int64_t tab_elems, int ir, int is1,
                         int is2, int I2, int nsm, cudaStream_t st);
+// order-4 mode with ONE small other mode s: table of order-3 cores, one per row of s
+void launch_smp_table1(const void* G, const void* As, int lda, int64_t Is, int J, int n, int a, int b, int s, void* T,
+                       int elem_bytes, cudaStream_t st);
+bool launch_table_update(const void* params, int elem_bytes, int J, int nsm, cudaStream_t st);
 // ---- index build helpers (index.cu) ----
 void launch_extract_col(const int32_t* coords, int64_t nnz, int N, int n, int32_t* keys, int32_t* iota,
                         cudaStream_t st);

@@ -168,6 +168,45 @@ __global__ void __launch_bounds__(kUpdThreads, 1) k_update_smp2(const UpdatePara
     }
 }
 
+// ---- one small other mode s: T[i][k_a][k_b][j] = sum_k G[..j..k_a..k_b..k..] a_s[i][k],
+//      laid out as a core permuted for an order-3 problem (blocks [k_a][gblk] with
+//      gblk = [k_b][j] padded), one block per small-mode row i ----
+template <typename TS>
+__global__ void k_table1(const TS* __restrict__ G, const TS* __restrict__ As, int lda, int64_t Is, int J, int n,
+                         int a, int b, int sm, int GB, TS* __restrict__ T) {
+    const int64_t total = Is * J * GB;
+    int strideG[4];
+    {
+        int st = 1;
+        for (int m = 3; m >= 0; --m) { strideG[m] = st; st *= J; }
+    }
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
+        const int w = (int)(t % GB);
+        const int ka = (int)((t / GB) % J);
+        const int64_t i = t / ((int64_t)GB * J);
+        if (w >= J * J) { T[t] = TS(0); continue; }
+        const int kb = w / J, j = w % J;
+        const TS* as = As + i * lda;
+        const int64_t base = (int64_t)j * strideG[n] + (int64_t)ka * strideG[a] + (int64_t)kb * strideG[b];
+        double acc = 0.0;
+        for (int k = 0; k < J; ++k) acc = fma(double(G[base + (int64_t)k * strideG[sm]]), double(as[k]), acc);
+        T[t] = TS(acc);
+    }
+}
+
+template <typename TS, int J>
+int launch_table_update(const UpdateParams<TS>& p, int nsm, cudaStream_t st) {
+    using TF = TS;
+    auto k = k_update<TS, TF, 3, J, 1, false, true>;
+    const size_t smem = gp_smem_bytes(p.gp_elems, sizeof(TS)) + (kUpdThreads / kWarp) * Stage<TS, 3, J>::BYTES_PER_WARP;
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    int nb = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k, kUpdThreads, smem);
+    if (nb < 1) nb = 1;
+    k<<<nsm * nb, kUpdThreads, smem, st>>>(p);
+    return 0;
+}
+
 template <typename TS, int J>
 int launch_smp2(const UpdateParams<TS>& p, const TS* T, int64_t tab_elems, int ir, int is1, int is2, int I2,
                 int nsm, cudaStream_t st) {
@@ -194,6 +233,34 @@ void launch_smp_table2(const void* G, const void* As1, const void* As2, int lda,
     else
         smp::k_table2<float><<<grid, 256, 0, st>>>((const float*)G, (const float*)As1, (const float*)As2, lda, I1, I2, J,
                                                    n, r, s1, s2, (float*)T);
+}
+
+void launch_smp_table1(const void* G, const void* As, int lda, int64_t Is, int J, int n, int a, int b, int s, void* T,
+                       int elem_bytes, cudaStream_t st) {
+    const int GB = gblk(J, elem_bytes);
+    const int64_t total = Is * J * GB;
+    const int grid = (int)((total + 255) / 256);
+    if (elem_bytes == 8)
+        smp::k_table1<double><<<grid, 256, 0, st>>>((const double*)G, (const double*)As, lda, Is, J, n, a, b, s, GB,
+                                                    (double*)T);
+    else
+        smp::k_table1<float><<<grid, 256, 0, st>>>((const float*)G, (const float*)As, lda, Is, J, n, a, b, s, GB,
+                                                   (float*)T);
+}
+
+bool launch_table_update(const void* params, int elem_bytes, int J, int nsm, cudaStream_t st) {
+#define PT_TU(JJ)                                                                                              \
+    case JJ:                                                                                                  \
+        if (elem_bytes == 4)                                                                                  \
+            smp::launch_table_update<float, JJ>(*reinterpret_cast<const UpdateParams<float>*>(params), nsm, st); \
+        else                                                                                                  \
+            smp::launch_table_update<double, JJ>(*reinterpret_cast<const UpdateParams<double>*>(params), nsm, st); \
+        return true;
+    switch (J) {
+        PT_TU(2) PT_TU(3) PT_TU(4) PT_TU(5) PT_TU(8) PT_TU(10)
+    }
+#undef PT_TU
+    return false;
 }
 
 bool launch_smp2_update(const void* params, int elem_bytes, int J, const void* T, int64_t tab_elems, int ir, int is1,

@@ -245,14 +245,16 @@ __device__ __forceinline__ void stage_row(const uint4* __restrict__ chunk0, TR (
 
 __host__ __device__ inline size_t gp_smem_bytes(int gp_elems, int esz) { return ((size_t)gp_elems * esz + 15) / 16 * 16; }
 
-template <typename TS, typename TF, int N, int J, int L64, bool LITERAL>
+// TABLE: the "core" is a table of blocks in shared memory (small-mode
+// precontraction, smp.cu) and each lane contracts with block lane_aux[slot].
+template <typename TS, typename TF, int N, int J, int L64, bool LITERAL, bool TABLE = false>
 __global__ void __launch_bounds__(kUpdThreads, 1) k_update(const UpdateParams<TS> p) {
     using TD = LevelT<TF, 0, L64>;  // type of delta
     constexpr int NB = J * (J + 1) / 2;
     using V = typename Vec16<TS>::type;
     constexpr int VN = Vec16<TS>::n;
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    constexpr bool GC = CoreInConst<TS, N, J>::value;
+    constexpr bool GC = CoreInConst<TS, N, J>::value && !TABLE;
     const TS* gs;
     if constexpr (GC) {
         gs = reinterpret_cast<const TS*>(c_core);
@@ -290,6 +292,8 @@ __global__ void __launch_bounds__(kUpdThreads, 1) k_update(const UpdateParams<TS
         const int len = p.lane_len[slot];
         const int iters = p.slice_len[s];
         const int64_t base = p.slice_off[s] + lane;
+        const TS* gl = gs;
+        if constexpr (TABLE) gl = gs + (int64_t)p.lane_aux[slot] * p.aux_stride;
 
         double B[NB], c[J], s2 = 0.0;
 #pragma unroll
@@ -349,7 +353,7 @@ __global__ void __launch_bounds__(kUpdThreads, 1) k_update(const UpdateParams<TS
                 for (int j = 0; j < J; ++j) a_out[0][j] = TS(0);
             }
             TD d[J];
-            compute_delta<TS, TF, N, J, L64>(gs, a_in, a_out,
+            compute_delta<TS, TF, N, J, L64>(gl, a_in, a_out,
                                             reinterpret_cast<const TS*>(stg + (st * NR) * NQ * kWarp), d);
 #pragma unroll
             for (int k = 0; k < NR; ++k) {

@@ -124,8 +124,10 @@ def test_mode_update_f64_c1(pt, orc):
     mode_update_parity(pt, orc, t, cfg, 1e-10, sweeps=2)        # mid-trajectory state
 
 
-@pytest.mark.parametrize("name,scale,seg", [("c2", 0.01, 256), ("c3", 0.002, 256), ("c3", 0.002, 7),
-                                            ("c4", 0.001, 256), ("c5", 0.0001, 256)])
+# c3 at scale 0.005 (690 x 135 x 21 x 24) exercises both small-mode tables (kind 2 for
+# modes 0/1, kind 1 for modes 2/3); 0.002 (276 x 54 x 21 x 24) the plain order-4 kernel
+@pytest.mark.parametrize("name,scale,seg", [("c2", 0.01, 256), ("c3", 0.002, 256), ("c3", 0.005, 256),
+                                            ("c3", 0.005, 7), ("c4", 0.001, 256), ("c5", 0.0001, 256)])
 def test_mode_update_f32(pt, orc, name, scale, seg):
     cfg = synth.small(name, scale)
     coords, vals = init_cfg(pt, cfg, seg_len=seg)
@@ -134,8 +136,10 @@ def test_mode_update_f32(pt, orc, name, scale, seg):
     w0 = mode_update_parity(pt, orc, t, cfg, 1e-5, sweeps=0)    # init state (worst case, survey E4)
     w1 = mode_update_parity(pt, orc, t, cfg, 1e-5, sweeps=1)    # mid-trajectory
     info = pt.ptucker_info()
-    print(f"{name} seg={seg} worst row rel err init {w0:.2e} mid {w1:.2e}; heavy rows "
-          f"{[m['heavy_rows'] for m in info['modes']]}")
+    print(f"{name}@{scale} seg={seg} worst row rel err init {w0:.2e} mid {w1:.2e}; heavy rows "
+          f"{[m['heavy_rows'] for m in info['modes']]}; smp {[m['smp'] for m in info['modes']]}")
+    if name == "c3" and scale == 0.005:
+        assert [m["smp"] for m in info["modes"]] == [2, 2, 1, 1]
 
 
 @pytest.mark.parametrize("name,scale", [("c2", 0.01), ("c4", 0.001)])
@@ -252,7 +256,7 @@ def test_worked_example(pt, orc):
 
 
 def test_determinism(pt):
-    cfg = synth.small("c3", 0.002)
+    cfg = synth.small("c3", 0.005)
     init_cfg(pt, cfg, seg_len=16)
     pt.ptucker_sweep()
     a = [pt.ptucker_get_factor(n).copy() for n in range(4)]
