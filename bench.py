@@ -253,6 +253,9 @@ def run_ours(args, cfg):
     launches = pt.ptucker_info()["kernel_launches"] - launches0
     upd_ms, upd_n = pt.ptucker_kernel_stats("update")
     fin_ms, _ = pt.ptucker_kernel_stats("finalize")
+    per_mode = {f"update_m{n}": round(pt.ptucker_kernel_stats(f"update_m{n}")[0] / args.steps, 4) for n in range(N)}
+    per_mode.update({f"finalize_m{n}": round(pt.ptucker_kernel_stats(f"finalize_m{n}")[0] / args.steps, 4)
+                     for n in range(N)})
     pt.ptucker_set_option("time_kernels", 0)
     if world > 1:
         t = torch.tensor([ms, upd_ms], dtype=torch.float64, device="cuda")
@@ -286,6 +289,7 @@ def run_ours(args, cfg):
         "frac_of_pipe_roofline_time": t_roof / avg_launch_s,
         "avg_launch_ms": avg_launch_s * 1e3, "launches": upd_n,
         "update_share_of_step": upd_ms / ms, "finalize_ms_per_step": fin_ms / args.steps,
+        "ms_per_step_by_kernel": per_mode,
     }
 
     # e2e: the whole job through the public API from pinned host buffers

@@ -135,6 +135,8 @@ int ptucker_get_partition(int32_t n, int64_t* bounds);
  *                 cores (3xTF32, default); 0 = the all-ALU kernel
  *  "smp"          1 = small-mode precontraction where it applies (order 4, two other modes with
  *                 <= 64 rows whose table fits on chip; default), 0 = off
+ *  "smp_table"    two-small-mode table for fp32 data: 0 = fp32 copy in shared memory, 1 = fp64
+ *                 table read from L2, 2 = hybrid: fp64 for single-segment rows (default)
  *  "time_kernels" 1 = bracket every kernel launch with CUDA events (ptucker_kernel_stats) */
 int ptucker_set_option(const char* key, int64_t value);
 

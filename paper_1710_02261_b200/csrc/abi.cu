@@ -63,6 +63,7 @@ int fail(int code, const char* fmt, ...) {
 
 struct Pending {
     std::string name;
+    int mode;
     cudaEvent_t a, b;
 };
 
@@ -103,13 +104,15 @@ struct Ctx {
     const UpdateKernel* kern_alu = nullptr;  // ALU kernel (literal error pass, and updates when tc = 0)
     int use_tc = 1;                          // option "tc"
     int use_smp = 1;                         // option "smp"
+    int smp_tab = 2;                         // option "smp_table": 0 fp32 smem, 1 fp64 L2, 2 hybrid (default)
     struct Smp {
         int kind = 0;                        // 2: order-4 mode with two small other modes (smp.cu)
         int r = 0, s1 = 0, s2 = 0;           // global mode ids
         int ir = 0, is1 = 0, is2 = 0;        // ordinals among the other modes (SELL/param order)
         int64_t elems = 0;                   // table elements
     } smp[kMaxN];
-    void* smp_T = nullptr;                   // device table (largest over modes)
+    void* smp_T = nullptr;                   // device table (largest over modes), fp64
+    void* smp_T32 = nullptr;                 // fp32 copy of a kind-2 table
     int nsm = 148;
     int grid_upd = 0, grid_lit = 0;
     int64_t launches = 0;        // kernels this library launched since init (gpu_launches evidence)
@@ -124,10 +127,11 @@ Ctx g;
 cudaStream_t S() { return g.stream; }
 
 template <class F>
-int timed(const char* name, F&& f) {
+int timed(const char* name, F&& f, int mode = -1) {
     if (!g.time_kernels) return f();
     Pending p;
     p.name = name;
+    p.mode = mode;
     CK(cudaEventCreate(&p.a));
     CK(cudaEventCreate(&p.b));
     CK(cudaEventRecord(p.a, S()));
@@ -145,6 +149,11 @@ int fold_stats() {
         auto& s = g.stats[p.name];
         s.first += ms;
         s.second += 1;
+        if (p.mode >= 0) {
+            auto& sm = g.stats[p.name + "_m" + std::to_string(p.mode)];
+            sm.first += ms;
+            sm.second += 1;
+        }
         cudaEventDestroy(p.a);
         cudaEventDestroy(p.b);
     }
@@ -226,17 +235,20 @@ int launch_update_kernel(int n, bool literal) {
     if (g.mi[n].nslices == 0) return PTUCKER_OK;
     CK(cudaMemsetAsync(g.d_work, 0, sizeof(unsigned int), S()));
     const Ctx::Smp& sp = g.smp[n];
-    if (!literal && g.use_smp && sp.kind == 2) {
+    if (!literal && g.use_smp && sp.kind == 2 && !(g.prec == PTUCKER_F32 && g.smp_tab != 1 && sp.elems * 4 > 200 * 1024)) {
         // small-mode precontraction: T from the (unchanged) small-mode factors, then J^2 per entry
+        const int mode = g.prec == PTUCKER_F64 ? 1 : g.smp_tab;
         launch_smp_table2(g.G, g.A[sp.s1], g.A[sp.s2], g.lda, g.dims[sp.s1], g.dims[sp.s2], g.J, n, sp.r, sp.s1, sp.s2,
-                          g.smp_T, g.esz, S());
+                          (double*)g.smp_T, mode == 1 ? nullptr : g.smp_T32, g.esz, S());
         bool ok;
         if (g.prec == PTUCKER_F64) {
             UpdateParams<double> p = make_params<double>(n, false);
-            ok = launch_smp2_update(&p, 8, g.J, g.smp_T, sp.elems, sp.ir, sp.is1, sp.is2, (int)g.dims[sp.s2], g.nsm, S());
+            ok = launch_smp2_update(&p, 8, g.J, (const double*)g.smp_T, nullptr, sp.elems, sp.ir, sp.is1, sp.is2,
+                                    (int)g.dims[sp.s2], 1, g.nsm, S());
         } else {
             UpdateParams<float> p = make_params<float>(n, false);
-            ok = launch_smp2_update(&p, 4, g.J, g.smp_T, sp.elems, sp.ir, sp.is1, sp.is2, (int)g.dims[sp.s2], g.nsm, S());
+            ok = launch_smp2_update(&p, 4, g.J, (const double*)g.smp_T, g.smp_T32, sp.elems, sp.ir, sp.is1, sp.is2,
+                                    (int)g.dims[sp.s2], mode, g.nsm, S());
         }
         if (!ok) return fail(PTUCKER_EINVAL, "no SMP kernel for J=%d", g.J);
         g.launches += 2;
@@ -335,6 +347,7 @@ void free_all() {
     }
     g.G = g.Gtmp = nullptr;
     g.smp_T = nullptr;
+    g.smp_T32 = nullptr;
     g.lit_part = g.red_part = g.red_out = g.qr = g.qd = nullptr;
     g.d_fail = g.d_qrfail = nullptr;
     g.d_work = nullptr;
@@ -427,6 +440,11 @@ int ptucker_set_option(const char* key, int64_t value) {
         if (value != 0 && value != 1) return fail(PTUCKER_EINVAL, "tc must be 0 or 1");
         g.use_tc = (int)value;
         if (g.inited) return choose_kernel();
+        return PTUCKER_OK;
+    }
+    if (k == "smp_table") {
+        if (value < 0 || value > 2) return fail(PTUCKER_EINVAL, "smp_table must be 0, 1 or 2");
+        g.smp_tab = (int)value;
         return PTUCKER_OK;
     }
     if (k == "smp") {
@@ -534,7 +552,7 @@ int ptucker_init(const int32_t* coords, const void* vals, int32_t vals_dtype, in
                     if (dims[oth[x]] > 64) r = x;
                 const int a = r == 0 ? 1 : 0, b = 3 - r - a;
                 const int64_t elems = dims[oth[a]] * dims[oth[b]] * (int64_t)J * J;
-                if (elems * esz <= 200 * 1024) {
+                if (elems * 8 <= (64 << 20)) {  // fp64 table in L2 (the fp32 shared-memory variant needs <= 200 KB)
                     sp.kind = 2;
                     sp.r = oth[r]; sp.s1 = oth[a]; sp.s2 = oth[b];
                     sp.ir = r; sp.is1 = a; sp.is2 = b;
@@ -556,7 +574,8 @@ int ptucker_init(const int32_t* coords, const void* vals, int32_t vals_dtype, in
             }
             if (sp.kind) tmax = std::max(tmax, sp.elems);
         }
-        if (tmax > 0) CK(A.alloc(&g.smp_T, (size_t)tmax * esz));
+        if (tmax > 0) CK(A.alloc(&g.smp_T, (size_t)tmax * 8));
+        if (tmax > 0) CK(A.alloc(&g.smp_T32, (size_t)tmax * 4));
     }
     // ---- device index of every mode ----
     DeviceArena input;
@@ -595,7 +614,7 @@ int ptucker_update_mode(int32_t n) {
     if (rc) return rc;
     if (n < 0 || n >= g.N) return fail(PTUCKER_EINVAL, "mode %d out of range", n);
     g.last_fail_mode = n;
-    rc = timed("update", [&]() -> int { return launch_update_kernel(n, false); });
+    rc = timed("update", [&]() -> int { return launch_update_kernel(n, false); }, n);
     if (rc) return rc;
     ModeIndex& m = g.mi[n];
     if (m.nheavy > 0) {
@@ -605,7 +624,7 @@ int ptucker_update_mode(int32_t n) {
             g.launches += 1;
             CK(cudaGetLastError());
             return PTUCKER_OK;
-        });
+        }, n);
         if (rc) return rc;
     }
     if (g.world > 1) {

@@ -28,9 +28,10 @@ void launch_core_mode_product(const void* G, void* Gout, int elem_bytes, int N, 
                               cudaStream_t st);
 // ---- small-mode precontraction for order-4 tensors with two small modes (smp.cu) ----
 void launch_smp_table2(const void* G, const void* As1, const void* As2, int lda, int64_t I1, int64_t I2, int J, int n,
-                       int r, int s1, int s2, void* T, int elem_bytes, cudaStream_t st);
-bool launch_smp2_update(const void* params, int elem_bytes, int J, const void* T, int64_t tab_elems, int ir, int is1,
-                        int is2, int I2, int nsm, cudaStream_t st);
+                       int r, int s1, int s2, double* T64, void* T32, int elem_bytes, cudaStream_t st);
+// mode: 0 = fp32 table in smem, 1 = fp64 table from L2, 2 = hybrid (fp64 for single-segment rows)
+bool launch_smp2_update(const void* params, int elem_bytes, int J, const double* T64, const void* T32,
+                        int64_t tab_elems, int ir, int is1, int is2, int I2, int mode, int nsm, cudaStream_t st);
 // order-4 mode with ONE small other mode s: table of order-3 cores, one per row of s
 void launch_smp_table1(const void* G, const void* As, int lda, int64_t Is, int J, int n, int a, int b, int s, void* T,
                        int elem_bytes, cudaStream_t st);

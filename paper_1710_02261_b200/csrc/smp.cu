@@ -16,6 +16,7 @@
 #include <cstdint>
 #include <cstdio>
 #include <cstdlib>
+#include <type_traits>
 
 #include "internal.cuh"
 #include "update.cuh"
@@ -24,9 +25,9 @@ namespace pt {
 namespace smp {
 
 // ---- table build: one thread per output T[i1][i2][k_r][j], fp64 accumulation ----
-template <typename TS>
+template <typename TS, typename TT>
 __global__ void k_table2(const TS* __restrict__ G, const TS* __restrict__ As1, const TS* __restrict__ As2, int lda,
-                         int64_t I1, int64_t I2, int J, int n, int r, int s1, int s2, TS* __restrict__ T) {
+                         int64_t I1, int64_t I2, int J, int n, int r, int s1, int s2, TT* __restrict__ T) {
     const int64_t total = I1 * I2 * J * J;
     int strideG[4];
     {
@@ -48,27 +49,33 @@ __global__ void k_table2(const TS* __restrict__ G, const TS* __restrict__ As1, c
                 inner = fma(double(G[base + (int64_t)k1 * strideG[s1] + (int64_t)k2 * strideG[s2]]), double(a2[k2]), inner);
             acc = fma(double(a1[k1]), inner, acc);
         }
-        T[t] = TS(acc);
+        T[t] = TT(acc);
     }
 }
 
 // ---- row update: lane per row segment (SELL-32, as k_update), per entry
 //      delta = a_r^T T[i_s1][i_s2] in fp64; B, c, solve as in k_update ----
-template <typename TS, int J>
-__global__ void __launch_bounds__(kUpdThreads, 1) k_update_smp2(const UpdateParams<TS> p, const TS* __restrict__ T,
-                                                               int64_t tab_elems, int ir, int is1, int is2, int I2) {
+// Table source (MODE): 0 = fp32 copy in shared memory; 1 = the fp64 table read
+// from global memory (L2-resident, 8*I_s1*I_s2*J^2 bytes) -- exact to fp64 but
+// ~4x the time; 2 = hybrid: the fp64 table for rows that fit one segment (the
+// light, ill-conditioned rows that dominate the fp32 table's rounding error),
+// the fp32 shared-memory copy for multi-segment (heavy) rows.
+template <typename TS, int J, int MODE>
+__global__ void __launch_bounds__(kUpdThreads, 1) k_update_smp2(const UpdateParams<TS> p, const double* __restrict__ T64,
+                                                               const TS* __restrict__ T32, int64_t tab_elems, int ir,
+                                                               int is1, int is2, int I2) {
     constexpr int NB = J * (J + 1) / 2;
     using V = typename Vec16<TS>::type;
     constexpr int VN = Vec16<TS>::n;
     constexpr int BLK = J * J;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     TS* ts = reinterpret_cast<TS*>(smem_raw);
-    {
-        const V* src = reinterpret_cast<const V*>(T);
+    if constexpr (MODE != 1) {
+        const V* src = reinterpret_cast<const V*>(T32);
         V* dst = reinterpret_cast<V*>(ts);
         for (int64_t i = threadIdx.x; i < tab_elems / VN; i += blockDim.x) dst[i] = src[i];
+        __syncthreads();
     }
-    __syncthreads();
     const int lane = threadIdx.x & (kWarp - 1);
     for (;;) {
         int s = 0;
@@ -80,6 +87,7 @@ __global__ void __launch_bounds__(kUpdThreads, 1) k_update_smp2(const UpdatePara
         const int len = p.lane_len[slot];
         const int iters = p.slice_len[s];
         const int64_t base = p.slice_off[s] + lane;
+        const bool use64 = MODE == 1 || (MODE == 2 && p.lane_pidx[slot] < 0);
         double B[NB], c[J], s2 = 0.0;
 #pragma unroll
         for (int q = 0; q < NB; ++q) B[q] = 0.0;
@@ -108,15 +116,26 @@ __global__ void __launch_bounds__(kUpdThreads, 1) k_update_smp2(const UpdatePara
                 load(e + 1, nr, n1, n2, nx);
                 load_row<TS, J>(p.A[ir] + (int64_t)nr * p.lda, nar);
             }
-            const TS* tb = ts + ((int64_t)c1 * I2 + c2) * BLK;
+            const int64_t boff = ((int64_t)c1 * I2 + c2) * BLK;
             double d[J];
 #pragma unroll
             for (int j = 0; j < J; ++j) d[j] = 0.0;
+            if (use64) {
+                const double* tb = T64 + boff;
 #pragma unroll
-            for (int k = 0; k < J; ++k) {
-                const double ak = double(ar[k]);
+                for (int k = 0; k < J; ++k) {
+                    const double ak = double(ar[k]);
 #pragma unroll
-                for (int j = 0; j < J; ++j) d[j] = fma(ak, double(tb[k * J + j]), d[j]);
+                    for (int j = 0; j < J; ++j) d[j] = fma(ak, __ldg(tb + k * J + j), d[j]);
+                }
+            } else {
+                const TS* tb = ts + boff;
+#pragma unroll
+                for (int k = 0; k < J; ++k) {
+                    const double ak = double(ar[k]);
+#pragma unroll
+                    for (int j = 0; j < J; ++j) d[j] = fma(ak, double(tb[k * J + j]), d[j]);
+                }
             }
             const bool act = e < len;
             const double xd = act ? double(x) : 0.0;
@@ -207,32 +226,38 @@ int launch_table_update(const UpdateParams<TS>& p, int nsm, cudaStream_t st) {
     return 0;
 }
 
-template <typename TS, int J>
-int launch_smp2(const UpdateParams<TS>& p, const TS* T, int64_t tab_elems, int ir, int is1, int is2, int I2,
-                int nsm, cudaStream_t st) {
-    auto k = k_update_smp2<TS, J>;
-    const size_t smem = (size_t)tab_elems * sizeof(TS);
+template <typename TS, int J, int MODE>
+int launch_smp2(const UpdateParams<TS>& p, const double* T64, const TS* T32, int64_t tab_elems, int ir, int is1,
+                int is2, int I2, int nsm, cudaStream_t st) {
+    auto k = k_update_smp2<TS, J, MODE>;
+    const size_t smem = MODE == 1 ? 0 : (size_t)tab_elems * sizeof(TS);
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     int nb = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k, kUpdThreads, smem);
     if (nb < 1) nb = 1;
-    k<<<nsm * nb, kUpdThreads, smem, st>>>(p, T, tab_elems, ir, is1, is2, I2);
+    k<<<nsm * nb, kUpdThreads, smem, st>>>(p, T64, T32, tab_elems, ir, is1, is2, I2);
     return 0;
 }
 
 }  // namespace smp
 
 // Host entry points (declared in kernels.cuh).
+__global__ void k_round_table(const double* T64, float* T32, int64_t n) {
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n; t += (int64_t)gridDim.x * blockDim.x)
+        T32[t] = float(T64[t]);
+}
+
 void launch_smp_table2(const void* G, const void* As1, const void* As2, int lda, int64_t I1, int64_t I2, int J, int n,
-                       int r, int s1, int s2, void* T, int elem_bytes, cudaStream_t st) {
+                       int r, int s1, int s2, double* T64, void* T32, int elem_bytes, cudaStream_t st) {
     const int64_t total = I1 * I2 * J * J;
     int grid = (int)((total + 255) / 256);
     if (elem_bytes == 8)
-        smp::k_table2<double><<<grid, 256, 0, st>>>((const double*)G, (const double*)As1, (const double*)As2, lda, I1, I2,
-                                                    J, n, r, s1, s2, (double*)T);
+        smp::k_table2<double, double><<<grid, 256, 0, st>>>((const double*)G, (const double*)As1, (const double*)As2, lda,
+                                                            I1, I2, J, n, r, s1, s2, T64);
     else
-        smp::k_table2<float><<<grid, 256, 0, st>>>((const float*)G, (const float*)As1, (const float*)As2, lda, I1, I2, J,
-                                                   n, r, s1, s2, (float*)T);
+        smp::k_table2<float, double><<<grid, 256, 0, st>>>((const float*)G, (const float*)As1, (const float*)As2, lda, I1,
+                                                           I2, J, n, r, s1, s2, T64);
+    if (T32) k_round_table<<<grid, 256, 0, st>>>(T64, (float*)T32, total);
 }
 
 void launch_smp_table1(const void* G, const void* As, int lda, int64_t Is, int J, int n, int a, int b, int s, void* T,
@@ -263,29 +288,25 @@ bool launch_table_update(const void* params, int elem_bytes, int J, int nsm, cud
     return false;
 }
 
-bool launch_smp2_update(const void* params, int elem_bytes, int J, const void* T, int64_t tab_elems, int ir, int is1,
-                        int is2, int I2, int nsm, cudaStream_t st) {
-    if (elem_bytes == 4) {
-        const auto& p = *reinterpret_cast<const UpdateParams<float>*>(params);
-        switch (J) {
-            case 2: smp::launch_smp2<float, 2>(p, (const float*)T, tab_elems, ir, is1, is2, I2, nsm, st); return true;
-            case 3: smp::launch_smp2<float, 3>(p, (const float*)T, tab_elems, ir, is1, is2, I2, nsm, st); return true;
-            case 4: smp::launch_smp2<float, 4>(p, (const float*)T, tab_elems, ir, is1, is2, I2, nsm, st); return true;
-            case 5: smp::launch_smp2<float, 5>(p, (const float*)T, tab_elems, ir, is1, is2, I2, nsm, st); return true;
-            case 8: smp::launch_smp2<float, 8>(p, (const float*)T, tab_elems, ir, is1, is2, I2, nsm, st); return true;
-            case 10: smp::launch_smp2<float, 10>(p, (const float*)T, tab_elems, ir, is1, is2, I2, nsm, st); return true;
-        }
-    } else {
-        const auto& p = *reinterpret_cast<const UpdateParams<double>*>(params);
-        switch (J) {
-            case 2: smp::launch_smp2<double, 2>(p, (const double*)T, tab_elems, ir, is1, is2, I2, nsm, st); return true;
-            case 3: smp::launch_smp2<double, 3>(p, (const double*)T, tab_elems, ir, is1, is2, I2, nsm, st); return true;
-            case 4: smp::launch_smp2<double, 4>(p, (const double*)T, tab_elems, ir, is1, is2, I2, nsm, st); return true;
-            case 5: smp::launch_smp2<double, 5>(p, (const double*)T, tab_elems, ir, is1, is2, I2, nsm, st); return true;
-            case 8: smp::launch_smp2<double, 8>(p, (const double*)T, tab_elems, ir, is1, is2, I2, nsm, st); return true;
-            case 10: smp::launch_smp2<double, 10>(p, (const double*)T, tab_elems, ir, is1, is2, I2, nsm, st); return true;
-        }
+bool launch_smp2_update(const void* params, int elem_bytes, int J, const double* T64, const void* T32,
+                        int64_t tab_elems, int ir, int is1, int is2, int I2, int mode, int nsm, cudaStream_t st) {
+#define PT_S2(JJ)                                                                                                 \
+    case JJ:                                                                                                     \
+        if (elem_bytes == 4) {                                                                                   \
+            const auto& p = *reinterpret_cast<const UpdateParams<float>*>(params);                               \
+            const float* t32 = (const float*)T32;                                                                \
+            if (mode == 1) smp::launch_smp2<float, JJ, 1>(p, T64, t32, tab_elems, ir, is1, is2, I2, nsm, st);     \
+            else if (mode == 2) smp::launch_smp2<float, JJ, 2>(p, T64, t32, tab_elems, ir, is1, is2, I2, nsm, st); \
+            else smp::launch_smp2<float, JJ, 0>(p, T64, t32, tab_elems, ir, is1, is2, I2, nsm, st);               \
+        } else {                                                                                                 \
+            const auto& p = *reinterpret_cast<const UpdateParams<double>*>(params);                              \
+            smp::launch_smp2<double, JJ, 1>(p, T64, nullptr, tab_elems, ir, is1, is2, I2, nsm, st);              \
+        }                                                                                                        \
+        return true;
+    switch (J) {
+        PT_S2(2) PT_S2(3) PT_S2(4) PT_S2(5) PT_S2(8) PT_S2(10)
     }
+#undef PT_S2
     return false;
 }
 
