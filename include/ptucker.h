@@ -137,6 +137,9 @@ int ptucker_get_partition(int32_t n, int64_t* bounds);
  *                 <= 64 rows whose table fits on chip; default), 0 = off
  *  "smp_table"    two-small-mode table for fp32 data: 0 = fp32 copy in shared memory, 1 = fp64
  *                 table read from L2, 2 = hybrid: fp64 for single-segment rows (default)
+ *  "emulate_world", "emulate_rank"  (before init, no communicator): build and update only
+ *                 this rank's row blocks of a `world`-way partition, without the exchange
+ *                 (tests of the partitioned path on one GPU)
  *  "time_kernels" 1 = bracket every kernel launch with CUDA events (ptucker_kernel_stats) */
 int ptucker_set_option(const char* key, int64_t value);
 

@@ -74,6 +74,7 @@ struct Ctx {
     bool own_stream = false;
     int rank = 0, world = 1;
     ncclComm_t comm = nullptr;
+    int emu_rank = 0, emu_world = 1;  // options "emulate_rank"/"emulate_world": partition without a communicator
     // problem
     int N = 0, J = 0, prec = 0, esz = 4;
     int64_t nnz = 0;
@@ -442,6 +443,19 @@ int ptucker_set_option(const char* key, int64_t value) {
         if (g.inited) return choose_kernel();
         return PTUCKER_OK;
     }
+    if (k == "emulate_world" || k == "emulate_rank") {
+        if (g.inited) return fail(PTUCKER_ESTATE, "%s must be set before ptucker_init", key);
+        if (g.comm) return fail(PTUCKER_ESTATE, "a communicator is active");
+        if (k == "emulate_world") {
+            if (value < 1 || value > 1024) return fail(PTUCKER_EINVAL, "emulate_world out of range");
+            g.emu_world = (int)value;
+        } else {
+            if (value < 0) return fail(PTUCKER_EINVAL, "emulate_rank out of range");
+            g.emu_rank = (int)value;
+        }
+        if (g.emu_rank >= g.emu_world) g.emu_rank = 0;
+        return PTUCKER_OK;
+    }
     if (k == "smp_table") {
         if (value < 0 || value > 2) return fail(PTUCKER_EINVAL, "smp_table must be 0, 1 or 2");
         g.smp_tab = (int)value;
@@ -585,6 +599,10 @@ int ptucker_init(const int32_t* coords, const void* vals, int32_t vals_dtype, in
     CK(input.alloc(&d_vals, (size_t)nnz * esz));
     CK(cudaMemcpyAsync(d_coords, coords, (size_t)nnz * order * sizeof(int32_t), cudaMemcpyHostToDevice, S()));
     CK(cudaMemcpyAsync(d_vals, vals, (size_t)nnz * esz, cudaMemcpyHostToDevice, S()));
+    if (!g.comm) {  // no communicator: a single rank, or an emulated rank of a partition (tests)
+        g.world = g.emu_world;
+        g.rank = g.emu_rank;
+    }
     for (int n = 0; n < order; ++n) {
         ModeIndex& m = g.mi[n];
         CK(build_mode_csr(d_coords, nnz, order, n, dims[n], m, g.arena, g.scratch, S()));
@@ -627,7 +645,7 @@ int ptucker_update_mode(int32_t n) {
         }, n);
         if (rc) return rc;
     }
-    if (g.world > 1) {
+    if (g.world > 1 && g.comm) {
         rc = timed("allgather", [&]() -> int {
             // all-gather-v of the row blocks (grouped broadcasts, in place)
             const ncclDataType_t dt = g.prec == PTUCKER_F64 ? ncclDouble : ncclFloat;
@@ -658,7 +676,7 @@ int ptucker_sweep(void) {
 }
 
 static int finish_error(double* out) {
-    if (g.world > 1) NK(ncclAllReduce(g.red_out, g.red_out, 1, ncclDouble, ncclSum, g.comm, S()));
+    if (g.world > 1 && g.comm) NK(ncclAllReduce(g.red_out, g.red_out, 1, ncclDouble, ncclSum, g.comm, S()));
     double h = 0.0;
     CK(cudaMemcpyAsync(&h, g.red_out, sizeof(double), cudaMemcpyDeviceToHost, S()));
     int rc = sync_and_check();
@@ -863,6 +881,8 @@ int ptucker_finalize(void) {
     }
     g.world = 1;
     g.rank = 0;
+    g.emu_world = 1;
+    g.emu_rank = 0;
     if (g.own_stream && g.stream) cudaStreamDestroy(g.stream);
     g.stream = nullptr;
     g.own_stream = false;
