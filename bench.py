@@ -219,6 +219,7 @@ def run_ours(args, cfg):
     pt.ptucker_init(coords, vals, cfg.dims, [J] * N, cfg.lam, cfg.seed)
     pt.ptucker_set_option("policy", POLICY[args.policy])
     pt.ptucker_set_option("tc", args.tc)
+    pt.ptucker_set_option("l0_group", args.l0_group)
     pt.ptucker_synchronize()
     init_s = time.perf_counter() - t0
     info = pt.ptucker_info()
@@ -303,6 +304,7 @@ def run_ours(args, cfg):
         pt.ptucker_init(pc, pv, cfg.dims, [J] * N, cfg.lam, cfg.seed)
         pt.ptucker_set_option("policy", POLICY[args.policy])
         pt.ptucker_set_option("tc", args.tc)
+        pt.ptucker_set_option("l0_group", args.l0_group)
         for _ in range(args.steps):
             pt.ptucker_sweep()
             pt.ptucker_error()
@@ -347,6 +349,7 @@ def main():
     ap.add_argument("--policy", default="auto", choices=list(POLICY))
     ap.add_argument("--seg-len", type=int, default=256)
     ap.add_argument("--tc", type=int, default=1, choices=[0, 1], help="tensor-core inner stage for order-3 fp32")
+    ap.add_argument("--l0-group", type=int, default=1, choices=[1, 2], help="tensor-core level-0 fp32 pairing")
     ap.add_argument("--ref-seconds", type=float, default=12.0)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")

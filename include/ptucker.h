@@ -152,6 +152,10 @@ int ptucker_reset_kernel_stats(void);
 /* JSON description of the context (sizes, segments, kernel variant); host buffer. */
 int ptucker_info(char* buf, int32_t len);
 
+/* Tools only: copy the per-phase clock trace recorded while option "trace" is on
+ * (host buffer of n int64; layout documented in tools/trace_tc.py). */
+int ptucker_debug_trace(long long* out, int32_t n);
+
 /* Wait for all enqueued work; reports deferred numeric failures. */
 int ptucker_synchronize(void);
 

@@ -104,6 +104,9 @@ struct Ctx {
     const UpdateKernel* kern = nullptr;      // row update (tensor-core variant when available)
     const UpdateKernel* kern_alu = nullptr;  // ALU kernel (literal error pass, and updates when tc = 0)
     int use_tc = 1;                          // option "tc"
+    int l0_group = 1;                        // option "l0_group" (tensor-core kernel, F32-B)
+    float* tc_hi = nullptr;                  // tf32 split of the innermost factor (tensor-core kernel)
+    float* tc_lo = nullptr;
     int use_smp = 1;                         // option "smp"
     int smp_tab = 2;                         // option "smp_table": 0 fp32 smem, 1 fp64 L2, 2 hybrid (default)
     struct Smp {
@@ -117,6 +120,7 @@ struct Ctx {
     int nsm = 148;
     int grid_upd = 0, grid_lit = 0;
     int64_t launches = 0;        // kernels this library launched since init (gpu_launches evidence)
+    long long* trace = nullptr;  // option "trace": device buffer of per-phase clocks (tools/)
     // timing
     bool time_kernels = false;
     std::vector<Pending> pending;
@@ -228,6 +232,10 @@ UpdateParams<TS> make_params(int n, bool literal) {
     p.fail = g.d_fail;
     p.work = g.d_work;
     p.policy = g.policy;
+    p.trace = g.trace;
+    p.ext0 = g.tc_hi;
+    p.ext1 = g.tc_lo;
+    p.l0_group = g.l0_group;
     return p;
 }
 
@@ -287,6 +295,18 @@ int launch_update_kernel(int n, bool literal) {
     }
     g.launches += 1;
     const UpdateKernel* k = literal ? g.kern_alu : g.kern;
+    if (!literal && k != g.kern_alu) {
+        // tensor-core kernel: tf32 hi/lo split of the innermost other factor (A operand)
+        const int inner = n == g.N - 1 ? g.N - 2 : g.N - 1;
+        if (!g.tc_hi) {
+            int64_t imax = 0;
+            for (int m = 0; m < g.N; ++m) imax = std::max(imax, g.dims[m]);
+            CK(g.arena.alloc((void**)&g.tc_hi, (size_t)imax * tc_kp(g.J) * sizeof(float)));
+            CK(g.arena.alloc((void**)&g.tc_lo, (size_t)imax * tc_kp(g.J) * sizeof(float)));
+        }
+        launch_tc_split((const float*)g.A[inner], g.dims[inner], g.lda, g.J, g.tc_hi, g.tc_lo, S());
+        g.launches += 1;
+    }
     if (g.prec == PTUCKER_F64) {
         UpdateParams<double> p = make_params<double>(n, literal);
         k->launch(&p, literal, grid, S());
@@ -349,6 +369,7 @@ void free_all() {
     g.G = g.Gtmp = nullptr;
     g.smp_T = nullptr;
     g.smp_T32 = nullptr;
+    g.tc_hi = g.tc_lo = nullptr;
     g.lit_part = g.red_part = g.red_out = g.qr = g.qd = nullptr;
     g.d_fail = g.d_qrfail = nullptr;
     g.d_work = nullptr;
@@ -437,6 +458,11 @@ int ptucker_set_option(const char* key, int64_t value) {
         g.seg_len = (int)value;
         return PTUCKER_OK;
     }
+    if (k == "l0_group") {
+        if (value != 1 && value != 2) return fail(PTUCKER_EINVAL, "l0_group must be 1 or 2");
+        g.l0_group = (int)value;
+        return PTUCKER_OK;
+    }
     if (k == "tc") {
         if (value != 0 && value != 1) return fail(PTUCKER_EINVAL, "tc must be 0 or 1");
         g.use_tc = (int)value;
@@ -454,6 +480,16 @@ int ptucker_set_option(const char* key, int64_t value) {
             g.emu_rank = (int)value;
         }
         if (g.emu_rank >= g.emu_world) g.emu_rank = 0;
+        return PTUCKER_OK;
+    }
+    if (k == "trace") {
+        if (value) {
+            if (!g.trace) CK(cudaMalloc((void**)&g.trace, 8 * 512 * sizeof(long long)));
+            CK(cudaMemset(g.trace, 0, 8 * 512 * sizeof(long long)));
+        } else if (g.trace) {
+            cudaFree(g.trace);
+            g.trace = nullptr;
+        }
         return PTUCKER_OK;
     }
     if (k == "smp_table") {
@@ -861,6 +897,12 @@ int ptucker_info(char* buf, int32_t len) {
     s += "]}";
     snprintf(buf, (size_t)len, "%s", s.c_str());
     return (int)s.size() < len ? PTUCKER_OK : fail(PTUCKER_EINVAL, "buffer too small (%zu)", s.size() + 1);
+}
+
+int ptucker_debug_trace(long long* out, int32_t n) {
+    if (!g.trace || !out || n <= 0) return fail(PTUCKER_EINVAL, "no trace");
+    CK(cudaMemcpy(out, g.trace, sizeof(long long) * std::min<int32_t>(n, 8 * 512), cudaMemcpyDeviceToHost));
+    return PTUCKER_OK;
 }
 
 int ptucker_synchronize(void) {

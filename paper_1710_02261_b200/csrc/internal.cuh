@@ -53,6 +53,10 @@ struct UpdateParams {
     int* fail;                    // numeric failure flag (row+1)
     unsigned int* work;           // dynamic slice counter (reset to 0 before launch)
     int policy;                   // runtime copy of the precision policy (info only)
+    long long* trace;             // optional per-phase clock trace (tools; null in production)
+    const void* ext0;             // kernel-specific extra inputs (tensor-core kernel: tf32 hi/lo split
+    const void* ext1;             //   tables of the innermost factor, KP floats per row)
+    int l0_group;                 // tensor-core kernel: level-0 terms summed in fp32 before fp64 (1 or 2)
 };
 
 using UpdateLauncher = void (*)(const void* params, bool literal, int grid, cudaStream_t st);
@@ -74,6 +78,8 @@ const UpdateKernel* update_kernels_f64(int* count);
 const UpdateKernel* find_update_kernel(int prec, int l64, int N, int J);
 // Tensor-core variant (fp32, N = 3): innermost TTV stage on tcgen05 (update_tc.cu).
 const UpdateKernel* find_update_kernel_tc(int l64, int J);
+int tc_kp(int J);  // K padding of the tensor-core A operand (floats per split row)
+void launch_tc_split(const float* A, int64_t I, int lda, int J, float* hi, float* lo, cudaStream_t st);
 
 // (N, J) pairs compiled: N = 2..5, J in {2,3,4,5,8,10}, J^N <= 10^4.
 #define PT_NJ_LIST(X) \

@@ -87,6 +87,28 @@ __device__ __forceinline__ void tmem_ld32(uint32_t addr, float (&v)[32]) {
     for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
 }
 
+__device__ __forceinline__ void tmem_ld4_nowait(uint32_t addr, float (&v)[4]) {
+    uint32_t r[4];
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+                 : "r"(addr));
+#pragma unroll
+    for (int i = 0; i < 4; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+__device__ __forceinline__ void tmem_ld16_nowait(uint32_t addr, float (&v)[16]) {
+    uint32_t r[16];
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
+          "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+        : "r"(addr));
+#pragma unroll
+    for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+__device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+
 __device__ __forceinline__ void tmem_ld16(uint32_t addr, float (&v)[16]) {
     uint32_t r[16];
     asm volatile(
@@ -106,24 +128,43 @@ struct Shape {
     static constexpr int NP = (J * J + 15) / 16 * 16;      // N padded to 16 (M = 128)
     static constexpr int TCOLS = 2 * NP <= 32 ? 32 : (2 * NP <= 64 ? 64 : (2 * NP <= 128 ? 128 : (2 * NP <= 256 ? 256 : 512)));
     static constexpr int LD = factor_ld(J, 4);             // padded factor row (floats)
-    static constexpr int NQ = LD / 4;                       // 16-byte chunks per row
+    static constexpr int NQ = LD / 4;                       // 16-byte chunks per factor row
+    static constexpr int KQ = KP / 4;                       // 16-byte chunks per A row
+    static constexpr int STAGES = 3;                        // gather/A-tile pipeline depth
     // shared memory map (bytes)
     static constexpr int B_BYTES = NP * KP * 4;                     // one of B_hi / B_lo
     static constexpr int A_BYTES = kThreads * KP * 4;               // one of A_hi / A_lo (per stage)
-    static constexpr int RING_CHUNKS = 3 * 2 * NQ * kThreads;       // 3 stages x 2 rows
+    static constexpr int RING_CHUNKS = STAGES * NQ * kThreads;      // the level-0 rows a0
     static constexpr int OFF_BHI = 0;
     static constexpr int OFF_BLO = OFF_BHI + B_BYTES;
     static constexpr int OFF_A = OFF_BLO + B_BYTES;                 // [stage][hi,lo]
-    static constexpr int OFF_RING = OFF_A + 4 * A_BYTES;
+    static constexpr int OFF_RING = OFF_A + STAGES * 2 * A_BYTES;
     static constexpr int OFF_BAR = OFF_RING + RING_CHUNKS * 16;     // mbarriers: acc_full[2]
-    static constexpr int OFF_MISC = OFF_BAR + 32;                   // tmem base, group id
-    static constexpr int SMEM = OFF_MISC + 16;
+    static constexpr int OFF_MISC = OFF_BAR + 32;                   // tmem base, group id, arrival counters
+    static constexpr int SMEM = OFF_MISC + 32;
 };
 
-template <int J, bool LAST64>
+// Split of the innermost factor into tf32 hi/lo parts (3xTF32 operand), K-padded:
+// out rows of KP floats, hi = tf32_rna(a), lo = tf32_rna(a - hi), zeros for k >= J.
+__global__ void k_split_tf32(const float* __restrict__ A, int64_t I, int lda, int J, int KP, float* __restrict__ hi,
+                             float* __restrict__ lo) {
+    const int64_t total = I * KP;
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t i = t / KP;
+        const int k = (int)(t % KP);
+        const float v = k < J ? A[i * lda + k] : 0.f;
+        const float h = tf32_rna(v);
+        hi[t] = h;
+        lo[t] = tf32_rna(v - h);
+    }
+}
+
+// G0 = level-0 terms summed in fp32 before each fp64 accumulation (1: every term
+// converted, the F32-B policy; 2: pairs -- half the fp32->fp64 conversions).
+template <int J, bool LAST64, int G0>
 __global__ void __launch_bounds__(kThreads, 2) k_update_tc(const UpdateParams<float> p) {
     using SH = Shape<J>;
-    constexpr int KP = SH::KP, NP = SH::NP, NQ = SH::NQ;
+    constexpr int KP = SH::KP, NP = SH::NP, NQ = SH::NQ, KQ = SH::KQ, ST = SH::STAGES;
     constexpr int NB = J * (J + 1) / 2;
     constexpr int GB = gblk(J, 4);
     using TD = typename std::conditional<LAST64, double, float>::type;
@@ -133,6 +174,8 @@ __global__ void __launch_bounds__(kThreads, 2) k_update_tc(const UpdateParams<fl
     uint4* ring = reinterpret_cast<uint4*>(sm + SH::OFF_RING);
     uint64_t* mbar = reinterpret_cast<uint64_t*>(sm + SH::OFF_BAR);
     uint32_t* misc = reinterpret_cast<uint32_t*>(sm + SH::OFF_MISC);
+    const float* __restrict__ Ahi_g = reinterpret_cast<const float*>(p.ext0);
+    const float* __restrict__ Alo_g = reinterpret_cast<const float*>(p.ext1);
     const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
 
     // ---- B = core (hi/lo tf32 split), K-major: Bt[(k0, j)][k1] = G'[k0][k1][j] ----
@@ -152,8 +195,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_update_tc(const UpdateParams<fl
     if (t == 0) {
         asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(&mbar[0])), "r"(1));
         asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(&mbar[1])), "r"(1));
-        misc[2] = 0;  // arrival counters of the two A stages
-        misc[3] = 0;
+        for (int q = 0; q < ST; ++q) misc[2 + q] = 0;  // arrival counters of the A stages
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -166,44 +208,23 @@ __global__ void __launch_bounds__(kThreads, 2) k_update_tc(const UpdateParams<fl
     const uint32_t a_base = smem_u32(sm + SH::OFF_A);
     uint32_t ntile = 0;  // tiles issued so far by this CTA (mbarrier phases, buffer parity)
 
-    // ring chunk (stage, row k, q) of this thread
-    auto ring_at = [&](int st, int k, int q) -> uint4* { return ring + ((st * 2 + k) * NQ + q) * kThreads + t; };
-    auto issue_rows = [&](int st, int c0, int c1) {
+    auto ring_at = [&](int st, int q) -> uint4* { return ring + (st * NQ + q) * kThreads + t; };
+    // cp.async the entry's level-0 row a0 (ring) and its pre-split A row (hi, lo) into stage st
+    auto issue = [&](int st, int c0, int c1) {
         const char* s0 = reinterpret_cast<const char*>(p.A[0] + (int64_t)c0 * p.lda);
-        const char* s1 = reinterpret_cast<const char*>(p.A[1] + (int64_t)c1 * p.lda);
 #pragma unroll
-        for (int q = 0; q < NQ; ++q) {
-            cp_async16(ring_at(st, 0, q), s0 + 16 * q);
-            cp_async16(ring_at(st, 1, q), s1 + 16 * q);
-        }
-    };
-    // A tile of stage `st` (hi, lo), row t = this thread's a1 row, zero-padded to KP
-    auto build_a = [&](int rst, int st) {
-        float a1[NQ * 4];
+        for (int q = 0; q < NQ; ++q) cp_async16(ring_at(st, q), s0 + 16 * q);
+        const char* sh = reinterpret_cast<const char*>(Ahi_g + (int64_t)c1 * KP);
+        const char* sl = reinterpret_cast<const char*>(Alo_g + (int64_t)c1 * KP);
+        unsigned char* dh = sm + SH::OFF_A + (st * 2 + 0) * SH::A_BYTES;
+        unsigned char* dl = sm + SH::OFF_A + (st * 2 + 1) * SH::A_BYTES;
 #pragma unroll
-        for (int q = 0; q < NQ; ++q) {
-            const float4 v = *reinterpret_cast<const float4*>(ring_at(rst, 1, q));
-            a1[4 * q] = v.x; a1[4 * q + 1] = v.y; a1[4 * q + 2] = v.z; a1[4 * q + 3] = v.w;
-        }
-        float* Ahi = reinterpret_cast<float*>(sm + SH::OFF_A + (st * 2 + 0) * SH::A_BYTES);
-        float* Alo = reinterpret_cast<float*>(sm + SH::OFF_A + (st * 2 + 1) * SH::A_BYTES);
-#pragma unroll
-        for (int q = 0; q < KP / 4; ++q) {
-            float h[4], l[4];
-#pragma unroll
-            for (int u = 0; u < 4; ++u) {
-                const int k = 4 * q + u;
-                const float v = (k < J) ? a1[k] : 0.f;
-                h[u] = tf32_rna(v);
-                l[u] = tf32_rna(v - h[u]);
-            }
-            *reinterpret_cast<float4*>(Ahi + kmaj<KP>(t, 4 * q)) = make_float4(h[0], h[1], h[2], h[3]);
-            *reinterpret_cast<float4*>(Alo + kmaj<KP>(t, 4 * q)) = make_float4(l[0], l[1], l[2], l[3]);
+        for (int q = 0; q < KQ; ++q) {
+            cp_async16(dh + kmaj<KP>(t, 4 * q) * 4, sh + 16 * q);
+            cp_async16(dl + kmaj<KP>(t, 4 * q) * 4, sl + 16 * q);
         }
     };
     // 3xTF32 into TMEM buffer `buf` from A stage `st`: lo*hi, hi*lo, hi*hi (small terms first)
-    // A tile of stage `st` complete (all 128 rows arrived): the a_full barrier
-    // of that stage completes once per use, so its phase is (tile >> 1) & 1.
     auto issue_mma = [&](int st, int buf) {
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
         const uint32_t ahi = a_base + (st * 2 + 0) * SH::A_BYTES, alo = a_base + (st * 2 + 1) * SH::A_BYTES;
@@ -222,11 +243,10 @@ __global__ void __launch_bounds__(kThreads, 2) k_update_tc(const UpdateParams<fl
         asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
                          smem_u32(&mbar[buf])) : "memory");
     };
-
-    // A row written: make it visible to the tensor core's async proxy, then count
-    // the arrival; the LAST of the 128 threads issues the MMAs for that stage, so
-    // no thread ever blocks on the others here.  (acq_rel atomic: the issuer
-    // observes every writer's row and its completed tcgen05.ld of the buffer.)
+    // This thread's A row of stage st has landed: make it visible to the tensor
+    // core's async proxy and count the arrival; the LAST of the 128 threads issues
+    // the MMAs, so no thread blocks on the others here (acq_rel atomic: the issuer
+    // observes every row and every completed tcgen05.ld of the TMEM buffer).
     auto arrive_a = [&](int st, int buf) {
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -274,18 +294,17 @@ __global__ void __launch_bounds__(kThreads, 2) k_update_tc(const UpdateParams<fl
             load_crd(0, ca0, cb0, x0);
             load_crd(1, ca1, cb1, x1);
             load_crd(2, ca2, cb2, x2);
-            issue_rows(0, ca0, cb0);
+            const int st0 = (int)(ntile % ST);
+            issue(st0, ca0, cb0);
             cp_async_commit();
-            if (iters > 1) issue_rows(1, ca1, cb1);
+            if (iters > 1) issue((st0 + 1) % ST, ca1, cb1);
             cp_async_commit();
             cp_async_wait<1>();
-            build_a(0, ntile & 1);
-            arrive_a(ntile & 1, ntile & 1);
-            int rs = 0;  // ring stage of entry e
+            arrive_a(st0, ntile & 1);
             for (int e = 0; e < iters; ++e) {
                 const uint32_t tile = ntile + e;
-                const int rs1 = rs == 2 ? 0 : rs + 1, rs2 = rs1 == 2 ? 0 : rs1 + 1;
-                if (e + 2 < iters) issue_rows(rs2, ca2, cb2);
+                const int rs = (int)(tile % ST), rs1 = (int)((tile + 1) % ST), rs2 = (int)((tile + 2) % ST);
+                if (e + 2 < iters) issue(rs2, ca2, cb2);
                 cp_async_commit();
                 const float x = x0;
                 // advance the coordinate queue: entry e+1 -> q0, e+2 -> q1, load e+3 -> q2
@@ -294,45 +313,62 @@ __global__ void __launch_bounds__(kThreads, 2) k_update_tc(const UpdateParams<fl
                 load_crd(e + 3, ca2, cb2, x2);
                 if (e + 1 < iters) {
                     cp_async_wait<1>();
-                    build_a(rs1, (tile + 1) & 1);
-                    arrive_a((tile + 1) & 1, (tile + 1) & 1);
+                    arrive_a(rs1, (tile + 1) & 1);
                 }
                 // ---- epilogue of entry e ----
-                TD a0[J];
+                float a0f[J];
 #pragma unroll
                 for (int q = 0; q < NQ; ++q) {
-                    const float4 v = *reinterpret_cast<const float4*>(ring_at(rs, 0, q));
+                    const float4 v = *reinterpret_cast<const float4*>(ring_at(rs, q));
                     const float w[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
                     for (int u = 0; u < 4; ++u)
-                        if (4 * q + u < J) a0[4 * q + u] = TD(w[u]);
+                        if (4 * q + u < J) a0f[4 * q + u] = w[u];
                 }
-                rs = rs1;
                 mbar_wait(smem_u32(&mbar[tile & 1]), (tile >> 1) & 1);
                 asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
                 TD d[J];
 #pragma unroll
                 for (int j = 0; j < J; ++j) d[j] = TD(0);
                 const uint32_t taddr = tmem + ((uint32_t)(warp * 32) << 16) + (tile & 1) * NP;
+                // level 0: d[j] = sum_k0 a0[k0] t[k0][j]; t[k0][j] is TMEM column k0*J + j
+                if constexpr (G0 == 2 && LAST64 && J == 10) {
+                    // pairs (k0, k0+1) = columns [20p, 20p+20): summed in fp32, one fp64 accumulation
 #pragma unroll
-                for (int c0 = 0; c0 < J * J; c0 += 32) {
-                    if (c0 + 16 >= J * J) {
-                        float v[16];
-                        tmem_ld16(taddr + c0, v);
+                    for (int pp = 0; pp < J / 2; ++pp) {
+                        float v[16], w[4];
+                        tmem_ld16_nowait(taddr + pp * 20, v);
+                        tmem_ld4_nowait(taddr + pp * 20 + 16, w);
+                        tmem_wait_ld();
+                        float t1[J];
 #pragma unroll
-                        for (int i = 0; i < 16; ++i) {
-                            const int cc = c0 + i;
-                            if (cc < J * J) d[cc % J] = fma(a0[cc / J], TD(v[i]), d[cc % J]);
-                        }
-                    } else {
-                        float v[32];
-                        tmem_ld32(taddr + c0, v);
+                        for (int j = 0; j < J; ++j) t1[j] = (J + j < 16) ? v[J + j] : w[J + j - 16];
 #pragma unroll
-                        for (int i = 0; i < 32; ++i) {
-                            const int cc = c0 + i;
-                            if (cc < J * J) d[cc % J] = fma(a0[cc / J], TD(v[i]), d[cc % J]);
-                        }
+                        for (int j = 0; j < J; ++j)
+                            d[j] = d[j] + TD(fmaf(a0f[2 * pp + 1], t1[j], a0f[2 * pp] * v[j]));
                     }
+                } else {
+                constexpr int NCH = (J * J + 31) / 32;
+#pragma unroll
+                for (int ch = 0; ch < NCH; ++ch) {
+                    float v[32];
+                    if (ch * 32 + 16 >= J * J) {
+                        float v16[16];
+                        tmem_ld16(taddr + ch * 32, v16);
+#pragma unroll
+                        for (int i = 0; i < 16; ++i) v[i] = v16[i];
+                    } else {
+                        tmem_ld32(taddr + ch * 32, v);
+                    }
+#pragma unroll
+                    for (int i = 0; i < 32; ++i) {
+                        const int cc = ch * 32 + i;
+                        if (cc >= J * J) continue;
+                        const int k0 = cc / J, j = cc % J;
+                        if constexpr (!LAST64) d[j] = fmaf(a0f[k0], v[i], d[j]);
+                        else d[j] = fma(TD(a0f[k0]), TD(v[i]), d[j]);
+                    }
+                }
                 }
                 asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
                 const bool act = e < len;
@@ -364,13 +400,13 @@ __global__ void __launch_bounds__(kThreads, 2) k_update_tc(const UpdateParams<fl
             }
             float* out = p.An + (int64_t)row * p.lda;
             double sse = s2, ac = 0.0, aa = 0.0, ec = 0.0;
-            float st[SH::LD];
+            float stv[SH::LD];
 #pragma unroll
-            for (int j = 0; j < SH::LD; ++j) st[j] = 0.f;
+            for (int j = 0; j < SH::LD; ++j) stv[j] = 0.f;
 #pragma unroll
             for (int j = 0; j < J; ++j) {
-                st[j] = float(a[j]);
-                const double at = double(st[j]);
+                stv[j] = float(a[j]);
+                const double at = double(stv[j]);
                 sse = fma(-2.0 * at, c[j], sse);
                 ac = fma(a[j], c[j], ac);
                 aa = fma(a[j], a[j], aa);
@@ -379,7 +415,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_update_tc(const UpdateParams<fl
             sse += ac - p.lambda * aa + 2.0 * ec;  // SSE of the stored row (see update.cuh)
 #pragma unroll
             for (int q = 0; q < SH::NQ; ++q)
-                reinterpret_cast<float4*>(out)[q] = make_float4(st[4 * q], st[4 * q + 1], st[4 * q + 2], st[4 * q + 3]);
+                reinterpret_cast<float4*>(out)[q] = make_float4(stv[4 * q], stv[4 * q + 1], stv[4 * q + 2], stv[4 * q + 3]);
             p.sse_row[row] = sse;
         } else {
             const int stp = p.lane_pstride[slot];
@@ -400,17 +436,24 @@ template <int J, bool LAST64>
 void launch_tc(const void* params, bool literal, int grid, cudaStream_t st) {
     (void)literal;
     const UpdateParams<float>& p = *reinterpret_cast<const UpdateParams<float>*>(params);
-    auto k = k_update_tc<J, LAST64>;
-    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, Shape<J>::SMEM);
-    cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
-    k<<<grid, kThreads, Shape<J>::SMEM, st>>>(p);
+    if (p.l0_group == 2 && LAST64) {
+        auto k = k_update_tc<J, LAST64, 2>;
+        cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, Shape<J>::SMEM);
+        cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+        k<<<grid, kThreads, Shape<J>::SMEM, st>>>(p);
+    } else {
+        auto k = k_update_tc<J, LAST64, 1>;
+        cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, Shape<J>::SMEM);
+        cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+        k<<<grid, kThreads, Shape<J>::SMEM, st>>>(p);
+    }
 }
 
 template <int J, bool LAST64>
 int occupancy_tc(bool literal, size_t gp_bytes) {
     (void)literal;
     (void)gp_bytes;
-    auto k = k_update_tc<J, LAST64>;
+    auto k = k_update_tc<J, LAST64, 1>;
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, Shape<J>::SMEM);
     cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
     // Resident CTAs per SM from the kernel's own resource use (the occupancy API
@@ -442,6 +485,27 @@ namespace {
 const UpdateKernel kTcTable[] = {PT_TC_J_LIST(PT_TC_ENTRY)};
 #undef PT_TC_ENTRY
 }  // namespace
+
+// Host: tf32 hi/lo split of the innermost factor (rows of KP floats) for the A operand.
+int tc_kp(int J) {
+    switch (J) {
+        case 2: return tc::Shape<2>::KP;
+        case 3: return tc::Shape<3>::KP;
+        case 4: return tc::Shape<4>::KP;
+        case 5: return tc::Shape<5>::KP;
+        case 8: return tc::Shape<8>::KP;
+        case 10: return tc::Shape<10>::KP;
+    }
+    return 0;
+}
+
+void launch_tc_split(const float* A, int64_t I, int lda, int J, float* hi, float* lo, cudaStream_t st) {
+    const int KP = tc_kp(J);
+    const int64_t total = I * KP;
+    int grid = (int)((total + 255) / 256);
+    if (grid > 148 * 16) grid = 148 * 16;
+    tc::k_split_tf32<<<grid, 256, 0, st>>>(A, I, lda, J, KP, hi, lo);
+}
 
 const UpdateKernel* find_update_kernel_tc(int l64, int J) {
     const int want = l64 > 0 ? 1 : 0;

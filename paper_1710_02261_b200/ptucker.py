@@ -44,6 +44,7 @@ _SIGS = {
     "ptucker_kernel_stats": (C.c_int, [C.c_char_p, C.POINTER(C.c_double), C.POINTER(C.c_int64)]),
     "ptucker_reset_kernel_stats": (C.c_int, []),
     "ptucker_info": (C.c_int, [C.c_char_p, C.c_int32]),
+    "ptucker_debug_trace": (C.c_int, [C.c_void_p, C.c_int32]),
     "ptucker_synchronize": (C.c_int, []),
     "ptucker_finalize": (C.c_int, []),
 }
@@ -217,6 +218,12 @@ def ptucker_info() -> dict:
     buf = C.create_string_buffer(1 << 16)
     _check(load().ptucker_info(buf, len(buf)))
     return json.loads(buf.value.decode())
+
+
+def ptucker_debug_trace(n: int = 4096) -> np.ndarray:
+    out = np.zeros(n, np.int64)
+    _check(load().ptucker_debug_trace(_ptr(out), n))
+    return out
 
 
 def ptucker_synchronize():
