@@ -295,18 +295,7 @@ int launch_update_kernel(int n, bool literal) {
     }
     g.launches += 1;
     const UpdateKernel* k = literal ? g.kern_alu : g.kern;
-    if (!literal && k != g.kern_alu) {
-        // tensor-core kernel: tf32 hi/lo split of the innermost other factor (A operand)
-        const int inner = n == g.N - 1 ? g.N - 2 : g.N - 1;
-        if (!g.tc_hi) {
-            int64_t imax = 0;
-            for (int m = 0; m < g.N; ++m) imax = std::max(imax, g.dims[m]);
-            CK(g.arena.alloc((void**)&g.tc_hi, (size_t)imax * tc_kp(g.J) * sizeof(float)));
-            CK(g.arena.alloc((void**)&g.tc_lo, (size_t)imax * tc_kp(g.J) * sizeof(float)));
-        }
-        launch_tc_split((const float*)g.A[inner], g.dims[inner], g.lda, g.J, g.tc_hi, g.tc_lo, S());
-        g.launches += 1;
-    }
+
     if (g.prec == PTUCKER_F64) {
         UpdateParams<double> p = make_params<double>(n, literal);
         k->launch(&p, literal, grid, S());

@@ -134,7 +134,7 @@ struct Shape {
     // shared memory map (bytes)
     static constexpr int B_BYTES = NP * KP * 4;                     // one of B_hi / B_lo
     static constexpr int A_BYTES = kThreads * KP * 4;               // one of A_hi / A_lo (per stage)
-    static constexpr int RING_CHUNKS = STAGES * NQ * kThreads;      // the level-0 rows a0
+    static constexpr int RING_CHUNKS = STAGES * 2 * NQ * kThreads;  // the gathered rows a0, a1
     static constexpr int OFF_BHI = 0;
     static constexpr int OFF_BLO = OFF_BHI + B_BYTES;
     static constexpr int OFF_A = OFF_BLO + B_BYTES;                 // [stage][hi,lo]
@@ -174,8 +174,6 @@ __global__ void __launch_bounds__(kThreads, 2) k_update_tc(const UpdateParams<fl
     uint4* ring = reinterpret_cast<uint4*>(sm + SH::OFF_RING);
     uint64_t* mbar = reinterpret_cast<uint64_t*>(sm + SH::OFF_BAR);
     uint32_t* misc = reinterpret_cast<uint32_t*>(sm + SH::OFF_MISC);
-    const float* __restrict__ Ahi_g = reinterpret_cast<const float*>(p.ext0);
-    const float* __restrict__ Alo_g = reinterpret_cast<const float*>(p.ext1);
     const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
 
     // ---- B = core (hi/lo tf32 split), K-major: Bt[(k0, j)][k1] = G'[k0][k1][j] ----
@@ -192,6 +190,12 @@ __global__ void __launch_bounds__(kThreads, 2) k_update_tc(const UpdateParams<fl
                      "n"(SH::TCOLS));
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
     }
+    // K-padding chunks (k >= 4*NQ) of every A tile are zero once and never rewritten
+#pragma unroll
+    for (int st = 0; st < ST * 2; ++st)
+#pragma unroll
+        for (int q = NQ; q < KQ; ++q)
+            *reinterpret_cast<float4*>(sm + SH::OFF_A + st * SH::A_BYTES + kmaj<KP>(t, 4 * q) * 4) = make_float4(0.f, 0.f, 0.f, 0.f);
     if (t == 0) {
         asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(&mbar[0])), "r"(1));
         asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(&mbar[1])), "r"(1));
@@ -208,20 +212,36 @@ __global__ void __launch_bounds__(kThreads, 2) k_update_tc(const UpdateParams<fl
     const uint32_t a_base = smem_u32(sm + SH::OFF_A);
     uint32_t ntile = 0;  // tiles issued so far by this CTA (mbarrier phases, buffer parity)
 
-    auto ring_at = [&](int st, int q) -> uint4* { return ring + (st * NQ + q) * kThreads + t; };
-    // cp.async the entry's level-0 row a0 (ring) and its pre-split A row (hi, lo) into stage st
+    // ring chunk (stage, row k, q) of this thread: k = 0 the level-0 row a0, k = 1 the innermost row a1
+    auto ring_at = [&](int st, int k, int q) -> uint4* { return ring + ((st * 2 + k) * NQ + q) * kThreads + t; };
     auto issue = [&](int st, int c0, int c1) {
         const char* s0 = reinterpret_cast<const char*>(p.A[0] + (int64_t)c0 * p.lda);
+        const char* s1 = reinterpret_cast<const char*>(p.A[1] + (int64_t)c1 * p.lda);
 #pragma unroll
-        for (int q = 0; q < NQ; ++q) cp_async16(ring_at(st, q), s0 + 16 * q);
-        const char* sh = reinterpret_cast<const char*>(Ahi_g + (int64_t)c1 * KP);
-        const char* sl = reinterpret_cast<const char*>(Alo_g + (int64_t)c1 * KP);
+        for (int q = 0; q < NQ; ++q) {
+            cp_async16(ring_at(st, 0, q), s0 + 16 * q);
+            cp_async16(ring_at(st, 1, q), s1 + 16 * q);
+        }
+    };
+    // A row of stage st from the gathered a1: hi = a rounded to tf32 (nearest, ties away:
+    // two integer ops), lo = a - hi (exact; the tensor core truncates it to tf32, an
+    // error <= 2^-23 |a|).  Padding k in [J, 4*NQ) is zero in the padded factor rows.
+    auto build_a = [&](int st) {
         unsigned char* dh = sm + SH::OFF_A + (st * 2 + 0) * SH::A_BYTES;
         unsigned char* dl = sm + SH::OFF_A + (st * 2 + 1) * SH::A_BYTES;
 #pragma unroll
-        for (int q = 0; q < KQ; ++q) {
-            cp_async16(dh + kmaj<KP>(t, 4 * q) * 4, sh + 16 * q);
-            cp_async16(dl + kmaj<KP>(t, 4 * q) * 4, sl + 16 * q);
+        for (int q = 0; q < NQ; ++q) {
+            const uint4 r = *ring_at(st, 1, q);
+            const uint32_t w[4] = {r.x, r.y, r.z, r.w};
+            uint32_t h[4];
+            float l[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                h[u] = (w[u] + 0x1000u) & 0xFFFFE000u;
+                l[u] = __uint_as_float(w[u]) - __uint_as_float(h[u]);
+            }
+            *reinterpret_cast<uint4*>(dh + kmaj<KP>(t, 4 * q) * 4) = make_uint4(h[0], h[1], h[2], h[3]);
+            *reinterpret_cast<float4*>(dl + kmaj<KP>(t, 4 * q) * 4) = make_float4(l[0], l[1], l[2], l[3]);
         }
     };
     // 3xTF32 into TMEM buffer `buf` from A stage `st`: lo*hi, hi*lo, hi*hi (small terms first)
@@ -300,6 +320,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_update_tc(const UpdateParams<fl
             if (iters > 1) issue((st0 + 1) % ST, ca1, cb1);
             cp_async_commit();
             cp_async_wait<1>();
+            build_a(st0);
             arrive_a(st0, ntile & 1);
             for (int e = 0; e < iters; ++e) {
                 const uint32_t tile = ntile + e;
@@ -313,13 +334,14 @@ __global__ void __launch_bounds__(kThreads, 2) k_update_tc(const UpdateParams<fl
                 load_crd(e + 3, ca2, cb2, x2);
                 if (e + 1 < iters) {
                     cp_async_wait<1>();
+                    build_a(rs1);
                     arrive_a(rs1, (tile + 1) & 1);
                 }
                 // ---- epilogue of entry e ----
                 float a0f[J];
 #pragma unroll
                 for (int q = 0; q < NQ; ++q) {
-                    const float4 v = *reinterpret_cast<const float4*>(ring_at(rs, q));
+                    const float4 v = *reinterpret_cast<const float4*>(ring_at(rs, 0, q));
                     const float w[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
                     for (int u = 0; u < 4; ++u)

@@ -32,6 +32,8 @@ __device__ __forceinline__ float to_tf32(float x) {
     return __uint_as_float(r);
 }
 
+__device__ __forceinline__ float trunc_tf32(float x) { return __uint_as_float(__float_as_uint(x) & 0xFFFFE000u); }
+
 __global__ void k_probe(const float* A, const float* B, float* C, int mode) {
     __shared__ __align__(128) float sA_hi[M * K], sA_lo[M * K], sB_hi[NN * K], sB_lo[NN * K];
     __shared__ __align__(8) uint64_t mbar;
@@ -39,16 +41,26 @@ __global__ void k_probe(const float* A, const float* B, float* C, int mode) {
     const int t = threadIdx.x, warp = t / 32, lane = t % 32;
     for (int k = 0; k < K; ++k) {
         float a = A[t * K + k];
-        float h = to_tf32(a);
-        sA_hi[kmaj_off(t, k)] = h;
-        sA_lo[kmaj_off(t, k)] = to_tf32(a - h);
+        if (mode >= 3) {  // raw fp32 as "hi" (the tensor core truncates), lo = a - trunc(a) unrounded
+            sA_hi[kmaj_off(t, k)] = a;
+            sA_lo[kmaj_off(t, k)] = a - trunc_tf32(a);
+        } else {
+            float h = to_tf32(a);
+            sA_hi[kmaj_off(t, k)] = h;
+            sA_lo[kmaj_off(t, k)] = to_tf32(a - h);
+        }
     }
     for (int i = t; i < NN * K; i += blockDim.x) {
         int r = i / K, k = i % K;
         float b = B[r * K + k];
-        float h = to_tf32(b);
-        sB_hi[kmaj_off(r, k)] = h;
-        sB_lo[kmaj_off(r, k)] = to_tf32(b - h);
+        if (mode >= 3) {
+            sB_hi[kmaj_off(r, k)] = b;
+            sB_lo[kmaj_off(r, k)] = b - trunc_tf32(b);
+        } else {
+            float h = to_tf32(b);
+            sB_hi[kmaj_off(r, k)] = h;
+            sB_lo[kmaj_off(r, k)] = to_tf32(b - h);
+        }
     }
     if (warp == 0) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&tmem_base)), "r"(128));
@@ -67,7 +79,7 @@ __global__ void k_probe(const float* A, const float* B, float* C, int mode) {
         const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(NN >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
         const float* As[4] = {sA_lo, sA_hi, sA_lo, sA_hi};
         const float* Bs[4] = {sB_lo, sB_lo, sB_hi, sB_hi};
-        const int first = mode == 0 ? 3 : (mode == 1 ? 1 : 0);
+        const int first = mode == 0 ? 3 : (mode == 1 || mode == 3 ? 1 : 0);
         const int nprod = 4;
         int issued = 0;
         for (int p = first; p < nprod; ++p)
@@ -118,7 +130,7 @@ int main() {
     cudaMalloc(&dA, A.size() * 4); cudaMalloc(&dB, B.size() * 4); cudaMalloc(&dC, C.size() * 4);
     cudaMemcpy(dA, A.data(), A.size() * 4, cudaMemcpyHostToDevice);
     cudaMemcpy(dB, B.data(), B.size() * 4, cudaMemcpyHostToDevice);
-    for (int mode = 0; mode < 3; ++mode) {
+    for (int mode = 0; mode < 4; ++mode) {
         cudaMemset(dC, 0, C.size() * 4);
         k_probe<<<1, 128>>>(dA, dB, dC, mode);
         cudaError_t e = cudaDeviceSynchronize();
@@ -133,7 +145,7 @@ int main() {
                 fp32max = fmax(fp32max, fabs(f32 - ref) / fabs(ref));
             }
         printf("mode %s: max rel err vs fp64 %.3e (sequential fp32 FMA: %.3e); C[0]=%g C[last]=%g\n",
-               mode == 2 ? "4xTF32 small-first" : (mode ? "3xTF32 small-first" : "1xTF32"), maxrel, fp32max, C[0], C[M * NN - 1]);
+               mode == 3 ? "3xTF32 raw-hi/trunc small-first" : (mode == 2 ? "4xTF32 small-first" : (mode ? "3xTF32 small-first" : "1xTF32")), maxrel, fp32max, C[0], C[M * NN - 1]);
     }
     return 0;
 }
