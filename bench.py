@@ -349,7 +349,7 @@ def main():
     ap.add_argument("--policy", default="auto", choices=list(POLICY))
     ap.add_argument("--seg-len", type=int, default=256)
     ap.add_argument("--tc", type=int, default=1, choices=[0, 1], help="tensor-core inner stage for order-3 fp32")
-    ap.add_argument("--l0-group", type=int, default=1, choices=[1, 2], help="tensor-core level-0 fp32 pairing")
+    ap.add_argument("--l0-group", type=int, default=1, choices=[1, 2, 5], help="tensor-core level-0 grouping (1 = fp64 per term, g = fp32 partial sums of g terms)")
     ap.add_argument("--ref-seconds", type=float, default=12.0)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")

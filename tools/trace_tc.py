@@ -1,8 +1,11 @@
 """Per-phase clock trace of the tensor-core update kernel (CTA 0, lane 0 of each of its
-4 warps, first 64 entries of its first slice group).  Phases per entry:
-0 start, 1 after cp.async issue + coordinate loads, 2 after cp.async wait, 3 after
-building the next A tile, 4 after arriving (MMA issued by the last arriver),
-5 after waiting for this entry's MMA, 6 after TMEM loads + level 0, 7 after B/c."""
+4 warps, tiles 64..127 of its sequence).  Phases per tile k:
+0 start, 1 after the cp.async issue step (coordinates k+7, rows k+3), 2 after the
+cp.async wait for the rows of k+1, 3 after splitting them into the A tile, 4 after
+arriving (MMA issued by the last arriver), 5 after waiting for tile k's MMA,
+6 after TMEM loads + level 0, 7 after B/c.
+
+    python tools/trace_tc.py [scale] [l0_group]"""
 import sys
 import numpy as np
 import torch
@@ -14,12 +17,14 @@ torch.cuda.set_device(0)
 cfg = synth.small("c5", float(sys.argv[1]) if len(sys.argv) > 1 else 0.1)
 coords, vals = synth.generate(cfg)
 pt.ptucker_init(coords, vals, cfg.dims, [10] * 3, cfg.lam, 0)
+if len(sys.argv) > 2:
+    pt.ptucker_set_option("l0_group", int(sys.argv[2]))
 pt.ptucker_update_mode(0)
 pt.ptucker_set_option("trace", 1)
 pt.ptucker_update_mode(1)
 pt.ptucker_synchronize()
 tr = pt.ptucker_debug_trace(4 * 512).reshape(4, 64, 8)
-names = ["issue/coords", "cp.wait", "build A", "arrive", "mma wait", "tmem+L0", "B/c", "->next"]
+names = ["issue", "cp.wait", "split", "arrive", "mma wait", "tmem+L0", "B/c", "->next"]
 for w in range(4):
     t = tr[w]
     ok = t[:, 0] > 0
