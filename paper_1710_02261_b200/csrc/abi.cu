@@ -475,6 +475,10 @@ int ptucker_set_option(const char* key, int64_t value) {
         if (value) {
             if (!g.trace) CK(cudaMalloc((void**)&g.trace, 8 * 512 * sizeof(long long)));
             CK(cudaMemset(g.trace, 0, 8 * 512 * sizeof(long long)));
+            if (value == 2) {  // tensor-core kernel: the MMA warp also waits for each traced tile (latency probe)
+                const long long one = 1;
+                CK(cudaMemcpy(g.trace + 8 * 512 - 1, &one, sizeof(one), cudaMemcpyHostToDevice));
+            }
         } else if (g.trace) {
             cudaFree(g.trace);
             g.trace = nullptr;

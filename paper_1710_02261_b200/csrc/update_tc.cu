@@ -4,33 +4,36 @@
 //
 // For mode n with other modes m0 < m1, Eq. 12 regrouped as a TTV
 // chain is   delta(j) = sum_k0 a0[k0] * t[k0][j],   t[k0][j] = sum_k1 a1[k1] G'[k0][k1][j].
-// The inner stage, over the 128 entries a CTA holds at a time ("tile"), is a
-// dense GEMM
+// The inner stage, over 128 entries at a time ("tile"), is a dense GEMM
 //     T (128 x J^2) = A1 (128 x J) * Bt^T,   Bt[(k0,j)][k1] = G'[k0][k1][j],
 // with B = the core, shared by every entry.  It runs as 3xTF32 (a = a_hi + a_lo,
 // small products first: lo*hi, hi*lo, hi*hi) so its accuracy matches an fp32
 // FMA chain (tools/tc_probe.cu), accumulating in TMEM.
 //
-// CTA = 4 warps, two CTAs per SM (255 registers per thread; TMEM columns
-// [0, TCOLS) of each CTA hold two accumulator buffers).  Thread t owns TMEM lane
-// t and row segment t of the current group of 4 SELL-32 slices,
-// and streams its own entries through two per-thread cp.async rings in shared
-// memory: the coordinates/value kCPref tiles ahead, the two gathered factor
-// rows kRPref tiles ahead (no cross-thread handshake: each thread reads only
-// what it fetched).  Per tile k a thread
-//   (a) splits its gathered a1 row of tile k+1 into tf32 hi/lo rows of the A
-//       operand; the last of the 4 warps to do so issues that tile's MMAs
-//       (double-buffered A stages and TMEM accumulators), so the MMA of tile
-//       k+1 runs while
-//   (b) the epilogue of tile k reads t[k0][j] from TMEM, finishes level 0 in
-//       fp64 (F32-B), accumulates B += delta delta^T, c += x delta, sum x^2
-//       (fp64, Eq. 10-11), and at the end of the segment solves
-//       a = c [B + lambda I]^-1 (Cholesky, Eq. 9) and stores the row with its
-//       SSE (fused Eq. 5).
-// Groups are assigned statically (serpentine over the CTAs; SELL groups are
-// sorted by length, so neighbouring CTAs get near-equal work), so every thread
-// knows its whole tile sequence and the rings run ahead across group
-// boundaries.
+// One CTA per SM runs two independent pipelines h = 0, 1 (12 warps):
+//   warps 4h..4h+3  EPILOGUE (128 threads; 224 registers via setmaxnreg): thread
+//                   t owns TMEM lane t and row segment t of the pipeline's current
+//                   group of 4 SELL-32 slices.  Per tile it reads
+//                   t[k0][j] from TMEM, finishes level 0 (fp64 per term, or fp32
+//                   partial sums of G0 terms added in fp64), accumulates
+//                   B += delta delta^T, c += x delta, sum x^2 in fp64 registers
+//                   (Eq. 10-11) and at the end of the segment solves
+//                   a = c [B + lambda I]^-1 (Cholesky, Eq. 9) and stores the row
+//                   with its SSE (fused Eq. 5).
+//   warp 8+h        LOADER: streams the SELL coordinates/values of the pipeline's
+//                   tiles into a coordinate ring (cp.async, kCPref tiles ahead)
+//                   and gathers the two factor rows of every entry into a
+//                   kRing-slot row ring (cp.async; mbarrier full/empty).
+//   warp 10+h       MMA: lane 0 issues a tile's MMAs into one of two TMEM
+//                   accumulators once the epilogue warps have written its A rows.
+// Before the epilogue of tile k, each epilogue thread splits its own gathered a1
+// row of tile k+1 into tf32 hi/lo rows of the A operand (double-buffered stage),
+// so the MMA of tile k+1 overlaps the epilogue of tile k.  The epilogue warps
+// touch no global memory inside the tile loop: the loads and every
+// long-latency wait live in the helper warps.
+// Groups are assigned statically (serpentine over the 2 x #CTA pipelines; SELL
+// groups are sorted by length, so neighbouring pipelines get near-equal work),
+// so every role knows the pipeline's whole tile sequence in advance.
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -43,12 +46,19 @@
 namespace pt {
 namespace tc {
 
-constexpr int kThreads = 128;  // = TMEM lanes = segments per group (4 SELL slices)
-constexpr int kCPref = 7;      // coordinates fetched this many tiles ahead of their epilogue
-constexpr int kCRing = 8;      // coordinate ring slots (> kCPref)
-constexpr int kRPref = 3;      // factor rows gathered this many tiles ahead
-constexpr int kRRing = 4;      // row ring slots (> kRPref)
-static_assert(kCRing > kCPref && kRRing > kRPref && kCPref > 2 * kRPref - 1, "ring depths");
+constexpr int kE = 128;                      // epilogue threads of a pipeline = TMEM lanes = segments per group
+constexpr int kPipes = 2;                    // pipelines per CTA (one CTA per SM)
+constexpr int kThreads = kPipes * kE + 4 * kWarp;  // + loader and MMA warps of both pipelines
+constexpr int kRing = 6;                     // row ring slots (tiles in flight between loader and epilogue)
+constexpr int kCPref = 7;                    // loader: coordinates fetched this many tiles ahead of the gathers
+constexpr int kCRing = 8;                    // coordinate ring slots (> kCPref)
+constexpr int kRegLaunch = 65536 / kThreads / 8 * 8;  // registers per thread at launch (168)
+constexpr int kRegE = 232;                   // setmaxnreg: epilogue warpgroups
+constexpr int kRegP = 40;                    //             loader/MMA warpgroup
+static_assert(kCRing > kCPref, "ring depths");
+// setmaxnreg moves registers inside the CTA's launch allocation: the epilogue's
+// increase must be covered by the helpers' release, or it waits forever
+static_assert(2 * 4 * kWarp * kRegE + 4 * kWarp * kRegP <= kRegLaunch * kThreads, "register pool");
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 
@@ -78,6 +88,27 @@ __device__ __forceinline__ void mma_tf32(uint32_t tmem_d, uint64_t da, uint64_t 
         "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
         "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(tmem_d),
         "l"(da), "l"(db), "r"(idesc), "r"(acc));
+}
+
+// A operand in tensor memory (lane = row, K along columns), B from shared memory
+__device__ __forceinline__ void mma_tf32_ta(uint32_t tmem_d, uint32_t tmem_a, uint64_t db, uint32_t idesc, uint32_t acc) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n\t}\n" ::"r"(tmem_d),
+        "r"(tmem_a), "l"(db), "r"(idesc), "r"(acc));
+}
+__device__ __forceinline__ void tmem_st16(uint32_t addr, const uint32_t (&r)[16]) {
+    asm volatile(
+        "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(addr),
+        "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]), "r"(r[9]),
+        "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15])
+        : "memory");
+}
+
+__device__ __forceinline__ void tmem_st8(uint32_t addr, const uint32_t (&r)[16]) {
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(addr), "r"(r[0]), "r"(r[1]),
+                 "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7])
+                 : "memory");
 }
 
 __device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
@@ -146,24 +177,27 @@ struct Shape {
     static constexpr int KP = (J + 7) / 8 * 8;             // K padded to the tf32 MMA K-step (8)
     static constexpr int KSTEPS = KP / 8;
     static constexpr int NP = (J * J + 15) / 16 * 16;      // N padded to 16 (M = 128)
-    static constexpr int TCOLS = 2 * NP <= 32 ? 32 : (2 * NP <= 64 ? 64 : (2 * NP <= 128 ? 128 : (2 * NP <= 256 ? 256 : 512)));
+    static constexpr int ACOL = 2 * NP;                     // TMEM: T buffers [0, 2NP), A_hi [ACOL, +KP), A_lo [ACOL+KP, +KP)
+    static constexpr int TCOLS = ACOL + 2 * KP <= 32 ? 32 : (ACOL + 2 * KP <= 64 ? 64 : (ACOL + 2 * KP <= 128 ? 128 : 256));
     static constexpr int LD = factor_ld(J, 4);             // padded factor row (floats)
     static constexpr int NQ = LD / 4;                       // 16-byte chunks per factor row
     static constexpr int KQ = KP / 4;                       // 16-byte chunks per A row
     static constexpr int NCH = (J * J + 15) / 16;           // 16-column TMEM chunks holding t
     // shared memory map (bytes)
     static constexpr int B_BYTES = NP * KP * 4;             // one of B_hi / B_lo
-    static constexpr int A_BYTES = kThreads * KP * 4;       // one of A_hi / A_lo (per stage)
-    static constexpr int CSLOT = 3 * kThreads * 4;          // coordinate ring slot: c0[128], c1[128], x[128]
-    static constexpr int RSLOT = 2 * NQ * kThreads * 16;    // row ring slot: a0, a1 rows, chunk-major
+    static constexpr int RSLOT = 2 * NQ * kE * 16 + kE * 4; // row ring slot: rows a0, a1 (chunk-major), x
+    static constexpr int CSLOT = 3 * kE * 4;                // coordinate ring slot: c0, c1, x
     static constexpr int OFF_BHI = 0;
     static constexpr int OFF_BLO = OFF_BHI + B_BYTES;
-    static constexpr int OFF_A = OFF_BLO + B_BYTES;         // [stage 0,1][hi,lo]
-    static constexpr int OFF_CRD = OFF_A + 2 * 2 * A_BYTES;
-    static constexpr int OFF_ROW = OFF_CRD + kCRing * CSLOT;
-    static constexpr int OFF_BAR = OFF_ROW + kRRing * RSLOT;  // acc_full[2]
-    static constexpr int OFF_MISC = OFF_BAR + 2 * 8;          // tmem base, A-stage arrival counters[2], tiles
-    static constexpr int SMEM = OFF_MISC + 16;
+    static constexpr int OFF_MISC = OFF_BLO + B_BYTES;      // tmem base, tiles per pipeline
+    static constexpr int OFF_PIPE = (OFF_MISC + 64 + 127) / 128 * 128;
+    // per pipeline, at OFF_PIPE + h * PIPE_BYTES
+    static constexpr int P_ROW = 0;
+    static constexpr int P_CRD = P_ROW + kRing * RSLOT;
+    static constexpr int P_BAR = P_CRD + kCRing * CSLOT;    // raw_full[kRing], raw_empty[kRing], acc_full[2], acc_empty[2], a_full
+    static constexpr int PIPE_BYTES = (P_BAR + (2 * kRing + 5) * 8 + 127) / 128 * 128;
+    static constexpr int SMEM = OFF_PIPE + kPipes * PIPE_BYTES;
+    static_assert(kPipes * TCOLS <= 512 && ACOL + 2 * KP <= TCOLS, "TMEM columns");
 };
 
 // Split of the innermost factor into tf32 hi/lo parts (3xTF32 operand), K-padded
@@ -181,36 +215,32 @@ __global__ void k_split_tf32(const float* __restrict__ A, int64_t I, int lda, in
     }
 }
 
-// Static serpentine assignment of groups (4 slices each) to CTAs.
+// Static serpentine assignment of groups (4 slices each) to pipelines.
 struct Sched {
-    int64_t ngroups, r;
+    int ngroups, r;
     int G, b;
-    __device__ int64_t group() const { return r * G + ((r & 1) ? (G - 1 - b) : b); }
+    __device__ int group() const { return r * G + ((r & 1) ? (G - 1 - b) : b); }
     __device__ bool valid() const { return group() < ngroups; }
 };
 
-// Segment data of the current group for one thread.
+// Segment data of the current group for one epilogue thread.
 struct Seg {
     int iters;     // tiles of the group (longest slice = its first)
     int row, len;  // segment row (-1: pad lane) and length
-    int64_t slot;  // SELL lane slot (partials)
+    int slot;      // SELL lane slot (partials)
 };
 
-// This thread's slice of a group, for the coordinate cursor.
-struct SliceMeta {
-    int iters, slen;
-    int64_t off;
-    bool valid;
-};
+__device__ __forceinline__ void setmaxnreg_inc() { asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(kRegE)); }
+__device__ __forceinline__ void setmaxnreg_dec() { asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(kRegP)); }
 
 // G0 (level-0 grouping, LAST64 only): 1 = every a0[k0] t[k0][j] product and the sum
 // in fp64 (F32-B); g > 1 = partial sums over runs of g consecutive k0 in fp32
 // (one rounded product, then FMAs), each partial converted to fp64 once and the
-// partials summed in fp64: ceil(J/g) instead of J^2 fp32->fp64 conversions per
+// partials summed in fp64: J*ceil(J/g) instead of J^2 fp32->fp64 conversions per
 // entry (F2F runs on the quarter-rate XU pipe; tools/level0_emulation.py measures
 // the row error of each g).
 template <int J, bool LAST64, int G0>
-__global__ void __launch_bounds__(kThreads, 2) k_update_tc(const UpdateParams<float> p) {
+__global__ void __launch_bounds__(kThreads, 1) k_update_tc(const UpdateParams<float> p) {
     using SH = Shape<J>;
     constexpr int KP = SH::KP, NP = SH::NP, NQ = SH::NQ, KQ = SH::KQ;
     constexpr int NB = J * (J + 1) / 2;
@@ -220,45 +250,50 @@ __global__ void __launch_bounds__(kThreads, 2) k_update_tc(const UpdateParams<fl
     float* sBhi = reinterpret_cast<float*>(sm + SH::OFF_BHI);
     float* sBlo = reinterpret_cast<float*>(sm + SH::OFF_BLO);
     uint32_t* misc = reinterpret_cast<uint32_t*>(sm + SH::OFF_MISC);
-    const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
-    const uint32_t bar0 = smem_u32(sm + SH::OFF_BAR);
-    auto acc_bar = [&](int b) { return bar0 + 8u * b; };
-    // coordinate ring slot s: c0, c1, x of this thread's entry
-    auto crd = [&](int s, int a) -> uint32_t* {
-        return reinterpret_cast<uint32_t*>(sm + SH::OFF_CRD + s * SH::CSLOT) + a * kThreads + t;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    // role: 0 epilogue (warps 0-7), 1 loader (8, 9), 2 MMA issue (10, 11)
+    const int role = warp < 4 * kPipes ? 0 : (warp < 4 * kPipes + 2 ? 1 : 2);
+    const int h = role == 0 ? (warp >> 2) : (warp & 1);
+    unsigned char* pipe = sm + SH::OFF_PIPE + h * SH::PIPE_BYTES;
+    const uint32_t bar0 = smem_u32(pipe + SH::P_BAR);
+    auto raw_full = [&](int s) { return bar0 + 8u * s; };
+    auto raw_empty = [&](int s) { return bar0 + 8u * (kRing + s); };
+    auto acc_full = [&](int b) { return bar0 + 8u * (2 * kRing + b); };
+    auto acc_empty = [&](int b) { return bar0 + 8u * (2 * kRing + 2 + b); };
+    const uint32_t a_full = bar0 + 8u * (2 * kRing + 4);  // single A buffer (TMEM)
+    // row ring slot s: chunk q of row k (0: a0, 1: a1) of segment u; x of segment u
+    auto rowc = [&](int s, int k, int q, int u) -> uint4* {
+        return reinterpret_cast<uint4*>(pipe + SH::P_ROW + s * SH::RSLOT) + ((k * NQ + q) * kE + u);
     };
-    // row ring slot s: chunk q of row k (0: a0, 1: a1) of this thread's entry
-    auto rowc = [&](int s, int k, int q) -> uint4* {
-        return reinterpret_cast<uint4*>(sm + SH::OFF_ROW + s * SH::RSLOT) + ((k * NQ + q) * kThreads + t);
+    auto rowx = [&](int s, int u) -> float* {
+        return reinterpret_cast<float*>(pipe + SH::P_ROW + s * SH::RSLOT + 2 * NQ * kE * 16) + u;
     };
+    // coordinate ring slot s: c0, c1, x (a = 0, 1, 2) of segment u
+    auto crd = [&](int s, int a, int u) -> uint32_t* {
+        return reinterpret_cast<uint32_t*>(pipe + SH::P_CRD + s * SH::CSLOT) + a * kE + u;
+    };
+    const int ngroups = (int)((p.nslices + 3) / 4);  // nslices * 32 < 2^31 (nnz <= INT32_MAX)
+    const Sched s0{ngroups, 0, kPipes * (int)gridDim.x, kPipes * (int)blockIdx.x + h};
 
-    // ---- B = core (hi/lo tf32 split), K-major: Bt[(k0, j)][k1] = G'[k0][k1][j] ----
-    for (int i = t; i < NP * KP; i += kThreads) {
+    // ---------------------------------------------------------------- setup
+    // B = core (hi/lo tf32 split), K-major: Bt[(k0, j)][k1] = G'[k0][k1][j]
+    for (int i = threadIdx.x; i < NP * KP; i += kThreads) {
         const int c = i / KP, k1 = i % KP;
         float v = 0.f;
         if (c < J * J && k1 < J) v = p.Gp[(c / J) * GB + k1 * J + (c % J)];
-        const float h = tf32_rna(v);
-        sBhi[kmaj<KP>(c, k1)] = h;
-        sBlo[kmaj<KP>(c, k1)] = tf32_rna(v - h);
+        const float hv = tf32_rna(v);
+        sBhi[kmaj<KP>(c, k1)] = hv;
+        sBlo[kmaj<KP>(c, k1)] = tf32_rna(v - hv);
     }
     if (warp == 0) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&misc[0])),
-                     "n"(SH::TCOLS));
+                     "n"(kPipes * SH::TCOLS));
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
     }
-    // K-padding chunks (k >= 4*NQ) of every A tile are zero once and never rewritten
-#pragma unroll
-    for (int st = 0; st < 4; ++st)
-#pragma unroll
-        for (int q = NQ; q < KQ; ++q)
-            *reinterpret_cast<float4*>(sm + SH::OFF_A + st * SH::A_BYTES + kmaj<KP>(t, 4 * q) * 4) =
-                make_float4(0.f, 0.f, 0.f, 0.f);
-    const int64_t ngroups = (p.nslices + 3) / 4;
-    const Sched s0{ngroups, 0, (int)gridDim.x, (int)blockIdx.x};
-    if (warp == 1) {
-        // tiles of this CTA = sum of the iteration counts of its groups
+    if (role == 1) {
+        // tiles of this pipeline = sum of the iteration counts of its groups
         uint32_t n = 0;
-        for (int64_t r = lane;; r += kWarp) {
+        for (int r = lane;; r += kWarp) {
             Sched q = s0;
             q.r = r;
             if (!q.valid()) break;
@@ -266,281 +301,319 @@ __global__ void __launch_bounds__(kThreads, 2) k_update_tc(const UpdateParams<fl
         }
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) n += __shfl_xor_sync(0xffffffffu, n, o);
-        if (lane == 0) misc[3] = n;
-    }
-    if (t == 0) {
-        mbar_init(acc_bar(0), 1);
-        mbar_init(acc_bar(1), 1);
-        misc[1] = misc[2] = 0;  // arrival counters of the two A stages
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        if (lane == 0) {
+            misc[2 + h] = n;
+            for (int s = 0; s < kRing; ++s) {
+                mbar_init(raw_full(s), 2 * kWarp);  // loader lanes: cp.async completion + plain arrive (x)
+                mbar_init(raw_empty(s), 4);         // the 4 epilogue warps
+            }
+            for (int b = 0; b < 2; ++b) {
+                mbar_init(acc_full(b), 1);   // tcgen05.commit
+                mbar_init(acc_empty(b), 4);  // epilogue warps done reading the TMEM buffer
+            }
+            mbar_init(a_full, 4);            // epilogue warps wrote their A rows (TMEM)
+            asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        }
     }
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     __syncthreads();
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-    const uint32_t tmem = misc[0];
-    const uint32_t total = misc[3];
+    const uint32_t tmem = misc[0] + h * SH::TCOLS;
+    const uint32_t total = misc[2 + h];
 
-    // ------------------------------------------------------------------
-    // Coordinate cursor: walks this thread's entries kCPref tiles ahead of
-    // the epilogue and cp.asyncs c0, c1, x into the coordinate ring.
-    // ------------------------------------------------------------------
-    auto load_meta = [&](const Sched& q, SliceMeta& m) {
-        m.valid = q.valid();
-        if (!m.valid) return;
-        const int64_t g0 = q.group() * 4, sl = g0 + warp;
-        const bool v = sl < p.nslices;
-        m.iters = __ldg(p.slice_len + g0);
-        m.slen = v ? __ldg(p.slice_len + sl) : 0;
-        m.off = v ? __ldg(p.slice_off + sl) + lane : 0;
-    };
-    Sched cs = s0;
-    SliceMeta cm, cn;  // cursor group, next group
-    load_meta(cs, cm);
-    {
-        Sched q = cs;
-        ++q.r;
-        load_meta(q, cn);
-    }
-    int ce = 0;
-    bool cend = !cm.valid || cm.iters == 0;
-    const uint64_t pol_stream = policy_evict_first(), pol_rows = policy_evict_last();
-    uint32_t ck = 0;  // tile index of the cursor
-    auto issue_crd = [&]() {
-        if (cend) return;
-        const int s = (int)(ck % kCRing);
-        const bool v = ce < cm.slen;
-        const int64_t idx = cm.off + (int64_t)ce * kWarp;
-        if (v) {
-            cp_async4_hint(crd(s, 0), p.sc[0] + idx, pol_stream);
-            cp_async4_hint(crd(s, 1), p.sc[1] + idx, pol_stream);
-            cp_async4_hint(crd(s, 2), p.sv + idx, pol_stream);
-        } else {
-            *crd(s, 0) = 0u;  // padding entry: gather row 0 (its result is masked)
-            *crd(s, 1) = 0u;
-        }
-        ++ck;
-        if (++ce == cm.iters) {
-            ce = 0;
-            if (!cn.valid || cn.iters == 0) {
-                cend = true;  // groups are sorted by length: nothing follows an empty group
-            } else {
-                cm = cn;
-                ++cs.r;
-                Sched q = cs;
-                ++q.r;
-                load_meta(q, cn);
+    if (role == 1) {
+        // ======================================================== loader
+        setmaxnreg_dec();
+        const uint64_t pol_stream = policy_evict_first(), pol_rows = policy_evict_last();
+        // coordinate cursor (tile kc): this lane's 4 segments u = lane + 32 i, i = slice of the group
+        Sched pc = s0;
+        int pe = 0, piters = 0, plen[4];
+        int64_t poff[4];
+        bool pend = total == 0;
+        auto load_group = [&]() {
+            const int64_t g0 = pc.group() * 4;
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                const bool v = g0 + i < p.nslices;
+                plen[i] = v ? __ldg(p.slice_len + g0 + i) : 0;
+                poff[i] = v ? __ldg(p.slice_off + g0 + i) + lane : 0;
             }
-        }
-    };
-    // rows of tile k (its coordinates have landed): cp.async a0, a1 into row slot k % kRRing
-    auto issue_rows = [&](uint32_t k) {
-        const int s = (int)(k % kRRing), cslot = (int)(k % kCRing);
-        const int c0 = (int)*crd(cslot, 0), c1 = (int)*crd(cslot, 1);
-        const char* r0 = reinterpret_cast<const char*>(p.A[0] + (int64_t)c0 * p.lda);
-        const char* r1 = reinterpret_cast<const char*>(p.A[1] + (int64_t)c1 * p.lda);
+            piters = plen[0];
+            pe = 0;
+            if (piters == 0) pend = true;  // groups are sorted by length: nothing follows an empty group
+        };
+        if (!pend) load_group();
+        uint32_t kc = 0;
+        auto issue_crd = [&]() {
+            if (pend) return;
+            const int s = (int)(kc % kCRing);
 #pragma unroll
-        for (int q = 0; q < NQ; ++q) {
-            cp_async16_hint(rowc(s, 0, q), r0 + 16 * q, pol_rows);
-            cp_async16_hint(rowc(s, 1, q), r1 + 16 * q, pol_rows);
-        }
-    };
-    // Step s (s = -kCPref .. total-1): coordinates of tile s+kCPref, rows of tile
-    // s+kRPref, one cp.async group per step (groups are numbered by step).
-    auto step = [&](int s) {
-        issue_crd();
-        const int kr = s + kRPref;
-        // coordinates of tile kr were committed at step kr - kCPref
-        cp_async_wait<kCPref - kRPref - 1>();
-        if (kr >= 0 && kr < (int)total) issue_rows((uint32_t)kr);
-        cp_async_commit();
-    };
-
-    const uint32_t idesc =
-        (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(NP >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
-    const uint32_t bhi = smem_u32(sBhi), blo = smem_u32(sBlo);
-    const uint32_t a_base = smem_u32(sm + SH::OFF_A);
-    const uint32_t tm_lane = tmem + ((uint32_t)(warp * 32) << 16);
-
-    // 3xTF32 into TMEM buffer `buf` from A stage `buf`: lo*hi, hi*lo, hi*hi (small terms first)
-    auto issue_mma = [&](int buf) {
-        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-        const uint32_t ahi = a_base + (buf * 2 + 0) * SH::A_BYTES, alo = a_base + (buf * 2 + 1) * SH::A_BYTES;
-        const uint32_t d = tmem + buf * NP;
-        const uint32_t as[3] = {alo, ahi, ahi}, bs[3] = {bhi, blo, bhi};
-        uint32_t acc = 0;
-#pragma unroll
-        for (int pr = 0; pr < 3; ++pr)
-#pragma unroll
-            for (int ks = 0; ks < SH::KSTEPS; ++ks) {
-                // LBO: next 16-byte K chunk = next core matrix (128 B); SBO: next 8 rows
-                mma_tf32(d, umma_desc(as[pr] + ks * 256, 128, KP * 32), umma_desc(bs[pr] + ks * 256, 128, KP * 32),
-                         idesc, acc);
-                acc = 1;
-            }
-        asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(acc_bar(buf))
-                     : "memory");
-    };
-    // Tile k (its rows have landed): write this thread's A row of stage k&1
-    // (hi = a rounded to tf32 by two integer ops, lo = a - hi exact; the tensor
-    // core truncates lo to tf32, an error <= 2^-23 |a|), make it visible to the
-    // async proxy and count the arrival (one per warp); the lane 0 of the LAST
-    // warp issues the MMAs (acq_rel atomic: it observes every row and every
-    // completed tcgen05.ld of the TMEM buffer it overwrites).
-    auto prepare = [&](uint32_t k, auto&& after_split) {
-        const int s = (int)(k % kRRing), st = (int)(k & 1);
-        unsigned char* dh = sm + SH::OFF_A + (st * 2 + 0) * SH::A_BYTES;
-        unsigned char* dl = sm + SH::OFF_A + (st * 2 + 1) * SH::A_BYTES;
-#pragma unroll
-        for (int q = 0; q < NQ; ++q) {
-            const uint4 r = *rowc(s, 1, q);
-            const uint32_t w[4] = {r.x, r.y, r.z, r.w};
-            uint32_t h[4];
-            float l[4];
-#pragma unroll
-            for (int u = 0; u < 4; ++u) {
-                h[u] = (w[u] + 0x1000u) & 0xFFFFE000u;
-                l[u] = __uint_as_float(w[u]) - __uint_as_float(h[u]);
-            }
-            *reinterpret_cast<uint4*>(dh + kmaj<KP>(t, 4 * q) * 4) = make_uint4(h[0], h[1], h[2], h[3]);
-            *reinterpret_cast<float4*>(dl + kmaj<KP>(t, 4 * q) * 4) = make_float4(l[0], l[1], l[2], l[3]);
-        }
-        after_split();
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-        __syncwarp();
-        // one arrival per warp (its lanes are ordered before lane 0 by the warp barrier)
-        if (lane == 0) {
-            uint32_t old;
-            asm volatile("atom.acq_rel.cta.shared::cta.add.u32 %0, [%1], 1;"
-                         : "=r"(old)
-                         : "r"(smem_u32(&misc[1 + st]))
-                         : "memory");
-            if (old == kThreads / kWarp - 1) {
-                misc[1 + st] = 0;
-                issue_mma(st);
-            }
-        }
-    };
-    auto load_seg = [&](const Sched& s, Seg& g) {
-        const int64_t g0 = s.group() * 4;
-        const int64_t sl = g0 + warp;
-        g.slot = sl * kWarp + lane;
-        const bool v = sl < p.nslices;
-        g.iters = __ldg(p.slice_len + g0);
-        g.row = v ? __ldg(p.lane_row + g.slot) : -1;
-        g.len = v ? __ldg(p.lane_len + g.slot) : 0;
-    };
-    double B[NB], c[J], s2;
-    auto zero = [&]() {
-#pragma unroll
-        for (int q = 0; q < NB; ++q) B[q] = 0.0;
-#pragma unroll
-        for (int q = 0; q < J; ++q) c[q] = 0.0;
-        s2 = 0.0;
-    };
-    // end of a segment: solve and store (Eq. 9 + fused Eq. 5), or write the heavy-row partial
-    auto finalize = [&](const Seg& g) {
-        if (g.row < 0) return;
-        const int64_t pidx = p.lane_pidx[g.slot];
-        if (pidx < 0) {
-            double a[J];
-            const bool ok = chol_solve<J>(B, c, p.lambda, a);
-            if (!ok) {
-                atomicCAS(p.fail, 0, g.row + 1);
-#pragma unroll
-                for (int j = 0; j < J; ++j) a[j] = 0.0;
-            }
-            float* out = p.An + (int64_t)g.row * p.lda;
-            double sse = s2, ac = 0.0, aa = 0.0, ec = 0.0;
-            float stv[SH::LD];
-#pragma unroll
-            for (int j = 0; j < SH::LD; ++j) stv[j] = 0.f;
-#pragma unroll
-            for (int j = 0; j < J; ++j) {
-                stv[j] = float(a[j]);
-                const double at = double(stv[j]);
-                sse = fma(-2.0 * at, c[j], sse);
-                ac = fma(a[j], c[j], ac);
-                aa = fma(a[j], a[j], aa);
-                ec = fma(at - a[j], c[j] - p.lambda * a[j], ec);
-            }
-            sse += ac - p.lambda * aa + 2.0 * ec;  // SSE of the stored row (see update.cuh)
-#pragma unroll
-            for (int q = 0; q < SH::NQ; ++q)
-                reinterpret_cast<float4*>(out)[q] = make_float4(stv[4 * q], stv[4 * q + 1], stv[4 * q + 2], stv[4 * q + 3]);
-            p.sse_row[g.row] = sse;
-        } else {
-            const int stp = p.lane_pstride[g.slot];
-            double* dst = p.partials + pidx;
-#pragma unroll
-            for (int q = 0; q < NB; ++q) dst[(int64_t)q * stp] = B[q];
-#pragma unroll
-            for (int q = 0; q < J; ++q) dst[(int64_t)(NB + q) * stp] = c[q];
-            dst[(int64_t)(NB + J) * stp] = s2;
-        }
-    };
-
-    Sched sc = s0;
-    if (sc.valid()) {
-        Seg cur, nxt;
-        load_seg(sc, cur);
-        Sched sn = sc;
-        ++sn.r;
-        const bool tiles = total > 0;
-        zero();
-        if (tiles) {
-            bool nvalid = sn.valid();
-            if (nvalid) load_seg(sn, nxt);
-            for (int s = -kCPref; s < 0; ++s) step(s);
-            cp_async_wait<kRPref - 1>();  // rows of tile 0 (committed at step -kRPref)
-            prepare(0, []() {});
-            int e = 0;
-            // optional per-phase clock trace (tools/trace_tc.py): CTA 0, lane 0 of each warp, tiles [64, 128)
-            long long* const trb = (p.trace && blockIdx.x == 0 && lane == 0) ? p.trace + warp * 512 : nullptr;
-            auto mark = [&](uint32_t k, int ph) {
-                if (trb && k >= 64 && k < 128) trb[(k - 64) * 8 + ph] = clock64();
-            };
-            for (uint32_t k = 0; k < total; ++k) {
-                mark(k, 0);
-                step((int)k);
-                mark(k, 1);
-                if (k + 1 < total) {
-                    cp_async_wait<kRPref - 1>();  // rows of tile k+1 (committed at step k+1-kRPref)
-                    mark(k, 2);
-                    prepare(k + 1, [&]() { mark(k, 3); });
+            for (int i = 0; i < 4; ++i) {
+                const int u = lane + kWarp * i;
+                const int64_t idx = poff[i] + (int64_t)pe * kWarp;
+                if (pe < plen[i]) {
+                    cp_async4_hint(crd(s, 0, u), p.sc[0] + idx, pol_stream);
+                    cp_async4_hint(crd(s, 1, u), p.sc[1] + idx, pol_stream);
+                    cp_async4_hint(crd(s, 2, u), p.sv + idx, pol_stream);
+                } else {
+                    *crd(s, 0, u) = 0u;  // padding entry: gather row 0 (its result is masked)
+                    *crd(s, 1, u) = 0u;
                 }
-                mark(k, 4);
-                // ---- epilogue of tile k ----
-                const int s = (int)(k % kRRing), buf = (int)(k & 1);
-                // an inactive lane (entry beyond its segment) gets a0 = 0, hence delta = 0
-                // (the gathered rows are always real factor rows, never stale data)
-                const bool act = e < cur.len;
-                float a0f[J];
+            }
+            ++kc;
+            if (++pe == piters) {
+                ++pc.r;
+                if (pc.valid()) load_group();
+                else pend = true;
+            }
+        };
+        for (int s = 0; s < kCPref; ++s) {
+            issue_crd();
+            cp_async_commit();
+        }
+        for (uint32_t k = 0; k < total; ++k) {
+            const int s = (int)(k % kRing), cs = (int)(k % kCRing);
+            if (k >= (uint32_t)kRing) mbar_wait(raw_empty(s), ((k / kRing) + 1) & 1);
+            cp_async_wait<kCPref - 1>();  // coordinates of tile k (committed kCPref groups ago)
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                const int u = lane + kWarp * i;
+                const char* r0 = reinterpret_cast<const char*>(p.A[0] + (int64_t)(int)*crd(cs, 0, u) * p.lda);
+                const char* r1 = reinterpret_cast<const char*>(p.A[1] + (int64_t)(int)*crd(cs, 1, u) * p.lda);
 #pragma unroll
                 for (int q = 0; q < NQ; ++q) {
-                    const float4 v = *reinterpret_cast<const float4*>(rowc(s, 0, q));
+                    cp_async16_hint(rowc(s, 0, q, u), r0 + 16 * q, pol_rows);
+                    cp_async16_hint(rowc(s, 1, q, u), r1 + 16 * q, pol_rows);
+                }
+                *rowx(s, u) = __uint_as_float(*crd(cs, 2, u));
+            }
+            cp_async_mbar_arrive(raw_full(s));  // fires when this lane's rows have landed
+            mbar_arrive(raw_full(s));           // x (plain stores), release
+            issue_crd();
+            cp_async_commit();
+        }
+        cp_async_wait<0>();
+    } else if (role == 2) {
+        // ================================================================ MMA issue
+        setmaxnreg_dec();
+        if (lane == 0) {
+            const uint32_t idesc =
+                (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(NP >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
+            // B descriptors (K-major, SWIZZLE_NONE; LBO: next 16-byte K chunk = next core
+            // matrix (128 B); SBO: next 8 rows), per K-step of 8
+            uint64_t dbhi[SH::KSTEPS], dblo[SH::KSTEPS];
+#pragma unroll
+            for (int ks = 0; ks < SH::KSTEPS; ++ks) {
+                dbhi[ks] = umma_desc(smem_u32(sBhi) + ks * 256, 128, KP * 32);
+                dblo[ks] = umma_desc(smem_u32(sBlo) + ks * 256, 128, KP * 32);
+            }
+            const uint32_t ahi = tmem + SH::ACOL, alo = tmem + SH::ACOL + KP;  // A in TMEM (lane = entry)
+            // optional trace (tools/trace_tc.py): CTA 0 pipeline 0, tiles [64, 128)
+            long long* const trm = (p.trace && blockIdx.x == 0 && h == 0) ? p.trace + 4 * 512 : nullptr;
+            for (uint32_t k = 0; k < total; ++k) {
+                const int st = (int)(k & 1);
+                const bool tr = trm && k >= 64 && k < 128;
+                if (tr) trm[(k - 64) * 8 + 0] = clock64();
+                mbar_wait(a_full, k & 1);                                     // A rows of tile k written
+                if (tr) trm[(k - 64) * 8 + 1] = clock64();
+                if (k >= 2) mbar_wait(acc_empty(st), ((k - 2) >> 1) & 1);  // TMEM buffer st read (tile k-2)
+                if (tr) trm[(k - 64) * 8 + 2] = clock64();
+                asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+                // 3xTF32 into TMEM buffer st: lo*hi, hi*lo, hi*hi (small terms first)
+                const uint32_t d = tmem + st * NP;
+                uint32_t acc = 0;
+#pragma unroll
+                for (int pr = 0; pr < 3; ++pr)
+#pragma unroll
+                    for (int ks = 0; ks < SH::KSTEPS; ++ks) {
+                        mma_tf32_ta(d, (pr == 0 ? alo : ahi) + 8 * ks, pr == 1 ? dblo[ks] : dbhi[ks], idesc, acc);
+                        acc = 1;
+                    }
+                asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                                 acc_full(st))
+                             : "memory");
+                if (tr) {
+                    trm[(k - 64) * 8 + 3] = clock64();
+                    if (p.trace[8 * 512 - 1] == 1) {  // latency probe: wait for this tile's MMAs
+                        mbar_wait(acc_full(st), (k >> 1) & 1);
+                        trm[(k - 64) * 8 + 4] = clock64();
+                    }
+                }
+            }
+        }
+    } else {
+        // ============================================================ epilogue
+        setmaxnreg_inc();
+        const int te = (warp & 3) * kWarp + lane;  // TMEM lane = segment of the group
+        const uint32_t tm_lane = tmem + ((uint32_t)((warp & 3) * 32) << 16);
+        auto load_seg = [&](const Sched& s, Seg& g) {
+            const int64_t g0 = s.group() * 4;
+            const int64_t sl = g0 + (warp & 3);
+            g.slot = sl * kWarp + lane;
+            const bool v = sl < p.nslices;
+            g.iters = __ldg(p.slice_len + g0);
+            g.row = v ? __ldg(p.lane_row + g.slot) : -1;
+            g.len = v ? __ldg(p.lane_len + g.slot) : 0;
+        };
+        double B[NB], c[J], s2;
+        auto zero = [&]() {
+#pragma unroll
+            for (int q = 0; q < NB; ++q) B[q] = 0.0;
+#pragma unroll
+            for (int q = 0; q < J; ++q) c[q] = 0.0;
+            s2 = 0.0;
+        };
+        // end of a segment: solve and store (Eq. 9 + fused Eq. 5), or write the heavy-row partial
+        auto finalize = [&](const Seg& g) {
+            if (g.row < 0) return;
+            const int64_t pidx = p.lane_pidx[g.slot];
+            if (pidx < 0) {
+                double a[J];
+                const bool ok = chol_solve<J>(B, c, p.lambda, a);
+                if (!ok) {
+                    atomicCAS(p.fail, 0, g.row + 1);
+#pragma unroll
+                    for (int j = 0; j < J; ++j) a[j] = 0.0;
+                }
+                float* out = p.An + (int64_t)g.row * p.lda;
+                double sse = s2, ac = 0.0, aa = 0.0, ec = 0.0;
+                float stv[SH::LD];
+#pragma unroll
+                for (int j = 0; j < SH::LD; ++j) stv[j] = 0.f;
+#pragma unroll
+                for (int j = 0; j < J; ++j) {
+                    stv[j] = float(a[j]);
+                    const double at = double(stv[j]);
+                    sse = fma(-2.0 * at, c[j], sse);
+                    ac = fma(a[j], c[j], ac);
+                    aa = fma(a[j], a[j], aa);
+                    ec = fma(at - a[j], c[j] - p.lambda * a[j], ec);
+                }
+                sse += ac - p.lambda * aa + 2.0 * ec;  // SSE of the stored row (see update.cuh)
+#pragma unroll
+                for (int q = 0; q < SH::NQ; ++q)
+                    reinterpret_cast<float4*>(out)[q] =
+                        make_float4(stv[4 * q], stv[4 * q + 1], stv[4 * q + 2], stv[4 * q + 3]);
+                p.sse_row[g.row] = sse;
+            } else {
+                const int stp = p.lane_pstride[g.slot];
+                double* dst = p.partials + pidx;
+#pragma unroll
+                for (int q = 0; q < NB; ++q) dst[(int64_t)q * stp] = B[q];
+#pragma unroll
+                for (int q = 0; q < J; ++q) dst[(int64_t)(NB + q) * stp] = c[q];
+                dst[(int64_t)(NB + J) * stp] = s2;
+            }
+        };
+        // optional per-phase clock trace (tools/trace_tc.py): CTA 0, lane 0 of warps 0-3, tiles [64, 128)
+        long long* const trb = (p.trace && blockIdx.x == 0 && lane == 0 && warp < 4) ? p.trace + warp * 512 : nullptr;
+        auto mark = [&](uint32_t k, int ph) {
+            if (trb && k >= 64 && k < 128) trb[(k - 64) * 8 + ph] = clock64();
+        };
+
+        Sched sc = s0;
+        if (sc.valid()) {
+            Seg cur, nxt;
+            load_seg(sc, cur);
+            Sched sn = sc;
+            ++sn.r;
+            bool nvalid = sn.valid();
+            if (nvalid) load_seg(sn, nxt);
+            zero();
+            int e = 0;
+            // Tile k (its rows have landed): write this thread's A row into TMEM lane te
+            // (hi = a rounded to tf32 by two integer ops, lo = a - hi exact; the tensor
+            // core truncates lo to tf32, an error <= 2^-21 |a|; columns k >= J are zero)
+            // and arrive (one arrival per warp) for the MMA warp.  The single A buffer
+            // was last read by MMA k-1, complete once this thread waited for its
+            // accumulator.
+            auto split = [&](uint32_t k) {
+                const int s = (int)(k % kRing);
+                mbar_wait(raw_full(s), (k / kRing) & 1);
+                uint32_t hi[16], lo[16];
+#pragma unroll
+                for (int q = 0; q < KQ; ++q) {
+                    uint32_t w[4] = {0u, 0u, 0u, 0u};
+                    if (q < NQ) {
+                        const uint4 r = *rowc(s, 1, q, te);
+                        w[0] = r.x, w[1] = r.y, w[2] = r.z, w[3] = r.w;
+                    }
+#pragma unroll
+                    for (int v = 0; v < 4; ++v) {
+                        const uint32_t hh = (w[v] + 0x1000u) & 0xFFFFE000u;
+                        hi[4 * q + v] = hh;
+                        lo[4 * q + v] = __float_as_uint(__uint_as_float(w[v]) - __uint_as_float(hh));
+                    }
+                }
+                const uint32_t ta = tm_lane + SH::ACOL;
+                if constexpr (KP == 16) {
+                    tmem_st16(ta, hi);
+                    tmem_st16(ta + KP, lo);
+                } else {
+                    tmem_st8(ta, hi);
+                    tmem_st8(ta + KP, lo);
+                }
+                asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+                asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+                __syncwarp();
+                if (lane == 0) mbar_arrive(a_full);
+            };
+            // Software pipeline over tiles: MMA k+1 runs during level 0 and the normal
+            // equations of tile k; MMA k+2 is issued right after and runs during level 0
+            // and the normal equations of tile k+1.
+            float a0f[J];  // a0 of the tile whose level 0 is next (0 for an inactive lane)
+            float x = 0.f;
+            bool act = false;
+            uint32_t rb[2][16];  // TMEM chunks (16 columns) in flight
+            // a0/x of tile k (its rows landed: split(k) waited for them), then release the slot
+            auto fetch_a0 = [&](uint32_t k, bool active) {
+                const int s = (int)(k % kRing);
+#pragma unroll
+                for (int q = 0; q < NQ; ++q) {
+                    const float4 v = *reinterpret_cast<const float4*>(rowc(s, 0, q, te));
                     const float w[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
                     for (int u = 0; u < 4; ++u)
-                        if (4 * q + u < J) a0f[4 * q + u] = act ? w[u] : 0.f;
+                        if (4 * q + u < J) a0f[4 * q + u] = active ? w[u] : 0.f;
                 }
-                const float x = __uint_as_float(*crd((int)(k % kCRing), 2));
-                mbar_wait(acc_bar(buf), (k >> 1) & 1);
+                x = *rowx(s, te);
+                act = active;
+                __syncwarp();
+                if (lane == 0) mbar_arrive(raw_empty(s));
+            };
+            // wait for tile k's accumulator (MMA k complete: the A buffer is free again)
+            auto wait_acc = [&](uint32_t k) {
+                mbar_wait(acc_full((int)(k & 1)), (k >> 1) & 1);
                 asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-                mark(k, 5);
-                // level 0: d[j] = sum_k0 a0[k0] t[k0][j]; t[k0][j] is TMEM column k0*J + j
+            };
+            // start loading tile k's first two chunks
+            auto start_tmem = [&](uint32_t k) {
+                const uint32_t taddr = tm_lane + (k & 1) * NP;
+                tmem_ld16(taddr, rb[0]);
+                if (SH::NCH > 1) tmem_ld16(taddr + 16, rb[1]);
+            };
+            if (total > 0) {
+                split(0);
+                wait_acc(0);
+                start_tmem(0);
+                if (total > 1) split(1);
+                fetch_a0(0, 0 < cur.len);
+            }
+            for (uint32_t k = 0; k < total; ++k) {
+                const int buf = (int)(k & 1);
+                mark(k, 0);
+                // ---- level 0 of tile k: d[j] = sum_k0 a0[k0] t[k0][j], t[k0][j] = TMEM column k0*J + j.
+                // Chunks arrive in pairs: one wait covers chunks (2m, 2m+1); chunk 2m+2 is
+                // issued after 2m is consumed, 2m+3 after 2m+1.
                 TD d[J];
                 float pf[J];  // fp32 partial sums (G0 > 1)
 #pragma unroll
                 for (int j = 0; j < J; ++j) d[j] = TD(0);
                 const uint32_t taddr = tm_lane + buf * NP;
-                uint32_t rb[2][16];
-                tmem_ld16(taddr, rb[0]);
 #pragma unroll
                 for (int ch = 0; ch < SH::NCH; ++ch) {
-                    tmem_wait16(rb[ch & 1]);
-                    if (ch + 1 < SH::NCH) tmem_ld16(taddr + (ch + 1) * 16, rb[(ch + 1) & 1]);
+                    if ((ch & 1) == 0) tmem_wait16(rb[0]), tmem_wait16(rb[1]);
 #pragma unroll
                     for (int i = 0; i < 16; ++i) {
                         const int cc = ch * 16 + i;
@@ -557,22 +630,39 @@ __global__ void __launch_bounds__(kThreads, 2) k_update_tc(const UpdateParams<fl
                             if (k0 % G0 == G0 - 1 || k0 == J - 1) d[j] = d[j] + TD(pf[j]);
                         }
                     }
+                    if (ch + 2 < SH::NCH) tmem_ld16(taddr + (ch + 2) * 16, rb[ch & 1]);
                 }
                 asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-                mark(k, 6);
+                __syncwarp();
+                if (lane == 0) mbar_arrive(acc_empty(buf));
+                mark(k, 1);
                 double dd[J];
 #pragma unroll
                 for (int j = 0; j < J; ++j) dd[j] = double(d[j]);
                 const double xd = act ? double(x) : 0.0;
+                // ---- normal equations of tile k (Eq. 10-11)
+                auto normal_eq = [&]() {
 #pragma unroll
-                for (int i = 0; i < J; ++i) {
-                    c[i] = fma(xd, dd[i], c[i]);
+                    for (int i = 0; i < J; ++i) {
+                        c[i] = fma(xd, dd[i], c[i]);
 #pragma unroll
-                    for (int j = i; j < J; ++j) B[up_idx(i, j, J)] = fma(dd[i], dd[j], B[up_idx(i, j, J)]);
-                }
-                s2 = fma(xd, xd, s2);
-                mark(k, 7);
-                if (++e == cur.iters) {
+                        for (int j = i; j < J; ++j) B[up_idx(i, j, J)] = fma(dd[i], dd[j], B[up_idx(i, j, J)]);
+                    }
+                    s2 = fma(xd, xd, s2);
+                };
+                // ---- then tile k+1's first TMEM chunks and tile k+2's A rows (the single
+                // TMEM A buffer is free once MMA k+1 has completed), whose latencies
+                // overlap each other; then a0/x of tile k+1 (the next entry of the segment,
+                // or the first of the next group's)
+                if (k + 1 < total) wait_acc(k + 1);
+                mark(k, 2);
+                normal_eq();
+                mark(k, 3);
+                bool next_act;
+                if (e + 1 < cur.iters) {
+                    next_act = e + 1 < cur.len;
+                    ++e;
+                } else {
                     finalize(cur);
                     zero();
                     e = 0;
@@ -583,21 +673,26 @@ __global__ void __launch_bounds__(kThreads, 2) k_update_tc(const UpdateParams<fl
                         nvalid = sn.valid();
                         if (nvalid) load_seg(sn, nxt);
                     }
+                    next_act = 0 < cur.len;
                 }
+                if (k + 1 < total) start_tmem(k + 1);
+                if (k + 2 < total) split(k + 2);
+                if (k + 1 < total) fetch_a0(k + 1, next_act);
+                mark(k, 4);
             }
-            cp_async_wait<0>();
-        }
-        // the groups after the last one with entries are empty (sorted by length):
-        // their rows get a = 0 and SSE 0
-        for (; sc.valid(); ++sc.r) {
-            load_seg(sc, cur);
-            zero();
-            finalize(cur);
+            // the groups after the last one with entries are empty (sorted by length):
+            // their rows get a = 0 and SSE 0
+            for (; sc.valid(); ++sc.r) {
+                load_seg(sc, cur);
+                zero();
+                finalize(cur);
+            }
         }
     }
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     __syncthreads();
-    if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(SH::TCOLS));
+    if (warp == 0)
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(misc[0]), "n"(kPipes * SH::TCOLS));
 }
 
 template <int J, bool LAST64, int G0>
@@ -628,23 +723,17 @@ int occupancy_tc(bool literal, size_t gp_bytes) {
     auto k = k_update_tc<J, LAST64, 1>;
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, Shape<J>::SMEM);
     cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
-    // Resident CTAs per SM from the kernel's own resource use (the occupancy API
-    // under-reports this kernel on sm_100a): registers, shared memory, TMEM.
-    cudaFuncAttributes fa;
-    cudaFuncGetAttributes(&fa, k);
-    int dev = 0, smem_sm = 0, regs_sm = 0;
+    int dev = 0, smem_sm = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&smem_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev);
-    cudaDeviceGetAttribute(&regs_sm, cudaDevAttrMaxRegistersPerMultiprocessor, dev);
-    const int regs = (fa.numRegs + 7) / 8 * 8;
-    const int by_regs = regs_sm / (regs * kThreads);
-    const int by_smem = smem_sm / (Shape<J>::SMEM + 1024);
-    int nb = by_regs < by_smem ? by_regs : by_smem;
-    const int tm = 512 / Shape<J>::TCOLS;  // TMEM: every resident CTA allocates TCOLS of the 512 columns
-    if (getenv("PTUCKER_DEBUG"))
-        fprintf(stderr, "[ptucker] tc occupancy J=%d smem=%d regs=%d: by_regs=%d by_smem=%d tmem=%d\n", J,
-                Shape<J>::SMEM, fa.numRegs, by_regs, by_smem, tm);
-    return nb < tm ? nb : tm;
+    if (getenv("PTUCKER_DEBUG")) {
+        cudaFuncAttributes fa;
+        cudaFuncGetAttributes(&fa, k);
+        fprintf(stderr, "[ptucker] tc J=%d smem=%d regs=%d (one CTA of %d threads per SM)\n", J, Shape<J>::SMEM,
+                fa.numRegs, kThreads);
+    }
+    // one CTA per SM: it allocates all 512 TMEM columns and most of the shared memory
+    return Shape<J>::SMEM + 1024 <= smem_sm ? 1 : 0;
 }
 
 }  // namespace tc

@@ -89,7 +89,7 @@ __global__ void k_f2f(float* out, float s, unsigned long long* clk) {
 #pragma unroll
         for (int i = 0; i < CH; ++i) a[i] += (double)f[i];
 #pragma unroll
-        for (int i = 0; i < CH; ++i) f[i] = __int_as_float(__float_as_int(f[i]) ^ 1);  // keep the cvt in the loop
+        for (int i = 0; i < CH; ++i) f[i] = __int_as_float(__float_as_int(f[i]) + 1);  // a new value every iteration
     }
     double r = 0;
 #pragma unroll
@@ -115,7 +115,7 @@ __global__ void k_dadd_lop(float* out, float s, unsigned long long* clk) {
 #pragma unroll
         for (int i = 0; i < CH; ++i) a[i] += d[i];
 #pragma unroll
-        for (int i = 0; i < CH; ++i) f[i] = __int_as_float(__float_as_int(f[i]) ^ 1);
+        for (int i = 0; i < CH; ++i) f[i] = __int_as_float(__float_as_int(f[i]) + 1);
     }
     double r = 0;
 #pragma unroll
@@ -143,7 +143,7 @@ __global__ void k_f2f_int(float* out, float s, unsigned long long* clk) {
             a[i] += __hiloint2double((int)hi, (int)lo);
         }
 #pragma unroll
-        for (int i = 0; i < CH; ++i) f[i] = __int_as_float(__float_as_int(f[i]) ^ 1);
+        for (int i = 0; i < CH; ++i) f[i] = __int_as_float(__float_as_int(f[i]) + 1);
     }
     double r = 0;
 #pragma unroll

@@ -1,11 +1,10 @@
-"""Per-phase clock trace of the tensor-core update kernel (CTA 0, lane 0 of each of its
-4 warps, tiles 64..127 of its sequence).  Phases per tile k:
-0 start, 1 after the cp.async issue step (coordinates k+7, rows k+3), 2 after the
-cp.async wait for the rows of k+1, 3 after splitting them into the A tile, 4 after
-arriving (MMA issued by the last arriver), 5 after waiting for tile k's MMA,
-6 after TMEM loads + level 0, 7 after B/c.
+"""Per-phase clock trace of the tensor-core update kernel (CTA 0, lane 0 of the 4
+epilogue warps of pipeline 0, tiles 64..127 of its sequence).  Phases per tile k:
+0 start, 1 after level 0 of tile k (TMEM loads + F2F/DFMA), 2 after waiting for
+MMA k+1, 3 after the normal equations of tile k, 4 (group end) ..., 4 after the
+first TMEM loads of k+1, the A rows of tile k+2 and a0/x of tile k+1.
 
-    python tools/trace_tc.py [scale] [l0_group]"""
+    python tools/trace_tc.py [scale] [l0_group] [latency]"""
 import sys
 import numpy as np
 import torch
@@ -23,8 +22,19 @@ pt.ptucker_update_mode(0)
 pt.ptucker_set_option("trace", 1)
 pt.ptucker_update_mode(1)
 pt.ptucker_synchronize()
-tr = pt.ptucker_debug_trace(4 * 512).reshape(4, 64, 8)
-names = ["issue", "cp.wait", "split", "arrive", "mma wait", "tmem+L0", "B/c", "->next"]
+full = pt.ptucker_debug_trace(8 * 512)
+m = full[4 * 512:4 * 512 + 512].reshape(64, 8)
+if len(sys.argv) > 3:  # latency probe: MMA issue -> completion, measured serialised
+    pt.ptucker_set_option("trace", 2)
+    pt.ptucker_update_mode(2)
+    pt.ptucker_synchronize()
+    f2 = pt.ptucker_debug_trace(8 * 512)[4 * 512:4 * 512 + 512].reshape(64, 8)
+    print("MMA latency (issue -> accumulator ready, serialised): median %d cycles" % np.median(f2[:, 4] - f2[:, 3]))
+print("MMA warp (pipeline 0), median cycles: a_full wait %d, acc_empty wait %d, issue %d; per tile %d" % (
+    np.median(m[:, 1] - m[:, 0]), np.median(m[:, 2] - m[:, 1]), np.median(m[:, 3] - m[:, 2]),
+    np.median(np.diff(m[:, 0]))))
+tr = pt.ptucker_debug_trace(4 * 512).reshape(4, 64, 8)[:, :, [0, 1, 2, 3, 4]]
+names = ["L0(k)", "wait mma(k+1)", "B/c(k)", "group end+tmem+split+a0", "->next"]
 for w in range(4):
     t = tr[w]
     ok = t[:, 0] > 0
