@@ -10,30 +10,31 @@
 // small products first: lo*hi, hi*lo, hi*hi) so its accuracy matches an fp32
 // FMA chain (tools/tc_probe.cu), accumulating in TMEM.
 //
-// One CTA per SM runs two independent pipelines h = 0, 1 (12 warps):
-//   warps 4h..4h+3  EPILOGUE (128 threads; 224 registers via setmaxnreg): thread
-//                   t owns TMEM lane t and row segment t of the pipeline's current
-//                   group of 4 SELL-32 slices.  Per tile it reads
-//                   t[k0][j] from TMEM, finishes level 0 (fp64 per term, or fp32
-//                   partial sums of G0 terms added in fp64), accumulates
-//                   B += delta delta^T, c += x delta, sum x^2 in fp64 registers
-//                   (Eq. 10-11) and at the end of the segment solves
-//                   a = c [B + lambda I]^-1 (Cholesky, Eq. 9) and stores the row
-//                   with its SSE (fused Eq. 5).
-//   warp 8+h        LOADER: streams the SELL coordinates/values of the pipeline's
-//                   tiles into a coordinate ring (cp.async, kCPref tiles ahead)
-//                   and gathers the two factor rows of every entry into a
-//                   kRing-slot row ring (cp.async; mbarrier full/empty).
-//   warp 10+h       MMA: lane 0 issues a tile's MMAs into one of two TMEM
-//                   accumulators once the epilogue warps have written its A rows.
-// Before the epilogue of tile k, each epilogue thread splits its own gathered a1
-// row of tile k+1 into tf32 hi/lo rows of the A operand (double-buffered stage),
-// so the MMA of tile k+1 overlaps the epilogue of tile k.  The epilogue warps
-// touch no global memory inside the tile loop: the loads and every
-// long-latency wait live in the helper warps.
-// Groups are assigned statically (serpentine over the 2 x #CTA pipelines; SELL
-// groups are sorted by length, so neighbouring pipelines get near-equal work),
-// so every role knows the pipeline's whole tile sequence in advance.
+// One CTA per SM, 16 warps.  Warps w, w+4 (level 0) and w+8 (normal equations)
+// serve TMEM lane quarter w: thread t owns TMEM lane 32w+t = row segment 32w+t
+// of the current group of 4 SELL-32 slices.
+//   warps 0-7   LEVEL 0 (120 registers via setmaxnreg; warps w and w+4 take
+//               alternate tiles): per tile, load the J^2 columns t[k0][j] from
+//               TMEM (kBCH chunks per wait), finish level 0 (fp64 per term, or
+//               fp32 partial sums of G0 terms added in fp64) and hand delta (fp64)
+//               and x to warp w+8 through a shared-memory ring.
+//   warps 8-11  NORMAL EQUATIONS (232 registers): write the A row (tf32 hi/lo
+//               split of the gathered a1 row) of the tile kNA ahead into TMEM, then
+//               B += delta delta^T, c += x delta, sum x^2 in fp64 registers
+//               (Eq. 10-11), and at the end of the segment a = c [B + lambda I]^-1
+//               (Cholesky, Eq. 9) and the row's SSE (fused Eq. 5).
+//   warp 14     LOADER: streams the SELL coordinates/values into a coordinate ring
+//               (cp.async, kCPref tiles ahead) and gathers the two factor rows of
+//               every entry into a kRing-slot row ring (cp.async).
+//   warp 15     MMA: lane 0 issues a tile's MMAs into one of kNT TMEM accumulators.
+//   (warps 12, 13 idle.)
+// Splitting level 0 from the normal equations keeps each role's registers small
+// enough for two level-0 warps per SM sub-partition (the XU conversions of one
+// overlap the waits of the other) and lets the XU and fp64 pipes work on
+// different tiles concurrently.
+// Groups are assigned statically (serpentine over the CTAs; SELL groups are
+// sorted by length, so neighbouring CTAs get near-equal work), so every role
+// knows the CTA's whole tile sequence in advance.
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -46,19 +47,23 @@
 namespace pt {
 namespace tc {
 
-constexpr int kE = 128;                      // epilogue threads of a pipeline = TMEM lanes = segments per group
-constexpr int kPipes = 2;                    // pipelines per CTA (one CTA per SM)
-constexpr int kThreads = kPipes * kE + 4 * kWarp;  // + loader and MMA warps of both pipelines
-constexpr int kRing = 6;                     // row ring slots (tiles in flight between loader and epilogue)
+constexpr int kE = 128;                      // TMEM lanes = segments per group (4 slices)
+constexpr int kThreads = 16 * 32;            // 2 level-0 WGs, normal-equation WG, loader/MMA WG
+constexpr int kRing = 6;                     // row ring slots (tiles between loader and level 0)
 constexpr int kCPref = 7;                    // loader: coordinates fetched this many tiles ahead of the gathers
 constexpr int kCRing = 8;                    // coordinate ring slots (> kCPref)
-constexpr int kRegLaunch = 65536 / kThreads / 8 * 8;  // registers per thread at launch (168)
-constexpr int kRegE = 232;                   // setmaxnreg: epilogue warpgroups
+constexpr int kNT = 3;                       // TMEM accumulator buffers
+constexpr int kNA = 4;                       // TMEM A buffers (the normal-equation warps write A kNA tiles ahead)
+constexpr int kD = 4;                        // delta ring slots (level 0 -> normal equations)
+constexpr int kRegLaunch = 65536 / kThreads / 8 * 8;  // registers per thread at launch (128)
+constexpr int kRegL0 = 120;                  // setmaxnreg: level-0 warpgroups
+constexpr int kRegNE = 232;                  //             normal-equation warpgroup
 constexpr int kRegP = 40;                    //             loader/MMA warpgroup
+constexpr int kBCH = 4;                      // level 0: TMEM chunks per load batch (registers)
 static_assert(kCRing > kCPref, "ring depths");
-// setmaxnreg moves registers inside the CTA's launch allocation: the epilogue's
-// increase must be covered by the helpers' release, or it waits forever
-static_assert(2 * 4 * kWarp * kRegE + 4 * kWarp * kRegP <= kRegLaunch * kThreads, "register pool");
+// setmaxnreg moves registers inside the CTA's launch allocation: the increases
+// must be covered by the helpers' release, or they wait forever
+static_assert(4 * kWarp * (2 * kRegL0 + kRegNE + kRegP) <= kRegLaunch * kThreads, "register pool");
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 
@@ -177,45 +182,33 @@ struct Shape {
     static constexpr int KP = (J + 7) / 8 * 8;             // K padded to the tf32 MMA K-step (8)
     static constexpr int KSTEPS = KP / 8;
     static constexpr int NP = (J * J + 15) / 16 * 16;      // N padded to 16 (M = 128)
-    static constexpr int ACOL = 2 * NP;                     // TMEM: T buffers [0, 2NP), A_hi [ACOL, +KP), A_lo [ACOL+KP, +KP)
-    static constexpr int TCOLS = ACOL + 2 * KP <= 32 ? 32 : (ACOL + 2 * KP <= 64 ? 64 : (ACOL + 2 * KP <= 128 ? 128 : 256));
     static constexpr int LD = factor_ld(J, 4);             // padded factor row (floats)
     static constexpr int NQ = LD / 4;                       // 16-byte chunks per factor row
     static constexpr int KQ = KP / 4;                       // 16-byte chunks per A row
     static constexpr int NCH = (J * J + 15) / 16;           // 16-column TMEM chunks holding t
+    // TMEM (all 512 columns): accumulators [b*NP, (b+1)*NP), A buffers at ACOL + a*2*KP (hi, then lo)
+    static constexpr int ACOL = kNT * NP;
+    static constexpr int TCOLS = 512;
+    static_assert(ACOL + kNA * 2 * KP <= TCOLS, "TMEM columns");
     // shared memory map (bytes)
     static constexpr int B_BYTES = NP * KP * 4;             // one of B_hi / B_lo
     static constexpr int RSLOT = 2 * NQ * kE * 16 + kE * 4; // row ring slot: rows a0, a1 (chunk-major), x
     static constexpr int CSLOT = 3 * kE * 4;                // coordinate ring slot: c0, c1, x
+    static constexpr int DSLOT = J * kE * 8 + kE * 4;       // delta ring slot: delta[j][u] (fp64), x[u]
     static constexpr int OFF_BHI = 0;
     static constexpr int OFF_BLO = OFF_BHI + B_BYTES;
-    static constexpr int OFF_MISC = OFF_BLO + B_BYTES;      // tmem base, tiles per pipeline
-    static constexpr int OFF_PIPE = (OFF_MISC + 64 + 127) / 128 * 128;
-    // per pipeline, at OFF_PIPE + h * PIPE_BYTES
-    static constexpr int P_ROW = 0;
-    static constexpr int P_CRD = P_ROW + kRing * RSLOT;
-    static constexpr int P_BAR = P_CRD + kCRing * CSLOT;    // raw_full[kRing], raw_empty[kRing], acc_full[2], acc_empty[2], a_full
-    static constexpr int PIPE_BYTES = (P_BAR + (2 * kRing + 5) * 8 + 127) / 128 * 128;
-    static constexpr int SMEM = OFF_PIPE + kPipes * PIPE_BYTES;
-    static_assert(kPipes * TCOLS <= 512 && ACOL + 2 * KP <= TCOLS, "TMEM columns");
+    static constexpr int OFF_MISC = OFF_BLO + B_BYTES;      // tmem base, tiles
+    static constexpr int OFF_ROW = (OFF_MISC + 64 + 127) / 128 * 128;
+    static constexpr int OFF_CRD = OFF_ROW + kRing * RSLOT;
+    static constexpr int OFF_DEL = OFF_CRD + kCRing * CSLOT;
+    static constexpr int OFF_BAR = (OFF_DEL + kD * DSLOT + 7) / 8 * 8;
+    // raw_full[kRing], raw_empty[kRing], acc_full[kNT], acc_empty[kNT], a_full[kNA], d_full[4][kD], d_empty[4][kD],
+    // a_empty[kNA]
+    static constexpr int NBAR = 2 * kRing + 2 * kNT + 2 * kNA + 8 * kD;
+    static constexpr int SMEM = OFF_BAR + NBAR * 8;
 };
 
-// Split of the innermost factor into tf32 hi/lo parts (3xTF32 operand), K-padded
-// (diagnostic helper kept for tools/; the update kernel splits in place).
-__global__ void k_split_tf32(const float* __restrict__ A, int64_t I, int lda, int J, int KP, float* __restrict__ hi,
-                             float* __restrict__ lo) {
-    const int64_t total = I * KP;
-    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t i = t / KP;
-        const int k = (int)(t % KP);
-        const float v = k < J ? A[i * lda + k] : 0.f;
-        const float h = tf32_rna(v);
-        hi[t] = h;
-        lo[t] = tf32_rna(v - h);
-    }
-}
-
-// Static serpentine assignment of groups (4 slices each) to pipelines.
+// Static serpentine assignment of groups (4 slices each) to CTAs.
 struct Sched {
     int ngroups, r;
     int G, b;
@@ -223,26 +216,27 @@ struct Sched {
     __device__ bool valid() const { return group() < ngroups; }
 };
 
-// Segment data of the current group for one epilogue thread.
+// Segment data of the current group for one normal-equation thread.
 struct Seg {
     int iters;     // tiles of the group (longest slice = its first)
     int row, len;  // segment row (-1: pad lane) and length
     int slot;      // SELL lane slot (partials)
 };
 
-__device__ __forceinline__ void setmaxnreg_inc() { asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(kRegE)); }
+__device__ __forceinline__ void setmaxnreg_ne() { asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(kRegNE)); }
+__device__ __forceinline__ void setmaxnreg_l0() { asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(kRegL0)); }
 __device__ __forceinline__ void setmaxnreg_dec() { asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(kRegP)); }
 
 // G0 (level-0 grouping, LAST64 only): 1 = every a0[k0] t[k0][j] product and the sum
 // in fp64 (F32-B); g > 1 = partial sums over runs of g consecutive k0 in fp32
 // (one rounded product, then FMAs), each partial converted to fp64 once and the
 // partials summed in fp64: J*ceil(J/g) instead of J^2 fp32->fp64 conversions per
-// entry (F2F runs on the quarter-rate XU pipe; tools/level0_emulation.py measures
-// the row error of each g).
+// entry (F2F runs on the quarter-rate XU pipe; tools/l0_row_errors.py and
+// tools/level0_emulation.py measure the row error of each g).
 template <int J, bool LAST64, int G0>
 __global__ void __launch_bounds__(kThreads, 1) k_update_tc(const UpdateParams<float> p) {
     using SH = Shape<J>;
-    constexpr int KP = SH::KP, NP = SH::NP, NQ = SH::NQ, KQ = SH::KQ;
+    constexpr int KP = SH::KP, NP = SH::NP, NQ = SH::NQ, KQ = SH::KQ, NCH = SH::NCH;
     constexpr int NB = J * (J + 1) / 2;
     constexpr int GB = gblk(J, 4);
     using TD = typename std::conditional<LAST64, double, float>::type;
@@ -251,29 +245,37 @@ __global__ void __launch_bounds__(kThreads, 1) k_update_tc(const UpdateParams<fl
     float* sBlo = reinterpret_cast<float*>(sm + SH::OFF_BLO);
     uint32_t* misc = reinterpret_cast<uint32_t*>(sm + SH::OFF_MISC);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    // role: 0 epilogue (warps 0-7), 1 loader (8, 9), 2 MMA issue (10, 11)
-    const int role = warp < 4 * kPipes ? 0 : (warp < 4 * kPipes + 2 ? 1 : 2);
-    const int h = role == 0 ? (warp >> 2) : (warp & 1);
-    unsigned char* pipe = sm + SH::OFF_PIPE + h * SH::PIPE_BYTES;
-    const uint32_t bar0 = smem_u32(pipe + SH::P_BAR);
+    const int w4 = warp & 3;                 // slice of the group = TMEM lane quarter of the warp
+    const int te = w4 * kWarp + lane;        // TMEM lane = segment of the group
+    const uint32_t bar0 = smem_u32(sm + SH::OFF_BAR);
     auto raw_full = [&](int s) { return bar0 + 8u * s; };
     auto raw_empty = [&](int s) { return bar0 + 8u * (kRing + s); };
     auto acc_full = [&](int b) { return bar0 + 8u * (2 * kRing + b); };
-    auto acc_empty = [&](int b) { return bar0 + 8u * (2 * kRing + 2 + b); };
-    const uint32_t a_full = bar0 + 8u * (2 * kRing + 4);  // single A buffer (TMEM)
+    auto acc_empty = [&](int b) { return bar0 + 8u * (2 * kRing + kNT + b); };
+    auto a_full = [&](int a) { return bar0 + 8u * (2 * kRing + 2 * kNT + a); };
+    auto d_full = [&](int w, int s) { return bar0 + 8u * (2 * kRing + 2 * kNT + kNA + w * kD + s); };
+    auto d_empty = [&](int w, int s) { return bar0 + 8u * (2 * kRing + 2 * kNT + kNA + 4 * kD + w * kD + s); };
+    auto a_empty = [&](int a) { return bar0 + 8u * (2 * kRing + 2 * kNT + kNA + 8 * kD + a); };
     // row ring slot s: chunk q of row k (0: a0, 1: a1) of segment u; x of segment u
     auto rowc = [&](int s, int k, int q, int u) -> uint4* {
-        return reinterpret_cast<uint4*>(pipe + SH::P_ROW + s * SH::RSLOT) + ((k * NQ + q) * kE + u);
+        return reinterpret_cast<uint4*>(sm + SH::OFF_ROW + s * SH::RSLOT) + ((k * NQ + q) * kE + u);
     };
     auto rowx = [&](int s, int u) -> float* {
-        return reinterpret_cast<float*>(pipe + SH::P_ROW + s * SH::RSLOT + 2 * NQ * kE * 16) + u;
+        return reinterpret_cast<float*>(sm + SH::OFF_ROW + s * SH::RSLOT + 2 * NQ * kE * 16) + u;
     };
     // coordinate ring slot s: c0, c1, x (a = 0, 1, 2) of segment u
     auto crd = [&](int s, int a, int u) -> uint32_t* {
-        return reinterpret_cast<uint32_t*>(pipe + SH::P_CRD + s * SH::CSLOT) + a * kE + u;
+        return reinterpret_cast<uint32_t*>(sm + SH::OFF_CRD + s * SH::CSLOT) + a * kE + u;
+    };
+    // delta ring slot s: delta[j] of segment u (fp64), x of segment u
+    auto dslot = [&](int s, int j, int u) -> double* {
+        return reinterpret_cast<double*>(sm + SH::OFF_DEL + s * SH::DSLOT) + j * kE + u;
+    };
+    auto dslot_x = [&](int s, int u) -> float* {
+        return reinterpret_cast<float*>(sm + SH::OFF_DEL + s * SH::DSLOT + J * kE * 8) + u;
     };
     const int ngroups = (int)((p.nslices + 3) / 4);  // nslices * 32 < 2^31 (nnz <= INT32_MAX)
-    const Sched s0{ngroups, 0, kPipes * (int)gridDim.x, kPipes * (int)blockIdx.x + h};
+    const Sched s0{ngroups, 0, (int)gridDim.x, (int)blockIdx.x};
 
     // ---------------------------------------------------------------- setup
     // B = core (hi/lo tf32 split), K-major: Bt[(k0, j)][k1] = G'[k0][k1][j]
@@ -287,11 +289,11 @@ __global__ void __launch_bounds__(kThreads, 1) k_update_tc(const UpdateParams<fl
     }
     if (warp == 0) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&misc[0])),
-                     "n"(kPipes * SH::TCOLS));
+                     "n"(SH::TCOLS));
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
     }
-    if (role == 1) {
-        // tiles of this pipeline = sum of the iteration counts of its groups
+    if (warp == 14) {
+        // tiles of this CTA = sum of the iteration counts of its groups
         uint32_t n = 0;
         for (int r = lane;; r += kWarp) {
             Sched q = s0;
@@ -302,16 +304,24 @@ __global__ void __launch_bounds__(kThreads, 1) k_update_tc(const UpdateParams<fl
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) n += __shfl_xor_sync(0xffffffffu, n, o);
         if (lane == 0) {
-            misc[2 + h] = n;
+            misc[1] = n;
             for (int s = 0; s < kRing; ++s) {
                 mbar_init(raw_full(s), 2 * kWarp);  // loader lanes: cp.async completion + plain arrive (x)
-                mbar_init(raw_empty(s), 4);         // the 4 epilogue warps
+                mbar_init(raw_empty(s), 8);         // the 4 level-0 warps (a0) + the 4 normal-equation warps (a1)
             }
-            for (int b = 0; b < 2; ++b) {
+            for (int b = 0; b < kNT; ++b) {
                 mbar_init(acc_full(b), 1);   // tcgen05.commit
-                mbar_init(acc_empty(b), 4);  // epilogue warps done reading the TMEM buffer
+                mbar_init(acc_empty(b), 4);  // level-0 warps done reading the accumulator
             }
-            mbar_init(a_full, 4);            // epilogue warps wrote their A rows (TMEM)
+            for (int a = 0; a < kNA; ++a) {
+                mbar_init(a_full(a), 4);   // normal-equation warps wrote their A rows
+                mbar_init(a_empty(a), 1);  // tcgen05.commit: the MMAs reading A buffer a completed
+            }
+            for (int w = 0; w < 4; ++w)
+                for (int s = 0; s < kD; ++s) {
+                    mbar_init(d_full(w, s), kWarp);  // every lane of level-0 warp w (its delta stores)
+                    mbar_init(d_empty(w, s), 1);     // normal-equation warp 4+w read the slot
+                }
             asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         }
     }
@@ -319,85 +329,84 @@ __global__ void __launch_bounds__(kThreads, 1) k_update_tc(const UpdateParams<fl
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     __syncthreads();
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-    const uint32_t tmem = misc[0] + h * SH::TCOLS;
-    const uint32_t total = misc[2 + h];
+    const uint32_t tmem = misc[0];
+    const uint32_t total = misc[1];
 
-    if (role == 1) {
-        // ======================================================== loader
+    if (warp >= 12) {
         setmaxnreg_dec();
-        const uint64_t pol_stream = policy_evict_first(), pol_rows = policy_evict_last();
-        // coordinate cursor (tile kc): this lane's 4 segments u = lane + 32 i, i = slice of the group
-        Sched pc = s0;
-        int pe = 0, piters = 0, plen[4];
-        int64_t poff[4];
-        bool pend = total == 0;
-        auto load_group = [&]() {
-            const int64_t g0 = pc.group() * 4;
+        if (warp == 14) {
+            // ======================================================== loader
+            const uint64_t pol_stream = policy_evict_first(), pol_rows = policy_evict_last();
+            // coordinate cursor (tile kc): this lane's 4 segments u = lane + 32 i, i = slice of the group
+            Sched pc = s0;
+            int pe = 0, piters = 0, plen[4];
+            int64_t poff[4];
+            bool pend = total == 0;
+            auto load_group = [&]() {
+                const int64_t g0 = (int64_t)pc.group() * 4;
 #pragma unroll
-            for (int i = 0; i < 4; ++i) {
-                const bool v = g0 + i < p.nslices;
-                plen[i] = v ? __ldg(p.slice_len + g0 + i) : 0;
-                poff[i] = v ? __ldg(p.slice_off + g0 + i) + lane : 0;
-            }
-            piters = plen[0];
-            pe = 0;
-            if (piters == 0) pend = true;  // groups are sorted by length: nothing follows an empty group
-        };
-        if (!pend) load_group();
-        uint32_t kc = 0;
-        auto issue_crd = [&]() {
-            if (pend) return;
-            const int s = (int)(kc % kCRing);
-#pragma unroll
-            for (int i = 0; i < 4; ++i) {
-                const int u = lane + kWarp * i;
-                const int64_t idx = poff[i] + (int64_t)pe * kWarp;
-                if (pe < plen[i]) {
-                    cp_async4_hint(crd(s, 0, u), p.sc[0] + idx, pol_stream);
-                    cp_async4_hint(crd(s, 1, u), p.sc[1] + idx, pol_stream);
-                    cp_async4_hint(crd(s, 2, u), p.sv + idx, pol_stream);
-                } else {
-                    *crd(s, 0, u) = 0u;  // padding entry: gather row 0 (its result is masked)
-                    *crd(s, 1, u) = 0u;
+                for (int i = 0; i < 4; ++i) {
+                    const bool v = g0 + i < p.nslices;
+                    plen[i] = v ? __ldg(p.slice_len + g0 + i) : 0;
+                    poff[i] = v ? __ldg(p.slice_off + g0 + i) + lane : 0;
                 }
-            }
-            ++kc;
-            if (++pe == piters) {
-                ++pc.r;
-                if (pc.valid()) load_group();
-                else pend = true;
-            }
-        };
-        for (int s = 0; s < kCPref; ++s) {
-            issue_crd();
-            cp_async_commit();
-        }
-        for (uint32_t k = 0; k < total; ++k) {
-            const int s = (int)(k % kRing), cs = (int)(k % kCRing);
-            if (k >= (uint32_t)kRing) mbar_wait(raw_empty(s), ((k / kRing) + 1) & 1);
-            cp_async_wait<kCPref - 1>();  // coordinates of tile k (committed kCPref groups ago)
+                piters = plen[0];
+                pe = 0;
+                if (piters == 0) pend = true;  // groups are sorted by length: nothing follows an empty group
+            };
+            if (!pend) load_group();
+            uint32_t kc = 0;
+            auto issue_crd = [&]() {
+                if (pend) return;
+                const int s = (int)(kc % kCRing);
 #pragma unroll
-            for (int i = 0; i < 4; ++i) {
-                const int u = lane + kWarp * i;
-                const char* r0 = reinterpret_cast<const char*>(p.A[0] + (int64_t)(int)*crd(cs, 0, u) * p.lda);
-                const char* r1 = reinterpret_cast<const char*>(p.A[1] + (int64_t)(int)*crd(cs, 1, u) * p.lda);
-#pragma unroll
-                for (int q = 0; q < NQ; ++q) {
-                    cp_async16_hint(rowc(s, 0, q, u), r0 + 16 * q, pol_rows);
-                    cp_async16_hint(rowc(s, 1, q, u), r1 + 16 * q, pol_rows);
+                for (int i = 0; i < 4; ++i) {
+                    const int u = lane + kWarp * i;
+                    const int64_t idx = poff[i] + (int64_t)pe * kWarp;
+                    if (pe < plen[i]) {
+                        cp_async4_hint(crd(s, 0, u), p.sc[0] + idx, pol_stream);
+                        cp_async4_hint(crd(s, 1, u), p.sc[1] + idx, pol_stream);
+                        cp_async4_hint(crd(s, 2, u), p.sv + idx, pol_stream);
+                    } else {
+                        *crd(s, 0, u) = 0u;  // padding entry: gather row 0 (its result is masked)
+                        *crd(s, 1, u) = 0u;
+                    }
                 }
-                *rowx(s, u) = __uint_as_float(*crd(cs, 2, u));
+                ++kc;
+                if (++pe == piters) {
+                    ++pc.r;
+                    if (pc.valid()) load_group();
+                    else pend = true;
+                }
+            };
+            for (int s = 0; s < kCPref; ++s) {
+                issue_crd();
+                cp_async_commit();
             }
-            cp_async_mbar_arrive(raw_full(s));  // fires when this lane's rows have landed
-            mbar_arrive(raw_full(s));           // x (plain stores), release
-            issue_crd();
-            cp_async_commit();
-        }
-        cp_async_wait<0>();
-    } else if (role == 2) {
-        // ================================================================ MMA issue
-        setmaxnreg_dec();
-        if (lane == 0) {
+            for (uint32_t k = 0; k < total; ++k) {
+                const int s = (int)(k % kRing), cs = (int)(k % kCRing);
+                if (k >= (uint32_t)kRing) mbar_wait(raw_empty(s), ((k / kRing) + 1) & 1);
+                cp_async_wait<kCPref - 1>();  // coordinates of tile k (committed kCPref groups ago)
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                    const int u = lane + kWarp * i;
+                    const char* r0 = reinterpret_cast<const char*>(p.A[0] + (int64_t)(int)*crd(cs, 0, u) * p.lda);
+                    const char* r1 = reinterpret_cast<const char*>(p.A[1] + (int64_t)(int)*crd(cs, 1, u) * p.lda);
+#pragma unroll
+                    for (int q = 0; q < NQ; ++q) {
+                        cp_async16_hint(rowc(s, 0, q, u), r0 + 16 * q, pol_rows);
+                        cp_async16_hint(rowc(s, 1, q, u), r1 + 16 * q, pol_rows);
+                    }
+                    *rowx(s, u) = __uint_as_float(*crd(cs, 2, u));
+                }
+                cp_async_mbar_arrive(raw_full(s));  // fires when this lane's rows have landed
+                mbar_arrive(raw_full(s));           // x (plain stores), release
+                issue_crd();
+                cp_async_commit();
+            }
+            cp_async_wait<0>();
+        } else if (warp == 15 && lane == 0) {
+            // ====================================================== MMA issue
             const uint32_t idesc =
                 (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(NP >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
             // B descriptors (K-major, SWIZZLE_NONE; LBO: next 16-byte K chunk = next core
@@ -408,20 +417,20 @@ __global__ void __launch_bounds__(kThreads, 1) k_update_tc(const UpdateParams<fl
                 dbhi[ks] = umma_desc(smem_u32(sBhi) + ks * 256, 128, KP * 32);
                 dblo[ks] = umma_desc(smem_u32(sBlo) + ks * 256, 128, KP * 32);
             }
-            const uint32_t ahi = tmem + SH::ACOL, alo = tmem + SH::ACOL + KP;  // A in TMEM (lane = entry)
-            // optional trace (tools/trace_tc.py): CTA 0 pipeline 0, tiles [64, 128)
-            long long* const trm = (p.trace && blockIdx.x == 0 && h == 0) ? p.trace + 4 * 512 : nullptr;
+            // optional trace (tools/trace_tc.py): CTA 0, tiles [64, 128)
+            long long* const trm = (p.trace && blockIdx.x == 0) ? p.trace + 4 * 512 : nullptr;
             for (uint32_t k = 0; k < total; ++k) {
-                const int st = (int)(k & 1);
+                const int a = (int)(k % kNA), b = (int)(k % kNT);
                 const bool tr = trm && k >= 64 && k < 128;
                 if (tr) trm[(k - 64) * 8 + 0] = clock64();
-                mbar_wait(a_full, k & 1);                                     // A rows of tile k written
+                mbar_wait(a_full(a), (k / kNA) & 1);  // A rows of tile k written
                 if (tr) trm[(k - 64) * 8 + 1] = clock64();
-                if (k >= 2) mbar_wait(acc_empty(st), ((k - 2) >> 1) & 1);  // TMEM buffer st read (tile k-2)
+                if (k >= (uint32_t)kNT) mbar_wait(acc_empty(b), ((k / kNT) + 1) & 1);  // accumulator b read (tile k-kNT)
                 if (tr) trm[(k - 64) * 8 + 2] = clock64();
                 asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-                // 3xTF32 into TMEM buffer st: lo*hi, hi*lo, hi*hi (small terms first)
-                const uint32_t d = tmem + st * NP;
+                // 3xTF32: lo*hi, hi*lo, hi*hi (small terms first)
+                const uint32_t d = tmem + b * NP;
+                const uint32_t ahi = tmem + SH::ACOL + a * 2 * KP, alo = ahi + KP;
                 uint32_t acc = 0;
 #pragma unroll
                 for (int pr = 0; pr < 3; ++pr)
@@ -431,26 +440,149 @@ __global__ void __launch_bounds__(kThreads, 1) k_update_tc(const UpdateParams<fl
                         acc = 1;
                     }
                 asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
-                                 acc_full(st))
+                                 acc_full(b))
+                             : "memory");
+                asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                                 a_empty(a))
                              : "memory");
                 if (tr) {
                     trm[(k - 64) * 8 + 3] = clock64();
                     if (p.trace[8 * 512 - 1] == 1) {  // latency probe: wait for this tile's MMAs
-                        mbar_wait(acc_full(st), (k >> 1) & 1);
+                        mbar_wait(acc_full(b), (k / kNT) & 1);
                         trm[(k - 64) * 8 + 4] = clock64();
                     }
                 }
             }
         }
+    } else if (warp < 8) {
+        // ================================================================ level 0
+        setmaxnreg_l0();
+        const uint32_t par = (uint32_t)(warp >> 2);  // this warp takes the tiles k = par (mod 2)
+        const uint32_t tm_lane = tmem + ((uint32_t)(w4 * 32) << 16);
+        long long* const trb = (p.trace && blockIdx.x == 0 && lane == 0 && warp < 4) ? p.trace + warp * 512 : nullptr;
+        auto mark = [&](uint32_t k, int ph) {
+            if (trb && k >= 64 && k < 192) trb[((k - 64) >> 1) * 8 + ph] = clock64();
+        };
+        for (uint32_t k = par; k < total; k += 2) {
+            const int b = (int)(k % kNT), s = (int)(k % kRing);
+            mark(k, 0);
+            mbar_wait(acc_full(b), (k / kNT) & 1);
+            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+            mark(k, 1);
+            // the first kBCH chunks of t in flight (the rest follow once those are consumed)
+            uint32_t rb[kBCH][16];
+            const uint32_t taddr = tm_lane + b * NP;
+#pragma unroll
+            for (int ch = 0; ch < kBCH && ch < NCH; ++ch) tmem_ld16(taddr + ch * 16, rb[ch]);
+            // a0 and x of tile k; release the slot (the normal-equation warps read a1)
+            mbar_wait(raw_full(s), (k / kRing) & 1);
+            float a0f[J];
+#pragma unroll
+            for (int q = 0; q < NQ; ++q) {
+                const float4 v = *reinterpret_cast<const float4*>(rowc(s, 0, q, te));
+                const float wv[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+                for (int u = 0; u < 4; ++u)
+                    if (4 * q + u < J) a0f[4 * q + u] = wv[u];
+            }
+            const float x = *rowx(s, te);
+            __syncwarp();
+            if (lane == 0) mbar_arrive(raw_empty(s));
+            mark(k, 2);
+#pragma unroll
+            for (int ch = 0; ch < kBCH && ch < NCH; ++ch) tmem_wait16(rb[ch]);
+            mark(k, 3);
+            // level 0: d[j] = sum_k0 a0[k0] t[k0][j]; t[k0][j] is TMEM column k0*J + j
+            TD d[J];
+            float pf[J];  // fp32 partial sums (G0 > 1)
+#pragma unroll
+            for (int j = 0; j < J; ++j) d[j] = TD(0);
+#pragma unroll
+            for (int cc = 0; cc < J * J; ++cc) {
+                const int k0 = cc / J, j = cc % J;
+                if (cc % (16 * kBCH) == 0 && cc > 0) {  // next batch of chunks
+#pragma unroll
+                    for (int q = 0; q < kBCH; ++q)
+                        if (cc / 16 + q < NCH) tmem_ld16(taddr + (cc / 16 + q) * 16, rb[q]);
+#pragma unroll
+                    for (int q = 0; q < kBCH; ++q)
+                        if (cc / 16 + q < NCH) tmem_wait16(rb[q]);
+                }
+                const float tv = __uint_as_float(rb[(cc / 16) % kBCH][cc % 16]);
+                if constexpr (!LAST64) {
+                    d[j] = fmaf(a0f[k0], tv, d[j]);
+                } else if constexpr (G0 == 1) {
+                    d[j] = fma(TD(a0f[k0]), TD(tv), d[j]);
+                } else {
+                    if (k0 % G0 == 0) pf[j] = a0f[k0] * tv;
+                    else pf[j] = fmaf(a0f[k0], tv, pf[j]);
+                    if (k0 % G0 == G0 - 1 || k0 == J - 1) d[j] = d[j] + TD(pf[j]);
+                }
+            }
+            asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+            __syncwarp();
+            if (lane == 0) mbar_arrive(acc_empty(b));
+            mark(k, 4);
+            // hand delta (fp64) and x to normal-equation warp 8 + w4
+            const int ds = (int)(k % kD);
+            if (k >= (uint32_t)kD) mbar_wait(d_empty(w4, ds), ((k / kD) + 1) & 1);
+#pragma unroll
+            for (int j = 0; j < J; ++j) *dslot(ds, j, te) = double(d[j]);
+            *dslot_x(ds, te) = x;
+            mbar_arrive(d_full(w4, ds));
+            mark(k, 5);
+        }
     } else {
-        // ============================================================ epilogue
-        setmaxnreg_inc();
-        const int te = (warp & 3) * kWarp + lane;  // TMEM lane = segment of the group
-        const uint32_t tm_lane = tmem + ((uint32_t)((warp & 3) * 32) << 16);
+        // ====================================================== normal equations
+        setmaxnreg_ne();
+        const uint32_t tm_lane = tmem + ((uint32_t)(w4 * 32) << 16);
+        // Tile k: once its rows have landed and MMA k - kNA (the last reader of A buffer
+        // k % kNA) has completed, write this thread's A row into TMEM lane te of that
+        // buffer (hi = a rounded to tf32 by two integer ops, lo = a - hi exact; the
+        // tensor core truncates lo to tf32, an error <= 2^-21 |a|; columns k >= J are
+        // zero) and arrive (one arrival per warp) for the MMA warp.
+        auto split = [&](uint32_t k) {
+            const int s = (int)(k % kRing);
+            mbar_wait(raw_full(s), (k / kRing) & 1);
+            // A buffer k % kNA was last read by MMA k - kNA (its own barrier: each phase
+            // is one use of the buffer, so this wait can never be two phases behind)
+            if (k >= (uint32_t)kNA) mbar_wait(a_empty((int)(k % kNA)), ((k / kNA) + 1) & 1);
+            uint32_t hi[16], lo[16];
+#pragma unroll
+            for (int q = 0; q < KQ; ++q) {
+                uint32_t wv[4] = {0u, 0u, 0u, 0u};
+                if (q < NQ) {
+                    const uint4 r = *rowc(s, 1, q, te);
+                    wv[0] = r.x, wv[1] = r.y, wv[2] = r.z, wv[3] = r.w;
+                }
+#pragma unroll
+                for (int v = 0; v < 4; ++v) {
+                    const uint32_t hh = (wv[v] + 0x1000u) & 0xFFFFE000u;
+                    hi[4 * q + v] = hh;
+                    lo[4 * q + v] = __float_as_uint(__uint_as_float(wv[v]) - __uint_as_float(hh));
+                }
+            }
+            const uint32_t ta = tm_lane + SH::ACOL + (k % kNA) * 2 * KP;
+            if constexpr (KP == 16) {
+                tmem_st16(ta, hi);
+                tmem_st16(ta + KP, lo);
+            } else {
+                tmem_st8(ta, hi);
+                tmem_st8(ta + KP, lo);
+            }
+            asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+            asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+            __syncwarp();
+            if (lane == 0) {
+                mbar_arrive(a_full((int)(k % kNA)));
+                mbar_arrive(raw_empty(s));
+            }
+        };
+        for (uint32_t k = 0; k < (uint32_t)kNA && k < total; ++k) split(k);
         auto load_seg = [&](const Sched& s, Seg& g) {
-            const int64_t g0 = s.group() * 4;
-            const int64_t sl = g0 + (warp & 3);
-            g.slot = sl * kWarp + lane;
+            const int64_t g0 = (int64_t)s.group() * 4;
+            const int64_t sl = g0 + w4;
+            g.slot = (int)(sl * kWarp + lane);
             const bool v = sl < p.nslices;
             g.iters = __ldg(p.slice_len + g0);
             g.row = v ? __ldg(p.lane_row + g.slot) : -1;
@@ -506,12 +638,6 @@ __global__ void __launch_bounds__(kThreads, 1) k_update_tc(const UpdateParams<fl
                 dst[(int64_t)(NB + J) * stp] = s2;
             }
         };
-        // optional per-phase clock trace (tools/trace_tc.py): CTA 0, lane 0 of warps 0-3, tiles [64, 128)
-        long long* const trb = (p.trace && blockIdx.x == 0 && lane == 0 && warp < 4) ? p.trace + warp * 512 : nullptr;
-        auto mark = [&](uint32_t k, int ph) {
-            if (trb && k >= 64 && k < 128) trb[(k - 64) * 8 + ph] = clock64();
-        };
-
         Sched sc = s0;
         if (sc.valid()) {
             Seg cur, nxt;
@@ -522,147 +648,37 @@ __global__ void __launch_bounds__(kThreads, 1) k_update_tc(const UpdateParams<fl
             if (nvalid) load_seg(sn, nxt);
             zero();
             int e = 0;
-            // Tile k (its rows have landed): write this thread's A row into TMEM lane te
-            // (hi = a rounded to tf32 by two integer ops, lo = a - hi exact; the tensor
-            // core truncates lo to tf32, an error <= 2^-21 |a|; columns k >= J are zero)
-            // and arrive (one arrival per warp) for the MMA warp.  The single A buffer
-            // was last read by MMA k-1, complete once this thread waited for its
-            // accumulator.
-            auto split = [&](uint32_t k) {
-                const int s = (int)(k % kRing);
-                mbar_wait(raw_full(s), (k / kRing) & 1);
-                uint32_t hi[16], lo[16];
-#pragma unroll
-                for (int q = 0; q < KQ; ++q) {
-                    uint32_t w[4] = {0u, 0u, 0u, 0u};
-                    if (q < NQ) {
-                        const uint4 r = *rowc(s, 1, q, te);
-                        w[0] = r.x, w[1] = r.y, w[2] = r.z, w[3] = r.w;
-                    }
-#pragma unroll
-                    for (int v = 0; v < 4; ++v) {
-                        const uint32_t hh = (w[v] + 0x1000u) & 0xFFFFE000u;
-                        hi[4 * q + v] = hh;
-                        lo[4 * q + v] = __float_as_uint(__uint_as_float(w[v]) - __uint_as_float(hh));
-                    }
-                }
-                const uint32_t ta = tm_lane + SH::ACOL;
-                if constexpr (KP == 16) {
-                    tmem_st16(ta, hi);
-                    tmem_st16(ta + KP, lo);
-                } else {
-                    tmem_st8(ta, hi);
-                    tmem_st8(ta + KP, lo);
-                }
-                asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
-                asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-                __syncwarp();
-                if (lane == 0) mbar_arrive(a_full);
+            long long* const trn = (p.trace && blockIdx.x == 0 && lane == 0 && w4 == 0) ? p.trace + 5 * 512 : nullptr;
+            auto markn = [&](uint32_t k, int ph) {
+                if (trn && k >= 64 && k < 128) trn[(k - 64) * 8 + ph] = clock64();
             };
-            // Software pipeline over tiles: MMA k+1 runs during level 0 and the normal
-            // equations of tile k; MMA k+2 is issued right after and runs during level 0
-            // and the normal equations of tile k+1.
-            float a0f[J];  // a0 of the tile whose level 0 is next (0 for an inactive lane)
-            float x = 0.f;
-            bool act = false;
-            uint32_t rb[2][16];  // TMEM chunks (16 columns) in flight
-            // a0/x of tile k (its rows landed: split(k) waited for them), then release the slot
-            auto fetch_a0 = [&](uint32_t k, bool active) {
-                const int s = (int)(k % kRing);
-#pragma unroll
-                for (int q = 0; q < NQ; ++q) {
-                    const float4 v = *reinterpret_cast<const float4*>(rowc(s, 0, q, te));
-                    const float w[4] = {v.x, v.y, v.z, v.w};
-#pragma unroll
-                    for (int u = 0; u < 4; ++u)
-                        if (4 * q + u < J) a0f[4 * q + u] = active ? w[u] : 0.f;
-                }
-                x = *rowx(s, te);
-                act = active;
-                __syncwarp();
-                if (lane == 0) mbar_arrive(raw_empty(s));
-            };
-            // wait for tile k's accumulator (MMA k complete: the A buffer is free again)
-            auto wait_acc = [&](uint32_t k) {
-                mbar_wait(acc_full((int)(k & 1)), (k >> 1) & 1);
-                asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-            };
-            // start loading tile k's first two chunks
-            auto start_tmem = [&](uint32_t k) {
-                const uint32_t taddr = tm_lane + (k & 1) * NP;
-                tmem_ld16(taddr, rb[0]);
-                if (SH::NCH > 1) tmem_ld16(taddr + 16, rb[1]);
-            };
-            if (total > 0) {
-                split(0);
-                wait_acc(0);
-                start_tmem(0);
-                if (total > 1) split(1);
-                fetch_a0(0, 0 < cur.len);
-            }
             for (uint32_t k = 0; k < total; ++k) {
-                const int buf = (int)(k & 1);
-                mark(k, 0);
-                // ---- level 0 of tile k: d[j] = sum_k0 a0[k0] t[k0][j], t[k0][j] = TMEM column k0*J + j.
-                // Chunks arrive in pairs: one wait covers chunks (2m, 2m+1); chunk 2m+2 is
-                // issued after 2m is consumed, 2m+3 after 2m+1.
-                TD d[J];
-                float pf[J];  // fp32 partial sums (G0 > 1)
-#pragma unroll
-                for (int j = 0; j < J; ++j) d[j] = TD(0);
-                const uint32_t taddr = tm_lane + buf * NP;
-#pragma unroll
-                for (int ch = 0; ch < SH::NCH; ++ch) {
-                    if ((ch & 1) == 0) tmem_wait16(rb[0]), tmem_wait16(rb[1]);
-#pragma unroll
-                    for (int i = 0; i < 16; ++i) {
-                        const int cc = ch * 16 + i;
-                        if (cc >= J * J) continue;
-                        const int k0 = cc / J, j = cc % J;
-                        const float tv = __uint_as_float(rb[ch & 1][i]);
-                        if constexpr (!LAST64) {
-                            d[j] = fmaf(a0f[k0], tv, d[j]);
-                        } else if constexpr (G0 == 1) {
-                            d[j] = fma(TD(a0f[k0]), TD(tv), d[j]);
-                        } else {
-                            if (k0 % G0 == 0) pf[j] = a0f[k0] * tv;
-                            else pf[j] = fmaf(a0f[k0], tv, pf[j]);
-                            if (k0 % G0 == G0 - 1 || k0 == J - 1) d[j] = d[j] + TD(pf[j]);
-                        }
-                    }
-                    if (ch + 2 < SH::NCH) tmem_ld16(taddr + (ch + 2) * 16, rb[ch & 1]);
-                }
-                asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-                __syncwarp();
-                if (lane == 0) mbar_arrive(acc_empty(buf));
-                mark(k, 1);
+                const int ds = (int)(k % kD);
+                markn(k, 0);
+                if (k + kNA < total) split(k + kNA);
+                markn(k, 1);
+                mbar_wait(d_full(w4, ds), (k / kD) & 1);
+                markn(k, 2);
                 double dd[J];
 #pragma unroll
-                for (int j = 0; j < J; ++j) dd[j] = double(d[j]);
+                for (int j = 0; j < J; ++j) dd[j] = *dslot(ds, j, te);
+                const float x = *dslot_x(ds, te);
+                __syncwarp();
+                if (lane == 0) mbar_arrive(d_empty(w4, ds));
+                // an inactive lane (entry beyond its segment) contributes nothing
+                const bool act = e < cur.len;
+#pragma unroll
+                for (int j = 0; j < J; ++j) dd[j] = act ? dd[j] : 0.0;
                 const double xd = act ? double(x) : 0.0;
-                // ---- normal equations of tile k (Eq. 10-11)
-                auto normal_eq = [&]() {
 #pragma unroll
-                    for (int i = 0; i < J; ++i) {
-                        c[i] = fma(xd, dd[i], c[i]);
+                for (int i = 0; i < J; ++i) {
+                    c[i] = fma(xd, dd[i], c[i]);
 #pragma unroll
-                        for (int j = i; j < J; ++j) B[up_idx(i, j, J)] = fma(dd[i], dd[j], B[up_idx(i, j, J)]);
-                    }
-                    s2 = fma(xd, xd, s2);
-                };
-                // ---- then tile k+1's first TMEM chunks and tile k+2's A rows (the single
-                // TMEM A buffer is free once MMA k+1 has completed), whose latencies
-                // overlap each other; then a0/x of tile k+1 (the next entry of the segment,
-                // or the first of the next group's)
-                if (k + 1 < total) wait_acc(k + 1);
-                mark(k, 2);
-                normal_eq();
-                mark(k, 3);
-                bool next_act;
-                if (e + 1 < cur.iters) {
-                    next_act = e + 1 < cur.len;
-                    ++e;
-                } else {
+                    for (int j = i; j < J; ++j) B[up_idx(i, j, J)] = fma(dd[i], dd[j], B[up_idx(i, j, J)]);
+                }
+                s2 = fma(xd, xd, s2);
+                markn(k, 3);
+                if (++e == cur.iters) {
                     finalize(cur);
                     zero();
                     e = 0;
@@ -673,12 +689,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_update_tc(const UpdateParams<fl
                         nvalid = sn.valid();
                         if (nvalid) load_seg(sn, nxt);
                     }
-                    next_act = 0 < cur.len;
                 }
-                if (k + 1 < total) start_tmem(k + 1);
-                if (k + 2 < total) split(k + 2);
-                if (k + 1 < total) fetch_a0(k + 1, next_act);
-                mark(k, 4);
             }
             // the groups after the last one with entries are empty (sorted by length):
             // their rows get a = 0 and SSE 0
@@ -691,8 +702,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_update_tc(const UpdateParams<fl
     }
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     __syncthreads();
-    if (warp == 0)
-        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(misc[0]), "n"(kPipes * SH::TCOLS));
+    if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(SH::TCOLS));
 }
 
 template <int J, bool LAST64, int G0>
@@ -732,8 +742,23 @@ int occupancy_tc(bool literal, size_t gp_bytes) {
         fprintf(stderr, "[ptucker] tc J=%d smem=%d regs=%d (one CTA of %d threads per SM)\n", J, Shape<J>::SMEM,
                 fa.numRegs, kThreads);
     }
-    // one CTA per SM: it allocates all 512 TMEM columns and most of the shared memory
+    // one CTA per SM: it allocates all 512 TMEM columns
     return Shape<J>::SMEM + 1024 <= smem_sm ? 1 : 0;
+}
+
+// Split of the innermost factor into tf32 hi/lo parts (3xTF32 operand), K-padded
+// (diagnostic helper kept for tools/; the update kernel splits in place).
+__global__ void k_split_tf32(const float* __restrict__ A, int64_t I, int lda, int J, int KP, float* __restrict__ hi,
+                             float* __restrict__ lo) {
+    const int64_t total = I * KP;
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t i = t / KP;
+        const int k = (int)(t % KP);
+        const float v = k < J ? A[i * lda + k] : 0.f;
+        const float h = tf32_rna(v);
+        hi[t] = h;
+        lo[t] = tf32_rna(v - h);
+    }
 }
 
 }  // namespace tc

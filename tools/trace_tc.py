@@ -1,8 +1,8 @@
 """Per-phase clock trace of the tensor-core update kernel (CTA 0, lane 0 of the 4
-epilogue warps of pipeline 0, tiles 64..127 of its sequence).  Phases per tile k:
-0 start, 1 after level 0 of tile k (TMEM loads + F2F/DFMA), 2 after waiting for
-MMA k+1, 3 after the normal equations of tile k, 4 (group end) ..., 4 after the
-first TMEM loads of k+1, the A rows of tile k+2 and a0/x of tile k+1.
+level-0 warps, tiles 64..127).  Phases per tile k: 0 start, 1 after waiting for MMA k,
+2 after issuing its TMEM loads + reading a0/x,
+3 after the TMEM wait, 4 after level 0, 5 after handing delta to the normal-equation
+warp.  Also the MMA warp: waits for the A rows and for a free accumulator, issue time.
 
     python tools/trace_tc.py [scale] [l0_group] [latency]"""
 import sys
@@ -30,11 +30,15 @@ if len(sys.argv) > 3:  # latency probe: MMA issue -> completion, measured serial
     pt.ptucker_synchronize()
     f2 = pt.ptucker_debug_trace(8 * 512)[4 * 512:4 * 512 + 512].reshape(64, 8)
     print("MMA latency (issue -> accumulator ready, serialised): median %d cycles" % np.median(f2[:, 4] - f2[:, 3]))
+ne = full[5 * 512:5 * 512 + 512].reshape(64, 8)
+print("normal-equation warp 8, median cycles: split %d, delta wait %d, B/c %d; per tile %d" % (
+    np.median(ne[:, 1] - ne[:, 0]), np.median(ne[:, 2] - ne[:, 1]), np.median(ne[:, 3] - ne[:, 2]),
+    np.median(np.diff(ne[:, 0]))))
 print("MMA warp (pipeline 0), median cycles: a_full wait %d, acc_empty wait %d, issue %d; per tile %d" % (
     np.median(m[:, 1] - m[:, 0]), np.median(m[:, 2] - m[:, 1]), np.median(m[:, 3] - m[:, 2]),
     np.median(np.diff(m[:, 0]))))
-tr = pt.ptucker_debug_trace(4 * 512).reshape(4, 64, 8)[:, :, [0, 1, 2, 3, 4]]
-names = ["L0(k)", "wait mma(k+1)", "B/c(k)", "group end+tmem+split+a0", "->next"]
+tr = pt.ptucker_debug_trace(4 * 512).reshape(4, 64, 8)[:, :, :6]
+names = ["mma wait", "ld+a0", "tmem wait", "L0", "handoff", "->next"]
 for w in range(4):
     t = tr[w]
     ok = t[:, 0] > 0
