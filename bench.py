@@ -36,18 +36,85 @@ UNIT = "entries/s"
 
 
 # ----------------------------------------------------------------------------- helpers
-def algorithmic_work(N: int, J: int, policy: str):
-    """FMAs per observed entry per mode update: innermost TTV
-    stage J^N (fp32 unless F64); outer level L (J^(L+2) FMAs, L = 0..N-3) in fp64
-    when the policy puts it there (F32-A: none, F32-B: level 0, F32-C: all);
-    normal equations J(J+1)/2 + J + 1 (fp64).  Returns (fp32 FMAs, fp64 FMAs)."""
+def measured_peaks():
+    try:
+        return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        return {}
+
+
+def roofline(N, J, policy, info, l0_group, nsm, clk_mhz, entries, launch_s, dtype, cfg_name):
+    """Roofline of the row-update kernel: T_roof = max over the pipes the
+    shipped kernel uses of (algorithmic work on that pipe / its peak), per launch.
+
+    Algorithmic work per observed entry: the delta contraction's FMAs
+    (innermost stage J^N, outer stages J^(L+2)), placed on the pipe this implementation
+    runs them on, plus the fp64 normal equations J(J+1)/2 + J + 1; compulsory HBM bytes
+    4(N-1) + s_v (the SELL entry stream).  Peaks: fp32/fp64 derived from unit counts x
+    clock (148 SMs x 128 / 64 FMA/clk; tools/pipe_probe.cu measures 123 and 63.2), tf32
+    tensor = measured bf16 (MEASURED_PEAKS.json) x 1/2 (nominal tf32/bf16 ratio), HBM =
+    measured copy bandwidth.  The fp32->fp64 conversions (XU pipe, 16/clk/SM measured) and
+    the tensor work the 3xTF32 split and K/N padding add are reported as diagnostics: they
+    are costs of the precision policy, not algorithmic work."""
+    mp = measured_peaks()
+    p32 = nsm * 128 * 2 * clk_mhz * 1e6 / 1e12
+    p64 = nsm * 64 * 2 * clk_mhz * 1e6 / 1e12
+    ptc = 0.5 * mp.get("bf16_tflops", 1590.0)
+    bw = mp.get("hbm_gbs", 6650.0)
     inner = J ** N
     levels = [J ** (L + 2) for L in range(N - 2)]
     bc = J * (J + 1) // 2 + J + 1
+    tc = bool(info.get("tensor_cores")) and N == 3 and dtype == "f32"
+    xu = 0
     if policy == "F64":
-        return 0, inner + sum(levels) + bc
-    n64 = {"F32-A": 0, "F32-B": 1, "F32-C": N - 2}[policy]
-    return inner + sum(levels[n64:]), sum(levels[:n64]) + bc
+        w32, w64, wtc = 0, inner + sum(levels) + bc, 0
+    elif tc:
+        # inner stage on tcgen05; level 0 (J^2) fp64 per term (l0_group 1) or fp32 partial sums
+        # of l0_group terms added in fp64 (J*ceil(J/g) DADDs)
+        g = l0_group if policy != "F32-A" else J
+        nparts = -(-J // g)
+        if g == 1:
+            w32, w64 = 0, J * J + bc
+            xu = J * J + J + 1
+        else:
+            w32, w64 = J * J, J * nparts + bc
+            xu = J * nparts + 1
+        wtc = inner
+    else:
+        n64 = {"F32-A": 0, "F32-B": 1, "F32-C": N - 2}[policy]
+        w32, w64, wtc = inner + sum(levels[n64:]), sum(levels[:n64]) + bc, 0
+        xu = sum(J ** (L + 1) for L in range(min(n64, N - 2)))  # fp32 inputs of the fp64 levels
+    sv = 8 if dtype == "f64" else 4
+    hbm_bytes = (4 * (N - 1) + sv) * entries
+    t = {"fp32": 2 * w32 * entries / (p32 * 1e12), "fp64": 2 * w64 * entries / (p64 * 1e12),
+         "tensor_tf32": 2 * wtc * entries / (ptc * 1e12), "hbm": hbm_bytes / (bw * 1e9)}
+    pipe = max(t, key=t.get)
+    peak = {"fp32": p32, "fp64": p64, "tensor_tf32": ptc, "hbm": bw}[pipe]
+    work = {"fp32": 2 * w32, "fp64": 2 * w64, "tensor_tf32": 2 * wtc}.get(pipe)
+    if pipe == "hbm":
+        achieved, unit, bound = hbm_bytes / launch_s / 1e9, "GB/s", "hbm"
+    else:
+        achieved, unit = work * entries / launch_s / 1e12, "TFLOP/s"
+        bound = "tensor" if pipe == "tensor_tf32" else "alu"
+    r = {"bound": bound, "achieved": achieved, "peak": peak, "unit": unit, "frac": achieved / peak,
+         "traffic": load_traffic(cfg_name), "pipe": pipe,
+         "kernel": "k_update_tc (tcgen05 3xTF32 inner stage + level 0 + fp64 normal equations + Cholesky)" if tc
+         else "k_update (fused TTV + fp64 normal equations + Cholesky)",
+         "peak_source": {"fp32": f"derived: {nsm} SMs x 128 FMA/clk x 2 x {clk_mhz:.0f} MHz",
+                         "fp64": f"derived: {nsm} SMs x 64 FMA/clk x 2 x {clk_mhz:.0f} MHz (pipe_probe: 63.2/clk measured)",
+                         "tensor_tf32": "MEASURED_PEAKS bf16_tflops x 0.5 (nominal tf32/bf16)",
+                         "hbm": "MEASURED_PEAKS hbm_gbs"}[pipe],
+         "work_per_entry": {"fp32_fma": w32, "fp64_fma": w64, "tc_mac": wtc, "hbm_bytes": 4 * (N - 1) + sv},
+         "roof_ms_by_pipe": {k: v * 1e3 for k, v in t.items()}, "roof_ms": t[pipe] * 1e3}
+    if xu:
+        xu_peak = nsm * 16 * clk_mhz * 1e6
+        r["xu_conversions_per_entry"] = xu
+        r["xu_floor_ms"] = xu * entries / xu_peak * 1e3
+    if tc:
+        kp, np_ = -(-J // 8) * 8, -(-(J * J) // 16) * 16
+        r["tc_executed_mac_per_entry"] = 3 * kp * np_
+        r["tc_executed_floor_ms"] = 2 * 3 * kp * np_ * entries / (ptc * 1e12) * 1e3
+    return r
 
 
 def clocks_sampler(device: int):
@@ -267,31 +334,14 @@ def run_ours(args, cfg):
 
     # roofline of the dominant kernel (the fused row update), per launch
     policy = info["policy"]
-    f32, f64 = algorithmic_work(N, J, policy)
     nsm = torch.cuda.get_device_properties(local).multi_processor_count
     clk_max = (clocks or {}).get("sm_max_mhz") or 1965.0
-    p32 = nsm * 128 * 2 * clk_max * 1e6 / 1e12   # TFLOP/s fp32 FMA pipe (unit counts x max clock)
-    p64 = nsm * 64 * 2 * clk_max * 1e6 / 1e12     # TFLOP/s fp64
     entries_per_launch = cfg.nnz / world           # each rank's launch covers its row block of one mode
     avg_launch_s = (upd_ms / max(upd_n, 1)) / 1e3
-    if f32 > 0:
-        achieved = 2 * f32 * entries_per_launch / avg_launch_s / 1e12
-        peak, bound_pipe = p32, "fp32"
-    else:
-        achieved = 2 * f64 * entries_per_launch / avg_launch_s / 1e12
-        peak, bound_pipe = p64, "fp64"
-    t_roof = max(2 * f32 * entries_per_launch / (p32 * 1e12), 2 * f64 * entries_per_launch / (p64 * 1e12))
-    roof = {
-        "bound": "alu", "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
-        "traffic": load_traffic(cfg.name),
-        "kernel": "k_update (fused TTV + fp64 normal equations + Cholesky)", "pipe": bound_pipe,
-        "peak_source": f"derived: {nsm} SMs x {'128' if bound_pipe == 'fp32' else '64'} FMA/clk x 2 x {clk_max:.0f} MHz",
-        "fp64_achieved_tflops": 2 * f64 * entries_per_launch / avg_launch_s / 1e12, "fp64_peak_tflops": p64,
-        "frac_of_pipe_roofline_time": t_roof / avg_launch_s,
-        "avg_launch_ms": avg_launch_s * 1e3, "launches": upd_n,
-        "update_share_of_step": upd_ms / ms, "finalize_ms_per_step": fin_ms / args.steps,
-        "ms_per_step_by_kernel": per_mode,
-    }
+    roof = roofline(N, J, policy, info, args.l0_group, nsm, clk_max, entries_per_launch, avg_launch_s,
+                    cfg.dtype, cfg.name)
+    roof.update({"avg_launch_ms": avg_launch_s * 1e3, "launches": upd_n, "update_share_of_step": upd_ms / ms,
+                 "finalize_ms_per_step": fin_ms / args.steps, "ms_per_step_by_kernel": per_mode})
 
     # e2e: the whole job through the public API from pinned host buffers
     e2e = None

@@ -4,11 +4,14 @@
 #include <nccl.h>
 
 #include <algorithm>
+#include <chrono>
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
 #include <map>
+#include <mutex>
+#include <thread>
 #include <string>
 #include <type_traits>
 #include <vector>
@@ -502,9 +505,25 @@ int ptucker_set_option(const char* key, int64_t value) {
     return fail(PTUCKER_EINVAL, "unknown option '%s'", key);
 }
 
+namespace {
+// PTUCKER_DEBUG: phase times of ptucker_init on stderr
+struct PhaseClock {
+    bool on = getenv("PTUCKER_DEBUG") != nullptr;
+    std::chrono::steady_clock::time_point t = std::chrono::steady_clock::now();
+    void lap(const char* what, cudaStream_t st = nullptr) {
+        if (!on) return;
+        if (st) cudaStreamSynchronize(st);
+        const auto now = std::chrono::steady_clock::now();
+        fprintf(stderr, "[ptucker] init %-28s %8.2f ms\n", what, std::chrono::duration<double, std::milli>(now - t).count());
+        t = now;
+    }
+};
+}  // namespace
+
 int ptucker_init(const int32_t* coords, const void* vals, int32_t vals_dtype, int64_t nnz, int32_t order,
                  const int64_t* dims, const int32_t* core_dims, double lambda, uint64_t seed) {
     // ---- validation (synchronous, EINVAL) ----
+    PhaseClock pc;
     if (!coords || !vals || !dims || !core_dims) return fail(PTUCKER_EINVAL, "null argument");
     if (vals_dtype != PTUCKER_F32 && vals_dtype != PTUCKER_F64) return fail(PTUCKER_EINVAL, "bad vals_dtype");
     if (order < 2 || order > kMaxN) return fail(PTUCKER_EINVAL, "order %d not in 2..%d", order, kMaxN);
@@ -516,21 +535,50 @@ int ptucker_init(const int32_t* coords, const void* vals, int32_t vals_dtype, in
     }
     const int J = core_dims[0];
     if (J < 1) return fail(PTUCKER_EINVAL, "core dim must be >= 1");
-    for (int64_t e = 0; e < nnz; ++e)
-        for (int n = 0; n < order; ++n) {
-            const int32_t c = coords[e * order + n];
-            if (c < 0 || c >= dims[n])
-                return fail(PTUCKER_EINVAL, "coordinate %d of entry %lld out of range", n, (long long)e);
-        }
     const int esz = vals_dtype == PTUCKER_F64 ? 8 : 4;
-    for (int64_t e = 0; e < nnz; ++e) {
-        const double v = esz == 8 ? ((const double*)vals)[e] : ((const float*)vals)[e];
-        if (!std::isfinite(v)) return fail(PTUCKER_EINVAL, "value of entry %lld is not finite", (long long)e);
+    {
+        // coordinates in range and values finite: first offending entry, scanned by
+        // all host threads (the check is O(|Omega| N) and must not dominate init)
+        int64_t bad_c = INT64_MAX, bad_v = INT64_MAX;
+        int bad_n = 0;
+        std::mutex mu;
+        auto scan = [&](int64_t e0, int64_t e1) {
+            int64_t bc = INT64_MAX, bv = INT64_MAX;
+            int bn = 0;
+            for (int64_t e = e0; e < e1 && bc == INT64_MAX; ++e)
+                for (int n = 0; n < order; ++n) {
+                    const int32_t c = coords[e * order + n];
+                    if (c < 0 || c >= dims[n]) {
+                        bc = e;
+                        bn = n;
+                        break;
+                    }
+                }
+            for (int64_t e = e0; e < e1; ++e) {
+                const double v = esz == 8 ? ((const double*)vals)[e] : ((const float*)vals)[e];
+                if (!std::isfinite(v)) {
+                    bv = e;
+                    break;
+                }
+            }
+            std::lock_guard<std::mutex> lk(mu);
+            if (bc < bad_c) bad_c = bc, bad_n = bn;
+            if (bv < bad_v) bad_v = bv;
+        };
+        const int64_t nt = std::max<int64_t>(1, std::min<int64_t>(std::thread::hardware_concurrency(), nnz / (1 << 20)));
+        std::vector<std::thread> th;
+        for (int64_t t = 1; t < nt; ++t) th.emplace_back(scan, nnz * t / nt, nnz * (t + 1) / nt);
+        scan(0, nnz / nt);
+        for (auto& x : th) x.join();
+        if (bad_c != INT64_MAX)
+            return fail(PTUCKER_EINVAL, "coordinate %d of entry %lld out of range", bad_n, (long long)bad_c);
+        if (bad_v != INT64_MAX) return fail(PTUCKER_EINVAL, "value of entry %lld is not finite", (long long)bad_v);
     }
     {
         if (!find_update_kernel(vals_dtype, 1, order, J))
             return fail(PTUCKER_EINVAL, "(N=%d, J=%d) is not a compiled kernel shape", order, J);
     }
+    pc.lap("validation (host)");
     // ---- fresh context ----
     free_all();
     CK(cudaGetDevice(&g.device));
@@ -620,6 +668,7 @@ int ptucker_init(const int32_t* coords, const void* vals, int32_t vals_dtype, in
         if (tmax > 0) CK(A.alloc(&g.smp_T, (size_t)tmax * 8));
         if (tmax > 0) CK(A.alloc(&g.smp_T32, (size_t)tmax * 4));
     }
+    pc.lap("allocation + factor init", S());
     // ---- device index of every mode ----
     DeviceArena input;
     int32_t* d_coords = nullptr;
@@ -628,6 +677,7 @@ int ptucker_init(const int32_t* coords, const void* vals, int32_t vals_dtype, in
     CK(input.alloc(&d_vals, (size_t)nnz * esz));
     CK(cudaMemcpyAsync(d_coords, coords, (size_t)nnz * order * sizeof(int32_t), cudaMemcpyHostToDevice, S()));
     CK(cudaMemcpyAsync(d_vals, vals, (size_t)nnz * esz, cudaMemcpyHostToDevice, S()));
+    pc.lap("H2D of the COO input", S());
     if (!g.comm) {  // no communicator: a single rank, or an emulated rank of a partition (tests)
         g.world = g.emu_world;
         g.rank = g.emu_rank;
@@ -635,12 +685,14 @@ int ptucker_init(const int32_t* coords, const void* vals, int32_t vals_dtype, in
     for (int n = 0; n < order; ++n) {
         ModeIndex& m = g.mi[n];
         CK(build_mode_csr(d_coords, nnz, order, n, dims[n], m, g.arena, g.scratch, S()));
+        pc.lap("CSR (sort, row_ptr)", S());
         m.bounds.assign((size_t)g.world + 1, 0);
         partition_rows(m.h_row_ptr.data(), dims[n], g.world, m.bounds.data());
         const int smode = g.smp[n].kind == 1 ? g.smp[n].s1 : -1;  // group each row by the small mode
         m.Is = smode >= 0 ? dims[smode] : 1;
         CK(build_mode_sell(d_coords, d_vals, esz, nnz, order, n, J, g.seg_len, m.bounds[g.rank],
                            m.bounds[g.rank + 1], smode, m, g.arena, g.scratch, S()));
+        pc.lap("SELL segments + scatter", S());
     }
     CK(A.alloc((void**)&g.lit_part, std::max<int64_t>(g.mi[0].nslices * 32, 1) * sizeof(double)));
 
