@@ -116,6 +116,17 @@ __device__ __forceinline__ void tmem_st8(uint32_t addr, const uint32_t (&r)[16])
                  : "memory");
 }
 
+// float -> double with integer operations (SHF, LOP3, IADD3 and a shift) instead of
+// the XU conversion: exact for normal floats of either sign; a zero or subnormal
+// input becomes +-2^-127 * (1 + m) (an absolute error below 1.2e-38, irrelevant
+// next to the O(1) terms of the level-0 sums it feeds).  Inputs here are finite
+// tensor-core outputs.
+__device__ __forceinline__ double f2d_int(float f) {
+    const uint32_t u = __float_as_uint(f);
+    const uint32_t hi = ((uint32_t)((int32_t)u >> 3) & 0x8FFFFFFFu) + 0x38000000u;
+    return __hiloint2double((int)hi, (int)(u << 29));
+}
+
 __device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count));
 }
@@ -512,7 +523,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_update_tc(const UpdateParams<fl
                 if constexpr (!LAST64) {
                     d[j] = fmaf(a0f[k0], tv, d[j]);
                 } else if constexpr (G0 == 1) {
-                    d[j] = fma(TD(a0f[k0]), TD(tv), d[j]);
+                    // half of the fp32 -> fp64 conversions by integer ops on the ALU pipe, the
+                    // other half on the (quarter-rate) XU pipe, so neither pipe saturates
+                    d[j] = fma(TD(a0f[k0]), (cc & 1) ? f2d_int(tv) : TD(tv), d[j]);
                 } else {
                     if (k0 % G0 == 0) pf[j] = a0f[k0] * tv;
                     else pf[j] = fmaf(a0f[k0], tv, pf[j]);

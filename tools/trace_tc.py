@@ -47,3 +47,19 @@ for w in range(4):
     print(f"warp {w}: entries {len(t)}; median cycles per phase: " +
           ", ".join(f"{n} {int(np.median(d[:, i]))}" for i, n in enumerate(names)) +
           f"; per entry {int(np.median(np.diff(t[:, 0])))}")
+
+# ---- critical path of the even tiles 72..120 on the common SM clock
+L0 = full[0:512].reshape(64, 8)          # level-0 warp 0: row m = tile 64 + 2m
+MM = full[4 * 512:4 * 512 + 512].reshape(64, 8)   # MMA warp: row m = tile 64 + m
+NE = full[5 * 512:5 * 512 + 512].reshape(64, 8)   # normal-equation warp 8: row m = iteration 64 + m
+KNA = 4
+print("tile: split(k) done -> MMA a_full ok -> MMA issued -> L0 acc_full ok -> L0 handoff done -> NE delta ok  (cycles after split)")
+for k in range(72, 122, 6):
+    if k % 2:
+        continue
+    j = k - KNA - 64
+    if j < 0:
+        continue
+    t0 = NE[j, 1]
+    row = [MM[k - 64, 1], MM[k - 64, 3], L0[(k - 64) // 2, 1], L0[(k - 64) // 2, 5], NE[k - 64, 2]]
+    print(k, [int(x - t0) for x in row])
