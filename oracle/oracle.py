@@ -57,6 +57,8 @@ def lib():
             "or_thin_qr": (C.c_int, [i64, C.c_int, P, P]),
             "or_core_mode_product": (None, [C.c_int, P, P, C.c_int, P]),
             "or_orthogonalize": (C.c_int, [C.c_int, P, P, P, P, P]),
+            "or_partial_errors": (None, [C.c_int, P, P, P, P, P, P, i64, P, P, C.c_int]),
+            "or_truncate": (i64, [i64, P, P, P, f64]),
         }
         for name, (res, args) in sig.items():
             fn = getattr(_lib, name)
@@ -276,3 +278,31 @@ def als(t: Tensor, m: Model, lam: float, iters: int, threads: int = 0):
         errs.append(error(t, m, threads))
         losses.append(loss(t, m, lam, threads))
     return np.array(errs), np.array(losses)
+
+
+# ---------------------------------------------------------------------- P-Tucker-Approx
+def partial_errors(t: Tensor, m: Model, present=None, threads: int = 0) -> np.ndarray:
+    """Eq. 13 for every core entry (C order); 0 for absent entries."""
+    gsize = int(np.prod(m.J))
+    pres = np.ones(gsize, np.uint8) if present is None else np.ascontiguousarray(present, np.uint8)
+    R = np.zeros(gsize, np.float64)
+    lib().or_partial_errors(m.N, _p(m.J), _p(m.G), _p(m.A_all), _p(m.dims), _p(t.coords), _p(t.vals), t.nnz,
+                            _p(pres), _p(R), int(threads))
+    return R
+
+
+def truncate(m: Model, R, present, p: float) -> int:
+    """Alg. 4 lines 3-4: zero the top floor(p|G|) present entries of G by R
+    (descending, ties by ascending index; at least one entry stays).  `present` (uint8,
+    C order) and m.G are updated in place.  Returns the number removed."""
+    assert present.dtype == np.uint8 and present.flags["C_CONTIGUOUS"]
+    R = np.ascontiguousarray(R, np.float64)
+    G = m.G.reshape(-1)
+    k = int(lib().or_truncate(G.size, _p(G), _p(present), _p(R), float(p)))
+    return k
+
+
+def truncate_core(t: Tensor, m: Model, present, p: float, threads: int = 0):
+    """Alg. 4: scores, then truncation.  Returns (R, removed)."""
+    R = partial_errors(t, m, present, threads)
+    return R, truncate(m, R, present, p)

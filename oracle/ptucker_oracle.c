@@ -16,6 +16,8 @@
  *   - reconstruction (Eq. 4), error (Eq. 5)  P:331-341, Alg. 2 line 4 P:499
  *   - loss (Eq. 6)
  *   - QR + core update (Eq. 7-8)             P:470-479, Alg. 2 lines 8-11 P:504-508
+ *   - P-Tucker-Approx: partial error R(beta) (Eq. 13) and core truncation
+ *     (Alg. 4)                               P:656-700, Alg. 2 lines 5-6 P:500-502
  * Readings where the paper is silent are listed in DESIGN.md ("Readings").
  *
  * Pins (tests/test_oracle_pins.py) check every function here against values
@@ -409,4 +411,96 @@ int or_orthogonalize(int N, const int32_t* J, double* G, double* A_all, const in
         roff += (int64_t)J[n] * J[n];
     }
     return rc;
+}
+
+/* ------------------------------------------------------------------------ */
+/* P-Tucker-Approx: partial reconstruction error and truncation. */
+/* ------------------------------------------------------------------------ */
+
+/* Eq. 13, second line, Alg. 4 lines 1-2: for every core
+ * entry beta with present[beta] != 0,
+ *   R(beta) = sum_alpha t_beta (-2 X_alpha + t_beta + 2 sum_{gamma != beta} t_gamma),
+ *   t_gamma = G_gamma prod_n a^(n)_{i_n j_n}   (gamma over the core, C order);
+ * absent entries (truncated earlier: G_gamma = 0) get R = 0.  Per observed entry the
+ * t_gamma are formed once and sum_{gamma != beta} t_gamma = x_hat - t_beta with
+ * x_hat = sum_gamma t_gamma (Eq. 4) -- the "one shared pass" of reading R27.
+ * Entries are taken in input order in fixed 4096-entry chunks whose partial
+ * sums are added in chunk order (independent of the thread count). */
+void or_partial_errors(int N, const int32_t* J, const double* G, const double* A_all, const int64_t* dims,
+                       const int32_t* coords, const double* vals, int64_t nnz, const uint8_t* present,
+                       double* R, int nthreads) {
+    const int64_t CH = 4096;
+    int64_t off[OR_MAXN + 1];
+    factor_offsets(N, dims, J, off);
+    const int64_t gsize = core_size(N, J);
+    const int64_t nch = (nnz + CH - 1) / CH;
+    double* part = (double*)calloc((size_t)(nch > 0 ? nch : 1) * (size_t)gsize, sizeof(double));
+#ifdef _OPENMP
+    if (nthreads <= 0) nthreads = omp_get_max_threads();
+#pragma omp parallel for schedule(dynamic, 1) num_threads(nthreads)
+#endif
+    for (int64_t ch = 0; ch < nch; ++ch) {
+        double* t = (double*)malloc((size_t)gsize * sizeof(double));
+        double* Rc = part + ch * gsize;
+        int64_t e1 = (ch + 1) * CH < nnz ? (ch + 1) * CH : nnz;
+        for (int64_t e = ch * CH; e < e1; ++e) {
+            const int32_t* coord = coords + e * N;
+            int jj[OR_MAXN];
+            for (int k = 0; k < N; ++k) jj[k] = 0;
+            double xhat = 0.0;
+            for (int64_t b = 0; b < gsize; ++b) {
+                double prod = G[b];
+                for (int k = 0; k < N; ++k) prod *= A_all[off[k] + (int64_t)coord[k] * J[k] + jj[k]];
+                t[b] = prod;
+                xhat += prod;
+                for (int k = N - 1; k >= 0; --k) {
+                    if (++jj[k] < J[k]) break;
+                    jj[k] = 0;
+                }
+            }
+            const double x = vals[e];
+            for (int64_t b = 0; b < gsize; ++b)
+                if (present[b]) Rc[b] += t[b] * (-2.0 * x + t[b] + 2.0 * (xhat - t[b]));
+        }
+        free(t);
+    }
+    (void)nthreads;
+    for (int64_t b = 0; b < gsize; ++b) {
+        double s = 0.0;
+        for (int64_t ch = 0; ch < nch; ++ch) s += part[ch * gsize + b];
+        R[b] = present[b] ? s : 0.0;
+    }
+    free(part);
+}
+
+/* Alg. 4 lines 3-4: among the present entries, sort R(beta) in
+ * descending order (ties: ascending C-order index, reading R28) and remove the
+ * top floor(p |G|) of them, never leaving fewer than one (reading R29): G_beta = 0,
+ * present[beta] = 0.  |G| counts the present entries.  Returns the number removed. */
+static const double* g_trunc_R;
+static int trunc_cmp(const void* a, const void* b) {
+    const int64_t i = *(const int64_t*)a, j = *(const int64_t*)b;
+    if (g_trunc_R[i] > g_trunc_R[j]) return -1;
+    if (g_trunc_R[i] < g_trunc_R[j]) return 1;
+    return i < j ? -1 : (i > j ? 1 : 0);
+}
+
+int64_t or_truncate(int64_t gsize, double* G, uint8_t* present, const double* R, double p) {
+    int64_t n = 0;
+    for (int64_t b = 0; b < gsize; ++b) n += present[b] != 0;
+    int64_t k = (int64_t)floor(p * (double)n);
+    if (k > n - 1) k = n - 1;
+    if (k <= 0) return 0;
+    int64_t* idx = (int64_t*)malloc((size_t)n * sizeof(int64_t));
+    int64_t m = 0;
+    for (int64_t b = 0; b < gsize; ++b)
+        if (present[b]) idx[m++] = b;
+    g_trunc_R = R;
+    qsort(idx, (size_t)n, sizeof(int64_t), trunc_cmp);
+    for (int64_t r = 0; r < k; ++r) {
+        G[idx[r]] = 0.0;
+        present[idx[r]] = 0;
+    }
+    free(idx);
+    return k;
 }

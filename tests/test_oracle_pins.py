@@ -414,3 +414,103 @@ def test_worked_example_advisory(orc):
     Rs = orc.orthogonalize(m)
     np.testing.assert_allclose(Rs[0], ex["R0_after_orthogonalize"], rtol=1e-10, atol=1e-13)
     assert np.abs(np_predict(m.G, m.factors, t.coords) - before).max() < 1e-14
+
+
+# ---------------------------------------------------------------- P-Tucker-Approx
+def np_partial_error_definition(G, A, coords, vals):
+    """Eq. 13, FIRST line: R(beta) = err with beta - err without beta,
+    two full reconstructions per beta (numpy), not the oracle's simplified second line."""
+    full = vals - np_predict(G, A, coords)
+    e_full = float(full @ full)
+    out = np.zeros(G.size)
+    for b in range(G.size):
+        G2 = G.copy().reshape(-1)
+        G2[b] = 0.0
+        r = vals - np_predict(G2.reshape(G.shape), A, coords)
+        out[b] = e_full - float(r @ r)
+    return out
+
+
+@pytest.mark.parametrize("dims,J", [((6, 5, 4), (2, 3, 2)), ((5, 4, 3, 3), (2, 2, 2, 2)), ((7, 6), (3, 2))])
+def test_partial_error_equals_two_reconstructions(orc, dims, J):
+    """Eq. 13: the simplified second line the oracle evaluates equals the
+    first line (difference of two full reconstructions) computed independently."""
+    rng = np.random.default_rng(11)
+    G = rng.standard_normal(J)
+    A = [rng.standard_normal((d, j)) for d, j in zip(dims, J)]
+    coords = np.stack([rng.integers(0, d, 40) for d in dims], 1).astype(np.int32)
+    vals = rng.standard_normal(40)
+    R = orc.partial_errors(orc.Tensor(coords, vals, dims), orc.Model(G, A))
+    ref = np_partial_error_definition(G, A, coords, vals)
+    np.testing.assert_allclose(R, ref, rtol=1e-9, atol=1e-9 * np.abs(ref).max())
+
+
+def test_partial_error_special_cases(orc):
+    """S (partial_error examples): a single present entry reconstructing every value
+    exactly gives R = -sum X^2; an entry with G_beta = 0 gives R = 0."""
+    rng = np.random.default_rng(3)
+    dims, J = (5, 4, 3), (2, 2, 2)
+    A = [rng.random((d, j)) + 0.1 for d, j in zip(dims, J)]
+    coords = np.stack([rng.integers(0, d, 25) for d in dims], 1).astype(np.int32)
+    G = np.zeros(J)
+    G[1, 0, 1] = 1.7
+    vals = np_predict(G, A, coords)  # exact fit by the single entry
+    pres = np.zeros(8, np.uint8)
+    pres[np.ravel_multi_index((1, 0, 1), J)] = 1
+    R = orc.partial_errors(orc.Tensor(coords, vals, dims), orc.Model(G, A), pres)
+    b = np.ravel_multi_index((1, 0, 1), J)
+    assert abs(R[b] - (-(vals @ vals))) <= 1e-12 * (vals @ vals)
+    assert np.all(R[np.arange(8) != b] == 0.0)
+    G2 = rng.random(J)
+    G2[0, 1, 1] = 0.0
+    R2 = orc.partial_errors(orc.Tensor(coords, vals, dims), orc.Model(G2, A))
+    assert R2[np.ravel_multi_index((0, 1, 1), J)] == 0.0
+
+
+def test_truncation_selection_examples(orc):
+    """S (truncate_core examples), Alg. 4 lines 3-4: scores [5, -2, 3, 0] with
+    p = 0.5 remove the entries scored 5 and 3 (|G| 4 -> 2); p = 0.2 removes
+    floor(0.8) = 0; a single remaining entry is never removed; ties go to the lower index."""
+    def run(scores, p, present=None):
+        G = np.arange(1.0, len(scores) + 1.0)
+        m = orc.Model(G.reshape(len(scores), 1, 1), [np.ones((1, len(scores))), np.ones((1, 1)), np.ones((1, 1))])
+        pres = np.ones(len(scores), np.uint8) if present is None else np.array(present, np.uint8)
+        k = orc.truncate(m, np.array(scores, float), pres, p)
+        return k, pres, m.G.reshape(-1)
+    k, pres, G = run([5.0, -2.0, 3.0, 0.0], 0.5)
+    assert k == 2 and list(pres) == [0, 1, 0, 1] and G[0] == 0 and G[2] == 0 and G[1] == 2 and G[3] == 4
+    k, pres, _ = run([5.0, -2.0, 3.0, 0.0], 0.2)
+    assert k == 0 and pres.all()
+    k, pres, _ = run([1.0, 9.0], 0.9, present=[0, 1])          # |G| = 1: nothing removed
+    assert k == 0 and list(pres) == [0, 1]
+    k, pres, _ = run([2.0, 7.0, 7.0, 7.0, 1.0], 0.4)            # floor(2.0) = 2 of three ties at 7
+    assert k == 2 and list(pres) == [1, 0, 0, 1, 1]
+
+
+def test_truncation_sequence_against_full_sort(orc):
+    """Alg. 2 lines 5-6 + Alg. 4: over several ALS iterations the
+    removed set equals the top floor(p|G|) of an independent numpy sort of the
+    definition-computed scores; |G| follows max(1, |G| - floor(p|G|))."""
+    rng = np.random.default_rng(5)
+    dims, J, lam, p = (12, 10, 9), (3, 3, 2), 0.05, 0.2
+    coords = np.stack([rng.integers(0, d, 150) for d in dims], 1).astype(np.int32)
+    vals = rng.random(150)
+    t = orc.Tensor(coords, vals, dims)
+    m = orc.init_model(dims, J, seed=2, prec=1)
+    pres = np.ones(int(np.prod(J)), np.uint8)
+    n_present = pres.size
+    for it in range(6):
+        for n in range(3):
+            orc.update_mode(t, m, n, lam)
+        A = [m.A(n).copy() for n in range(3)]
+        ref = np_partial_error_definition(m.G.copy(), A, coords, vals)
+        before = pres.copy()
+        R, k = orc.truncate_core(t, m, pres, p)
+        idx = np.flatnonzero(before)
+        order = idx[np.lexsort((idx, -ref[idx]))]
+        k_ref = min(int(np.floor(p * n_present)), n_present - 1)
+        assert k == k_ref
+        assert set(np.flatnonzero(before & ~pres)) == set(order[:k_ref].tolist())
+        n_present -= k
+        assert int(pres.sum()) == n_present == max(1, len(idx) - int(np.floor(p * len(idx))))
+        assert np.all(m.G.reshape(-1)[pres == 0] == 0.0)
