@@ -114,6 +114,21 @@ int ptucker_error_literal(double* out);
  * Requires I_n >= J_n; a rank-deficient A^(n) gives PTUCKER_ENUMERIC. */
 int ptucker_orthogonalize(void);
 
+/* P-Tucker-Approx.  Partial reconstruction error of every core entry,
+ * Eq. 13: R(beta) = sum over Omega of t_beta (-2 X + t_beta + 2 sum_{gamma!=beta}
+ * t_gamma), t_gamma = G_gamma prod_n a^(n)_{i_n gamma_n}, for the current state, summed over
+ * ranks.  out: host, prod J doubles in C order; NaN for entries already truncated.
+ * Computed in fp64 (approx.cu); synchronises. */
+int ptucker_core_scores(double* out);
+/* Alg. 4 with readings R28/R29: scores as above, then the
+ * floor(p * |G|) present entries with the largest R (ties: lower C-order index) are set to
+ * zero and marked truncated, never leaving fewer than one; *removed (may be null) receives
+ * the count.  p in (0, 1) else PTUCKER_EINVAL.  Alg. 2 runs it after each iteration's error
+ * (P:500-502); the final ptucker_orthogonalize makes G dense again. */
+int ptucker_truncate_core(double p, int64_t* removed);
+/* Number of core entries not truncated (|G| of Alg. 4). */
+int ptucker_core_nnz(int64_t* nnz);
+
 /* State access (host buffers of exactly I_n*J_n or prod J elements, context precision). */
 int ptucker_get_factor(int32_t n, void* out);
 int ptucker_set_factor(int32_t n, const void* in);

@@ -120,6 +120,11 @@ struct Ctx {
     } smp[kMaxN];
     void* smp_T = nullptr;                   // device table (largest over modes), fp64
     void* smp_T32 = nullptr;                 // fp32 copy of a kind-2 table
+    // P-Tucker-Approx (approx.cu): presence of the core entries (C order) and lazy scratch
+    std::vector<uint8_t> core_present;
+    double *ax_G64 = nullptr, *ax_A0 = nullptr, *ax_W = nullptr, *ax_W2 = nullptr, *ax_E = nullptr,
+           *ax_part = nullptr, *ax_UV = nullptr;
+    void** ax_ptrs = nullptr;  // device: sc[0..N-2] of mode 0, then A[0..N-1]
     int nsm = 148;
     int grid_upd = 0, grid_lit = 0;
     int64_t launches = 0;        // kernels this library launched since init (gpu_launches evidence)
@@ -363,6 +368,9 @@ void free_all() {
     g.smp_T32 = nullptr;
     g.tc_hi = g.tc_lo = nullptr;
     g.lit_part = g.red_part = g.red_out = g.qr = g.qd = nullptr;
+    g.ax_G64 = g.ax_A0 = g.ax_W = g.ax_W2 = g.ax_E = g.ax_part = g.ax_UV = nullptr;
+    g.ax_ptrs = nullptr;
+    g.core_present.clear();
     g.d_fail = g.d_qrfail = nullptr;
     g.d_work = nullptr;
     g.launches = 0;
@@ -621,6 +629,7 @@ int ptucker_init(const int32_t* coords, const void* vals, int32_t vals_dtype, in
         CK(A.alloc((void**)&g.sse_row[n], dims[n] * sizeof(double)));
         CK(cudaMemsetAsync(g.sse_row[n], 0, dims[n] * sizeof(double), S()));
     }
+    g.core_present.assign((size_t)gsize, 1);
     int rc = rebuild_gp();
     if (rc) return rc;
     // ---- small-mode precontraction plans, order 4 only ----
@@ -833,6 +842,7 @@ int ptucker_orthogonalize(void) {
     });
     if (rc) return rc;
     g.sse_mode = -1;
+    std::fill(g.core_present.begin(), g.core_present.end(), (uint8_t)1);  // G x_n R is dense again
     return sync_and_check();
 }
 
@@ -876,9 +886,119 @@ int ptucker_set_core(const void* in) {
     rc = rebuild_gp();
     if (rc) return rc;
     g.sse_mode = -1;
+    g.core_present.assign((size_t)gsize, 1);  // a pushed core is dense (no truncation history)
     CK(cudaStreamSynchronize(S()));
     return PTUCKER_OK;
 }
+
+// ---------------------------------------------------------------- P-Tucker-Approx
+namespace {
+// R(beta) (Eq. 13) of every core entry into R (C order; NaN for truncated entries).
+int compute_core_scores(std::vector<double>& R) {
+    const int N = g.N, J = g.J;
+    int64_t K1 = 1;
+    for (int n = 1; n < N; ++n) K1 *= J;
+    const int64_t gsize = K1 * J;
+    const int nsplit = 64;
+    const ModeIndex& m = g.mi[0];
+    const int64_t nlanes = m.nslices * 32;
+    if (!g.ax_UV) {
+        CK(g.arena.alloc((void**)&g.ax_G64, gsize * sizeof(double)));
+        CK(g.arena.alloc((void**)&g.ax_A0, std::max<int64_t>(nlanes, 1) * J * sizeof(double)));
+        CK(g.arena.alloc((void**)&g.ax_W, std::max<int64_t>(nlanes, 1) * K1 * sizeof(double)));
+        CK(g.arena.alloc((void**)&g.ax_W2, std::max<int64_t>(nlanes, 1) * K1 * sizeof(double)));
+        CK(g.arena.alloc((void**)&g.ax_E, std::max<int64_t>(m.nslots, 1) * sizeof(double)));
+        CK(g.arena.alloc((void**)&g.ax_part, (size_t)2 * nsplit * gsize * sizeof(double)));
+        CK(g.arena.alloc((void**)&g.ax_ptrs, 2 * kMaxN * sizeof(void*)));
+        CK(g.arena.alloc((void**)&g.ax_UV, 2 * gsize * sizeof(double)));
+        void* h[2 * kMaxN] = {nullptr};
+        for (int k = 0; k < N - 1; ++k) h[k] = m.sc[k];
+        for (int k = 0; k < N; ++k) h[kMaxN + k] = g.A[k];
+        CK(cudaMemcpyAsync(g.ax_ptrs, h, sizeof(h), cudaMemcpyHostToDevice, S()));
+    }
+    int rc = timed("approx_scores", [&]() -> int {
+        launch_approx_uv(N, J, g.esz, m.nslices, m.slice_off, m.lane_row, m.lane_len, (const int32_t* const*)g.ax_ptrs,
+                         m.sv, (const void* const*)(g.ax_ptrs + kMaxN), g.lda, g.G, g.ax_G64, g.ax_A0, g.ax_W,
+                         g.ax_W2, g.ax_E, g.ax_part, nsplit, g.ax_UV, g.nsm, S());
+        g.launches += m.nslices > 0 ? 4 : 3;
+        CK(cudaGetLastError());
+        return PTUCKER_OK;
+    });
+    if (rc) return rc;
+    if (g.world > 1 && g.comm) NK(ncclAllReduce(g.ax_UV, g.ax_UV, (size_t)(2 * gsize), ncclDouble, ncclSum, g.comm, S()));
+    std::vector<double> UV((size_t)(2 * gsize));
+    std::vector<char> graw((size_t)(gsize * g.esz));
+    CK(cudaMemcpyAsync(UV.data(), g.ax_UV, UV.size() * sizeof(double), cudaMemcpyDeviceToHost, S()));
+    CK(cudaMemcpyAsync(graw.data(), g.G, graw.size(), cudaMemcpyDeviceToHost, S()));
+    CK(cudaStreamSynchronize(S()));
+    R.assign((size_t)gsize, std::nan(""));
+    for (int64_t b = 0; b < gsize; ++b) {
+        if (!g.core_present[b]) continue;
+        const double Gb = g.esz == 8 ? ((const double*)graw.data())[b] : (double)((const float*)graw.data())[b];
+        R[b] = 2.0 * Gb * UV[b] - Gb * Gb * UV[gsize + b];
+    }
+    return PTUCKER_OK;
+}
+}  // namespace
+
+int ptucker_core_scores(double* out) {
+    int rc = require_init();
+    if (rc) return rc;
+    if (!out) return fail(PTUCKER_EINVAL, "null buffer");
+    std::vector<double> R;
+    rc = compute_core_scores(R);
+    if (rc) return rc;
+    memcpy(out, R.data(), R.size() * sizeof(double));
+    return PTUCKER_OK;
+}
+
+int ptucker_truncate_core(double p, int64_t* removed) {
+    int rc = require_init();
+    if (rc) return rc;
+    if (!(p > 0.0 && p < 1.0)) return fail(PTUCKER_EINVAL, "truncation rate p must be in (0, 1)");
+    std::vector<double> R;
+    rc = compute_core_scores(R);
+    if (rc) return rc;
+    const int64_t gsize = (int64_t)R.size();
+    std::vector<int64_t> idx;
+    for (int64_t b = 0; b < gsize; ++b)
+        if (g.core_present[b]) idx.push_back(b);
+    const int64_t n = (int64_t)idx.size();
+    int64_t k = (int64_t)std::floor(p * (double)n);  // reading R29: floor(p |G|), at least one entry stays
+    if (k > n - 1) k = n - 1;
+    if (k < 0) k = 0;
+    // reading R28: descending R, ties by ascending C-order index (stable sort of an ascending list)
+    std::stable_sort(idx.begin(), idx.end(), [&](int64_t a, int64_t b) { return R[a] > R[b]; });
+    if (k > 0) {
+        std::vector<char> graw((size_t)(gsize * g.esz));
+        CK(cudaMemcpyAsync(graw.data(), g.G, graw.size(), cudaMemcpyDeviceToHost, S()));
+        CK(cudaStreamSynchronize(S()));
+        for (int64_t r = 0; r < k; ++r) {
+            const int64_t b = idx[r];
+            g.core_present[b] = 0;
+            if (g.esz == 8) ((double*)graw.data())[b] = 0.0;
+            else ((float*)graw.data())[b] = 0.f;
+        }
+        CK(cudaMemcpyAsync(g.G, graw.data(), graw.size(), cudaMemcpyHostToDevice, S()));
+        rc = rebuild_gp();
+        if (rc) return rc;
+        g.sse_mode = -1;
+        CK(cudaStreamSynchronize(S()));
+    }
+    if (removed) *removed = k;
+    return PTUCKER_OK;
+}
+
+int ptucker_core_nnz(int64_t* nnz) {
+    int rc = require_init();
+    if (rc) return rc;
+    if (!nnz) return fail(PTUCKER_EINVAL, "null out");
+    int64_t c = 0;
+    for (uint8_t v : g.core_present) c += v != 0;
+    *nnz = c;
+    return PTUCKER_OK;
+}
+
 
 int ptucker_get_mode_index(int32_t n, int64_t* row_ptr, int64_t* perm) {
     int rc = require_init();

@@ -1,0 +1,198 @@
+// approx.cu -- P-Tucker-Approx: partial reconstruction error R(beta) of
+// every core entry (Eq. 13) for the core truncation of Alg. 4.
+//
+// Eq. 13's second line, t_beta(alpha) (-2 X_alpha + t_beta + 2 sum_{gamma != beta} t_gamma)
+// with t_gamma = G_gamma K_gamma(alpha), K_gamma(alpha) = prod_n a^(n)_{i_n gamma_n} and
+// sum_{gamma != beta} t_gamma = x_hat - t_beta, is  2 G_beta K_beta e_alpha - G_beta^2 K_beta^2
+// with e_alpha = x_hat_alpha - X_alpha.  Summed over Omega:
+//     R(beta) = 2 G_beta U_beta - G_beta^2 V_beta,
+//     U = sum_alpha e_alpha K(alpha),   V = sum_alpha K(alpha)^2   (J^N each).
+// Grouping the entries by their mode-0 segment s (this rank's SELL segments of
+// mode 0, row i_s) splits K = a^(0)_{i_s} (x) K'(alpha) with K' over the other modes:
+//     U[j0, b'] = sum_s a^(0)_{i_s j0}   W_s[b'],    W_s  = sum_{alpha in s} e_alpha K'(alpha)
+//     V[j0, b'] = sum_s a^(0)_{i_s j0}^2 W2_s[b'],   W2_s = sum_{alpha in s} K'(alpha)^2
+// so the per-entry work is J^(N-1) (not J^N) and the J x J^(N-1) outer sums over
+// segments are a small reduction.  x_hat_alpha = sum_b' K'_b' H_s[b'] with
+// H_s = a^(0)_{i_s} G_(0) (once per segment).  Everything is fp64 (the scores rank
+// the core entries; the oracle computes them in fp64 too).
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "internal.cuh"
+
+namespace pt {
+namespace {
+
+constexpr int kApproxWarps = 8;  // warps per block of k_approx_seg (one SELL segment per warp at a time)
+
+// One warp per SELL segment of mode 0 (pad lanes: zero outputs).
+template <typename TS>
+__global__ void __launch_bounds__(kApproxWarps * 32) k_approx_seg(
+    int N, int J, int K1, int64_t nlanes, const int64_t* slice_off, const int32_t* lane_row,
+    const int32_t* lane_len, const int32_t* const* sc, const TS* sv, const TS* const* A, int lda,
+    const double* G64, double* A0seg, double* W, double* W2, double* Eslot) {
+    // dynamic shared memory: per warp H[K1] (padded to 8 doubles) and the entry's rows of
+    // modes 1..N-1 (fp64, [4][16])
+    extern __shared__ double smem[];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int k1p = (K1 + 7) / 8 * 8;
+    double* H = smem + warp * (k1p + 64);
+    double (*sRw)[16] = reinterpret_cast<double (*)[16]>(H + k1p);
+    for (int64_t seg = (int64_t)blockIdx.x * kApproxWarps + warp; seg < nlanes;
+         seg += (int64_t)gridDim.x * kApproxWarps) {
+        const int row = lane_row[seg];
+        const int len = row >= 0 ? lane_len[seg] : 0;
+        double* w = W + seg * K1;
+        double* w2 = W2 + seg * K1;
+        if (row < 0) {
+            for (int b = lane; b < K1; b += 32) w[b] = w2[b] = 0.0;
+            if (lane < J) A0seg[seg * J + lane] = 0.0;
+            continue;
+        }
+        const int64_t base = slice_off[seg >> 5] + (seg & 31);
+        // a^(0) of the segment's row and H = a0 G_(0)
+        double a0[16];
+        for (int j = 0; j < J; ++j) a0[j] = (double)A[0][(int64_t)row * lda + j];
+        if (lane < J) A0seg[seg * J + lane] = a0[lane];
+        for (int b = lane; b < K1; b += 32) {
+            double h = 0.0;
+            for (int j = 0; j < J; ++j) h = fma(a0[j], G64[(int64_t)j * K1 + b], h);
+            H[b] = h;
+        }
+        __syncwarp();
+        // K'_b' for the staged rows: b' = (b_1, ..., b_{N-1}) in C order
+        auto kprod = [&](int b, const double (*r)[16]) {
+            double k = 1.0;
+            for (int n = N - 1; n >= 1; --n) {
+                k *= r[n - 1][b % J];
+                b /= J;
+            }
+            return k;
+        };
+        auto stage = [&](int e) {
+            const int64_t slot = base + (int64_t)e * 32;
+            if (lane < (N - 1) * J) {
+                const int n = lane / J, j = lane % J;
+                const int c = sc[n][slot];
+                sRw[n][j] = (double)A[n + 1][(int64_t)c * lda + j];
+            }
+            __syncwarp();
+        };
+        // pass 1: e_alpha = x_hat - X for every entry of the segment
+        for (int e = 0; e < len; ++e) {
+            stage(e);
+            double part = 0.0;
+            for (int b = lane; b < K1; b += 32) part = fma(kprod(b, sRw), H[b], part);
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
+            if (lane == 0) Eslot[base + (int64_t)e * 32] = part - (double)sv[base + (int64_t)e * 32];
+            __syncwarp();
+        }
+        __syncwarp();
+        // pass 2: W = sum e K', W2 = sum K'^2, eight b' per lane per sweep
+        for (int b0 = 0; b0 < K1; b0 += 256) {
+            double acc[8], acc2[8];
+#pragma unroll
+            for (int m = 0; m < 8; ++m) acc[m] = acc2[m] = 0.0;
+            for (int e = 0; e < len; ++e) {
+                stage(e);
+                const double ee = Eslot[base + (int64_t)e * 32];
+#pragma unroll
+                for (int m = 0; m < 8; ++m) {
+                    const int b = b0 + lane + 32 * m;
+                    if (b < K1) {
+                        const double k = kprod(b, sRw);
+                        acc[m] = fma(ee, k, acc[m]);
+                        acc2[m] = fma(k, k, acc2[m]);
+                    }
+                }
+                __syncwarp();
+            }
+#pragma unroll
+            for (int m = 0; m < 8; ++m) {
+                const int b = b0 + lane + 32 * m;
+                if (b < K1) {
+                    w[b] = acc[m];
+                    w2[b] = acc2[m];
+                }
+            }
+        }
+        __syncwarp();
+    }
+}
+
+// U[j0*K1 + b'] = sum_s A0seg[s][j0] W[s][b'],  V = sum_s A0seg[s][j0]^2 W2[s][b'];
+// blockIdx.y = a contiguous range of segments (per-range partials, fixed-order sum).
+__global__ void k_approx_outer(int J, int K1, int64_t nseg, int64_t per, const double* A0seg, const double* W,
+                               const double* W2, double* part) {
+    const int64_t out = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t nout = (int64_t)J * K1;
+    if (out >= nout) return;
+    const int j0 = (int)(out / K1), b = (int)(out % K1);
+    const int64_t s0 = (int64_t)blockIdx.y * per, s1 = s0 + per < nseg ? s0 + per : nseg;
+    double u = 0.0, v = 0.0;
+    for (int64_t s = s0; s < s1; ++s) {
+        const double a = A0seg[s * J + j0];
+        u = fma(a, W[s * K1 + b], u);
+        v = fma(a * a, W2[s * K1 + b], v);
+    }
+    part[((int64_t)blockIdx.y * 2 + 0) * nout + out] = u;
+    part[((int64_t)blockIdx.y * 2 + 1) * nout + out] = v;
+}
+
+__global__ void k_approx_sum(int64_t nout, int nsplit, const double* part, double* UV) {
+    const int64_t out = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (out >= nout) return;
+    double u = 0.0, v = 0.0;
+    for (int y = 0; y < nsplit; ++y) {
+        u += part[((int64_t)y * 2 + 0) * nout + out];
+        v += part[((int64_t)y * 2 + 1) * nout + out];
+    }
+    UV[out] = u;
+    UV[nout + out] = v;
+}
+
+template <typename TS>
+__global__ void k_to_f64(const TS* in, double* out, int64_t n) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        out[i] = (double)in[i];
+}
+
+}  // namespace
+
+// U, V (J^N each, C order over the core) of this rank's entries of mode 0 into UV[2*J^N].
+// Scratch: A0seg [nlanes*J], W, W2 [nlanes*K1], Eslot [nslots], part [2*nsplit*J^N], G64 [J^N].
+void launch_approx_uv(int N, int J, int elem_bytes, int64_t nslices, const int64_t* slice_off,
+                      const int32_t* lane_row, const int32_t* lane_len, const int32_t* const* d_sc, const void* sv,
+                      const void* const* d_A, int lda, const void* G, double* G64, double* A0seg, double* W,
+                      double* W2, double* Eslot, double* part, int nsplit, double* UV, int nsm, cudaStream_t st) {
+    int K1 = 1;
+    for (int n = 1; n < N; ++n) K1 *= J;
+    const int64_t gsize = (int64_t)K1 * J;
+    const int64_t nlanes = nslices * 32;
+    if (elem_bytes == 8) k_to_f64<double><<<64, 256, 0, st>>>((const double*)G, G64, gsize);
+    else k_to_f64<float><<<64, 256, 0, st>>>((const float*)G, G64, gsize);
+    if (nlanes > 0) {
+        int grid = (int)((nlanes + kApproxWarps - 1) / kApproxWarps);
+        if (grid > nsm * 8) grid = nsm * 8;
+        const size_t smem = (size_t)kApproxWarps * ((K1 + 7) / 8 * 8 + 64) * sizeof(double);
+        cudaFuncSetAttribute(k_approx_seg<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaFuncSetAttribute(k_approx_seg<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (elem_bytes == 8)
+            k_approx_seg<double><<<grid, kApproxWarps * 32, smem, st>>>(N, J, K1, nlanes, slice_off, lane_row, lane_len,
+                                                                    d_sc, (const double*)sv,
+                                                                    (const double* const*)d_A, lda, G64, A0seg, W,
+                                                                    W2, Eslot);
+        else
+            k_approx_seg<float><<<grid, kApproxWarps * 32, smem, st>>>(N, J, K1, nlanes, slice_off, lane_row, lane_len,
+                                                                   d_sc, (const float*)sv, (const float* const*)d_A,
+                                                                   lda, G64, A0seg, W, W2, Eslot);
+    }
+    const int64_t per = nlanes > 0 ? (nlanes + nsplit - 1) / nsplit : 1;
+    dim3 g2((unsigned)((gsize + 127) / 128), (unsigned)nsplit);
+    k_approx_outer<<<g2, 128, 0, st>>>(J, K1, nlanes, per, A0seg, W, W2, part);
+    k_approx_sum<<<(unsigned)((gsize + 127) / 128), 128, 0, st>>>(gsize, nsplit, part, UV);
+}
+
+}  // namespace pt

@@ -36,6 +36,11 @@ bool launch_smp2_update(const void* params, int elem_bytes, int J, const double*
 void launch_smp_table1(const void* G, const void* As, int lda, int64_t Is, int J, int n, int a, int b, int s, void* T,
                        int elem_bytes, cudaStream_t st);
 bool launch_table_update(const void* params, int elem_bytes, int J, int nsm, cudaStream_t st);
+// ---- P-Tucker-Approx scores (approx.cu): U = sum e K, V = sum K^2 over this rank's mode-0 entries ----
+void launch_approx_uv(int N, int J, int elem_bytes, int64_t nslices, const int64_t* slice_off,
+                      const int32_t* lane_row, const int32_t* lane_len, const int32_t* const* d_sc, const void* sv,
+                      const void* const* d_A, int lda, const void* G, double* G64, double* A0seg, double* W,
+                      double* W2, double* Eslot, double* part, int nsplit, double* UV, int nsm, cudaStream_t st);
 // ---- index build helpers (index.cu) ----
 void launch_extract_col(const int32_t* coords, int64_t nnz, int N, int n, int32_t* keys, int32_t* iota,
                         cudaStream_t st);

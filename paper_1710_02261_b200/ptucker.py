@@ -34,6 +34,9 @@ _SIGS = {
     "ptucker_error": (C.c_int, [C.POINTER(C.c_double)]),
     "ptucker_error_literal": (C.c_int, [C.POINTER(C.c_double)]),
     "ptucker_orthogonalize": (C.c_int, []),
+    "ptucker_core_scores": (C.c_int, [C.c_void_p]),
+    "ptucker_truncate_core": (C.c_int, [C.c_double, C.POINTER(C.c_int64)]),
+    "ptucker_core_nnz": (C.c_int, [C.POINTER(C.c_int64)]),
     "ptucker_get_factor": (C.c_int, [C.c_int32, C.c_void_p]),
     "ptucker_set_factor": (C.c_int, [C.c_int32, C.c_void_p]),
     "ptucker_get_core": (C.c_int, [C.c_void_p]),
@@ -158,6 +161,26 @@ def ptucker_error_literal() -> float:
 
 def ptucker_orthogonalize():
     _check(load().ptucker_orthogonalize())
+
+
+def ptucker_core_scores() -> np.ndarray:
+    """Eq. 13 partial reconstruction error of every core entry (C order, NaN = truncated)."""
+    out = np.empty(tuple(_state["J"]), np.float64)
+    _check(load().ptucker_core_scores(_ptr(out)))
+    return out
+
+
+def ptucker_truncate_core(p: float) -> int:
+    """Alg. 4: zero the top floor(p|G|) core entries by R(beta); returns the number removed."""
+    k = C.c_int64()
+    _check(load().ptucker_truncate_core(float(p), C.byref(k)))
+    return int(k.value)
+
+
+def ptucker_core_nnz() -> int:
+    k = C.c_int64()
+    _check(load().ptucker_core_nnz(C.byref(k)))
+    return int(k.value)
 
 
 def ptucker_get_factor(n: int, out: np.ndarray | None = None) -> np.ndarray:
