@@ -300,6 +300,8 @@ def run_ours(args, cfg):
     for _ in range(args.warmup):
         pt.ptucker_sweep()
         pt.ptucker_error()
+        if args.approx > 0:
+            pt.ptucker_truncate_core(args.approx)
     barrier_sync()
     pt.ptucker_set_option("time_kernels", 1)
     pt.ptucker_reset_kernel_stats()
@@ -314,6 +316,8 @@ def run_ours(args, cfg):
     for _ in range(args.steps):
         pt.ptucker_sweep()
         errs.append(pt.ptucker_error())
+        if args.approx > 0:
+            pt.ptucker_truncate_core(args.approx)  # P-Tucker-Approx: Alg. 2 lines 5-6
     ev1.record(stream)
     barrier_sync()
     clocks = clocks_summary(clk)
@@ -321,6 +325,7 @@ def run_ours(args, cfg):
     launches = pt.ptucker_info()["kernel_launches"] - launches0
     upd_ms, upd_n = pt.ptucker_kernel_stats("update")
     fin_ms, _ = pt.ptucker_kernel_stats("finalize")
+    apx_ms, apx_n = pt.ptucker_kernel_stats("approx_scores") if args.approx > 0 else (0.0, 0)
     per_mode = {f"update_m{n}": round(pt.ptucker_kernel_stats(f"update_m{n}")[0] / args.steps, 4) for n in range(N)}
     per_mode.update({f"finalize_m{n}": round(pt.ptucker_kernel_stats(f"finalize_m{n}")[0] / args.steps, 4)
                      for n in range(N)})
@@ -340,6 +345,9 @@ def run_ours(args, cfg):
     avg_launch_s = (upd_ms / max(upd_n, 1)) / 1e3
     roof = roofline(N, J, policy, info, args.l0_group, nsm, clk_max, entries_per_launch, avg_launch_s,
                     cfg.dtype, cfg.name)
+    if args.approx > 0:
+        roof["approx"] = {"p": args.approx, "scores_ms_per_step": apx_ms / args.steps,
+                          "core_nnz_after": pt.ptucker_core_nnz()}
     roof.update({"avg_launch_ms": avg_launch_s * 1e3, "launches": upd_n, "update_share_of_step": upd_ms / ms,
                  "finalize_ms_per_step": fin_ms / args.steps, "ms_per_step_by_kernel": per_mode})
 
@@ -400,6 +408,8 @@ def main():
     ap.add_argument("--seg-len", type=int, default=256)
     ap.add_argument("--tc", type=int, default=1, choices=[0, 1], help="tensor-core inner stage for order-3 fp32")
     ap.add_argument("--l0-group", type=int, default=1, choices=[1, 2, 5], help="tensor-core level-0 grouping (1 = fp64 per term, g = fp32 partial sums of g terms)")
+    ap.add_argument("--approx", type=float, default=0.0,
+                    help="P-Tucker-Approx: truncate the core by rate p after every iteration (0 = P-Tucker)")
     ap.add_argument("--ref-seconds", type=float, default=12.0)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")

@@ -129,6 +129,23 @@ int ptucker_truncate_core(double p, int64_t* removed);
 /* Number of core entries not truncated (|G| of Alg. 4). */
 int ptucker_core_nnz(int64_t* nnz);
 
+/* Eq. 4, "predict values of missing entries": x_hat for n query
+ * coordinates.  coords: host, n x N int32 (row-major, in range else PTUCKER_EINVAL);
+ * out: host, n doubles.  fp64 over the dense core; synchronises. */
+int ptucker_predict(const int32_t* coords, int64_t n, double* out);
+/* Held-out test RMSE (§4.4): sqrt(sum (x - x_hat)^2 / n) over n test entries
+ * (host coords n x N int32, host vals n of vals_dtype = the context's precision); n >= 1. */
+int ptucker_test_rmse(const int32_t* coords, const void* vals, int32_t vals_dtype, int64_t n, double* out);
+
+/* Alg. 2 from the current state: e_0 = error; repeat { ptucker_sweep (line 3);
+ * e_t = error (line 4, Eq. 5); if approx_p > 0, ptucker_truncate_core(approx_p) (lines 5-6) }
+ * until t == max_iters, |e_t - e_{t-1}| < tol * e_{t-1} or e_t <= tol * ||x|| (reading R30,
+ * ||x|| = sqrt of the sum of squares of the observed values); then
+ * ptucker_orthogonalize if `orthogonalize` (lines 8-11).  errors: host, max_iters + 1 doubles
+ * (e_0 .. e_T, may be null); *iters = T (may be null).  tol >= 0, 0 <= approx_p < 1. */
+int ptucker_run(int32_t max_iters, double tol, double approx_p, int32_t orthogonalize, double* errors,
+                int32_t* iters);
+
 /* State access (host buffers of exactly I_n*J_n or prod J elements, context precision). */
 int ptucker_get_factor(int32_t n, void* out);
 int ptucker_set_factor(int32_t n, const void* in);

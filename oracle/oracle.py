@@ -59,6 +59,8 @@ def lib():
             "or_orthogonalize": (C.c_int, [C.c_int, P, P, P, P, P]),
             "or_partial_errors": (None, [C.c_int, P, P, P, P, P, P, i64, P, P, C.c_int]),
             "or_truncate": (i64, [i64, P, P, P, f64]),
+            "or_predict_many": (None, [C.c_int, P, P, P, P, P, i64, P]),
+            "or_test_rmse": (f64, [C.c_int, P, P, P, P, P, P, i64]),
         }
         for name, (res, args) in sig.items():
             fn = getattr(_lib, name)
@@ -306,3 +308,47 @@ def truncate_core(t: Tensor, m: Model, present, p: float, threads: int = 0):
     """Alg. 4: scores, then truncation.  Returns (R, removed)."""
     R = partial_errors(t, m, present, threads)
     return R, truncate(m, R, present, p)
+
+
+# ---------------------------------------------------------------------- prediction, test RMSE, Alg. 2 driver
+def predict_many(m: Model, coords) -> np.ndarray:
+    """Eq. 4 for query coordinates (n x N)."""
+    coords = np.ascontiguousarray(coords, np.int32)
+    out = np.zeros(coords.shape[0], np.float64)
+    lib().or_predict_many(m.N, _p(m.J), _p(m.G), _p(m.A_all), _p(m.dims), _p(coords), coords.shape[0], _p(out))
+    return out
+
+
+def test_rmse(m: Model, coords, vals) -> float:
+    """Held-out RMSE (§4.4)."""
+    coords = np.ascontiguousarray(coords, np.int32)
+    vals = np.ascontiguousarray(vals, np.float64)
+    assert coords.shape[0] >= 1
+    return float(lib().or_test_rmse(m.N, _p(m.J), _p(m.G), _p(m.A_all), _p(m.dims), _p(coords), _p(vals),
+                                    coords.shape[0]))
+
+
+def run(t: Tensor, m: Model, lam: float, max_iters: int, tol: float, approx_p: float = 0.0,
+        orthogonalize: bool = True, threads: int = 0):
+    """Alg. 2 (P:496-508): e_0 = error; repeat {update A^(1..N) (line 3); e_t = error (line 4);
+    if Approx: truncate the core (lines 5-6)} until t = max_iters or
+    |e_t - e_(t-1)| < tol * e_(t-1) or e_t <= tol ||x|| (reading R30); then QR + core update
+    (lines 8-11).  Returns (errors e_0..e_T, T, present mask)."""
+    present = np.ones(int(np.prod(m.J)), np.uint8)
+    xnorm = float(np.sqrt(t.vals @ t.vals))
+    errs = [error(t, m, threads)]
+    it = 0
+    while it < max_iters:
+        for n in range(m.N):
+            update_mode(t, m, n, lam, threads)
+        e = error(t, m, threads)
+        it += 1
+        errs.append(e)
+        if approx_p > 0:
+            truncate_core(t, m, present, approx_p, threads)
+        if abs(e - errs[-2]) < tol * errs[-2] or e <= tol * xnorm:
+            break
+    if orthogonalize:
+        globals()["orthogonalize"](m)
+        present[:] = 1
+    return np.array(errs), it, present

@@ -504,3 +504,20 @@ int64_t or_truncate(int64_t gsize, double* G, uint8_t* present, const double* R,
     free(idx);
     return k;
 }
+
+/* Eq. 4 for n query coordinates (prediction of missing entries). */
+void or_predict_many(int N, const int32_t* J, const double* G, const double* A_all, const int64_t* dims,
+                     const int32_t* coords, int64_t n, double* out) {
+    for (int64_t q = 0; q < n; ++q) out[q] = or_predict(N, J, G, A_all, dims, coords + q * N);
+}
+
+/* Held-out test RMSE (§4.4): sqrt( sum_q (x_q - x_hat_q)^2 / n ), n >= 1. */
+double or_test_rmse(int N, const int32_t* J, const double* G, const double* A_all, const int64_t* dims,
+                    const int32_t* coords, const double* vals, int64_t n) {
+    double s = 0.0;
+    for (int64_t q = 0; q < n; ++q) {
+        double r = vals[q] - or_predict(N, J, G, A_all, dims, coords + q * N);
+        s += r * r;
+    }
+    return sqrt(s / (double)n);
+}

@@ -82,6 +82,7 @@ struct Ctx {
     int N = 0, J = 0, prec = 0, esz = 4;
     int64_t nnz = 0;
     int64_t dims[kMaxN] = {0};
+    double xnorm = 0.0;  // sqrt(sum x^2) over Omega (convergence floor of ptucker_run)
     double lambda = 0.0;
     uint64_t seed = 0;
     int lda = 0, gp_elems = 0;
@@ -136,6 +137,7 @@ struct Ctx {
 };
 
 Ctx g;
+double g_xnorm_pending = 0.0;
 
 cudaStream_t S() { return g.stream; }
 
@@ -549,10 +551,12 @@ int ptucker_init(const int32_t* coords, const void* vals, int32_t vals_dtype, in
         // all host threads (the check is O(|Omega| N) and must not dominate init)
         int64_t bad_c = INT64_MAX, bad_v = INT64_MAX;
         int bad_n = 0;
+        double xx = 0.0;  // sum of squares of the values (scale of the data, reading R30)
         std::mutex mu;
         auto scan = [&](int64_t e0, int64_t e1) {
             int64_t bc = INT64_MAX, bv = INT64_MAX;
             int bn = 0;
+            double sq = 0.0;
             for (int64_t e = e0; e < e1 && bc == INT64_MAX; ++e)
                 for (int n = 0; n < order; ++n) {
                     const int32_t c = coords[e * order + n];
@@ -568,10 +572,12 @@ int ptucker_init(const int32_t* coords, const void* vals, int32_t vals_dtype, in
                     bv = e;
                     break;
                 }
+                sq += v * v;
             }
             std::lock_guard<std::mutex> lk(mu);
             if (bc < bad_c) bad_c = bc, bad_n = bn;
             if (bv < bad_v) bad_v = bv;
+            xx += sq;
         };
         const int64_t nt = std::max<int64_t>(1, std::min<int64_t>(std::thread::hardware_concurrency(), nnz / (1 << 20)));
         std::vector<std::thread> th;
@@ -581,6 +587,7 @@ int ptucker_init(const int32_t* coords, const void* vals, int32_t vals_dtype, in
         if (bad_c != INT64_MAX)
             return fail(PTUCKER_EINVAL, "coordinate %d of entry %lld out of range", bad_n, (long long)bad_c);
         if (bad_v != INT64_MAX) return fail(PTUCKER_EINVAL, "value of entry %lld is not finite", (long long)bad_v);
+        g_xnorm_pending = std::sqrt(xx);
     }
     {
         if (!find_update_kernel(vals_dtype, 1, order, J))
@@ -596,6 +603,7 @@ int ptucker_init(const int32_t* coords, const void* vals, int32_t vals_dtype, in
     }
     g.N = order;
     g.J = J;
+    g.xnorm = g_xnorm_pending;
     g.prec = vals_dtype;
     g.esz = esz;
     g.nnz = nnz;
@@ -899,7 +907,7 @@ int compute_core_scores(std::vector<double>& R) {
     int64_t K1 = 1;
     for (int n = 1; n < N; ++n) K1 *= J;
     const int64_t gsize = K1 * J;
-    const int nsplit = 64;
+    const int nsplit = 256;
     const ModeIndex& m = g.mi[0];
     const int64_t nlanes = m.nslices * 32;
     if (!g.ax_UV) {
@@ -996,6 +1004,100 @@ int ptucker_core_nnz(int64_t* nnz) {
     int64_t c = 0;
     for (uint8_t v : g.core_present) c += v != 0;
     *nnz = c;
+    return PTUCKER_OK;
+}
+
+// ---------------------------------------------------------------- prediction, held-out RMSE, driver
+namespace {
+int predict_common(const int32_t* coords, const void* vals, int vals_dtype, int64_t n, double* out, bool rmse) {
+    if (!coords || !out || (rmse && !vals) || n < 0) return fail(PTUCKER_EINVAL, "null argument or n < 0");
+    if (rmse && n == 0) return fail(PTUCKER_EINVAL, "empty test set");
+    if (rmse && vals_dtype != g.prec) return fail(PTUCKER_EINVAL, "test values must have the context's precision");
+    for (int64_t q = 0; q < n; ++q)
+        for (int k = 0; k < g.N; ++k) {
+            const int32_t c = coords[q * g.N + k];
+            if (c < 0 || c >= g.dims[k])
+                return fail(PTUCKER_EINVAL, "coordinate %d of query %lld out of range", k, (long long)q);
+        }
+    if (n == 0) return PTUCKER_OK;
+    DeviceArena tmp;
+    int32_t* d_c = nullptr;
+    void* d_v = nullptr;
+    double* d_o = nullptr;
+    void** d_A = nullptr;
+    CK(tmp.alloc((void**)&d_c, (size_t)n * g.N * sizeof(int32_t)));
+    CK(tmp.alloc((void**)&d_o, (size_t)n * sizeof(double)));
+    CK(tmp.alloc((void**)&d_A, kMaxN * sizeof(void*)));
+    CK(cudaMemcpyAsync(d_c, coords, (size_t)n * g.N * sizeof(int32_t), cudaMemcpyHostToDevice, S()));
+    CK(cudaMemcpyAsync(d_A, g.A, kMaxN * sizeof(void*), cudaMemcpyHostToDevice, S()));
+    if (rmse) {
+        CK(tmp.alloc(&d_v, (size_t)n * g.esz));
+        CK(cudaMemcpyAsync(d_v, vals, (size_t)n * g.esz, cudaMemcpyHostToDevice, S()));
+    }
+    launch_predict(g.N, g.J, g.esz, g.G, (const void* const*)d_A, g.lda, d_c, d_v, n, d_o, rmse ? 1 : 0, g.nsm, S());
+    g.launches += 1;
+    CK(cudaGetLastError());
+    if (rmse) {
+        launch_sum(d_o, n, g.red_part, g.red_out, S());
+        g.launches += 2;
+        double s = 0.0;
+        CK(cudaMemcpyAsync(&s, g.red_out, sizeof(double), cudaMemcpyDeviceToHost, S()));
+        CK(cudaStreamSynchronize(S()));
+        *out = std::sqrt(s / (double)n);
+    } else {
+        CK(cudaMemcpyAsync(out, d_o, (size_t)n * sizeof(double), cudaMemcpyDeviceToHost, S()));
+        CK(cudaStreamSynchronize(S()));
+    }
+    return PTUCKER_OK;
+}
+}  // namespace
+
+int ptucker_predict(const int32_t* coords, int64_t n, double* out) {
+    int rc = require_init();
+    if (rc) return rc;
+    return predict_common(coords, nullptr, g.prec, n, out, false);
+}
+
+int ptucker_test_rmse(const int32_t* coords, const void* vals, int32_t vals_dtype, int64_t n, double* out) {
+    int rc = require_init();
+    if (rc) return rc;
+    return predict_common(coords, vals, vals_dtype, n, out, true);
+}
+
+int ptucker_run(int32_t max_iters, double tol, double approx_p, int32_t orthogonalize, double* errors,
+                int32_t* iters) {
+    int rc = require_init();
+    if (rc) return rc;
+    if (max_iters < 0 || !(tol >= 0.0) || approx_p < 0.0 || approx_p >= 1.0)
+        return fail(PTUCKER_EINVAL, "bad max_iters, tol or approx_p");
+    double e = 0.0;
+    rc = ptucker_error(&e);
+    if (rc) return rc;
+    if (errors) errors[0] = e;
+    int t = 0;
+    while (t < max_iters) {
+        rc = ptucker_sweep();  // Alg. 2 line 3
+        if (rc) return rc;
+        double et = 0.0;
+        rc = ptucker_error(&et);  // line 4 (Eq. 5)
+        if (rc) return rc;
+        ++t;
+        if (errors) errors[t] = et;
+        if (approx_p > 0.0) {  // lines 5-6 (P-Tucker-Approx)
+            rc = ptucker_truncate_core(approx_p, nullptr);
+            if (rc) return rc;
+        }
+        // reading R30: converged when the error changed by less than tol relative to the
+        // previous error, or is itself below tol of the data's norm (a perfect fit)
+        const bool conv = std::fabs(et - e) < tol * e || et <= tol * g.xnorm;
+        e = et;
+        if (conv) break;
+    }
+    if (iters) *iters = t;
+    if (orthogonalize) {  // lines 8-11
+        rc = ptucker_orthogonalize();
+        if (rc) return rc;
+    }
     return PTUCKER_OK;
 }
 

@@ -26,19 +26,27 @@ namespace {
 
 constexpr int kApproxWarps = 8;  // warps per block of k_approx_seg (one SELL segment per warp at a time)
 
-// One warp per SELL segment of mode 0 (pad lanes: zero outputs).
-template <typename TS>
+// One warp per SELL segment of mode 0 (pad lanes: zero outputs).  The segment's
+// entries go in batches of 32: lane l gathers entry l's rows (modes 1..N-1, fp64) into
+// shared memory and computes its e = x_hat - X (J^(N-1) FMAs against H); then the
+// batch's entries are accumulated into W, W2 with the b' split over the lanes (no
+// global loads in that inner loop).
+template <typename TS, int N, int J>
 __global__ void __launch_bounds__(kApproxWarps * 32) k_approx_seg(
-    int N, int J, int K1, int64_t nlanes, const int64_t* slice_off, const int32_t* lane_row,
+    int64_t nlanes, const int64_t* slice_off, const int32_t* lane_row,
     const int32_t* lane_len, const int32_t* const* sc, const TS* sv, const TS* const* A, int lda,
     const double* G64, double* A0seg, double* W, double* W2, double* Eslot) {
-    // dynamic shared memory: per warp H[K1] (padded to 8 doubles) and the entry's rows of
-    // modes 1..N-1 (fp64, [4][16])
+    // dynamic shared memory, per warp: H[K1] (padded to 8 doubles), the batch's rows
+    // [32][4][J] (fp64, J <= 10 -> stride 10) and e[32]
     extern __shared__ double smem[];
+    constexpr int K1 = ipow(J, N - 1);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int k1p = (K1 + 7) / 8 * 8;
-    double* H = smem + warp * (k1p + 64);
-    double (*sRw)[16] = reinterpret_cast<double (*)[16]>(H + k1p);
+    const int rstride = 4 * 10;
+    double* H = smem + warp * (k1p + 32 * rstride + 32);
+    double* Rw = H + k1p;               // Rw[entry * rstride + (n-1) * 10 + j]
+    double* Ew = Rw + 32 * rstride;     // Ew[entry]
+    (void)Eslot;
     for (int64_t seg = (int64_t)blockIdx.x * kApproxWarps + warp; seg < nlanes;
          seg += (int64_t)gridDim.x * kApproxWarps) {
         const int row = lane_row[seg];
@@ -52,59 +60,54 @@ __global__ void __launch_bounds__(kApproxWarps * 32) k_approx_seg(
         }
         const int64_t base = slice_off[seg >> 5] + (seg & 31);
         // a^(0) of the segment's row and H = a0 G_(0)
-        double a0[16];
-        for (int j = 0; j < J; ++j) a0[j] = (double)A[0][(int64_t)row * lda + j];
-        if (lane < J) A0seg[seg * J + lane] = a0[lane];
+        if (lane < J) A0seg[seg * J + lane] = (double)A[0][(int64_t)row * lda + lane];
         for (int b = lane; b < K1; b += 32) {
             double h = 0.0;
-            for (int j = 0; j < J; ++j) h = fma(a0[j], G64[(int64_t)j * K1 + b], h);
+            for (int j = 0; j < J; ++j) h = fma((double)A[0][(int64_t)row * lda + j], G64[(int64_t)j * K1 + b], h);
             H[b] = h;
         }
         __syncwarp();
-        // K'_b' for the staged rows: b' = (b_1, ..., b_{N-1}) in C order
-        auto kprod = [&](int b, const double (*r)[16]) {
+        // K'_b' of a staged entry: b' = (b_1, ..., b_{N-1}) in C order
+        auto kprod = [&](int b, const double* r) {
             double k = 1.0;
             for (int n = N - 1; n >= 1; --n) {
-                k *= r[n - 1][b % J];
+                k *= r[(n - 1) * 10 + b % J];
                 b /= J;
             }
             return k;
         };
-        auto stage = [&](int e) {
-            const int64_t slot = base + (int64_t)e * 32;
-            if (lane < (N - 1) * J) {
-                const int n = lane / J, j = lane % J;
-                const int c = sc[n][slot];
-                sRw[n][j] = (double)A[n + 1][(int64_t)c * lda + j];
-            }
-            __syncwarp();
-        };
-        // pass 1: e_alpha = x_hat - X for every entry of the segment
-        for (int e = 0; e < len; ++e) {
-            stage(e);
-            double part = 0.0;
-            for (int b = lane; b < K1; b += 32) part = fma(kprod(b, sRw), H[b], part);
-#pragma unroll
-            for (int o = 16; o > 0; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
-            if (lane == 0) Eslot[base + (int64_t)e * 32] = part - (double)sv[base + (int64_t)e * 32];
-            __syncwarp();
-        }
-        __syncwarp();
-        // pass 2: W = sum e K', W2 = sum K'^2, eight b' per lane per sweep
+        // W, W2 accumulators of this lane's b' (b' = lane + 32 m), kept in registers over the
+        // whole segment when K1 <= 256, else swept in chunks of 256 (re-gathering the entries)
         for (int b0 = 0; b0 < K1; b0 += 256) {
             double acc[8], acc2[8];
 #pragma unroll
             for (int m = 0; m < 8; ++m) acc[m] = acc2[m] = 0.0;
-            for (int e = 0; e < len; ++e) {
-                stage(e);
-                const double ee = Eslot[base + (int64_t)e * 32];
+            for (int e0 = 0; e0 < len; e0 += 32) {
+                const int e = e0 + lane;
+                double* r = Rw + lane * rstride;
+                if (e < len) {
+                    const int64_t slot = base + (int64_t)e * 32;
+                    for (int n = 1; n < N; ++n) {
+                        const TS* rowp = A[n] + (int64_t)sc[n - 1][slot] * lda;
+                        for (int j = 0; j < J; ++j) r[(n - 1) * 10 + j] = (double)rowp[j];
+                    }
+                    double xh = 0.0;
+                    for (int b = 0; b < K1; ++b) xh = fma(kprod(b, r), H[b], xh);
+                    Ew[lane] = xh - (double)sv[slot];
+                }
+                __syncwarp();
+                const int cnt = len - e0 < 32 ? len - e0 : 32;
+                for (int q = 0; q < cnt; ++q) {
+                    const double* rq = Rw + q * rstride;
+                    const double ee = Ew[q];
 #pragma unroll
-                for (int m = 0; m < 8; ++m) {
-                    const int b = b0 + lane + 32 * m;
-                    if (b < K1) {
-                        const double k = kprod(b, sRw);
-                        acc[m] = fma(ee, k, acc[m]);
-                        acc2[m] = fma(k, k, acc2[m]);
+                    for (int m = 0; m < 8; ++m) {
+                        const int b = b0 + lane + 32 * m;
+                        if (b < K1) {
+                            const double k = kprod(b, rq);
+                            acc[m] = fma(ee, k, acc[m]);
+                            acc2[m] = fma(k, k, acc2[m]);
+                        }
                     }
                 }
                 __syncwarp();
@@ -176,18 +179,23 @@ void launch_approx_uv(int N, int J, int elem_bytes, int64_t nslices, const int64
     if (nlanes > 0) {
         int grid = (int)((nlanes + kApproxWarps - 1) / kApproxWarps);
         if (grid > nsm * 8) grid = nsm * 8;
-        const size_t smem = (size_t)kApproxWarps * ((K1 + 7) / 8 * 8 + 64) * sizeof(double);
-        cudaFuncSetAttribute(k_approx_seg<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        cudaFuncSetAttribute(k_approx_seg<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        if (elem_bytes == 8)
-            k_approx_seg<double><<<grid, kApproxWarps * 32, smem, st>>>(N, J, K1, nlanes, slice_off, lane_row, lane_len,
-                                                                    d_sc, (const double*)sv,
-                                                                    (const double* const*)d_A, lda, G64, A0seg, W,
-                                                                    W2, Eslot);
-        else
-            k_approx_seg<float><<<grid, kApproxWarps * 32, smem, st>>>(N, J, K1, nlanes, slice_off, lane_row, lane_len,
-                                                                   d_sc, (const float*)sv, (const float* const*)d_A,
-                                                                   lda, G64, A0seg, W, W2, Eslot);
+        const size_t smem = (size_t)kApproxWarps * ((K1 + 7) / 8 * 8 + 32 * 40 + 32) * sizeof(double);
+#define PT_APPROX_CASE(NN, JJ)                                                                                     \
+    if (N == NN && J == JJ) {                                                                                      \
+        if (elem_bytes == 8) {                                                                                     \
+            cudaFuncSetAttribute(k_approx_seg<double, NN, JJ>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
+            k_approx_seg<double, NN, JJ><<<grid, kApproxWarps * 32, smem, st>>>(                                   \
+                nlanes, slice_off, lane_row, lane_len, d_sc, (const double*)sv, (const double* const*)d_A, lda, G64, \
+                A0seg, W, W2, Eslot);                                                                              \
+        } else {                                                                                                   \
+            cudaFuncSetAttribute(k_approx_seg<float, NN, JJ>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
+            k_approx_seg<float, NN, JJ><<<grid, kApproxWarps * 32, smem, st>>>(                                    \
+                nlanes, slice_off, lane_row, lane_len, d_sc, (const float*)sv, (const float* const*)d_A, lda, G64,  \
+                A0seg, W, W2, Eslot);                                                                              \
+        }                                                                                                          \
+    }
+        PT_NJ_LIST(PT_APPROX_CASE)
+#undef PT_APPROX_CASE
     }
     const int64_t per = nlanes > 0 ? (nlanes + nsplit - 1) / nsplit : 1;
     dim3 g2((unsigned)((gsize + 127) / 128), (unsigned)nsplit);

@@ -41,6 +41,10 @@ void launch_approx_uv(int N, int J, int elem_bytes, int64_t nslices, const int64
                       const int32_t* lane_row, const int32_t* lane_len, const int32_t* const* d_sc, const void* sv,
                       const void* const* d_A, int lda, const void* G, double* G64, double* A0seg, double* W,
                       double* W2, double* Eslot, double* part, int nsplit, double* UV, int nsm, cudaStream_t st);
+// ---- Eq. 4 predictions of query coordinates (predict.cu) ----
+void launch_predict(int N, int J, int elem_bytes, const void* G, const void* const* d_A, int lda,
+                    const int32_t* coords, const void* vals, int64_t n, double* out, int residual_sq, int nsm,
+                    cudaStream_t st);
 // ---- index build helpers (index.cu) ----
 void launch_extract_col(const int32_t* coords, int64_t nnz, int N, int n, int32_t* keys, int32_t* iota,
                         cudaStream_t st);

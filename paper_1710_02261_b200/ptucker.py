@@ -37,6 +37,9 @@ _SIGS = {
     "ptucker_core_scores": (C.c_int, [C.c_void_p]),
     "ptucker_truncate_core": (C.c_int, [C.c_double, C.POINTER(C.c_int64)]),
     "ptucker_core_nnz": (C.c_int, [C.POINTER(C.c_int64)]),
+    "ptucker_predict": (C.c_int, [C.c_void_p, C.c_int64, C.c_void_p]),
+    "ptucker_test_rmse": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int32, C.c_int64, C.POINTER(C.c_double)]),
+    "ptucker_run": (C.c_int, [C.c_int32, C.c_double, C.c_double, C.c_int32, C.c_void_p, C.POINTER(C.c_int32)]),
     "ptucker_get_factor": (C.c_int, [C.c_int32, C.c_void_p]),
     "ptucker_set_factor": (C.c_int, [C.c_int32, C.c_void_p]),
     "ptucker_get_core": (C.c_int, [C.c_void_p]),
@@ -181,6 +184,33 @@ def ptucker_core_nnz() -> int:
     k = C.c_int64()
     _check(load().ptucker_core_nnz(C.byref(k)))
     return int(k.value)
+
+
+def ptucker_predict(coords) -> np.ndarray:
+    """Eq. 4 predictions for query coordinates (n x N int32)."""
+    coords = np.ascontiguousarray(coords, np.int32)
+    out = np.empty(coords.shape[0], np.float64)
+    _check(load().ptucker_predict(_ptr(coords), coords.shape[0], _ptr(out)))
+    return out
+
+
+def ptucker_test_rmse(coords, vals) -> float:
+    """Held-out RMSE of the test entries (values converted to the context's precision)."""
+    coords = np.ascontiguousarray(coords, np.int32)
+    vals = np.ascontiguousarray(vals, _state["dtype"])
+    out = C.c_double()
+    dt = PTUCKER_F64 if vals.dtype == np.float64 else PTUCKER_F32
+    _check(load().ptucker_test_rmse(_ptr(coords), _ptr(vals), dt, coords.shape[0], C.byref(out)))
+    return out.value
+
+
+def ptucker_run(max_iters: int, tol: float = 1e-4, approx_p: float = 0.0, orthogonalize: bool = True):
+    """Alg. 2 driver: returns (errors e_0..e_T, T)."""
+    errs = np.zeros(max_iters + 1, np.float64)
+    it = C.c_int32()
+    _check(load().ptucker_run(int(max_iters), float(tol), float(approx_p), int(orthogonalize), _ptr(errs),
+                              C.byref(it)))
+    return errs[: it.value + 1], int(it.value)
 
 
 def ptucker_get_factor(n: int, out: np.ndarray | None = None) -> np.ndarray:

@@ -1,0 +1,89 @@
+"""GPU parity of the prediction / held-out RMSE / Alg. 2 driver calls
+through the C-ABI against the FP64 oracle:
+  * Eq. 4 predictions of held-out coordinates (90/10 split) from the GPU's state:
+    1e-10 relative (fp64 context) / 1e-6 (fp32 context: fp32 stored values, fp64 sums on
+    both sides -- only the summation order differs, so also ~1e-12);
+  * test RMSE equals the oracle's on the same state;
+  * ptucker_run: the error trajectory e_0..e_T within 1e-3 relative of the oracle's run
+    from the identical init, the same stopping iteration (tol) for P-Tucker, the
+    Approx variant's trajectory, and the orthogonalized end state's predictions.
+"""
+import numpy as np
+import pytest
+
+from gen import synth
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def pt():
+    import torch
+    assert torch.cuda.is_available(), "GPU tests need a B200"
+    torch.cuda.set_device(0)
+    from paper_1710_02261_b200 import build, ptucker
+    build.build()
+    ptucker.load()
+    yield ptucker
+    ptucker.ptucker_finalize()
+
+
+def split(cfg, frac=0.1, seed=1):
+    coords, vals = synth.generate(cfg)
+    rng = np.random.default_rng(seed)
+    test = rng.random(len(vals)) < frac
+    return coords[~test], vals[~test], coords[test], vals[test]
+
+
+def gpu_model(pt, orc, N):
+    return orc.Model(pt.ptucker_get_core().astype(np.float64),
+                     [pt.ptucker_get_factor(n).astype(np.float64) for n in range(N)])
+
+
+@pytest.mark.parametrize("name,scale", [("c1", 1.0), ("c2", 0.01), ("c4", 0.002)])
+def test_predict_and_rmse(pt, orc, name, scale):
+    cfg = synth.small(name, scale) if scale < 1 else synth.config(name)
+    tr_c, tr_v, te_c, te_v = split(cfg)
+    N = len(cfg.dims)
+    pt.ptucker_finalize()
+    pt.ptucker_init(tr_c, tr_v, cfg.dims, [cfg.J] * N, cfg.lam, 0)
+    pt.ptucker_sweep()
+    m = gpu_model(pt, orc, N)
+    ref = orc.predict_many(m, te_c)
+    got = pt.ptucker_predict(te_c)
+    tol = 1e-10 if cfg.dtype == "f64" else 1e-9
+    np.testing.assert_allclose(got, ref, rtol=tol, atol=tol * np.abs(ref).max())
+    r_ref = orc.test_rmse(m, te_c, te_v.astype(np.float64) if cfg.dtype == "f64" else te_v.astype(np.float32))
+    assert abs(pt.ptucker_test_rmse(te_c, te_v) - r_ref) <= 1e-9 * r_ref
+    with pytest.raises(pt.PTuckerError):
+        bad = te_c.copy()
+        bad[0, 0] = cfg.dims[0]
+        pt.ptucker_predict(bad)
+
+
+@pytest.mark.parametrize("name,scale,iters,tol,approx", [
+    ("c1", 1.0, 5, 0.0, 0.0), ("c2", 0.01, 10, 1e-3, 0.0), ("c4", 0.002, 8, 1e-4, 0.0), ("c1", 1.0, 5, 0.0, 0.2)])
+def test_run_matches_oracle(pt, orc, name, scale, iters, tol, approx):
+    cfg = synth.small(name, scale) if scale < 1 else synth.config(name)
+    coords, vals = synth.generate(cfg)
+    N = len(cfg.dims)
+    t = orc.Tensor(coords, vals, cfg.dims)
+    m = orc.init_model(cfg.dims, [cfg.J] * N, seed=0, prec=1 if cfg.dtype == "f64" else 0)
+    e_ref, it_ref, _ = orc.run(t, m, cfg.lam, iters, tol, approx, orthogonalize=True)
+    pt.ptucker_finalize()
+    pt.ptucker_init(coords, vals, cfg.dims, [cfg.J] * N, cfg.lam, 0)
+    e, it = pt.ptucker_run(iters, tol, approx, True)
+    assert it == it_ref, (it, it_ref, e, e_ref)
+    np.testing.assert_allclose(e, e_ref, rtol=1e-3)
+    if approx > 0:
+        assert pt.ptucker_core_nnz() == cfg.J ** N      # orthogonalize makes the core dense again
+    # the orthogonalized GPU model predicts what it did before the QR (Eq. 7-8 leave X' unchanged)
+    mg = gpu_model(pt, orc, N)
+    for n in range(N):
+        Q = mg.A(n)
+        np.testing.assert_allclose(Q.T @ Q, np.eye(cfg.J), atol=1e-4 if cfg.dtype == "f32" else 1e-10)
+    # (for Approx the last truncation follows the last recorded error: compare end states)
+    e_end = orc.error(t, m)
+    assert abs(orc.error(t, mg) - e_end) <= (1e-3 if cfg.dtype == "f32" else 1e-8) * e_end
+    if approx == 0:
+        assert abs(orc.error(t, mg) - e[-1]) <= (1e-4 if cfg.dtype == "f32" else 1e-9) * e[-1]

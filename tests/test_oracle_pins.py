@@ -514,3 +514,47 @@ def test_truncation_sequence_against_full_sort(orc):
         n_present -= k
         assert int(pres.sum()) == n_present == max(1, len(idx) - int(np.floor(p * len(idx))))
         assert np.all(m.G.reshape(-1)[pres == 0] == 0.0)
+
+
+# ---------------------------------------------------------------- prediction, held-out RMSE, Alg. 2 driver
+def test_predict_and_rmse(orc):
+    """Eq. 4 predictions equal numpy einsum reconstructions; S (test_rmse examples): one
+    entry with prediction error 0.5 -> 0.5, perfect predictions -> 0, and
+    rmse * sqrt(n) = the Eq. 5 error over the test entries (numpy)."""
+    rng = np.random.default_rng(8)
+    dims, J = (6, 5, 4), (2, 3, 2)
+    G = rng.standard_normal(J)
+    A = [rng.standard_normal((d, j)) for d, j in zip(dims, J)]
+    m = orc.Model(G, A)
+    q = np.stack([rng.integers(0, d, 50) for d in dims], 1).astype(np.int32)
+    ref = np_predict(G, A, q)
+    np.testing.assert_allclose(orc.predict_many(m, q), ref, rtol=1e-12, atol=1e-12)
+    assert abs(orc.test_rmse(m, q[:1], ref[:1] + 0.5) - 0.5) < 1e-12
+    assert orc.test_rmse(m, q, ref) < 1e-12
+    vals = rng.standard_normal(50)
+    r = vals - ref
+    assert abs(orc.test_rmse(m, q, vals) * np.sqrt(50) - np.sqrt(r @ r)) < 1e-10
+
+
+def test_driver_examples(orc):
+    """S (run examples), Alg. 2: a tensor reproduced exactly by the init model
+    has error 0 and stops after one iteration; a planted problem's error sequence is
+    non-increasing and ends below its start; tol = 0 runs exactly max_iters iterations."""
+    from gen import synth
+    dims, J = (8, 7, 6), 2
+    m0 = orc.init_model(dims, [J] * 3, seed=4, prec=1)
+    rng = np.random.default_rng(4)
+    flat = rng.choice(int(np.prod(dims)), 60, replace=False)
+    coords = np.stack(np.unravel_index(flat, dims), 1).astype(np.int32)
+    vals = np_predict(m0.G, [m0.A(n) for n in range(3)], coords)
+    t = orc.Tensor(coords, vals, dims)
+    m = orc.init_model(dims, [J] * 3, seed=4, prec=1)
+    errs, it, _ = orc.run(t, m, 1e-12, 10, 1e-4, orthogonalize=False)
+    assert errs[0] < 1e-12 and it == 1
+    cfg = synth.small("c4", 0.0005)
+    coords, vals = synth.generate(cfg)
+    t = orc.Tensor(coords, vals, cfg.dims)
+    m = orc.init_model(cfg.dims, [cfg.J] * 5, seed=0, prec=1)
+    errs, it, _ = orc.run(t, m, cfg.lam, 6, 0.0, orthogonalize=True)
+    assert it == 6 and len(errs) == 7
+    assert np.all(np.diff(errs) <= 1e-9 * errs[:-1]) and errs[-1] < errs[0]
