@@ -147,3 +147,12 @@ def small(name: str, scale: float, seed: int = 0) -> Config:
     c = CONFIGS[name]
     dims = tuple(max(d if d <= 64 else int(d * scale), 2) for d in c.dims)
     return dataclasses.replace(c, dims=dims, nnz=max(int(c.nnz * scale), 1), seed=seed)
+
+
+def order(N: int, J: int = 3, I: int = 100, nnz: int = 1000, dtype: str = "f64", seed: int = 0) -> Config:
+    """The order-scaling workload of P:1013-1014 (Fig. 8b): N-way, I = 100 per mode,
+    |Omega| = 10^3 uniform coordinates, values U[0,1), J = 3.  Coordinates are
+    deduplicated while the C-order key fits int64 (I^N < 2^63), else kept as drawn (a
+    collision among 10^3 draws from 100^10 cells has probability ~5e-15)."""
+    distinct = N * np.log2(max(I, 2)) < 62
+    return Config(f"order{N}", (I,) * N, nnz, J, 0.01, 5, dtype, "uniform", "uniform", bool(distinct), seed)

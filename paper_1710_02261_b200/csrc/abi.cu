@@ -107,6 +107,9 @@ struct Ctx {
     int last_fail_mode = -1;
     const UpdateKernel* kern = nullptr;      // row update (tensor-core variant when available)
     const UpdateKernel* kern_alu = nullptr;  // ALU kernel (literal error pass, and updates when tc = 0)
+    bool generic = false;                    // no compiled (N, J): update_generic.cu + device COO for the error
+    int32_t* coo_c = nullptr;                // generic shapes: the input COO kept on the device
+    void* coo_v = nullptr;
     int use_tc = 1;                          // option "tc"
     int l0_group = 1;                        // option "l0_group" (tensor-core kernel, F32-B)
     float* tc_hi = nullptr;                  // tf32 split of the innermost factor (tensor-core kernel)
@@ -304,6 +307,20 @@ int launch_update_kernel(int n, bool literal) {
         return PTUCKER_OK;
     }
     g.launches += 1;
+    if (g.generic) {
+        if (literal) return fail(PTUCKER_EINVAL, "internal: no literal pass for generic shapes");
+        if (g.prec == PTUCKER_F64) {
+            UpdateParams<double> p = make_params<double>(n, false);
+            p.Gp = (const double*)g.G;
+            launch_update_generic(&p, 8, g.N, g.J, g.nsm, S());
+        } else {
+            UpdateParams<float> p = make_params<float>(n, false);
+            p.Gp = (const float*)g.G;
+            launch_update_generic(&p, 4, g.N, g.J, g.nsm, S());
+        }
+        CK(cudaGetLastError());
+        return PTUCKER_OK;
+    }
     const UpdateKernel* k = literal ? g.kern_alu : g.kern;
 
     if (g.prec == PTUCKER_F64) {
@@ -318,6 +335,7 @@ int launch_update_kernel(int n, bool literal) {
 }
 
 int rebuild_gp() {
+    if (g.generic) return PTUCKER_OK;
     for (int n = 0; n < g.N; ++n) launch_permute_core(g.G, g.Gp[n], g.esz, g.N, g.J, n, S());
     g.launches += g.N;
     CK(cudaGetLastError());
@@ -336,6 +354,14 @@ int policy_l64() {
 
 int choose_kernel() {
     const int last64 = policy_l64();
+    int nsm0 = 148;
+    CK(cudaDeviceGetAttribute(&nsm0, cudaDevAttrMultiProcessorCount, g.device));
+    if (g.generic) {  // update_generic.cu
+        g.kern = g.kern_alu = nullptr;
+        g.nsm = nsm0;
+        g.grid_upd = g.grid_lit = nsm0;
+        return PTUCKER_OK;
+    }
     g.kern_alu = find_update_kernel(g.prec, last64, g.N, g.J);
     if (!g.kern_alu) return fail(PTUCKER_EINVAL, "no compiled kernel for N=%d J=%d", g.N, g.J);
     g.kern = g.kern_alu;
@@ -373,6 +399,9 @@ void free_all() {
     g.ax_G64 = g.ax_A0 = g.ax_W = g.ax_W2 = g.ax_E = g.ax_part = g.ax_UV = nullptr;
     g.ax_ptrs = nullptr;
     g.core_present.clear();
+    g.coo_c = nullptr;
+    g.coo_v = nullptr;
+    g.generic = false;
     g.d_fail = g.d_qrfail = nullptr;
     g.d_work = nullptr;
     g.launches = 0;
@@ -545,6 +574,11 @@ int ptucker_init(const int32_t* coords, const void* vals, int32_t vals_dtype, in
     }
     const int J = core_dims[0];
     if (J < 1) return fail(PTUCKER_EINVAL, "core dim must be >= 1");
+    {
+        double gs = 1.0;
+        for (int n = 0; n < order; ++n) gs *= J;
+        if (gs > (double)(1 << 26)) return fail(PTUCKER_EINVAL, "core of %g entries exceeds 2^26", gs);
+    }
     const int esz = vals_dtype == PTUCKER_F64 ? 8 : 4;
     {
         // coordinates in range and values finite: first offending entry, scanned by
@@ -590,8 +624,8 @@ int ptucker_init(const int32_t* coords, const void* vals, int32_t vals_dtype, in
         g_xnorm_pending = std::sqrt(xx);
     }
     {
-        if (!find_update_kernel(vals_dtype, 1, order, J))
-            return fail(PTUCKER_EINVAL, "(N=%d, J=%d) is not a compiled kernel shape", order, J);
+        if (!find_update_kernel(vals_dtype, 1, order, J) && !generic_shape_ok(order, J))
+            return fail(PTUCKER_EINVAL, "(N=%d, J=%d): J must be <= 16", order, J);
     }
     pc.lap("validation (host)");
     // ---- fresh context ----
@@ -603,6 +637,7 @@ int ptucker_init(const int32_t* coords, const void* vals, int32_t vals_dtype, in
     }
     g.N = order;
     g.J = J;
+    g.generic = find_update_kernel(vals_dtype, 1, order, J) == nullptr;
     g.xnorm = g_xnorm_pending;
     g.prec = vals_dtype;
     g.esz = esz;
@@ -613,7 +648,7 @@ int ptucker_init(const int32_t* coords, const void* vals, int32_t vals_dtype, in
     g.lda = factor_ld(J, esz);
     int64_t nblk = 1;
     for (int l = 0; l < order - 2; ++l) nblk *= J;
-    g.gp_elems = (int)(nblk * gblk(J, esz));
+    g.gp_elems = g.generic ? 0 : (int)(nblk * gblk(J, esz));  // generic kernel reads G itself
     DeviceArena& A = g.arena;
     CK(A.alloc((void**)&g.d_fail, sizeof(int)));
     CK(A.alloc((void**)&g.d_qrfail, sizeof(int)));
@@ -633,7 +668,7 @@ int ptucker_init(const int32_t* coords, const void* vals, int32_t vals_dtype, in
         CK(A.alloc(&g.A[n], dims[n] * g.lda * esz));
         CK(cudaMemsetAsync(g.A[n], 0, dims[n] * g.lda * esz, S()));
         launch_init_uniform(g.A[n], esz, dims[n], J, g.lda, seed, (uint64_t)(1 + n), S());
-        CK(A.alloc(&g.Gp[n], (size_t)g.gp_elems * esz));
+        if (!g.generic) CK(A.alloc(&g.Gp[n], (size_t)g.gp_elems * esz));
         CK(A.alloc((void**)&g.sse_row[n], dims[n] * sizeof(double)));
         CK(cudaMemsetAsync(g.sse_row[n], 0, dims[n] * sizeof(double), S()));
     }
@@ -646,7 +681,7 @@ int ptucker_init(const int32_t* coords, const void* vals, int32_t vals_dtype, in
         const int GBk = gblk(J, esz);
         for (int n = 0; n < order; ++n) {
             g.smp[n] = Ctx::Smp();
-            if (order != 4) continue;
+            if (order != 4 || g.generic) continue;
             int oth[3], c = 0;
             for (int m = 0; m < order; ++m)
                 if (m != n) oth[c++] = m;
@@ -714,6 +749,14 @@ int ptucker_init(const int32_t* coords, const void* vals, int32_t vals_dtype, in
     CK(A.alloc((void**)&g.lit_part, std::max<int64_t>(g.mi[0].nslices * 32, 1) * sizeof(double)));
 
     CK(cudaStreamSynchronize(S()));
+    if (g.generic) {
+        // the literal error of generic shapes runs over the COO (update_generic.cu has no literal pass)
+        CK(g.arena.alloc((void**)&g.coo_c, (size_t)nnz * order * sizeof(int32_t)));
+        CK(g.arena.alloc(&g.coo_v, (size_t)nnz * esz));
+        CK(cudaMemcpyAsync(g.coo_c, d_coords, (size_t)nnz * order * sizeof(int32_t), cudaMemcpyDeviceToDevice, S()));
+        CK(cudaMemcpyAsync(g.coo_v, d_vals, (size_t)nnz * esz, cudaMemcpyDeviceToDevice, S()));
+        CK(cudaStreamSynchronize(S()));
+    }
     input.release_all();
     g.inited = true;
     rc = choose_kernel();
@@ -787,6 +830,20 @@ int ptucker_error_literal(double* out) {
     int rc = require_init();
     if (rc) return rc;
     if (!out) return fail(PTUCKER_EINVAL, "null out");
+    if (g.generic) {  // (x - x_hat)^2 over this rank's mode-0 rows of the device COO, then the same reduction
+        void** d_A = nullptr;
+        double* d_r = nullptr;
+        DeviceArena tmp;
+        CK(tmp.alloc((void**)&d_A, kMaxN * sizeof(void*)));
+        CK(tmp.alloc((void**)&d_r, (size_t)g.nnz * sizeof(double)));
+        CK(cudaMemcpyAsync(d_A, g.A, kMaxN * sizeof(void*), cudaMemcpyHostToDevice, S()));
+        launch_predict(g.N, g.J, g.esz, g.G, (const void* const*)d_A, g.lda, g.coo_c, g.coo_v, g.nnz, d_r, 1, g.nsm,
+                       S(), g.mi[0].r0, g.mi[0].r1);
+        launch_sum(d_r, g.nnz, g.red_part, g.red_out, S());
+        g.launches += 3;
+        CK(cudaGetLastError());
+        return finish_error(out);  // synchronises before tmp is freed
+    }
     rc = timed("literal", [&]() -> int { return launch_update_kernel(0, true); });
     if (rc) return rc;
     rc = timed("error_reduce", [&]() -> int {
@@ -909,20 +966,39 @@ int compute_core_scores(std::vector<double>& R) {
     const int64_t gsize = K1 * J;
     const int nsplit = 256;
     const ModeIndex& m = g.mi[0];
-    const int64_t nlanes = m.nslices * 32;
-    if (!g.ax_UV) {
-        CK(g.arena.alloc((void**)&g.ax_G64, gsize * sizeof(double)));
-        CK(g.arena.alloc((void**)&g.ax_A0, std::max<int64_t>(nlanes, 1) * J * sizeof(double)));
-        CK(g.arena.alloc((void**)&g.ax_W, std::max<int64_t>(nlanes, 1) * K1 * sizeof(double)));
-        CK(g.arena.alloc((void**)&g.ax_W2, std::max<int64_t>(nlanes, 1) * K1 * sizeof(double)));
-        CK(g.arena.alloc((void**)&g.ax_E, std::max<int64_t>(m.nslots, 1) * sizeof(double)));
-        CK(g.arena.alloc((void**)&g.ax_part, (size_t)2 * nsplit * gsize * sizeof(double)));
-        CK(g.arena.alloc((void**)&g.ax_ptrs, 2 * kMaxN * sizeof(void*)));
-        CK(g.arena.alloc((void**)&g.ax_UV, 2 * gsize * sizeof(double)));
-        void* h[2 * kMaxN] = {nullptr};
-        for (int k = 0; k < N - 1; ++k) h[k] = m.sc[k];
-        for (int k = 0; k < N; ++k) h[kMaxN + k] = g.A[k];
-        CK(cudaMemcpyAsync(g.ax_ptrs, h, sizeof(h), cudaMemcpyHostToDevice, S()));
+    if (!approx_shape_ok(N, J)) {  // generic shapes: U, V by definition over the device COO
+        if (!g.coo_c) return fail(PTUCKER_EINVAL, "internal: no device COO for the generic Approx scores");
+        if (!g.ax_UV) {
+            CK(g.arena.alloc((void**)&g.ax_ptrs, kMaxN * sizeof(void*)));
+            CK(g.arena.alloc((void**)&g.ax_E, (size_t)g.nnz * sizeof(double)));
+            CK(g.arena.alloc((void**)&g.ax_UV, 2 * gsize * sizeof(double)));
+            CK(cudaMemcpyAsync(g.ax_ptrs, g.A, kMaxN * sizeof(void*), cudaMemcpyHostToDevice, S()));
+        }
+        int rc = timed("approx_scores", [&]() -> int {
+            launch_predict(N, J, g.esz, g.G, (const void* const*)g.ax_ptrs, g.lda, g.coo_c, g.coo_v, g.nnz, g.ax_E, 0,
+                           g.nsm, S());
+            launch_approx_literal(N, J, g.esz, (const void* const*)g.ax_ptrs, g.lda, g.coo_c, g.coo_v, g.ax_E, g.nnz,
+                                  m.r0, m.r1, g.ax_UV, S());
+            g.launches += 2;
+            CK(cudaGetLastError());
+            return PTUCKER_OK;
+        });
+        if (rc) return rc;
+    } else {
+        const int64_t nlanes = m.nslices * 32;
+        if (!g.ax_UV) {
+            CK(g.arena.alloc((void**)&g.ax_G64, gsize * sizeof(double)));
+            CK(g.arena.alloc((void**)&g.ax_A0, std::max<int64_t>(nlanes, 1) * J * sizeof(double)));
+            CK(g.arena.alloc((void**)&g.ax_W, std::max<int64_t>(nlanes, 1) * K1 * sizeof(double)));
+            CK(g.arena.alloc((void**)&g.ax_W2, std::max<int64_t>(nlanes, 1) * K1 * sizeof(double)));
+            CK(g.arena.alloc((void**)&g.ax_E, std::max<int64_t>(m.nslots, 1) * sizeof(double)));
+            CK(g.arena.alloc((void**)&g.ax_part, (size_t)2 * nsplit * gsize * sizeof(double)));
+            CK(g.arena.alloc((void**)&g.ax_ptrs, 2 * kMaxN * sizeof(void*)));
+            CK(g.arena.alloc((void**)&g.ax_UV, 2 * gsize * sizeof(double)));
+            void* h[2 * kMaxN] = {nullptr};
+            for (int k = 0; k < N - 1; ++k) h[k] = m.sc[k];
+            for (int k = 0; k < N; ++k) h[kMaxN + k] = g.A[k];
+            CK(cudaMemcpyAsync(g.ax_ptrs, h, sizeof(h), cudaMemcpyHostToDevice, S()));
     }
     int rc = timed("approx_scores", [&]() -> int {
         launch_approx_uv(N, J, g.esz, m.nslices, m.slice_off, m.lane_row, m.lane_len, (const int32_t* const*)g.ax_ptrs,
@@ -933,6 +1009,7 @@ int compute_core_scores(std::vector<double>& R) {
         return PTUCKER_OK;
     });
     if (rc) return rc;
+    }
     if (g.world > 1 && g.comm) NK(ncclAllReduce(g.ax_UV, g.ax_UV, (size_t)(2 * gsize), ncclDouble, ncclSum, g.comm, S()));
     std::vector<double> UV((size_t)(2 * gsize));
     std::vector<char> graw((size_t)(gsize * g.esz));
@@ -1146,11 +1223,11 @@ int ptucker_info(char* buf, int32_t len) {
     snprintf(tmp, sizeof(tmp),
              "\"inited\": %s, \"N\": %d, \"J\": %d, \"prec\": \"%s\", \"policy\": \"%s\", \"nnz\": %lld, "
              "\"lambda\": %.17g, \"seg_len\": %d, \"rank\": %d, \"world\": %d, \"grid_update\": %d, "
-             "\"threads_per_cta\": %d, \"smem_core_bytes\": %d, \"kernel_launches\": %lld, \"tensor_cores\": %s, \"modes\": [",
+             "\"threads_per_cta\": %d, \"smem_core_bytes\": %d, \"kernel_launches\": %lld, \"tensor_cores\": %s, \"generic\": %s, \"modes\": [",
              g.inited ? "true" : "false", g.N, g.J, g.prec == PTUCKER_F64 ? "f64" : "f32",
              g.prec == PTUCKER_F64 ? "F64" : (policy_l64() == 0 ? "F32-A" : (policy_l64() == 1 ? "F32-B" : "F32-C")), (long long)g.nnz, g.lambda, g.seg_len,
              g.rank, g.world, g.grid_upd, kUpdThreads, g.gp_elems * g.esz, (long long)g.launches,
-             (g.kern && g.kern != g.kern_alu) ? "true" : "false");
+             (g.kern && g.kern != g.kern_alu) ? "true" : "false", g.generic ? "true" : "false");
     s += tmp;
     for (int n = 0; n < g.N; ++n) {
         const ModeIndex& m = g.mi[n];

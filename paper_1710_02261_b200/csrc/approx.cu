@@ -162,7 +162,76 @@ __global__ void k_to_f64(const TS* in, double* out, int64_t n) {
         out[i] = (double)in[i];
 }
 
+// Shapes without a compiled (N, J) (order > 5, other J): U and V straight from their
+// definition, one thread per core entry beta looping over this rank's entries of the
+// device COO (mode-0 row in [row_lo, row_hi)); e_alpha = x_hat_alpha - X_alpha with
+// x_hat from k_predict (xhat[]).  Entries are staged in shared memory per chunk.
+constexpr int kLitChunk = 128;
+template <typename TS>
+__global__ void __launch_bounds__(256) k_approx_literal(int N, int J, int64_t gsize, const TS* const* A, int lda,
+                                                        const int32_t* coords, const TS* vals, const double* xhat,
+                                                        int64_t n, int64_t row_lo, int64_t row_hi, double* UV) {
+    __shared__ int32_t cs[kLitChunk * kMaxN];
+    __shared__ double es[kLitChunk];
+    __shared__ int keep[kLitChunk];
+    const int64_t beta = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    int bn[kMaxN];
+    {
+        int64_t b = beta < gsize ? beta : 0;
+        for (int m = N - 1; m >= 0; --m) {
+            bn[m] = (int)(b % J);
+            b /= J;
+        }
+    }
+    double u = 0.0, v = 0.0;
+    for (int64_t q0 = 0; q0 < n; q0 += kLitChunk) {
+        const int cnt = n - q0 < kLitChunk ? (int)(n - q0) : kLitChunk;
+        __syncthreads();
+        for (int t = threadIdx.x; t < cnt * N; t += blockDim.x) cs[t] = coords[q0 * N + t];
+        for (int t = threadIdx.x; t < cnt; t += blockDim.x) {
+            const int32_t i0 = coords[(q0 + t) * N];
+            keep[t] = i0 >= row_lo && i0 < row_hi;
+            es[t] = xhat[q0 + t] - (double)vals[q0 + t];
+        }
+        __syncthreads();
+        if (beta >= gsize) continue;
+        for (int t = 0; t < cnt; ++t) {
+            if (!keep[t]) continue;
+            double k = 1.0;
+            for (int m = 0; m < N; ++m) k *= (double)A[m][(int64_t)cs[t * N + m] * lda + bn[m]];
+            u = fma(es[t], k, u);
+            v = fma(k, k, v);
+        }
+    }
+    if (beta < gsize) {
+        UV[beta] = u;
+        UV[gsize + beta] = v;
+    }
+}
+
 }  // namespace
+
+void launch_approx_literal(int N, int J, int elem_bytes, const void* const* d_A, int lda, const int32_t* coords,
+                           const void* vals, const double* xhat, int64_t n, int64_t row_lo, int64_t row_hi,
+                           double* UV, cudaStream_t st) {
+    int64_t gsize = 1;
+    for (int m = 0; m < N; ++m) gsize *= J;
+    const unsigned grid = (unsigned)((gsize + 255) / 256);
+    if (elem_bytes == 8)
+        k_approx_literal<double><<<grid, 256, 0, st>>>(N, J, gsize, (const double* const*)d_A, lda, coords,
+                                                       (const double*)vals, xhat, n, row_lo, row_hi, UV);
+    else
+        k_approx_literal<float><<<grid, 256, 0, st>>>(N, J, gsize, (const float* const*)d_A, lda, coords,
+                                                      (const float*)vals, xhat, n, row_lo, row_hi, UV);
+}
+
+bool approx_shape_ok(int N, int J) {
+#define PT_APPROX_OK(NN, JJ) \
+    if (N == NN && J == JJ) return true;
+    PT_NJ_LIST(PT_APPROX_OK)
+#undef PT_APPROX_OK
+    return false;
+}
 
 // U, V (J^N each, C order over the core) of this rank's entries of mode 0 into UV[2*J^N].
 // Scratch: A0seg [nlanes*J], W, W2 [nlanes*K1], Eslot [nslots], part [2*nsplit*J^N], G64 [J^N].

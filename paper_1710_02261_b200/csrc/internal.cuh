@@ -8,7 +8,7 @@
 
 namespace pt {
 
-constexpr int kMaxN = 5;      // compiled orders N = 2..5
+constexpr int kMaxN = 10;     // orders N = 2..10 (templated kernels for 2..5, update_generic.cu beyond)
 constexpr int kWarp = 32;
 constexpr int kUpdThreads = 256;  // update kernel CTA size (8 warps, one slice per warp at a time)
 
@@ -79,6 +79,14 @@ const UpdateKernel* find_update_kernel(int prec, int l64, int N, int J);
 // Tensor-core variant (fp32, N = 3): innermost TTV stage on tcgen05 (update_tc.cu).
 const UpdateKernel* find_update_kernel_tc(int l64, int J);
 int tc_kp(int J);  // K padding of the tensor-core A operand (floats per split row)
+// Generic-order kernel (update_generic.cu): any N <= kMaxN, J <= 16, fp64; p.Gp = G in C order.
+void launch_update_generic(const void* params, int elem_bytes, int N, int J, int nsm, cudaStream_t st);
+bool generic_shape_ok(int N, int J);
+bool approx_shape_ok(int N, int J);  // approx.cu segment kernels instantiated for (N, J)
+// U, V of Eq. 13 from their definition over a device COO (shapes without a compiled (N, J))
+void launch_approx_literal(int N, int J, int elem_bytes, const void* const* d_A, int lda, const int32_t* coords,
+                           const void* vals, const double* xhat, int64_t n, int64_t row_lo, int64_t row_hi,
+                           double* UV, cudaStream_t st);
 void launch_tc_split(const float* A, int64_t I, int lda, int J, float* hi, float* lo, cudaStream_t st);
 
 // (N, J) pairs compiled: N = 2..5, J in {2,3,4,5,8,10}, J^N <= 10^4.

@@ -44,7 +44,7 @@ void launch_approx_uv(int N, int J, int elem_bytes, int64_t nslices, const int64
 // ---- Eq. 4 predictions of query coordinates (predict.cu) ----
 void launch_predict(int N, int J, int elem_bytes, const void* G, const void* const* d_A, int lda,
                     const int32_t* coords, const void* vals, int64_t n, double* out, int residual_sq, int nsm,
-                    cudaStream_t st);
+                    cudaStream_t st, int64_t row_lo = 0, int64_t row_hi = INT64_MAX);
 // ---- index build helpers (index.cu) ----
 void launch_extract_col(const int32_t* coords, int64_t nnz, int N, int n, int32_t* keys, int32_t* iota,
                         cudaStream_t st);

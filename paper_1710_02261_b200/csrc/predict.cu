@@ -14,8 +14,12 @@ namespace {
 template <typename TS>
 __global__ void k_predict(int N, int J, int64_t gsize, const TS* __restrict__ G, const TS* const* __restrict__ A,
                           int lda, const int32_t* __restrict__ coords, const TS* __restrict__ vals, int64_t n,
-                          double* __restrict__ out, int residual_sq) {
+                          double* __restrict__ out, int residual_sq, int64_t row_lo, int64_t row_hi) {
     for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < n; q += (int64_t)gridDim.x * blockDim.x) {
+        if (residual_sq && (coords[q * N] < row_lo || coords[q * N] >= row_hi)) {  // another rank's mode-0 rows
+            out[q] = 0.0;
+            continue;
+        }
         // the query's factor rows in fp64
         double r[kMaxN][16];
         for (int k = 0; k < N; ++k) {
@@ -47,10 +51,11 @@ __global__ void k_predict(int N, int J, int64_t gsize, const TS* __restrict__ G,
 
 }  // namespace
 
-// out[q] = x_hat (residual_sq = 0) or (x - x_hat)^2 (1) for n queries (device buffers).
+// out[q] = x_hat (residual_sq = 0) or (x - x_hat)^2 (1, 0 outside mode-0 rows [row_lo, row_hi))
+// for n queries (device buffers).
 void launch_predict(int N, int J, int elem_bytes, const void* G, const void* const* d_A, int lda,
                     const int32_t* coords, const void* vals, int64_t n, double* out, int residual_sq, int nsm,
-                    cudaStream_t st) {
+                    cudaStream_t st, int64_t row_lo, int64_t row_hi) {
     if (n <= 0) return;
     int64_t gsize = 1;
     for (int k = 0; k < N; ++k) gsize *= J;
@@ -58,10 +63,10 @@ void launch_predict(int N, int J, int elem_bytes, const void* G, const void* con
     if (grid > nsm * 16) grid = nsm * 16;
     if (elem_bytes == 8)
         k_predict<double><<<grid, 128, 0, st>>>(N, J, gsize, (const double*)G, (const double* const*)d_A, lda, coords,
-                                                (const double*)vals, n, out, residual_sq);
+                                                (const double*)vals, n, out, residual_sq, row_lo, row_hi);
     else
         k_predict<float><<<grid, 128, 0, st>>>(N, J, gsize, (const float*)G, (const float* const*)d_A, lda, coords,
-                                               (const float*)vals, n, out, residual_sq);
+                                               (const float*)vals, n, out, residual_sq, row_lo, row_hi);
 }
 
 }  // namespace pt

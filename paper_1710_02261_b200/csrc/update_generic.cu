@@ -1,0 +1,153 @@
+// update_generic.cu -- row update for any order N <= kMaxN and core size J <= 16 (the
+// shapes without a compiled (N, J) kernel: the order-scaling workload of P:1013-1014,
+// N = 3..10, J = 3, I = 100, |Omega| = 10^3, and any J outside {2,3,4,5,8,10}).
+//
+// One thread per SELL-32 lane (row segment) of mode n, everything in fp64:
+//   delta(j) = sum over the other modes' indices k of G[beta(k, beta_n = j)] prod_{m != n} a^(m)_{i_m k_m}
+// (Eq. 12, evaluated as written: J^(N-1) products of N-1 factors, each
+// feeding J FMAs), B += delta delta^T, c += x delta, sum x^2 (Eq. 10-11), then the
+// Cholesky solve a = c [B + lambda I]^-1 (Eq. 9) and the row's SSE by the identity
+// of update.cuh (fused Eq. 5), or the heavy-row partial record.  These shapes are
+// tiny (|Omega| = 10^3): the kernel favours generality over speed.
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "internal.cuh"
+
+namespace pt {
+namespace {
+
+constexpr int kGJ = 16;  // max J of the generic kernel
+
+__device__ __forceinline__ int upi(int i, int j, int J) { return i * J - i * (i - 1) / 2 + (j - i); }
+
+template <typename TS>
+__global__ void __launch_bounds__(128) k_update_gen(const UpdateParams<TS> p, int N, int J) {
+    const int64_t nl = p.nslices * kWarp;
+    const int n = p.n;
+    // stride of beta_m in the C-order core
+    int64_t stride[kMaxN];
+    {
+        int64_t s = 1;
+        for (int m = N - 1; m >= 0; --m) {
+            stride[m] = s;
+            s *= J;
+        }
+    }
+    int64_t ncomb = 1;
+    for (int m = 0; m < N - 1; ++m) ncomb *= J;
+    for (int64_t slot = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; slot < nl;
+         slot += (int64_t)gridDim.x * blockDim.x) {
+        const int row = p.lane_row[slot];
+        if (row < 0) continue;
+        const int len = p.lane_len[slot];
+        const int64_t base = p.slice_off[slot >> 5] + (slot & 31);
+        double B[kGJ * (kGJ + 1) / 2], c[kGJ], s2 = 0.0;
+        for (int q = 0; q < J * (J + 1) / 2; ++q) B[q] = 0.0;
+        for (int q = 0; q < J; ++q) c[q] = 0.0;
+        for (int e = 0; e < len; ++e) {
+            const int64_t es = base + (int64_t)e * kWarp;
+            const double x = (double)p.sv[es];
+            const TS* rows[kMaxN - 1];
+            for (int k = 0; k < N - 1; ++k) rows[k] = p.A[k] + (int64_t)p.sc[k][es] * p.lda;
+            double d[kGJ];
+            for (int j = 0; j < J; ++j) d[j] = 0.0;
+            // iterate the other modes' indices k_0..k_{N-2} (ascending mode order) as a counter
+            int kk[kMaxN - 1];
+            for (int k = 0; k < N - 1; ++k) kk[k] = 0;
+            for (int64_t t = 0; t < ncomb; ++t) {
+                double prod = 1.0;
+                int64_t gb = 0;
+                for (int k = 0; k < N - 1; ++k) {
+                    const int m = k < n ? k : k + 1;  // the mode of the k-th other row
+                    prod *= (double)rows[k][kk[k]];
+                    gb += kk[k] * stride[m];
+                }
+                for (int j = 0; j < J; ++j) d[j] = fma((double)p.Gp[gb + j * stride[n]], prod, d[j]);
+                for (int k = N - 2; k >= 0; --k) {
+                    if (++kk[k] < J) break;
+                    kk[k] = 0;
+                }
+            }
+            for (int i = 0; i < J; ++i) {
+                c[i] = fma(x, d[i], c[i]);
+                for (int j = i; j < J; ++j) B[upi(i, j, J)] = fma(d[i], d[j], B[upi(i, j, J)]);
+            }
+            s2 = fma(x, x, s2);
+        }
+        const int64_t pidx = p.lane_pidx[slot];
+        if (pidx >= 0) {
+            const int stp = p.lane_pstride[slot];
+            const int NB = J * (J + 1) / 2;
+            double* dst = p.partials + pidx;
+            for (int q = 0; q < NB; ++q) dst[(int64_t)q * stp] = B[q];
+            for (int q = 0; q < J; ++q) dst[(int64_t)(NB + q) * stp] = c[q];
+            dst[(int64_t)(NB + J) * stp] = s2;
+            continue;
+        }
+        // Cholesky of B + lambda I (upper triangle overwritten by L^T), then the two solves
+        bool ok = true;
+        double inv[kGJ], y[kGJ], a[kGJ];
+        for (int j = 0; j < J; ++j) {
+            double dj = B[upi(j, j, J)] + p.lambda;
+            for (int k = 0; k < j; ++k) dj = fma(-B[upi(k, j, J)], B[upi(k, j, J)], dj);
+            ok = ok && (dj > 0.0);
+            inv[j] = 1.0 / sqrt(fmax(dj, 1e-300));
+            for (int i = j + 1; i < J; ++i) {
+                double s = B[upi(j, i, J)];
+                for (int k = 0; k < j; ++k) s = fma(-B[upi(k, i, J)], B[upi(k, j, J)], s);
+                B[upi(j, i, J)] = s * inv[j];
+            }
+        }
+        for (int i = 0; i < J; ++i) {
+            double s = c[i];
+            for (int k = 0; k < i; ++k) s = fma(-B[upi(k, i, J)], y[k], s);
+            y[i] = s * inv[i];
+        }
+        for (int i = J - 1; i >= 0; --i) {
+            double s = y[i];
+            for (int k = i + 1; k < J; ++k) s = fma(-B[upi(i, k, J)], a[k], s);
+            a[i] = s * inv[i];
+        }
+        if (!ok) {
+            atomicCAS(p.fail, 0, row + 1);
+            for (int j = 0; j < J; ++j) a[j] = 0.0;
+        }
+        TS* out = p.An + (int64_t)row * p.lda;
+        double sse = s2, ac = 0.0, aa = 0.0, ec = 0.0;
+        for (int j = 0; j < J; ++j) {
+            const TS st = (TS)a[j];
+            out[j] = st;
+            const double at = (double)st;
+            sse = fma(-2.0 * at, c[j], sse);
+            ac = fma(a[j], c[j], ac);
+            aa = fma(a[j], a[j], aa);
+            ec = fma(at - a[j], c[j] - p.lambda * a[j], ec);
+        }
+        p.sse_row[row] = sse + ac - p.lambda * aa + 2.0 * ec;  // SSE of the stored row (update.cuh)
+    }
+}
+
+}  // namespace
+
+// The generic kernel reads the core in plain C order: p.Gp must be G itself.
+void launch_update_generic(const void* params, int elem_bytes, int N, int J, int nsm, cudaStream_t st) {
+    if (elem_bytes == 8) {
+        const UpdateParams<double>& p = *reinterpret_cast<const UpdateParams<double>*>(params);
+        const int64_t nl = p.nslices * kWarp;
+        int grid = (int)((nl + 127) / 128);
+        if (grid > nsm * 8) grid = nsm * 8;
+        if (grid > 0) k_update_gen<double><<<grid, 128, 0, st>>>(p, N, J);
+    } else {
+        const UpdateParams<float>& p = *reinterpret_cast<const UpdateParams<float>*>(params);
+        const int64_t nl = p.nslices * kWarp;
+        int grid = (int)((nl + 127) / 128);
+        if (grid > nsm * 8) grid = nsm * 8;
+        if (grid > 0) k_update_gen<float><<<grid, 128, 0, st>>>(p, N, J);
+    }
+}
+
+bool generic_shape_ok(int N, int J) { return N >= 2 && N <= kMaxN && J >= 1 && J <= kGJ; }
+
+}  // namespace pt

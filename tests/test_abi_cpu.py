@@ -56,7 +56,15 @@ def test_validation_without_gpu(pt):
         pt.ptucker_init(c + 5, v, [2, 2, 2], [2, 2, 2], 0.1, 0)  # coordinate out of range
     assert e.value.code == pt.PTUCKER_EINVAL
     with pytest.raises(pt.PTuckerError) as e:
-        pt.ptucker_init(c, v, [2, 2, 2], [7, 7, 7], 0.1, 0)      # (N, J) not compiled
+        pt.ptucker_init(c, v, [2, 2, 2], [17, 17, 17], 0.1, 0)   # J > 16 (no kernel at all)
+    assert e.value.code == pt.PTUCKER_EINVAL
+    c11 = np.zeros((4, 11), np.int32)
+    with pytest.raises(pt.PTuckerError) as e:
+        pt.ptucker_init(c11, v, [2] * 11, [2] * 11, 0.1, 0)      # N > 10
+    assert e.value.code == pt.PTUCKER_EINVAL
+    c8 = np.zeros((4, 8), np.int32)
+    with pytest.raises(pt.PTuckerError) as e:
+        pt.ptucker_init(c8, v, [2] * 8, [10] * 8, 0.1, 0)        # core 10^8 > 2^26 entries
     assert e.value.code == pt.PTUCKER_EINVAL
     with pytest.raises(pt.PTuckerError) as e:
         pt.ptucker_init(c, v, [2, 2, 2], [2, 3, 2], 0.1, 0)      # unequal J
