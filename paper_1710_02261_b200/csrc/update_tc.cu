@@ -13,21 +13,25 @@
 // One CTA per SM, 16 warps.  Warps w, w+4 (level 0) and w+8 (normal equations)
 // serve TMEM lane quarter w: thread t owns TMEM lane 32w+t = row segment 32w+t
 // of the current group of 4 SELL-32 slices.
-//   warps 0-7   LEVEL 0 (120 registers via setmaxnreg; warps w and w+4 take
-//               alternate tiles): per tile, load the J^2 columns t[k0][j] from
-//               TMEM (kBCH chunks per wait), finish level 0 (fp64 per term, or
-//               fp32 partial sums of G0 terms added in fp64) and hand delta (fp64)
-//               and x to warp w+8 through a shared-memory ring.
-//   warps 8-11  NORMAL EQUATIONS (232 registers): write the A row (tf32 hi/lo
-//               split of the gathered a1 row) of the tile kNA ahead into TMEM, then
-//               B += delta delta^T, c += x delta, sum x^2 in fp64 registers
-//               (Eq. 10-11), and at the end of the segment a = c [B + lambda I]^-1
-//               (Cholesky, Eq. 9) and the row's SSE (fused Eq. 5).
-//   warp 14     LOADER: streams the SELL coordinates/values into a coordinate ring
-//               (cp.async, kCPref tiles ahead) and gathers the two factor rows of
-//               every entry into a kRing-slot row ring (cp.async).
+//   warps 0-7   LEVEL 0 (kRegL0 registers via setmaxnreg; warps w and w+4 take
+//               alternate tiles).  At tile k a warp first writes the A rows of its
+//               tile k + kNA into TMEM (tf32 hi/lo split of the gathered a1 row)
+//               and copies that tile's a0 row and x into its own stash, releasing
+//               the row-ring slot early; then for tile k it loads the J^2 columns
+//               t[k0][j] from TMEM (kBCH chunks per wait), finishes level 0 (fp64
+//               per term, or fp32 partial sums of G0 terms added in fp64) and hands
+//               delta (fp64) and x to warp w+8 through a shared-memory ring.
+//   warps 8-11  NORMAL EQUATIONS (kRegNE registers): B += delta delta^T, c += x delta,
+//               sum x^2 in fp64 registers (Eq. 10-11), and at the end of the
+//               segment a = c [B + lambda I]^-1 (Cholesky, Eq. 9) and the row's SSE
+//               (fused Eq. 5).
+//   warps 14, 12, 13  LOADERS (tiles k = 0, 1, 2 mod kLoaders): stream the SELL
+//               coordinates/values into a coordinate ring (cp.async, kCPref own
+//               tiles ahead) and gather the two factor rows of every entry into a
+//               kRing-slot row ring (cp.async).  The gathers are bound by the
+//               L1TEX request rate of 16-byte lanes at distinct rows; three warps
+//               on three sub-partitions keep it fed.
 //   warp 15     MMA: lane 0 issues a tile's MMAs into one of kNT TMEM accumulators.
-//   (warps 12, 13 idle.)
 // Splitting level 0 from the normal equations keeps each role's registers small
 // enough for two level-0 warps per SM sub-partition (the XU conversions of one
 // overlap the waits of the other) and lets the XU and fp64 pipes work on
@@ -51,16 +55,34 @@ constexpr int kE = 128;                      // TMEM lanes = segments per group 
 constexpr int kThreads = 16 * 32;            // 2 level-0 WGs, normal-equation WG, loader/MMA WG
 constexpr int kRing = 6;                     // row ring slots (tiles between loader and level 0)
 constexpr int kCPref = 7;                    // loader: coordinates fetched this many tiles ahead of the gathers
-constexpr int kCRing = 8;                    // coordinate ring slots (> kCPref)
+#ifndef PT_LOADERS
+#define PT_LOADERS 3
+#endif
+constexpr int kLoaders = PT_LOADERS;         // loader warps (14, 12, 13): tiles k = lp (mod kLoaders)
+static_assert(kLoaders >= 1 && kLoaders <= 3, "loader warps");
+constexpr int kCRing = 8 * kLoaders;                    // coordinate ring slots (> kCPref)
 constexpr int kNT = 3;                       // TMEM accumulator buffers
-constexpr int kNA = 4;                       // TMEM A buffers (the normal-equation warps write A kNA tiles ahead)
+constexpr int kNA = 4;                       // TMEM A buffers (the level-0 warps write A kNA tiles ahead)
+constexpr int kStash = kNA / 2 + 1;          // a0/x stash slots per level-0 warp (its tiles k, k+2, .., k+kNA)
 constexpr int kD = 4;                        // delta ring slots (level 0 -> normal equations)
 constexpr int kRegLaunch = 65536 / kThreads / 8 * 8;  // registers per thread at launch (128)
-constexpr int kRegL0 = 120;                  // setmaxnreg: level-0 warpgroups
-constexpr int kRegNE = 232;                  //             normal-equation warpgroup
-constexpr int kRegP = 40;                    //             loader/MMA warpgroup
-constexpr int kBCH = 4;                      // level 0: TMEM chunks per load batch (registers)
-static_assert(kCRing > kCPref, "ring depths");
+#ifndef PT_REG_L0
+#define PT_REG_L0 136
+#endif
+#ifndef PT_REG_NE
+#define PT_REG_NE 200
+#endif
+#ifndef PT_BCH
+#define PT_BCH 4
+#endif
+constexpr int kRegL0 = PT_REG_L0;            // setmaxnreg: level-0 warpgroups
+constexpr int kRegNE = PT_REG_NE;            //             normal-equation warpgroup
+#ifndef PT_REG_P
+#define PT_REG_P 40
+#endif
+constexpr int kRegP = PT_REG_P;              //             loader/MMA warpgroup
+constexpr int kBCH = PT_BCH;                      // level 0: TMEM chunks per load batch (registers)
+static_assert(kCRing > kLoaders * kCPref, "ring depths");
 // setmaxnreg moves registers inside the CTA's launch allocation: the increases
 // must be covered by the helpers' release, or they wait forever
 static_assert(4 * kWarp * (2 * kRegL0 + kRegNE + kRegP) <= kRegLaunch * kThreads, "register pool");
@@ -212,7 +234,11 @@ struct Shape {
     static constexpr int OFF_ROW = (OFF_MISC + 64 + 127) / 128 * 128;
     static constexpr int OFF_CRD = OFF_ROW + kRing * RSLOT;
     static constexpr int OFF_DEL = OFF_CRD + kCRing * CSLOT;
-    static constexpr int OFF_BAR = (OFF_DEL + kD * DSLOT + 7) / 8 * 8;
+    // a0/x stash of the level-0 warps (copied out of the row ring when the A rows are
+    // split, kNA tiles before the tile is reduced): [warp 0..7][kStash][NQ][32] uint4 + [32] x
+    static constexpr int STSLOT = NQ * kWarp * 16 + kWarp * 4;
+    static constexpr int OFF_STASH = OFF_DEL + kD * DSLOT;
+    static constexpr int OFF_BAR = (OFF_STASH + 8 * kStash * STSLOT + 7) / 8 * 8;
     // raw_full[kRing], raw_empty[kRing], acc_full[kNT], acc_empty[kNT], a_full[kNA], d_full[4][kD], d_empty[4][kD],
     // a_empty[kNA]
     static constexpr int NBAR = 2 * kRing + 2 * kNT + 2 * kNA + 8 * kD;
@@ -235,7 +261,10 @@ struct Seg {
 };
 
 __device__ __forceinline__ void setmaxnreg_ne() { asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(kRegNE)); }
-__device__ __forceinline__ void setmaxnreg_l0() { asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(kRegL0)); }
+__device__ __forceinline__ void setmaxnreg_l0() {
+    if constexpr (kRegL0 > kRegLaunch) asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(kRegL0));
+    else asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(kRegL0));
+}
 __device__ __forceinline__ void setmaxnreg_dec() { asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(kRegP)); }
 
 // G0 (level-0 grouping, LAST64 only): 1 = every a0[k0] t[k0][j] product and the sum
@@ -318,14 +347,14 @@ __global__ void __launch_bounds__(kThreads, 1) k_update_tc(const UpdateParams<fl
             misc[1] = n;
             for (int s = 0; s < kRing; ++s) {
                 mbar_init(raw_full(s), 2 * kWarp);  // loader lanes: cp.async completion + plain arrive (x)
-                mbar_init(raw_empty(s), 8);         // the 4 level-0 warps (a0) + the 4 normal-equation warps (a1)
+                mbar_init(raw_empty(s), 4);         // the 4 level-0 warps of the tile (split: a1 to TMEM, a0/x to the stash)
             }
             for (int b = 0; b < kNT; ++b) {
                 mbar_init(acc_full(b), 1);   // tcgen05.commit
                 mbar_init(acc_empty(b), 4);  // level-0 warps done reading the accumulator
             }
             for (int a = 0; a < kNA; ++a) {
-                mbar_init(a_full(a), 4);   // normal-equation warps wrote their A rows
+                mbar_init(a_full(a), 4);   // the 4 level-0 warps of the tile wrote their A rows
                 mbar_init(a_empty(a), 1);  // tcgen05.commit: the MMAs reading A buffer a completed
             }
             for (int w = 0; w < 4; ++w)
@@ -345,8 +374,11 @@ __global__ void __launch_bounds__(kThreads, 1) k_update_tc(const UpdateParams<fl
 
     if (warp >= 12) {
         setmaxnreg_dec();
-        if (warp == 14) {
-            // ======================================================== loader
+        // loader warps 14, 12, 13 (the first kLoaders of them; 15 issues the MMAs)
+        const int lslot = warp == 14 ? 0 : (warp == 12 ? 1 : (warp == 13 ? 2 : 3));
+        if (lslot < kLoaders) {
+            // ======================================================== loader(s)
+            const uint32_t lp = (uint32_t)lslot;  // this loader's tiles: k = lp (mod kLoaders)
             const uint64_t pol_stream = policy_evict_first(), pol_rows = policy_evict_last();
             // coordinate cursor (tile kc): this lane's 4 segments u = lane + 32 i, i = slice of the group
             Sched pc = s0;
@@ -367,7 +399,17 @@ __global__ void __launch_bounds__(kThreads, 1) k_update_tc(const UpdateParams<fl
             };
             if (!pend) load_group();
             uint32_t kc = 0;
+            auto advance = [&]() {
+                ++kc;
+                if (++pe == piters) {
+                    ++pc.r;
+                    if (pc.valid()) load_group();
+                    else pend = true;
+                }
+            };
+            // coordinates of this loader's next tile (the cursor walks every tile)
             auto issue_crd = [&]() {
+                while (!pend && kc % kLoaders != lp) advance();
                 if (pend) return;
                 const int s = (int)(kc % kCRing);
 #pragma unroll
@@ -383,21 +425,25 @@ __global__ void __launch_bounds__(kThreads, 1) k_update_tc(const UpdateParams<fl
                         *crd(s, 1, u) = 0u;
                     }
                 }
-                ++kc;
-                if (++pe == piters) {
-                    ++pc.r;
-                    if (pc.valid()) load_group();
-                    else pend = true;
-                }
+                advance();
             };
             for (int s = 0; s < kCPref; ++s) {
                 issue_crd();
                 cp_async_commit();
             }
-            for (uint32_t k = 0; k < total; ++k) {
+#if defined(PT_TRACE) && defined(PT_TRACE_LOADER)
+            long long* const trl = (p.trace && blockIdx.x == 0 && lane == 0) ? p.trace + 6 * 512 : nullptr;
+#else
+            constexpr long long* trl = nullptr;  // loader trace off: the 40-register loader must not spill
+#endif
+            for (uint32_t k = lp; k < total; k += kLoaders) {
                 const int s = (int)(k % kRing), cs = (int)(k % kCRing);
+                const bool tl = trl && k >= 64 && k < 128;
+                if (tl) trl[(k - 64) * 8 + 0] = clock64();
                 if (k >= (uint32_t)kRing) mbar_wait(raw_empty(s), ((k / kRing) + 1) & 1);
+                if (tl) trl[(k - 64) * 8 + 1] = clock64();
                 cp_async_wait<kCPref - 1>();  // coordinates of tile k (committed kCPref groups ago)
+                if (tl) trl[(k - 64) * 8 + 2] = clock64();
 #pragma unroll
                 for (int i = 0; i < 4; ++i) {
                     const int u = lane + kWarp * i;
@@ -412,8 +458,10 @@ __global__ void __launch_bounds__(kThreads, 1) k_update_tc(const UpdateParams<fl
                 }
                 cp_async_mbar_arrive(raw_full(s));  // fires when this lane's rows have landed
                 mbar_arrive(raw_full(s));           // x (plain stores), release
+                if (tl) trl[(k - 64) * 8 + 3] = clock64();
                 issue_crd();
                 cp_async_commit();
+                if (tl) trl[(k - 64) * 8 + 4] = clock64();
             }
             cp_async_wait<0>();
         } else if (warp == 15 && lane == 0) {
@@ -429,7 +477,11 @@ __global__ void __launch_bounds__(kThreads, 1) k_update_tc(const UpdateParams<fl
                 dblo[ks] = umma_desc(smem_u32(sBlo) + ks * 256, 128, KP * 32);
             }
             // optional trace (tools/trace_tc.py): CTA 0, tiles [64, 128)
+#ifdef PT_TRACE
             long long* const trm = (p.trace && blockIdx.x == 0) ? p.trace + 4 * 512 : nullptr;
+#else
+            constexpr long long* trm = nullptr;
+#endif
             for (uint32_t k = 0; k < total; ++k) {
                 const int a = (int)(k % kNA), b = (int)(k % kNT);
                 const bool tr = trm && k >= 64 && k < 128;
@@ -469,14 +521,77 @@ __global__ void __launch_bounds__(kThreads, 1) k_update_tc(const UpdateParams<fl
         // ================================================================ level 0
         setmaxnreg_l0();
         const uint32_t par = (uint32_t)(warp >> 2);  // this warp takes the tiles k = par (mod 2)
+        unsigned char* const stash = sm + SH::OFF_STASH + warp * kStash * SH::STSLOT;
         const uint32_t tm_lane = tmem + ((uint32_t)(w4 * 32) << 16);
+#ifdef PT_TRACE
         long long* const trb = (p.trace && blockIdx.x == 0 && lane == 0 && warp < 4) ? p.trace + warp * 512 : nullptr;
+#else
+        constexpr long long* trb = nullptr;
+#endif
         auto mark = [&](uint32_t k, int ph) {
             if (trb && k >= 64 && k < 192) trb[((k - 64) >> 1) * 8 + ph] = clock64();
         };
+        // Tile k: once its rows have landed and MMA k - kNA (the last reader of A buffer
+        // k % kNA) has completed, write this thread's A row into TMEM lane te of that
+        // buffer (hi = a rounded to tf32 by two integer ops, lo = a - hi exact; the
+        // tensor core truncates lo to tf32, an error <= 2^-21 |a|; columns k >= J are
+        // zero) and arrive (one arrival per warp) for the MMA warp.
+        auto split = [&](uint32_t k) {
+            const int s = (int)(k % kRing);
+            mbar_wait(raw_full(s), (k / kRing) & 1);
+            if (k >= (uint32_t)kNA) mark(k - kNA, 7);
+            // A buffer k % kNA was last read by MMA k - kNA (its own barrier: each phase
+            // is one use of the buffer, so this wait can never be two phases behind)
+            if (k >= (uint32_t)kNA) mbar_wait(a_empty((int)(k % kNA)), ((k / kNA) + 1) & 1);
+            uint32_t hi[16], lo[16];
+#pragma unroll
+            for (int q = 0; q < KQ; ++q) {
+                uint32_t wv[4] = {0u, 0u, 0u, 0u};
+                if (q < NQ) {
+                    const uint4 r = *rowc(s, 1, q, te);
+                    wv[0] = r.x, wv[1] = r.y, wv[2] = r.z, wv[3] = r.w;
+                }
+#pragma unroll
+                for (int v = 0; v < 4; ++v) {
+                    const uint32_t hh = (wv[v] + 0x1000u) & 0xFFFFE000u;
+                    hi[4 * q + v] = hh;
+                    lo[4 * q + v] = __float_as_uint(__uint_as_float(wv[v]) - __uint_as_float(hh));
+                }
+            }
+            // a0 and x of the tile go to this warp's stash: the ring slot is free once split
+            {
+                const int st = (int)((k >> 1) % kStash);
+                unsigned char* sb = stash + st * SH::STSLOT;
+#pragma unroll
+                for (int q = 0; q < NQ; ++q)
+                    reinterpret_cast<uint4*>(sb)[q * kWarp + lane] = *rowc(s, 0, q, te);
+                reinterpret_cast<float*>(sb + NQ * kWarp * 16)[lane] = *rowx(s, te);
+            }
+            const uint32_t ta = tm_lane + SH::ACOL + (k % kNA) * 2 * KP;
+            if constexpr (KP == 16) {
+                tmem_st16(ta, hi);
+                tmem_st16(ta + KP, lo);
+            } else {
+                tmem_st8(ta, hi);
+                tmem_st8(ta + KP, lo);
+            }
+            asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+            asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+            __syncwarp();
+            if (lane == 0) {
+                mbar_arrive(a_full((int)(k % kNA)));
+                mbar_arrive(raw_empty(s));
+            }
+        };
+        // this warp writes the A rows of its own tiles (kNA is even: tile k + kNA has
+        // the parity of k), kNA tiles ahead of the one it reduces
+        static_assert(kNA % 2 == 0, "level-0 warps split their own tiles");
+        for (uint32_t k = par; k < (uint32_t)kNA && k < total; k += 2) split(k);
         for (uint32_t k = par; k < total; k += 2) {
             const int b = (int)(k % kNT), s = (int)(k % kRing);
             mark(k, 0);
+            if (k + kNA < total) split(k + kNA);
+            mark(k, 6);
             mbar_wait(acc_full(b), (k / kNT) & 1);
             asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
             mark(k, 1);
@@ -485,20 +600,18 @@ __global__ void __launch_bounds__(kThreads, 1) k_update_tc(const UpdateParams<fl
             const uint32_t taddr = tm_lane + b * NP;
 #pragma unroll
             for (int ch = 0; ch < kBCH && ch < NCH; ++ch) tmem_ld16(taddr + ch * 16, rb[ch]);
-            // a0 and x of tile k; release the slot (the normal-equation warps read a1)
-            mbar_wait(raw_full(s), (k / kRing) & 1);
+            // a0 and x of tile k from this warp's stash (written by this thread in split(k))
+            const unsigned char* sbk = stash + (int)((k >> 1) % kStash) * SH::STSLOT;
             float a0f[J];
 #pragma unroll
             for (int q = 0; q < NQ; ++q) {
-                const float4 v = *reinterpret_cast<const float4*>(rowc(s, 0, q, te));
+                const float4 v = reinterpret_cast<const float4*>(sbk)[q * kWarp + lane];
                 const float wv[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
                 for (int u = 0; u < 4; ++u)
                     if (4 * q + u < J) a0f[4 * q + u] = wv[u];
             }
-            const float x = *rowx(s, te);
-            __syncwarp();
-            if (lane == 0) mbar_arrive(raw_empty(s));
+            const float x = reinterpret_cast<const float*>(sbk + NQ * kWarp * 16)[lane];
             mark(k, 2);
 #pragma unroll
             for (int ch = 0; ch < kBCH && ch < NCH; ++ch) tmem_wait16(rb[ch]);
@@ -549,49 +662,6 @@ __global__ void __launch_bounds__(kThreads, 1) k_update_tc(const UpdateParams<fl
         // ====================================================== normal equations
         setmaxnreg_ne();
         const uint32_t tm_lane = tmem + ((uint32_t)(w4 * 32) << 16);
-        // Tile k: once its rows have landed and MMA k - kNA (the last reader of A buffer
-        // k % kNA) has completed, write this thread's A row into TMEM lane te of that
-        // buffer (hi = a rounded to tf32 by two integer ops, lo = a - hi exact; the
-        // tensor core truncates lo to tf32, an error <= 2^-21 |a|; columns k >= J are
-        // zero) and arrive (one arrival per warp) for the MMA warp.
-        auto split = [&](uint32_t k) {
-            const int s = (int)(k % kRing);
-            mbar_wait(raw_full(s), (k / kRing) & 1);
-            // A buffer k % kNA was last read by MMA k - kNA (its own barrier: each phase
-            // is one use of the buffer, so this wait can never be two phases behind)
-            if (k >= (uint32_t)kNA) mbar_wait(a_empty((int)(k % kNA)), ((k / kNA) + 1) & 1);
-            uint32_t hi[16], lo[16];
-#pragma unroll
-            for (int q = 0; q < KQ; ++q) {
-                uint32_t wv[4] = {0u, 0u, 0u, 0u};
-                if (q < NQ) {
-                    const uint4 r = *rowc(s, 1, q, te);
-                    wv[0] = r.x, wv[1] = r.y, wv[2] = r.z, wv[3] = r.w;
-                }
-#pragma unroll
-                for (int v = 0; v < 4; ++v) {
-                    const uint32_t hh = (wv[v] + 0x1000u) & 0xFFFFE000u;
-                    hi[4 * q + v] = hh;
-                    lo[4 * q + v] = __float_as_uint(__uint_as_float(wv[v]) - __uint_as_float(hh));
-                }
-            }
-            const uint32_t ta = tm_lane + SH::ACOL + (k % kNA) * 2 * KP;
-            if constexpr (KP == 16) {
-                tmem_st16(ta, hi);
-                tmem_st16(ta + KP, lo);
-            } else {
-                tmem_st8(ta, hi);
-                tmem_st8(ta + KP, lo);
-            }
-            asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
-            asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-            __syncwarp();
-            if (lane == 0) {
-                mbar_arrive(a_full((int)(k % kNA)));
-                mbar_arrive(raw_empty(s));
-            }
-        };
-        for (uint32_t k = 0; k < (uint32_t)kNA && k < total; ++k) split(k);
         auto load_seg = [&](const Sched& s, Seg& g) {
             const int64_t g0 = (int64_t)s.group() * 4;
             const int64_t sl = g0 + w4;
@@ -661,14 +731,17 @@ __global__ void __launch_bounds__(kThreads, 1) k_update_tc(const UpdateParams<fl
             if (nvalid) load_seg(sn, nxt);
             zero();
             int e = 0;
+#ifdef PT_TRACE
             long long* const trn = (p.trace && blockIdx.x == 0 && lane == 0 && w4 == 0) ? p.trace + 5 * 512 : nullptr;
+#else
+            constexpr long long* trn = nullptr;
+#endif
             auto markn = [&](uint32_t k, int ph) {
                 if (trn && k >= 64 && k < 128) trn[(k - 64) * 8 + ph] = clock64();
             };
             for (uint32_t k = 0; k < total; ++k) {
                 const int ds = (int)(k % kD);
                 markn(k, 0);
-                if (k + kNA < total) split(k + kNA);
                 markn(k, 1);
                 mbar_wait(d_full(w4, ds), (k / kD) & 1);
                 markn(k, 2);
