@@ -125,7 +125,13 @@ struct Ctx {
     void* smp_T = nullptr;                   // device table (largest over modes), fp64
     void* smp_T32 = nullptr;                 // fp32 copy of a kind-2 table
     // P-Tucker-Approx (approx.cu): presence of the core entries (C order) and lazy scratch
-    std::vector<uint8_t> core_present;
+    uint8_t* d_present = nullptr;            // [J^N] core entries not truncated (Alg. 4), device
+    int64_t n_present = 0;                   // their count (host bookkeeping of the truncation)
+    double* ax_R = nullptr;                  // [J^N] scores R(beta)
+    uint64_t *ax_key = nullptr, *ax_key2 = nullptr;  // selection sort keys (in/out)
+    int64_t *ax_idx = nullptr, *ax_idx2 = nullptr;   // selection sort values (in/out)
+    void* ax_tmp = nullptr;
+    size_t ax_tmp_bytes = 0;
     double *ax_G64 = nullptr, *ax_A0 = nullptr, *ax_W = nullptr, *ax_W2 = nullptr, *ax_E = nullptr,
            *ax_part = nullptr, *ax_UV = nullptr;
     void** ax_ptrs = nullptr;  // device: sc[0..N-2] of mode 0, then A[0..N-1]
@@ -398,7 +404,13 @@ void free_all() {
     g.lit_part = g.red_part = g.red_out = g.qr = g.qd = nullptr;
     g.ax_G64 = g.ax_A0 = g.ax_W = g.ax_W2 = g.ax_E = g.ax_part = g.ax_UV = nullptr;
     g.ax_ptrs = nullptr;
-    g.core_present.clear();
+    g.d_present = nullptr;
+    g.n_present = 0;
+    g.ax_R = nullptr;
+    g.ax_key = g.ax_key2 = nullptr;
+    g.ax_idx = g.ax_idx2 = nullptr;
+    g.ax_tmp = nullptr;
+    g.ax_tmp_bytes = 0;
     g.coo_c = nullptr;
     g.coo_v = nullptr;
     g.generic = false;
@@ -672,7 +684,9 @@ int ptucker_init(const int32_t* coords, const void* vals, int32_t vals_dtype, in
         CK(A.alloc((void**)&g.sse_row[n], dims[n] * sizeof(double)));
         CK(cudaMemsetAsync(g.sse_row[n], 0, dims[n] * sizeof(double), S()));
     }
-    g.core_present.assign((size_t)gsize, 1);
+    CK(A.alloc((void**)&g.d_present, (size_t)gsize));
+    CK(cudaMemsetAsync(g.d_present, 1, (size_t)gsize, S()));
+    g.n_present = gsize;
     int rc = rebuild_gp();
     if (rc) return rc;
     // ---- small-mode precontraction plans, order 4 only ----
@@ -907,7 +921,12 @@ int ptucker_orthogonalize(void) {
     });
     if (rc) return rc;
     g.sse_mode = -1;
-    std::fill(g.core_present.begin(), g.core_present.end(), (uint8_t)1);  // G x_n R is dense again
+    {
+        int64_t gs = 1;
+        for (int n = 0; n < g.N; ++n) gs *= g.J;
+        CK(cudaMemsetAsync(g.d_present, 1, (size_t)gs, S()));  // G x_n R is dense again
+        g.n_present = gs;
+    }
     return sync_and_check();
 }
 
@@ -951,7 +970,8 @@ int ptucker_set_core(const void* in) {
     rc = rebuild_gp();
     if (rc) return rc;
     g.sse_mode = -1;
-    g.core_present.assign((size_t)gsize, 1);  // a pushed core is dense (no truncation history)
+    CK(cudaMemsetAsync(g.d_present, 1, (size_t)gsize, S()));  // a pushed core is dense (no truncation history)
+    g.n_present = gsize;
     CK(cudaStreamSynchronize(S()));
     return PTUCKER_OK;
 }
@@ -959,7 +979,7 @@ int ptucker_set_core(const void* in) {
 // ---------------------------------------------------------------- P-Tucker-Approx
 namespace {
 // R(beta) (Eq. 13) of every core entry into R (C order; NaN for truncated entries).
-int compute_core_scores(std::vector<double>& R) {
+int compute_core_scores(bool with_keys) {
     const int N = g.N, J = g.J;
     int64_t K1 = 1;
     for (int n = 1; n < N; ++n) K1 *= J;
@@ -1011,17 +1031,20 @@ int compute_core_scores(std::vector<double>& R) {
     if (rc) return rc;
     }
     if (g.world > 1 && g.comm) NK(ncclAllReduce(g.ax_UV, g.ax_UV, (size_t)(2 * gsize), ncclDouble, ncclSum, g.comm, S()));
-    std::vector<double> UV((size_t)(2 * gsize));
-    std::vector<char> graw((size_t)(gsize * g.esz));
-    CK(cudaMemcpyAsync(UV.data(), g.ax_UV, UV.size() * sizeof(double), cudaMemcpyDeviceToHost, S()));
-    CK(cudaMemcpyAsync(graw.data(), g.G, graw.size(), cudaMemcpyDeviceToHost, S()));
-    CK(cudaStreamSynchronize(S()));
-    R.assign((size_t)gsize, std::nan(""));
-    for (int64_t b = 0; b < gsize; ++b) {
-        if (!g.core_present[b]) continue;
-        const double Gb = g.esz == 8 ? ((const double*)graw.data())[b] : (double)((const float*)graw.data())[b];
-        R[b] = 2.0 * Gb * UV[b] - Gb * Gb * UV[gsize + b];
+    // R (and the selection keys) on the device
+    if (!g.ax_R) {
+        CK(g.arena.alloc((void**)&g.ax_R, gsize * sizeof(double)));
+        CK(g.arena.alloc((void**)&g.ax_key, gsize * sizeof(uint64_t)));
+        CK(g.arena.alloc((void**)&g.ax_key2, gsize * sizeof(uint64_t)));
+        CK(g.arena.alloc((void**)&g.ax_idx, gsize * sizeof(int64_t)));
+        CK(g.arena.alloc((void**)&g.ax_idx2, gsize * sizeof(int64_t)));
+        g.ax_tmp_bytes = core_select_temp_bytes(gsize);
+        CK(g.arena.alloc(&g.ax_tmp, std::max<size_t>(g.ax_tmp_bytes, 16)));
     }
+    launch_core_scores(gsize, g.esz, g.G, g.ax_UV, g.d_present, g.ax_R, with_keys ? g.ax_key : nullptr,
+                       with_keys ? g.ax_idx : nullptr, S());
+    g.launches += 1;
+    CK(cudaGetLastError());
     return PTUCKER_OK;
 }
 }  // namespace
@@ -1030,10 +1053,12 @@ int ptucker_core_scores(double* out) {
     int rc = require_init();
     if (rc) return rc;
     if (!out) return fail(PTUCKER_EINVAL, "null buffer");
-    std::vector<double> R;
-    rc = compute_core_scores(R);
+    rc = compute_core_scores(false);
     if (rc) return rc;
-    memcpy(out, R.data(), R.size() * sizeof(double));
+    int64_t gsize = 1;
+    for (int n = 0; n < g.N; ++n) gsize *= g.J;
+    CK(cudaMemcpyAsync(out, g.ax_R, gsize * sizeof(double), cudaMemcpyDeviceToHost, S()));
+    CK(cudaStreamSynchronize(S()));
     return PTUCKER_OK;
 }
 
@@ -1041,34 +1066,23 @@ int ptucker_truncate_core(double p, int64_t* removed) {
     int rc = require_init();
     if (rc) return rc;
     if (!(p > 0.0 && p < 1.0)) return fail(PTUCKER_EINVAL, "truncation rate p must be in (0, 1)");
-    std::vector<double> R;
-    rc = compute_core_scores(R);
+    rc = compute_core_scores(true);
     if (rc) return rc;
-    const int64_t gsize = (int64_t)R.size();
-    std::vector<int64_t> idx;
-    for (int64_t b = 0; b < gsize; ++b)
-        if (g.core_present[b]) idx.push_back(b);
-    const int64_t n = (int64_t)idx.size();
+    int64_t gsize = 1;
+    for (int n = 0; n < g.N; ++n) gsize *= g.J;
+    const int64_t n = g.n_present;
     int64_t k = (int64_t)std::floor(p * (double)n);  // reading R29: floor(p |G|), at least one entry stays
     if (k > n - 1) k = n - 1;
     if (k < 0) k = 0;
-    // reading R28: descending R, ties by ascending C-order index (stable sort of an ascending list)
-    std::stable_sort(idx.begin(), idx.end(), [&](int64_t a, int64_t b) { return R[a] > R[b]; });
     if (k > 0) {
-        std::vector<char> graw((size_t)(gsize * g.esz));
-        CK(cudaMemcpyAsync(graw.data(), g.G, graw.size(), cudaMemcpyDeviceToHost, S()));
-        CK(cudaStreamSynchronize(S()));
-        for (int64_t r = 0; r < k; ++r) {
-            const int64_t b = idx[r];
-            g.core_present[b] = 0;
-            if (g.esz == 8) ((double*)graw.data())[b] = 0.0;
-            else ((float*)graw.data())[b] = 0.f;
-        }
-        CK(cudaMemcpyAsync(g.G, graw.data(), graw.size(), cudaMemcpyHostToDevice, S()));
+        // reading R28: descending R, ties by ascending C-order index (stable device sort)
+        CK(launch_core_truncate(gsize, k, g.ax_key, g.ax_idx, g.ax_key2, g.ax_idx2, g.ax_tmp, g.ax_tmp_bytes, g.esz,
+                                g.G, g.d_present, S()));
+        g.launches += 2;
+        g.n_present -= k;
         rc = rebuild_gp();
         if (rc) return rc;
         g.sse_mode = -1;
-        CK(cudaStreamSynchronize(S()));
     }
     if (removed) *removed = k;
     return PTUCKER_OK;
@@ -1078,9 +1092,7 @@ int ptucker_core_nnz(int64_t* nnz) {
     int rc = require_init();
     if (rc) return rc;
     if (!nnz) return fail(PTUCKER_EINVAL, "null out");
-    int64_t c = 0;
-    for (uint8_t v : g.core_present) c += v != 0;
-    *nnz = c;
+    *nnz = g.n_present;
     return PTUCKER_OK;
 }
 

@@ -273,3 +273,76 @@ void launch_approx_uv(int N, int J, int elem_bytes, int64_t nslices, const int64
 }
 
 }  // namespace pt
+
+// ---------------------------------------------------------------------------
+// Alg. 4 on the device: scores R(beta) = 2 G U - G^2 V of the present entries (NaN for
+// truncated ones), then the top-k present entries by R (descending; ties by ascending
+// C-order index, reading R28) are zeroed in G and marked absent.  The order comes from
+// a stable radix sort of order-preserving 64-bit keys (absent entries key 0, below any
+// real score), so the removed set is exactly the reading's.
+// ---------------------------------------------------------------------------
+#include <cub/cub.cuh>
+
+namespace pt {
+namespace {
+
+template <typename TS>
+__global__ void k_core_scores(int64_t gsize, const TS* G, const double* UV, const uint8_t* present, double* R,
+                              uint64_t* key, int64_t* idx) {
+    for (int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; b < gsize; b += (int64_t)gridDim.x * blockDim.x) {
+        const double g = (double)G[b];
+        const bool on = present[b] != 0;
+        const double r = on ? 2.0 * g * UV[b] - g * g * UV[gsize + b] : __longlong_as_double(0x7ff8000000000000LL);
+        R[b] = r;
+        if (key) {
+            // order-preserving map of a finite double to uint64 (negatives: all bits flipped,
+            // non-negatives: sign bit set); absent entries 0
+            const uint64_t u = (uint64_t)__double_as_longlong(r);
+            key[b] = on ? ((u >> 63) ? ~u : (u | 0x8000000000000000ULL)) : 0ULL;
+            idx[b] = b;
+        }
+    }
+}
+
+template <typename TS>
+__global__ void k_zero_top(int64_t k, const int64_t* order, TS* G, uint8_t* present) {
+    for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < k; r += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t b = order[r];
+        G[b] = TS(0);
+        present[b] = 0;
+    }
+}
+
+}  // namespace
+
+// R[gsize] on the device from UV (and, when key != null, the sort keys + identity indices).
+void launch_core_scores(int64_t gsize, int elem_bytes, const void* G, const double* UV, const uint8_t* present,
+                        double* R, uint64_t* key, int64_t* idx, cudaStream_t st) {
+    const unsigned grid = (unsigned)std::min<int64_t>((gsize + 255) / 256, 148 * 16);
+    if (elem_bytes == 8) k_core_scores<double><<<grid, 256, 0, st>>>(gsize, (const double*)G, UV, present, R, key, idx);
+    else k_core_scores<float><<<grid, 256, 0, st>>>(gsize, (const float*)G, UV, present, R, key, idx);
+}
+
+// Scratch bytes for core_truncate_select (keys/indices in and out + CUB temp).
+size_t core_select_temp_bytes(int64_t gsize) {
+    size_t tb = 0;
+    cub::DeviceRadixSort::SortPairsDescending(nullptr, tb, (const uint64_t*)nullptr, (uint64_t*)nullptr,
+                                              (const int64_t*)nullptr, (int64_t*)nullptr, (int)gsize);
+    return tb;
+}
+
+// Zero the k first entries of the (descending, stable) order of key: G[b] = 0, present[b] = 0.
+cudaError_t launch_core_truncate(int64_t gsize, int64_t k, const uint64_t* key, const int64_t* idx, uint64_t* key_out,
+                                 int64_t* idx_out, void* temp, size_t temp_bytes, int elem_bytes, void* G,
+                                 uint8_t* present, cudaStream_t st) {
+    cudaError_t e = cub::DeviceRadixSort::SortPairsDescending(temp, temp_bytes, key, key_out, idx, idx_out, (int)gsize,
+                                                              0, 64, st);
+    if (e != cudaSuccess) return e;
+    if (k <= 0) return cudaSuccess;
+    const unsigned grid = (unsigned)std::min<int64_t>((k + 255) / 256, 148 * 16);
+    if (elem_bytes == 8) k_zero_top<double><<<grid, 256, 0, st>>>(k, idx_out, (double*)G, present);
+    else k_zero_top<float><<<grid, 256, 0, st>>>(k, idx_out, (float*)G, present);
+    return cudaGetLastError();
+}
+
+}  // namespace pt

@@ -83,6 +83,13 @@ int tc_kp(int J);  // K padding of the tensor-core A operand (floats per split r
 void launch_update_generic(const void* params, int elem_bytes, int N, int J, int nsm, cudaStream_t st);
 bool generic_shape_ok(int N, int J);
 bool approx_shape_ok(int N, int J);  // approx.cu segment kernels instantiated for (N, J)
+// Alg. 4 on the device (approx.cu): scores from U, V; stable top-k truncation
+void launch_core_scores(int64_t gsize, int elem_bytes, const void* G, const double* UV, const uint8_t* present,
+                        double* R, uint64_t* key, int64_t* idx, cudaStream_t st);
+size_t core_select_temp_bytes(int64_t gsize);
+cudaError_t launch_core_truncate(int64_t gsize, int64_t k, const uint64_t* key, const int64_t* idx, uint64_t* key_out,
+                                 int64_t* idx_out, void* temp, size_t temp_bytes, int elem_bytes, void* G,
+                                 uint8_t* present, cudaStream_t st);
 // U, V of Eq. 13 from their definition over a device COO (shapes without a compiled (N, J))
 void launch_approx_literal(int N, int J, int elem_bytes, const void* const* d_A, int lda, const int32_t* coords,
                            const void* vals, const double* xhat, int64_t n, int64_t row_lo, int64_t row_hi,

@@ -81,6 +81,14 @@ constexpr int kRegNE = PT_REG_NE;            //             normal-equation warp
 #define PT_REG_P 40
 #endif
 constexpr int kRegP = PT_REG_P;              //             loader/MMA warpgroup
+#ifndef PT_L0_XU_MOD
+#define PT_L0_XU_MOD 2
+#endif
+#ifndef PT_A0_INT
+#define PT_A0_INT 0
+#endif
+constexpr int kXuMod = PT_L0_XU_MOD;         // level 0 (G0 = 1): every kXuMod-th t converted on the XU pipe, the rest by integer ops
+constexpr bool kA0Int = PT_A0_INT != 0;      // a0 converted by integer ops too
 constexpr int kBCH = PT_BCH;                      // level 0: TMEM chunks per load batch (registers)
 static_assert(kCRing > kLoaders * kCPref, "ring depths");
 // setmaxnreg moves registers inside the CTA's launch allocation: the increases
@@ -619,6 +627,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_update_tc(const UpdateParams<fl
             // level 0: d[j] = sum_k0 a0[k0] t[k0][j]; t[k0][j] is TMEM column k0*J + j
             TD d[J];
             float pf[J];  // fp32 partial sums (G0 > 1)
+            double a0d[J];
+#pragma unroll
+            for (int q = 0; q < J; ++q) a0d[q] = kA0Int ? f2d_int(a0f[q]) : double(a0f[q]);
 #pragma unroll
             for (int j = 0; j < J; ++j) d[j] = TD(0);
 #pragma unroll
@@ -638,7 +649,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_update_tc(const UpdateParams<fl
                 } else if constexpr (G0 == 1) {
                     // half of the fp32 -> fp64 conversions by integer ops on the ALU pipe, the
                     // other half on the (quarter-rate) XU pipe, so neither pipe saturates
-                    d[j] = fma(TD(a0f[k0]), (cc & 1) ? f2d_int(tv) : TD(tv), d[j]);
+                    d[j] = fma(a0d[k0], (cc % kXuMod == 0) ? TD(tv) : f2d_int(tv), d[j]);
                 } else {
                     if (k0 % G0 == 0) pf[j] = a0f[k0] * tv;
                     else pf[j] = fmaf(a0f[k0], tv, pf[j]);
