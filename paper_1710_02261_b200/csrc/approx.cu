@@ -127,21 +127,32 @@ __global__ void __launch_bounds__(kApproxWarps * 32) k_approx_seg(
 
 // U[j0*K1 + b'] = sum_s A0seg[s][j0] W[s][b'],  V = sum_s A0seg[s][j0]^2 W2[s][b'];
 // blockIdx.y = a contiguous range of segments (per-range partials, fixed-order sum).
-__global__ void k_approx_outer(int J, int K1, int64_t nseg, int64_t per, const double* A0seg, const double* W,
+template <int J>
+__global__ void k_approx_outer(int K1, int64_t nseg, int64_t per, const double* A0seg, const double* W,
                                const double* W2, double* part) {
-    const int64_t out = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    // thread per b' (all J values of j0 at once, so W and W2 are read once);
+    // blockIdx.y = a contiguous range of segments (per-range partials, fixed-order sum)
+    const int b = blockIdx.x * blockDim.x + threadIdx.x;
+    if (b >= K1) return;
     const int64_t nout = (int64_t)J * K1;
-    if (out >= nout) return;
-    const int j0 = (int)(out / K1), b = (int)(out % K1);
     const int64_t s0 = (int64_t)blockIdx.y * per, s1 = s0 + per < nseg ? s0 + per : nseg;
-    double u = 0.0, v = 0.0;
+    double u[J], v[J];
+#pragma unroll
+    for (int j0 = 0; j0 < J; ++j0) u[j0] = v[j0] = 0.0;
     for (int64_t s = s0; s < s1; ++s) {
-        const double a = A0seg[s * J + j0];
-        u = fma(a, W[s * K1 + b], u);
-        v = fma(a * a, W2[s * K1 + b], v);
+        const double w = W[s * K1 + b], w2 = W2[s * K1 + b];
+#pragma unroll
+        for (int j0 = 0; j0 < J; ++j0) {
+            const double a = A0seg[s * J + j0];
+            u[j0] = fma(a, w, u[j0]);
+            v[j0] = fma(a * a, w2, v[j0]);
+        }
     }
-    part[((int64_t)blockIdx.y * 2 + 0) * nout + out] = u;
-    part[((int64_t)blockIdx.y * 2 + 1) * nout + out] = v;
+#pragma unroll
+    for (int j0 = 0; j0 < J; ++j0) {
+        part[((int64_t)blockIdx.y * 2 + 0) * nout + (int64_t)j0 * K1 + b] = u[j0];
+        part[((int64_t)blockIdx.y * 2 + 1) * nout + (int64_t)j0 * K1 + b] = v[j0];
+    }
 }
 
 __global__ void k_approx_sum(int64_t nout, int nsplit, const double* part, double* UV) {
@@ -267,8 +278,14 @@ void launch_approx_uv(int N, int J, int elem_bytes, int64_t nslices, const int64
 #undef PT_APPROX_CASE
     }
     const int64_t per = nlanes > 0 ? (nlanes + nsplit - 1) / nsplit : 1;
-    dim3 g2((unsigned)((gsize + 127) / 128), (unsigned)nsplit);
-    k_approx_outer<<<g2, 128, 0, st>>>(J, K1, nlanes, per, A0seg, W, W2, part);
+    dim3 g2((unsigned)((K1 + 127) / 128), (unsigned)nsplit);
+    switch (J) {
+#define PT_OUTER_CASE(JJ) \
+    case JJ: k_approx_outer<JJ><<<g2, 128, 0, st>>>(K1, nlanes, per, A0seg, W, W2, part); break;
+        PT_OUTER_CASE(2) PT_OUTER_CASE(3) PT_OUTER_CASE(4) PT_OUTER_CASE(5) PT_OUTER_CASE(8) PT_OUTER_CASE(10)
+#undef PT_OUTER_CASE
+        default: break;  // not reached: launch_approx_uv is called for compiled (N, J) only
+    }
     k_approx_sum<<<(unsigned)((gsize + 127) / 128), 128, 0, st>>>(gsize, nsplit, part, UV);
 }
 
