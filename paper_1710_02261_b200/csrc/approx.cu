@@ -80,8 +80,18 @@ __global__ void __launch_bounds__(kApproxWarps * 32) k_approx_seg(
         // whole segment when K1 <= 256, else swept in chunks of 256 (re-gathering the entries)
         for (int b0 = 0; b0 < K1; b0 += 256) {
             double acc[8], acc2[8];
+            int ix[8][N - 1];  // this lane's b' = b0 + lane + 32 m as row offsets (n - 1) * 10 + b_n
 #pragma unroll
-            for (int m = 0; m < 8; ++m) acc[m] = acc2[m] = 0.0;
+            for (int m = 0; m < 8; ++m) {
+                acc[m] = acc2[m] = 0.0;
+                int b = b0 + lane + 32 * m;
+                b = b < K1 ? b : 0;
+#pragma unroll
+                for (int n = N - 1; n >= 1; --n) {
+                    ix[m][n - 1] = (n - 1) * 10 + b % J;
+                    b /= J;
+                }
+            }
             for (int e0 = 0; e0 < len; e0 += 32) {
                 const int e = e0 + lane;
                 double* r = Rw + lane * rstride;
@@ -92,7 +102,17 @@ __global__ void __launch_bounds__(kApproxWarps * 32) k_approx_seg(
                         for (int j = 0; j < J; ++j) r[(n - 1) * 10 + j] = (double)rowp[j];
                     }
                     double xh = 0.0;
-                    for (int b = 0; b < K1; ++b) xh = fma(kprod(b, r), H[b], xh);
+                    if constexpr (N == 3) {  // x_hat = sum_b1 r1[b1] sum_b2 H[b1][b2] r2[b2]
+#pragma unroll
+                        for (int b1 = 0; b1 < J; ++b1) {
+                            double t = 0.0;
+#pragma unroll
+                            for (int b2 = 0; b2 < J; ++b2) t = fma(H[b1 * J + b2], r[10 + b2], t);
+                            xh = fma(r[b1], t, xh);
+                        }
+                    } else {
+                        for (int b = 0; b < K1; ++b) xh = fma(kprod(b, r), H[b], xh);
+                    }
                     Ew[lane] = xh - (double)sv[slot];
                 }
                 __syncwarp();
@@ -104,7 +124,9 @@ __global__ void __launch_bounds__(kApproxWarps * 32) k_approx_seg(
                     for (int m = 0; m < 8; ++m) {
                         const int b = b0 + lane + 32 * m;
                         if (b < K1) {
-                            const double k = kprod(b, rq);
+                            double k = rq[ix[m][0]];
+#pragma unroll
+                            for (int n = 1; n < N - 1; ++n) k *= rq[ix[m][n]];
                             acc[m] = fma(ee, k, acc[m]);
                             acc2[m] = fma(k, k, acc2[m]);
                         }
