@@ -43,7 +43,7 @@ def measured_peaks():
         return {}
 
 
-def roofline(N, J, policy, info, l0_group, nsm, clk_mhz, entries, launch_s, dtype, cfg_name):
+def roofline(N, J, policy, info, l0_group, nsm, clk_mhz, entries, launch_s, dtype, cfg_name, mode_s=None):
     """Roofline of the row-update kernel: T_roof = max over the pipes the
     shipped kernel uses of (algorithmic work on that pipe / its peak), per launch.
 
@@ -55,7 +55,14 @@ def roofline(N, J, policy, info, l0_group, nsm, clk_mhz, entries, launch_s, dtyp
     tensor = measured bf16 (MEASURED_PEAKS.json) x 1/2 (nominal tf32/bf16 ratio), HBM =
     measured copy bandwidth.  The fp32->fp64 conversions (XU pipe, 16/clk/SM measured) and
     the tensor work the 3xTF32 split and K/N padding add are reported as diagnostics: they
-    are costs of the precision policy, not algorithmic work."""
+    are costs of the precision policy, not algorithmic work.
+
+    Modes that run the small-mode precontraction (SMP, order 4) are counted
+    with the work that kernel performs (SURVEY §8(d) rule 2): kind 2 (two small other modes)
+    J^2 fp64 + the normal equations per entry, kind 1 (one small other mode) J^3 fp32 +
+    J^2 fp64 + the normal equations; the per-update table precompute is < 0.1% and left out.
+    With per-mode launch times `mode_s`, T_roof and T_meas are summed over the modes
+    (SURVEY §8(d) rule 1) and frac = sum T_roof / sum T_meas."""
     mp = measured_peaks()
     p32 = nsm * 128 * 2 * clk_mhz * 1e6 / 1e12
     p64 = nsm * 64 * 2 * clk_mhz * 1e6 / 1e12
@@ -86,12 +93,33 @@ def roofline(N, J, policy, info, l0_group, nsm, clk_mhz, entries, launch_s, dtyp
         xu = sum(J ** (L + 1) for L in range(min(n64, N - 2)))  # fp32 inputs of the fp64 levels
     sv = 8 if dtype == "f64" else 4
     hbm_bytes = (4 * (N - 1) + sv) * entries
-    t = {"fp32": 2 * w32 * entries / (p32 * 1e12), "fp64": 2 * w64 * entries / (p64 * 1e12),
-         "tensor_tf32": 2 * wtc * entries / (ptc * 1e12), "hbm": hbm_bytes / (bw * 1e9)}
+
+    def pipe_times(a32, a64, atc):
+        return {"fp32": 2 * a32 * entries / (p32 * 1e12), "fp64": 2 * a64 * entries / (p64 * 1e12),
+                "tensor_tf32": 2 * atc * entries / (ptc * 1e12), "hbm": hbm_bytes / (bw * 1e9)}
+
+    t = pipe_times(w32, w64, wtc)
     pipe = max(t, key=t.get)
     peak = {"fp32": p32, "fp64": p64, "tensor_tf32": ptc, "hbm": bw}[pipe]
     work = {"fp32": 2 * w32, "fp64": 2 * w64, "tensor_tf32": 2 * wtc}.get(pipe)
-    if pipe == "hbm":
+    kinds = [m.get("smp", 0) for m in info.get("modes", [])]
+    per_mode = None
+    if mode_s and any(kinds) and policy != "F64":
+        per_mode, roof_sum, pipe_sum = [], 0.0, {}
+        for n, kind in enumerate(kinds):
+            a32, a64 = {0: (w32, w64), 1: (J ** 3, J * J + bc), 2: (0, J * J + bc)}[kind]
+            tn = pipe_times(a32, a64, 0)
+            pn = max(tn, key=tn.get)
+            roof_sum += tn[pn]
+            pipe_sum[pn] = pipe_sum.get(pn, 0.0) + tn[pn]
+            per_mode.append({"mode": n, "smp": kind, "fp32_fma": a32, "fp64_fma": a64, "pipe": pn,
+                             "roof_ms": tn[pn] * 1e3, "measured_ms": mode_s[n] * 1e3})
+        frac_t = roof_sum / sum(mode_s)
+        pipe = max(pipe_sum, key=pipe_sum.get)
+        peak = {"fp32": p32, "fp64": p64, "tensor_tf32": ptc, "hbm": bw}[pipe]
+        achieved, unit = frac_t * peak, ("GB/s" if pipe == "hbm" else "TFLOP/s")
+        bound = "hbm" if pipe == "hbm" else ("tensor" if pipe == "tensor_tf32" else "alu")
+    elif pipe == "hbm":
         achieved, unit, bound = hbm_bytes / launch_s / 1e9, "GB/s", "hbm"
     else:
         achieved, unit = work * entries / launch_s / 1e12, "TFLOP/s"
@@ -106,6 +134,10 @@ def roofline(N, J, policy, info, l0_group, nsm, clk_mhz, entries, launch_s, dtyp
                          "hbm": "MEASURED_PEAKS hbm_gbs"}[pipe],
          "work_per_entry": {"fp32_fma": w32, "fp64_fma": w64, "tc_mac": wtc, "hbm_bytes": 4 * (N - 1) + sv},
          "roof_ms_by_pipe": {k: v * 1e3 for k, v in t.items()}, "roof_ms": t[pipe] * 1e3}
+    if per_mode:
+        r["per_mode"] = per_mode
+        r["roof_ms"] = sum(m["roof_ms"] for m in per_mode)
+        r["kernel"] = "k_update / k_update_smp2 / table k_update (per mode, SMP)"
     if xu:
         xu_peak = nsm * 16 * clk_mhz * 1e6
         r["xu_conversions_per_entry"] = xu
@@ -343,8 +375,9 @@ def run_ours(args, cfg):
     clk_max = (clocks or {}).get("sm_max_mhz") or 1965.0
     entries_per_launch = cfg.nnz / world           # each rank's launch covers its row block of one mode
     avg_launch_s = (upd_ms / max(upd_n, 1)) / 1e3
+    mode_s = [per_mode[f"update_m{n}"] / 1e3 for n in range(N)]
     roof = roofline(N, J, policy, info, args.l0_group, nsm, clk_max, entries_per_launch, avg_launch_s,
-                    cfg.dtype, cfg.name)
+                    cfg.dtype, cfg.name, mode_s)
     if args.approx > 0:
         roof["approx"] = {"p": args.approx, "scores_ms_per_step": apx_ms / args.steps,
                           "core_nnz_after": pt.ptucker_core_nnz()}

@@ -1,0 +1,46 @@
+"""bench.py's roofline accounting on CPU: the pipe that
+bounds each kernel, per-mode sums for the small-mode precontraction, frac <= 1 for a
+measured time at or above the roof."""
+import importlib.util
+import os
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.fixture(scope="module")
+def bench():
+    spec = importlib.util.spec_from_file_location("bench_mod", os.path.join(ROOT, "bench.py"))
+    m = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(m)
+    return m
+
+
+def test_tc_path_is_fp64_bound(bench):
+    info = {"tensor_cores": True, "modes": [{"smp": 0}] * 3}
+    r = bench.roofline(3, 10, "F32-B", info, 1, 148, 1965.0, 1e8, 4.2e-3, "f32", "c5")
+    assert r["pipe"] == "fp64" and r["work_per_entry"]["fp64_fma"] == 100 + 66
+    # 166 fp64 FMAs x 1e8 entries at 148 x 64 x 2 x 1.965 GHz = 0.892 ms
+    assert abs(r["roof_ms"] - 0.8919) < 1e-3
+    assert abs(r["frac"] - r["roof_ms"] / 4.2) < 1e-9
+
+
+def test_alu_path_counts_ttv_chain(bench):
+    info = {"tensor_cores": False, "modes": [{"smp": 0}] * 5}
+    r = bench.roofline(5, 5, "F32-C", info, 1, 148, 1965.0, 1e7, 6e-3, "f32", "c4")
+    # inner J^N = 3125 fp32; the outer levels 25 + 125 + 625 in fp64 (F32-C) + 21 (B, c, x^2)
+    assert r["work_per_entry"]["fp32_fma"] == 3125
+    assert r["work_per_entry"]["fp64_fma"] == 25 + 125 + 625 + 21
+    assert r["pipe"] == "fp32"
+
+
+def test_smp_modes_use_the_shipped_work(bench):
+    info = {"tensor_cores": False, "modes": [{"smp": 2}, {"smp": 2}, {"smp": 1}, {"smp": 1}]}
+    mode_s = [1.9e-3, 1.7e-3, 3.2e-3, 3.2e-3]
+    r = bench.roofline(4, 10, "F32-C", info, 1, 148, 1965.0, 2e7, sum(mode_s) / 4, "f32", "c3", mode_s)
+    kinds = [m["smp"] for m in r["per_mode"]]
+    assert kinds == [2, 2, 1, 1]
+    assert r["per_mode"][0]["fp64_fma"] == 100 + 66 and r["per_mode"][2]["fp32_fma"] == 1000
+    assert 0 < r["frac"] <= 1.0
+    assert abs(r["frac"] - r["roof_ms"] / (sum(mode_s) * 1e3)) < 1e-9
