@@ -37,6 +37,29 @@ struct CoreInConst {
     static constexpr bool value = (size_t)ipow(J, N - 2) * gblk(J, sizeof(TS)) * sizeof(TS) <= sizeof(c_core);
 };
 
+// float -> double by integer operations (ALU pipe) instead of the quarter-rate XU
+// conversion: exact for normal floats of either sign; zero or subnormal inputs become
+// +-2^-127 (1 + m) (absolute error < 1.2e-38).  Used for half of the fp32 -> fp64
+// conversions between TTV levels so that neither pipe saturates.
+__device__ __forceinline__ double f2d_alu(float f) {
+    const uint32_t u = __float_as_uint(f);
+    const uint32_t hi = ((uint32_t)((int32_t)u >> 3) & 0x8FFFFFFFu) + 0x38000000u;
+    return __hiloint2double((int)hi, (int)(u << 29));
+}
+// TO(x) for the level outputs: half by the ALU (odd j), half by the XU
+template <typename TO, typename TI>
+__device__ __forceinline__ TO widen(TI x, int j) {
+    if constexpr (std::is_same<TO, double>::value && std::is_same<TI, float>::value) {
+#ifndef PT_NO_F2D_ALU
+        return (j & 1) ? f2d_alu(x) : double(x);
+#else
+        return double(x);
+#endif
+    } else {
+        return TO(x);
+    }
+}
+
 template <typename T> struct Vec16;
 template <> struct Vec16<float> { using type = float4; static constexpr int n = 4; };
 template <> struct Vec16<double> { using type = double2; static constexpr int n = 2; };
@@ -98,7 +121,7 @@ __device__ __forceinline__ void ttv_level(const TS* __restrict__ g, const TF (&a
             TF ti[J];
             ttv_inner<TS, J, TF, TF>(g + k * sub, a_in, ti);
 #pragma unroll
-            for (int j = 0; j < J; ++j) t[j] = TO(ti[j]);
+            for (int j = 0; j < J; ++j) t[j] = widen<TO>(ti[j], j);
         } else {
             LevelT<TF, L + 1, L64> tc[J];
             ttv_level<TS, TF, N, J, L64, L + 1>(g + k * sub, a_in, a_out, tc);
@@ -130,7 +153,7 @@ __device__ __forceinline__ void compute_delta(const TS* __restrict__ g, const TF
             ttv_inner<TS, J, TF, TF>(g + k * GB, a_in, t);
             const TO ak = TO(a_out[0][k]);
 #pragma unroll
-            for (int j = 0; j < J; ++j) d[j] = fma(ak, TO(t[j]), d[j]);
+            for (int j = 0; j < J; ++j) d[j] = fma(ak, widen<TO>(t[j], j), d[j]);
         }
     } else {
         constexpr int sub = ipow(J, N - 3) * GB;
@@ -247,8 +270,16 @@ __host__ __device__ inline size_t gp_smem_bytes(int gp_elems, int esz) { return 
 
 // TABLE: the "core" is a table of blocks in shared memory (small-mode
 // precontraction, smp.cu) and each lane contracts with block lane_aux[slot].
+// CTAs per SM the update kernel is compiled for: small J keeps its fp64 normal
+// equations in <= 128 registers, so two CTAs (16 warps) hide the core-load latency
+// (c4: 8 warps per SM left the FFMAs waiting on their LDS.128 operands).
+#ifndef PT_UPD_MINB_SMALLJ
+#define PT_UPD_MINB_SMALLJ 2
+#endif
+constexpr int upd_min_blocks(int J, int esz) { return (J <= 5 && esz == 4) ? PT_UPD_MINB_SMALLJ : 1; }
+
 template <typename TS, typename TF, int N, int J, int L64, bool LITERAL, bool TABLE = false>
-__global__ void __launch_bounds__(kUpdThreads, 1) k_update(const UpdateParams<TS> p) {
+__global__ void __launch_bounds__(kUpdThreads, upd_min_blocks(J, (int)sizeof(TS))) k_update(const UpdateParams<TS> p) {
     using TD = LevelT<TF, 0, L64>;  // type of delta
     constexpr int NB = J * (J + 1) / 2;
     using V = typename Vec16<TS>::type;
