@@ -32,19 +32,22 @@ constexpr int kApproxWarps = 8;  // warps per block of k_approx_seg (one SELL se
 // batch's entries are accumulated into W, W2 with the b' split over the lanes (no
 // global loads in that inner loop).
 template <typename TS, int N, int J>
-__global__ void __launch_bounds__(kApproxWarps * 32) k_approx_seg(
+#ifndef PT_APPROX_MINB
+#define PT_APPROX_MINB 2
+#endif
+__global__ void __launch_bounds__(kApproxWarps * 32, PT_APPROX_MINB) k_approx_seg(
     int64_t nlanes, const int64_t* slice_off, const int32_t* lane_row,
     const int32_t* lane_len, const int32_t* const* sc, const TS* sv, const TS* const* A, int lda,
     const double* G64, double* A0seg, double* W, double* W2, double* Eslot) {
     // dynamic shared memory, per warp: H[K1] (padded to 8 doubles), the batch's rows
-    // [32][4][J] (fp64, J <= 10 -> stride 10) and e[32]
+    // [32][N-1][J] (fp64) and e[32]
     extern __shared__ double smem[];
     constexpr int K1 = ipow(J, N - 1);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int k1p = (K1 + 7) / 8 * 8;
-    const int rstride = 4 * 10;
+    constexpr int rstride = (N - 1) * J;  // staged rows of one entry (fp64)
     double* H = smem + warp * (k1p + 32 * rstride + 32);
-    double* Rw = H + k1p;               // Rw[entry * rstride + (n-1) * 10 + j]
+    double* Rw = H + k1p;               // Rw[entry * rstride + (n-1) * J + j]
     double* Ew = Rw + 32 * rstride;     // Ew[entry]
     (void)Eslot;
     for (int64_t seg = (int64_t)blockIdx.x * kApproxWarps + warp; seg < nlanes;
@@ -71,24 +74,25 @@ __global__ void __launch_bounds__(kApproxWarps * 32) k_approx_seg(
         auto kprod = [&](int b, const double* r) {
             double k = 1.0;
             for (int n = N - 1; n >= 1; --n) {
-                k *= r[(n - 1) * 10 + b % J];
+                k *= r[(n - 1) * J + b % J];
                 b /= J;
             }
             return k;
         };
         // W, W2 accumulators of this lane's b' (b' = lane + 32 m), kept in registers over the
         // whole segment when K1 <= 256, else swept in chunks of 256 (re-gathering the entries)
+        constexpr int MB = (K1 < 256 ? K1 : 256) / 32 + ((K1 < 256 ? K1 : 256) % 32 != 0);  // b' per lane per chunk
         for (int b0 = 0; b0 < K1; b0 += 256) {
-            double acc[8], acc2[8];
-            int ix[8][N - 1];  // this lane's b' = b0 + lane + 32 m as row offsets (n - 1) * 10 + b_n
+            double acc[MB], acc2[MB];
+            int ix[MB][N - 1];  // this lane's b' = b0 + lane + 32 m as row offsets (n - 1) * J + b_n
 #pragma unroll
-            for (int m = 0; m < 8; ++m) {
+            for (int m = 0; m < MB; ++m) {
                 acc[m] = acc2[m] = 0.0;
                 int b = b0 + lane + 32 * m;
                 b = b < K1 ? b : 0;
 #pragma unroll
                 for (int n = N - 1; n >= 1; --n) {
-                    ix[m][n - 1] = (n - 1) * 10 + b % J;
+                    ix[m][n - 1] = (n - 1) * J + b % J;
                     b /= J;
                 }
             }
@@ -99,7 +103,7 @@ __global__ void __launch_bounds__(kApproxWarps * 32) k_approx_seg(
                     const int64_t slot = base + (int64_t)e * 32;
                     for (int n = 1; n < N; ++n) {
                         const TS* rowp = A[n] + (int64_t)sc[n - 1][slot] * lda;
-                        for (int j = 0; j < J; ++j) r[(n - 1) * 10 + j] = (double)rowp[j];
+                        for (int j = 0; j < J; ++j) r[(n - 1) * J + j] = (double)rowp[j];
                     }
                     double xh = 0.0;
                     if constexpr (N == 3) {  // x_hat = sum_b1 r1[b1] sum_b2 H[b1][b2] r2[b2]
@@ -107,7 +111,7 @@ __global__ void __launch_bounds__(kApproxWarps * 32) k_approx_seg(
                         for (int b1 = 0; b1 < J; ++b1) {
                             double t = 0.0;
 #pragma unroll
-                            for (int b2 = 0; b2 < J; ++b2) t = fma(H[b1 * J + b2], r[10 + b2], t);
+                            for (int b2 = 0; b2 < J; ++b2) t = fma(H[b1 * J + b2], r[J + b2], t);
                             xh = fma(r[b1], t, xh);
                         }
                     } else {
@@ -121,7 +125,7 @@ __global__ void __launch_bounds__(kApproxWarps * 32) k_approx_seg(
                     const double* rq = Rw + q * rstride;
                     const double ee = Ew[q];
 #pragma unroll
-                    for (int m = 0; m < 8; ++m) {
+                    for (int m = 0; m < MB; ++m) {
                         const int b = b0 + lane + 32 * m;
                         if (b < K1) {
                             double k = rq[ix[m][0]];
@@ -135,7 +139,7 @@ __global__ void __launch_bounds__(kApproxWarps * 32) k_approx_seg(
                 __syncwarp();
             }
 #pragma unroll
-            for (int m = 0; m < 8; ++m) {
+            for (int m = 0; m < MB; ++m) {
                 const int b = b0 + lane + 32 * m;
                 if (b < K1) {
                     w[b] = acc[m];
@@ -281,7 +285,7 @@ void launch_approx_uv(int N, int J, int elem_bytes, int64_t nslices, const int64
     if (nlanes > 0) {
         int grid = (int)((nlanes + kApproxWarps - 1) / kApproxWarps);
         if (grid > nsm * 8) grid = nsm * 8;
-        const size_t smem = (size_t)kApproxWarps * ((K1 + 7) / 8 * 8 + 32 * 40 + 32) * sizeof(double);
+        const size_t smem = (size_t)kApproxWarps * ((K1 + 7) / 8 * 8 + 32 * (N - 1) * J + 32) * sizeof(double);
 #define PT_APPROX_CASE(NN, JJ)                                                                                     \
     if (N == NN && J == JJ) {                                                                                      \
         if (elem_bytes == 8) {                                                                                     \
