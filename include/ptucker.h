@@ -172,7 +172,13 @@ int ptucker_get_partition(int32_t n, int64_t* bounds);
  *  "emulate_world", "emulate_rank"  (before init, no communicator): build and update only
  *                 this rank's row blocks of a `world`-way partition, without the exchange
  *                 (tests of the partitioned path on one GPU)
- *  "time_kernels" 1 = bracket every kernel launch with CUDA events (ptucker_kernel_stats) */
+ *  "time_kernels" 1 = bracket every kernel launch with CUDA events (ptucker_kernel_stats)
+ *  "l0_group"     tensor-core kernel, F32-B: level-0 terms summed in fp32 in runs of g before
+ *                 the fp64 sum (1 = every term in fp64, default; 2; 5 fails the 1e-5 row bound)
+ *  "l2_persist_mb" L2 set-aside (MB) for the evict_last factor-row gathers: -1 = the device
+ *                 maximum (default; applied at init, released by ptucker_finalize), 0 = leave
+ *                 the driver default (a device-wide limit: other users of the GPU see it)
+ *  "trace"        1 = per-phase clock marks of the tensor-core kernel (builds with -DPT_TRACE) */
 int ptucker_set_option(const char* key, int64_t value);
 
 /* Device time (CUDA events on the library stream) accumulated for kernel
