@@ -321,6 +321,7 @@ def run_ours(args, cfg):
     pt.ptucker_set_option("l0_group", args.l0_group)
     if args.l2_persist_mb is not None:
         pt.ptucker_set_option("l2_persist_mb", args.l2_persist_mb)
+    pt.ptucker_set_option("pack_gathers", args.pack_gathers)
     pt.ptucker_synchronize()
     init_s = time.perf_counter() - t0
     info = pt.ptucker_info()
@@ -453,6 +454,8 @@ def main():
     ap.add_argument("--tc", type=int, default=1, choices=[0, 1], help="tensor-core inner stage for order-3 fp32")
     ap.add_argument("--l2-persist-mb", type=int, default=None,
                     help="L2 set-aside for evict_last accesses in MB (-1 = device maximum; default: driver default)")
+    ap.add_argument("--pack-gathers", type=int, default=0, choices=[0, 1],
+                    help="J = 10 tensor-core gathers from packed 40-byte tables (less DRAM traffic, slower)")
     ap.add_argument("--l0-group", type=int, default=1, choices=[1, 2, 5], help="tensor-core level-0 grouping (1 = fp64 per term, g = fp32 partial sums of g terms)")
     ap.add_argument("--approx", type=float, default=0.0,
                     help="P-Tucker-Approx: truncate the core by rate p after every iteration (0 = P-Tucker)")

@@ -113,8 +113,9 @@ struct Ctx {
     int use_tc = 1;                          // option "tc"
     int l0_group = 1;                        // option "l0_group" (tensor-core kernel, F32-B)
     int64_t l2_persist_mb = -1;              // option "l2_persist_mb": L2 set-aside for evict_last lines (-1 = max)
-    float* tc_hi = nullptr;                  // tf32 split of the innermost factor (tensor-core kernel)
-    float* tc_lo = nullptr;
+    int pack_gathers = 0;                    // option "pack_gathers": J = 10 tensor-core gathers from packed tables
+    float* pk_head[2] = {nullptr, nullptr};  // tensor-core kernel, J = 10: packed gather tables
+    float* pk_tail[2] = {nullptr, nullptr};
     int use_smp = 1;                         // option "smp"
     int smp_tab = 2;                         // option "smp_table": 0 fp32 smem, 1 fp64 L2, 2 hybrid (default)
     struct Smp {
@@ -253,8 +254,10 @@ UpdateParams<TS> make_params(int n, bool literal) {
     p.work = g.d_work;
     p.policy = g.policy;
     p.trace = g.trace;
-    p.ext0 = g.tc_hi;
-    p.ext1 = g.tc_lo;
+    p.gmain[0] = g.pk_head[0];
+    p.gmain[1] = g.pk_head[1];
+    p.gtail[0] = g.pk_tail[0];
+    p.gtail[1] = g.pk_tail[1];
     p.l0_group = g.l0_group;
     return p;
 }
@@ -334,7 +337,26 @@ int launch_update_kernel(int n, bool literal) {
         UpdateParams<double> p = make_params<double>(n, literal);
         k->launch(&p, literal, grid, S());
     } else {
+        const bool packed = g.pack_gathers && !literal && k != g.kern_alu && g.J == 10;
+        if (packed) {  // tensor-core kernel: pack the two gathered factors (L2-resident gathers)
+            if (!g.pk_head[0]) {
+                int64_t imax = 0;
+                for (int m = 0; m < g.N; ++m) imax = std::max<int64_t>(imax, g.dims[m]);
+                for (int t = 0; t < 2; ++t) {
+                    CK(g.arena.alloc((void**)&g.pk_head[t], (size_t)imax * 8 * sizeof(float)));
+                    CK(g.arena.alloc((void**)&g.pk_tail[t], (size_t)imax * 2 * sizeof(float)));
+                }
+            }
+            int t = 0;
+            for (int m = 0; m < g.N; ++m) {
+                if (m == n) continue;
+                launch_pack_rows10((const float*)g.A[m], g.dims[m], g.lda, g.pk_head[t], g.pk_tail[t], S());
+                ++t;
+            }
+            g.launches += 2;
+        }
         UpdateParams<float> p = make_params<float>(n, literal);
+        if (!packed) p.gmain[0] = p.gmain[1] = p.gtail[0] = p.gtail[1] = nullptr;
         k->launch(&p, literal, grid, S());
     }
     CK(cudaGetLastError());
@@ -401,7 +423,7 @@ void free_all() {
     g.G = g.Gtmp = nullptr;
     g.smp_T = nullptr;
     g.smp_T32 = nullptr;
-    g.tc_hi = g.tc_lo = nullptr;
+    g.pk_head[0] = g.pk_head[1] = g.pk_tail[0] = g.pk_tail[1] = nullptr;
     g.lit_part = g.red_part = g.red_out = g.qr = g.qd = nullptr;
     g.ax_G64 = g.ax_A0 = g.ax_W = g.ax_W2 = g.ax_E = g.ax_part = g.ax_UV = nullptr;
     g.ax_ptrs = nullptr;
@@ -514,6 +536,10 @@ int ptucker_set_option(const char* key, int64_t value) {
         if (value < 1 || value > (1 << 20)) return fail(PTUCKER_EINVAL, "seg_len out of range");
         if (g.inited) return fail(PTUCKER_ESTATE, "seg_len must be set before ptucker_init");
         g.seg_len = (int)value;
+        return PTUCKER_OK;
+    }
+    if (k == "pack_gathers") {
+        g.pack_gathers = value != 0;
         return PTUCKER_OK;
     }
     if (k == "l2_persist_mb") {

@@ -54,8 +54,8 @@ struct UpdateParams {
     unsigned int* work;           // dynamic slice counter (reset to 0 before launch)
     int policy;                   // runtime copy of the precision policy (info only)
     long long* trace;             // optional per-phase clock trace (tools; null in production)
-    const void* ext0;             // kernel-specific extra inputs (tensor-core kernel: tf32 hi/lo split
-    const void* ext1;             //   tables of the innermost factor, KP floats per row)
+    const float* gmain[2];        // tensor-core kernel, J = 10: the two gathered factors with rows split
+    const float* gtail[2];        //   into 32-byte heads (floats 0..7) and packed 8-byte tails (8..9)
     int l0_group;                 // tensor-core kernel: level-0 terms summed in fp32 before fp64 (1 or 2)
 };
 
@@ -79,6 +79,9 @@ const UpdateKernel* find_update_kernel(int prec, int l64, int N, int J);
 // Tensor-core variant (fp32, N = 3): innermost TTV stage on tcgen05 (update_tc.cu).
 const UpdateKernel* find_update_kernel_tc(int l64, int J);
 int tc_kp(int J);  // K padding of the tensor-core A operand (floats per split row)
+// J = 10 gather tables of the tensor-core kernel (kernels.cu): head[i] = A[i][0..8), tail[i] = A[i][8..10)
+void launch_pack_rows10(const float* A, int64_t I, int lda, float* head, float* tail, cudaStream_t st);
+
 // Generic-order kernel (update_generic.cu): any N <= kMaxN, J <= 16, fp64; p.Gp = G in C order.
 void launch_update_generic(const void* params, int elem_bytes, int N, int J, int nsm, cudaStream_t st);
 bool generic_shape_ok(int N, int J);

@@ -2,6 +2,7 @@
 // heavy-row finalize, deterministic sums, CholeskyQR2 and the core update.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdint>
 
 #include "internal.cuh"
@@ -366,6 +367,25 @@ void launch_core_mode_product(const void* G, void* Gout, int elem_bytes, int N, 
     const int grid = (int)((total + 255) / 256);
     if (elem_bytes == 8) k_core_mode_product<double><<<grid, 256, 0, st>>>((const double*)G, (double*)Gout, N, J, n, R);
     else k_core_mode_product<float><<<grid, 256, 0, st>>>((const float*)G, (float*)Gout, N, J, n, R);
+}
+
+// Rows of a J = 10 fp32 factor (48-byte padded) split for the tensor-core kernel's
+// gathers: 32-byte heads and 8-byte tails, 40 of 48 bytes per row, so the two tables a
+// mode update gathers from (80 MB at c5) fit the L2 set-aside.
+__global__ void k_pack_rows10(const float* __restrict__ A, int64_t I, int lda, float4* __restrict__ head,
+                              float2* __restrict__ tail) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < I; i += (int64_t)gridDim.x * blockDim.x) {
+        const float4* r = reinterpret_cast<const float4*>(A + i * lda);
+        head[2 * i] = r[0];
+        head[2 * i + 1] = r[1];
+        tail[i] = *reinterpret_cast<const float2*>(A + i * lda + 8);
+    }
+}
+
+void launch_pack_rows10(const float* A, int64_t I, int lda, float* head, float* tail, cudaStream_t st) {
+    const int grid = (int)std::min<int64_t>((I + 255) / 256, 148 * 16);
+    if (grid > 0)
+        k_pack_rows10<<<grid, 256, 0, st>>>(A, I, lda, reinterpret_cast<float4*>(head), reinterpret_cast<float2*>(tail));
 }
 
 }  // namespace pt

@@ -70,7 +70,7 @@ constexpr int kRegLaunch = 65536 / kThreads / 8 * 8;  // registers per thread at
 #define PT_REG_L0 136
 #endif
 #ifndef PT_REG_NE
-#define PT_REG_NE 200
+#define PT_REG_NE 192
 #endif
 #ifndef PT_BCH
 #define PT_BCH 4
@@ -78,7 +78,7 @@ constexpr int kRegLaunch = 65536 / kThreads / 8 * 8;  // registers per thread at
 constexpr int kRegL0 = PT_REG_L0;            // setmaxnreg: level-0 warpgroups
 constexpr int kRegNE = PT_REG_NE;            //             normal-equation warpgroup
 #ifndef PT_REG_P
-#define PT_REG_P 40
+#define PT_REG_P 48
 #endif
 constexpr int kRegP = PT_REG_P;              //             loader/MMA warpgroup
 #ifndef PT_L0_XU_MOD
@@ -191,6 +191,11 @@ __device__ __forceinline__ uint64_t policy_evict_last() {
 }
 __device__ __forceinline__ void cp_async4_hint(void* smem, const void* gmem, uint64_t pol) {
     asm volatile("cp.async.ca.shared.global.L2::cache_hint [%0], [%1], 4, %2;\n" ::"r"(smem_u32(smem)), "l"(gmem),
+                 "l"(pol)
+                 : "memory");
+}
+__device__ __forceinline__ void cp_async8_hint(void* smem, const void* gmem, uint64_t pol) {
+    asm volatile("cp.async.ca.shared.global.L2::cache_hint [%0], [%1], 8, %2;\n" ::"r"(smem_u32(smem)), "l"(gmem),
                  "l"(pol)
                  : "memory");
 }
@@ -335,6 +340,15 @@ __global__ void __launch_bounds__(kThreads, 1) k_update_tc(const UpdateParams<fl
         sBhi[kmaj<KP>(c, k1)] = hv;
         sBlo[kmaj<KP>(c, k1)] = tf32_rna(v - hv);
     }
+    if constexpr (NQ == 3) {
+        // packed J = 10 gathers write 8 of chunk 2's 16 bytes: the rest (row padding) stays zero
+        for (int i = threadIdx.x; i < kRing * 2 * kE; i += kThreads) {
+            const int sl = i / (2 * kE), k = (i / kE) % 2, u = i % kE;
+            float* c2 = reinterpret_cast<float*>(rowc(sl, k, 2, u));
+            c2[2] = 0.f;
+            c2[3] = 0.f;
+        }
+    }
     if (warp == 0) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&misc[0])),
                      "n"(SH::TCOLS));
@@ -387,6 +401,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_update_tc(const UpdateParams<fl
         if (lslot < kLoaders) {
             // ======================================================== loader(s)
             const uint32_t lp = (uint32_t)lslot;  // this loader's tiles: k = lp (mod kLoaders)
+            // J = 10 with packed gather tables (option "pack_gathers"): 2.5x less DRAM traffic,
+            // but the 8-byte tail copies make the update ~10% slower
+            const bool kPacked = J == 10 && p.gmain[0] != nullptr;
             const uint64_t pol_stream = policy_evict_first(), pol_rows = policy_evict_last();
             // coordinate cursor (tile kc): this lane's 4 segments u = lane + 32 i, i = slice of the group
             Sched pc = s0;
@@ -452,6 +469,24 @@ __global__ void __launch_bounds__(kThreads, 1) k_update_tc(const UpdateParams<fl
                 if (tl) trl[(k - 64) * 8 + 1] = clock64();
                 cp_async_wait<kCPref - 1>();  // coordinates of tile k (committed kCPref groups ago)
                 if (tl) trl[(k - 64) * 8 + 2] = clock64();
+                if (kPacked) {
+                    // J = 10 packed tables: 32-byte head (2 chunks) + 8-byte tail per row; the
+                    // upper half of chunk 2 stays zero (set once at setup)
+#pragma unroll
+                    for (int i = 0; i < 4; ++i) {
+                        const int u = lane + kWarp * i;
+                        const int64_t c0 = (int)*crd(cs, 0, u), c1 = (int)*crd(cs, 1, u);
+                        const char* h0 = reinterpret_cast<const char*>(p.gmain[0] + c0 * 8);
+                        const char* h1 = reinterpret_cast<const char*>(p.gmain[1] + c1 * 8);
+                        cp_async16_hint(rowc(s, 0, 0, u), h0, pol_rows);
+                        cp_async16_hint(rowc(s, 1, 0, u), h1, pol_rows);
+                        cp_async16_hint(rowc(s, 0, 1, u), h0 + 16, pol_rows);
+                        cp_async16_hint(rowc(s, 1, 1, u), h1 + 16, pol_rows);
+                        cp_async8_hint(rowc(s, 0, 2, u), p.gtail[0] + c0 * 2, pol_rows);
+                        cp_async8_hint(rowc(s, 1, 2, u), p.gtail[1] + c1 * 2, pol_rows);
+                        *rowx(s, u) = __uint_as_float(*crd(cs, 2, u));
+                    }
+                } else {
 #pragma unroll
                 for (int i = 0; i < 4; ++i) {
                     const int u = lane + kWarp * i;
@@ -463,6 +498,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_update_tc(const UpdateParams<fl
                         cp_async16_hint(rowc(s, 1, q, u), r1 + 16 * q, pol_rows);
                     }
                     *rowx(s, u) = __uint_as_float(*crd(cs, 2, u));
+                }
                 }
                 cp_async_mbar_arrive(raw_full(s));  // fires when this lane's rows have landed
                 mbar_arrive(raw_full(s));           // x (plain stores), release

@@ -142,6 +142,29 @@ def test_mode_update_f32(pt, orc, name, scale, seg):
         assert [m["smp"] for m in info["modes"]] == [2, 2, 1, 1]
 
 
+@pytest.mark.parametrize("name,scale", [("c2", 0.01), ("c5", 0.0005)])
+def test_mode_update_tc_packed_gathers(pt, orc, name, scale):
+    """J = 10 tensor-core updates with the packed 32 + 8-byte gather tables (option
+    pack_gathers): same rows as the oracle within 1e-5, and bit-identical to the
+    unpacked gathers (the same values reach the same arithmetic)."""
+    cfg = synth.small(name, scale)
+    coords, vals = init_cfg(pt, cfg)
+    t = orc.Tensor(coords, vals, cfg.dims)
+    pt.ptucker_set_option("pack_gathers", 1)
+    try:
+        mode_update_parity(pt, orc, t, cfg, 1e-5, sweeps=1)
+        s0 = oracle_state(orc, t, cfg, 1)
+        got = {}
+        for pk in (0, 1):
+            pt.ptucker_set_option("pack_gathers", pk)
+            push_state(pt, s0, np.float32)
+            pt.ptucker_update_mode(1)
+            got[pk] = pt.ptucker_get_factor(1).copy()
+        assert np.array_equal(got[0], got[1])
+    finally:
+        pt.ptucker_set_option("pack_gathers", 0)
+
+
 @pytest.mark.parametrize("name,scale", [("c2", 0.01), ("c4", 0.001)])
 def test_mode_update_f64_variants(pt, orc, name, scale):
     """Every config also runs in FP64 mode (1e-10 per row)."""
