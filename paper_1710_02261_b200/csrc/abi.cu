@@ -839,9 +839,9 @@ int ptucker_update_mode(int32_t n) {
     ModeIndex& m = g.mi[n];
     if (m.nheavy > 0) {
         rc = timed("finalize", [&]() -> int {
-            launch_heavy_finalize(m.nheavy, m.hrow, m.hnseg, m.hpbase, m.partials, g.J, g.lambda, g.A[n], g.esz,
+            launch_heavy_finalize(m.nheavy, m.hrow, m.hnseg, m.hpbase, m.partials, m.hrec, g.J, g.lambda, g.A[n], g.esz,
                                   g.lda, g.sse_row[n], g.d_fail, S());
-            g.launches += 1;
+            g.launches += 2;
             CK(cudaGetLastError());
             return PTUCKER_OK;
         }, n);

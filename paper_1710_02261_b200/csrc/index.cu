@@ -7,7 +7,7 @@
 //   3. Every row becomes ceil(len/S) segments of <= S entries (S = seg_len;
 //      an empty row is one segment of length 0, which solves to a = 0).  Rows
 //      with more than one segment are "heavy": their segments write partial
-//      (B, c, sum x^2) records that k_heavy_finalize reduces in a fixed order.
+//      (B, c, sum x^2) records that k_heavy_sum / k_heavy_solve reduce in a fixed order.
 //   4. Segments are stably sorted by length (descending) and cut into slices
 //      of 32 -- one warp per slice, one lane per segment, so lanes of a warp
 //      do near-equal work (the paper's load balancing concern).
@@ -330,6 +330,7 @@ cudaError_t build_mode_sell(const int32_t* d_coords, const void* d_vals, int ele
     IB_CHECK(dalloc(&mi.hnseg, mi.nheavy, arena));
     IB_CHECK(dalloc(&mi.hpbase, mi.nheavy, arena));
     IB_CHECK(dalloc(&mi.partials, mi.npartial_doubles, arena));
+    IB_CHECK(dalloc(&mi.hrec, mi.nheavy * PW, arena));
     if (nrows > 0)
         k_heavy_list<<<grid_for(nrows), 256, 0, st>>>(r0, nrows, PW, nseg_r, hidx, hbase, mi.hrow, mi.hnseg, mi.hpbase);
     if (ngroups > 0)

@@ -50,6 +50,7 @@ struct ModeIndex {
     int32_t* hnseg = nullptr;
     int64_t* hpbase = nullptr;
     double* partials = nullptr;
+    double* hrec = nullptr;          // [nheavy][PW] summed records (heavy-row finalize scratch)
     std::vector<int64_t> bounds;     // world+1 row-block bounds
 };
 

@@ -7,6 +7,7 @@
 
 #include "internal.cuh"
 #include "kernels.cuh"
+#include "update.cuh"
 
 namespace pt {
 
@@ -121,32 +122,57 @@ __device__ bool chol_solve_rt(const double* rec, int J, double lam, double* a) {
     return ok;
 }
 
-// Heavy rows: the partial records of a row's segments are stored
-// component-major (partials[pbase + p*nseg + s]).  Warp w sums components
-// p = w, w+8, ...: lane l adds segments l, l+32, ... in order, then a fixed
-// xor-butterfly -- the result depends only on the row's own segments (F9).
-template <typename T>
-__global__ void __launch_bounds__(256) k_heavy_finalize(const int32_t* hrow, const int32_t* hnseg,
-                                                        const int64_t* hpbase, const double* partials, int J,
-                                                        double lambda, T* An, int lda, double* sse_row, int* fail) {
-    __shared__ double rec[16 * 17 / 2 + 16 + 1];
-    const int h = blockIdx.x;
-    const int PW = J * (J + 1) / 2 + J + 1;
-    const int nseg = hnseg[h];
-    const int64_t pb = hpbase[h];
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    for (int p = warp; p < PW; p += 8) {
-        double acc = 0.0;
-        const double* src = partials + pb + (int64_t)p * nseg;
-        for (int s = lane; s < nseg; s += 32) acc += src[s];
+// Heavy rows: the partial records of a row's segments are stored component-major
+// (partials[pbase + p*nseg + s]).  Stage 1: one warp per (row, component): lane l adds
+// segments l, l+32, ... into four interleaved accumulators (more loads in flight),
+// combined in a fixed order, then a fixed xor-butterfly -- the result depends only on
+// the row's own segments (F9).  Stage 2: one thread per row solves in registers.
+__global__ void __launch_bounds__(256) k_heavy_sum(int64_t nheavy, int PW, const int32_t* hnseg,
+                                                   const int64_t* hpbase, const double* partials, double* rec) {
+    const int lane = threadIdx.x & 31;
+    const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
+    for (int64_t w = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); w < nheavy * PW; w += nw) {
+        const int64_t h = w / PW;
+        const int p = (int)(w % PW);
+        const int nseg = hnseg[h];
+        const double* src = partials + hpbase[h] + (int64_t)p * nseg;
+        double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+        int s = lane;
+        for (; s + 96 < nseg; s += 128) {
+            a0 += src[s];
+            a1 += src[s + 32];
+            a2 += src[s + 64];
+            a3 += src[s + 96];
+        }
+        for (; s < nseg; s += 32) a0 += src[s];
+        double acc = (a0 + a1) + (a2 + a3);
         for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-        if (lane == 0) rec[p] = acc;
+        if (lane == 0) rec[w] = acc;
     }
-    __syncthreads();
-    if (threadIdx.x == 0) {
+}
+
+// JC > 0: the solve in registers (chol_solve<JC>, update.cuh); JC = 0: runtime J <= 16.
+template <typename T, int JC>
+__global__ void __launch_bounds__(128) k_heavy_solve(int64_t nheavy, const int32_t* hrow, const double* recs, int J,
+                                                     double lambda, T* An, int lda, double* sse_row, int* fail) {
+    const int PW = J * (J + 1) / 2 + J + 1;
+    for (int64_t h = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; h < nheavy; h += (int64_t)gridDim.x * blockDim.x) {
+        const double* rec = recs + h * PW;
         const int row = hrow[h];
         double a[16];
-        const bool ok = chol_solve_rt(rec, J, lambda, a);
+        bool ok;
+        if constexpr (JC > 0) {
+            double B[JC * (JC + 1) / 2], c[JC], x[JC];
+#pragma unroll
+            for (int q = 0; q < JC * (JC + 1) / 2; ++q) B[q] = rec[q];
+#pragma unroll
+            for (int q = 0; q < JC; ++q) c[q] = rec[JC * (JC + 1) / 2 + q];
+            ok = chol_solve<JC>(B, c, lambda, x);
+#pragma unroll
+            for (int q = 0; q < JC; ++q) a[q] = x[q];
+        } else {
+            ok = chol_solve_rt(rec, J, lambda, a);
+        }
         if (!ok) {
             atomicCAS(fail, 0, row + 1);
             for (int j = 0; j < J; ++j) a[j] = 0.0;
@@ -169,15 +195,29 @@ __global__ void __launch_bounds__(256) k_heavy_finalize(const int32_t* hrow, con
 }
 
 void launch_heavy_finalize(int64_t nheavy, const int32_t* hrow, const int32_t* hnseg, const int64_t* hpbase,
-                           const double* partials, int J, double lambda, void* An, int elem_bytes, int lda,
-                           double* sse_row, int* fail, cudaStream_t st) {
+                           const double* partials, double* rec, int J, double lambda, void* An, int elem_bytes,
+                           int lda, double* sse_row, int* fail, cudaStream_t st) {
     if (nheavy <= 0) return;
-    if (elem_bytes == 8)
-        k_heavy_finalize<double><<<(unsigned)nheavy, 256, 0, st>>>(hrow, hnseg, hpbase, partials, J, lambda,
-                                                                   (double*)An, lda, sse_row, fail);
-    else
-        k_heavy_finalize<float><<<(unsigned)nheavy, 256, 0, st>>>(hrow, hnseg, hpbase, partials, J, lambda,
-                                                                  (float*)An, lda, sse_row, fail);
+    const int PW = J * (J + 1) / 2 + J + 1;
+    const int64_t nwarps = nheavy * PW;
+    const unsigned g1 = (unsigned)std::min<int64_t>((nwarps + 7) / 8, 148 * 32);
+    k_heavy_sum<<<g1, 256, 0, st>>>(nheavy, PW, hnseg, hpbase, partials, rec);
+    const unsigned g2 = (unsigned)std::min<int64_t>((nheavy + 127) / 128, 148 * 16);
+#define PT_HF(JC)                                                                                                  \
+    if (elem_bytes == 8)                                                                                           \
+        k_heavy_solve<double, JC><<<g2, 128, 0, st>>>(nheavy, hrow, rec, J, lambda, (double*)An, lda, sse_row, fail); \
+    else                                                                                                           \
+        k_heavy_solve<float, JC><<<g2, 128, 0, st>>>(nheavy, hrow, rec, J, lambda, (float*)An, lda, sse_row, fail);
+    switch (J) {
+        case 2: PT_HF(2) break;
+        case 3: PT_HF(3) break;
+        case 4: PT_HF(4) break;
+        case 5: PT_HF(5) break;
+        case 8: PT_HF(8) break;
+        case 10: PT_HF(10) break;
+        default: PT_HF(0) break;
+    }
+#undef PT_HF
 }
 
 // ---------------------------------------------------------------------------
