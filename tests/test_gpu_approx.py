@@ -138,3 +138,41 @@ def test_truncation_edges(pt, orc):
     assert np.count_nonzero(pt.ptucker_get_core()) == 1
     pt.ptucker_sweep()                                # still a valid model
     assert np.isfinite(pt.ptucker_error())
+
+
+def test_truncation_ties_lower_index_first(pt, orc):
+    """Reading R28 on the device path: two core entries with bit-identical scores (equal
+    G values, identical factor columns, so every term of U and V is the same) are removed
+    lower C-order index first, as the oracle's stable sort does."""
+    rng = np.random.default_rng(7)
+    I0, I1, J = 40, 30, 3
+    coords = np.stack([rng.integers(0, I0, 400), rng.integers(0, I1, 400)], 1).astype(np.int32)
+    vals = rng.random(400)
+    pt.ptucker_finalize()
+    pt.ptucker_set_option("emulate_world", 1)
+    pt.ptucker_set_option("emulate_rank", 0)
+    pt.ptucker_init(coords, vals, [I0, I1], [J, J], 0.1, 0)
+    A0 = rng.random((I0, J))
+    col = rng.random(I1)
+    A1 = np.stack([col, col, rng.random(I1)], 1)       # columns 0 and 1 identical
+    G = rng.random((J, J))
+    G[:, 1] = G[:, 0]                                  # beta = (j, 0) and (j, 1) tie for every j
+    G *= 10.0                                          # make the tied pairs the top scores
+    G[:, 2] = 0.01
+    pt.ptucker_set_core(G)
+    pt.ptucker_set_factor(0, A0)
+    pt.ptucker_set_factor(1, A1)
+    R = pt.ptucker_core_scores().reshape(-1)
+    assert R[0] == R[1] and R[3] == R[4] and R[6] == R[7]
+    t = orc.Tensor(coords, vals, [I0, I1])
+    m = orc.Model(G.astype(np.float64).copy(), [A0.copy(), A1.copy()])
+    present = np.ones(J * J, np.uint8)
+    for p in (0.15, 0.2, 0.3):                         # removes 1 (a tie split), then 1, then 2
+        before = present.copy()
+        _, k_o = orc.truncate_core(t, m, present, p)
+        k_g = pt.ptucker_truncate_core(p)
+        assert k_g == k_o
+        G_g = pt.ptucker_get_core().reshape(-1)
+        removed_g = set(np.flatnonzero((G_g == 0) & (before == 1)).tolist())
+        removed_o = set(np.flatnonzero(before & ~present).tolist())
+        assert removed_g == removed_o, (p, removed_g, removed_o)
