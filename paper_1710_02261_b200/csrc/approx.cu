@@ -96,6 +96,16 @@ __global__ void __launch_bounds__(kApproxWarps * 32, PT_APPROX_MINB) k_approx_se
                     b /= J;
                 }
             }
+            // order 3: lane (g, b2) = (lane / J, lane % J) accumulates W[b1][b2], W2[b1][b2] for
+            // all b1 over the batch entries q = g (mod 32 / J): each r2 value is loaded once and
+            // the r1 row is a broadcast read (about half the shared-memory loads per b')
+            constexpr int NG3 = 32 / J;
+            const int g3 = lane / J, c3 = lane % J;
+            double a3[N == 3 ? J : 1], a3s[N == 3 ? J : 1];
+            if constexpr (N == 3) {
+#pragma unroll
+                for (int b1 = 0; b1 < J; ++b1) a3[b1] = a3s[b1] = 0.0;
+            }
             for (int e0 = 0; e0 < len; e0 += 32) {
                 const int e = e0 + lane;
                 double* r = Rw + lane * rstride;
@@ -121,6 +131,23 @@ __global__ void __launch_bounds__(kApproxWarps * 32, PT_APPROX_MINB) k_approx_se
                 }
                 __syncwarp();
                 const int cnt = len - e0 < 32 ? len - e0 : 32;
+                if constexpr (N == 3) {
+                    if (g3 < NG3) {
+                        for (int q = g3; q < cnt; q += NG3) {
+                            const double* rq = Rw + q * rstride;
+                            const double ee = Ew[q];
+                            const double r2 = rq[J + c3];
+#pragma unroll
+                            for (int b1 = 0; b1 < J; ++b1) {
+                                const double k = rq[b1] * r2;
+                                a3[b1] = fma(ee, k, a3[b1]);
+                                a3s[b1] = fma(k, k, a3s[b1]);
+                            }
+                        }
+                    }
+                    __syncwarp();
+                    continue;
+                }
                 for (int q = 0; q < cnt; ++q) {
                     const double* rq = Rw + q * rstride;
                     const double ee = Ew[q];
@@ -137,6 +164,29 @@ __global__ void __launch_bounds__(kApproxWarps * 32, PT_APPROX_MINB) k_approx_se
                     }
                 }
                 __syncwarp();
+            }
+            if constexpr (N == 3) {
+                // add the groups' partials (group 0 collects, groups in order) and store
+#pragma unroll
+                for (int q = 1; q < NG3; ++q) {
+#pragma unroll
+                    for (int b1 = 0; b1 < J; ++b1) {
+                        const double o = __shfl_down_sync(0xffffffffu, a3[b1], q * J);
+                        const double o2 = __shfl_down_sync(0xffffffffu, a3s[b1], q * J);
+                        if (g3 == 0) {
+                            a3[b1] += o;
+                            a3s[b1] += o2;
+                        }
+                    }
+                }
+                if (g3 == 0) {
+#pragma unroll
+                    for (int b1 = 0; b1 < J; ++b1) {
+                        w[b1 * J + c3] = a3[b1];
+                        w2[b1 * J + c3] = a3s[b1];
+                    }
+                }
+                continue;
             }
 #pragma unroll
             for (int m = 0; m < MB; ++m) {
