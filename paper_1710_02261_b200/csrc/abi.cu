@@ -114,6 +114,7 @@ struct Ctx {
     int l0_group = 1;                        // option "l0_group" (tensor-core kernel, F32-B)
     int64_t l2_persist_mb = -1;              // option "l2_persist_mb": L2 set-aside for evict_last lines (-1 = max)
     int pack_gathers = 0;                    // option "pack_gathers": J = 10 tensor-core gathers from packed tables
+    int tc_table = 1;                        // option "tc_table": order-4 one-small-mode tables on the tensor cores
     float* pk_head[2] = {nullptr, nullptr};  // tensor-core kernel, J = 10: packed gather tables
     float* pk_tail[2] = {nullptr, nullptr};
     int use_smp = 1;                         // option "smp"
@@ -302,10 +303,18 @@ int launch_update_kernel(int n, bool literal) {
             p.gp_elems = (int)sp.elems;
             p.aux_stride = (int64_t)g.J * GBk;
         };
+        const UpdateKernel* ktc = g.mi[n].aux_groups ? find_update_kernel_tc(1, g.J) : nullptr;
         if (g.prec == PTUCKER_F64) {
             UpdateParams<double> p = make_params<double>(n, false);
             fill(p);
             ok = launch_table_update(&p, 8, g.J, g.nsm, S());
+        } else if (ktc) {  // tensor-core kernel with the group's table block as the core
+            UpdateParams<float> p = make_params<float>(n, false);
+            fill(p);
+            p.gmain[0] = p.gmain[1] = p.gtail[0] = p.gtail[1] = nullptr;
+            CK(cudaMemsetAsync(g.d_work, 0, sizeof(unsigned int), S()));
+            ktc->launch(&p, false, g.nsm, S());
+            ok = true;
         } else {
             UpdateParams<float> p = make_params<float>(n, false);
             fill(p);
@@ -536,6 +545,11 @@ int ptucker_set_option(const char* key, int64_t value) {
         if (value < 1 || value > (1 << 20)) return fail(PTUCKER_EINVAL, "seg_len out of range");
         if (g.inited) return fail(PTUCKER_ESTATE, "seg_len must be set before ptucker_init");
         g.seg_len = (int)value;
+        return PTUCKER_OK;
+    }
+    if (k == "tc_table") {
+        if (g.inited) return fail(PTUCKER_ESTATE, "tc_table must be set before ptucker_init");
+        g.tc_table = value != 0;
         return PTUCKER_OK;
     }
     if (k == "pack_gathers") {
@@ -801,8 +815,11 @@ int ptucker_init(const int32_t* coords, const void* vals, int32_t vals_dtype, in
         partition_rows(m.h_row_ptr.data(), dims[n], g.world, m.bounds.data());
         const int smode = g.smp[n].kind == 1 ? g.smp[n].s1 : -1;  // group each row by the small mode
         m.Is = smode >= 0 ? dims[smode] : 1;
+        // kind-1 modes on the tensor cores: lanes in (i_s, length) order, one i_s per group
+        const bool aux_groups = smode >= 0 && g.tc_table && g.use_tc && vals_dtype == PTUCKER_F32 &&
+                                find_update_kernel_tc(1, J) != nullptr;
         CK(build_mode_sell(d_coords, d_vals, esz, nnz, order, n, J, g.seg_len, m.bounds[g.rank],
-                           m.bounds[g.rank + 1], smode, m, g.arena, g.scratch, S()));
+                           m.bounds[g.rank + 1], smode, m, g.arena, g.scratch, S(), aux_groups));
         pc.lap("SELL segments + scatter", S());
     }
     CK(A.alloc((void**)&g.lit_part, std::max<int64_t>(g.mi[0].nslices * 32, 1) * sizeof(double)));

@@ -16,6 +16,7 @@
 #include <cub/cub.cuh>
 
 #include <cstdint>
+#include <vector>
 
 #include "index.cuh"
 #include "internal.cuh"
@@ -250,9 +251,61 @@ static cudaError_t exclusive_sum(const T* in, T* out, int64_t n, DeviceArena& sc
     return cudaSuccess;
 }
 
+// aux-major segment order (tensor-core table kernel): key = (i_s, descending length), the
+// empty segments of empty rows last; per-class counts for the padded lane layout.
+__global__ void k_aux_key(int64_t nS, const int32_t* seg_aux, const int32_t* seg_len, int64_t Is, int S,
+                          uint32_t* seg_key) {
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < nS; t += (int64_t)gridDim.x * blockDim.x) {
+        const int l = seg_len[t];
+        seg_key[t] = l == 0 ? (uint32_t)(Is * (S + 1)) : (uint32_t)(seg_aux[t] * (S + 1) + (S - l));
+    }
+}
+__global__ void k_class_count(int64_t nS, const int32_t* seg_aux, const int32_t* seg_len, int64_t Is,
+                              unsigned long long* cnt) {
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < nS; t += (int64_t)gridDim.x * blockDim.x)
+        atomicAdd(cnt + (seg_len[t] == 0 ? Is : seg_aux[t]), 1ull);
+}
+// Lanes of the padded aux-major layout: class a occupies lanes [ps[a], ps[a+1]) (its count
+// rounded up to 128 = one group of 4 slices, so no group spans two classes; the empty class
+// last, unpadded); real lanes take sorted positions cs[a] + r, the rest are pad lanes.
+__global__ void k_slices_aux(const int32_t* order, int64_t nslices, int nclass, const int64_t* ps, const int64_t* cs,
+                             const int64_t* cnt, const int32_t* seg_row, const int64_t* seg_src, const int32_t* seg_aux,
+                             const int32_t* seg_len, const int64_t* seg_pidx, const int32_t* seg_pstride,
+                             int32_t* slice_len, int64_t* slice_slots, int32_t* lane_row, int32_t* lane_len,
+                             int64_t* lane_pidx, int32_t* lane_pstride, int64_t* lane_src, int32_t* lane_aux) {
+    const int64_t total = nslices * 32;
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
+        int a = 0;
+        while (a + 1 < nclass && t >= ps[a + 1]) ++a;
+        const int64_t r = t - ps[a];
+        int32_t l = 0;
+        if (r < cnt[a] && t < ps[nclass]) {
+            const int32_t sid = order[cs[a] + r];
+            l = seg_len[sid];
+            lane_row[t] = seg_row[sid];
+            lane_len[t] = l;
+            lane_pidx[t] = seg_pidx[sid];
+            lane_pstride[t] = seg_pstride[sid];
+            lane_src[t] = seg_src[sid];
+            lane_aux[t] = seg_aux[sid];
+        } else {
+            lane_row[t] = -1;
+            lane_len[t] = 0;
+            lane_pidx[t] = -1;
+            lane_pstride[t] = 0;
+            lane_src[t] = 0;
+            lane_aux[t] = a < nclass - 1 ? a : 0;  // the class's table block (pad lanes of a group)
+        }
+        if ((t & 31) == 0) {
+            slice_len[t >> 5] = l;
+            slice_slots[t >> 5] = (int64_t)l * 32;
+        }
+    }
+}
+
 cudaError_t build_mode_sell(const int32_t* d_coords, const void* d_vals, int elem_bytes, int64_t nnz, int N, int n,
                             int J, int S, int64_t r0, int64_t r1, int smode, ModeIndex& mi, DeviceArena& arena,
-                            DeviceArena& scratch, cudaStream_t st) {
+                            DeviceArena& scratch, cudaStream_t st, bool aux_groups) {
     const int PW = rec_width(J);
     const int64_t nrows = r1 - r0;
     mi.r0 = r0;
@@ -337,11 +390,14 @@ cudaError_t build_mode_sell(const int32_t* d_coords, const void* d_vals, int ele
         k_group_fill<<<grid_for(ngroups), 256, 0, st>>>(group_ptr, g0, ngroups, Is, S, PW, seg_start_g, nseg_r, hbase,
                                                         seg_row, seg_src, seg_aux, seg_len, seg_key, seg_pidx,
                                                         seg_pstride);
-    // ---- 4. stable sort of segments by length (descending) ----
+    // ---- 4. stable sort of segments by length (descending); aux-major when requested ----
+    aux_groups = aux_groups && smode >= 0;
+    if (aux_groups && nS > 0) k_aux_key<<<grid_for(nS), 256, 0, st>>>(nS, seg_aux, seg_len, Is, S, seg_key);
     {
         if (nS > 0) k_iota<<<grid_for(nS), 256, 0, st>>>(seg_iota, nS);
         int bits = 1;
-        while ((int64_t(1) << bits) <= S) ++bits;
+        const int64_t kmax = aux_groups ? Is * (S + 1) : S;
+        while ((int64_t(1) << bits) <= kmax) ++bits;
         size_t tb = 0;
         IB_CHECK(cub::DeviceRadixSort::SortPairs(nullptr, tb, seg_key, seg_key_sorted, seg_iota, order, (int)nS, 0,
                                                  bits, st));
@@ -350,7 +406,30 @@ cudaError_t build_mode_sell(const int32_t* d_coords, const void* d_vals, int ele
         IB_CHECK(cub::DeviceRadixSort::SortPairs(tmp, tb, seg_key, seg_key_sorted, seg_iota, order, (int)nS, 0, bits,
                                                  st));
     }
-    mi.nslices = (nS + 31) / 32;
+    // padded class layout (aux_groups): counts -> host -> lane offsets
+    const int nclass = (int)Is + 1;
+    std::vector<int64_t> h_cnt(nclass, 0), h_cs(nclass + 1, 0), h_ps(nclass + 1, 0);
+    int64_t *d_ps = nullptr, *d_cs = nullptr, *d_cnt = nullptr;
+    if (aux_groups) {
+        unsigned long long* cnt_u = nullptr;
+        IB_CHECK(dalloc(&cnt_u, nclass, scratch));
+        IB_CHECK(cudaMemsetAsync(cnt_u, 0, sizeof(unsigned long long) * nclass, st));
+        if (nS > 0) k_class_count<<<grid_for(nS), 256, 0, st>>>(nS, seg_aux, seg_len, Is, cnt_u);
+        IB_CHECK(cudaMemcpyAsync(h_cnt.data(), cnt_u, sizeof(int64_t) * nclass, cudaMemcpyDeviceToHost, st));
+        IB_CHECK(cudaStreamSynchronize(st));
+        for (int a = 0; a < nclass; ++a) {
+            h_cs[a + 1] = h_cs[a] + h_cnt[a];
+            h_ps[a + 1] = h_ps[a] + (a < nclass - 1 ? (h_cnt[a] + 127) / 128 * 128 : h_cnt[a]);
+        }
+        IB_CHECK(dalloc(&d_ps, nclass + 1, scratch));
+        IB_CHECK(dalloc(&d_cs, nclass + 1, scratch));
+        IB_CHECK(dalloc(&d_cnt, nclass, scratch));
+        IB_CHECK(cudaMemcpyAsync(d_ps, h_ps.data(), sizeof(int64_t) * (nclass + 1), cudaMemcpyHostToDevice, st));
+        IB_CHECK(cudaMemcpyAsync(d_cs, h_cs.data(), sizeof(int64_t) * (nclass + 1), cudaMemcpyHostToDevice, st));
+        IB_CHECK(cudaMemcpyAsync(d_cnt, h_cnt.data(), sizeof(int64_t) * nclass, cudaMemcpyHostToDevice, st));
+    }
+    mi.nslices = aux_groups ? (h_ps[nclass] + 31) / 32 : (nS + 31) / 32;
+    mi.aux_groups = aux_groups;
     const int64_t nlanes = mi.nslices * 32;
     int64_t *slice_slots = nullptr, *lane_src = nullptr;
     IB_CHECK(dalloc(&slice_slots, mi.nslices + 1, scratch));
@@ -363,7 +442,12 @@ cudaError_t build_mode_sell(const int32_t* d_coords, const void* d_vals, int ele
     IB_CHECK(dalloc(&mi.lane_pstride, nlanes, arena));
     IB_CHECK(dalloc(&mi.lane_aux, nlanes, arena));
     IB_CHECK(cudaMemsetAsync(slice_slots, 0, sizeof(int64_t) * (mi.nslices + 1), st));
-    if (nlanes > 0)
+    if (nlanes > 0 && aux_groups)
+        k_slices_aux<<<grid_for(nlanes), 256, 0, st>>>(order, mi.nslices, nclass, d_ps, d_cs, d_cnt, seg_row, seg_src,
+                                                       seg_aux, seg_len, seg_pidx, seg_pstride, mi.slice_len,
+                                                       slice_slots, mi.lane_row, mi.lane_len, mi.lane_pidx,
+                                                       mi.lane_pstride, lane_src, mi.lane_aux);
+    else if (nlanes > 0)
         k_slices<<<grid_for(nlanes), 256, 0, st>>>(order, nS, mi.nslices, seg_row, seg_src, seg_aux, seg_len, seg_pidx,
                                                    seg_pstride, mi.slice_len, slice_slots, mi.lane_row, mi.lane_len,
                                                    mi.lane_pidx, mi.lane_pstride, lane_src, mi.lane_aux);

@@ -42,6 +42,7 @@ struct ModeIndex {
     int32_t* lane_pstride = nullptr;
     int32_t* lane_aux = nullptr;     // small-mode index i_s of the segment (SMP table block), else 0
     int64_t Is = 1;                  // rows of the grouping small mode (1 = none)
+    bool aux_groups = false;         // lanes in (i_s, length) order, each class padded to 128 lanes
     int32_t* sc[kMaxN] = {nullptr};  // coordinates of the other modes, SELL order
     void* sv = nullptr;              // values, SELL order
     // heavy rows (more than one segment)
@@ -58,6 +59,6 @@ cudaError_t build_mode_csr(const int32_t* d_coords, int64_t nnz, int N, int n, i
                            DeviceArena& arena, DeviceArena& scratch, cudaStream_t st);
 cudaError_t build_mode_sell(const int32_t* d_coords, const void* d_vals, int elem_bytes, int64_t nnz, int N, int n,
                             int J, int S, int64_t r0, int64_t r1, int smode, ModeIndex& mi, DeviceArena& arena,
-                            DeviceArena& scratch, cudaStream_t st);
+                            DeviceArena& scratch, cudaStream_t st, bool aux_groups = false);
 
 }  // namespace pt

@@ -254,7 +254,7 @@ struct Shape {
     static constexpr int OFF_BAR = (OFF_STASH + 8 * kStash * STSLOT + 7) / 8 * 8;
     // raw_full[kRing], raw_empty[kRing], acc_full[kNT], acc_empty[kNT], a_full[kNA], d_full[4][kD], d_empty[4][kD],
     // a_empty[kNA]
-    static constexpr int NBAR = 2 * kRing + 2 * kNT + 2 * kNA + 8 * kD;
+    static constexpr int NBAR = 2 * kRing + 2 * kNT + 2 * kNA + 8 * kD + 1;  // + b_free (table mode)
     static constexpr int SMEM = OFF_BAR + NBAR * 8;
 };
 
@@ -309,6 +309,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_update_tc(const UpdateParams<fl
     auto d_full = [&](int w, int s) { return bar0 + 8u * (2 * kRing + 2 * kNT + kNA + w * kD + s); };
     auto d_empty = [&](int w, int s) { return bar0 + 8u * (2 * kRing + 2 * kNT + kNA + 4 * kD + w * kD + s); };
     auto a_empty = [&](int a) { return bar0 + 8u * (2 * kRing + 2 * kNT + kNA + 8 * kD + a); };
+    const uint32_t b_free = bar0 + 8u * (2 * kRing + 2 * kNT + 2 * kNA + 8 * kD);  // all MMAs so far done
     // row ring slot s: chunk q of row k (0: a0, 1: a1) of segment u; x of segment u
     auto rowc = [&](int s, int k, int q, int u) -> uint4* {
         return reinterpret_cast<uint4*>(sm + SH::OFF_ROW + s * SH::RSLOT) + ((k * NQ + q) * kE + u);
@@ -378,6 +379,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_update_tc(const UpdateParams<fl
             for (int a = 0; a < kNA; ++a) {
                 mbar_init(a_full(a), 4);   // the 4 level-0 warps of the tile wrote their A rows
                 mbar_init(a_empty(a), 1);  // tcgen05.commit: the MMAs reading A buffer a completed
+                if (a == 0) mbar_init(b_free, 1);  // table mode: tcgen05.commit before a core-block switch
             }
             for (int w = 0; w < 4; ++w)
                 for (int s = 0; s < kD; ++s) {
@@ -508,8 +510,25 @@ __global__ void __launch_bounds__(kThreads, 1) k_update_tc(const UpdateParams<fl
                 if (tl) trl[(k - 64) * 8 + 4] = clock64();
             }
             cp_async_wait<0>();
-        } else if (warp == 15 && lane == 0) {
-            // ====================================================== MMA issue
+        } else if (warp == 15) {
+            // ====================================================== MMA issue (lane 0)
+            // Table mode (order-4 small-mode tables, p.aux_stride > 0): the core block B is
+            // T[i_s] of the group's class (every group has one i_s, index aux_groups); at a
+            // class change the warp waits for all issued MMAs (b_free), rewrites B hi/lo and
+            // makes it visible to the tensor core before the group's first MMA.
+            const bool tbl = p.aux_stride > 0;
+            Sched gs = s0;
+            int g_left = 0, cur_aux = 0;
+            uint32_t bpar = 0;
+            auto next_group = [&]() {  // first group (from gs on) with tiles; its tile count
+                while (gs.valid()) {
+                    const int it = __ldg(p.slice_len + gs.group() * 4);
+                    if (it > 0) return it;
+                    ++gs.r;
+                }
+                return 0;
+            };
+            if (tbl) g_left = next_group();
             const uint32_t idesc =
                 (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(NP >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
             // B descriptors (K-major, SWIZZLE_NONE; LBO: next 16-byte K chunk = next core
@@ -528,6 +547,35 @@ __global__ void __launch_bounds__(kThreads, 1) k_update_tc(const UpdateParams<fl
 #endif
             for (uint32_t k = 0; k < total; ++k) {
                 const int a = (int)(k % kNA), b = (int)(k % kNT);
+                if (tbl) {
+                    if (g_left == 0) {
+                        ++gs.r;
+                        g_left = next_group();
+                    }
+                    const int aux = __ldg(p.lane_aux + (int64_t)gs.group() * 128);
+                    if (aux != cur_aux) {
+                        if (lane == 0)
+                            asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                                             b_free)
+                                         : "memory");
+                        mbar_wait(b_free, bpar);
+                        bpar ^= 1u;
+                        const float* T = p.Gp + (int64_t)aux * p.aux_stride;
+                        for (int i = lane; i < NP * KP; i += kWarp) {
+                            const int c = i / KP, k1 = i % KP;
+                            float v = 0.f;
+                            if (c < J * J && k1 < J) v = T[(c / J) * GB + k1 * J + (c % J)];
+                            const float hv = tf32_rna(v);
+                            sBhi[kmaj<KP>(c, k1)] = hv;
+                            sBlo[kmaj<KP>(c, k1)] = tf32_rna(v - hv);
+                        }
+                        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                        __syncwarp();
+                        cur_aux = aux;
+                    }
+                    --g_left;
+                }
+                if (lane != 0) continue;
                 const bool tr = trm && k >= 64 && k < 128;
                 if (tr) trm[(k - 64) * 8 + 0] = clock64();
                 mbar_wait(a_full(a), (k / kNA) & 1);  // A rows of tile k written
