@@ -518,7 +518,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_update_tc(const UpdateParams<fl
             // makes it visible to the tensor core before the group's first MMA.
             const bool tbl = p.aux_stride > 0;
             Sched gs = s0;
-            int g_left = 0, cur_aux = 0;
+            int g_left = 0, cur_aux = 0, g_aux = 0;
             uint32_t bpar = 0;
             auto next_group = [&]() {  // first group (from gs on) with tiles; its tile count
                 while (gs.valid()) {
@@ -528,7 +528,10 @@ __global__ void __launch_bounds__(kThreads, 1) k_update_tc(const UpdateParams<fl
                 }
                 return 0;
             };
-            if (tbl) g_left = next_group();
+            if (tbl) {
+                g_left = next_group();
+                if (gs.valid()) g_aux = __ldg(p.lane_aux + (int64_t)gs.group() * 128);
+            }
             const uint32_t idesc =
                 (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(NP >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
             // B descriptors (K-major, SWIZZLE_NONE; LBO: next 16-byte K chunk = next core
@@ -545,14 +548,17 @@ __global__ void __launch_bounds__(kThreads, 1) k_update_tc(const UpdateParams<fl
 #else
             constexpr long long* trm = nullptr;
 #endif
-            for (uint32_t k = 0; k < total; ++k) {
+            // table mode: the whole warp runs the loop in lockstep (lane 0 issues); otherwise
+            // lane 0 alone (a diverged remainder of the warp must not spin beside it)
+            for (uint32_t k = 0; (tbl || lane == 0) && k < total; ++k) {
                 const int a = (int)(k % kNA), b = (int)(k % kNT);
                 if (tbl) {
-                    if (g_left == 0) {
+                    if (g_left == 0) {  // next group: its class, loaded once
                         ++gs.r;
                         g_left = next_group();
+                        g_aux = __ldg(p.lane_aux + (int64_t)gs.group() * 128);
                     }
-                    const int aux = __ldg(p.lane_aux + (int64_t)gs.group() * 128);
+                    const int aux = g_aux;
                     if (aux != cur_aux) {
                         if (lane == 0)
                             asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
@@ -575,14 +581,14 @@ __global__ void __launch_bounds__(kThreads, 1) k_update_tc(const UpdateParams<fl
                     }
                     --g_left;
                 }
-                if (lane != 0) continue;
-                const bool tr = trm && k >= 64 && k < 128;
+                const bool tr = trm && lane == 0 && k >= 64 && k < 128;
                 if (tr) trm[(k - 64) * 8 + 0] = clock64();
                 mbar_wait(a_full(a), (k / kNA) & 1);  // A rows of tile k written
                 if (tr) trm[(k - 64) * 8 + 1] = clock64();
                 if (k >= (uint32_t)kNT) mbar_wait(acc_empty(b), ((k / kNT) + 1) & 1);  // accumulator b read (tile k-kNT)
                 if (tr) trm[(k - 64) * 8 + 2] = clock64();
                 asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+                if (lane == 0) {
                 // 3xTF32: lo*hi, hi*lo, hi*hi (small terms first)
                 const uint32_t d = tmem + b * NP;
                 const uint32_t ahi = tmem + SH::ACOL + a * 2 * KP, alo = ahi + KP;
@@ -600,6 +606,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_update_tc(const UpdateParams<fl
                 asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
                                  a_empty(a))
                              : "memory");
+                }
                 if (tr) {
                     trm[(k - 64) * 8 + 3] = clock64();
                     if (p.trace[8 * 512 - 1] == 1) {  // latency probe: wait for this tile's MMAs
@@ -607,6 +614,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_update_tc(const UpdateParams<fl
                         trm[(k - 64) * 8 + 4] = clock64();
                     }
                 }
+                if (tbl) __syncwarp();
             }
         }
     } else if (warp < 8) {

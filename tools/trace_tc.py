@@ -17,9 +17,13 @@ from gen import synth
 from paper_1710_02261_b200 import ptucker as pt
 
 torch.cuda.set_device(0)
-cfg = synth.small("c5", float(sys.argv[1]) if len(sys.argv) > 1 else 0.1)
+import os
+_name = os.environ.get("PT_TRACE_CFG", "c5")
+_scale = float(sys.argv[1]) if len(sys.argv) > 1 else 0.1
+cfg = synth.small(_name, _scale) if _scale < 1 else synth.config(_name)
 coords, vals = synth.generate(cfg)
-pt.ptucker_init(coords, vals, cfg.dims, [10] * 3, cfg.lam, 0)
+pt.ptucker_init(coords, vals, cfg.dims, [cfg.J] * len(cfg.dims), cfg.lam, 0)
+_mode = int(os.environ.get("PT_TRACE_MODE", "1"))
 if len(sys.argv) > 2:
     pt.ptucker_set_option("l0_group", int(sys.argv[2]))
 import os
@@ -27,7 +31,7 @@ if os.environ.get("PT_TRACE_POLICY"):
     pt.ptucker_set_option("policy", int(os.environ["PT_TRACE_POLICY"]))
 pt.ptucker_update_mode(0)
 pt.ptucker_set_option("trace", 1)
-pt.ptucker_update_mode(1)
+pt.ptucker_update_mode(_mode)
 pt.ptucker_synchronize()
 full = pt.ptucker_debug_trace(8 * 512)
 m = full[4 * 512:4 * 512 + 512].reshape(64, 8)
