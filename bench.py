@@ -60,7 +60,8 @@ def roofline(N, J, policy, info, l0_group, nsm, clk_mhz, entries, launch_s, dtyp
     Modes that run the small-mode precontraction (SMP, order 4) are counted
     with the work that kernel performs (SURVEY §8(d) rule 2): kind 2 (two small other modes)
     J^2 fp64 + the normal equations per entry, kind 1 (one small other mode) J^3 fp32 +
-    J^2 fp64 + the normal equations; the per-update table precompute is < 0.1% and left out.
+    J^2 fp64 + the normal equations (the J^3 stage on the tensor cores when the mode runs the
+    tensor-core kernel in table mode); the per-update table precompute is < 0.1% and left out.
     With per-mode launch times `mode_s`, T_roof and T_meas are summed over the modes
     (SURVEY §8(d) rule 1) and frac = sum T_roof / sum T_meas."""
     mp = measured_peaks()
@@ -108,11 +109,14 @@ def roofline(N, J, policy, info, l0_group, nsm, clk_mhz, entries, launch_s, dtyp
         per_mode, roof_sum, pipe_sum = [], 0.0, {}
         for n, kind in enumerate(kinds):
             a32, a64 = {0: (w32, w64), 1: (J ** 3, J * J + bc), 2: (0, J * J + bc)}[kind]
-            tn = pipe_times(a32, a64, 0)
+            atc = 0
+            if kind == 1 and info["modes"][n].get("tc_table"):  # J^3 stage on the tensor cores
+                a32, atc = 0, J ** 3
+            tn = pipe_times(a32, a64, atc)
             pn = max(tn, key=tn.get)
             roof_sum += tn[pn]
             pipe_sum[pn] = pipe_sum.get(pn, 0.0) + tn[pn]
-            per_mode.append({"mode": n, "smp": kind, "fp32_fma": a32, "fp64_fma": a64, "pipe": pn,
+            per_mode.append({"mode": n, "smp": kind, "fp32_fma": a32, "fp64_fma": a64, "tc_mac": atc, "pipe": pn,
                              "roof_ms": tn[pn] * 1e3, "measured_ms": mode_s[n] * 1e3})
         frac_t = roof_sum / sum(mode_s)
         pipe = max(pipe_sum, key=pipe_sum.get)

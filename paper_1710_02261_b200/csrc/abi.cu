@@ -1309,9 +1309,10 @@ int ptucker_info(char* buf, int32_t len) {
         const ModeIndex& m = g.mi[n];
         snprintf(tmp, sizeof(tmp),
                  "%s{\"I\": %lld, \"rows\": [%lld, %lld], \"segments\": %lld, \"slices\": %lld, \"slots\": %lld, "
-                 "\"heavy_rows\": %lld, \"smp\": %d}",
+                 "\"heavy_rows\": %lld, \"smp\": %d, \"tc_table\": %s}",
                  n ? ", " : "", (long long)m.I, (long long)m.r0, (long long)m.r1, (long long)m.nsegments,
-                 (long long)m.nslices, (long long)m.nslots, (long long)m.nheavy, g.use_smp ? g.smp[n].kind : 0);
+                 (long long)m.nslices, (long long)m.nslots, (long long)m.nheavy, g.use_smp ? g.smp[n].kind : 0,
+                 m.aux_groups ? "true" : "false");
         s += tmp;
     }
     s += "]}";

@@ -44,3 +44,13 @@ def test_smp_modes_use_the_shipped_work(bench):
     assert r["per_mode"][0]["fp64_fma"] == 100 + 66 and r["per_mode"][2]["fp32_fma"] == 1000
     assert 0 < r["frac"] <= 1.0
     assert abs(r["frac"] - r["roof_ms"] / (sum(mode_s) * 1e3)) < 1e-9
+
+
+def test_smp_table_mode_on_tensor_cores(bench):
+    info = {"tensor_cores": False, "modes": [{"smp": 2}, {"smp": 2}, {"smp": 1, "tc_table": True},
+                                             {"smp": 1, "tc_table": True}]}
+    mode_s = [1.9e-3, 1.7e-3, 2.4e-3, 2.4e-3]
+    r = bench.roofline(4, 10, "F32-C", info, 1, 148, 1965.0, 2e7, sum(mode_s) / 4, "f32", "c3", mode_s)
+    m2 = r["per_mode"][2]
+    assert m2["fp32_fma"] == 0 and m2["tc_mac"] == 1000 and m2["fp64_fma"] == 166 and m2["pipe"] == "fp64"
+    assert 0 < r["frac"] <= 1.0
