@@ -64,7 +64,10 @@ constexpr int kCRing = 8 * kLoaders;                    // coordinate ring slots
 constexpr int kNT = 3;                       // TMEM accumulator buffers
 constexpr int kNA = 4;                       // TMEM A buffers (the level-0 warps write A kNA tiles ahead)
 constexpr int kStash = kNA / 2 + 1;          // a0/x stash slots per level-0 warp (its tiles k, k+2, .., k+kNA)
-constexpr int kD = 4;                        // delta ring slots (level 0 -> normal equations)
+#ifndef PT_KD
+#define PT_KD 4
+#endif
+constexpr int kD = PT_KD;                        // delta ring slots (level 0 -> normal equations)
 constexpr int kRegLaunch = 65536 / kThreads / 8 * 8;  // registers per thread at launch (128)
 #ifndef PT_REG_L0
 #define PT_REG_L0 136
@@ -286,7 +289,10 @@ __device__ __forceinline__ void setmaxnreg_dec() { asm volatile("setmaxnreg.dec.
 // partials summed in fp64: J*ceil(J/g) instead of J^2 fp32->fp64 conversions per
 // entry (F2F runs on the quarter-rate XU pipe; tools/l0_row_errors.py and
 // tools/level0_emulation.py measure the row error of each g).
-template <int J, bool LAST64, int G0>
+// TBL: table mode (order-4 one-small-mode tables, p.aux_stride > 0): the core block B is
+// swapped per i_s class by the MMA warp (a separate instantiation: the runtime check
+// cost the plain kernel ~2%).
+template <int J, bool LAST64, int G0, bool TBL = false>
 __global__ void __launch_bounds__(kThreads, 1) k_update_tc(const UpdateParams<float> p) {
     using SH = Shape<J>;
     constexpr int KP = SH::KP, NP = SH::NP, NQ = SH::NQ, KQ = SH::KQ, NCH = SH::NCH;
@@ -516,7 +522,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_update_tc(const UpdateParams<fl
             // T[i_s] of the group's class (every group has one i_s, index aux_groups); at a
             // class change the warp waits for all issued MMAs (b_free), rewrites B hi/lo and
             // makes it visible to the tensor core before the group's first MMA.
-            const bool tbl = p.aux_stride > 0;
+            constexpr bool tbl = TBL;
             Sched gs = s0;
             int g_left = 0, cur_aux = 0, g_aux = 0;
             uint32_t bpar = 0;
@@ -528,7 +534,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_update_tc(const UpdateParams<fl
                 }
                 return 0;
             };
-            if (tbl) {
+            if constexpr (tbl) {
                 g_left = next_group();
                 if (gs.valid()) g_aux = __ldg(p.lane_aux + (int64_t)gs.group() * 128);
             }
@@ -552,7 +558,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_update_tc(const UpdateParams<fl
             // lane 0 alone (a diverged remainder of the warp must not spin beside it)
             for (uint32_t k = 0; (tbl || lane == 0) && k < total; ++k) {
                 const int a = (int)(k % kNA), b = (int)(k % kNT);
-                if (tbl) {
+                if constexpr (tbl) {
                     if (g_left == 0) {  // next group: its class, loaded once
                         ++gs.r;
                         g_left = next_group();
@@ -614,7 +620,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_update_tc(const UpdateParams<fl
                         trm[(k - 64) * 8 + 4] = clock64();
                     }
                 }
-                if (tbl) __syncwarp();
+                if constexpr (tbl) __syncwarp();
             }
         }
     } else if (warp < 8) {
@@ -894,9 +900,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_update_tc(const UpdateParams<fl
     if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(SH::TCOLS));
 }
 
-template <int J, bool LAST64, int G0>
+template <int J, bool LAST64, int G0, bool TBL = false>
 void launch_tc_g(const UpdateParams<float>& p, int grid, cudaStream_t st) {
-    auto k = k_update_tc<J, LAST64, G0>;
+    auto k = k_update_tc<J, LAST64, G0, TBL>;
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, Shape<J>::SMEM);
     cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
     k<<<grid, kThreads, Shape<J>::SMEM, st>>>(p);
@@ -909,7 +915,8 @@ void launch_tc(const void* params, bool literal, int grid, cudaStream_t st) {
     if constexpr (!LAST64) {
         launch_tc_g<J, false, 1>(p, grid, st);
     } else {
-        if (p.l0_group == 1) launch_tc_g<J, true, 1>(p, grid, st);
+        if (p.aux_stride > 0) launch_tc_g<J, true, 1, true>(p, grid, st);  // table mode
+        else if (p.l0_group == 1) launch_tc_g<J, true, 1>(p, grid, st);
         else if (p.l0_group == 2) launch_tc_g<J, true, 2>(p, grid, st);
         else launch_tc_g<J, true, 5>(p, grid, st);
     }
