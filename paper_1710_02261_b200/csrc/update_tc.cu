@@ -243,7 +243,8 @@ struct Shape {
     static constexpr int B_BYTES = NP * KP * 4;             // one of B_hi / B_lo
     static constexpr int RSLOT = 2 * NQ * kE * 16 + kE * 4; // row ring slot: rows a0, a1 (chunk-major), x
     static constexpr int CSLOT = 3 * kE * 4;                // coordinate ring slot: c0, c1, x
-    static constexpr int DSLOT = J * kE * 8 + kE * 4;       // delta ring slot: delta[j][u] (fp64), x[u]
+    static constexpr int JD = (J + 1) / 2 * 2;              // delta doubles per lane (even: 16-byte pairs)
+    static constexpr int DSLOT = JD * kE * 8 + kE * 4;      // delta ring slot: delta[u][j] (fp64), x[u]
     static constexpr int OFF_BHI = 0;
     static constexpr int OFF_BLO = OFF_BHI + B_BYTES;
     static constexpr int OFF_MISC = OFF_BLO + B_BYTES;      // tmem base, tiles
@@ -328,11 +329,14 @@ __global__ void __launch_bounds__(kThreads, 1) k_update_tc(const UpdateParams<fl
         return reinterpret_cast<uint32_t*>(sm + SH::OFF_CRD + s * SH::CSLOT) + a * kE + u;
     };
     // delta ring slot s: delta[j] of segment u (fp64), x of segment u
-    auto dslot = [&](int s, int j, int u) -> double* {
-        return reinterpret_cast<double*>(sm + SH::OFF_DEL + s * SH::DSLOT) + j * kE + u;
+    // lane u's delta contiguous (JD doubles): 16-byte stores/loads; the lane stride JD*8
+    // bytes (an odd multiple of 16 for J = 10) keeps a quarter-warp's 16-byte accesses
+    // on distinct banks
+    auto dslot2 = [&](int s, int q, int u) -> double2* {
+        return reinterpret_cast<double2*>(sm + SH::OFF_DEL + s * SH::DSLOT) + u * (SH::JD / 2) + q;
     };
     auto dslot_x = [&](int s, int u) -> float* {
-        return reinterpret_cast<float*>(sm + SH::OFF_DEL + s * SH::DSLOT + J * kE * 8) + u;
+        return reinterpret_cast<float*>(sm + SH::OFF_DEL + s * SH::DSLOT + SH::JD * kE * 8) + u;
     };
     const int ngroups = (int)((p.nslices + 3) / 4);  // nslices * 32 < 2^31 (nnz <= INT32_MAX)
     const Sched s0{ngroups, 0, (int)gridDim.x, (int)blockIdx.x};
@@ -573,6 +577,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_update_tc(const UpdateParams<fl
                         mbar_wait(b_free, bpar);
                         bpar ^= 1u;
                         const float* T = p.Gp + (int64_t)aux * p.aux_stride;
+#pragma unroll 8
                         for (int i = lane; i < NP * KP; i += kWarp) {
                             const int c = i / KP, k1 = i % KP;
                             float v = 0.f;
@@ -762,7 +767,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_update_tc(const UpdateParams<fl
             const int ds = (int)(k % kD);
             if (k >= (uint32_t)kD) mbar_wait(d_empty(w4, ds), ((k / kD) + 1) & 1);
 #pragma unroll
-            for (int j = 0; j < J; ++j) *dslot(ds, j, te) = double(d[j]);
+            for (int q = 0; q < SH::JD / 2; ++q)
+                *dslot2(ds, q, te) = make_double2(double(d[2 * q]), 2 * q + 1 < J ? double(d[2 * q + 1]) : 0.0);
             *dslot_x(ds, te) = x;
             mbar_arrive(d_full(w4, ds));
             mark(k, 5);
@@ -856,7 +862,11 @@ __global__ void __launch_bounds__(kThreads, 1) k_update_tc(const UpdateParams<fl
                 markn(k, 2);
                 double dd[J];
 #pragma unroll
-                for (int j = 0; j < J; ++j) dd[j] = *dslot(ds, j, te);
+                for (int q = 0; q < SH::JD / 2; ++q) {
+                    const double2 v = *dslot2(ds, q, te);
+                    dd[2 * q] = v.x;
+                    if (2 * q + 1 < J) dd[2 * q + 1] = v.y;
+                }
                 const float x = *dslot_x(ds, te);
                 __syncwarp();
                 if (lane == 0) mbar_arrive(d_empty(w4, ds));
