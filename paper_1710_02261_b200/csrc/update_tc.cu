@@ -870,18 +870,18 @@ __global__ void __launch_bounds__(kThreads, 1) k_update_tc(const UpdateParams<fl
                 const float x = *dslot_x(ds, te);
                 __syncwarp();
                 if (lane == 0) mbar_arrive(d_empty(w4, ds));
-                // an inactive lane (entry beyond its segment) contributes nothing
-                const bool act = e < cur.len;
+                // an inactive lane (entry beyond its segment: only in a group's tail) skips the
+                // update; the branch is warp-uniform almost always, so no per-entry selects
+                if (e < cur.len) {
+                    const double xd = double(x);
 #pragma unroll
-                for (int j = 0; j < J; ++j) dd[j] = act ? dd[j] : 0.0;
-                const double xd = act ? double(x) : 0.0;
+                    for (int i = 0; i < J; ++i) {
+                        c[i] = fma(xd, dd[i], c[i]);
 #pragma unroll
-                for (int i = 0; i < J; ++i) {
-                    c[i] = fma(xd, dd[i], c[i]);
-#pragma unroll
-                    for (int j = i; j < J; ++j) B[up_idx(i, j, J)] = fma(dd[i], dd[j], B[up_idx(i, j, J)]);
+                        for (int j = i; j < J; ++j) B[up_idx(i, j, J)] = fma(dd[i], dd[j], B[up_idx(i, j, J)]);
+                    }
+                    s2 = fma(xd, xd, s2);
                 }
-                s2 = fma(xd, xd, s2);
                 markn(k, 3);
                 if (++e == cur.iters) {
                     finalize(cur);
