@@ -858,7 +858,7 @@ int ptucker_update_mode(int32_t n) {
         rc = timed("finalize", [&]() -> int {
             launch_heavy_finalize(m.nheavy, m.hrow, m.hnseg, m.hpbase, m.partials, m.hrec, g.J, g.lambda, g.A[n], g.esz,
                                   g.lda, g.sse_row[n], g.d_fail, S());
-            g.launches += 2;
+            g.launches += 3;
             CK(cudaGetLastError());
             return PTUCKER_OK;
         }, n);

@@ -127,6 +127,25 @@ __device__ bool chol_solve_rt(const double* rec, int J, double lam, double* a) {
 // segments l, l+32, ... into four interleaved accumulators (more loads in flight),
 // combined in a fixed order, then a fixed xor-butterfly -- the result depends only on
 // the row's own segments (F9).  Stage 2: one thread per row solves in registers.
+// Rows with at most kSmallSeg segments: one thread per (row, component), the segments
+// added in order (many short heavy rows, e.g. a small seg_len); longer rows: a warp each.
+constexpr int kSmallSeg = 64;
+__global__ void __launch_bounds__(256) k_heavy_sum_small(int64_t nheavy, int PW, const int32_t* hnseg,
+                                                         const int64_t* hpbase, const double* partials,
+                                                         double* rec) {
+    for (int64_t w = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; w < nheavy * PW;
+         w += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t h = w / PW;
+        const int nseg = hnseg[h];
+        if (nseg > kSmallSeg) continue;
+        const int p = (int)(w % PW);
+        const double* src = partials + hpbase[h] + (int64_t)p * nseg;
+        double acc = 0.0;
+        for (int s = 0; s < nseg; ++s) acc += src[s];
+        rec[w] = acc;
+    }
+}
+
 __global__ void __launch_bounds__(256) k_heavy_sum(int64_t nheavy, int PW, const int32_t* hnseg,
                                                    const int64_t* hpbase, const double* partials, double* rec) {
     const int lane = threadIdx.x & 31;
@@ -135,6 +154,7 @@ __global__ void __launch_bounds__(256) k_heavy_sum(int64_t nheavy, int PW, const
         const int64_t h = w / PW;
         const int p = (int)(w % PW);
         const int nseg = hnseg[h];
+        if (nseg <= kSmallSeg) continue;
         const double* src = partials + hpbase[h] + (int64_t)p * nseg;
         double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
         int s = lane;
@@ -199,8 +219,10 @@ void launch_heavy_finalize(int64_t nheavy, const int32_t* hrow, const int32_t* h
                            int lda, double* sse_row, int* fail, cudaStream_t st) {
     if (nheavy <= 0) return;
     const int PW = J * (J + 1) / 2 + J + 1;
-    const int64_t nwarps = nheavy * PW;
-    const unsigned g1 = (unsigned)std::min<int64_t>((nwarps + 7) / 8, 148 * 32);
+    const int64_t nitems = nheavy * PW;
+    const unsigned g0 = (unsigned)std::min<int64_t>((nitems + 255) / 256, 148 * 32);
+    k_heavy_sum_small<<<g0, 256, 0, st>>>(nheavy, PW, hnseg, hpbase, partials, rec);
+    const unsigned g1 = (unsigned)std::min<int64_t>((nitems + 7) / 8, 148 * 32);
     k_heavy_sum<<<g1, 256, 0, st>>>(nheavy, PW, hnseg, hpbase, partials, rec);
     const unsigned g2 = (unsigned)std::min<int64_t>((nheavy + 127) / 128, 148 * 16);
 #define PT_HF(JC)                                                                                                  \
