@@ -1048,7 +1048,9 @@ int compute_core_scores(bool with_keys) {
     int64_t K1 = 1;
     for (int n = 1; n < N; ++n) K1 *= J;
     const int64_t gsize = K1 * J;
-    const int nsplit = 256;
+    // segment ranges of the outer reduction: ~256 segments each (enough blocks to fill the
+    // GPU: 3.8 ms at a fixed 256 ranges for c5's 10^6 segments), at most 4096 ranges
+    const int nsplit = (int)std::min<int64_t>(4096, std::max<int64_t>(256, g.mi[0].nslices * 32 / 256));
     const ModeIndex& m = g.mi[0];
     if (!approx_shape_ok(N, J)) {  // generic shapes: U, V by definition over the device COO
         if (!g.coo_c) return fail(PTUCKER_EINVAL, "internal: no device COO for the generic Approx scores");

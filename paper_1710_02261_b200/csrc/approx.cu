@@ -49,7 +49,7 @@ __global__ void __launch_bounds__(kApproxWarps * 32, PT_APPROX_MINB) k_approx_se
     double* H = smem + warp * (k1p + 32 * rstride + 32);
     double* Rw = H + k1p;               // Rw[entry * rstride + (n-1) * J + j]
     double* Ew = Rw + 32 * rstride;     // Ew[entry]
-    (void)Eslot;
+    // Eslot[slot]: e of each entry, computed in the first chunk pass (K1 > 256) and reused
     for (int64_t seg = (int64_t)blockIdx.x * kApproxWarps + warp; seg < nlanes;
          seg += (int64_t)gridDim.x * kApproxWarps) {
         const int row = lane_row[seg];
@@ -115,8 +115,15 @@ __global__ void __launch_bounds__(kApproxWarps * 32, PT_APPROX_MINB) k_approx_se
                         const TS* rowp = A[n] + (int64_t)sc[n - 1][slot] * lda;
                         for (int j = 0; j < J; ++j) r[(n - 1) * J + j] = (double)rowp[j];
                     }
+                    if (b0 > 0) {  // later chunk pass: e from the first
+                        Ew[lane] = Eslot[slot];
+                    } else {
+                    // x_hat as a contraction chain of H with the staged rows (innermost mode first)
                     double xh = 0.0;
-                    if constexpr (N == 3) {  // x_hat = sum_b1 r1[b1] sum_b2 H[b1][b2] r2[b2]
+                    if constexpr (N == 2) {
+#pragma unroll
+                        for (int b1 = 0; b1 < J; ++b1) xh = fma(H[b1], r[b1], xh);
+                    } else if constexpr (N == 3) {  // x_hat = sum_b1 r1[b1] sum_b2 H[b1][b2] r2[b2]
 #pragma unroll
                         for (int b1 = 0; b1 < J; ++b1) {
                             double t = 0.0;
@@ -124,10 +131,41 @@ __global__ void __launch_bounds__(kApproxWarps * 32, PT_APPROX_MINB) k_approx_se
                             for (int b2 = 0; b2 < J; ++b2) t = fma(H[b1 * J + b2], r[J + b2], t);
                             xh = fma(r[b1], t, xh);
                         }
+                    } else if constexpr (N == 4) {
+                        for (int b1 = 0; b1 < J; ++b1) {
+                            double t1 = 0.0;
+#pragma unroll
+                            for (int b2 = 0; b2 < J; ++b2) {
+                                double t2 = 0.0;
+#pragma unroll
+                                for (int b3 = 0; b3 < J; ++b3) t2 = fma(H[(b1 * J + b2) * J + b3], r[2 * J + b3], t2);
+                                t1 = fma(r[J + b2], t2, t1);
+                            }
+                            xh = fma(r[b1], t1, xh);
+                        }
+                    } else if constexpr (N == 5) {
+                        for (int b1 = 0; b1 < J; ++b1) {
+                            double t1 = 0.0;
+                            for (int b2 = 0; b2 < J; ++b2) {
+                                double t2 = 0.0;
+#pragma unroll
+                                for (int b3 = 0; b3 < J; ++b3) {
+                                    double t3 = 0.0;
+#pragma unroll
+                                    for (int b4 = 0; b4 < J; ++b4)
+                                        t3 = fma(H[((b1 * J + b2) * J + b3) * J + b4], r[3 * J + b4], t3);
+                                    t2 = fma(r[2 * J + b3], t3, t2);
+                                }
+                                t1 = fma(r[J + b2], t2, t1);
+                            }
+                            xh = fma(r[b1], t1, xh);
+                        }
                     } else {
                         for (int b = 0; b < K1; ++b) xh = fma(kprod(b, r), H[b], xh);
                     }
                     Ew[lane] = xh - (double)sv[slot];
+                    if (K1 > 256) Eslot[slot] = Ew[lane];
+                    }
                 }
                 __syncwarp();
                 const int cnt = len - e0 < 32 ? len - e0 : 32;
