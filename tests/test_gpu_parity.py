@@ -142,6 +142,29 @@ def test_mode_update_f32(pt, orc, name, scale, seg):
         assert [m["smp"] for m in info["modes"]] == [2, 2, 1, 1]
 
 
+@pytest.mark.parametrize("tc_table", [0, 1])
+def test_mode_update_c3_table_modes(pt, orc, tc_table):
+    """Order-4 modes with one small other mode (c3 modes 2/3, SMP kind 1) on the ALU table
+    kernel (tc_table 0) and on the tensor-core kernel in table mode (tc_table 1, the
+    default: lanes in (i_s, length) order, core block swapped per class)."""
+    cfg = synth.small("c3", 0.005)
+    coords, vals = synth.generate(cfg)
+    t = orc.Tensor(coords, vals, cfg.dims)
+    pt.ptucker_finalize()
+    pt.ptucker_set_option("seg_len", 256)
+    pt.ptucker_set_option("tc_table", tc_table)
+    try:
+        pt.ptucker_init(coords, vals, cfg.dims, [cfg.J] * 4, cfg.lam, 0)
+        info = pt.ptucker_info()
+        assert [m["smp"] for m in info["modes"]] == [2, 2, 1, 1]
+        assert [m["tc_table"] for m in info["modes"]] == [False, False, bool(tc_table), bool(tc_table)]
+        mode_update_parity(pt, orc, t, cfg, 1e-5, sweeps=0, modes=[2, 3])
+        mode_update_parity(pt, orc, t, cfg, 1e-5, sweeps=1, modes=[2, 3])
+    finally:
+        pt.ptucker_finalize()
+        pt.ptucker_set_option("tc_table", 1)
+
+
 @pytest.mark.parametrize("name,scale", [("c2", 0.01), ("c5", 0.0005)])
 def test_mode_update_tc_packed_gathers(pt, orc, name, scale):
     """J = 10 tensor-core updates with the packed 32 + 8-byte gather tables (option
