@@ -46,13 +46,16 @@ __device__ __forceinline__ double f2d_alu(float f) {
     const uint32_t hi = ((uint32_t)((int32_t)u >> 3) & 0x8FFFFFFFu) + 0x38000000u;
     return __hiloint2double((int)hi, (int)(u << 29));
 }
-// TO(x) for the level outputs: half by the ALU (odd j), half by the XU
+// TO(x) for the level outputs.  The ALU kernel is issue-bound at two CTAs per SM (c4:
+// issue active 75%), so the one-instruction XU conversion wins over f2d_alu's four
+// (c4 3.46 -> 2.78 ms per mode); -DPT_F2D_ALU puts half of them on the ALU pipe.
 template <typename TO, typename TI>
 __device__ __forceinline__ TO widen(TI x, int j) {
     if constexpr (std::is_same<TO, double>::value && std::is_same<TI, float>::value) {
-#ifndef PT_NO_F2D_ALU
+#ifdef PT_F2D_ALU
         return (j & 1) ? f2d_alu(x) : double(x);
 #else
+        (void)j;
         return double(x);
 #endif
     } else {
