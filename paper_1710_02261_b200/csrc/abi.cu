@@ -114,6 +114,8 @@ struct Ctx {
     int l0_group = 1;                        // option "l0_group" (tensor-core kernel, F32-B)
     int64_t l2_persist_mb = -1;              // option "l2_persist_mb": L2 set-aside for evict_last lines (-1 = max)
     int pack_gathers = 0;                    // option "pack_gathers": J = 10 tensor-core gathers from packed tables
+    int rows_l1[kMaxN] = {0};                // per updated mode: gather rows through L1 (skewed other modes)
+    int rows_l1_opt = -1;                    // option "rows_l1": -1 = automatic (row skew), 0 / 1 = forced
     int tc_table = 1;                        // option "tc_table": order-4 one-small-mode tables on the tensor cores
     float* pk_head[2] = {nullptr, nullptr};  // tensor-core kernel, J = 10: packed gather tables
     float* pk_tail[2] = {nullptr, nullptr};
@@ -260,6 +262,7 @@ UpdateParams<TS> make_params(int n, bool literal) {
     p.gtail[0] = g.pk_tail[0];
     p.gtail[1] = g.pk_tail[1];
     p.l0_group = g.l0_group;
+    p.rows_l1 = g.rows_l1[n];
     return p;
 }
 
@@ -433,6 +436,7 @@ void free_all() {
     g.smp_T = nullptr;
     g.smp_T32 = nullptr;
     g.pk_head[0] = g.pk_head[1] = g.pk_tail[0] = g.pk_tail[1] = nullptr;
+    for (int n = 0; n < kMaxN; ++n) g.rows_l1[n] = 0;
     g.lit_part = g.red_part = g.red_out = g.qr = g.qd = nullptr;
     g.ax_G64 = g.ax_A0 = g.ax_W = g.ax_W2 = g.ax_E = g.ax_part = g.ax_UV = nullptr;
     g.ax_ptrs = nullptr;
@@ -532,6 +536,22 @@ int apply_l2_persist() {
     return PTUCKER_OK;
 }
 
+// Factor-row gathers of mode n's update through L1 when a gathered (other) mode is
+// skewed: its most frequent row holds >= 1% of the entries (a Zipf head row), so one L2
+// slice would serve a large share of all gathers; uniform modes keep the L2-only path.
+int rows_l1_auto(int n) {
+    if (g.rows_l1_opt >= 0) return g.rows_l1_opt;
+    if (!g.inited && g.mi[0].h_row_ptr.empty()) return 0;
+    for (int m = 0; m < g.N; ++m) {
+        if (m == n) continue;
+        const std::vector<int64_t>& rp = g.mi[m].h_row_ptr;
+        int64_t mx = 0;
+        for (size_t i = 0; i + 1 < rp.size(); ++i) mx = std::max<int64_t>(mx, rp[i + 1] - rp[i]);
+        if (g.nnz > 0 && mx * 100 >= g.nnz) return 1;
+    }
+    return 0;
+}
+
 int ptucker_set_option(const char* key, int64_t value) {
     if (!key) return fail(PTUCKER_EINVAL, "null key");
     const std::string k = key;
@@ -550,6 +570,12 @@ int ptucker_set_option(const char* key, int64_t value) {
     if (k == "tc_table") {
         if (g.inited) return fail(PTUCKER_ESTATE, "tc_table must be set before ptucker_init");
         g.tc_table = value != 0;
+        return PTUCKER_OK;
+    }
+    if (k == "rows_l1") {
+        if (value < -1 || value > 1) return fail(PTUCKER_EINVAL, "rows_l1 must be -1, 0 or 1");
+        g.rows_l1_opt = (int)value;
+        for (int n = 0; n < g.N; ++n) g.rows_l1[n] = rows_l1_auto(n);
         return PTUCKER_OK;
     }
     if (k == "pack_gathers") {
@@ -842,6 +868,7 @@ int ptucker_init(const int32_t* coords, const void* vals, int32_t vals_dtype, in
     }
     rc = apply_l2_persist();
     if (rc) return rc;
+    for (int n = 0; n < order; ++n) g.rows_l1[n] = rows_l1_auto(n);
     g.sse_mode = -1;
     return PTUCKER_OK;
 }

@@ -57,6 +57,7 @@ struct UpdateParams {
     const float* gmain[2];        // tensor-core kernel, J = 10: the two gathered factors with rows split
     const float* gtail[2];        //   into 32-byte heads (floats 0..7) and packed 8-byte tails (8..9)
     int l0_group;                 // tensor-core kernel: level-0 terms summed in fp32 before fp64 (1 or 2)
+    int rows_l1;                  // gather factor rows through L1 (skewed gathered modes: hot rows)
 };
 
 using UpdateLauncher = void (*)(const void* params, bool literal, int grid, cudaStream_t st);

@@ -207,6 +207,14 @@ __device__ __forceinline__ void cp_async16_hint(void* smem, const void* gmem, ui
                  "l"(pol)
                  : "memory");
 }
+// the same through L1 (.ca): a hot factor row (Zipf-skewed modes, p.rows_l1) is served by
+// each SM's L1 instead of hammering the one L2 slice that holds it (c3 table modes 2.36 ->
+// 1.07 ms); with uniform rows (c5) L1 allocation only thrashes (4.1 -> 7.0 ms)
+__device__ __forceinline__ void cp_async16_l1(void* smem, const void* gmem, uint64_t pol) {
+    asm volatile("cp.async.ca.shared.global.L2::cache_hint [%0], [%1], 16, %2;\n" ::"r"(smem_u32(smem)), "l"(gmem),
+                 "l"(pol)
+                 : "memory");
+}
 
 // 16 TMEM columns of this warp's 32 lanes (32x32b shape: thread i <- lane i).
 __device__ __forceinline__ void tmem_ld16(uint32_t addr, uint32_t (&r)[16]) {
@@ -416,6 +424,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_update_tc(const UpdateParams<fl
             // J = 10 with packed gather tables (option "pack_gathers"): 2.5x less DRAM traffic,
             // but the 8-byte tail copies make the update ~10% slower
             const bool kPacked = J == 10 && p.gmain[0] != nullptr;
+            const bool rows_l1 = p.rows_l1 != 0;
             const uint64_t pol_stream = policy_evict_first(), pol_rows = policy_evict_last();
             // coordinate cursor (tile kc): this lane's 4 segments u = lane + 32 i, i = slice of the group
             Sched pc = s0;
@@ -498,6 +507,19 @@ __global__ void __launch_bounds__(kThreads, 1) k_update_tc(const UpdateParams<fl
                         cp_async8_hint(rowc(s, 1, 2, u), p.gtail[1] + c1 * 2, pol_rows);
                         *rowx(s, u) = __uint_as_float(*crd(cs, 2, u));
                     }
+                } else if (rows_l1) {
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                    const int u = lane + kWarp * i;
+                    const char* r0 = reinterpret_cast<const char*>(p.A[0] + (int64_t)(int)*crd(cs, 0, u) * p.lda);
+                    const char* r1 = reinterpret_cast<const char*>(p.A[1] + (int64_t)(int)*crd(cs, 1, u) * p.lda);
+#pragma unroll
+                    for (int q = 0; q < NQ; ++q) {
+                        cp_async16_l1(rowc(s, 0, q, u), r0 + 16 * q, pol_rows);
+                        cp_async16_l1(rowc(s, 1, q, u), r1 + 16 * q, pol_rows);
+                    }
+                    *rowx(s, u) = __uint_as_float(*crd(cs, 2, u));
+                }
                 } else {
 #pragma unroll
                 for (int i = 0; i < 4; ++i) {
