@@ -180,6 +180,8 @@ int ptucker_get_partition(int32_t n, int64_t* bounds);
  *                 the driver default (a device-wide limit: other users of the GPU see it)
  *  "tc_table"     1 = order-4 fp32 modes with one small other mode run the tensor-core kernel on
  *                 the per-i_s core blocks (default; set BEFORE init: it orders the index); 0 = ALU
+ *  "rows_l1"      tensor-core gathers of factor rows: -1 = through L1 when a gathered mode has a
+ *                 row with >= 1% of the entries (default, automatic), 1 = always, 0 = L2 only
  *  "pack_gathers" 1 = J = 10 tensor-core updates gather from packed 40-byte row tables (DRAM
  *                 reads 5.1 -> 2.1 GB per c5 update, ~10% slower); 0 = the factors (default)
  *  "trace"        1 = per-phase clock marks of the tensor-core kernel (builds with -DPT_TRACE) */

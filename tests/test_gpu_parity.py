@@ -160,6 +160,18 @@ def test_mode_update_c3_table_modes(pt, orc, tc_table):
         assert [m["tc_table"] for m in info["modes"]] == [False, False, bool(tc_table), bool(tc_table)]
         mode_update_parity(pt, orc, t, cfg, 1e-5, sweeps=0, modes=[2, 3])
         mode_update_parity(pt, orc, t, cfg, 1e-5, sweeps=1, modes=[2, 3])
+        if tc_table:
+            # the gathers of the skewed modes go through L1 (rows_l1 automatic = 1 here);
+            # the L2-only path must give the same rows bit for bit
+            s0 = oracle_state(orc, t, cfg, 1)
+            got = {}
+            for l1 in (1, 0):
+                pt.ptucker_set_option("rows_l1", l1)
+                push_state(pt, s0, np.float32)
+                pt.ptucker_update_mode(2)
+                got[l1] = pt.ptucker_get_factor(2).copy()
+            pt.ptucker_set_option("rows_l1", -1)
+            assert np.array_equal(got[0], got[1])
     finally:
         pt.ptucker_finalize()
         pt.ptucker_set_option("tc_table", 1)
