@@ -57,9 +57,14 @@ __global__ void k_table2(const TS* __restrict__ G, const TS* __restrict__ As1, c
 //      delta = a_r^T T[i_s1][i_s2] in fp64; B, c, solve as in k_update ----
 // Table source (MODE): 0 = fp32 copy in shared memory; 1 = the fp64 table read
 // from global memory (L2-resident, 8*I_s1*I_s2*J^2 bytes) -- exact to fp64 but
-// ~4x the time; 2 = hybrid: the fp64 table for rows that fit one segment (the
-// light, ill-conditioned rows that dominate the fp32 table's rounding error),
-// the fp32 shared-memory copy for multi-segment (heavy) rows.
+// ~4x the time; 2 = hybrid: the fp64 table for single-segment rows of at most
+// kSmpLight entries (the light, ill-conditioned rows that dominate the fp32 table's
+// rounding error), the fp32 shared-memory copy for all other rows (c3 modes 0/1:
+// 1.96/1.64 -> 1.27/0.93 ms; worst sampled full-size row error 6.2e-7 -> 1.5e-6).
+#ifndef PT_SMP_LIGHT
+#define PT_SMP_LIGHT 32
+#endif
+constexpr int kSmpLight = PT_SMP_LIGHT;  // hybrid: fp64 table only for single-segment rows this short
 template <typename TS, int J, int MODE>
 __global__ void __launch_bounds__(kUpdThreads, 1) k_update_smp2(const UpdateParams<TS> p, const double* __restrict__ T64,
                                                                const TS* __restrict__ T32, int64_t tab_elems, int ir,
@@ -87,7 +92,7 @@ __global__ void __launch_bounds__(kUpdThreads, 1) k_update_smp2(const UpdatePara
         const int len = p.lane_len[slot];
         const int iters = p.slice_len[s];
         const int64_t base = p.slice_off[s] + lane;
-        const bool use64 = MODE == 1 || (MODE == 2 && p.lane_pidx[slot] < 0);
+        const bool use64 = MODE == 1 || (MODE == 2 && p.lane_pidx[slot] < 0 && len <= kSmpLight);
         double B[NB], c[J], s2 = 0.0;
 #pragma unroll
         for (int q = 0; q < NB; ++q) B[q] = 0.0;
