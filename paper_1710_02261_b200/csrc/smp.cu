@@ -98,10 +98,13 @@ __global__ void __launch_bounds__(kUpdThreads, 1) k_update_smp2(const UpdatePara
         for (int q = 0; q < NB; ++q) B[q] = 0.0;
 #pragma unroll
         for (int q = 0; q < J; ++q) c[q] = 0.0;
-        // one entry ahead: coordinates, value and the gathered row a_r
+        // the gathered row a_r one entry ahead, the coordinates and value two ahead (the
+        // row's address is known an iteration before it is requested: no dependent stall)
         int cr = 0, c1 = 0, c2 = 0;
         TS x = TS(0);
         TS ar[J];
+        int mr = 0, m1 = 0, m2 = 0;  // entry e + 1
+        TS mx = TS(0);
         auto load = [&](int e, int& r_, int& a_, int& b_, TS& x_) {
             const int64_t idx = base + (int64_t)e * kWarp;
             r_ = __ldg(p.sc[ir] + idx);
@@ -113,14 +116,13 @@ __global__ void __launch_bounds__(kUpdThreads, 1) k_update_smp2(const UpdatePara
             load(0, cr, c1, c2, x);
             load_row<TS, J>(p.A[ir] + (int64_t)cr * p.lda, ar);
         }
+        if (iters > 1) load(1, mr, m1, m2, mx);
         for (int e = 0; e < iters; ++e) {
-            int nr = 0, n1 = 0, n2 = 0;
-            TS nx = TS(0);
+            int nr = mr, n1 = m1, n2 = m2;
+            TS nx = mx;
             TS nar[J];
-            if (e + 1 < iters) {
-                load(e + 1, nr, n1, n2, nx);
-                load_row<TS, J>(p.A[ir] + (int64_t)nr * p.lda, nar);
-            }
+            if (e + 1 < iters) load_row<TS, J>(p.A[ir] + (int64_t)nr * p.lda, nar);
+            if (e + 2 < iters) load(e + 2, mr, m1, m2, mx);
             const int64_t boff = ((int64_t)c1 * I2 + c2) * BLK;
             double d[J];
 #pragma unroll
@@ -142,17 +144,16 @@ __global__ void __launch_bounds__(kUpdThreads, 1) k_update_smp2(const UpdatePara
                     for (int j = 0; j < J; ++j) d[j] = fma(ak, double(tb[k * J + j]), d[j]);
                 }
             }
-            const bool act = e < len;
-            const double xd = act ? double(x) : 0.0;
+            if (e < len) {  // inactive lanes (beyond their segment) skip the update
+                const double xd = double(x);
 #pragma unroll
-            for (int j = 0; j < J; ++j) d[j] = act ? d[j] : 0.0;
+                for (int i = 0; i < J; ++i) {
+                    c[i] = fma(xd, d[i], c[i]);
 #pragma unroll
-            for (int i = 0; i < J; ++i) {
-                c[i] = fma(xd, d[i], c[i]);
-#pragma unroll
-                for (int j = i; j < J; ++j) B[up_idx(i, j, J)] = fma(d[i], d[j], B[up_idx(i, j, J)]);
+                    for (int j = i; j < J; ++j) B[up_idx(i, j, J)] = fma(d[i], d[j], B[up_idx(i, j, J)]);
+                }
+                s2 = fma(xd, xd, s2);
             }
-            s2 = fma(xd, xd, s2);
             cr = nr; c1 = n1; c2 = n2; x = nx;
 #pragma unroll
             for (int j = 0; j < J; ++j) ar[j] = nar[j];
