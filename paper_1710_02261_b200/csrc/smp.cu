@@ -141,7 +141,14 @@ __global__ void __launch_bounds__(kUpdThreads, 1) k_update_smp2(const UpdatePara
                 for (int k = 0; k < J; ++k) {
                     const double ak = double(ar[k]);
 #pragma unroll
-                    for (int j = 0; j < J; ++j) d[j] = fma(ak, double(tb[k * J + j]), d[j]);
+                    for (int j = 0; j < J; ++j) {
+#ifndef PT_SMP_F2D_XU  // half of the table conversions on the ALU (latency-bound kernel, XU 37%)
+                        if constexpr (std::is_same<TS, float>::value)
+                            d[j] = fma(ak, (j & 1) ? f2d_alu(tb[k * J + j]) : double(tb[k * J + j]), d[j]);
+                        else
+#endif
+                            d[j] = fma(ak, double(tb[k * J + j]), d[j]);
+                    }
                 }
             }
             if (e < len) {  // inactive lanes (beyond their segment) skip the update
