@@ -62,7 +62,8 @@ def test_predict_and_rmse(pt, orc, name, scale):
 
 
 @pytest.mark.parametrize("name,scale,iters,tol,approx", [
-    ("c1", 1.0, 5, 0.0, 0.0), ("c2", 0.01, 10, 1e-3, 0.0), ("c4", 0.002, 8, 1e-4, 0.0), ("c1", 1.0, 5, 0.0, 0.2)])
+    ("c1", 1.0, 5, 0.0, 0.0), ("c2", 0.01, 10, 1e-3, 0.0), ("c4", 0.002, 8, 1e-4, 0.0), ("c1", 1.0, 5, 0.0, 0.2),
+    ("c3", 0.001, 4, 0.0, 0.2)])
 def test_run_matches_oracle(pt, orc, name, scale, iters, tol, approx):
     cfg = synth.small(name, scale) if scale < 1 else synth.config(name)
     coords, vals = synth.generate(cfg)
