@@ -53,7 +53,10 @@ namespace tc {
 
 constexpr int kE = 128;                      // TMEM lanes = segments per group (4 slices)
 constexpr int kThreads = 16 * 32;            // 2 level-0 WGs, normal-equation WG, loader/MMA WG
-constexpr int kRing = 6;                     // row ring slots (tiles between loader and level 0)
+#ifndef PT_RING
+#define PT_RING 6
+#endif
+constexpr int kRing = PT_RING;                     // row ring slots (tiles between loader and level 0)
 constexpr int kCPref = 7;                    // loader: coordinates fetched this many tiles ahead of the gathers
 #ifndef PT_LOADERS
 #define PT_LOADERS 3
