@@ -54,3 +54,23 @@ def test_smp_table_mode_on_tensor_cores(bench):
     m2 = r["per_mode"][2]
     assert m2["fp32_fma"] == 0 and m2["tc_mac"] == 1000 and m2["fp64_fma"] == 166 and m2["pipe"] == "fp64"
     assert 0 < r["frac"] <= 1.0
+
+
+def test_reference_arm_json_line():
+    """`bench.py --impl reference` (the oracle arm, CPU only) prints one JSON line with the
+    contract's keys; its e2e and cpu_baseline describe the same run."""
+    import json
+    import subprocess
+    import sys
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference", "--config", "c1",
+                        "--steps", "1", "--warmup", "1", "--ref-seconds", "1"],
+                       capture_output=True, text=True, timeout=600, cwd=ROOT)
+    assert r.returncode == 0, r.stderr[-2000:]
+    line = [l for l in r.stdout.splitlines() if l.startswith("{")][-1]
+    d = json.loads(line)
+    for k in ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "higher_is_better",
+              "scaling", "vs_baseline", "dtype", "data", "config", "cpu_baseline", "e2e"):
+        assert k in d, k
+    assert d["impl"] == "reference" and d["value"] > 0
+    assert d["cpu_baseline"]["kind"] == "oracle" and d["cpu_baseline"]["value"] == d["value"]
+    assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["e2e"]["value"] == d["value"]
