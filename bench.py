@@ -363,11 +363,33 @@ def run_ours(args, cfg):
     ms = ev0.elapsed_time(ev1)
     launches = pt.ptucker_info()["kernel_launches"] - launches0
     upd_ms, upd_n = pt.ptucker_kernel_stats("update")
+    upd_ms_rank = upd_ms
     fin_ms, _ = pt.ptucker_kernel_stats("finalize")
     apx_ms, apx_n = pt.ptucker_kernel_stats("approx_scores") if args.approx > 0 else (0.0, 0)
     per_mode = {f"update_m{n}": round(pt.ptucker_kernel_stats(f"update_m{n}")[0] / args.steps, 4) for n in range(N)}
     per_mode.update({f"finalize_m{n}": round(pt.ptucker_kernel_stats(f"finalize_m{n}")[0] / args.steps, 4)
                      for n in range(N)})
+    # multi-GPU self-check (F9: factors are bit-identical for any number of GPUs): a hash
+    # of every A^(n) and of G after the timed run, the last error, the communicator size
+    # and each rank's update / all-gather device time -- equal hashes and errors across
+    # N = 1, 2, 4, 8 lines prove the exchange moved every row
+    import hashlib
+    hsh = hashlib.sha256()
+    for n in range(N):
+        hsh.update(np.ascontiguousarray(pt.ptucker_get_factor(n)).tobytes())
+    hsh.update(np.ascontiguousarray(pt.ptucker_get_core()).tobytes())
+    ag_ms, _ = pt.ptucker_kernel_stats("allgather")
+    per_rank = [[upd_ms_rank / args.steps, ag_ms / args.steps]]
+    if world > 1:
+        t = torch.tensor(per_rank[0], dtype=torch.float64, device="cuda")
+        allt = [torch.zeros_like(t) for _ in range(world)]
+        dist.all_gather(allt, t)
+        per_rank = [x.tolist() for x in allt]
+    selfcheck = {"factors_sha256": hsh.hexdigest()[:32], "last_error": errs[-1],
+                 "comm_ranks": pt.ptucker_info()["comm_ranks"], "world": world,
+                 "update_ms_per_step_by_rank": [round(x[0], 4) for x in per_rank],
+                 "allgather_ms_per_step_by_rank": [round(x[1], 4) for x in per_rank]}
+
     pt.ptucker_set_option("time_kernels", 0)
     if world > 1:
         t = torch.tensor([ms, upd_ms], dtype=torch.float64, device="cuda")
@@ -438,7 +460,7 @@ def run_ours(args, cfg):
             "vs_baseline": None, "dtype": "fp32 storage/contraction + fp64 normal equations" if cfg.dtype == "f32"
             else "f64", "data": "synthetic", "config": workload_config(cfg, args) | {"policy": policy},
             "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "clocks": clocks,
-            "init_s": init_s, "errors": errs[-1:], "info": {k: info[k] for k in ("grid_update", "seg_len", "tensor_cores", "modes")},
+            "init_s": init_s, "errors": errs[-1:], "selfcheck": selfcheck, "info": {k: info[k] for k in ("grid_update", "seg_len", "tensor_cores", "modes")},
         }
         print(json.dumps(line), flush=True)
     if world > 1:
@@ -457,7 +479,8 @@ def main():
     ap.add_argument("--seg-len", type=int, default=256)
     ap.add_argument("--tc", type=int, default=1, choices=[0, 1], help="tensor-core inner stage for order-3 fp32")
     ap.add_argument("--l2-persist-mb", type=int, default=None,
-                    help="L2 set-aside for evict_last accesses in MB (-1 = device maximum; default: driver default)")
+                    help="L2 set-aside for evict_last accesses in MB (-1 = device maximum, the library's "
+                         "default; 0 = leave the driver's setting)")
     ap.add_argument("--pack-gathers", type=int, default=0, choices=[0, 1],
                     help="J = 10 tensor-core gathers from packed 40-byte tables (less DRAM traffic, slower)")
     ap.add_argument("--l0-group", type=int, default=1, choices=[1, 2, 5], help="tensor-core level-0 grouping (1 = fp64 per term, g = fp32 partial sums of g terms)")

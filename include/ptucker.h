@@ -52,7 +52,9 @@ const char* ptucker_last_error(void);
 /* ---------------- multi-GPU bootstrap (skip both when world == 1) --------
  * ptucker_get_unique_id: rank 0 creates an NCCL unique id (128 bytes, host);
  * the caller broadcasts the bytes (e.g. torch.distributed) and every rank then
- * calls ptucker_comm_init(rank, world, id) before ptucker_init.  Rows of each
+ * calls ptucker_comm_init(rank, world, id) before ptucker_init (a call while a
+ * context is initialised returns PTUCKER_ESTATE: the row blocks of every mode are
+ * fixed at init for the world size seen then).  Rows of each
  * mode are then split into nnz-balanced contiguous blocks (see
  * ptucker_partition_rows); each rank updates its block and the blocks are
  * all-gathered over NVLink after each mode (the paper aggregates "all updated
@@ -76,11 +78,15 @@ int ptucker_set_stream(void* cuda_stream);
  *  coords    host, nnz x order int32, row-major, 0-based; coords[e*order+n] in [0, dims[n])
  *  vals      host, nnz values; vals_dtype selects the context precision
  *  vals_dtype PTUCKER_F32 | PTUCKER_F64
- *  nnz       >= 1 (duplicate coordinates are accepted: multiset, reading R14)
- *  order     N >= 2
- *  dims      host, N int64, each >= 1
- *  core_dims host, N int32; this version requires all J_n equal and the pair
- *            (N, J) in the compiled set (N in 2..5, J in {2,3,4,5,8,10}, J^N <= 10^4)
+ *  nnz       1 <= nnz <= INT32_MAX (duplicate coordinates are accepted: multiset,
+ *            reading R14); EINVAL outside
+ *  order     2 <= N <= 10
+ *  dims      host, N int64, each 1 <= I_n <= INT32_MAX
+ *  core_dims host, N int32; this version requires all J_n equal (EINVAL otherwise),
+ *            1 <= J <= 16 and J^N <= 2^26.  Compiled fast paths: N in 2..5 with
+ *            J in {2,3,4,5,8,10} (tensor cores for N = 3 fp32, and for order-4 modes
+ *            with one small other mode); any other (N, J) runs the generic kernel
+ *            (update_generic.cu: delta by Eq. 12 as written)
  *  lambda    > 0 (makes B + lambda I positive definite)
  *  seed      init RNG seed: G and every A^(n) ~ U[0,1) (reading R2)
  * Copies the COO to the device, draws the init, builds every mode's slice
@@ -177,7 +183,11 @@ int ptucker_get_partition(int32_t n, int64_t* bounds);
  *                 the fp64 sum (1 = every term in fp64, default; 2; 5 fails the 1e-5 row bound)
  *  "l2_persist_mb" L2 set-aside (MB) for the evict_last factor-row gathers: -1 = the device
  *                 maximum (default; applied at init, released by ptucker_finalize), 0 = leave
- *                 the driver default (a device-wide limit: other users of the GPU see it)
+ *                 the driver default.  Side effect: cudaLimitPersistingL2CacheSize is a
+ *                 process-wide (context) limit, so other work in the same process (torch)
+ *                 runs with that much less normal L2 while the context lives, and
+ *                 ptucker_finalize calls cudaCtxResetPersistingL2Cache, which also resets
+ *                 lines other code marked persisting
  *  "tc_table"     1 = order-4 fp32 modes with one small other mode run the tensor-core kernel on
  *                 the per-i_s core blocks (default; set BEFORE init: it orders the index); 0 = ALU
  *  "rows_l1"      tensor-core gathers of factor rows: -1 = through L1 when a gathered mode has a

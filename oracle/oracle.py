@@ -328,6 +328,13 @@ def test_rmse(m: Model, coords, vals) -> float:
                                     coords.shape[0]))
 
 
+def converged(e_prev: float, e: float, tol: float, xnorm: float) -> bool:
+    """Alg. 2 line 2 "until ... ||X - X'|| converges", reading R30: the relative
+    change of the error falls below tol, |e_t - e_(t-1)| < tol * e_(t-1), or the fit is
+    already within tol of the data scale, e_t <= tol * ||x||."""
+    return abs(e - e_prev) < tol * e_prev or e <= tol * xnorm
+
+
 def run(t: Tensor, m: Model, lam: float, max_iters: int, tol: float, approx_p: float = 0.0,
         orthogonalize: bool = True, threads: int = 0):
     """Alg. 2 (P:496-508): e_0 = error; repeat {update A^(1..N) (line 3); e_t = error (line 4);
@@ -346,7 +353,7 @@ def run(t: Tensor, m: Model, lam: float, max_iters: int, tol: float, approx_p: f
         errs.append(e)
         if approx_p > 0:
             truncate_core(t, m, present, approx_p, threads)
-        if abs(e - errs[-2]) < tol * errs[-2] or e <= tol * xnorm:
+        if converged(errs[-2], e, tol, xnorm):
             break
     if orthogonalize:
         globals()["orthogonalize"](m)

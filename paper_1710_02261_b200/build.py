@@ -46,6 +46,22 @@ def _headers():
     return glob.glob(os.path.join(CSRC, "*.cuh")) + glob.glob(os.path.join(INC, "*.h"))
 
 
+def _flags_hash(extra=()) -> str:
+    """Everything that changes the generated code besides the sources: nvcc, the arch,
+    the flags and NVCC_APPEND_FLAGS (the -D knobs of tools/*_variant.sh)."""
+    import hashlib
+    key = "\0".join([NVCC, *ARCH, *FLAGS, *extra, os.environ.get("NVCC_APPEND_FLAGS", "")])
+    return hashlib.sha256(key.encode()).hexdigest()[:16]
+
+
+def _stamp_ok(path: str, h: str) -> bool:
+    try:
+        with open(path) as f:
+            return f.read().strip() == h
+    except OSError:
+        return False
+
+
 def _stale(target, deps):
     if not os.path.exists(target):
         return True
@@ -53,12 +69,12 @@ def _stale(target, deps):
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def _compile(src: str, force: bool) -> str:
-    obj = os.path.join(OBJ, os.path.basename(src)[:-3] + ".o")
+def _compile(src: str, force: bool, obj_dir: str = OBJ, extra=()) -> str:
+    obj = os.path.join(obj_dir, os.path.basename(src)[:-3] + ".o")
     if force or _stale(obj, [src] + _headers()):
         log = obj[:-2] + ".ptxas.txt"
         tmp = obj + f".tmp{os.getpid()}"
-        r = subprocess.run([NVCC, *ARCH, *FLAGS, "-c", src, "-o", tmp], capture_output=True, text=True)
+        r = subprocess.run([NVCC, *ARCH, *FLAGS, *extra, "-c", src, "-o", tmp], capture_output=True, text=True)
         with open(log, "w") as f:
             f.write(r.stdout + r.stderr)
         if r.returncode != 0:
@@ -67,22 +83,43 @@ def _compile(src: str, force: bool) -> str:
     return obj
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    os.makedirs(OBJ, exist_ok=True)
+def build(force: bool = False, verbose: bool = False, variant: str | None = None, extra=()) -> str:
+    """Build libptucker.so; with `variant`, a tools-only experiment build (extra nvcc
+    flags, e.g. -D knobs) into _variants/<variant>/ that never touches the product
+    library (tools load it through PTUCKER_LIB)."""
+    obj_dir, lib = OBJ, LIB
+    if variant:
+        obj_dir = os.path.join(HERE, "_variants", variant)
+        lib = os.path.join(obj_dir, "libptucker.so")
+    os.makedirs(obj_dir, exist_ok=True)
+    h = _flags_hash(extra)
+    obj_stamp, lib_stamp = os.path.join(obj_dir, ".flags"), lib + ".flags"
+    if not _stamp_ok(obj_stamp, h):
+        force = True  # objects of other flags (a variant build, or another nvcc) are stale
     srcs = sorted(glob.glob(os.path.join(CSRC, "*.cu")))
     with cf.ThreadPoolExecutor(max_workers=min(8, os.cpu_count() or 1)) as ex:
-        objs = list(ex.map(lambda s: _compile(s, force), srcs))
-    if force or _stale(LIB, objs):
-        tmp = LIB + f".tmp{os.getpid()}"
+        objs = list(ex.map(lambda s: _compile(s, force, obj_dir, extra), srcs))
+    with open(obj_stamp, "w") as f:
+        f.write(h)
+    if force or _stale(lib, objs) or not _stamp_ok(lib_stamp, h):
+        tmp = lib + f".tmp{os.getpid()}"
         cmd = [NVCC, *ARCH, "-shared", "-o", tmp, *objs, *LINK_NCCL, "-Xlinker", "--no-undefined"]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError(f"link failed:\n{r.stderr[-4000:]}")
-        os.replace(tmp, LIB)
+        os.replace(tmp, lib)
+        with open(lib_stamp, "w") as f:
+            f.write(h)
     if verbose:
-        print(LIB)
-    return LIB
+        print(lib)
+    return lib
 
 
 if __name__ == "__main__":
-    build(force="--force" in sys.argv, verbose=True)
+    # python -m paper_1710_02261_b200.build [--force] [--variant NAME -DKNOB=1 ...]
+    argv = sys.argv[1:]
+    var, extra = None, []
+    if "--variant" in argv:
+        i = argv.index("--variant")
+        var, extra = argv[i + 1], argv[i + 2:]
+    build(force="--force" in argv, verbose=True, variant=var, extra=tuple(extra))

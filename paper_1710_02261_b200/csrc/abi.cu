@@ -306,7 +306,9 @@ int launch_update_kernel(int n, bool literal) {
             p.gp_elems = (int)sp.elems;
             p.aux_stride = (int64_t)g.J * GBk;
         };
-        const UpdateKernel* ktc = g.mi[n].aux_groups ? find_update_kernel_tc(1, g.J) : nullptr;
+        // the lanes of an aux-grouped index are in (i_s, length) order, which the ALU table
+        // kernel also accepts (it reads lane_aux per lane): option tc = 0 takes that kernel
+        const UpdateKernel* ktc = g.mi[n].aux_groups && g.use_tc ? find_update_kernel_tc(1, g.J) : nullptr;
         if (g.prec == PTUCKER_F64) {
             UpdateParams<double> p = make_params<double>(n, false);
             fill(p);
@@ -490,6 +492,9 @@ int ptucker_get_unique_id(uint8_t out[128]) {
 
 int ptucker_comm_init(int32_t rank, int32_t world, const uint8_t id[128]) {
     if (world < 1 || rank < 0 || rank >= world) return fail(PTUCKER_EINVAL, "bad rank/world %d/%d", rank, world);
+    // the row blocks of every mode (m.bounds, the SELL index of this rank) are fixed by
+    // ptucker_init for the world it saw: a communicator must come first
+    if (g.inited) return fail(PTUCKER_ESTATE, "ptucker_comm_init must precede ptucker_init (or follow ptucker_finalize)");
     if (g.comm) {
         ncclCommDestroy(g.comm);
         g.comm = nullptr;
@@ -807,7 +812,10 @@ int ptucker_init(const int32_t* coords, const void* vals, int32_t vals_dtype, in
                     if (dims[oth[x]] <= 64) sx = x;
                 const int a = sx == 0 ? 1 : 0, b = sx == 2 ? 1 : 2;
                 const int64_t elems = dims[oth[sx]] * (int64_t)J * GBk;
-                if (elems * esz <= 128 * 1024) {
+                // the index groups each row by the small mode with a 32-bit composite key
+                // i_n * I_s + i_s (index.cu k_composite_key): it must fit
+                const bool key32 = dims[n] * dims[oth[sx]] < ((int64_t)1 << 32);
+                if (elems * esz <= 128 * 1024 && key32) {
                     sp.kind = 1;
                     sp.s1 = oth[sx]; sp.r = oth[a]; sp.s2 = oth[b];   // r, s2 = the two large modes (a < b)
                     sp.is1 = sx; sp.ir = a; sp.is2 = b;
@@ -1325,6 +1333,10 @@ int ptucker_info(char* buf, int32_t len) {
     if (!buf || len <= 0) return fail(PTUCKER_EINVAL, "bad buffer");
     std::string s = "{";
     char tmp[512];
+    int comm_ranks = 0;  // size of the library's NCCL communicator (0: none)
+    if (g.comm && ncclCommCount(g.comm, &comm_ranks) != ncclSuccess) comm_ranks = -1;
+    snprintf(tmp, sizeof(tmp), "\"comm_ranks\": %d, ", comm_ranks);
+    s += tmp;
     snprintf(tmp, sizeof(tmp),
              "\"inited\": %s, \"N\": %d, \"J\": %d, \"prec\": \"%s\", \"policy\": \"%s\", \"nnz\": %lld, "
              "\"lambda\": %.17g, \"seg_len\": %d, \"rank\": %d, \"world\": %d, \"grid_update\": %d, "

@@ -94,6 +94,17 @@ constexpr int kRegP = PT_REG_P;              //             loader/MMA warpgroup
 #define PT_A0_INT 0
 #endif
 constexpr int kXuMod = PT_L0_XU_MOD;         // level 0 (G0 = 1): every kXuMod-th t converted on the XU pipe, the rest by integer ops
+// level 0 (G0 = 1), conversion scheme 1: the t[k0][.] of the k0 in kXuMask are converted on
+// the XU pipe, the others by three integer operations into t * 2^-896 (f2d_scaled), whose
+// a0[k0] is pre-multiplied by 2^896 (exact); scheme 0 = the kXuMod interleave of f2d_int
+#ifndef PT_L0_CONV
+#define PT_L0_CONV 1
+#endif
+#ifndef PT_XU_MASK
+#define PT_XU_MASK 0x049
+#endif
+constexpr int kL0Conv = PT_L0_CONV;
+constexpr unsigned kXuMask = PT_XU_MASK;
 constexpr bool kA0Int = PT_A0_INT != 0;      // a0 converted by integer ops too
 constexpr int kBCH = PT_BCH;                      // level 0: TMEM chunks per load batch (registers)
 static_assert(kCRing > kLoaders * kCPref, "ring depths");
@@ -160,6 +171,17 @@ __device__ __forceinline__ void tmem_st8(uint32_t addr, const uint32_t (&r)[16])
 __device__ __forceinline__ double f2d_int(float f) {
     const uint32_t u = __float_as_uint(f);
     const uint32_t hi = ((uint32_t)((int32_t)u >> 3) & 0x8FFFFFFFu) + 0x38000000u;
+    return __hiloint2double((int)hi, (int)(u << 29));
+}
+
+// float -> double scaled by 2^-896, in three integer operations (SHF, LOP3, SHL): the
+// fp32 exponent field e8 is placed unchanged in the fp64 exponent field, i.e. the fp64
+// bias 1023 replaces the fp32 bias 127 without the +896 rebias.  Exact for every finite
+// float: normal f -> f * 2^-896 (a normal double, >= 2^-1022), zero -> +-0, and a
+// subnormal f = 0.m * 2^-126 -> the subnormal double 0.m * 2^-1022 = f * 2^-896.
+__device__ __forceinline__ double f2d_scaled(float f) {
+    const uint32_t u = __float_as_uint(f);
+    const uint32_t hi = (uint32_t)((int32_t)u >> 3) & 0x8FFFFFFFu;
     return __hiloint2double((int)hi, (int)(u << 29));
 }
 
@@ -757,7 +779,11 @@ __global__ void __launch_bounds__(kThreads, 1) k_update_tc(const UpdateParams<fl
             float pf[J];  // fp32 partial sums (G0 > 1)
             double a0d[J];
 #pragma unroll
-            for (int q = 0; q < J; ++q) a0d[q] = kA0Int ? f2d_int(a0f[q]) : double(a0f[q]);
+            for (int q = 0; q < J; ++q) {
+                a0d[q] = kA0Int ? f2d_int(a0f[q]) : double(a0f[q]);
+                // scheme 1: a0[k0] * 2^896 pairs with f2d_scaled(t) = t * 2^-896 (both exact)
+                if (kL0Conv == 1 && LAST64 && G0 == 1 && !((kXuMask >> q) & 1u)) a0d[q] *= 0x1p896;
+            }
 #pragma unroll
             for (int j = 0; j < J; ++j) d[j] = TD(0);
 #pragma unroll
@@ -777,7 +803,10 @@ __global__ void __launch_bounds__(kThreads, 1) k_update_tc(const UpdateParams<fl
                 } else if constexpr (G0 == 1) {
                     // half of the fp32 -> fp64 conversions by integer ops on the ALU pipe, the
                     // other half on the (quarter-rate) XU pipe, so neither pipe saturates
-                    d[j] = fma(a0d[k0], (cc % kXuMod == 0) ? TD(tv) : f2d_int(tv), d[j]);
+                    if constexpr (kL0Conv == 1)
+                        d[j] = fma(a0d[k0], ((kXuMask >> k0) & 1u) ? TD(tv) : f2d_scaled(tv), d[j]);
+                    else
+                        d[j] = fma(a0d[k0], (cc % kXuMod == 0) ? TD(tv) : f2d_int(tv), d[j]);
                 } else {
                     if (k0 % G0 == 0) pf[j] = a0f[k0] * tv;
                     else pf[j] = fmaf(a0f[k0], tv, pf[j]);

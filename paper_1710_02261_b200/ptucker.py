@@ -14,7 +14,9 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libptucker.so")
+# PTUCKER_LIB: a tools-only experiment build (build.py --variant) loaded instead of the
+# in-tree product library; unset in tests, smoke() and the bench
+LIB_PATH = os.environ.get("PTUCKER_LIB") or os.path.join(_HERE, "libptucker.so")
 
 PTUCKER_OK, PTUCKER_EINVAL, PTUCKER_ENUMERIC, PTUCKER_ERESOURCE = 0, 1, 2, 3
 PTUCKER_ECUDA, PTUCKER_ENCCL, PTUCKER_ESTATE = 4, 5, 6

@@ -225,7 +225,7 @@ def test_policies_reported(pt, orc, name, scale, policy):
 
 # ---------------------------------------------------------------- error (Eq. 5) and trajectory
 @pytest.mark.parametrize("name,scale,iters", [("c1", 1.0, 5), ("c2", 0.01, 10), ("c3", 0.001, 10),
-                                              ("c4", 0.001, 10)])
+                                              ("c4", 0.001, 10), ("c5", 0.001, 10)])
 def test_error_trajectory(pt, orc, name, scale, iters):
     cfg = synth.config(name) if scale == 1.0 else synth.small(name, scale)
     coords, vals = init_cfg(pt, cfg)

@@ -558,3 +558,33 @@ def test_driver_examples(orc):
     errs, it, _ = orc.run(t, m, cfg.lam, 6, 0.0, orthogonalize=True)
     assert it == 6 and len(errs) == 7
     assert np.all(np.diff(errs) <= 1e-9 * errs[:-1]) and errs[-1] < errs[0]
+
+
+def test_stop_rule_relative_change(orc):
+    """Reading R30 (Alg. 2 line 2): both branches of the stop test on hand-built
+    error sequences, then the driver on a real problem stops exactly where a stop
+    index recomputed here from the fixed-iteration error sequence says it must."""
+    # relative-change branch: |e_t - e_(t-1)| < tol * e_(t-1), strict
+    assert orc.converged(8.0, 7.875, 0.03125, 0.0)         # change 1/64 of 8 (binary-exact values)
+    assert not orc.converged(8.0, 7.75, 0.03125, 0.0)      # change exactly tol * e_prev: not below
+    assert not orc.converged(10.0, 9.0, 1e-2, 0.0)
+    assert orc.converged(10.0, 10.005, 1e-3, 0.0)          # an increase counts by its size too
+    # absolute branch: e_t <= tol * ||x||
+    assert orc.converged(10.0, 0.5, 1e-2, 100.0) and not orc.converged(10.0, 1.5, 1e-2, 100.0)
+    # the driver: errors of 8 fixed iterations, a tol strictly between two consecutive
+    # relative changes, and the first index whose change is below it
+    from gen import synth
+    cfg = synth.small("c2", 0.002)
+    coords, vals = synth.generate(cfg)
+    t = orc.Tensor(coords, vals, cfg.dims)
+    m = orc.init_model(cfg.dims, [cfg.J] * 3, seed=0, prec=1)
+    errs, _ = orc.als(t, m, cfg.lam, 8)
+    rel = np.abs(np.diff(errs)) / errs[:-1]                 # rel[k] = change of iteration k + 1
+    assert np.all(rel > 0) and errs[-1] > 1e-3 * np.sqrt(t.vals @ t.vals)
+    order = np.sort(rel)
+    tol = float(np.sqrt(order[2] * order[3]))               # between the 3rd and 4th smallest changes
+    expect = int(np.flatnonzero(rel < tol)[0]) + 1          # iterations run when it stops
+    m = orc.init_model(cfg.dims, [cfg.J] * 3, seed=0, prec=1)
+    e_run, it, _ = orc.run(t, m, cfg.lam, 8, tol, orthogonalize=False)
+    assert it == expect and len(e_run) == expect + 1
+    np.testing.assert_allclose(e_run, errs[:expect + 1], rtol=0, atol=0)
