@@ -104,6 +104,10 @@ constexpr int kXuMod = PT_L0_XU_MOD;         // level 0 (G0 = 1): every kXuMod-t
 #define PT_XU_MASK 0x049
 #endif
 constexpr int kL0Conv = PT_L0_CONV;
+#ifndef PT_ACC_EARLY
+#define PT_ACC_EARLY 1
+#endif
+constexpr bool kAccEarly = PT_ACC_EARLY != 0;  // release the accumulator once its last TMEM chunk is in registers
 constexpr unsigned kXuMask = PT_XU_MASK;
 constexpr bool kA0Int = PT_A0_INT != 0;      // a0 converted by integer ops too
 constexpr int kBCH = PT_BCH;                      // level 0: TMEM chunks per load batch (registers)
@@ -796,8 +800,20 @@ __global__ void __launch_bounds__(kThreads, 1) k_update_tc(const UpdateParams<fl
 #pragma unroll
                     for (int q = 0; q < kBCH; ++q)
                         if (cc / 16 + q < NCH) tmem_wait16(rb[q]);
+                    if (kAccEarly && cc / 16 + kBCH >= NCH) {
+                        // the last batch is in registers: accumulator b is free for MMA k + kNT
+                        asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+                        __syncwarp();
+                        if (lane == 0) mbar_arrive(acc_empty(b));
+                    }
                 }
                 const float tv = __uint_as_float(rb[(cc / 16) % kBCH][cc % 16]);
+#ifdef PT_EXP_NOL0  // experiment (wrong results): level-0 arithmetic reduced to one fp32 add per term
+                if (true) {
+                    pf[j] = (k0 == 0 ? 0.f : pf[j]) + tv;
+                    if (k0 == J - 1) d[j] = TD(pf[j]);
+                } else
+#endif
                 if constexpr (!LAST64) {
                     d[j] = fmaf(a0f[k0], tv, d[j]);
                 } else if constexpr (G0 == 1) {
@@ -813,9 +829,11 @@ __global__ void __launch_bounds__(kThreads, 1) k_update_tc(const UpdateParams<fl
                     if (k0 % G0 == G0 - 1 || k0 == J - 1) d[j] = d[j] + TD(pf[j]);
                 }
             }
-            asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-            __syncwarp();
-            if (lane == 0) mbar_arrive(acc_empty(b));
+            if (!(kAccEarly && NCH > kBCH)) {
+                asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+                __syncwarp();
+                if (lane == 0) mbar_arrive(acc_empty(b));
+            }
             mark(k, 4);
             // hand delta (fp64) and x to normal-equation warp 8 + w4
             const int ds = (int)(k % kD);
@@ -926,6 +944,13 @@ __global__ void __launch_bounds__(kThreads, 1) k_update_tc(const UpdateParams<fl
                 if (lane == 0) mbar_arrive(d_empty(w4, ds));
                 // an inactive lane (entry beyond its segment: only in a group's tail) skips the
                 // update; the branch is warp-uniform almost always, so no per-entry selects
+#ifdef PT_EXP_NONE  // experiment (wrong results): normal equations reduced to c += x delta
+                if (e < cur.len) {
+                    const double xd = double(x);
+#pragma unroll
+                    for (int i = 0; i < J; ++i) c[i] = fma(xd, dd[i], c[i]);
+                } else
+#endif
                 if (e < cur.len) {
                     const double xd = double(x);
 #pragma unroll

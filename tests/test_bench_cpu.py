@@ -74,3 +74,6 @@ def test_reference_arm_json_line():
     assert d["impl"] == "reference" and d["value"] > 0
     assert d["cpu_baseline"]["kind"] == "oracle" and d["cpu_baseline"]["value"] == d["value"]
     assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["e2e"]["value"] == d["value"]
+    # every step is one sampled iteration: ms_per_step is what ran, and the sample says how much
+    assert d["sample"]["steps_timed"] == 1 and 0 < d["sample"]["fraction_of_full_iteration"] <= 1
+    assert d["ms_per_step"] * d["steps"] / 1e3 <= d["sample"]["timed_wall_s"] + 1e-6
