@@ -316,12 +316,26 @@ def workload_config(cfg, args):
         "workload": f"{cfg.name}: order-{len(cfg.dims)} {'x'.join(str(d) for d in cfg.dims)}, |Omega|={cfg.nnz}, "
                     f"J={cfg.J}, lambda={cfg.lam}, values={cfg.values}, coords={cfg.coords}",
         "dims": list(cfg.dims), "nnz": cfg.nnz, "J": cfg.J, "lambda": cfg.lam, "seed": cfg.seed,
-        "parallelism": f"rows of each mode sharded over {args.gpus} GPU(s), all-gather per mode",
+        "parallelism": f"rows of each mode sharded over {args.gpus} GPU(s); replicas refreshed by "
+                       f"{'NVLink row pushes from the update kernels' if getattr(args, 'exchange', 'push') == 'push' else 'NCCL all-gather-v'} per mode",
         "l2": "inputs larger than L2 (no flush)",
     }
 
 
 # ----------------------------------------------------------------------------- our arm
+def open_peers(pt, dist, world, args):
+    """Multi-GPU replica refresh by push: every rank opens the other
+    ranks' factor replicas from their CUDA IPC handles; the update kernels then store
+    each solved row into every replica over NVLink.  --exchange nccl keeps the NCCL
+    all-gather-v instead."""
+    pt.ptucker_set_option("exchange", 1 if args.exchange == "push" else 0)
+    if world == 1 or args.exchange != "push":
+        return
+    hs = [None] * world
+    dist.all_gather_object(hs, pt.ptucker_peer_handles())
+    pt.ptucker_open_peers(b"".join(hs), world)
+
+
 def run_ours(args, cfg):
     import torch
     import torch.distributed as dist
@@ -356,6 +370,7 @@ def run_ours(args, cfg):
     if args.l2_persist_mb is not None:
         pt.ptucker_set_option("l2_persist_mb", args.l2_persist_mb)
     pt.ptucker_set_option("pack_gathers", args.pack_gathers)
+    open_peers(pt, dist, world, args)
     pt.ptucker_synchronize()
     init_s = time.perf_counter() - t0
     info = pt.ptucker_info()
@@ -417,6 +432,7 @@ def run_ours(args, cfg):
         per_rank = [x.tolist() for x in allt]
     selfcheck = {"factors_sha256": hsh.hexdigest()[:32], "last_error": errs[-1],
                  "comm_ranks": pt.ptucker_info()["comm_ranks"], "world": world,
+                 "exchange": pt.ptucker_info()["exchange"],
                  "update_ms_per_step_by_rank": [round(x[0], 4) for x in per_rank],
                  "allgather_ms_per_step_by_rank": [round(x[1], 4) for x in per_rank]}
 
@@ -461,6 +477,7 @@ def run_ours(args, cfg):
         pt.ptucker_set_option("policy", POLICY[args.policy])
         pt.ptucker_set_option("tc", args.tc)
         pt.ptucker_set_option("l0_group", args.l0_group)
+        open_peers(pt, dist, world, args)
         pt.ptucker_synchronize()
         t_init = time.perf_counter() - t0
         for _ in range(args.steps):
@@ -514,6 +531,8 @@ def main():
     ap.add_argument("--pack-gathers", type=int, default=0, choices=[0, 1],
                     help="J = 10 tensor-core gathers from packed 40-byte tables (less DRAM traffic, slower)")
     ap.add_argument("--l0-group", type=int, default=1, choices=[1, 2, 5], help="tensor-core level-0 grouping (1 = fp64 per term, g = fp32 partial sums of g terms)")
+    ap.add_argument("--exchange", default="push", choices=["push", "nccl"],
+                    help="multi-GPU replica refresh: rows pushed by the kernels over NVLink, or NCCL all-gather-v")
     ap.add_argument("--approx", type=float, default=0.0,
                     help="P-Tucker-Approx: truncate the core by rate p after every iteration (0 = P-Tucker)")
     ap.add_argument("--ref-seconds", type=float, default=12.0, help="oracle seconds per sampled step (upper bound)")

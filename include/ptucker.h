@@ -62,6 +62,24 @@ const char* ptucker_last_error(void);
 int ptucker_get_unique_id(uint8_t out[128]);
 int ptucker_comm_init(int32_t rank, int32_t world, const uint8_t id[128]);
 
+/* Row exchange by push (S5, "aggregates all updated rows from all threads", Fig. 3
+ * caption P:517-518), after ptucker_init on every rank:
+ *  ptucker_peer_handles: writes this rank's N CUDA IPC handles (64 bytes each, A^(0..N-1)
+ *    in mode order) into out (host, cap >= 64*N bytes); EINVAL if cap is too small.
+ *  ptucker_open_peers: handles = the world ranks' outputs concatenated in rank order
+ *    (host, world*64*N bytes, e.g. all-gathered with torch.distributed); opens the other
+ *    ranks' replicas (cudaIpcOpenMemHandle, peer access over NVLink).  From then on every
+ *    kernel that solves a row of A^(n) also stores it into each peer's replica, so the
+ *    exchange overlaps the update; ptucker_update_mode ends with a one-int NCCL all-reduce
+ *    that orders all ranks' pushes before the next mode (with no communicator -- ranks
+ *    emulated as processes in tests -- the caller must synchronise and barrier between
+ *    modes).  world must equal the context's world (communicator or emulate_world);
+ *    at most 8 ranks.  ECUDA if a handle cannot be opened (then the NCCL all-gather-v of
+ *    ptucker_update_mode stays in use).  The handles are closed by ptucker_finalize /
+ *    the next ptucker_init. */
+int ptucker_peer_handles(uint8_t* out, int32_t cap);
+int ptucker_open_peers(const uint8_t* handles, int32_t world);
+
 /* Pure host helper (no GPU needed): nnz-balanced contiguous row blocks.
  * row_ptr: host, I+1 int64 prefix counts of a mode's slices.  bounds: host,
  * world+1 int64 output; bounds[0] = 0, bounds[world] = I and bounds[g] is the
@@ -178,6 +196,8 @@ int ptucker_get_partition(int32_t n, int64_t* bounds);
  *  "emulate_world", "emulate_rank"  (before init, no communicator): build and update only
  *                 this rank's row blocks of a `world`-way partition, without the exchange
  *                 (tests of the partitioned path on one GPU)
+ *  "exchange"     multi-GPU replica refresh: 1 = push from the kernels when peers are open
+ *                 (default), 0 = NCCL all-gather-v (grouped broadcasts) after each mode
  *  "time_kernels" 1 = bracket every kernel launch with CUDA events (ptucker_kernel_stats)
  *  "l0_group"     tensor-core kernel, F32-B: level-0 terms summed in fp32 in runs of g before
  *                 the fp64 sum (1 = every term in fp64, default; 2; 5 fails the 1e-5 row bound)

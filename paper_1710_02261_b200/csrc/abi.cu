@@ -140,6 +140,11 @@ struct Ctx {
     double *ax_G64 = nullptr, *ax_A0 = nullptr, *ax_W = nullptr, *ax_W2 = nullptr, *ax_E = nullptr,
            *ax_part = nullptr, *ax_UV = nullptr;
     void** ax_ptrs = nullptr;  // device: sc[0..N-2] of mode 0, then A[0..N-1]
+    // multi-GPU push exchange (ptucker_open_peers): the other ranks' replicas of every A^(n)
+    void* peer_A[kMaxN][kMaxPeers] = {{nullptr}};
+    int npeer = 0;
+    int exchange = 1;            // option "exchange": 1 = push when peers are open, 0 = NCCL all-gather-v
+    int* d_barrier = nullptr;    // 1 int: the NCCL all-reduce that orders the pushes before the next mode
     int nsm = 148;
     int grid_upd = 0, grid_lit = 0;
     int64_t launches = 0;        // kernels this library launched since init (gpu_launches evidence)
@@ -152,6 +157,18 @@ struct Ctx {
 
 Ctx g;
 double g_xnorm_pending = 0.0;
+
+void close_peers() {
+    for (int n = 0; n < kMaxN; ++n)
+        for (int r = 0; r < kMaxPeers; ++r) {
+            if (g.peer_A[n][r]) cudaIpcCloseMemHandle(g.peer_A[n][r]);
+            g.peer_A[n][r] = nullptr;
+        }
+    g.npeer = 0;
+}
+
+bool pushing() { return g.npeer > 0 && g.exchange == 1; }
+
 
 cudaStream_t S() { return g.stream; }
 
@@ -263,6 +280,10 @@ UpdateParams<TS> make_params(int n, bool literal) {
     p.gtail[1] = g.pk_tail[1];
     p.l0_group = g.l0_group;
     p.rows_l1 = g.rows_l1[n];
+    if (pushing()) {
+        p.peers.n = g.npeer;
+        for (int r = 0; r < g.npeer; ++r) p.peers.base[r] = g.peer_A[n][r];
+    }
     return p;
 }
 
@@ -426,6 +447,8 @@ int choose_kernel() {
 }
 
 void free_all() {
+    close_peers();
+    g.d_barrier = nullptr;
     g.arena.release_all();
     g.scratch.release_all();
     for (int n = 0; n < kMaxN; ++n) {
@@ -639,6 +662,11 @@ int ptucker_set_option(const char* key, int64_t value) {
         g.use_smp = (int)value;
         return PTUCKER_OK;
     }
+    if (k == "exchange") {
+        if (value != 0 && value != 1) return fail(PTUCKER_EINVAL, "exchange must be 0 (NCCL all-gather) or 1 (push)");
+        g.exchange = (int)value;
+        return PTUCKER_OK;
+    }
     if (k == "time_kernels") {
         g.time_kernels = value != 0;
         return PTUCKER_OK;
@@ -755,6 +783,8 @@ int ptucker_init(const int32_t* coords, const void* vals, int32_t vals_dtype, in
     CK(A.alloc((void**)&g.d_fail, sizeof(int)));
     CK(A.alloc((void**)&g.d_qrfail, sizeof(int)));
     CK(A.alloc((void**)&g.d_work, sizeof(unsigned int)));
+    CK(A.alloc((void**)&g.d_barrier, sizeof(int)));
+    CK(cudaMemsetAsync(g.d_barrier, 0, sizeof(int), S()));
     CK(A.alloc((void**)&g.red_part, 256 * sizeof(double)));
     CK(A.alloc((void**)&g.red_out, 4 * sizeof(double)));
     CK(A.alloc((void**)&g.qr, (5 * 256 + 256 * 256) * sizeof(double)));
@@ -881,6 +911,45 @@ int ptucker_init(const int32_t* coords, const void* vals, int32_t vals_dtype, in
     return PTUCKER_OK;
 }
 
+int ptucker_peer_handles(uint8_t* out, int32_t cap) {
+    int rc = require_init();
+    if (rc) return rc;
+    if (!out || cap < g.N * 64) return fail(PTUCKER_EINVAL, "need %d bytes", g.N * 64);
+    static_assert(sizeof(cudaIpcMemHandle_t) == 64, "IPC handle size");
+    for (int n = 0; n < g.N; ++n) {
+        cudaIpcMemHandle_t h;
+        CK(cudaIpcGetMemHandle(&h, g.A[n]));  // A^(n) is its own cudaMalloc (DeviceArena)
+        memcpy(out + 64 * n, &h, 64);
+    }
+    return PTUCKER_OK;
+}
+
+int ptucker_open_peers(const uint8_t* handles, int32_t world) {
+    int rc = require_init();
+    if (rc) return rc;
+    if (!handles || world != g.world) return fail(PTUCKER_EINVAL, "handles of %d ranks expected", g.world);
+    if (g.world - 1 > kMaxPeers) return fail(PTUCKER_EINVAL, "at most %d peers", kMaxPeers);
+    close_peers();
+    int k = 0;
+    for (int r = 0; r < world; ++r) {
+        if (r == g.rank) continue;
+        for (int n = 0; n < g.N; ++n) {
+            cudaIpcMemHandle_t h;
+            memcpy(&h, handles + 64 * ((size_t)r * g.N + n), 64);
+            const cudaError_t e = cudaIpcOpenMemHandle(&g.peer_A[n][k], h, cudaIpcMemLazyEnablePeerAccess);
+            if (e != cudaSuccess) {
+                g.peer_A[n][k] = nullptr;
+                close_peers();
+                cudaGetLastError();
+                return fail(PTUCKER_ECUDA, "cudaIpcOpenMemHandle(rank %d, A^(%d)): %s", r, n, cudaGetErrorString(e));
+            }
+        }
+        ++k;
+    }
+    g.npeer = k;
+    return PTUCKER_OK;
+}
+
 int ptucker_update_mode(int32_t n) {
     int rc = require_init();
     if (rc) return rc;
@@ -891,15 +960,31 @@ int ptucker_update_mode(int32_t n) {
     ModeIndex& m = g.mi[n];
     if (m.nheavy > 0) {
         rc = timed("finalize", [&]() -> int {
+            PeerRows pr;
+            if (pushing()) {
+                pr.n = g.npeer;
+                for (int r = 0; r < g.npeer; ++r) pr.base[r] = g.peer_A[n][r];
+            }
             launch_heavy_finalize(m.nheavy, m.hrow, m.hnseg, m.hpbase, m.partials, m.hrec, g.J, g.lambda, g.A[n], g.esz,
-                                  g.lda, g.sse_row[n], g.d_fail, S());
+                                  g.lda, g.sse_row[n], g.d_fail, S(), pr);
             g.launches += 3;
             CK(cudaGetLastError());
             return PTUCKER_OK;
         }, n);
         if (rc) return rc;
     }
-    if (g.world > 1 && g.comm) {
+    if (g.world > 1 && pushing()) {
+        // the rows already sit in every replica (pushed by the kernels above); an all-reduce
+        // of one int orders every rank's pushes before any rank's next mode.  Without a
+        // communicator (tests: ranks as processes on one GPU) the caller orders the ranks.
+        if (g.comm) {
+            rc = timed("allgather", [&]() -> int {
+                NK(ncclAllReduce(g.d_barrier, g.d_barrier, 1, ncclInt32, ncclSum, g.comm, S()));
+                return PTUCKER_OK;
+            });
+            if (rc) return rc;
+        }
+    } else if (g.world > 1 && g.comm) {
         rc = timed("allgather", [&]() -> int {
             // all-gather-v of the row blocks (grouped broadcasts, in place)
             const ncclDataType_t dt = g.prec == PTUCKER_F64 ? ncclDouble : ncclFloat;
@@ -1335,7 +1420,8 @@ int ptucker_info(char* buf, int32_t len) {
     char tmp[512];
     int comm_ranks = 0;  // size of the library's NCCL communicator (0: none)
     if (g.comm && ncclCommCount(g.comm, &comm_ranks) != ncclSuccess) comm_ranks = -1;
-    snprintf(tmp, sizeof(tmp), "\"comm_ranks\": %d, ", comm_ranks);
+    snprintf(tmp, sizeof(tmp), "\"comm_ranks\": %d, \"peers\": %d, \"exchange\": \"%s\", ", comm_ranks, g.npeer,
+             g.world == 1 ? "none" : (pushing() ? "push" : (g.comm ? "nccl_allgather" : "none")));
     s += tmp;
     snprintf(tmp, sizeof(tmp),
              "\"inited\": %s, \"N\": %d, \"J\": %d, \"prec\": \"%s\", \"policy\": \"%s\", \"nnz\": %lld, "

@@ -25,6 +25,27 @@ __host__ __device__ constexpr int gblk(int J, int elem_bytes) {
 }
 __host__ __device__ constexpr int ipow(int b, int e) { return e == 0 ? 1 : b * ipow(b, e - 1); }
 
+// Multi-GPU row exchange by push: the other ranks' replicas of A^(n),
+// opened from their CUDA IPC handles (ptucker_open_peers).  Every kernel that stores a
+// solved row of A^(n) also stores it into each peer replica (NVLink P2P stores), so the
+// exchange overlaps the update; a barrier per mode (NCCL) orders it before the next mode.
+constexpr int kMaxPeers = 7;
+struct PeerRows {
+    int n = 0;                          // peers (world - 1), 0: no push
+    void* base[kMaxPeers] = {nullptr};  // peer replica of A^(n), same row stride as the local one
+};
+// Copy the row just stored at `local` (row_bytes, a multiple of 16) into every peer
+// replica at the same row.  The reads return this thread's own stores.
+__device__ __forceinline__ void push_row(const PeerRows& pr, const void* local, int64_t row, int row_bytes) {
+    if (pr.n == 0) return;
+    const uint4* src = reinterpret_cast<const uint4*>(local);
+    for (int q = 0; q < row_bytes / 16; ++q) {
+        const uint4 v = src[q];
+        for (int r = 0; r < pr.n; ++r)
+            reinterpret_cast<uint4*>(static_cast<char*>(pr.base[r]) + row * row_bytes)[q] = v;
+    }
+}
+
 // Arguments of the fused row-update kernel for mode n over this rank's
 // length-sorted segments (SELL-32 layout).
 template <typename TS>
@@ -58,6 +79,7 @@ struct UpdateParams {
     const float* gtail[2];        //   into 32-byte heads (floats 0..7) and packed 8-byte tails (8..9)
     int l0_group;                 // tensor-core kernel: level-0 terms summed in fp32 before fp64 (1 or 2)
     int rows_l1;                  // gather factor rows through L1 (skewed gathered modes: hot rows)
+    PeerRows peers;               // multi-GPU push: the other ranks' replicas of A^(n) (n = 0: none)
 };
 
 using UpdateLauncher = void (*)(const void* params, bool literal, int grid, cudaStream_t st);

@@ -174,7 +174,8 @@ __global__ void __launch_bounds__(256) k_heavy_sum(int64_t nheavy, int PW, const
 // JC > 0: the solve in registers (chol_solve<JC>, update.cuh); JC = 0: runtime J <= 16.
 template <typename T, int JC>
 __global__ void __launch_bounds__(128) k_heavy_solve(int64_t nheavy, const int32_t* hrow, const double* recs, int J,
-                                                     double lambda, T* An, int lda, double* sse_row, int* fail) {
+                                                     double lambda, T* An, int lda, double* sse_row, int* fail,
+                                                     const PeerRows peers) {
     const int PW = J * (J + 1) / 2 + J + 1;
     for (int64_t h = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; h < nheavy; h += (int64_t)gridDim.x * blockDim.x) {
         const double* rec = recs + h * PW;
@@ -211,12 +212,13 @@ __global__ void __launch_bounds__(128) k_heavy_solve(int64_t nheavy, const int32
             ec = fma(at - a[j], c[j] - lambda * a[j], ec);
         }
         sse_row[row] = sse + ac - lambda * aa + 2.0 * ec;
+        push_row(peers, out, row, lda * (int)sizeof(T));
     }
 }
 
 void launch_heavy_finalize(int64_t nheavy, const int32_t* hrow, const int32_t* hnseg, const int64_t* hpbase,
                            const double* partials, double* rec, int J, double lambda, void* An, int elem_bytes,
-                           int lda, double* sse_row, int* fail, cudaStream_t st) {
+                           int lda, double* sse_row, int* fail, cudaStream_t st, const PeerRows& peers) {
     if (nheavy <= 0) return;
     const int PW = J * (J + 1) / 2 + J + 1;
     const int64_t nitems = nheavy * PW;
@@ -227,9 +229,9 @@ void launch_heavy_finalize(int64_t nheavy, const int32_t* hrow, const int32_t* h
     const unsigned g2 = (unsigned)std::min<int64_t>((nheavy + 127) / 128, 148 * 16);
 #define PT_HF(JC)                                                                                                  \
     if (elem_bytes == 8)                                                                                           \
-        k_heavy_solve<double, JC><<<g2, 128, 0, st>>>(nheavy, hrow, rec, J, lambda, (double*)An, lda, sse_row, fail); \
+        k_heavy_solve<double, JC><<<g2, 128, 0, st>>>(nheavy, hrow, rec, J, lambda, (double*)An, lda, sse_row, fail, peers); \
     else                                                                                                           \
-        k_heavy_solve<float, JC><<<g2, 128, 0, st>>>(nheavy, hrow, rec, J, lambda, (float*)An, lda, sse_row, fail);
+        k_heavy_solve<float, JC><<<g2, 128, 0, st>>>(nheavy, hrow, rec, J, lambda, (float*)An, lda, sse_row, fail, peers);
     switch (J) {
         case 2: PT_HF(2) break;
         case 3: PT_HF(3) break;

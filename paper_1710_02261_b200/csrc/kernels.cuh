@@ -14,7 +14,7 @@ void launch_permute_core(const void* G, void* Gp, int elem_bytes, int N, int J, 
 // ---- heavy rows: reduce the segment partials in a fixed order and solve (Eq. 9) ----
 void launch_heavy_finalize(int64_t nheavy, const int32_t* hrow, const int32_t* hnseg, const int64_t* hpbase,
                            const double* partials, double* rec, int J, double lambda, void* An, int elem_bytes,
-                           int lda, double* sse_row, int* fail, cudaStream_t st);
+                           int lda, double* sse_row, int* fail, cudaStream_t st, const PeerRows& peers);
 // ---- deterministic sum of x[0..n) (fixed 256-block tree) into *out (device) ----
 void launch_sum(const double* x, int64_t n, double* part256, double* out, cudaStream_t st);
 // ---- QR (Eq. 7) by CholeskyQR2 in fp64, and G <- G x_n R (Eq. 8) ----

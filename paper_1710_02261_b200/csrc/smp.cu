@@ -188,6 +188,7 @@ __global__ void __launch_bounds__(kUpdThreads, 1) k_update_smp2(const UpdatePara
                 ec = fma(at - a[j], c[j] - p.lambda * a[j], ec);
             }
             p.sse_row[row] = sse + ac - p.lambda * aa + 2.0 * ec;
+            push_row(p.peers, out, row, p.lda * (int)sizeof(TS));
         } else {
             const int stp = p.lane_pstride[slot];
             double* dst = p.partials + pidx;

@@ -457,6 +457,9 @@ __global__ void __launch_bounds__(kUpdThreads, upd_min_blocks(J, (int)sizeof(TS)
                     if constexpr (VN == 4) v = make_float4(e4[0], e4[1], e4[2], e4[3]);
                     else v = make_double2(e4[0], e4[1]);
                     reinterpret_cast<V*>(out)[q] = v;
+                    for (int r = 0; r < p.peers.n; ++r)  // multi-GPU push into the peer replicas
+                        reinterpret_cast<V*>(static_cast<char*>(p.peers.base[r]) +
+                                             (int64_t)row * p.lda * (int64_t)sizeof(TS))[q] = v;
                 }
                 p.sse_row[row] = sse;
             } else {

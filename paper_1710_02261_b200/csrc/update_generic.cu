@@ -125,7 +125,8 @@ __global__ void __launch_bounds__(128) k_update_gen(const UpdateParams<TS> p, in
             aa = fma(a[j], a[j], aa);
             ec = fma(at - a[j], c[j] - p.lambda * a[j], ec);
         }
-        p.sse_row[row] = sse + ac - p.lambda * aa + 2.0 * ec;  // SSE of the stored row (update.cuh)
+        p.sse_row[row] = sse + ac - p.lambda * aa + 2.0 * ec;
+        push_row(p.peers, out, row, p.lda * (int)sizeof(TS));  // SSE of the stored row (update.cuh)
     }
 }
 

@@ -553,8 +553,17 @@ __global__ void __launch_bounds__(kThreads, 1) k_update_tc(const UpdateParams<fl
 #pragma unroll
                 for (int i = 0; i < 4; ++i) {
                     const int u = lane + kWarp * i;
+#if defined(PT_EXP_SMALLGATHER)  // experiment (wrong results): rows of a 4096-row window (L2-resident)
+                    const char* r0 = reinterpret_cast<const char*>(p.A[0] + (int64_t)((int)*crd(cs, 0, u) & 4095) * p.lda);
+                    const char* r1 = reinterpret_cast<const char*>(p.A[1] + (int64_t)((int)*crd(cs, 1, u) & 4095) * p.lda);
+#elif defined(PT_EXP_NOGATHER)  // experiment (wrong results): no row gathers at all
+                    if (true) { *rowx(s, u) = 0.f; continue; }
+                    const char* r0 = reinterpret_cast<const char*>(p.A[0]);
+                    const char* r1 = reinterpret_cast<const char*>(p.A[1]);
+#else
                     const char* r0 = reinterpret_cast<const char*>(p.A[0] + (int64_t)(int)*crd(cs, 0, u) * p.lda);
                     const char* r1 = reinterpret_cast<const char*>(p.A[1] + (int64_t)(int)*crd(cs, 1, u) * p.lda);
+#endif
 #pragma unroll
                     for (int q = 0; q < NQ; ++q) {
                         cp_async16_hint(rowc(s, 0, q, u), r0 + 16 * q, pol_rows);
@@ -655,6 +664,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_update_tc(const UpdateParams<fl
                 const uint32_t d = tmem + b * NP;
                 const uint32_t ahi = tmem + SH::ACOL + a * 2 * KP, alo = ahi + KP;
                 uint32_t acc = 0;
+#ifdef PT_EXP_NOMMA  // experiment (wrong results): one MMA per tile instead of 3 x KSTEPS
+                mma_tf32_ta(d, ahi, dbhi[0], idesc, 0);
+#else
 #pragma unroll
                 for (int pr = 0; pr < 3; ++pr)
 #pragma unroll
@@ -662,6 +674,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_update_tc(const UpdateParams<fl
                         mma_tf32_ta(d, (pr == 0 ? alo : ahi) + 8 * ks, pr == 1 ? dblo[ks] : dbhi[ks], idesc, acc);
                         acc = 1;
                     }
+#endif
                 asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
                                  acc_full(b))
                              : "memory");
@@ -894,9 +907,13 @@ __global__ void __launch_bounds__(kThreads, 1) k_update_tc(const UpdateParams<fl
                 }
                 sse += ac - p.lambda * aa + 2.0 * ec;  // SSE of the stored row (see update.cuh)
 #pragma unroll
-                for (int q = 0; q < SH::NQ; ++q)
-                    reinterpret_cast<float4*>(out)[q] =
-                        make_float4(stv[4 * q], stv[4 * q + 1], stv[4 * q + 2], stv[4 * q + 3]);
+                for (int q = 0; q < SH::NQ; ++q) {
+                    const float4 v = make_float4(stv[4 * q], stv[4 * q + 1], stv[4 * q + 2], stv[4 * q + 3]);
+                    reinterpret_cast<float4*>(out)[q] = v;
+                    for (int r = 0; r < p.peers.n; ++r)  // multi-GPU push into the peer replicas (NVLink)
+                        reinterpret_cast<float4*>(static_cast<char*>(p.peers.base[r]) +
+                                                  (int64_t)g.row * p.lda * 4)[q] = v;
+                }
                 p.sse_row[g.row] = sse;
             } else {
                 const int stp = p.lane_pstride[g.slot];

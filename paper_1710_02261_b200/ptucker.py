@@ -28,6 +28,8 @@ _SIGS = {
     "ptucker_get_unique_id": (C.c_int, [C.c_void_p]),
     "ptucker_comm_init": (C.c_int, [C.c_int32, C.c_int32, C.c_void_p]),
     "ptucker_partition_rows": (C.c_int, [C.c_void_p, C.c_int64, C.c_int32, C.c_void_p]),
+    "ptucker_peer_handles": (C.c_int, [C.c_void_p, C.c_int32]),
+    "ptucker_open_peers": (C.c_int, [C.c_void_p, C.c_int32]),
     "ptucker_set_stream": (C.c_int, [C.c_void_p]),
     "ptucker_init": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int32, C.c_int64, C.c_int32, C.c_void_p, C.c_void_p,
                                C.c_double, C.c_uint64]),
@@ -109,6 +111,18 @@ def ptucker_get_unique_id() -> bytes:
     buf = (C.c_uint8 * 128)()
     _check(load().ptucker_get_unique_id(buf))
     return bytes(buf)
+
+
+def ptucker_peer_handles() -> bytes:
+    n = ptucker_info()["N"]
+    buf = C.create_string_buffer(64 * n)
+    _check(load().ptucker_peer_handles(buf, 64 * n))
+    return buf.raw
+
+
+def ptucker_open_peers(handles: bytes, world: int):
+    buf = C.create_string_buffer(bytes(handles), len(handles))
+    _check(load().ptucker_open_peers(buf, world))
 
 
 def ptucker_comm_init(rank: int, world: int, uid: bytes | None):
