@@ -100,11 +100,12 @@ int ptucker_set_stream(void* cuda_stream);
  *            reading R14); EINVAL outside
  *  order     2 <= N <= 10
  *  dims      host, N int64, each 1 <= I_n <= INT32_MAX
- *  core_dims host, N int32; this version requires all J_n equal (EINVAL otherwise),
- *            1 <= J <= 16 and J^N <= 2^26.  Compiled fast paths: N in 2..5 with
- *            J in {2,3,4,5,8,10} (tensor cores for N = 3 fp32, and for order-4 modes
- *            with one small other mode); any other (N, J) runs the generic kernel
- *            (update_generic.cu: delta by Eq. 12 as written)
+ *  core_dims host, N int32, J_1..J_N (Alg. 2 input): each 1 <= J_n <= 16 and
+ *            prod J_n <= 2^26 (EINVAL otherwise).  Compiled fast paths for equal J_n: N in
+ *            2..5 with J in {2,3,4,5,8,10} (tensor cores for N = 3 fp32, and for order-4
+ *            modes with one small other mode); unequal J_n and any other (N, J) run the
+ *            generic kernel (update_generic.cu: delta by Eq. 12 as written).  Factors are
+ *            I_n x J_n and the core J_1 x ... x J_N (C order) in every getter/setter
  *  lambda    > 0 (makes B + lambda I positive definite)
  *  seed      init RNG seed: G and every A^(n) ~ U[0,1) (reading R2)
  * Copies the COO to the device, draws the init, builds every mode's slice
@@ -186,7 +187,6 @@ int ptucker_get_partition(int32_t n, int64_t* bounds);
  *  "policy"       precision of the fp32 contraction: -1 = automatic
  *                 (default: every outer TTV stage in fp64), 0 = F32-A (all fp32), 1 = F32-B
  *                 (outermost stage fp64), 2 = F32-C (all outer stages fp64)
- *  "seg_len"      max entries per row segment (>= 1, default 256; set BEFORE init)
  *  "tc"           1 = order-3 fp32 updates run the innermost contraction on the tcgen05 tensor
  *                 cores (3xTF32, default); 0 = the all-ALU kernel
  *  "smp"          1 = small-mode precontraction where it applies (order 4, two other modes with
@@ -198,6 +198,11 @@ int ptucker_get_partition(int32_t n, int64_t* bounds);
  *                 (tests of the partitioned path on one GPU)
  *  "exchange"     multi-GPU replica refresh: 1 = push from the kernels when peers are open
  *                 (default), 0 = NCCL all-gather-v (grouped broadcasts) after each mode
+ *  "graph"        1 = ptucker_sweep records its launches once as a CUDA graph and replays it
+ *                 (default); the graph is dropped by any option change, init, finalize,
+ *                 QR and ptucker_open_peers; not used while time_kernels is on.  0 = direct
+ *  "seg_len"      segment length S of the index (before init): -1 = automatic (default: the
+ *                 power of two >= |Omega| / (SMs x 128) in [8, 256]), else 1..2^20
  *  "time_kernels" 1 = bracket every kernel launch with CUDA events (ptucker_kernel_stats)
  *  "l0_group"     tensor-core kernel, F32-B: level-0 terms summed in fp32 in runs of g before
  *                 the fp64 sum (1 = every term in fp64, default; 2; 5 fails the 1e-5 row bound)

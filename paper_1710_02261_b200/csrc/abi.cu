@@ -79,7 +79,9 @@ struct Ctx {
     ncclComm_t comm = nullptr;
     int emu_rank = 0, emu_world = 1;  // options "emulate_rank"/"emulate_world": partition without a communicator
     // problem
-    int N = 0, J = 0, prec = 0, esz = 4;
+    int N = 0, J = 0, prec = 0, esz = 4;  // J: max_n J_n (equal J_n: the J of the compiled paths)
+    JDims Jv;                             // J_1..J_N (unequal J_n run the generic path)
+    bool ujn = false;                     // unequal J_n
     int64_t nnz = 0;
     int64_t dims[kMaxN] = {0};
     double xnorm = 0.0;  // sqrt(sum x^2) over Omega (convergence floor of ptucker_run)
@@ -87,7 +89,8 @@ struct Ctx {
     uint64_t seed = 0;
     int lda = 0, gp_elems = 0;
     int policy = -1;    // -1 = automatic per order; else outer fp64 levels
-    int seg_len = 256;  // S
+    int seg_len = -1;       // option "seg_len" (S); -1 = automatic (resolve_seg_len)
+    int seg_len_eff = 256;  // the S of the current index
     DeviceArena arena, scratch;
     void* A[kMaxN] = {nullptr};
     void* G = nullptr;
@@ -149,6 +152,11 @@ struct Ctx {
     int grid_upd = 0, grid_lit = 0;
     int64_t launches = 0;        // kernels this library launched since init (gpu_launches evidence)
     long long* trace = nullptr;  // option "trace": device buffer of per-phase clocks (tools/)
+    // CUDA graph of a whole sweep (option "graph"): captured at the first ptucker_sweep
+    // and replayed while the launch parameters stay valid (invalidate_graph)
+    int use_graph = 1;
+    cudaGraphExec_t graph_exec = nullptr;
+    int64_t graph_launches = 0;  // kernels in the captured sweep
     // timing
     bool time_kernels = false;
     std::vector<Pending> pending;
@@ -168,6 +176,14 @@ void close_peers() {
 }
 
 bool pushing() { return g.npeer > 0 && g.exchange == 1; }
+
+// A captured sweep bakes in pointers (G for the small-mode tables, the packed gather tables,
+// the peer replicas) and the kernel choice: any option change, init, finalize, QR (which
+// swaps G) or a new peer set drops it.
+void invalidate_graph() {
+    if (g.graph_exec) cudaGraphExecDestroy(g.graph_exec);
+    g.graph_exec = nullptr;
+}
 
 
 cudaStream_t S() { return g.stream; }
@@ -357,11 +373,11 @@ int launch_update_kernel(int n, bool literal) {
         if (g.prec == PTUCKER_F64) {
             UpdateParams<double> p = make_params<double>(n, false);
             p.Gp = (const double*)g.G;
-            launch_update_generic(&p, 8, g.N, g.J, g.nsm, S());
+            launch_update_generic(&p, 8, g.N, g.Jv, g.nsm, S());
         } else {
             UpdateParams<float> p = make_params<float>(n, false);
             p.Gp = (const float*)g.G;
-            launch_update_generic(&p, 4, g.N, g.J, g.nsm, S());
+            launch_update_generic(&p, 4, g.N, g.Jv, g.nsm, S());
         }
         CK(cudaGetLastError());
         return PTUCKER_OK;
@@ -447,6 +463,7 @@ int choose_kernel() {
 }
 
 void free_all() {
+    invalidate_graph();
     close_peers();
     g.d_barrier = nullptr;
     g.arena.release_all();
@@ -583,6 +600,12 @@ int rows_l1_auto(int n) {
 int ptucker_set_option(const char* key, int64_t value) {
     if (!key) return fail(PTUCKER_EINVAL, "null key");
     const std::string k = key;
+    invalidate_graph();
+    if (k == "graph") {
+        if (value != 0 && value != 1) return fail(PTUCKER_EINVAL, "graph must be 0 or 1");
+        g.use_graph = (int)value;
+        return PTUCKER_OK;
+    }
     if (k == "policy") {
         if (value < -1 || value > 2) return fail(PTUCKER_EINVAL, "policy must be -1 (auto), 0, 1 or 2");
         g.policy = (int)value;
@@ -590,7 +613,7 @@ int ptucker_set_option(const char* key, int64_t value) {
         return PTUCKER_OK;
     }
     if (k == "seg_len") {
-        if (value < 1 || value > (1 << 20)) return fail(PTUCKER_EINVAL, "seg_len out of range");
+        if (value != -1 && (value < 1 || value > (1 << 20))) return fail(PTUCKER_EINVAL, "seg_len out of range");
         if (g.inited) return fail(PTUCKER_ESTATE, "seg_len must be set before ptucker_init");
         g.seg_len = (int)value;
         return PTUCKER_OK;
@@ -698,15 +721,17 @@ int ptucker_init(const int32_t* coords, const void* vals, int32_t vals_dtype, in
     if (order < 2 || order > kMaxN) return fail(PTUCKER_EINVAL, "order %d not in 2..%d", order, kMaxN);
     if (nnz < 1 || nnz > INT32_MAX) return fail(PTUCKER_EINVAL, "nnz %lld out of range", (long long)nnz);
     if (!(lambda > 0.0) || !std::isfinite(lambda)) return fail(PTUCKER_EINVAL, "lambda must be > 0");
+    bool ujn = false;
+    int J = 0;  // max_n J_n
     for (int n = 0; n < order; ++n) {
         if (dims[n] < 1 || dims[n] > INT32_MAX) return fail(PTUCKER_EINVAL, "dims[%d] out of range", n);
-        if (core_dims[n] != core_dims[0]) return fail(PTUCKER_EINVAL, "unequal core dims are not supported");
+        if (core_dims[n] < 1 || core_dims[n] > 16) return fail(PTUCKER_EINVAL, "core_dims[%d] must be in 1..16", n);
+        ujn = ujn || core_dims[n] != core_dims[0];
+        J = std::max(J, (int)core_dims[n]);
     }
-    const int J = core_dims[0];
-    if (J < 1) return fail(PTUCKER_EINVAL, "core dim must be >= 1");
     {
         double gs = 1.0;
-        for (int n = 0; n < order; ++n) gs *= J;
+        for (int n = 0; n < order; ++n) gs *= core_dims[n];
         if (gs > (double)(1 << 26)) return fail(PTUCKER_EINVAL, "core of %g entries exceeds 2^26", gs);
     }
     const int esz = vals_dtype == PTUCKER_F64 ? 8 : 4;
@@ -754,7 +779,7 @@ int ptucker_init(const int32_t* coords, const void* vals, int32_t vals_dtype, in
         g_xnorm_pending = std::sqrt(xx);
     }
     {
-        if (!find_update_kernel(vals_dtype, 1, order, J) && !generic_shape_ok(order, J))
+        if (!ujn && !find_update_kernel(vals_dtype, 1, order, J) && !generic_shape_ok(order, J))
             return fail(PTUCKER_EINVAL, "(N=%d, J=%d): J must be <= 16", order, J);
     }
     pc.lap("validation (host)");
@@ -767,7 +792,11 @@ int ptucker_init(const int32_t* coords, const void* vals, int32_t vals_dtype, in
     }
     g.N = order;
     g.J = J;
-    g.generic = find_update_kernel(vals_dtype, 1, order, J) == nullptr;
+    g.ujn = ujn;
+    g.Jv = JDims();
+    for (int n = 0; n < order; ++n) g.Jv.j[n] = core_dims[n];
+    // unequal J_n: the generic kernel (delta by Eq. 12 as written, any J_n <= 16)
+    g.generic = ujn || find_update_kernel(vals_dtype, 1, order, J) == nullptr;
     g.xnorm = g_xnorm_pending;
     g.prec = vals_dtype;
     g.esz = esz;
@@ -775,7 +804,7 @@ int ptucker_init(const int32_t* coords, const void* vals, int32_t vals_dtype, in
     g.lambda = lambda;
     g.seed = seed;
     for (int n = 0; n < order; ++n) g.dims[n] = dims[n];
-    g.lda = factor_ld(J, esz);
+    g.lda = factor_ld(J, esz);  // every factor padded to max_n J_n (rows beyond J_n stay zero)
     int64_t nblk = 1;
     for (int l = 0; l < order - 2; ++l) nblk *= J;
     g.gp_elems = g.generic ? 0 : (int)(nblk * gblk(J, esz));  // generic kernel reads G itself
@@ -792,14 +821,14 @@ int ptucker_init(const int32_t* coords, const void* vals, int32_t vals_dtype, in
     CK(cudaMemsetAsync(g.d_qrfail, 0, sizeof(int), S()));
     // ---- init (Alg. 2 line 1) ----
     int64_t gsize = 1;
-    for (int n = 0; n < order; ++n) gsize *= J;
+    for (int n = 0; n < order; ++n) gsize *= g.Jv.j[n];
     CK(A.alloc(&g.G, gsize * esz));
     CK(A.alloc(&g.Gtmp, gsize * esz));
     launch_init_uniform(g.G, esz, 1, (int)gsize, (int)gsize, seed, 0, S());
     for (int n = 0; n < order; ++n) {
         CK(A.alloc(&g.A[n], dims[n] * g.lda * esz));
         CK(cudaMemsetAsync(g.A[n], 0, dims[n] * g.lda * esz, S()));
-        launch_init_uniform(g.A[n], esz, dims[n], J, g.lda, seed, (uint64_t)(1 + n), S());
+        launch_init_uniform(g.A[n], esz, dims[n], g.Jv.j[n], g.lda, seed, (uint64_t)(1 + n), S());  // idx = i*J_n + j
         if (!g.generic) CK(A.alloc(&g.Gp[n], (size_t)g.gp_elems * esz));
         CK(A.alloc((void**)&g.sse_row[n], dims[n] * sizeof(double)));
         CK(cudaMemsetAsync(g.sse_row[n], 0, dims[n] * sizeof(double), S()));
@@ -871,6 +900,24 @@ int ptucker_init(const int32_t* coords, const void* vals, int32_t vals_dtype, in
         g.world = g.emu_world;
         g.rank = g.emu_rank;
     }
+    {
+        // automatic S (option seg_len = -1): at least one full 128-lane group per SM, i.e.
+        // S = the power of two >= |Omega| / (SMs * 128), clamped to [8, 256].  Small tensors
+        // (c1, c2) get short segments so every SM has work (their multi-segment rows are
+        // reduced by the heavy-row finalize); large ones keep S = 256.  It depends only on
+        // |Omega| and the device (not on the rank count), so factors stay bit-identical for
+        // any number of GPUs (F9).
+        int nsm_dev = 148;
+        CK(cudaDeviceGetAttribute(&nsm_dev, cudaDevAttrMultiProcessorCount, g.device));
+        if (g.seg_len > 0) {
+            g.seg_len_eff = g.seg_len;
+        } else {
+            const int64_t want = (nnz + (int64_t)nsm_dev * 128 - 1) / ((int64_t)nsm_dev * 128);
+            int sl = 8;
+            while (sl < want && sl < 256) sl *= 2;
+            g.seg_len_eff = sl;
+        }
+    }
     for (int n = 0; n < order; ++n) {
         ModeIndex& m = g.mi[n];
         CK(build_mode_csr(d_coords, nnz, order, n, dims[n], m, g.arena, g.scratch, S()));
@@ -882,8 +929,14 @@ int ptucker_init(const int32_t* coords, const void* vals, int32_t vals_dtype, in
         // kind-1 modes on the tensor cores: lanes in (i_s, length) order, one i_s per group
         const bool aux_groups = smode >= 0 && g.tc_table && g.use_tc && vals_dtype == PTUCKER_F32 &&
                                 find_update_kernel_tc(1, J) != nullptr;
-        CK(build_mode_sell(d_coords, d_vals, esz, nnz, order, n, J, g.seg_len, m.bounds[g.rank],
+        CK(build_mode_sell(d_coords, d_vals, esz, nnz, order, n, g.Jv.j[n], g.seg_len_eff, m.bounds[g.rank],
                            m.bounds[g.rank + 1], smode, m, g.arena, g.scratch, S(), aux_groups));
+        {   // most segments of one of this rank's rows (the heavy-row finalize picks its kernels by it)
+            int64_t mx = 0;
+            for (int64_t r = m.bounds[g.rank]; r < m.bounds[g.rank + 1]; ++r)
+                mx = std::max<int64_t>(mx, m.h_row_ptr[r + 1] - m.h_row_ptr[r]);
+            m.hmaxseg = (mx + g.seg_len_eff - 1) / g.seg_len_eff;
+        }
         pc.lap("SELL segments + scatter", S());
     }
     CK(A.alloc((void**)&g.lit_part, std::max<int64_t>(g.mi[0].nslices * 32, 1) * sizeof(double)));
@@ -930,6 +983,7 @@ int ptucker_open_peers(const uint8_t* handles, int32_t world) {
     if (!handles || world != g.world) return fail(PTUCKER_EINVAL, "handles of %d ranks expected", g.world);
     if (g.world - 1 > kMaxPeers) return fail(PTUCKER_EINVAL, "at most %d peers", kMaxPeers);
     close_peers();
+    invalidate_graph();
     int k = 0;
     for (int r = 0; r < world; ++r) {
         if (r == g.rank) continue;
@@ -965,8 +1019,8 @@ int ptucker_update_mode(int32_t n) {
                 pr.n = g.npeer;
                 for (int r = 0; r < g.npeer; ++r) pr.base[r] = g.peer_A[n][r];
             }
-            launch_heavy_finalize(m.nheavy, m.hrow, m.hnseg, m.hpbase, m.partials, m.hrec, g.J, g.lambda, g.A[n], g.esz,
-                                  g.lda, g.sse_row[n], g.d_fail, S(), pr);
+            launch_heavy_finalize(m.nheavy, m.hrow, m.hnseg, m.hpbase, m.partials, m.hrec, g.Jv.j[n], g.lambda, g.A[n], g.esz,
+                                  g.lda, g.sse_row[n], g.d_fail, S(), pr, m.hmaxseg);
             g.launches += 3;
             CK(cudaGetLastError());
             return PTUCKER_OK;
@@ -1007,9 +1061,40 @@ int ptucker_update_mode(int32_t n) {
 int ptucker_sweep(void) {
     int rc = require_init();
     if (rc) return rc;
+    // replay the captured sweep (one graph launch instead of ~2-5 launches per mode); kernel
+    // timing (time_kernels) needs the per-launch events, so it runs the sweep directly
+    const bool graphs = g.use_graph && !g.time_kernels;
+    if (graphs && g.graph_exec) {
+        CK(cudaGraphLaunch(g.graph_exec, S()));
+        g.launches += g.graph_launches;
+        g.last_fail_mode = g.N - 1;
+        g.sse_mode = g.N - 1;
+        return PTUCKER_OK;
+    }
+    cudaGraph_t graph = nullptr;
+    const int64_t l0 = g.launches;
+    if (graphs) CK(cudaStreamBeginCapture(S(), cudaStreamCaptureModeRelaxed));
     for (int n = 0; n < g.N; ++n) {
         rc = ptucker_update_mode(n);
-        if (rc) return rc;
+        if (rc) {
+            if (graphs) {
+                cudaStreamEndCapture(S(), &graph);
+                if (graph) cudaGraphDestroy(graph);
+                cudaGetLastError();
+            }
+            return rc;
+        }
+    }
+    if (graphs) {
+        CK(cudaStreamEndCapture(S(), &graph));
+        const cudaError_t e = cudaGraphInstantiate(&g.graph_exec, graph, 0);
+        cudaGraphDestroy(graph);
+        if (e != cudaSuccess) {
+            g.graph_exec = nullptr;
+            return fail(PTUCKER_ECUDA, "cudaGraphInstantiate: %s", cudaGetErrorString(e));
+        }
+        g.graph_launches = g.launches - l0;
+        CK(cudaGraphLaunch(g.graph_exec, S()));  // the capture recorded the work; run it once
     }
     return PTUCKER_OK;
 }
@@ -1035,7 +1120,7 @@ int ptucker_error_literal(double* out) {
         CK(tmp.alloc((void**)&d_A, kMaxN * sizeof(void*)));
         CK(tmp.alloc((void**)&d_r, (size_t)g.nnz * sizeof(double)));
         CK(cudaMemcpyAsync(d_A, g.A, kMaxN * sizeof(void*), cudaMemcpyHostToDevice, S()));
-        launch_predict(g.N, g.J, g.esz, g.G, (const void* const*)d_A, g.lda, g.coo_c, g.coo_v, g.nnz, d_r, 1, g.nsm,
+        launch_predict(g.N, g.Jv, g.esz, g.G, (const void* const*)d_A, g.lda, g.coo_c, g.coo_v, g.nnz, d_r, 1, g.nsm,
                        S(), g.mi[0].r0, g.mi[0].r1);
         launch_sum(d_r, g.nnz, g.red_part, g.red_out, S());
         g.launches += 3;
@@ -1073,9 +1158,10 @@ int ptucker_error(double* out) {
 int ptucker_orthogonalize(void) {
     int rc = require_init();
     if (rc) return rc;
-    const int J = g.J;
+    invalidate_graph();  // swaps G and Gtmp
+    const int J = g.J;  // max_n J_n (scratch sizes)
     for (int n = 0; n < g.N; ++n)
-        if (g.dims[n] < J) return fail(PTUCKER_EINVAL, "orthogonalize needs I_%d >= J", n);
+        if (g.dims[n] < g.Jv.j[n]) return fail(PTUCKER_EINVAL, "orthogonalize needs I_%d >= J_%d", n, n);
     if (!g.qd) {
         int64_t imax = 0;
         for (int n = 0; n < g.N; ++n) imax = std::max(imax, g.dims[n]);
@@ -1089,14 +1175,15 @@ int ptucker_orthogonalize(void) {
     rc = timed("qr", [&]() -> int {
         for (int n = 0; n < g.N; ++n) {
             const int64_t I = g.dims[n];
-            launch_gram(g.A[n], g.esz, false, I, J, g.lda, part, W, S());
-            launch_chol_upper(W, J, R1, g.d_qrfail, n + 1, S());
-            launch_apply_rinv(g.A[n], g.esz, g.lda, g.qd, 8, J, I, J, R1, S());
-            launch_gram(g.qd, 8, true, I, J, J, part, W, S());
-            launch_chol_upper(W, J, R2, g.d_qrfail, n + 1, S());
-            launch_apply_rinv(g.qd, 8, J, g.A[n], g.esz, g.lda, I, J, R2, S());
-            launch_mat_upper_mul(R2, R1, R, J, S());
-            launch_core_mode_product(g.G, g.Gtmp, g.esz, g.N, J, n, R, S());
+            const int Jn = g.Jv.j[n];
+            launch_gram(g.A[n], g.esz, false, I, Jn, g.lda, part, W, S());
+            launch_chol_upper(W, Jn, R1, g.d_qrfail, n + 1, S());
+            launch_apply_rinv(g.A[n], g.esz, g.lda, g.qd, 8, Jn, I, Jn, R1, S());
+            launch_gram(g.qd, 8, true, I, Jn, Jn, part, W, S());
+            launch_chol_upper(W, Jn, R2, g.d_qrfail, n + 1, S());
+            launch_apply_rinv(g.qd, 8, Jn, g.A[n], g.esz, g.lda, I, Jn, R2, S());
+            launch_mat_upper_mul(R2, R1, R, Jn, S());
+            launch_core_mode_product(g.G, g.Gtmp, g.esz, g.N, g.Jv, n, R, S());
             g.launches += 9;
             std::swap(g.G, g.Gtmp);
         }
@@ -1107,7 +1194,7 @@ int ptucker_orthogonalize(void) {
     g.sse_mode = -1;
     {
         int64_t gs = 1;
-        for (int n = 0; n < g.N; ++n) gs *= g.J;
+        for (int n = 0; n < g.N; ++n) gs *= g.Jv.j[n];
         CK(cudaMemsetAsync(g.d_present, 1, (size_t)gs, S()));  // G x_n R is dense again
         g.n_present = gs;
     }
@@ -1118,8 +1205,8 @@ int ptucker_get_factor(int32_t n, void* out) {
     int rc = require_init();
     if (rc) return rc;
     if (n < 0 || n >= g.N || !out) return fail(PTUCKER_EINVAL, "bad mode or buffer");
-    CK(cudaMemcpy2DAsync(out, (size_t)g.J * g.esz, g.A[n], (size_t)g.lda * g.esz, (size_t)g.J * g.esz, g.dims[n],
-                         cudaMemcpyDeviceToHost, S()));
+    const size_t rb = (size_t)g.Jv.j[n] * g.esz;  // I_n x J_n, row-major
+    CK(cudaMemcpy2DAsync(out, rb, g.A[n], (size_t)g.lda * g.esz, rb, g.dims[n], cudaMemcpyDeviceToHost, S()));
     return sync_and_check();
 }
 
@@ -1127,8 +1214,8 @@ int ptucker_set_factor(int32_t n, const void* in) {
     int rc = require_init();
     if (rc) return rc;
     if (n < 0 || n >= g.N || !in) return fail(PTUCKER_EINVAL, "bad mode or buffer");
-    CK(cudaMemcpy2DAsync(g.A[n], (size_t)g.lda * g.esz, in, (size_t)g.J * g.esz, (size_t)g.J * g.esz, g.dims[n],
-                         cudaMemcpyHostToDevice, S()));
+    const size_t rb = (size_t)g.Jv.j[n] * g.esz;
+    CK(cudaMemcpy2DAsync(g.A[n], (size_t)g.lda * g.esz, in, rb, rb, g.dims[n], cudaMemcpyHostToDevice, S()));
     g.sse_mode = -1;
     CK(cudaStreamSynchronize(S()));
     return PTUCKER_OK;
@@ -1139,7 +1226,7 @@ int ptucker_get_core(void* out) {
     if (rc) return rc;
     if (!out) return fail(PTUCKER_EINVAL, "null buffer");
     int64_t gsize = 1;
-    for (int n = 0; n < g.N; ++n) gsize *= g.J;
+    for (int n = 0; n < g.N; ++n) gsize *= g.Jv.j[n];
     CK(cudaMemcpyAsync(out, g.G, gsize * g.esz, cudaMemcpyDeviceToHost, S()));
     return sync_and_check();
 }
@@ -1149,7 +1236,7 @@ int ptucker_set_core(const void* in) {
     if (rc) return rc;
     if (!in) return fail(PTUCKER_EINVAL, "null buffer");
     int64_t gsize = 1;
-    for (int n = 0; n < g.N; ++n) gsize *= g.J;
+    for (int n = 0; n < g.N; ++n) gsize *= g.Jv.j[n];
     CK(cudaMemcpyAsync(g.G, in, gsize * g.esz, cudaMemcpyHostToDevice, S()));
     rc = rebuild_gp();
     if (rc) return rc;
@@ -1166,13 +1253,13 @@ namespace {
 int compute_core_scores(bool with_keys) {
     const int N = g.N, J = g.J;
     int64_t K1 = 1;
-    for (int n = 1; n < N; ++n) K1 *= J;
-    const int64_t gsize = K1 * J;
+    for (int n = 1; n < N; ++n) K1 *= g.Jv.j[n];
+    const int64_t gsize = K1 * g.Jv.j[0];
     // segment ranges of the outer reduction: ~256 segments each (enough blocks to fill the
     // GPU: 3.8 ms at a fixed 256 ranges for c5's 10^6 segments), at most 4096 ranges
     const int nsplit = (int)std::min<int64_t>(4096, std::max<int64_t>(256, g.mi[0].nslices * 32 / 256));
     const ModeIndex& m = g.mi[0];
-    if (!approx_shape_ok(N, J)) {  // generic shapes: U, V by definition over the device COO
+    if (g.ujn || !approx_shape_ok(N, J)) {  // generic shapes: U, V by definition over the device COO
         if (!g.coo_c) return fail(PTUCKER_EINVAL, "internal: no device COO for the generic Approx scores");
         if (!g.ax_UV) {
             CK(g.arena.alloc((void**)&g.ax_ptrs, kMaxN * sizeof(void*)));
@@ -1181,9 +1268,9 @@ int compute_core_scores(bool with_keys) {
             CK(cudaMemcpyAsync(g.ax_ptrs, g.A, kMaxN * sizeof(void*), cudaMemcpyHostToDevice, S()));
         }
         int rc = timed("approx_scores", [&]() -> int {
-            launch_predict(N, J, g.esz, g.G, (const void* const*)g.ax_ptrs, g.lda, g.coo_c, g.coo_v, g.nnz, g.ax_E, 0,
+            launch_predict(N, g.Jv, g.esz, g.G, (const void* const*)g.ax_ptrs, g.lda, g.coo_c, g.coo_v, g.nnz, g.ax_E, 0,
                            g.nsm, S());
-            launch_approx_literal(N, J, g.esz, (const void* const*)g.ax_ptrs, g.lda, g.coo_c, g.coo_v, g.ax_E, g.nnz,
+            launch_approx_literal(N, g.Jv, g.esz, (const void* const*)g.ax_ptrs, g.lda, g.coo_c, g.coo_v, g.ax_E, g.nnz,
                                   m.r0, m.r1, g.ax_UV, S());
             g.launches += 2;
             CK(cudaGetLastError());
@@ -1242,7 +1329,7 @@ int ptucker_core_scores(double* out) {
     rc = compute_core_scores(false);
     if (rc) return rc;
     int64_t gsize = 1;
-    for (int n = 0; n < g.N; ++n) gsize *= g.J;
+    for (int n = 0; n < g.N; ++n) gsize *= g.Jv.j[n];
     CK(cudaMemcpyAsync(out, g.ax_R, gsize * sizeof(double), cudaMemcpyDeviceToHost, S()));
     CK(cudaStreamSynchronize(S()));
     return PTUCKER_OK;
@@ -1255,7 +1342,7 @@ int ptucker_truncate_core(double p, int64_t* removed) {
     rc = compute_core_scores(true);
     if (rc) return rc;
     int64_t gsize = 1;
-    for (int n = 0; n < g.N; ++n) gsize *= g.J;
+    for (int n = 0; n < g.N; ++n) gsize *= g.Jv.j[n];
     const int64_t n = g.n_present;
     int64_t k = (int64_t)std::floor(p * (double)n);  // reading R29: floor(p |G|), at least one entry stays
     if (k > n - 1) k = n - 1;
@@ -1309,7 +1396,7 @@ int predict_common(const int32_t* coords, const void* vals, int vals_dtype, int6
         CK(tmp.alloc(&d_v, (size_t)n * g.esz));
         CK(cudaMemcpyAsync(d_v, vals, (size_t)n * g.esz, cudaMemcpyHostToDevice, S()));
     }
-    launch_predict(g.N, g.J, g.esz, g.G, (const void* const*)d_A, g.lda, d_c, d_v, n, d_o, rmse ? 1 : 0, g.nsm, S());
+    launch_predict(g.N, g.Jv, g.esz, g.G, (const void* const*)d_A, g.lda, d_c, d_v, n, d_o, rmse ? 1 : 0, g.nsm, S());
     g.launches += 1;
     CK(cudaGetLastError());
     if (rmse) {
@@ -1418,6 +1505,11 @@ int ptucker_info(char* buf, int32_t len) {
     if (!buf || len <= 0) return fail(PTUCKER_EINVAL, "bad buffer");
     std::string s = "{";
     char tmp[512];
+    {
+        std::string jl = "\"core_dims\": [";
+        for (int n = 0; n < g.N; ++n) jl += (n ? ", " : "") + std::to_string(g.Jv.j[n]);
+        s += jl + "], ";
+    }
     int comm_ranks = 0;  // size of the library's NCCL communicator (0: none)
     if (g.comm && ncclCommCount(g.comm, &comm_ranks) != ncclSuccess) comm_ranks = -1;
     snprintf(tmp, sizeof(tmp), "\"comm_ranks\": %d, \"peers\": %d, \"exchange\": \"%s\", ", comm_ranks, g.npeer,
@@ -1428,7 +1520,7 @@ int ptucker_info(char* buf, int32_t len) {
              "\"lambda\": %.17g, \"seg_len\": %d, \"rank\": %d, \"world\": %d, \"grid_update\": %d, "
              "\"threads_per_cta\": %d, \"smem_core_bytes\": %d, \"kernel_launches\": %lld, \"tensor_cores\": %s, \"generic\": %s, \"modes\": [",
              g.inited ? "true" : "false", g.N, g.J, g.prec == PTUCKER_F64 ? "f64" : "f32",
-             g.prec == PTUCKER_F64 ? "F64" : (policy_l64() == 0 ? "F32-A" : (policy_l64() == 1 ? "F32-B" : "F32-C")), (long long)g.nnz, g.lambda, g.seg_len,
+             g.prec == PTUCKER_F64 ? "F64" : (policy_l64() == 0 ? "F32-A" : (policy_l64() == 1 ? "F32-B" : "F32-C")), (long long)g.nnz, g.lambda, g.seg_len_eff,
              g.rank, g.world, g.grid_upd, kUpdThreads, g.gp_elems * g.esz, (long long)g.launches,
              (g.kern && g.kern != g.kern_alu) ? "true" : "false", g.generic ? "true" : "false");
     s += tmp;

@@ -293,7 +293,7 @@ __global__ void k_to_f64(const TS* in, double* out, int64_t n) {
 // x_hat from k_predict (xhat[]).  Entries are staged in shared memory per chunk.
 constexpr int kLitChunk = 128;
 template <typename TS>
-__global__ void __launch_bounds__(256) k_approx_literal(int N, int J, int64_t gsize, const TS* const* A, int lda,
+__global__ void __launch_bounds__(256) k_approx_literal(int N, const JDims jd, int64_t gsize, const TS* const* A, int lda,
                                                         const int32_t* coords, const TS* vals, const double* xhat,
                                                         int64_t n, int64_t row_lo, int64_t row_hi, double* UV) {
     __shared__ int32_t cs[kLitChunk * kMaxN];
@@ -304,8 +304,8 @@ __global__ void __launch_bounds__(256) k_approx_literal(int N, int J, int64_t gs
     {
         int64_t b = beta < gsize ? beta : 0;
         for (int m = N - 1; m >= 0; --m) {
-            bn[m] = (int)(b % J);
-            b /= J;
+            bn[m] = (int)(b % jd.j[m]);
+            b /= jd.j[m];
         }
     }
     double u = 0.0, v = 0.0;
@@ -336,11 +336,11 @@ __global__ void __launch_bounds__(256) k_approx_literal(int N, int J, int64_t gs
 
 }  // namespace
 
-void launch_approx_literal(int N, int J, int elem_bytes, const void* const* d_A, int lda, const int32_t* coords,
+void launch_approx_literal(int N, const JDims& J, int elem_bytes, const void* const* d_A, int lda, const int32_t* coords,
                            const void* vals, const double* xhat, int64_t n, int64_t row_lo, int64_t row_hi,
                            double* UV, cudaStream_t st) {
     int64_t gsize = 1;
-    for (int m = 0; m < N; ++m) gsize *= J;
+    for (int m = 0; m < N; ++m) gsize *= J.j[m];
     const unsigned grid = (unsigned)((gsize + 255) / 256);
     if (elem_bytes == 8)
         k_approx_literal<double><<<grid, 256, 0, st>>>(N, J, gsize, (const double* const*)d_A, lda, coords,

@@ -25,6 +25,17 @@ __host__ __device__ constexpr int gblk(int J, int elem_bytes) {
 }
 __host__ __device__ constexpr int ipow(int b, int e) { return e == 0 ? 1 : b * ipow(b, e - 1); }
 
+// Core dimensionality J_1..J_N (Alg. 2 input) for the kernels that accept
+// unequal J_n (generic path, predictions, QR core update, Approx literal scores).
+struct JDims {
+    int j[kMaxN] = {0};
+};
+inline JDims jdims_uniform(int N, int J) {
+    JDims d;
+    for (int m = 0; m < N; ++m) d.j[m] = J;
+    return d;
+}
+
 // Multi-GPU row exchange by push: the other ranks' replicas of A^(n),
 // opened from their CUDA IPC handles (ptucker_open_peers).  Every kernel that stores a
 // solved row of A^(n) also stores it into each peer replica (NVLink P2P stores), so the
@@ -41,8 +52,9 @@ __device__ __forceinline__ void push_row(const PeerRows& pr, const void* local, 
     const uint4* src = reinterpret_cast<const uint4*>(local);
     for (int q = 0; q < row_bytes / 16; ++q) {
         const uint4 v = src[q];
-        for (int r = 0; r < pr.n; ++r)
-            reinterpret_cast<uint4*>(static_cast<char*>(pr.base[r]) + row * row_bytes)[q] = v;
+#pragma unroll
+        for (int r = 0; r < kMaxPeers; ++r)  // constant indices: the parameter struct stays in param space
+            if (r < pr.n) reinterpret_cast<uint4*>(static_cast<char*>(pr.base[r]) + row * row_bytes)[q] = v;
     }
 }
 
@@ -106,7 +118,7 @@ int tc_kp(int J);  // K padding of the tensor-core A operand (floats per split r
 void launch_pack_rows10(const float* A, int64_t I, int lda, float* head, float* tail, cudaStream_t st);
 
 // Generic-order kernel (update_generic.cu): any N <= kMaxN, J <= 16, fp64; p.Gp = G in C order.
-void launch_update_generic(const void* params, int elem_bytes, int N, int J, int nsm, cudaStream_t st);
+void launch_update_generic(const void* params, int elem_bytes, int N, const JDims& J, int nsm, cudaStream_t st);
 bool generic_shape_ok(int N, int J);
 bool approx_shape_ok(int N, int J);  // approx.cu segment kernels instantiated for (N, J)
 // Alg. 4 on the device (approx.cu): scores from U, V; stable top-k truncation
@@ -117,7 +129,7 @@ cudaError_t launch_core_truncate(int64_t gsize, int64_t k, const uint64_t* key, 
                                  int64_t* idx_out, void* temp, size_t temp_bytes, int elem_bytes, void* G,
                                  uint8_t* present, cudaStream_t st);
 // U, V of Eq. 13 from their definition over a device COO (shapes without a compiled (N, J))
-void launch_approx_literal(int N, int J, int elem_bytes, const void* const* d_A, int lda, const int32_t* coords,
+void launch_approx_literal(int N, const JDims& J, int elem_bytes, const void* const* d_A, int lda, const int32_t* coords,
                            const void* vals, const double* xhat, int64_t n, int64_t row_lo, int64_t row_hi,
                            double* UV, cudaStream_t st);
 void launch_tc_split(const float* A, int64_t I, int lda, int J, float* hi, float* lo, cudaStream_t st);

@@ -173,13 +173,50 @@ __global__ void __launch_bounds__(256) k_heavy_sum(int64_t nheavy, int PW, const
 
 // JC > 0: the solve in registers (chol_solve<JC>, update.cuh); JC = 0: runtime J <= 16.
 template <typename T, int JC>
+__device__ __forceinline__ void heavy_solve_row(const double* rec, int J, int row, double lambda, T* An, int lda,
+                                                double* sse_row, int* fail, const PeerRows& peers);
+
+template <typename T, int JC>
 __global__ void __launch_bounds__(128) k_heavy_solve(int64_t nheavy, const int32_t* hrow, const double* recs, int J,
                                                      double lambda, T* An, int lda, double* sse_row, int* fail,
                                                      const PeerRows peers) {
     const int PW = J * (J + 1) / 2 + J + 1;
-    for (int64_t h = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; h < nheavy; h += (int64_t)gridDim.x * blockDim.x) {
-        const double* rec = recs + h * PW;
-        const int row = hrow[h];
+    for (int64_t h = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; h < nheavy; h += (int64_t)gridDim.x * blockDim.x)
+        heavy_solve_row<T, JC>(recs + h * PW, J, hrow[h], lambda, An, lda, sse_row, fail, peers);
+}
+
+// Heavy rows with at most kSmallSeg segments each, one launch (small tensors whose
+// automatic S makes most rows heavy: c1, c2): a warp per row, lane l summing components
+// l, l + 32, ... over the row's segments in order -- the additions of k_heavy_sum_small, so
+// the same bits -- into shared memory, then lane 0 solves from there.
+template <typename T, int JC>
+__global__ void __launch_bounds__(128) k_heavy_warp(int64_t nheavy, const int32_t* hrow, const int32_t* hnseg,
+                                                    const int64_t* hpbase, const double* partials, double lambda,
+                                                    T* An, int lda, double* sse_row, int* fail, const PeerRows peers) {
+    constexpr int PW = JC * (JC + 1) / 2 + JC + 1;
+    __shared__ double rec[4][PW];
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    for (int64_t h = (int64_t)blockIdx.x * 4 + w; h < nheavy; h += (int64_t)gridDim.x * 4) {
+        const int nseg = hnseg[h];
+        const double* src = partials + hpbase[h];
+        for (int q = lane; q < PW; q += 32) {
+            const double* sq = src + (int64_t)q * nseg;
+            double acc = 0.0;
+            for (int s = 0; s < nseg; ++s) acc += sq[s];
+            rec[w][q] = acc;
+        }
+        __syncwarp();
+        if (lane == 0) heavy_solve_row<T, JC>(rec[w], JC, hrow[h], lambda, An, lda, sse_row, fail, peers);
+        __syncwarp();
+    }
+}
+
+// Eq. 9 (Cholesky) for one heavy row from its summed record, the stored row, its SSE by
+// the identity of update.cuh, and the push into the peer replicas.
+template <typename T, int JC>
+__device__ __forceinline__ void heavy_solve_row(const double* rec, int J, int row, double lambda, T* An, int lda,
+                                                double* sse_row, int* fail, const PeerRows& peers) {
+    {
         double a[16];
         bool ok;
         if constexpr (JC > 0) {
@@ -194,15 +231,19 @@ __global__ void __launch_bounds__(128) k_heavy_solve(int64_t nheavy, const int32
         } else {
             ok = chol_solve_rt(rec, J, lambda, a);
         }
+        // compile-time J when instantiated for one (the fused record stays in registers)
+        const int Jr = JC > 0 ? JC : J;
         if (!ok) {
             atomicCAS(fail, 0, row + 1);
-            for (int j = 0; j < J; ++j) a[j] = 0.0;
+#pragma unroll
+            for (int j = 0; j < Jr; ++j) a[j] = 0.0;
         }
-        const int NB = J * (J + 1) / 2;
+        const int NB = Jr * (Jr + 1) / 2;
         const double* c = rec + NB;
-        double sse = rec[NB + J], ac = 0.0, aa = 0.0, ec = 0.0;
+        double sse = rec[NB + Jr], ac = 0.0, aa = 0.0, ec = 0.0;
         T* out = An + (int64_t)row * lda;
-        for (int j = 0; j < J; ++j) {
+#pragma unroll
+        for (int j = 0; j < Jr; ++j) {
             const T st = T(a[j]);
             out[j] = st;
             const double at = double(st);
@@ -218,8 +259,29 @@ __global__ void __launch_bounds__(128) k_heavy_solve(int64_t nheavy, const int32
 
 void launch_heavy_finalize(int64_t nheavy, const int32_t* hrow, const int32_t* hnseg, const int64_t* hpbase,
                            const double* partials, double* rec, int J, double lambda, void* An, int elem_bytes,
-                           int lda, double* sse_row, int* fail, cudaStream_t st, const PeerRows& peers) {
+                           int lda, double* sse_row, int* fail, cudaStream_t st, const PeerRows& peers,
+                           int64_t max_seg) {
     if (nheavy <= 0) return;
+    if (max_seg <= kSmallSeg && (J == 2 || J == 3 || J == 4 || J == 5 || J == 8 || J == 10)) {
+        const unsigned gf = (unsigned)std::min<int64_t>((nheavy + 3) / 4, 148 * 32);
+#define PT_HFF(JC)                                                                                               \
+    if (elem_bytes == 8)                                                                                         \
+        k_heavy_warp<double, JC><<<gf, 128, 0, st>>>(nheavy, hrow, hnseg, hpbase, partials, lambda, (double*)An,   \
+                                                     lda, sse_row, fail, peers);                                 \
+    else                                                                                                         \
+        k_heavy_warp<float, JC><<<gf, 128, 0, st>>>(nheavy, hrow, hnseg, hpbase, partials, lambda, (float*)An,     \
+                                                    lda, sse_row, fail, peers);
+        switch (J) {
+            case 2: PT_HFF(2) break;
+            case 3: PT_HFF(3) break;
+            case 4: PT_HFF(4) break;
+            case 5: PT_HFF(5) break;
+            case 8: PT_HFF(8) break;
+            default: PT_HFF(10) break;
+        }
+#undef PT_HFF
+        return;
+    }
     const int PW = J * (J + 1) / 2 + J + 1;
     const int64_t nitems = nheavy * PW;
     const unsigned g0 = (unsigned)std::min<int64_t>((nitems + 255) / 256, 148 * 32);
@@ -410,10 +472,11 @@ void launch_mat_upper_mul(const double* R2, const double* R1, double* R, int J, 
 
 // Eq. 2 with U = R (Eq. 8): G'[..k..] = sum_j R[k][j] G[..j..]   (fp64 accumulation)
 template <typename T>
-__global__ void k_core_mode_product(const T* G, T* Gout, int N, int J, int n, const double* R) {
+__global__ void k_core_mode_product(const T* G, T* Gout, int N, const JDims jd, int n, const double* R) {
     int64_t inner = 1, total = 1;
-    for (int m = n + 1; m < N; ++m) inner *= J;
-    for (int m = 0; m < N; ++m) total *= J;
+    const int J = jd.j[n];  // R is J_n x J_n
+    for (int m = n + 1; m < N; ++m) inner *= jd.j[m];
+    for (int m = 0; m < N; ++m) total *= jd.j[m];
     for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
         const int64_t in = t % inner;
         const int k = (int)((t / inner) % J);
@@ -424,10 +487,10 @@ __global__ void k_core_mode_product(const T* G, T* Gout, int N, int J, int n, co
     }
 }
 
-void launch_core_mode_product(const void* G, void* Gout, int elem_bytes, int N, int J, int n, const double* R,
-                              cudaStream_t st) {
+void launch_core_mode_product(const void* G, void* Gout, int elem_bytes, int N, const JDims& J, int n,
+                              const double* R, cudaStream_t st) {
     int64_t total = 1;
-    for (int m = 0; m < N; ++m) total *= J;
+    for (int m = 0; m < N; ++m) total *= J.j[m];
     const int grid = (int)((total + 255) / 256);
     if (elem_bytes == 8) k_core_mode_product<double><<<grid, 256, 0, st>>>((const double*)G, (double*)Gout, N, J, n, R);
     else k_core_mode_product<float><<<grid, 256, 0, st>>>((const float*)G, (float*)Gout, N, J, n, R);

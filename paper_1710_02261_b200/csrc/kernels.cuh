@@ -4,6 +4,8 @@
 
 #include <cstdint>
 
+#include "internal.cuh"
+
 namespace pt {
 
 // ---- init (Alg. 2 line 1; reading R2: counter-based SplitMix64) ----
@@ -14,7 +16,8 @@ void launch_permute_core(const void* G, void* Gp, int elem_bytes, int N, int J, 
 // ---- heavy rows: reduce the segment partials in a fixed order and solve (Eq. 9) ----
 void launch_heavy_finalize(int64_t nheavy, const int32_t* hrow, const int32_t* hnseg, const int64_t* hpbase,
                            const double* partials, double* rec, int J, double lambda, void* An, int elem_bytes,
-                           int lda, double* sse_row, int* fail, cudaStream_t st, const PeerRows& peers);
+                           int lda, double* sse_row, int* fail, cudaStream_t st, const PeerRows& peers,
+                           int64_t max_seg);  // max segments of a heavy row (<= 64: one fused launch)
 // ---- deterministic sum of x[0..n) (fixed 256-block tree) into *out (device) ----
 void launch_sum(const double* x, int64_t n, double* part256, double* out, cudaStream_t st);
 // ---- QR (Eq. 7) by CholeskyQR2 in fp64, and G <- G x_n R (Eq. 8) ----
@@ -24,7 +27,7 @@ void launch_chol_upper(const double* W, int J, double* R, int* fail, int fail_co
 void launch_apply_rinv(const void* A, int a_bytes, int lda_a, void* Q, int q_bytes, int lda_q, int64_t I, int J,
                        const double* R, cudaStream_t st);
 void launch_mat_upper_mul(const double* R2, const double* R1, double* R, int J, cudaStream_t st);
-void launch_core_mode_product(const void* G, void* Gout, int elem_bytes, int N, int J, int n, const double* R,
+void launch_core_mode_product(const void* G, void* Gout, int elem_bytes, int N, const JDims& J, int n, const double* R,
                               cudaStream_t st);
 // ---- small-mode precontraction for order-4 tensors with two small modes (smp.cu) ----
 void launch_smp_table2(const void* G, const void* As1, const void* As2, int lda, int64_t I1, int64_t I2, int J, int n,
@@ -42,7 +45,7 @@ void launch_approx_uv(int N, int J, int elem_bytes, int64_t nslices, const int64
                       const void* const* d_A, int lda, const void* G, double* G64, double* A0seg, double* W,
                       double* W2, double* Eslot, double* part, int nsplit, double* UV, int nsm, cudaStream_t st);
 // ---- Eq. 4 predictions of query coordinates (predict.cu) ----
-void launch_predict(int N, int J, int elem_bytes, const void* G, const void* const* d_A, int lda,
+void launch_predict(int N, const JDims& J, int elem_bytes, const void* G, const void* const* d_A, int lda,
                     const int32_t* coords, const void* vals, int64_t n, double* out, int residual_sq, int nsm,
                     cudaStream_t st, int64_t row_lo = 0, int64_t row_hi = INT64_MAX);
 // ---- index build helpers (index.cu) ----

@@ -2,6 +2,7 @@
 // shapes without a compiled (N, J) kernel: the order-scaling workload of P:1013-1014,
 // N = 3..10, J = 3, I = 100, |Omega| = 10^3, and any J outside {2,3,4,5,8,10}).
 //
+// Unequal core dimensions J_1..J_N (Alg. 2 input) run here too.
 // One thread per SELL-32 lane (row segment) of mode n, everything in fp64:
 //   delta(j) = sum over the other modes' indices k of G[beta(k, beta_n = j)] prod_{m != n} a^(m)_{i_m k_m}
 // (Eq. 12, evaluated as written: J^(N-1) products of N-1 factors, each
@@ -23,20 +24,23 @@ constexpr int kGJ = 16;  // max J of the generic kernel
 __device__ __forceinline__ int upi(int i, int j, int J) { return i * J - i * (i - 1) / 2 + (j - i); }
 
 template <typename TS>
-__global__ void __launch_bounds__(128) k_update_gen(const UpdateParams<TS> p, int N, int J) {
+__global__ void __launch_bounds__(128) k_update_gen(const UpdateParams<TS> p, int N, const JDims jd) {
     const int64_t nl = p.nslices * kWarp;
     const int n = p.n;
-    // stride of beta_m in the C-order core
+    const int J = jd.j[n];  // J_n: size of delta, B and c of this mode
+    // stride of beta_m in the C-order core, and J of the k-th other mode (ascending)
     int64_t stride[kMaxN];
+    int Jo[kMaxN - 1];
     {
         int64_t s = 1;
         for (int m = N - 1; m >= 0; --m) {
             stride[m] = s;
-            s *= J;
+            s *= jd.j[m];
         }
+        for (int k = 0; k < N - 1; ++k) Jo[k] = jd.j[k < n ? k : k + 1];
     }
     int64_t ncomb = 1;
-    for (int m = 0; m < N - 1; ++m) ncomb *= J;
+    for (int k = 0; k < N - 1; ++k) ncomb *= Jo[k];
     for (int64_t slot = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; slot < nl;
          slot += (int64_t)gridDim.x * blockDim.x) {
         const int row = p.lane_row[slot];
@@ -66,7 +70,7 @@ __global__ void __launch_bounds__(128) k_update_gen(const UpdateParams<TS> p, in
                 }
                 for (int j = 0; j < J; ++j) d[j] = fma((double)p.Gp[gb + j * stride[n]], prod, d[j]);
                 for (int k = N - 2; k >= 0; --k) {
-                    if (++kk[k] < J) break;
+                    if (++kk[k] < Jo[k]) break;
                     kk[k] = 0;
                 }
             }
@@ -125,15 +129,15 @@ __global__ void __launch_bounds__(128) k_update_gen(const UpdateParams<TS> p, in
             aa = fma(a[j], a[j], aa);
             ec = fma(at - a[j], c[j] - p.lambda * a[j], ec);
         }
-        p.sse_row[row] = sse + ac - p.lambda * aa + 2.0 * ec;
-        push_row(p.peers, out, row, p.lda * (int)sizeof(TS));  // SSE of the stored row (update.cuh)
+        p.sse_row[row] = sse + ac - p.lambda * aa + 2.0 * ec;  // SSE of the stored row (update.cuh)
+        push_row(p.peers, out, row, p.lda * (int)sizeof(TS));
     }
 }
 
 }  // namespace
 
 // The generic kernel reads the core in plain C order: p.Gp must be G itself.
-void launch_update_generic(const void* params, int elem_bytes, int N, int J, int nsm, cudaStream_t st) {
+void launch_update_generic(const void* params, int elem_bytes, int N, const JDims& J, int nsm, cudaStream_t st) {
     if (elem_bytes == 8) {
         const UpdateParams<double>& p = *reinterpret_cast<const UpdateParams<double>*>(params);
         const int64_t nl = p.nslices * kWarp;

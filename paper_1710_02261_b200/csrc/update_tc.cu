@@ -107,7 +107,22 @@ constexpr int kL0Conv = PT_L0_CONV;
 #ifndef PT_ACC_EARLY
 #define PT_ACC_EARLY 1
 #endif
-constexpr bool kAccEarly = PT_ACC_EARLY != 0;  // release the accumulator once its last TMEM chunk is in registers
+constexpr bool kAccEarly = PT_ACC_EARLY != 0;
+// 3xTF32 as ONE K-sweep: A = [a_hi | a_lo | a_hi] and B = [b_hi ; b_hi ; b_lo] along K
+// (3J columns padded to the K-step), so every MMA K-step carries useful products:
+// J = 10 takes 4 MMAs (K = 32) per tile instead of 3 x 2 (K = 16 each, 10 used)
+#ifndef PT_KCAT
+#define PT_KCAT 1
+#endif
+constexpr bool kKcat = PT_KCAT != 0;
+#ifndef PT_LOADER_SLEEP
+#define PT_LOADER_SLEEP 0
+#endif
+#ifndef PT_NE_SLEEP
+#define PT_NE_SLEEP 0
+#endif
+constexpr uint32_t kLoaderSleep = PT_LOADER_SLEEP;  // ns between polls of the loaders' slot waits (0: suspend-hint try_wait)
+constexpr uint32_t kNeSleep = PT_NE_SLEEP;          // ns between polls of the normal-equation warps' delta waits  // release the accumulator once its last TMEM chunk is in registers
 constexpr unsigned kXuMask = PT_XU_MASK;
 constexpr bool kA0Int = PT_A0_INT != 0;      // a0 converted by integer ops too
 constexpr int kBCH = PT_BCH;                      // level 0: TMEM chunks per load batch (registers)
@@ -202,6 +217,21 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
             : "memory");
     }
 }
+// Wait with a nanosleep back-off between polls: for the roles with slack (loaders far
+// ahead of the ring, normal-equation warps behind level 0), so their polling does not take
+// issue slots from the level-0 warps of the same sub-partition.
+__device__ __forceinline__ void mbar_wait_sleep(uint32_t bar, uint32_t parity, uint32_t ns) {
+    uint32_t done = 0;
+    while (true) {
+        asm volatile(
+            "{\n\t.reg .pred P1;\n\tmbarrier.test_wait.parity.shared::cta.b64 P1, [%1], %2;\n\tselp.b32 %0, 1, 0, P1;\n\t}\n"
+            : "=r"(done)
+            : "r"(bar), "r"(parity)
+            : "memory");
+        if (done) break;
+        __nanosleep(ns);
+    }
+}
 __device__ __forceinline__ void mbar_arrive(uint32_t bar) {
     asm volatile("{\n\t.reg .b64 st;\n\tmbarrier.arrive.release.cta.shared::cta.b64 st, [%0];\n\t}\n" ::"r"(bar) : "memory");
 }
@@ -267,17 +297,21 @@ template <int J>
 struct Shape {
     static constexpr int KP = (J + 7) / 8 * 8;             // K padded to the tf32 MMA K-step (8)
     static constexpr int KSTEPS = KP / 8;
+    static constexpr int KC = (3 * J + 7) / 8 * 8;          // concatenated K (kKcat): [hi | lo | hi]
+    static constexpr int KCSTEPS = KC / 8;
+    static constexpr int ACOLS = kKcat ? KC : 2 * KP;       // TMEM columns of one A buffer
     static constexpr int NP = (J * J + 15) / 16 * 16;      // N padded to 16 (M = 128)
     static constexpr int LD = factor_ld(J, 4);             // padded factor row (floats)
     static constexpr int NQ = LD / 4;                       // 16-byte chunks per factor row
     static constexpr int KQ = KP / 4;                       // 16-byte chunks per A row
     static constexpr int NCH = (J * J + 15) / 16;           // 16-column TMEM chunks holding t
-    // TMEM (all 512 columns): accumulators [b*NP, (b+1)*NP), A buffers at ACOL + a*2*KP (hi, then lo)
+    // TMEM (all 512 columns): accumulators [b*NP, (b+1)*NP), A buffers at ACOL + a*ACOLS
+    // (hi, then lo; or the concatenated [hi | lo | hi])
     static constexpr int ACOL = kNT * NP;
     static constexpr int TCOLS = 512;
-    static_assert(ACOL + kNA * 2 * KP <= TCOLS, "TMEM columns");
+    static_assert(ACOL + kNA * ACOLS <= TCOLS, "TMEM columns");
     // shared memory map (bytes)
-    static constexpr int B_BYTES = NP * KP * 4;             // one of B_hi / B_lo
+    static constexpr int B_BYTES = kKcat ? NP * KC * 4 / 2 : NP * KP * 4;  // one of B_hi / B_lo (kKcat: half of B)
     static constexpr int RSLOT = 2 * NQ * kE * 16 + kE * 4; // row ring slot: rows a0, a1 (chunk-major), x
     static constexpr int CSLOT = 3 * kE * 4;                // coordinate ring slot: c0, c1, x
     static constexpr int JD = (J + 1) / 2 * 2;              // delta doubles per lane (even: 16-byte pairs)
@@ -298,6 +332,24 @@ struct Shape {
     static constexpr int NBAR = 2 * kRing + 2 * kNT + 2 * kNA + 8 * kD + 1;  // + b_free (table mode)
     static constexpr int SMEM = OFF_BAR + NBAR * 8;
 };
+
+// kKcat: B = [b_hi ; b_hi ; b_lo] along K (Shape::KC rows of K), K-major canonical layout,
+// b = the core block G'[(k0, j)][k1] = T[k0*GB + k1*J + j]; rows c >= J^2 and K padding 0.
+template <int J>
+__device__ __forceinline__ void load_bcat(const float* T, float* sB, int t0, int nt) {
+    constexpr int NP = (J * J + 15) / 16 * 16, KC = (3 * J + 7) / 8 * 8, GB = gblk(J, 4);
+    for (int i = t0; i < NP * KC; i += nt) {
+        const int c = i / KC, k = i % KC;
+        float v = 0.f;
+        if (c < J * J && k < 3 * J) {
+            const int k1 = k % J;
+            const float g = T[(c / J) * GB + k1 * J + (c % J)];
+            const float hv = tf32_rna(g);
+            v = k < 2 * J ? hv : tf32_rna(g - hv);
+        }
+        sB[kmaj<KC>(c, k)] = v;
+    }
+}
 
 // Static serpentine assignment of groups (4 slices each) to CTAs.
 struct Sched {
@@ -380,6 +432,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_update_tc(const UpdateParams<fl
 
     // ---------------------------------------------------------------- setup
     // B = core (hi/lo tf32 split), K-major: Bt[(k0, j)][k1] = G'[k0][k1][j]
+    if constexpr (kKcat) {
+        load_bcat<J>(p.Gp, sBhi, threadIdx.x, kThreads);
+    } else {
     for (int i = threadIdx.x; i < NP * KP; i += kThreads) {
         const int c = i / KP, k1 = i % KP;
         float v = 0.f;
@@ -387,6 +442,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_update_tc(const UpdateParams<fl
         const float hv = tf32_rna(v);
         sBhi[kmaj<KP>(c, k1)] = hv;
         sBlo[kmaj<KP>(c, k1)] = tf32_rna(v - hv);
+    }
     }
     if constexpr (NQ == 3) {
         // packed J = 10 gathers write 8 of chunk 2's 16 bytes: the rest (row padding) stays zero
@@ -515,7 +571,10 @@ __global__ void __launch_bounds__(kThreads, 1) k_update_tc(const UpdateParams<fl
                 const int s = (int)(k % kRing), cs = (int)(k % kCRing);
                 const bool tl = trl && k >= 64 && k < 128;
                 if (tl) trl[(k - 64) * 8 + 0] = clock64();
-                if (k >= (uint32_t)kRing) mbar_wait(raw_empty(s), ((k / kRing) + 1) & 1);
+                if (k >= (uint32_t)kRing) {
+                    if constexpr (kLoaderSleep > 0) mbar_wait_sleep(raw_empty(s), ((k / kRing) + 1) & 1, kLoaderSleep);
+                    else mbar_wait(raw_empty(s), ((k / kRing) + 1) & 1);
+                }
                 if (tl) trl[(k - 64) * 8 + 1] = clock64();
                 cp_async_wait<kCPref - 1>();  // coordinates of tile k (committed kCPref groups ago)
                 if (tl) trl[(k - 64) * 8 + 2] = clock64();
@@ -606,12 +665,14 @@ __global__ void __launch_bounds__(kThreads, 1) k_update_tc(const UpdateParams<fl
                 (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(NP >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
             // B descriptors (K-major, SWIZZLE_NONE; LBO: next 16-byte K chunk = next core
             // matrix (128 B); SBO: next 8 rows), per K-step of 8
-            uint64_t dbhi[SH::KSTEPS], dblo[SH::KSTEPS];
+            uint64_t dbhi[SH::KSTEPS], dblo[SH::KSTEPS], dbc[SH::KCSTEPS];
 #pragma unroll
             for (int ks = 0; ks < SH::KSTEPS; ++ks) {
                 dbhi[ks] = umma_desc(smem_u32(sBhi) + ks * 256, 128, KP * 32);
                 dblo[ks] = umma_desc(smem_u32(sBlo) + ks * 256, 128, KP * 32);
             }
+#pragma unroll
+            for (int ks = 0; ks < SH::KCSTEPS; ++ks) dbc[ks] = umma_desc(smem_u32(sBhi) + ks * 256, 128, SH::KC * 32);
             // optional trace (tools/trace_tc.py): CTA 0, tiles [64, 128)
 #ifdef PT_TRACE
             long long* const trm = (p.trace && blockIdx.x == 0) ? p.trace + 4 * 512 : nullptr;
@@ -637,6 +698,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_update_tc(const UpdateParams<fl
                         mbar_wait(b_free, bpar);
                         bpar ^= 1u;
                         const float* T = p.Gp + (int64_t)aux * p.aux_stride;
+if constexpr (kKcat) {
+                            load_bcat<J>(T, sBhi, lane, kWarp);
+                        } else {
 #pragma unroll 8
                         for (int i = lane; i < NP * KP; i += kWarp) {
                             const int c = i / KP, k1 = i % KP;
@@ -645,6 +709,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_update_tc(const UpdateParams<fl
                             const float hv = tf32_rna(v);
                             sBhi[kmaj<KP>(c, k1)] = hv;
                             sBlo[kmaj<KP>(c, k1)] = tf32_rna(v - hv);
+                        }
                         }
                         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
                         __syncwarp();
@@ -662,18 +727,30 @@ __global__ void __launch_bounds__(kThreads, 1) k_update_tc(const UpdateParams<fl
                 if (lane == 0) {
                 // 3xTF32: lo*hi, hi*lo, hi*hi (small terms first)
                 const uint32_t d = tmem + b * NP;
-                const uint32_t ahi = tmem + SH::ACOL + a * 2 * KP, alo = ahi + KP;
+                const uint32_t ahi = tmem + SH::ACOL + a * SH::ACOLS;
+                [[maybe_unused]] const uint32_t alo = ahi + KP;
                 uint32_t acc = 0;
 #ifdef PT_EXP_NOMMA  // experiment (wrong results): one MMA per tile instead of 3 x KSTEPS
                 mma_tf32_ta(d, ahi, dbhi[0], idesc, 0);
 #else
+                // (braces around both branches: a discarded `else` followed by a #pragma-annotated
+                // loop once swallowed the next statement, the accumulator commit, and the kernel hung)
+                if constexpr (kKcat) {
 #pragma unroll
-                for (int pr = 0; pr < 3; ++pr)
-#pragma unroll
-                    for (int ks = 0; ks < SH::KSTEPS; ++ks) {
-                        mma_tf32_ta(d, (pr == 0 ? alo : ahi) + 8 * ks, pr == 1 ? dblo[ks] : dbhi[ks], idesc, acc);
+                    for (int ks = 0; ks < SH::KCSTEPS; ++ks) {
+                        mma_tf32_ta(d, ahi + 8 * ks, dbc[ks], idesc, acc);
                         acc = 1;
                     }
+                } else {
+#pragma unroll
+                    for (int pr = 0; pr < 3; ++pr) {
+#pragma unroll
+                        for (int ks = 0; ks < SH::KSTEPS; ++ks) {
+                            mma_tf32_ta(d, (pr == 0 ? alo : ahi) + 8 * ks, pr == 1 ? dblo[ks] : dbhi[ks], idesc, acc);
+                            acc = 1;
+                        }
+                    }
+                }
 #endif
                 asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
                                  acc_full(b))
@@ -742,8 +819,22 @@ __global__ void __launch_bounds__(kThreads, 1) k_update_tc(const UpdateParams<fl
                     reinterpret_cast<uint4*>(sb)[q * kWarp + lane] = *rowc(s, 0, q, te);
                 reinterpret_cast<float*>(sb + NQ * kWarp * 16)[lane] = *rowx(s, te);
             }
-            const uint32_t ta = tm_lane + SH::ACOL + (k % kNA) * 2 * KP;
-            if constexpr (KP == 16) {
+            const uint32_t ta = tm_lane + SH::ACOL + (k % kNA) * SH::ACOLS;
+            if constexpr (kKcat) {
+                // [a_hi | a_lo | a_hi | 0] over KC columns, stored 16 (or 8) at a time
+                uint32_t v[SH::KC];
+#pragma unroll
+                for (int i = 0; i < SH::KC; ++i)
+                    v[i] = i < J ? hi[i] : (i < 2 * J ? lo[i - J] : (i < 3 * J ? hi[i - 2 * J] : 0u));
+#pragma unroll
+                for (int c0 = 0; c0 < SH::KC; c0 += 16) {
+                    uint32_t w[16];
+#pragma unroll
+                    for (int i = 0; i < 16; ++i) w[i] = c0 + i < SH::KC ? v[c0 + i] : 0u;
+                    if (c0 + 16 <= SH::KC) tmem_st16(ta + c0, w);
+                    else tmem_st8(ta + c0, w);
+                }
+            } else if constexpr (KP == 16) {
                 tmem_st16(ta, hi);
                 tmem_st16(ta + KP, lo);
             } else {
@@ -947,7 +1038,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_update_tc(const UpdateParams<fl
                 const int ds = (int)(k % kD);
                 markn(k, 0);
                 markn(k, 1);
-                mbar_wait(d_full(w4, ds), (k / kD) & 1);
+                if constexpr (kNeSleep > 0) mbar_wait_sleep(d_full(w4, ds), (k / kD) & 1, kNeSleep);
+                else mbar_wait(d_full(w4, ds), (k / kD) & 1);
                 markn(k, 2);
                 double dd[J];
 #pragma unroll

@@ -26,6 +26,7 @@ def main():
     cfg = synth.small(name, scale)
     coords, vals = synth.generate(cfg)
     N = len(cfg.dims)
+    pt.ptucker_set_option("seg_len", -1)
     pt.ptucker_set_option("emulate_world", world)
     pt.ptucker_set_option("emulate_rank", rank)
     pt.ptucker_init(coords, vals, cfg.dims, [cfg.J] * N, cfg.lam, 0)

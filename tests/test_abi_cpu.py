@@ -67,7 +67,7 @@ def test_validation_without_gpu(pt):
         pt.ptucker_init(c8, v, [2] * 8, [10] * 8, 0.1, 0)        # core 10^8 > 2^26 entries
     assert e.value.code == pt.PTUCKER_EINVAL
     with pytest.raises(pt.PTuckerError) as e:
-        pt.ptucker_init(c, v, [2, 2, 2], [2, 3, 2], 0.1, 0)      # unequal J
+        pt.ptucker_init(c, v, [2, 2, 2], [2, 17, 2], 0.1, 0)     # a J_n above 16 (unequal J_n are valid)
     assert e.value.code == pt.PTUCKER_EINVAL
     with pytest.raises(pt.PTuckerError) as e:
         pt.ptucker_init(c, np.array([1, np.nan, 1, 1], np.float32), [2, 2, 2], [2, 2, 2], 0.1, 0)

@@ -1,5 +1,5 @@
 """Parity at BASELINE.json's full sizes, in the launch configuration bench.py times
-(default options: tensor cores for order-3 fp32, seg_len 256, F32-B): one mode
+(default options: tensor cores for order-3 fp32, automatic seg_len, F32-B): one mode
 update from the init state, checked on sampled rows that the FP64 oracle can
 compute one by one, plus size-independent properties (fused vs literal error).
 
@@ -37,7 +37,7 @@ def test_fullsize_sampled_rows(pt, orc, name, policy):
     coords, vals = synth.generate(cfg)
     N, J = len(cfg.dims), cfg.J
     pt.ptucker_finalize()
-    pt.ptucker_set_option("seg_len", 256)
+    pt.ptucker_set_option("seg_len", -1)   # automatic, as bench.py runs it
     pt.ptucker_init(coords, vals, cfg.dims, [J] * N, cfg.lam, cfg.seed)
     pt.ptucker_set_option("policy", policy)
     info = pt.ptucker_info()

@@ -38,7 +38,7 @@ def pt():
 def _init(pt, cfg):
     coords, vals = synth.generate(cfg)
     pt.ptucker_finalize()
-    pt.ptucker_set_option("seg_len", 256)
+    pt.ptucker_set_option("seg_len", -1)   # automatic, as bench.py runs it
     pt.ptucker_init(coords, vals, cfg.dims, [cfg.J] * len(cfg.dims), cfg.lam, cfg.seed)
     return coords, vals
 

@@ -116,18 +116,24 @@ def test_init_and_index_bit_exact(pt, orc, name, scale):
 
 
 # ---------------------------------------------------------------- one mode update from an identical state
-def test_mode_update_f64_c1(pt, orc):
+@pytest.mark.parametrize("seg", [256, -1])
+def test_mode_update_f64_c1(pt, orc, seg):
+    """c1 at full size; seg = -1 is the automatic S bench.py runs (8 for c1: every row is
+    a multi-segment heavy row, reduced by the fused heavy-row finalize)."""
     cfg = synth.config("c1")
-    coords, vals = init_cfg(pt, cfg)
+    coords, vals = init_cfg(pt, cfg, seg_len=seg)
     t = orc.Tensor(coords, vals, cfg.dims)
     mode_update_parity(pt, orc, t, cfg, 1e-10, sweeps=0)        # init state
     mode_update_parity(pt, orc, t, cfg, 1e-10, sweeps=2)        # mid-trajectory state
+    if seg < 0:
+        assert pt.ptucker_info()["seg_len"] == 8
 
 
 # c3 at scale 0.005 (690 x 135 x 21 x 24) exercises both small-mode tables (kind 2 for
 # modes 0/1, kind 1 for modes 2/3); 0.002 (276 x 54 x 21 x 24) the plain order-4 kernel
 @pytest.mark.parametrize("name,scale,seg", [("c2", 0.01, 256), ("c3", 0.002, 256), ("c3", 0.005, 256),
-                                            ("c3", 0.005, 7), ("c4", 0.001, 256), ("c5", 0.0001, 256)])
+                                            ("c3", 0.005, 7), ("c4", 0.001, 256), ("c5", 0.0001, 256),
+                                            ("c2", 0.05, -1), ("c5", 0.0005, -1)])
 def test_mode_update_f32(pt, orc, name, scale, seg):
     cfg = synth.small(name, scale)
     coords, vals = init_cfg(pt, cfg, seg_len=seg)
@@ -362,3 +368,33 @@ def test_partitioned_rows_bit_identical(pt, orc, world):
     for n in range(4):
         assert np.array_equal(got[n], ref[n]), n
     assert abs(sse - ref_sse) <= 1e-9 * ref_sse
+
+
+@pytest.mark.parametrize("name,scale", [("c1", 1.0), ("c3", 0.005), ("c5", 0.0005)])
+def test_graph_sweep_bit_identical(pt, orc, name, scale):
+    """ptucker_sweep replays a captured CUDA graph of the sweep (option graph, default on):
+    the same factors and errors bit for bit as direct launches, also across the events that
+    drop the graph (an option change, Approx truncation, QR which swaps the core buffers)."""
+    cfg = synth.config(name) if scale == 1.0 else synth.small(name, scale)
+    N = len(cfg.dims)
+    runs = {}
+    for graph in (0, 1):
+        init_cfg(pt, cfg, seg_len=-1)
+        pt.ptucker_set_option("graph", graph)
+        errs = []
+        for it in range(4):
+            pt.ptucker_sweep()
+            errs.append(pt.ptucker_error())
+            if it == 1:
+                pt.ptucker_truncate_core(0.2)
+            if it == 2:
+                pt.ptucker_set_option("l0_group", 1)     # an option change drops the graph
+        pt.ptucker_orthogonalize()
+        pt.ptucker_sweep()
+        errs.append(pt.ptucker_error())
+        runs[graph] = ([pt.ptucker_get_factor(n).copy() for n in range(N)], pt.ptucker_get_core().copy(), errs)
+    pt.ptucker_set_option("graph", 1)
+    for n in range(N):
+        assert np.array_equal(runs[0][0][n], runs[1][0][n]), n
+    assert np.array_equal(runs[0][1], runs[1][1])
+    assert runs[0][2] == runs[1][2]

@@ -39,6 +39,7 @@ def test_push_exchange_bit_identical(tmp_path, name, scale, world):
     coords, vals = synth.generate(cfg)
     N = len(cfg.dims)
     pt.ptucker_finalize()
+    pt.ptucker_set_option("seg_len", -1)      # the workers' (default) automatic S
     pt.ptucker_init(coords, vals, cfg.dims, [cfg.J] * N, cfg.lam, 0)
     for _ in range(sweeps):
         pt.ptucker_sweep()
