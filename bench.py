@@ -551,6 +551,8 @@ def main():
     ap.add_argument("--l0-group", type=int, default=1, choices=[1, 2, 5], help="tensor-core level-0 grouping (1 = fp64 per term, g = fp32 partial sums of g terms)")
     ap.add_argument("--exchange", default="push", choices=["push", "nccl"],
                     help="multi-GPU replica refresh: rows pushed by the kernels over NVLink, or NCCL all-gather-v")
+    ap.add_argument("--dtype", default=None, choices=["f32", "f64"],
+                    help="storage precision override (default: the config's; f64 = the FP64 mode)")
     ap.add_argument("--approx", type=float, default=0.0,
                     help="P-Tucker-Approx: truncate the core by rate p after every iteration (0 = P-Tucker)")
     ap.add_argument("--ref-seconds", type=float, default=12.0, help="oracle seconds per sampled step (upper bound)")
@@ -559,6 +561,9 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
     cfg = synth.config(args.config) if args.scale == 1.0 else synth.small(args.config, args.scale)
+    if args.dtype:   # FP64 mode of a config (values, factors and core stored in fp64: 1e-10 parity class)
+        import dataclasses
+        cfg = dataclasses.replace(cfg, dtype=args.dtype)
     if args.impl == "reference":
         run_reference(args, cfg)
     else:

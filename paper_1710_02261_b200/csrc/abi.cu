@@ -275,10 +275,12 @@ UpdateParams<TS> make_params(int n, bool literal) {
         if (k == n) continue;
         p.sc[l] = m.sc[l];
         p.A[l] = (const TS*)g.A[k];
+        p.dim_other[l] = g.dims[k];
         ++l;
     }
     p.sv = (const TS*)m.sv;
     p.An = (TS*)g.A[n];
+    p.dim_n = g.dims[n];
     p.lda = g.lda;
     p.Gp = (const TS*)g.Gp[n];
     p.gp_elems = g.gp_elems;
@@ -339,6 +341,8 @@ int launch_update_kernel(int n, bool literal) {
             p.sc[1] = g.mi[n].sc[sp.is2];
             p.A[0] = (const TSp*)g.A[sp.r];
             p.A[1] = (const TSp*)g.A[sp.s2];
+            p.dim_other[0] = g.dims[sp.r];
+            p.dim_other[1] = g.dims[sp.s2];
             p.Gp = (const TSp*)g.smp_T;
             p.gp_elems = (int)sp.elems;
             p.aux_stride = (int64_t)g.J * GBk;

@@ -25,6 +25,19 @@ __host__ __device__ constexpr int gblk(int J, int elem_bytes) {
 }
 __host__ __device__ constexpr int ipow(int b, int e) { return e == 0 ? 1 : b * ipow(b, e - 1); }
 
+// Checked builds (-DPT_CHECKED, tools/checked_build.sh; compute-sanitizer is closed on this
+// pool): index and row bounds asserted in the kernels, a violation traps the kernel.
+#ifdef PT_CHECKED
+#define PT_CHK(c)           \
+    do {                    \
+        if (!(c)) __trap(); \
+    } while (0)
+#else
+#define PT_CHK(c) \
+    do {          \
+    } while (0)
+#endif
+
 // Core dimensionality J_1..J_N (Alg. 2 input) for the kernels that accept
 // unequal J_n (generic path, predictions, QR core update, Approx literal scores).
 struct JDims {
@@ -92,6 +105,8 @@ struct UpdateParams {
     int l0_group;                 // tensor-core kernel: level-0 terms summed in fp32 before fp64 (1 or 2)
     int rows_l1;                  // gather factor rows through L1 (skewed gathered modes: hot rows)
     PeerRows peers;               // multi-GPU push: the other ranks' replicas of A^(n) (n = 0: none)
+    int64_t dim_other[kMaxN - 1]; // I of the other modes (same order as A[]) -- bounds checks
+    int64_t dim_n;                // I_n
 };
 
 using UpdateLauncher = void (*)(const void* params, bool literal, int grid, cudaStream_t st);

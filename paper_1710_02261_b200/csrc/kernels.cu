@@ -241,6 +241,7 @@ __device__ __forceinline__ void heavy_solve_row(const double* rec, int J, int ro
         const int NB = Jr * (Jr + 1) / 2;
         const double* c = rec + NB;
         double sse = rec[NB + Jr], ac = 0.0, aa = 0.0, ec = 0.0;
+        PT_CHK(row >= 0);
         T* out = An + (int64_t)row * lda;
 #pragma unroll
         for (int j = 0; j < Jr; ++j) {

@@ -111,6 +111,8 @@ __global__ void __launch_bounds__(kUpdThreads, 1) k_update_smp2(const UpdatePara
             a_ = __ldg(p.sc[is1] + idx);
             b_ = __ldg(p.sc[is2] + idx);
             x_ = __ldg(p.sv + idx);
+            PT_CHK(r_ >= 0 && r_ < p.dim_other[ir] && a_ >= 0 && a_ < p.dim_other[is1] && b_ >= 0 &&
+                   b_ < p.dim_other[is2]);
         };
         if (iters > 0) {
             load(0, cr, c1, c2, x);
@@ -175,6 +177,7 @@ __global__ void __launch_bounds__(kUpdThreads, 1) k_update_smp2(const UpdatePara
 #pragma unroll
                 for (int j = 0; j < J; ++j) a[j] = 0.0;
             }
+            PT_CHK(row < p.dim_n);
             TS* out = p.An + (int64_t)row * p.lda;
             double sse = s2, ac = 0.0, aa = 0.0, ec = 0.0;
 #pragma unroll

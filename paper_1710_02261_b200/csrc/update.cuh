@@ -150,13 +150,30 @@ __device__ __forceinline__ void compute_delta(const TS* __restrict__ g, const TF
     } else if constexpr (N == 3) {
 #pragma unroll
         for (int j = 0; j < J; ++j) d[j] = TO(0);
-#pragma unroll
-        for (int k = 0; k < J; ++k) {
+        auto level0 = [&](int k) {
             TF t[J];
             ttv_inner<TS, J, TF, TF>(g + k * GB, a_in, t);
             const TO ak = TO(a_out[0][k]);
 #pragma unroll
             for (int j = 0; j < J; ++j) d[j] = fma(ak, widen<TO>(t[j], j), d[j]);
+        };
+        if constexpr (sizeof(TS) == 8 && J >= 8) {
+            // fp64 with J >= 8: the fully unrolled k loop held ~2 core blocks of doubles beside
+            // the 55-double B and spilled 472 bytes (round 1); one block at a time does not.
+            // a0[k] comes from the staged row (a register array indexed by a runtime k would
+            // go to local memory)
+            constexpr int VN = Vec16<TS>::n;
+#pragma unroll 1
+            for (int k = 0; k < J; ++k) {
+                TF t[J];
+                ttv_inner<TS, J, TF, TF>(g + k * GB, a_in, t);
+                const TO ak = TO(a0row[(k / VN) * (kWarp * VN) + (k % VN)]);
+#pragma unroll
+                for (int j = 0; j < J; ++j) d[j] = fma(ak, widen<TO>(t[j], j), d[j]);
+            }
+        } else {
+#pragma unroll
+            for (int k = 0; k < J; ++k) level0(k);
         }
     } else {
         constexpr int sub = ipow(J, N - 3) * GB;
@@ -309,6 +326,7 @@ __global__ void __launch_bounds__(kUpdThreads, upd_min_blocks(J, (int)sizeof(TS)
     auto issue_rows = [&](int st, const int (&crd)[NR]) {
 #pragma unroll
         for (int k = 0; k < NR; ++k) {
+            PT_CHK(crd[k] >= 0 && crd[k] < p.dim_other[k]);
             const char* src = reinterpret_cast<const char*>(p.A[k] + (int64_t)crd[k] * p.lda);
 #pragma unroll
             for (int q = 0; q < NQ; ++q) cp_async16(stg + ((st * NR + k) * NQ + q) * kWarp, src + 16 * q);
@@ -431,6 +449,7 @@ __global__ void __launch_bounds__(kUpdThreads, upd_min_blocks(J, (int)sizeof(TS)
 #pragma unroll
                     for (int j = 0; j < J; ++j) a[j] = 0.0;
                 }
+                PT_CHK(row < p.dim_n);
                 TS* out = p.An + (int64_t)row * p.lda;
                 double sse = s2, ac = 0.0, aa = 0.0, ec = 0.0;
                 TS st[J];

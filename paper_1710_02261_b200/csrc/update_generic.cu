@@ -54,7 +54,10 @@ __global__ void __launch_bounds__(128) k_update_gen(const UpdateParams<TS> p, in
             const int64_t es = base + (int64_t)e * kWarp;
             const double x = (double)p.sv[es];
             const TS* rows[kMaxN - 1];
-            for (int k = 0; k < N - 1; ++k) rows[k] = p.A[k] + (int64_t)p.sc[k][es] * p.lda;
+            for (int k = 0; k < N - 1; ++k) {
+                PT_CHK(p.sc[k][es] >= 0 && p.sc[k][es] < p.dim_other[k]);
+                rows[k] = p.A[k] + (int64_t)p.sc[k][es] * p.lda;
+            }
             double d[kGJ];
             for (int j = 0; j < J; ++j) d[j] = 0.0;
             // iterate the other modes' indices k_0..k_{N-2} (ascending mode order) as a counter
@@ -118,6 +121,7 @@ __global__ void __launch_bounds__(128) k_update_gen(const UpdateParams<TS> p, in
             atomicCAS(p.fail, 0, row + 1);
             for (int j = 0; j < J; ++j) a[j] = 0.0;
         }
+        PT_CHK(row < p.dim_n);
         TS* out = p.An + (int64_t)row * p.lda;
         double sse = s2, ac = 0.0, aa = 0.0, ec = 0.0;
         for (int j = 0; j < J; ++j) {

@@ -620,6 +620,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_update_tc(const UpdateParams<fl
                     const char* r0 = reinterpret_cast<const char*>(p.A[0]);
                     const char* r1 = reinterpret_cast<const char*>(p.A[1]);
 #else
+                    PT_CHK((int)*crd(cs, 0, u) >= 0 && (int)*crd(cs, 0, u) < p.dim_other[0]);
+                    PT_CHK((int)*crd(cs, 1, u) >= 0 && (int)*crd(cs, 1, u) < p.dim_other[1]);
                     const char* r0 = reinterpret_cast<const char*>(p.A[0] + (int64_t)(int)*crd(cs, 0, u) * p.lda);
                     const char* r1 = reinterpret_cast<const char*>(p.A[1] + (int64_t)(int)*crd(cs, 1, u) * p.lda);
 #endif
@@ -982,7 +984,7 @@ if constexpr (kKcat) {
 #pragma unroll
                     for (int j = 0; j < J; ++j) a[j] = 0.0;
                 }
-                float* out = p.An + (int64_t)g.row * p.lda;
+                float* out = p.An + (int64_t)g.row * p.lda;  // (no PT_CHK here: it made the 192-register role spill)
                 double sse = s2, ac = 0.0, aa = 0.0, ec = 0.0;
                 float stv[SH::LD];
 #pragma unroll
