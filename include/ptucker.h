@@ -196,6 +196,13 @@ int ptucker_get_partition(int32_t n, int64_t* bounds);
  *  "emulate_world", "emulate_rank"  (before init, no communicator): build and update only
  *                 this rank's row blocks of a `world`-way partition, without the exchange
  *                 (tests of the partitioned path on one GPU)
+ *  "cache"        1 = P-Tucker-Cache (Alg. 3 TOP branch; set BEFORE init): a cache
+ *                 table Pres of |Omega| x |G| fp64 products G_beta prod_k a^(k) (lines 1-4), delta
+ *                 read from it (line 12; a factor value of exactly 0 takes the product loop,
+ *                 P:639), the table rescaled by a_new / a_old after every mode (lines 16-19) and
+ *                 rebuilt after set_factor / set_core / QR / truncation.  Runs on the generic
+ *                 path; ERESOURCE at init when |Omega| |G| 8 bytes exceed 80% of free device
+ *                 memory (c1: 10 MB, c2: 8 GB; c3-c5 do not fit).  0 = P-Tucker (default)
  *  "exchange"     multi-GPU replica refresh: 1 = push from the kernels when peers are open
  *                 (default), 0 = NCCL all-gather-v (grouped broadcasts) after each mode
  *  "graph"        1 = ptucker_sweep records its launches once as a CUDA graph and replays it

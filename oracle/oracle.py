@@ -61,6 +61,9 @@ def lib():
             "or_truncate": (i64, [i64, P, P, P, f64]),
             "or_predict_many": (None, [C.c_int, P, P, P, P, P, i64, P]),
             "or_test_rmse": (f64, [C.c_int, P, P, P, P, P, P, i64]),
+            "or_pres_init": (None, [C.c_int, P, P, P, P, P, i64, P, C.c_int]),
+            "or_delta_cache": (None, [C.c_int, P, P, P, P, P, P, C.c_int, P]),
+            "or_update_mode_cache": (C.c_int, [C.c_int, P, P, P, P, P, P, i64, C.c_int, P, P, f64, P, C.c_int]),
         }
         for name, (res, args) in sig.items():
             fn = getattr(_lib, name)
@@ -359,3 +362,33 @@ def run(t: Tensor, m: Model, lam: float, max_iters: int, tol: float, approx_p: f
         globals()["orthogonalize"](m)
         present[:] = 1
     return np.array(errs), it, present
+
+
+# ---------------------------------------------------------------------- P-Tucker-Cache
+def pres_init(t: Tensor, m: Model, threads: int = 0) -> np.ndarray:
+    """Alg. 3 lines 1-4: Pres[alpha][beta] = G_beta prod_k a^(k)_{i_k j_k},
+    |Omega| x |G| (beta in C order)."""
+    gsize = int(np.prod(m.J))
+    pres = np.zeros((t.nnz, gsize), np.float64)
+    lib().or_pres_init(m.N, _p(m.J), _p(m.G), _p(m.A_all), _p(m.dims), _p(t.coords), t.nnz, _p(pres), int(threads))
+    return pres
+
+
+def delta_cache(t: Tensor, m: Model, pres, entry: int, n: int) -> np.ndarray:
+    """Alg. 3 line 12: delta of one entry for mode n from its cache row."""
+    out = np.zeros(int(m.J[n]), np.float64)
+    coord = np.ascontiguousarray(t.coords[entry])
+    row = np.ascontiguousarray(pres[entry])
+    lib().or_delta_cache(m.N, _p(m.J), _p(m.G), _p(m.A_all), _p(m.dims), _p(coord), _p(row), n, _p(out))
+    return out
+
+
+def update_mode_cache(t: Tensor, m: Model, pres, n: int, lam: float, threads: int = 0) -> None:
+    """Alg. 3 lines 6-19, TOP branch: every row of A^(n) from the cached
+    products, then Pres rescaled by a_new / a_old (in place, both m and pres)."""
+    assert pres.flags["C_CONTIGUOUS"] and pres.dtype == np.float64
+    row_ptr, perm = t.mode_index(n)
+    rc = lib().or_update_mode_cache(m.N, _p(m.J), _p(m.G), _p(m.A_all), _p(m.dims), _p(t.coords), _p(t.vals),
+                                    t.nnz, n, _p(row_ptr), _p(perm), float(lam), _p(pres), int(threads))
+    if rc:
+        raise FloatingPointError("non-positive pivot")

@@ -18,6 +18,8 @@
  *   - QR + core update (Eq. 7-8)             P:470-479, Alg. 2 lines 8-11 P:504-508
  *   - P-Tucker-Approx: partial error R(beta) (Eq. 13) and core truncation
  *     (Alg. 4)                               P:656-700, Alg. 2 lines 5-6 P:500-502
+ *   - P-Tucker-Cache: cache table Pres, delta from it, its update
+ *     (Alg. 3 TOP branch)
  * Readings where the paper is silent are listed in DESIGN.md ("Readings").
  *
  * Pins (tests/test_oracle_pins.py) check every function here against values
@@ -520,4 +522,134 @@ double or_test_rmse(int N, const int32_t* J, const double* G, const double* A_al
         s += r * r;
     }
     return sqrt(s / (double)n);
+}
+
+/* ------------------------------------------------------------------------ */
+/* P-Tucker-Cache (TOP), Alg. 3 with the cache table Pres in R^{|Omega| x |G|} */
+/* (P:581-626), literally:                                         */
+/*   lines 1-4  : Pres[alpha][beta] = G_beta prod_{k=1..N} a^(k)_{i_k j_k}    */
+/*   line 12    : delta(j_n) += Pres[alpha][beta] / a^(n)_{i_n j_n}           */
+/*                (when a^(n)_{i_n j_n} = 0: as MOP, line 10)          */
+/*   lines 16-19: after A^(n) is updated, Pres[alpha][beta] =                 */
+/*                Pres[alpha][beta] / a_old^(n)_{i_n j_n} x a_new^(n)_{i_n j_n}*/
+/*                (a_old = 0: recomputed as in lines 1-4)              */
+/* Pres is row-major |Omega| x |G| with beta in C order.                      */
+/* ------------------------------------------------------------------------ */
+static void pres_entry(int N, const int32_t* J, const double* G, const double* A_all, const int64_t* dims,
+                       const int32_t* coord, double* out /* [|G|] */) {
+    int64_t off[OR_MAXN + 1];
+    factor_offsets(N, dims, J, off);
+    int64_t gsize = core_size(N, J);
+    int jj[OR_MAXN];
+    for (int k = 0; k < N; ++k) jj[k] = 0;
+    for (int64_t b = 0; b < gsize; ++b) {
+        double prod = G[b];
+        for (int k = 0; k < N; ++k) prod *= A_all[off[k] + (int64_t)coord[k] * J[k] + jj[k]];
+        out[b] = prod;
+        for (int k = N - 1; k >= 0; --k) {
+            if (++jj[k] < J[k]) break;
+            jj[k] = 0;
+        }
+    }
+}
+
+/* Alg. 3 lines 1-4. */
+void or_pres_init(int N, const int32_t* J, const double* G, const double* A_all, const int64_t* dims,
+                  const int32_t* coords, int64_t nnz, double* pres, int nthreads) {
+    const int64_t gsize = core_size(N, J);
+#ifdef _OPENMP
+    if (nthreads <= 0) nthreads = omp_get_max_threads();
+#pragma omp parallel for schedule(static) num_threads(nthreads)
+#endif
+    for (int64_t e = 0; e < nnz; ++e) pres_entry(N, J, G, A_all, dims, coords + e * N, pres + e * gsize);
+    (void)nthreads;
+}
+
+/* Alg. 3 lines 9-12, TOP branch: delta of entry e for mode n from Pres. */
+void or_delta_cache(int N, const int32_t* J, const double* G, const double* A_all, const int64_t* dims,
+                    const int32_t* coord, const double* pres_e, int n, double* delta) {
+    int64_t off[OR_MAXN + 1];
+    factor_offsets(N, dims, J, off);
+    int64_t gsize = core_size(N, J);
+    int jj[OR_MAXN];
+    for (int k = 0; k < N; ++k) jj[k] = 0;
+    for (int j = 0; j < J[n]; ++j) delta[j] = 0.0;
+    for (int64_t b = 0; b < gsize; ++b) {
+        const double a = A_all[off[n] + (int64_t)coord[n] * J[n] + jj[n]];
+        if (a != 0.0) {
+            delta[jj[n]] += pres_e[b] / a;                   /* line 12 */
+        } else {                                              /* line 10 */
+            double prod = G[b];
+            for (int k = 0; k < N; ++k) {
+                if (k == n) continue;
+                prod *= A_all[off[k] + (int64_t)coord[k] * J[k] + jj[k]];
+            }
+            delta[jj[n]] += prod;
+        }
+        for (int k = N - 1; k >= 0; --k) {
+            if (++jj[k] < J[k]) break;
+            jj[k] = 0;
+        }
+    }
+}
+
+/* Alg. 3 lines 6-15 for every row of mode n with the TOP delta, then lines 16-19
+ * (P:610-619): Pres rescaled by a_new / a_old (recomputed where a_old = 0).
+ * pres: |Omega| x |G| (updated in place).  Returns 0 or 2 (non-positive pivot). */
+int or_update_mode_cache(int N, const int32_t* J, const double* G, double* A_all, const int64_t* dims,
+                         const int32_t* coords, const double* vals, int64_t nnz, int n, const int64_t* row_ptr,
+                         const int64_t* perm, double lambda, double* pres, int nthreads) {
+    int64_t off[OR_MAXN + 1];
+    factor_offsets(N, dims, J, off);
+    const int64_t gsize = core_size(N, J);
+    const int Jn = J[n];
+    const int64_t I = dims[n];
+    double* old = (double*)malloc(sizeof(double) * (size_t)(I * Jn));
+    memcpy(old, A_all + off[n], sizeof(double) * (size_t)(I * Jn));
+    int bad = 0;
+#ifdef _OPENMP
+    if (nthreads <= 0) nthreads = omp_get_max_threads();
+#pragma omp parallel for schedule(dynamic, 64) num_threads(nthreads) reduction(| : bad)
+#endif
+    for (int64_t i = 0; i < I; ++i) {
+        double B[64 * 64], c[64], a[64], delta[64];
+        for (int t = 0; t < Jn * Jn; ++t) B[t] = 0.0;
+        for (int t = 0; t < Jn; ++t) c[t] = 0.0;
+        for (int64_t p = row_ptr[i]; p < row_ptr[i + 1]; ++p) {
+            const int64_t e = perm[p];
+            or_delta_cache(N, J, G, A_all, dims, coords + e * N, pres + e * gsize, n, delta);
+            const double x = vals[e];
+            for (int j1 = 0; j1 < Jn; ++j1) {
+                for (int j2 = 0; j2 < Jn; ++j2) B[j1 * Jn + j2] += delta[j1] * delta[j2];
+                c[j1] += x * delta[j1];
+            }
+        }
+        if (or_solve(Jn, B, c, lambda, a)) bad |= 1;
+        else for (int j = 0; j < Jn; ++j) A_all[off[n] + i * Jn + j] = a[j];
+    }
+    /* lines 16-19: every entry's cache row, the mode-n factor value swapped */
+#ifdef _OPENMP
+#pragma omp parallel for schedule(static) num_threads(nthreads)
+#endif
+    for (int64_t e = 0; e < nnz; ++e) {
+        const int32_t* coord = coords + e * N;
+        double* pe = pres + e * gsize;
+        int recompute = 0;
+        int jj[OR_MAXN];
+        for (int k = 0; k < N; ++k) jj[k] = 0;
+        for (int64_t b = 0; b < gsize; ++b) {
+            const double ao = old[(int64_t)coord[n] * Jn + jj[n]];
+            const double an = A_all[off[n] + (int64_t)coord[n] * Jn + jj[n]];
+            if (ao != 0.0) pe[b] = pe[b] / ao * an;
+            else recompute = 1;
+            for (int k = N - 1; k >= 0; --k) {
+                if (++jj[k] < J[k]) break;
+                jj[k] = 0;
+            }
+        }
+        if (recompute) pres_entry(N, J, G, A_all, dims, coord, pe);
+    }
+    free(old);
+    (void)nthreads;
+    return bad ? 2 : 0;
 }

@@ -152,6 +152,12 @@ struct Ctx {
     int grid_upd = 0, grid_lit = 0;
     int64_t launches = 0;        // kernels this library launched since init (gpu_launches evidence)
     long long* trace = nullptr;  // option "trace": device buffer of per-phase clocks (tools/)
+    // P-Tucker-Cache (option "cache", before init): the cache table Pres (|Omega| x |G| fp64)
+    int use_cache = 0;
+    double* pres = nullptr;
+    void* cache_old = nullptr;     // A^(n) before its update (lines 16-19 divide by it)
+    void** cache_ptrs = nullptr;   // device: A[0..N-1]
+    bool pres_stale = false;       // factors / core changed outside the ALS sweep: rebuild Pres
     // CUDA graph of a whole sweep (option "graph"): captured at the first ptucker_sweep
     // and replayed while the launch parameters stay valid (invalidate_graph)
     int use_graph = 1;
@@ -374,14 +380,25 @@ int launch_update_kernel(int n, bool literal) {
     g.launches += 1;
     if (g.generic) {
         if (literal) return fail(PTUCKER_EINVAL, "internal: no literal pass for generic shapes");
+        if (g.use_cache) {
+            if (g.pres_stale) {  // factors or core were set / orthogonalized / truncated: lines 1-4 again
+                launch_pres_init(g.N, g.Jv, g.esz, g.G, (const void* const*)g.cache_ptrs, g.lda, g.coo_c, g.nnz,
+                                 g.pres, S());
+                g.pres_stale = false;
+                g.launches += 1;
+            }
+            // a_old of lines 16-19
+            CK(cudaMemcpyAsync(g.cache_old, g.A[n], (size_t)g.dims[n] * g.lda * g.esz, cudaMemcpyDeviceToDevice, S()));
+        }
+        const double* pres = g.use_cache ? g.pres : nullptr;
         if (g.prec == PTUCKER_F64) {
             UpdateParams<double> p = make_params<double>(n, false);
             p.Gp = (const double*)g.G;
-            launch_update_generic(&p, 8, g.N, g.Jv, g.nsm, S());
+            launch_update_generic(&p, 8, g.N, g.Jv, g.nsm, S(), pres, g.mi[n].sid);
         } else {
             UpdateParams<float> p = make_params<float>(n, false);
             p.Gp = (const float*)g.G;
-            launch_update_generic(&p, 4, g.N, g.Jv, g.nsm, S());
+            launch_update_generic(&p, 4, g.N, g.Jv, g.nsm, S(), pres, g.mi[n].sid);
         }
         CK(cudaGetLastError());
         return PTUCKER_OK;
@@ -495,6 +512,10 @@ void free_all() {
     g.ax_tmp_bytes = 0;
     g.coo_c = nullptr;
     g.coo_v = nullptr;
+    g.pres = nullptr;
+    g.cache_old = nullptr;
+    g.cache_ptrs = nullptr;
+    g.pres_stale = false;
     g.generic = false;
     g.d_fail = g.d_qrfail = nullptr;
     g.d_work = nullptr;
@@ -689,6 +710,12 @@ int ptucker_set_option(const char* key, int64_t value) {
         g.use_smp = (int)value;
         return PTUCKER_OK;
     }
+    if (k == "cache") {
+        if (value != 0 && value != 1) return fail(PTUCKER_EINVAL, "cache must be 0 or 1");
+        if (g.inited) return fail(PTUCKER_ESTATE, "cache must be set before ptucker_init");
+        g.use_cache = (int)value;
+        return PTUCKER_OK;
+    }
     if (k == "exchange") {
         if (value != 0 && value != 1) return fail(PTUCKER_EINVAL, "exchange must be 0 (NCCL all-gather) or 1 (push)");
         g.exchange = (int)value;
@@ -800,7 +827,8 @@ int ptucker_init(const int32_t* coords, const void* vals, int32_t vals_dtype, in
     g.Jv = JDims();
     for (int n = 0; n < order; ++n) g.Jv.j[n] = core_dims[n];
     // unequal J_n: the generic kernel (delta by Eq. 12 as written, any J_n <= 16)
-    g.generic = ujn || find_update_kernel(vals_dtype, 1, order, J) == nullptr;
+    // P-Tucker-Cache runs on the generic path (delta from the cache table, any shape)
+    g.generic = g.use_cache || ujn || find_update_kernel(vals_dtype, 1, order, J) == nullptr;
     g.xnorm = g_xnorm_pending;
     g.prec = vals_dtype;
     g.esz = esz;
@@ -934,7 +962,7 @@ int ptucker_init(const int32_t* coords, const void* vals, int32_t vals_dtype, in
         const bool aux_groups = smode >= 0 && g.tc_table && g.use_tc && vals_dtype == PTUCKER_F32 &&
                                 find_update_kernel_tc(1, J) != nullptr;
         CK(build_mode_sell(d_coords, d_vals, esz, nnz, order, n, g.Jv.j[n], g.seg_len_eff, m.bounds[g.rank],
-                           m.bounds[g.rank + 1], smode, m, g.arena, g.scratch, S(), aux_groups));
+                           m.bounds[g.rank + 1], smode, m, g.arena, g.scratch, S(), aux_groups, g.use_cache != 0));
         {   // most segments of one of this rank's rows (the heavy-row finalize picks its kernels by it)
             int64_t mx = 0;
             for (int64_t r = m.bounds[g.rank]; r < m.bounds[g.rank + 1]; ++r)
@@ -952,6 +980,25 @@ int ptucker_init(const int32_t* coords, const void* vals, int32_t vals_dtype, in
         CK(g.arena.alloc(&g.coo_v, (size_t)nnz * esz));
         CK(cudaMemcpyAsync(g.coo_c, d_coords, (size_t)nnz * order * sizeof(int32_t), cudaMemcpyDeviceToDevice, S()));
         CK(cudaMemcpyAsync(g.coo_v, d_vals, (size_t)nnz * esz, cudaMemcpyDeviceToDevice, S()));
+        CK(cudaStreamSynchronize(S()));
+    }
+    if (g.use_cache) {
+        // Alg. 3 lines 1-4: the table for every entry (every rank holds all of it:
+        // each mode's rows need the entries of that mode's row block)
+        const double bytes = (double)nnz * (double)gsize * 8.0;
+        size_t fr = 0, tot = 0;
+        CK(cudaMemGetInfo(&fr, &tot));
+        if (bytes > 0.8 * (double)fr)
+            return fail(PTUCKER_ERESOURCE, "P-Tucker-Cache table of %.3g GB (|Omega| x |G| doubles) exceeds device memory",
+                        bytes / 1e9);
+        CK(g.arena.alloc((void**)&g.pres, (size_t)bytes));
+        int64_t imax = 0;
+        for (int n = 0; n < order; ++n) imax = std::max<int64_t>(imax, dims[n]);
+        CK(g.arena.alloc(&g.cache_old, (size_t)imax * g.lda * esz));
+        CK(g.arena.alloc((void**)&g.cache_ptrs, kMaxN * sizeof(void*)));
+        CK(cudaMemcpyAsync(g.cache_ptrs, g.A, kMaxN * sizeof(void*), cudaMemcpyHostToDevice, S()));
+        launch_pres_init(order, g.Jv, esz, g.G, (const void* const*)g.cache_ptrs, g.lda, g.coo_c, nnz, g.pres, S());
+        CK(cudaGetLastError());
         CK(cudaStreamSynchronize(S()));
     }
     input.release_all();
@@ -1058,6 +1105,18 @@ int ptucker_update_mode(int32_t n) {
         });
         if (rc) return rc;
     }
+    if (g.use_cache) {
+        // Alg. 3 lines 16-19: every entry's cache row with the new A^(n) (all ranks
+        // hold the refreshed replica by now)
+        rc = timed("cache_update", [&]() -> int {
+            launch_pres_update(g.N, g.Jv, g.esz, n, g.G, (const void* const*)g.cache_ptrs, g.lda, g.cache_old, g.coo_c,
+                               g.nnz, g.pres, S());
+            g.launches += 1;
+            CK(cudaGetLastError());
+            return PTUCKER_OK;
+        }, n);
+        if (rc) return rc;
+    }
     g.sse_mode = n;
     return PTUCKER_OK;
 }
@@ -1067,7 +1126,7 @@ int ptucker_sweep(void) {
     if (rc) return rc;
     // replay the captured sweep (one graph launch instead of ~2-5 launches per mode); kernel
     // timing (time_kernels) needs the per-launch events, so it runs the sweep directly
-    const bool graphs = g.use_graph && !g.time_kernels;
+    const bool graphs = g.use_graph && !g.time_kernels && !g.use_cache;  // Cache: table rebuilds are host-decided
     if (graphs && g.graph_exec) {
         CK(cudaGraphLaunch(g.graph_exec, S()));
         g.launches += g.graph_launches;
@@ -1163,6 +1222,7 @@ int ptucker_orthogonalize(void) {
     int rc = require_init();
     if (rc) return rc;
     invalidate_graph();  // swaps G and Gtmp
+    g.pres_stale = true;
     const int J = g.J;  // max_n J_n (scratch sizes)
     for (int n = 0; n < g.N; ++n)
         if (g.dims[n] < g.Jv.j[n]) return fail(PTUCKER_EINVAL, "orthogonalize needs I_%d >= J_%d", n, n);
@@ -1221,6 +1281,7 @@ int ptucker_set_factor(int32_t n, const void* in) {
     const size_t rb = (size_t)g.Jv.j[n] * g.esz;
     CK(cudaMemcpy2DAsync(g.A[n], (size_t)g.lda * g.esz, in, rb, rb, g.dims[n], cudaMemcpyHostToDevice, S()));
     g.sse_mode = -1;
+    g.pres_stale = true;
     CK(cudaStreamSynchronize(S()));
     return PTUCKER_OK;
 }
@@ -1245,6 +1306,7 @@ int ptucker_set_core(const void* in) {
     rc = rebuild_gp();
     if (rc) return rc;
     g.sse_mode = -1;
+    g.pres_stale = true;
     CK(cudaMemsetAsync(g.d_present, 1, (size_t)gsize, S()));  // a pushed core is dense (no truncation history)
     g.n_present = gsize;
     CK(cudaStreamSynchronize(S()));
@@ -1357,6 +1419,7 @@ int ptucker_truncate_core(double p, int64_t* removed) {
                                 g.G, g.d_present, S()));
         g.launches += 2;
         g.n_present -= k;
+        g.pres_stale = true;  // G changed (P-Tucker-Cache: the table is rebuilt before the next update)
         rc = rebuild_gp();
         if (rc) return rc;
         g.sse_mode = -1;
@@ -1516,6 +1579,8 @@ int ptucker_info(char* buf, int32_t len) {
     }
     int comm_ranks = 0;  // size of the library's NCCL communicator (0: none)
     if (g.comm && ncclCommCount(g.comm, &comm_ranks) != ncclSuccess) comm_ranks = -1;
+    snprintf(tmp, sizeof(tmp), "\"cache\": %s, ", g.use_cache ? "true" : "false");
+    s += tmp;
     snprintf(tmp, sizeof(tmp), "\"comm_ranks\": %d, \"peers\": %d, \"exchange\": \"%s\", ", comm_ranks, g.npeer,
              g.world == 1 ? "none" : (pushing() ? "push" : (g.comm ? "nccl_allgather" : "none")));
     s += tmp;

@@ -159,7 +159,8 @@ __global__ void k_slices(const int32_t* order, int64_t nseg, int64_t nslices, co
 template <typename TS>
 __global__ void k_sell_fill(int64_t nslices, const int64_t* slice_off, const int32_t* lane_row,
                             const int32_t* lane_len, const int64_t* lane_src, const int32_t* perm,
-                            const int32_t* coords, const TS* vals, int N, int n, int32_t* const* sc, TS* sv) {
+                            const int32_t* coords, const TS* vals, int N, int n, int32_t* const* sc, TS* sv,
+                            int32_t* sid) {
     const int64_t total = nslices * 32;
     for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
         const int32_t row = lane_row[t];
@@ -177,6 +178,7 @@ __global__ void k_sell_fill(int64_t nslices, const int64_t* slice_off, const int
                 ++l;
             }
             sv[dst] = vals[src];
+            if (sid) sid[dst] = (int32_t)src;  // input entry id (P-Tucker-Cache: the row of Pres)
         }
     }
 }
@@ -305,7 +307,7 @@ __global__ void k_slices_aux(const int32_t* order, int64_t nslices, int nclass, 
 
 cudaError_t build_mode_sell(const int32_t* d_coords, const void* d_vals, int elem_bytes, int64_t nnz, int N, int n,
                             int J, int S, int64_t r0, int64_t r1, int smode, ModeIndex& mi, DeviceArena& arena,
-                            DeviceArena& scratch, cudaStream_t st, bool aux_groups) {
+                            DeviceArena& scratch, cudaStream_t st, bool aux_groups, bool with_sid) {
     const int PW = rec_width(J);
     const int64_t nrows = r1 - r0;
     mi.r0 = r0;
@@ -464,15 +466,19 @@ cudaError_t build_mode_sell(const int32_t* d_coords, const void* d_vals, int ele
     int32_t** d_sc = nullptr;
     IB_CHECK(dalloc(&d_sc, kMaxN, scratch));
     IB_CHECK(cudaMemcpyAsync(d_sc, mi.sc, sizeof(int32_t*) * kMaxN, cudaMemcpyHostToDevice, st));
+    if (with_sid) {
+        IB_CHECK(dalloc(&mi.sid, mi.nslots, arena));
+        IB_CHECK(cudaMemsetAsync(mi.sid, 0, sizeof(int32_t) * (size_t)(mi.nslots > 0 ? mi.nslots : 1), st));
+    }
     if (nlanes > 0) {
         if (elem_bytes == 8)
             k_sell_fill<double><<<grid_for(nlanes), 256, 0, st>>>(mi.nslices, mi.slice_off, mi.lane_row, mi.lane_len,
                                                                   lane_src, perm, d_coords, (const double*)d_vals, N, n,
-                                                                  d_sc, (double*)mi.sv);
+                                                                  d_sc, (double*)mi.sv, mi.sid);
         else
             k_sell_fill<float><<<grid_for(nlanes), 256, 0, st>>>(mi.nslices, mi.slice_off, mi.lane_row, mi.lane_len,
                                                                  lane_src, perm, d_coords, (const float*)d_vals, N, n,
-                                                                 d_sc, (float*)mi.sv);
+                                                                 d_sc, (float*)mi.sv, mi.sid);
     }
     IB_CHECK(cudaGetLastError());
     IB_CHECK(cudaStreamSynchronize(st));

@@ -53,6 +53,7 @@ struct ModeIndex {
     int64_t* hpbase = nullptr;
     double* partials = nullptr;
     double* hrec = nullptr;          // [nheavy][PW] summed records (heavy-row finalize scratch)
+    int32_t* sid = nullptr;          // [nslots] input entry id per SELL slot (P-Tucker-Cache only)
     std::vector<int64_t> bounds;     // world+1 row-block bounds
 };
 
@@ -60,6 +61,6 @@ cudaError_t build_mode_csr(const int32_t* d_coords, int64_t nnz, int N, int n, i
                            DeviceArena& arena, DeviceArena& scratch, cudaStream_t st);
 cudaError_t build_mode_sell(const int32_t* d_coords, const void* d_vals, int elem_bytes, int64_t nnz, int N, int n,
                             int J, int S, int64_t r0, int64_t r1, int smode, ModeIndex& mi, DeviceArena& arena,
-                            DeviceArena& scratch, cudaStream_t st, bool aux_groups = false);
+                            DeviceArena& scratch, cudaStream_t st, bool aux_groups = false, bool with_sid = false);
 
 }  // namespace pt

@@ -133,7 +133,13 @@ int tc_kp(int J);  // K padding of the tensor-core A operand (floats per split r
 void launch_pack_rows10(const float* A, int64_t I, int lda, float* head, float* tail, cudaStream_t st);
 
 // Generic-order kernel (update_generic.cu): any N <= kMaxN, J <= 16, fp64; p.Gp = G in C order.
-void launch_update_generic(const void* params, int elem_bytes, int N, const JDims& J, int nsm, cudaStream_t st);
+void launch_update_generic(const void* params, int elem_bytes, int N, const JDims& J, int nsm, cudaStream_t st,
+                           const double* pres = nullptr, const int32_t* sid = nullptr);
+// P-Tucker-Cache (cache.cu): the cache table Pres (|Omega| x |G|, fp64) over the device COO
+void launch_pres_init(int N, const JDims& J, int elem_bytes, const void* G, const void* const* d_A, int lda,
+                      const int32_t* coords, int64_t nnz, double* pres, cudaStream_t st);
+void launch_pres_update(int N, const JDims& J, int elem_bytes, int n, const void* G, const void* const* d_A, int lda,
+                        const void* A_old, const int32_t* coords, int64_t nnz, double* pres, cudaStream_t st);
 bool generic_shape_ok(int N, int J);
 bool approx_shape_ok(int N, int J);  // approx.cu segment kernels instantiated for (N, J)
 // Alg. 4 on the device (approx.cu): scores from U, V; stable top-k truncation

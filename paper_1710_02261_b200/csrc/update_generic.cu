@@ -23,8 +23,14 @@ constexpr int kGJ = 16;  // max J of the generic kernel
 
 __device__ __forceinline__ int upi(int i, int j, int J) { return i * J - i * (i - 1) / 2 + (j - i); }
 
-template <typename TS>
-__global__ void __launch_bounds__(128) k_update_gen(const UpdateParams<TS> p, int N, const JDims jd) {
+// CACHE (P-Tucker-Cache, Alg. 3 line 12): delta(j_n) = sum over beta with beta_n = j_n
+// of Pres[alpha][beta] / a^(n)_{i_n j_n}, the division taken once per j (the same sum); a
+// factor value of exactly 0 takes the product loop instead.  Pres is |Omega| x |G|
+// (beta in C order), alpha = the slot's input entry id (ModeIndex::sid).
+template <typename TS, bool CACHE>
+__global__ void __launch_bounds__(128) k_update_gen(const UpdateParams<TS> p, int N, const JDims jd,
+                                                    const double* __restrict__ pres, const int32_t* __restrict__ sid,
+                                                    int64_t gsize) {
     const int64_t nl = p.nslices * kWarp;
     const int n = p.n;
     const int J = jd.j[n];  // J_n: size of delta, B and c of this mode
@@ -60,10 +66,26 @@ __global__ void __launch_bounds__(128) k_update_gen(const UpdateParams<TS> p, in
             }
             double d[kGJ];
             for (int j = 0; j < J; ++j) d[j] = 0.0;
+            bool mop = !CACHE;  // product loop (P-Tucker) for every j, or only where a^(n)_{i_n j} = 0
+            unsigned zero_j = 0;
+            if constexpr (CACHE) {
+                const double* pr = pres + (int64_t)sid[es] * gsize;
+                const TS* an = p.An + (int64_t)row * p.lda;  // a^(n)_{i_n .} before this update
+                for (int64_t b = 0; b < gsize; ++b) d[(int)((b / stride[n]) % J)] += pr[b];
+                for (int j = 0; j < J; ++j) {
+                    const double a = (double)an[j];
+                    if (a != 0.0) d[j] /= a;
+                    else {
+                        d[j] = 0.0;
+                        zero_j |= 1u << j;
+                        mop = true;
+                    }
+                }
+            }
             // iterate the other modes' indices k_0..k_{N-2} (ascending mode order) as a counter
             int kk[kMaxN - 1];
             for (int k = 0; k < N - 1; ++k) kk[k] = 0;
-            for (int64_t t = 0; t < ncomb; ++t) {
+            for (int64_t t = 0; mop && t < ncomb; ++t) {
                 double prod = 1.0;
                 int64_t gb = 0;
                 for (int k = 0; k < N - 1; ++k) {
@@ -71,7 +93,8 @@ __global__ void __launch_bounds__(128) k_update_gen(const UpdateParams<TS> p, in
                     prod *= (double)rows[k][kk[k]];
                     gb += kk[k] * stride[m];
                 }
-                for (int j = 0; j < J; ++j) d[j] = fma((double)p.Gp[gb + j * stride[n]], prod, d[j]);
+                for (int j = 0; j < J; ++j)
+                    if (!CACHE || ((zero_j >> j) & 1u)) d[j] = fma((double)p.Gp[gb + j * stride[n]], prod, d[j]);
                 for (int k = N - 2; k >= 0; --k) {
                     if (++kk[k] < Jo[k]) break;
                     kk[k] = 0;
@@ -141,19 +164,24 @@ __global__ void __launch_bounds__(128) k_update_gen(const UpdateParams<TS> p, in
 }  // namespace
 
 // The generic kernel reads the core in plain C order: p.Gp must be G itself.
-void launch_update_generic(const void* params, int elem_bytes, int N, const JDims& J, int nsm, cudaStream_t st) {
+void launch_update_generic(const void* params, int elem_bytes, int N, const JDims& J, int nsm, cudaStream_t st,
+                           const double* pres, const int32_t* sid) {
+    int64_t gsize = 1;
+    for (int m = 0; m < N; ++m) gsize *= J.j[m];
     if (elem_bytes == 8) {
         const UpdateParams<double>& p = *reinterpret_cast<const UpdateParams<double>*>(params);
         const int64_t nl = p.nslices * kWarp;
         int grid = (int)((nl + 127) / 128);
         if (grid > nsm * 8) grid = nsm * 8;
-        if (grid > 0) k_update_gen<double><<<grid, 128, 0, st>>>(p, N, J);
+        if (grid > 0 && pres) k_update_gen<double, true><<<grid, 128, 0, st>>>(p, N, J, pres, sid, gsize);
+        else if (grid > 0) k_update_gen<double, false><<<grid, 128, 0, st>>>(p, N, J, nullptr, nullptr, gsize);
     } else {
         const UpdateParams<float>& p = *reinterpret_cast<const UpdateParams<float>*>(params);
         const int64_t nl = p.nslices * kWarp;
         int grid = (int)((nl + 127) / 128);
         if (grid > nsm * 8) grid = nsm * 8;
-        if (grid > 0) k_update_gen<float><<<grid, 128, 0, st>>>(p, N, J);
+        if (grid > 0 && pres) k_update_gen<float, true><<<grid, 128, 0, st>>>(p, N, J, pres, sid, gsize);
+        else if (grid > 0) k_update_gen<float, false><<<grid, 128, 0, st>>>(p, N, J, nullptr, nullptr, gsize);
     }
 }
 

@@ -588,3 +588,53 @@ def test_stop_rule_relative_change(orc):
     e_run, it, _ = orc.run(t, m, cfg.lam, 8, tol, orthogonalize=False)
     assert it == expect and len(e_run) == expect + 1
     np.testing.assert_allclose(e_run, errs[:expect + 1], rtol=0, atol=0)
+
+
+def test_cache_variant(orc):
+    """P-Tucker-Cache (Alg. 3 TOP branch) in the oracle, pinned independently:
+    Pres (lines 1-4) = numpy products; delta from Pres (line 12) = numpy einsum of the core
+    with the other modes' rows (Eq. 12), also where a factor value is exactly 0 (the MOP
+    fallback of P:639); a mode update through the cache = numpy's dense normal equations
+    solve; after the update (lines 16-19) Pres = numpy products of the updated model."""
+    rng = np.random.default_rng(11)
+    dims, J, nnz, lam = (7, 6, 5, 4), [2, 3, 2, 2], 60, 0.05
+    flat = rng.choice(int(np.prod(dims)), nnz, replace=False)
+    coords = np.stack(np.unravel_index(flat, dims), 1).astype(np.int32)
+    vals = rng.random(nnz)
+    t = orc.Tensor(coords, vals, dims)
+    m = orc.init_model(dims, J, seed=2, prec=1)
+    m.A(1)[coords[0, 1], 2] = 0.0          # a zero factor value under entry 0 (P:639 branch)
+
+    def np_pres(m):
+        out = np.empty((nnz, int(np.prod(J))))
+        for e in range(nnz):
+            K = m.G.copy()
+            for k in range(4):
+                shape = [1] * 4
+                shape[k] = J[k]
+                K = K * m.A(k)[coords[e, k]].reshape(shape)
+            out[e] = K.ravel()
+        return out
+
+    def np_delta(m, e, n):
+        T = np.moveaxis(m.G, n, 0)
+        for k in [k for k in range(4) if k != n][::-1]:
+            T = T @ m.A(k)[coords[e, k]] if T.ndim > 1 else T
+        return T
+
+    pres = orc.pres_init(t, m)
+    np.testing.assert_allclose(pres, np_pres(m), rtol=1e-14, atol=0)
+    for n in range(4):
+        for e in range(nnz):
+            np.testing.assert_allclose(orc.delta_cache(t, m, pres, e, n), np_delta(m, e, n), rtol=1e-12, atol=1e-15)
+    for sweep in range(2):
+        for n in range(4):
+            ref = m.copy()
+            rows = []
+            for i in range(dims[n]):
+                es = np.flatnonzero(coords[:, n] == i)
+                D = np.array([np_delta(ref, e, n) for e in es]).reshape(len(es), J[n])
+                rows.append(np.linalg.solve(D.T @ D + lam * np.eye(J[n]), D.T @ vals[es]))
+            orc.update_mode_cache(t, m, pres, n, lam)
+            np.testing.assert_allclose(m.A(n), np.array(rows), rtol=1e-10, atol=1e-13)
+            np.testing.assert_allclose(pres, np_pres(m), rtol=1e-12, atol=1e-15)
