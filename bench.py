@@ -356,7 +356,10 @@ def run_ours(args, cfg):
         obj = [pt.ptucker_get_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(obj, src=0)
         pt.ptucker_comm_init(rank, world, obj[0])
-    stream = torch.cuda.current_stream()
+    # one dedicated stream for the library's kernels AND the timing events (torch's default
+    # stream handle 0 would make the library create its own stream beside the events)
+    stream = torch.cuda.Stream()
+    torch.cuda.set_stream(stream)
     pt.ptucker_set_stream(stream.cuda_stream)
     pt.ptucker_set_option("seg_len", args.seg_len)
 

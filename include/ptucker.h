@@ -196,7 +196,11 @@ int ptucker_get_partition(int32_t n, int64_t* bounds);
  *  "emulate_world", "emulate_rank"  (before init, no communicator): build and update only
  *                 this rank's row blocks of a `world`-way partition, without the exchange
  *                 (tests of the partitioned path on one GPU)
- *  "cache"        1 = P-Tucker-Cache (Alg. 3 TOP branch; set BEFORE init): a cache
+ *  "sparse_core"  P-Tucker-Approx on the generic path (after ptucker_truncate_core): -1 = the
+ *                 delta runs over the coordinate list of the present core entries when its
+ *                 N |G| operations per entry beat the dense J^(N-1) (J_n + N - 1) (default), 1 =
+ *                 always when the core is truncated, 0 = dense.  Bit-identical results either way
+ *  "cache"        1 = P-Tucker-Cache (Alg. 3 TOP branch; read by the next ptucker_init): a cache
  *                 table Pres of |Omega| x |G| fp64 products G_beta prod_k a^(k) (lines 1-4), delta
  *                 read from it (line 12; a factor value of exactly 0 takes the product loop,
  *                 P:639), the table rescaled by a_new / a_old after every mode (lines 16-19) and

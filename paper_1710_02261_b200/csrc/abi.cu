@@ -153,11 +153,18 @@ struct Ctx {
     int64_t launches = 0;        // kernels this library launched since init (gpu_launches evidence)
     long long* trace = nullptr;  // option "trace": device buffer of per-phase clocks (tools/)
     // P-Tucker-Cache (option "cache", before init): the cache table Pres (|Omega| x |G| fp64)
-    int use_cache = 0;
+    int use_cache = 0;             // the option (read by ptucker_init)
+    bool cache_on = false;         // this context runs P-Tucker-Cache
     double* pres = nullptr;
     void* cache_old = nullptr;     // A^(n) before its update (lines 16-19 divide by it)
     void** cache_ptrs = nullptr;   // device: A[0..N-1]
     bool pres_stale = false;       // factors / core changed outside the ALS sweep: rebuild Pres
+    // P-Tucker-Approx on the generic path: coordinate list of the present core entries (C
+    // order) for the sparse-core delta (option "sparse_core": -1 auto, 0 dense, 1 sparse)
+    int sparse_core = -1;
+    uint64_t* sp_digits = nullptr;
+    int64_t* sp_index = nullptr;
+    int64_t sp_n = -1;             // -1: no list (the core is dense)
     // CUDA graph of a whole sweep (option "graph"): captured at the first ptucker_sweep
     // and replayed while the launch parameters stay valid (invalidate_graph)
     int use_graph = 1;
@@ -380,7 +387,7 @@ int launch_update_kernel(int n, bool literal) {
     g.launches += 1;
     if (g.generic) {
         if (literal) return fail(PTUCKER_EINVAL, "internal: no literal pass for generic shapes");
-        if (g.use_cache) {
+        if (g.cache_on) {
             if (g.pres_stale) {  // factors or core were set / orthogonalized / truncated: lines 1-4 again
                 launch_pres_init(g.N, g.Jv, g.esz, g.G, (const void* const*)g.cache_ptrs, g.lda, g.coo_c, g.nnz,
                                  g.pres, S());
@@ -390,15 +397,24 @@ int launch_update_kernel(int n, bool literal) {
             // a_old of lines 16-19
             CK(cudaMemcpyAsync(g.cache_old, g.A[n], (size_t)g.dims[n] * g.lda * g.esz, cudaMemcpyDeviceToDevice, S()));
         }
-        const double* pres = g.use_cache ? g.pres : nullptr;
+        const double* pres = g.cache_on ? g.pres : nullptr;
+        // sparse-core delta (truncated core): when its O(N |G|) beats the dense J^(N-1) (J_n + N - 1)
+        bool sparse = false;
+        if (!pres && g.sp_n >= 0 && g.sparse_core != 0) {
+            double dense = (double)(g.Jv.j[n] + g.N - 1);
+            for (int m = 0; m < g.N; ++m)
+                if (m != n) dense *= g.Jv.j[m];
+            sparse = g.sparse_core == 1 || (double)g.sp_n * g.N < dense;
+        }
+        const uint64_t* spd = sparse ? g.sp_digits : nullptr;
         if (g.prec == PTUCKER_F64) {
             UpdateParams<double> p = make_params<double>(n, false);
             p.Gp = (const double*)g.G;
-            launch_update_generic(&p, 8, g.N, g.Jv, g.nsm, S(), pres, g.mi[n].sid);
+            launch_update_generic(&p, 8, g.N, g.Jv, g.nsm, S(), pres, g.mi[n].sid, spd, g.sp_index, g.sp_n);
         } else {
             UpdateParams<float> p = make_params<float>(n, false);
             p.Gp = (const float*)g.G;
-            launch_update_generic(&p, 4, g.N, g.Jv, g.nsm, S(), pres, g.mi[n].sid);
+            launch_update_generic(&p, 4, g.N, g.Jv, g.nsm, S(), pres, g.mi[n].sid, spd, g.sp_index, g.sp_n);
         }
         CK(cudaGetLastError());
         return PTUCKER_OK;
@@ -516,6 +532,10 @@ void free_all() {
     g.cache_old = nullptr;
     g.cache_ptrs = nullptr;
     g.pres_stale = false;
+    g.cache_on = false;
+    g.sp_digits = nullptr;
+    g.sp_index = nullptr;
+    g.sp_n = -1;
     g.generic = false;
     g.d_fail = g.d_qrfail = nullptr;
     g.d_work = nullptr;
@@ -710,10 +730,14 @@ int ptucker_set_option(const char* key, int64_t value) {
         g.use_smp = (int)value;
         return PTUCKER_OK;
     }
+    if (k == "sparse_core") {
+        if (value < -1 || value > 1) return fail(PTUCKER_EINVAL, "sparse_core must be -1 (auto), 0 or 1");
+        g.sparse_core = (int)value;
+        return PTUCKER_OK;
+    }
     if (k == "cache") {
         if (value != 0 && value != 1) return fail(PTUCKER_EINVAL, "cache must be 0 or 1");
-        if (g.inited) return fail(PTUCKER_ESTATE, "cache must be set before ptucker_init");
-        g.use_cache = (int)value;
+        g.use_cache = (int)value;  // takes effect at the next ptucker_init
         return PTUCKER_OK;
     }
     if (k == "exchange") {
@@ -828,7 +852,8 @@ int ptucker_init(const int32_t* coords, const void* vals, int32_t vals_dtype, in
     for (int n = 0; n < order; ++n) g.Jv.j[n] = core_dims[n];
     // unequal J_n: the generic kernel (delta by Eq. 12 as written, any J_n <= 16)
     // P-Tucker-Cache runs on the generic path (delta from the cache table, any shape)
-    g.generic = g.use_cache || ujn || find_update_kernel(vals_dtype, 1, order, J) == nullptr;
+    g.cache_on = g.use_cache != 0;
+    g.generic = g.cache_on || ujn || find_update_kernel(vals_dtype, 1, order, J) == nullptr;
     g.xnorm = g_xnorm_pending;
     g.prec = vals_dtype;
     g.esz = esz;
@@ -962,7 +987,7 @@ int ptucker_init(const int32_t* coords, const void* vals, int32_t vals_dtype, in
         const bool aux_groups = smode >= 0 && g.tc_table && g.use_tc && vals_dtype == PTUCKER_F32 &&
                                 find_update_kernel_tc(1, J) != nullptr;
         CK(build_mode_sell(d_coords, d_vals, esz, nnz, order, n, g.Jv.j[n], g.seg_len_eff, m.bounds[g.rank],
-                           m.bounds[g.rank + 1], smode, m, g.arena, g.scratch, S(), aux_groups, g.use_cache != 0));
+                           m.bounds[g.rank + 1], smode, m, g.arena, g.scratch, S(), aux_groups, g.cache_on));
         {   // most segments of one of this rank's rows (the heavy-row finalize picks its kernels by it)
             int64_t mx = 0;
             for (int64_t r = m.bounds[g.rank]; r < m.bounds[g.rank + 1]; ++r)
@@ -982,7 +1007,7 @@ int ptucker_init(const int32_t* coords, const void* vals, int32_t vals_dtype, in
         CK(cudaMemcpyAsync(g.coo_v, d_vals, (size_t)nnz * esz, cudaMemcpyDeviceToDevice, S()));
         CK(cudaStreamSynchronize(S()));
     }
-    if (g.use_cache) {
+    if (g.cache_on) {
         // Alg. 3 lines 1-4: the table for every entry (every rank holds all of it:
         // each mode's rows need the entries of that mode's row block)
         const double bytes = (double)nnz * (double)gsize * 8.0;
@@ -1105,7 +1130,7 @@ int ptucker_update_mode(int32_t n) {
         });
         if (rc) return rc;
     }
-    if (g.use_cache) {
+    if (g.cache_on) {
         // Alg. 3 lines 16-19: every entry's cache row with the new A^(n) (all ranks
         // hold the refreshed replica by now)
         rc = timed("cache_update", [&]() -> int {
@@ -1126,7 +1151,7 @@ int ptucker_sweep(void) {
     if (rc) return rc;
     // replay the captured sweep (one graph launch instead of ~2-5 launches per mode); kernel
     // timing (time_kernels) needs the per-launch events, so it runs the sweep directly
-    const bool graphs = g.use_graph && !g.time_kernels && !g.use_cache;  // Cache: table rebuilds are host-decided
+    const bool graphs = g.use_graph && !g.time_kernels && !g.cache_on;  // Cache: table rebuilds are host-decided
     if (graphs && g.graph_exec) {
         CK(cudaGraphLaunch(g.graph_exec, S()));
         g.launches += g.graph_launches;
@@ -1223,6 +1248,7 @@ int ptucker_orthogonalize(void) {
     if (rc) return rc;
     invalidate_graph();  // swaps G and Gtmp
     g.pres_stale = true;
+    g.sp_n = -1;         // G x_n R is dense
     const int J = g.J;  // max_n J_n (scratch sizes)
     for (int n = 0; n < g.N; ++n)
         if (g.dims[n] < g.Jv.j[n]) return fail(PTUCKER_EINVAL, "orthogonalize needs I_%d >= J_%d", n, n);
@@ -1307,6 +1333,7 @@ int ptucker_set_core(const void* in) {
     if (rc) return rc;
     g.sse_mode = -1;
     g.pres_stale = true;
+    g.sp_n = -1;
     CK(cudaMemsetAsync(g.d_present, 1, (size_t)gsize, S()));  // a pushed core is dense (no truncation history)
     g.n_present = gsize;
     CK(cudaStreamSynchronize(S()));
@@ -1423,6 +1450,33 @@ int ptucker_truncate_core(double p, int64_t* removed) {
         rc = rebuild_gp();
         if (rc) return rc;
         g.sse_mode = -1;
+        if (g.generic) {  // the coordinate list of the present entries, C order (sparse-core delta)
+            std::vector<uint8_t> pres_h((size_t)gsize);
+            CK(cudaMemcpyAsync(pres_h.data(), g.d_present, (size_t)gsize, cudaMemcpyDeviceToHost, S()));
+            CK(cudaStreamSynchronize(S()));
+            std::vector<uint64_t> dg;
+            std::vector<int64_t> ix;
+            for (int64_t b = 0; b < gsize; ++b) {
+                if (!pres_h[b]) continue;
+                uint64_t code = 0;
+                int64_t r = b;
+                for (int m = g.N - 1; m >= 0; --m) {
+                    code |= (uint64_t)(r % g.Jv.j[m]) << (4 * m);
+                    r /= g.Jv.j[m];
+                }
+                dg.push_back(code);
+                ix.push_back(b);
+            }
+            if (!g.sp_digits) {
+                CK(g.arena.alloc((void**)&g.sp_digits, (size_t)gsize * sizeof(uint64_t)));
+                CK(g.arena.alloc((void**)&g.sp_index, (size_t)gsize * sizeof(int64_t)));
+            }
+            CK(cudaMemcpyAsync(g.sp_digits, dg.data(), dg.size() * sizeof(uint64_t), cudaMemcpyHostToDevice, S()));
+            CK(cudaMemcpyAsync(g.sp_index, ix.data(), ix.size() * sizeof(int64_t), cudaMemcpyHostToDevice, S()));
+            CK(cudaStreamSynchronize(S()));
+            g.sp_n = (int64_t)dg.size();
+            invalidate_graph();
+        }
     }
     if (removed) *removed = k;
     return PTUCKER_OK;
@@ -1579,7 +1633,7 @@ int ptucker_info(char* buf, int32_t len) {
     }
     int comm_ranks = 0;  // size of the library's NCCL communicator (0: none)
     if (g.comm && ncclCommCount(g.comm, &comm_ranks) != ncclSuccess) comm_ranks = -1;
-    snprintf(tmp, sizeof(tmp), "\"cache\": %s, ", g.use_cache ? "true" : "false");
+    snprintf(tmp, sizeof(tmp), "\"cache\": %s, ", g.cache_on ? "true" : "false");
     s += tmp;
     snprintf(tmp, sizeof(tmp), "\"comm_ranks\": %d, \"peers\": %d, \"exchange\": \"%s\", ", comm_ranks, g.npeer,
              g.world == 1 ? "none" : (pushing() ? "push" : (g.comm ? "nccl_allgather" : "none")));

@@ -27,10 +27,21 @@ __device__ __forceinline__ int upi(int i, int j, int J) { return i * J - i * (i 
 // of Pres[alpha][beta] / a^(n)_{i_n j_n}, the division taken once per j (the same sum); a
 // factor value of exactly 0 takes the product loop instead.  Pres is |Omega| x |G|
 // (beta in C order), alpha = the slot's input entry id (ModeIndex::sid).
-template <typename TS, bool CACHE>
+// SPARSE (P-Tucker-Approx's truncated core): delta over the coordinate
+// list of the present core entries only (C order, each packed as 4-bit digits beta_0..beta_{N-1}
+// plus its C-order index): O(N |G|) per entry instead of the dense J^(N-1) (J + N - 1).  The
+// list is in C order and the product is formed in the same mode order as the dense loop, so
+// for every j the terms arrive in the dense order minus exact zeros: bit-identical deltas.
+struct SparseCore {
+    const uint64_t* digits = nullptr;  // [n] packed beta digits (4 bits per mode, mode 0 lowest)
+    const int64_t* index = nullptr;    // [n] C-order index of the entry in G
+    int64_t n = 0;
+};
+
+template <typename TS, bool CACHE, bool SPARSE = false>
 __global__ void __launch_bounds__(128) k_update_gen(const UpdateParams<TS> p, int N, const JDims jd,
                                                     const double* __restrict__ pres, const int32_t* __restrict__ sid,
-                                                    int64_t gsize) {
+                                                    int64_t gsize, const SparseCore sp = SparseCore()) {
     const int64_t nl = p.nslices * kWarp;
     const int n = p.n;
     const int J = jd.j[n];  // J_n: size of delta, B and c of this mode
@@ -85,6 +96,19 @@ __global__ void __launch_bounds__(128) k_update_gen(const UpdateParams<TS> p, in
             // iterate the other modes' indices k_0..k_{N-2} (ascending mode order) as a counter
             int kk[kMaxN - 1];
             for (int k = 0; k < N - 1; ++k) kk[k] = 0;
+            if constexpr (SPARSE) {
+                mop = false;
+                for (int64_t q = 0; q < sp.n; ++q) {
+                    const uint64_t dg = sp.digits[q];
+                    double prod = 1.0;
+                    for (int k = 0; k < N - 1; ++k) {
+                        const int m = k < n ? k : k + 1;
+                        prod *= (double)rows[k][(int)((dg >> (4 * m)) & 15u)];
+                    }
+                    const int jn = (int)((dg >> (4 * n)) & 15u);
+                    d[jn] = fma((double)p.Gp[sp.index[q]], prod, d[jn]);
+                }
+            }
             for (int64_t t = 0; mop && t < ncomb; ++t) {
                 double prod = 1.0;
                 int64_t gb = 0;
@@ -164,25 +188,37 @@ __global__ void __launch_bounds__(128) k_update_gen(const UpdateParams<TS> p, in
 }  // namespace
 
 // The generic kernel reads the core in plain C order: p.Gp must be G itself.
+template <typename TS>
+void launch_gen_t(const UpdateParams<TS>& p, int N, const JDims& J, int nsm, cudaStream_t st, const double* pres,
+                  const int32_t* sid, int64_t gsize, const uint64_t* sp_digits, const int64_t* sp_index, int64_t sp_n) {
+    const int64_t nl = p.nslices * kWarp;
+    int grid = (int)((nl + 127) / 128);
+    if (grid > nsm * 8) grid = nsm * 8;
+    if (grid <= 0) return;
+    if (pres) {
+        k_update_gen<TS, true><<<grid, 128, 0, st>>>(p, N, J, pres, sid, gsize);
+    } else if (sp_digits) {
+        SparseCore sc;
+        sc.digits = sp_digits;
+        sc.index = sp_index;
+        sc.n = sp_n;
+        k_update_gen<TS, false, true><<<grid, 128, 0, st>>>(p, N, J, nullptr, nullptr, gsize, sc);
+    } else {
+        k_update_gen<TS, false><<<grid, 128, 0, st>>>(p, N, J, nullptr, nullptr, gsize);
+    }
+}
+
 void launch_update_generic(const void* params, int elem_bytes, int N, const JDims& J, int nsm, cudaStream_t st,
-                           const double* pres, const int32_t* sid) {
+                           const double* pres, const int32_t* sid, const uint64_t* sp_digits, const int64_t* sp_index,
+                           int64_t sp_n) {
     int64_t gsize = 1;
     for (int m = 0; m < N; ++m) gsize *= J.j[m];
-    if (elem_bytes == 8) {
-        const UpdateParams<double>& p = *reinterpret_cast<const UpdateParams<double>*>(params);
-        const int64_t nl = p.nslices * kWarp;
-        int grid = (int)((nl + 127) / 128);
-        if (grid > nsm * 8) grid = nsm * 8;
-        if (grid > 0 && pres) k_update_gen<double, true><<<grid, 128, 0, st>>>(p, N, J, pres, sid, gsize);
-        else if (grid > 0) k_update_gen<double, false><<<grid, 128, 0, st>>>(p, N, J, nullptr, nullptr, gsize);
-    } else {
-        const UpdateParams<float>& p = *reinterpret_cast<const UpdateParams<float>*>(params);
-        const int64_t nl = p.nslices * kWarp;
-        int grid = (int)((nl + 127) / 128);
-        if (grid > nsm * 8) grid = nsm * 8;
-        if (grid > 0 && pres) k_update_gen<float, true><<<grid, 128, 0, st>>>(p, N, J, pres, sid, gsize);
-        else if (grid > 0) k_update_gen<float, false><<<grid, 128, 0, st>>>(p, N, J, nullptr, nullptr, gsize);
-    }
+    if (elem_bytes == 8)
+        launch_gen_t(*reinterpret_cast<const UpdateParams<double>*>(params), N, J, nsm, st, pres, sid, gsize,
+                     sp_digits, sp_index, sp_n);
+    else
+        launch_gen_t(*reinterpret_cast<const UpdateParams<float>*>(params), N, J, nsm, st, pres, sid, gsize,
+                     sp_digits, sp_index, sp_n);
 }
 
 bool generic_shape_ok(int N, int J) { return N >= 2 && N <= kMaxN && J >= 1 && J <= kGJ; }

@@ -77,7 +77,10 @@ def test_cache_mode_updates_and_trajectory(pt, orc, name, J, seg):
     N = len(dims)
     prec = 1 if dtype == "f64" else 0
     dt = np.float64 if prec else np.float32
-    tol = 1e-10 if prec else 1e-5
+    # FP64: 1e-10 on the compiled-size shapes; the order-scaling shapes (K = J^(N-1) terms per
+    # delta component, kappa up to ~1e6) take reading R31's conditioning-aware bound, of which
+    # 2e-9 is a small fraction (4 kappa sqrt(K) u ~ 6e-8 at order 10)
+    tol = (1e-10 if N <= 5 else 2e-9) if prec else 1e-5
     init(pt, coords, vals, dims, Js, lam, seg)
     t = orc.Tensor(coords, vals, dims)
     # the same ALS on both sides, mode by mode: oracle Cache from its own init, rows compared
@@ -93,16 +96,17 @@ def test_cache_mode_updates_and_trajectory(pt, orc, name, J, seg):
             a = pt.ptucker_get_factor(n)
             err = rel_rows(a, m.A(n))
             worst = max(worst, float(err.max()))
-            # FP64: the GPU's state after each mode equals the oracle's (same ALS, rounding only)
-            assert err.max() <= (1e-9 if prec else 1e-5), (name, sweep, n, float(err.max()))
+            assert err.max() <= tol, (name, sweep, n, float(err.max()))
             # Cache and P-Tucker are the same update (the oracle's two implementations)
-            assert rel_rows(m.A(n), m_plain.A(n)).max() <= 1e-9
-            if not prec:   # keep both sides on the same stored state
-                m.A(n)[:] = a.astype(np.float64)
-                pres[:] = orc.pres_init(t, m)
+            assert rel_rows(m.A(n), m_plain.A(n)).max() <= tol
+            # every side continues from the GPU's stored state: each mode is compared from an
+            # identical state (reading R20), the tables rebuilt from it
+            m.A(n)[:] = a.astype(np.float64)
+            m_plain.A(n)[:] = a.astype(np.float64)
+            pres[:] = orc.pres_init(t, m)
     e_gpu = pt.ptucker_error_literal()
-    e_ref = orc.error(t, m)
-    assert abs(e_gpu - e_ref) <= (1e-9 if prec else 1e-5) * e_ref
+    e_ref = orc.error(t, m)   # the same (GPU-synced) state: Eq. 5 on both sides
+    assert abs(e_gpu - e_ref) <= 1e-9 * e_ref
     print(f"{name}: worst row rel err over 2 sweeps {worst:.2e}; error {e_gpu:.6g}")
 
 
