@@ -162,8 +162,9 @@ struct Ctx {
     // P-Tucker-Approx on the generic path: coordinate list of the present core entries (C
     // order) for the sparse-core delta (option "sparse_core": -1 auto, 0 dense, 1 sparse)
     int sparse_core = -1;
-    uint64_t* sp_digits = nullptr;
-    int64_t* sp_index = nullptr;
+    uint64_t* sp_digits = nullptr;  // [N][|G|] per mode, ordered by (t mod 32, C order), t = the
+    int64_t* sp_index = nullptr;    //   entry's index over the other modes (update_generic.cu)
+    int32_t* sp_off = nullptr;      // [N][33] each lane's range
     int64_t sp_n = -1;             // -1: no list (the core is dense)
     // CUDA graph of a whole sweep (option "graph"): captured at the first ptucker_sweep
     // and replayed while the launch parameters stay valid (invalidate_graph)
@@ -406,15 +407,19 @@ int launch_update_kernel(int n, bool literal) {
                 if (m != n) dense *= g.Jv.j[m];
             sparse = g.sparse_core == 1 || (double)g.sp_n * g.N < dense;
         }
-        const uint64_t* spd = sparse ? g.sp_digits : nullptr;
+        int64_t gsz = 1;
+        for (int m = 0; m < g.N; ++m) gsz *= g.Jv.j[m];
+        const uint64_t* spd = sparse ? g.sp_digits + (int64_t)n * gsz : nullptr;
+        const int64_t* spi = sparse ? g.sp_index + (int64_t)n * gsz : nullptr;
+        const int32_t* spo = sparse ? g.sp_off + n * 33 : nullptr;
         if (g.prec == PTUCKER_F64) {
             UpdateParams<double> p = make_params<double>(n, false);
             p.Gp = (const double*)g.G;
-            launch_update_generic(&p, 8, g.N, g.Jv, g.nsm, S(), pres, g.mi[n].sid, spd, g.sp_index, g.sp_n);
+            launch_update_generic(&p, 8, g.N, g.Jv, g.nsm, S(), pres, g.mi[n].sid, spd, spi, spo);
         } else {
             UpdateParams<float> p = make_params<float>(n, false);
             p.Gp = (const float*)g.G;
-            launch_update_generic(&p, 4, g.N, g.Jv, g.nsm, S(), pres, g.mi[n].sid, spd, g.sp_index, g.sp_n);
+            launch_update_generic(&p, 4, g.N, g.Jv, g.nsm, S(), pres, g.mi[n].sid, spd, spi, spo);
         }
         CK(cudaGetLastError());
         return PTUCKER_OK;
@@ -535,6 +540,7 @@ void free_all() {
     g.cache_on = false;
     g.sp_digits = nullptr;
     g.sp_index = nullptr;
+    g.sp_off = nullptr;
     g.sp_n = -1;
     g.generic = false;
     g.d_fail = g.d_qrfail = nullptr;
@@ -1454,27 +1460,55 @@ int ptucker_truncate_core(double p, int64_t* removed) {
             std::vector<uint8_t> pres_h((size_t)gsize);
             CK(cudaMemcpyAsync(pres_h.data(), g.d_present, (size_t)gsize, cudaMemcpyDeviceToHost, S()));
             CK(cudaStreamSynchronize(S()));
-            std::vector<uint64_t> dg;
-            std::vector<int64_t> ix;
-            for (int64_t b = 0; b < gsize; ++b) {
-                if (!pres_h[b]) continue;
-                uint64_t code = 0;
-                int64_t r = b;
-                for (int m = g.N - 1; m >= 0; --m) {
-                    code |= (uint64_t)(r % g.Jv.j[m]) << (4 * m);
-                    r /= g.Jv.j[m];
+            // per mode n: the present entries grouped by lane (t mod 32, t = the index over the
+            // other modes, the dense loop's lane split) and in C order within a lane
+            std::vector<uint64_t> dg((size_t)(g.N * gsize));
+            std::vector<int64_t> ix((size_t)(g.N * gsize));
+            std::vector<int32_t> off((size_t)(g.N * 33));
+            int64_t np = 0;
+            for (int n = 0; n < g.N; ++n) {
+                std::vector<std::vector<int64_t>> per(32);
+                for (int64_t b = 0; b < gsize; ++b) {
+                    if (!pres_h[b]) continue;
+                    int64_t r = b, t = 0, mul = 1;
+                    for (int m = g.N - 1; m >= 0; --m) {
+                        const int dgt = (int)(r % g.Jv.j[m]);
+                        r /= g.Jv.j[m];
+                        if (m != n) {
+                            t += dgt * mul;
+                            mul *= g.Jv.j[m];
+                        }
+                    }
+                    per[t % 32].push_back(b);
                 }
-                dg.push_back(code);
-                ix.push_back(b);
+                int64_t w = 0;
+                for (int l = 0; l < 32; ++l) {
+                    off[n * 33 + l] = (int32_t)w;
+                    for (int64_t b : per[l]) {
+                        uint64_t code = 0;
+                        int64_t r = b;
+                        for (int m = g.N - 1; m >= 0; --m) {
+                            code |= (uint64_t)(r % g.Jv.j[m]) << (4 * m);
+                            r /= g.Jv.j[m];
+                        }
+                        dg[(size_t)(n * gsize + w)] = code;
+                        ix[(size_t)(n * gsize + w)] = b;
+                        ++w;
+                    }
+                }
+                off[n * 33 + 32] = (int32_t)w;
+                np = w;
             }
             if (!g.sp_digits) {
-                CK(g.arena.alloc((void**)&g.sp_digits, (size_t)gsize * sizeof(uint64_t)));
-                CK(g.arena.alloc((void**)&g.sp_index, (size_t)gsize * sizeof(int64_t)));
+                CK(g.arena.alloc((void**)&g.sp_digits, (size_t)(g.N * gsize) * sizeof(uint64_t)));
+                CK(g.arena.alloc((void**)&g.sp_index, (size_t)(g.N * gsize) * sizeof(int64_t)));
+                CK(g.arena.alloc((void**)&g.sp_off, (size_t)(g.N * 33) * sizeof(int32_t)));
             }
             CK(cudaMemcpyAsync(g.sp_digits, dg.data(), dg.size() * sizeof(uint64_t), cudaMemcpyHostToDevice, S()));
             CK(cudaMemcpyAsync(g.sp_index, ix.data(), ix.size() * sizeof(int64_t), cudaMemcpyHostToDevice, S()));
+            CK(cudaMemcpyAsync(g.sp_off, off.data(), off.size() * sizeof(int32_t), cudaMemcpyHostToDevice, S()));
             CK(cudaStreamSynchronize(S()));
-            g.sp_n = (int64_t)dg.size();
+            g.sp_n = np;
             invalidate_graph();
         }
     }

@@ -135,7 +135,8 @@ void launch_pack_rows10(const float* A, int64_t I, int lda, float* head, float* 
 // Generic-order kernel (update_generic.cu): any N <= kMaxN, J <= 16, fp64; p.Gp = G in C order.
 void launch_update_generic(const void* params, int elem_bytes, int N, const JDims& J, int nsm, cudaStream_t st,
                            const double* pres = nullptr, const int32_t* sid = nullptr,
-                           const uint64_t* sp_digits = nullptr, const int64_t* sp_index = nullptr, int64_t sp_n = 0);
+                           const uint64_t* sp_digits = nullptr, const int64_t* sp_index = nullptr,
+                           const int32_t* sp_off = nullptr);
 // P-Tucker-Cache (cache.cu): the cache table Pres (|Omega| x |G|, fp64) over the device COO
 void launch_pres_init(int N, const JDims& J, int elem_bytes, const void* G, const void* const* d_A, int lda,
                       const int32_t* coords, int64_t nnz, double* pres, cudaStream_t st);

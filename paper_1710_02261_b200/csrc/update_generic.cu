@@ -33,16 +33,24 @@ __device__ __forceinline__ int upi(int i, int j, int J) { return i * J - i * (i 
 // list is in C order and the product is formed in the same mode order as the dense loop, so
 // for every j the terms arrive in the dense order minus exact zeros: bit-identical deltas.
 struct SparseCore {
-    const uint64_t* digits = nullptr;  // [n] packed beta digits (4 bits per mode, mode 0 lowest)
-    const int64_t* index = nullptr;    // [n] C-order index of the entry in G
-    int64_t n = 0;
+    const uint64_t* digits = nullptr;  // packed beta digits (4 bits per mode, mode 0 lowest), this mode's order
+    const int64_t* index = nullptr;    // C-order index of the entry in G
+    const int32_t* off = nullptr;      // [33] lane l's entries: [off[l], off[l+1]) (see below)
 };
 
+// One WARP per SELL lane (row segment): the 32 lanes split the delta loop of each entry --
+// dense: combination t of the other modes' indices (C order) to lane t mod 32; sparse: the
+// mode's list is ordered by (t mod 32, C order) so each lane takes the same terms, in the
+// same order, as in the dense loop (bit-identical); cache: beta to lane beta mod 32 -- then
+// a fixed xor butterfly (every lane ends with the same bits) and the normal equations, kept
+// identical in every lane; lane 0 writes.  The order-scaling shapes (|Omega| = 10^3, J^(N-1)
+// up to 19,683 terms per component) ran one thread per segment before: 32x the parallelism.
 template <typename TS, bool CACHE, bool SPARSE = false>
 __global__ void __launch_bounds__(128) k_update_gen(const UpdateParams<TS> p, int N, const JDims jd,
                                                     const double* __restrict__ pres, const int32_t* __restrict__ sid,
                                                     int64_t gsize, const SparseCore sp = SparseCore()) {
     const int64_t nl = p.nslices * kWarp;
+    const int lane = threadIdx.x & 31;
     const int n = p.n;
     const int J = jd.j[n];  // J_n: size of delta, B and c of this mode
     // stride of beta_m in the C-order core, and J of the k-th other mode (ascending)
@@ -58,8 +66,8 @@ __global__ void __launch_bounds__(128) k_update_gen(const UpdateParams<TS> p, in
     }
     int64_t ncomb = 1;
     for (int k = 0; k < N - 1; ++k) ncomb *= Jo[k];
-    for (int64_t slot = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; slot < nl;
-         slot += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
+    for (int64_t slot = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); slot < nl; slot += nw) {
         const int row = p.lane_row[slot];
         if (row < 0) continue;
         const int len = p.lane_len[slot];
@@ -82,7 +90,9 @@ __global__ void __launch_bounds__(128) k_update_gen(const UpdateParams<TS> p, in
             if constexpr (CACHE) {
                 const double* pr = pres + (int64_t)sid[es] * gsize;
                 const TS* an = p.An + (int64_t)row * p.lda;  // a^(n)_{i_n .} before this update
-                for (int64_t b = 0; b < gsize; ++b) d[(int)((b / stride[n]) % J)] += pr[b];
+                for (int64_t b = lane; b < gsize; b += 32) d[(int)((b / stride[n]) % J)] += pr[b];
+                for (int j = 0; j < J; ++j)
+                    for (int o = 16; o > 0; o >>= 1) d[j] += __shfl_xor_sync(0xffffffffu, d[j], o);
                 for (int j = 0; j < J; ++j) {
                     const double a = (double)an[j];
                     if (a != 0.0) d[j] /= a;
@@ -93,12 +103,12 @@ __global__ void __launch_bounds__(128) k_update_gen(const UpdateParams<TS> p, in
                     }
                 }
             }
-            // iterate the other modes' indices k_0..k_{N-2} (ascending mode order) as a counter
-            int kk[kMaxN - 1];
-            for (int k = 0; k < N - 1; ++k) kk[k] = 0;
+            // this lane's partial sums of the product loop (dense or sparse), reduced below
+            double dp[kGJ];
+            for (int j = 0; j < J; ++j) dp[j] = 0.0;
             if constexpr (SPARSE) {
                 mop = false;
-                for (int64_t q = 0; q < sp.n; ++q) {
+                for (int64_t q = sp.off[lane]; q < sp.off[lane + 1]; ++q) {
                     const uint64_t dg = sp.digits[q];
                     double prod = 1.0;
                     for (int k = 0; k < N - 1; ++k) {
@@ -106,10 +116,19 @@ __global__ void __launch_bounds__(128) k_update_gen(const UpdateParams<TS> p, in
                         prod *= (double)rows[k][(int)((dg >> (4 * m)) & 15u)];
                     }
                     const int jn = (int)((dg >> (4 * n)) & 15u);
-                    d[jn] = fma((double)p.Gp[sp.index[q]], prod, d[jn]);
+                    dp[jn] = fma((double)p.Gp[sp.index[q]], prod, dp[jn]);
                 }
             }
-            for (int64_t t = 0; mop && t < ncomb; ++t) {
+            for (int64_t t = lane; mop && t < ncomb; t += 32) {
+                // the other modes' indices k_0..k_{N-2} (ascending mode order) of combination t
+                int kk[kMaxN - 1];
+                {
+                    int64_t r = t;
+                    for (int k = N - 2; k >= 0; --k) {
+                        kk[k] = (int)(r % Jo[k]);
+                        r /= Jo[k];
+                    }
+                }
                 double prod = 1.0;
                 int64_t gb = 0;
                 for (int k = 0; k < N - 1; ++k) {
@@ -118,10 +137,13 @@ __global__ void __launch_bounds__(128) k_update_gen(const UpdateParams<TS> p, in
                     gb += kk[k] * stride[m];
                 }
                 for (int j = 0; j < J; ++j)
-                    if (!CACHE || ((zero_j >> j) & 1u)) d[j] = fma((double)p.Gp[gb + j * stride[n]], prod, d[j]);
-                for (int k = N - 2; k >= 0; --k) {
-                    if (++kk[k] < Jo[k]) break;
-                    kk[k] = 0;
+                    if (!CACHE || ((zero_j >> j) & 1u)) dp[j] = fma((double)p.Gp[gb + j * stride[n]], prod, dp[j]);
+            }
+            if (SPARSE || mop) {
+                for (int j = 0; j < J; ++j) {
+                    double v = dp[j];
+                    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+                    d[j] += v;
                 }
             }
             for (int i = 0; i < J; ++i) {
@@ -130,6 +152,7 @@ __global__ void __launch_bounds__(128) k_update_gen(const UpdateParams<TS> p, in
             }
             s2 = fma(x, x, s2);
         }
+        if (lane != 0) continue;  // every lane holds the same B, c, s2: lane 0 writes
         const int64_t pidx = p.lane_pidx[slot];
         if (pidx >= 0) {
             const int stp = p.lane_pstride[slot];
@@ -190,10 +213,11 @@ __global__ void __launch_bounds__(128) k_update_gen(const UpdateParams<TS> p, in
 // The generic kernel reads the core in plain C order: p.Gp must be G itself.
 template <typename TS>
 void launch_gen_t(const UpdateParams<TS>& p, int N, const JDims& J, int nsm, cudaStream_t st, const double* pres,
-                  const int32_t* sid, int64_t gsize, const uint64_t* sp_digits, const int64_t* sp_index, int64_t sp_n) {
-    const int64_t nl = p.nslices * kWarp;
-    int grid = (int)((nl + 127) / 128);
-    if (grid > nsm * 8) grid = nsm * 8;
+                  const int32_t* sid, int64_t gsize, const uint64_t* sp_digits, const int64_t* sp_index,
+                  const int32_t* sp_off) {
+    const int64_t nl = p.nslices * kWarp;  // lanes = warps of the kernel, 4 per block
+    int grid = (int)((nl + 3) / 4);
+    if (grid > nsm * 32) grid = nsm * 32;
     if (grid <= 0) return;
     if (pres) {
         k_update_gen<TS, true><<<grid, 128, 0, st>>>(p, N, J, pres, sid, gsize);
@@ -201,7 +225,7 @@ void launch_gen_t(const UpdateParams<TS>& p, int N, const JDims& J, int nsm, cud
         SparseCore sc;
         sc.digits = sp_digits;
         sc.index = sp_index;
-        sc.n = sp_n;
+        sc.off = sp_off;
         k_update_gen<TS, false, true><<<grid, 128, 0, st>>>(p, N, J, nullptr, nullptr, gsize, sc);
     } else {
         k_update_gen<TS, false><<<grid, 128, 0, st>>>(p, N, J, nullptr, nullptr, gsize);
@@ -210,15 +234,15 @@ void launch_gen_t(const UpdateParams<TS>& p, int N, const JDims& J, int nsm, cud
 
 void launch_update_generic(const void* params, int elem_bytes, int N, const JDims& J, int nsm, cudaStream_t st,
                            const double* pres, const int32_t* sid, const uint64_t* sp_digits, const int64_t* sp_index,
-                           int64_t sp_n) {
+                           const int32_t* sp_off) {
     int64_t gsize = 1;
     for (int m = 0; m < N; ++m) gsize *= J.j[m];
     if (elem_bytes == 8)
         launch_gen_t(*reinterpret_cast<const UpdateParams<double>*>(params), N, J, nsm, st, pres, sid, gsize,
-                     sp_digits, sp_index, sp_n);
+                     sp_digits, sp_index, sp_off);
     else
         launch_gen_t(*reinterpret_cast<const UpdateParams<float>*>(params), N, J, nsm, st, pres, sid, gsize,
-                     sp_digits, sp_index, sp_n);
+                     sp_digits, sp_index, sp_off);
 }
 
 bool generic_shape_ok(int N, int J) { return N >= 2 && N <= kMaxN && J >= 1 && J <= kGJ; }

@@ -108,7 +108,8 @@ constexpr int kL0Conv = PT_L0_CONV;
 #define PT_ACC_EARLY 1
 #endif
 constexpr bool kAccEarly = PT_ACC_EARLY != 0;
-// 3xTF32 as ONE K-sweep: A = [a_hi | a_lo | a_hi] and B = [b_hi ; b_hi ; b_lo] along K
+// 3xTF32 as ONE K-sweep: A = [a_lo | a_hi | a_hi] and B = [b_hi ; b_lo ; b_hi] along K
+// (the small products lo*hi and hi*lo first, then hi*hi)
 // (3J columns padded to the K-step), so every MMA K-step carries useful products:
 // J = 10 takes 4 MMAs (K = 32) per tile instead of 3 x 2 (K = 16 each, 10 used)
 #ifndef PT_KCAT
@@ -333,7 +334,7 @@ struct Shape {
     static constexpr int SMEM = OFF_BAR + NBAR * 8;
 };
 
-// kKcat: B = [b_hi ; b_hi ; b_lo] along K (Shape::KC rows of K), K-major canonical layout,
+// kKcat: B = [b_hi ; b_lo ; b_hi] along K (Shape::KC rows of K), K-major canonical layout,
 // b = the core block G'[(k0, j)][k1] = T[k0*GB + k1*J + j]; rows c >= J^2 and K padding 0.
 template <int J>
 __device__ __forceinline__ void load_bcat(const float* T, float* sB, int t0, int nt) {
@@ -345,7 +346,7 @@ __device__ __forceinline__ void load_bcat(const float* T, float* sB, int t0, int
             const int k1 = k % J;
             const float g = T[(c / J) * GB + k1 * J + (c % J)];
             const float hv = tf32_rna(g);
-            v = k < 2 * J ? hv : tf32_rna(g - hv);
+            v = (k >= J && k < 2 * J) ? tf32_rna(g - hv) : hv;  // [b_hi ; b_lo ; b_hi]
         }
         sB[kmaj<KC>(c, k)] = v;
     }
@@ -823,11 +824,13 @@ if constexpr (kKcat) {
             }
             const uint32_t ta = tm_lane + SH::ACOL + (k % kNA) * SH::ACOLS;
             if constexpr (kKcat) {
-                // [a_hi | a_lo | a_hi | 0] over KC columns, stored 16 (or 8) at a time
+                // [a_lo | a_hi | a_hi | 0] over KC columns (against [b_hi ; b_lo ; b_hi]: the two
+                // small products first, as in the 3-sweep order -- big-first doubled the worst
+                // full-size c5 row error to 1.9e-5), stored 16 (or 8) at a time
                 uint32_t v[SH::KC];
 #pragma unroll
                 for (int i = 0; i < SH::KC; ++i)
-                    v[i] = i < J ? hi[i] : (i < 2 * J ? lo[i - J] : (i < 3 * J ? hi[i - 2 * J] : 0u));
+                    v[i] = i < J ? lo[i] : (i < 2 * J ? hi[i - J] : (i < 3 * J ? hi[i - 2 * J] : 0u));
 #pragma unroll
                 for (int c0 = 0; c0 < SH::KC; c0 += 16) {
                     uint32_t w[16];
