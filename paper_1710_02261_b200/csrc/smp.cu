@@ -131,11 +131,29 @@ __global__ void __launch_bounds__(kUpdThreads, 1) k_update_smp2(const UpdatePara
             for (int j = 0; j < J; ++j) d[j] = 0.0;
             if (use64) {
                 const double* tb = T64 + boff;
+                if constexpr (BLK % 4 == 0) {
+                    // the block (BLK doubles, 32-byte aligned: BLK * 8 is a multiple of 32) in
+                    // 256-bit loads: a quarter of the LSU requests of 8-byte loads (the fp64-table
+                    // path was LSU-throttled, profiles/r02/smp2_c3_mode0_full.txt)
 #pragma unroll
-                for (int k = 0; k < J; ++k) {
-                    const double ak = double(ar[k]);
+                    for (int q = 0; q < BLK / 4; ++q) {
+                        double v[4];
+                        asm volatile("ld.global.nc.v4.f64 {%0,%1,%2,%3}, [%4];"
+                                     : "=d"(v[0]), "=d"(v[1]), "=d"(v[2]), "=d"(v[3])
+                                     : "l"(tb + 4 * q));
 #pragma unroll
-                    for (int j = 0; j < J; ++j) d[j] = fma(ak, __ldg(tb + k * J + j), d[j]);
+                        for (int u = 0; u < 4; ++u) {
+                            const int kj = 4 * q + u, k = kj / J, j = kj % J;
+                            d[j] = fma(double(ar[k]), v[u], d[j]);
+                        }
+                    }
+                } else {
+#pragma unroll
+                    for (int k = 0; k < J; ++k) {
+                        const double ak = double(ar[k]);
+#pragma unroll
+                        for (int j = 0; j < J; ++j) d[j] = fma(ak, __ldg(tb + k * J + j), d[j]);
+                    }
                 }
             } else {
                 const TS* tb = ts + boff;

@@ -64,8 +64,14 @@ constexpr int kCPref = 7;                    // loader: coordinates fetched this
 constexpr int kLoaders = PT_LOADERS;         // loader warps (14, 12, 13): tiles k = lp (mod kLoaders)
 static_assert(kLoaders >= 1 && kLoaders <= 3, "loader warps");
 constexpr int kCRing = 8 * kLoaders;                    // coordinate ring slots (> kCPref)
-constexpr int kNT = 3;                       // TMEM accumulator buffers
-constexpr int kNA = 4;                       // TMEM A buffers (the level-0 warps write A kNA tiles ahead)
+#ifndef PT_NT
+#define PT_NT 3
+#endif
+#ifndef PT_NA
+#define PT_NA 4
+#endif
+constexpr int kNT = PT_NT;                   // TMEM accumulator buffers
+constexpr int kNA = PT_NA;                   // TMEM A buffers (the level-0 warps write A kNA tiles ahead)
 constexpr int kStash = kNA / 2 + 1;          // a0/x stash slots per level-0 warp (its tiles k, k+2, .., k+kNA)
 #ifndef PT_KD
 #define PT_KD 4
