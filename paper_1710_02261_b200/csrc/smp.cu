@@ -160,11 +160,16 @@ __global__ void __launch_bounds__(kUpdThreads, 1) k_update_smp2(const UpdatePara
 #pragma unroll
                 for (int k = 0; k < J; ++k) {
                     const double ak = double(ar[k]);
+                    // odd j: the table value widened exactly by three integer operations into
+                    // t * 2^-896 (f2d_scaled below), paired with ak * 2^896 (exact); even j on
+                    // the XU (latency-bound kernel: neither pipe saturates)
+                    const double aks = ak * 0x1p896;
 #pragma unroll
                     for (int j = 0; j < J; ++j) {
-#ifndef PT_SMP_F2D_XU  // half of the table conversions on the ALU (latency-bound kernel, XU 37%)
+#ifndef PT_SMP_F2D_XU
                         if constexpr (std::is_same<TS, float>::value)
-                            d[j] = fma(ak, (j & 1) ? f2d_alu(tb[k * J + j]) : double(tb[k * J + j]), d[j]);
+                            d[j] = (j & 1) ? fma(aks, f2d_scaled896(tb[k * J + j]), d[j])
+                                           : fma(ak, double(tb[k * J + j]), d[j]);
                         else
 #endif
                             d[j] = fma(ak, double(tb[k * J + j]), d[j]);

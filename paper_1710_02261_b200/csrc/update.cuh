@@ -46,6 +46,15 @@ __device__ __forceinline__ double f2d_alu(float f) {
     const uint32_t hi = ((uint32_t)((int32_t)u >> 3) & 0x8FFFFFFFu) + 0x38000000u;
     return __hiloint2double((int)hi, (int)(u << 29));
 }
+// float -> double scaled by 2^-896 in three integer operations (no exponent rebias): exact for
+// every finite float, zero and subnormals included (the fp64 bias replaces the fp32 one);
+// the caller multiplies the other factor by 2^896 (exact).  Same construction as
+// update_tc.cu's f2d_scaled.
+__device__ __forceinline__ double f2d_scaled896(float f) {
+    const uint32_t u = __float_as_uint(f);
+    const uint32_t hi = (uint32_t)((int32_t)u >> 3) & 0x8FFFFFFFu;
+    return __hiloint2double((int)hi, (int)(u << 29));
+}
 // TO(x) for the level outputs.  The ALU kernel is issue-bound at two CTAs per SM (c4:
 // issue active 75%), so the one-instruction XU conversion wins over f2d_alu's four
 // (c4 3.46 -> 2.78 ms per mode); -DPT_F2D_ALU puts half of them on the ALU pipe.
