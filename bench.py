@@ -333,7 +333,17 @@ def open_peers(pt, dist, world, args):
         return
     hs = [None] * world
     dist.all_gather_object(hs, pt.ptucker_peer_handles())
-    pt.ptucker_open_peers(b"".join(hs), world)
+    ok = True
+    try:
+        pt.ptucker_open_peers(b"".join(hs), world)
+    except pt.PTuckerError as e:   # no peer access: the NCCL all-gather-v keeps the replicas fresh
+        print(f"[bench] rank {dist.get_rank()}: peer replicas not opened ({e}); NCCL all-gather-v instead",
+              file=sys.stderr, flush=True)
+        ok = False
+    flags = [None] * world
+    dist.all_gather_object(flags, ok)
+    if not all(flags):             # every rank must use the same exchange
+        pt.ptucker_set_option("exchange", 0)
 
 
 def run_ours(args, cfg):

@@ -40,6 +40,7 @@ def _init(pt, cfg):
     pt.ptucker_finalize()
     pt.ptucker_set_option("seg_len", -1)   # automatic, as bench.py runs it
     pt.ptucker_init(coords, vals, cfg.dims, [cfg.J] * len(cfg.dims), cfg.lam, cfg.seed)
+    pt.ptucker_set_option("policy", -1)    # the automatic precision policy (what bench.py runs)
     return coords, vals
 
 
