@@ -10,8 +10,6 @@
 #include <cstdio>
 #include <cstring>
 #include <map>
-#include <mutex>
-#include <thread>
 #include <string>
 #include <type_traits>
 #include <vector>
@@ -797,60 +795,52 @@ int ptucker_init(const int32_t* coords, const void* vals, int32_t vals_dtype, in
     }
     const int esz = vals_dtype == PTUCKER_F64 ? 8 : 4;
     {
-        // coordinates in range and values finite: first offending entry, scanned by
-        // all host threads (the check is O(|Omega| N) and must not dominate init)
-        int64_t bad_c = INT64_MAX, bad_v = INT64_MAX;
-        int bad_n = 0;
-        double xx = 0.0;  // sum of squares of the values (scale of the data, reading R30)
-        std::mutex mu;
-        auto scan = [&](int64_t e0, int64_t e1) {
-            int64_t bc = INT64_MAX, bv = INT64_MAX;
-            int bn = 0;
-            double sq = 0.0;
-            for (int64_t e = e0; e < e1 && bc == INT64_MAX; ++e)
-                for (int n = 0; n < order; ++n) {
-                    const int32_t c = coords[e * order + n];
-                    if (c < 0 || c >= dims[n]) {
-                        bc = e;
-                        bn = n;
-                        break;
-                    }
-                }
-            for (int64_t e = e0; e < e1; ++e) {
-                const double v = esz == 8 ? ((const double*)vals)[e] : ((const float*)vals)[e];
-                if (!std::isfinite(v)) {
-                    bv = e;
-                    break;
-                }
-                sq += v * v;
-            }
-            std::lock_guard<std::mutex> lk(mu);
-            if (bc < bad_c) bad_c = bc, bad_n = bn;
-            if (bv < bad_v) bad_v = bv;
-            xx += sq;
-        };
-        const int64_t nt = std::max<int64_t>(1, std::min<int64_t>(std::thread::hardware_concurrency(), nnz / (1 << 20)));
-        std::vector<std::thread> th;
-        for (int64_t t = 1; t < nt; ++t) th.emplace_back(scan, nnz * t / nt, nnz * (t + 1) / nt);
-        scan(0, nnz / nt);
-        for (auto& x : th) x.join();
-        if (bad_c != INT64_MAX)
-            return fail(PTUCKER_EINVAL, "coordinate %d of entry %lld out of range", bad_n, (long long)bad_c);
-        if (bad_v != INT64_MAX) return fail(PTUCKER_EINVAL, "value of entry %lld is not finite", (long long)bad_v);
-        g_xnorm_pending = std::sqrt(xx);
-    }
-    {
         if (!ujn && !find_update_kernel(vals_dtype, 1, order, J) && !generic_shape_ok(order, J))
             return fail(PTUCKER_EINVAL, "(N=%d, J=%d): J must be <= 16", order, J);
     }
-    pc.lap("validation (host)");
-    // ---- fresh context ----
-    free_all();
-    CK(cudaGetDevice(&g.device));
+    // ---- the COO on the device, validated there (coordinates in range, values finite:
+    // the first offending entry; sum of x^2 for reading R30) before the previous context is
+    // released, so an invalid call leaves it intact.  (Round 1 scanned on the host threads:
+    // ~40 ms of c5's init.)
     if (!g.stream) {
         CK(cudaStreamCreateWithFlags(&g.stream, cudaStreamNonBlocking));
         g.own_stream = true;
     }
+    DeviceArena input;
+    int32_t* d_coords = nullptr;
+    void* d_vals = nullptr;
+    CK(input.alloc((void**)&d_coords, (size_t)nnz * order * sizeof(int32_t)));
+    CK(input.alloc(&d_vals, (size_t)nnz * esz));
+    CK(cudaMemcpyAsync(d_coords, coords, (size_t)nnz * order * sizeof(int32_t), cudaMemcpyHostToDevice, S()));
+    CK(cudaMemcpyAsync(d_vals, vals, (size_t)nnz * esz, cudaMemcpyHostToDevice, S()));
+    pc.lap("H2D of the COO input", S());
+    {
+        int64_t* d_val = nullptr;  // [0] first bad coordinate key (entry * 16 + mode), [1] first bad value
+        double* d_part = nullptr;  // per-block sums of x^2 (fixed grid: a deterministic total)
+        const int vgrid = 148 * 8;
+        CK(input.alloc((void**)&d_val, 2 * sizeof(int64_t)));
+        CK(input.alloc((void**)&d_part, vgrid * sizeof(double)));
+        launch_validate_coo(d_coords, d_vals, esz, nnz, order, dims, d_val, d_part, vgrid, S());
+        CK(cudaGetLastError());
+        int64_t hv[2];
+        std::vector<double> hp(vgrid);
+        CK(cudaMemcpyAsync(hv, d_val, sizeof(hv), cudaMemcpyDeviceToHost, S()));
+        CK(cudaMemcpyAsync(hp.data(), d_part, vgrid * sizeof(double), cudaMemcpyDeviceToHost, S()));
+        CK(cudaStreamSynchronize(S()));
+        const uint64_t none = ~0ull;  // all bits set: no offending entry
+        if ((uint64_t)hv[0] != none)
+            return fail(PTUCKER_EINVAL, "coordinate %d of entry %lld out of range", (int)((uint64_t)hv[0] % 16),
+                        (long long)((uint64_t)hv[0] / 16));
+        if ((uint64_t)hv[1] != none)
+            return fail(PTUCKER_EINVAL, "value of entry %lld is not finite", (long long)hv[1]);
+        double xx = 0.0;
+        for (double v : hp) xx += v;
+        g_xnorm_pending = std::sqrt(xx);
+    }
+    pc.lap("validation (device)", S());
+    // ---- fresh context ----
+    free_all();
+    CK(cudaGetDevice(&g.device));
     g.N = order;
     g.J = J;
     g.ujn = ujn;
@@ -951,14 +941,6 @@ int ptucker_init(const int32_t* coords, const void* vals, int32_t vals_dtype, in
     }
     pc.lap("allocation + factor init", S());
     // ---- device index of every mode ----
-    DeviceArena input;
-    int32_t* d_coords = nullptr;
-    void* d_vals = nullptr;
-    CK(input.alloc((void**)&d_coords, (size_t)nnz * order * sizeof(int32_t)));
-    CK(input.alloc(&d_vals, (size_t)nnz * esz));
-    CK(cudaMemcpyAsync(d_coords, coords, (size_t)nnz * order * sizeof(int32_t), cudaMemcpyHostToDevice, S()));
-    CK(cudaMemcpyAsync(d_vals, vals, (size_t)nnz * esz, cudaMemcpyHostToDevice, S()));
-    pc.lap("H2D of the COO input", S());
     if (!g.comm) {  // no communicator: a single rank, or an emulated rank of a partition (tests)
         g.world = g.emu_world;
         g.rank = g.emu_rank;

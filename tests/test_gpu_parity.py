@@ -398,3 +398,27 @@ def test_graph_sweep_bit_identical(pt, orc, name, scale):
         assert np.array_equal(runs[0][0][n], runs[1][0][n]), n
     assert np.array_equal(runs[0][1], runs[1][1])
     assert runs[0][2] == runs[1][2]
+
+
+def test_invalid_data_keeps_context(pt, orc):
+    """ptucker_init validates the COO on the device before releasing the previous context:
+    an out-of-range coordinate or a non-finite value is EINVAL naming the first offending
+    entry (and mode), and the previous context keeps working."""
+    cfg = synth.small("c2", 0.01)
+    coords, vals = init_cfg(pt, cfg)
+    pt.ptucker_sweep()
+    e0 = pt.ptucker_error()
+    bad = coords.copy()
+    bad[123, 1] = cfg.dims[1]          # entry 123, mode 1 out of range
+    bad[456, 0] = -1
+    with pytest.raises(pt.PTuckerError) as e:
+        pt.ptucker_init(bad, vals, cfg.dims, [cfg.J] * 3, cfg.lam, 0)
+    assert e.value.code == pt.PTUCKER_EINVAL and "coordinate 1 of entry 123" in str(e.value)
+    badv = vals.copy()
+    badv[77] = np.inf
+    badv[900] = np.nan
+    with pytest.raises(pt.PTuckerError) as e:
+        pt.ptucker_init(coords, badv, cfg.dims, [cfg.J] * 3, cfg.lam, 0)
+    assert e.value.code == pt.PTUCKER_EINVAL and "entry 77" in str(e.value)
+    assert pt.ptucker_error() == e0            # the previous context is intact
+    pt.ptucker_sweep()
