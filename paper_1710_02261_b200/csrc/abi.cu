@@ -974,13 +974,39 @@ int ptucker_init(const int32_t* coords, const void* vals, int32_t vals_dtype, in
         // kind-1 modes on the tensor cores: lanes in (i_s, length) order, one i_s per group
         const bool aux_groups = smode >= 0 && g.tc_table && g.use_tc && vals_dtype == PTUCKER_F32 &&
                                 find_update_kernel_tc(1, J) != nullptr;
-        CK(build_mode_sell(d_coords, d_vals, esz, nnz, order, n, g.Jv.j[n], g.seg_len_eff, m.bounds[g.rank],
+        // Per-mode S for the tensor-core kernel (automatic S only): its 128-lane groups are
+        // assigned to the CTAs statically, so with few long groups the CTA with one group more
+        // than the average sets the time (c3's table modes: 624 groups of ~256 tiles on 148
+        // CTAs, 5 vs 4.2); take the largest S <= the global one that gives >= 8 groups per SM,
+        // when one down to 32 does (c3 modes 2/3: S = 128, update 1.085 -> 1.045 ms; S = 64 was
+        // slower, 1.12 ms, its heavy-row partials doubling the finalize).  Computed from all
+        // rows (not this rank's block), so it does not depend on the number of GPUs.
+        int S_n = g.seg_len_eff;
+        const bool on_tc = !g.generic && vals_dtype == PTUCKER_F32 && g.use_tc &&
+                           ((order == 3 && find_update_kernel_tc(1, J) != nullptr) || aux_groups);
+        if (g.seg_len < 0 && on_tc) {
+            int nsm_dev = 148;
+            CK(cudaDeviceGetAttribute(&nsm_dev, cudaDevAttrMultiProcessorCount, g.device));
+            for (int Sc = g.seg_len_eff; Sc >= 32; Sc /= 2) {
+                int64_t segs = 0;
+                for (int64_t r = 0; r < dims[n]; ++r) {
+                    const int64_t len = m.h_row_ptr[r + 1] - m.h_row_ptr[r];
+                    segs += len == 0 ? 1 : (len + Sc - 1) / Sc;
+                }
+                if (segs / 128 >= 8 * (int64_t)nsm_dev) {
+                    S_n = Sc;
+                    break;
+                }
+            }
+        }
+        m.seg_len = S_n;
+        CK(build_mode_sell(d_coords, d_vals, esz, nnz, order, n, g.Jv.j[n], S_n, m.bounds[g.rank],
                            m.bounds[g.rank + 1], smode, m, g.arena, g.scratch, S(), aux_groups, g.cache_on));
         {   // most segments of one of this rank's rows (the heavy-row finalize picks its kernels by it)
             int64_t mx = 0;
             for (int64_t r = m.bounds[g.rank]; r < m.bounds[g.rank + 1]; ++r)
                 mx = std::max<int64_t>(mx, m.h_row_ptr[r + 1] - m.h_row_ptr[r]);
-            m.hmaxseg = (mx + g.seg_len_eff - 1) / g.seg_len_eff;
+            m.hmaxseg = (mx + S_n - 1) / S_n;
         }
         pc.lap("SELL segments + scatter", S());
     }
@@ -1667,10 +1693,10 @@ int ptucker_info(char* buf, int32_t len) {
         const ModeIndex& m = g.mi[n];
         snprintf(tmp, sizeof(tmp),
                  "%s{\"I\": %lld, \"rows\": [%lld, %lld], \"segments\": %lld, \"slices\": %lld, \"slots\": %lld, "
-                 "\"heavy_rows\": %lld, \"smp\": %d, \"tc_table\": %s}",
+                 "\"heavy_rows\": %lld, \"smp\": %d, \"tc_table\": %s, \"seg_len\": %d}",
                  n ? ", " : "", (long long)m.I, (long long)m.r0, (long long)m.r1, (long long)m.nsegments,
                  (long long)m.nslices, (long long)m.nslots, (long long)m.nheavy, g.use_smp ? g.smp[n].kind : 0,
-                 m.aux_groups ? "true" : "false");
+                 m.aux_groups ? "true" : "false", m.seg_len);
         s += tmp;
     }
     s += "]}";
