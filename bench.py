@@ -31,7 +31,7 @@ sys.path.insert(0, ROOT)
 from gen import synth  # noqa: E402
 
 METRIC = "observed entries/sec per full ALS iteration"
-POLICY = {"auto": -1, "F32-A": 0, "F32-B": 1, "F32-C": 2}
+POLICY = {"auto": -1, "F32-A": 0, "F32-B": 1, "F32-C": 2, "F32-C2": 3}
 UNIT = "entries/s"
 
 
@@ -89,7 +89,7 @@ def roofline(N, J, policy, info, l0_group, nsm, clk_mhz, entries, launch_s, dtyp
             xu = J * nparts + 1
         wtc = inner
     else:
-        n64 = {"F32-A": 0, "F32-B": 1, "F32-C": N - 2}[policy]
+        n64 = {"F32-A": 0, "F32-B": 1, "F32-C": N - 2, "F32-C2": N - 3 if N >= 5 else N - 2}[policy]
         w32, w64, wtc = inner + sum(levels[n64:]), sum(levels[:n64]) + bc, 0
         xu = sum(J ** (L + 1) for L in range(min(n64, N - 2)))  # fp32 inputs of the fp64 levels
     sv = 8 if dtype == "f64" else 4
@@ -383,6 +383,9 @@ def run_ours(args, cfg):
     if args.l2_persist_mb is not None:
         pt.ptucker_set_option("l2_persist_mb", args.l2_persist_mb)
     pt.ptucker_set_option("pack_gathers", args.pack_gathers)
+    for kv in args.opt:  # experiments: any library option (include/ptucker.h), e.g. fin_inline=0
+        k, v = kv.split("=")
+        pt.ptucker_set_option(k, int(v))
     open_peers(pt, dist, world, args)
     pt.ptucker_synchronize()
     init_s = time.perf_counter() - t0
@@ -570,6 +573,7 @@ def main():
                     help="P-Tucker-Approx: truncate the core by rate p after every iteration (0 = P-Tucker)")
     ap.add_argument("--ref-seconds", type=float, default=12.0, help="oracle seconds per sampled step (upper bound)")
     ap.add_argument("--ref-total", type=float, default=150.0, help="reference arm: seconds for all W + K sampled steps")
+    ap.add_argument("--opt", action="append", default=[], help="library option key=value (repeatable; experiments)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()

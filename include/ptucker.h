@@ -186,7 +186,9 @@ int ptucker_get_partition(int32_t n, int64_t* bounds);
 /* Options (set after init unless noted):
  *  "policy"       precision of the fp32 contraction: -1 = automatic
  *                 (default: every outer TTV stage in fp64), 0 = F32-A (all fp32), 1 = F32-B
- *                 (outermost stage fp64), 2 = F32-C (all outer stages fp64)
+ *                 (outermost stage fp64), 2 = F32-C (all outer stages fp64), 3 = F32-C2 (order 5:
+ *                 every outer stage in fp64 but the innermost one's parent: J^3 instead of J^4
+ *                 fp32 -> fp64 conversions per entry; other orders: as 2)
  *  "tc"           1 = order-3 fp32 updates run the innermost contraction on the tcgen05 tensor
  *                 cores (3xTF32, default); 0 = the all-ALU kernel
  *  "smp"          1 = small-mode precontraction where it applies (order 4, two other modes with
@@ -215,6 +217,13 @@ int ptucker_get_partition(int32_t n, int64_t* bounds);
  *  "seg_len"      segment length S of the index (before init): -1 = automatic (default: the
  *                 power of two >= |Omega| / (SMs x 128) in [8, 256]), else 1..2^20
  *  "time_kernels" 1 = bracket every kernel launch with CUDA events (ptucker_kernel_stats)
+ *  "fin_inline"   1 = rows cut into 2..64 segments (heavy rows) are solved inside the
+ *                 tensor-core / ALU / table update kernels by the lane that stores the row's
+ *                 last partial (same additions, same bits as the finalize launch); measured
+ *                 slower (c1 0.10 -> 0.19, c2 0.33 -> 0.38 ms per iteration: one lane's serial
+ *                 sum and solve lengthen the kernel's tail).  0 = a separate finalize launch
+ *                 (default).  Modes with longer rows, the SMP and the generic kernels always
+ *                 use the finalize launch
  *  "l0_group"     tensor-core kernel, F32-B: level-0 terms summed in fp32 in runs of g before
  *                 the fp64 sum (1 = every term in fp64, default; 2; 5 fails the 1e-5 row bound)
  *  "l2_persist_mb" L2 set-aside (MB) for the evict_last factor-row gathers: -1 = the device

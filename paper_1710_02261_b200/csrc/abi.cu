@@ -26,7 +26,9 @@ const UpdateKernel* find_update_kernel(int prec, int l64, int N, int J) {
     if (prec == PTUCKER_F32 && N <= 3 && l64 > 1) l64 = 1;  // N = 3 has a single outer level
     const UpdateKernel* t = prec == PTUCKER_F64 ? update_kernels_f64(&cnt)
                             : (l64 == 0 ? update_kernels_f32a(&cnt)
-                                        : (l64 == 1 ? update_kernels_f32b(&cnt) : update_kernels_f32c(&cnt)));
+                                        : (l64 == 1 ? update_kernels_f32b(&cnt)
+                                                    : (N == 5 && l64 == 2 ? update_kernels_f32c2(&cnt)
+                                                                          : update_kernels_f32c(&cnt))));
     for (int i = 0; i < cnt; ++i)
         if (t[i].N == N && t[i].J == J) return &t[i];
     return nullptr;
@@ -113,6 +115,8 @@ struct Ctx {
     void* coo_v = nullptr;
     int use_tc = 1;                          // option "tc"
     int l0_group = 1;                        // option "l0_group" (tensor-core kernel, F32-B)
+    int fin_inline = 0;                      // option "fin_inline": heavy rows (<= 64 segments) solved in the update kernel
+    bool inline_used = false;                // the last update launch finished its heavy rows itself
     int64_t l2_persist_mb = -1;              // option "l2_persist_mb": L2 set-aside for evict_last lines (-1 = max)
     int pack_gathers = 0;                    // option "pack_gathers": J = 10 tensor-core gathers from packed tables
     int rows_l1[kMaxN] = {0};                // per updated mode: gather rows through L1 (skewed other modes)
@@ -310,6 +314,11 @@ UpdateParams<TS> make_params(int n, bool literal) {
     p.gtail[1] = g.pk_tail[1];
     p.l0_group = g.l0_group;
     p.rows_l1 = g.rows_l1[n];
+    if (!literal && g.fin_inline && m.nheavy > 0 && m.hmaxseg <= 64) {
+        // (pointers offset by the block's first row: the kernels index them by global row)
+        p.seg_done = m.seg_done - m.hr0;
+        p.row_pbase = m.row_pbase - m.hr0;
+    }
     if (pushing()) {
         p.peers.n = g.npeer;
         for (int r = 0; r < g.npeer; ++r) p.peers.base[r] = g.peer_A[n][r];
@@ -319,6 +328,7 @@ UpdateParams<TS> make_params(int n, bool literal) {
 
 int launch_update_kernel(int n, bool literal) {
     const int grid = literal ? g.grid_lit : g.grid_upd;
+    g.inline_used = false;
     if (g.mi[n].nslices == 0) return PTUCKER_OK;
     CK(cudaMemsetAsync(g.d_work, 0, sizeof(unsigned int), S()));
     const Ctx::Smp& sp = g.smp[n];
@@ -330,10 +340,12 @@ int launch_update_kernel(int n, bool literal) {
         bool ok;
         if (g.prec == PTUCKER_F64) {
             UpdateParams<double> p = make_params<double>(n, false);
+            p.seg_done = nullptr;  // (the SMP kernel leaves its heavy rows to the finalize launch)
             ok = launch_smp2_update(&p, 8, g.J, (const double*)g.smp_T, nullptr, sp.elems, sp.ir, sp.is1, sp.is2,
                                     (int)g.dims[sp.s2], 1, g.nsm, S());
         } else {
             UpdateParams<float> p = make_params<float>(n, false);
+            p.seg_done = nullptr;
             ok = launch_smp2_update(&p, 4, g.J, (const double*)g.smp_T, g.smp_T32, sp.elems, sp.ir, sp.is1, sp.is2,
                                     (int)g.dims[sp.s2], mode, g.nsm, S());
         }
@@ -365,17 +377,20 @@ int launch_update_kernel(int n, bool literal) {
         if (g.prec == PTUCKER_F64) {
             UpdateParams<double> p = make_params<double>(n, false);
             fill(p);
+            g.inline_used = p.seg_done != nullptr;
             ok = launch_table_update(&p, 8, g.J, g.nsm, S());
         } else if (ktc) {  // tensor-core kernel with the group's table block as the core
             UpdateParams<float> p = make_params<float>(n, false);
             fill(p);
             p.gmain[0] = p.gmain[1] = p.gtail[0] = p.gtail[1] = nullptr;
             CK(cudaMemsetAsync(g.d_work, 0, sizeof(unsigned int), S()));
+            g.inline_used = p.seg_done != nullptr;
             ktc->launch(&p, false, g.nsm, S());
             ok = true;
         } else {
             UpdateParams<float> p = make_params<float>(n, false);
             fill(p);
+            g.inline_used = p.seg_done != nullptr;
             ok = launch_table_update(&p, 4, g.J, g.nsm, S());
         }
         if (!ok) return fail(PTUCKER_EINVAL, "no table kernel for J=%d", g.J);
@@ -413,10 +428,12 @@ int launch_update_kernel(int n, bool literal) {
         if (g.prec == PTUCKER_F64) {
             UpdateParams<double> p = make_params<double>(n, false);
             p.Gp = (const double*)g.G;
+            p.seg_done = nullptr;  // (the generic kernel leaves its heavy rows to the finalize launch)
             launch_update_generic(&p, 8, g.N, g.Jv, g.nsm, S(), pres, g.mi[n].sid, spd, spi, spo);
         } else {
             UpdateParams<float> p = make_params<float>(n, false);
             p.Gp = (const float*)g.G;
+            p.seg_done = nullptr;
             launch_update_generic(&p, 4, g.N, g.Jv, g.nsm, S(), pres, g.mi[n].sid, spd, spi, spo);
         }
         CK(cudaGetLastError());
@@ -426,6 +443,7 @@ int launch_update_kernel(int n, bool literal) {
 
     if (g.prec == PTUCKER_F64) {
         UpdateParams<double> p = make_params<double>(n, literal);
+        g.inline_used = p.seg_done != nullptr;
         k->launch(&p, literal, grid, S());
     } else {
         const bool packed = g.pack_gathers && !literal && k != g.kern_alu && g.J == 10;
@@ -448,6 +466,7 @@ int launch_update_kernel(int n, bool literal) {
         }
         UpdateParams<float> p = make_params<float>(n, literal);
         if (!packed) p.gmain[0] = p.gmain[1] = p.gtail[0] = p.gtail[1] = nullptr;
+        g.inline_used = p.seg_done != nullptr;
         k->launch(&p, literal, grid, S());
     }
     CK(cudaGetLastError());
@@ -468,6 +487,7 @@ int rebuild_gp() {
 int policy_l64() {
     if (g.prec == PTUCKER_F64) return 1;
     const int all = g.N >= 4 ? g.N - 2 : 1;
+    if (g.policy == 3) return g.N >= 5 ? g.N - 3 : all;  // F32-C2 (order 5): all outer levels but the innermost's parent
     if (g.policy >= 0) return g.policy == 2 ? all : g.policy;
     return all;
 }
@@ -656,7 +676,7 @@ int ptucker_set_option(const char* key, int64_t value) {
         return PTUCKER_OK;
     }
     if (k == "policy") {
-        if (value < -1 || value > 2) return fail(PTUCKER_EINVAL, "policy must be -1 (auto), 0, 1 or 2");
+        if (value < -1 || value > 3) return fail(PTUCKER_EINVAL, "policy must be -1 (auto), 0, 1, 2 or 3");
         g.policy = (int)value;
         if (g.inited) return choose_kernel();
         return PTUCKER_OK;
@@ -685,6 +705,11 @@ int ptucker_set_option(const char* key, int64_t value) {
     if (k == "l2_persist_mb") {
         g.l2_persist_mb = value;
         return g.inited ? apply_l2_persist() : PTUCKER_OK;
+    }
+    if (k == "fin_inline") {
+        if (value != 0 && value != 1) return fail(PTUCKER_EINVAL, "fin_inline must be 0 or 1");
+        g.fin_inline = (int)value;
+        return PTUCKER_OK;
     }
     if (k == "l0_group") {
         if (value != 1 && value != 2 && value != 5) return fail(PTUCKER_EINVAL, "l0_group must be 1, 2 or 5");
@@ -1102,7 +1127,7 @@ int ptucker_update_mode(int32_t n) {
     rc = timed("update", [&]() -> int { return launch_update_kernel(n, false); }, n);
     if (rc) return rc;
     ModeIndex& m = g.mi[n];
-    if (m.nheavy > 0) {
+    if (m.nheavy > 0 && !g.inline_used) {
         rc = timed("finalize", [&]() -> int {
             PeerRows pr;
             if (pushing()) {
@@ -1685,7 +1710,7 @@ int ptucker_info(char* buf, int32_t len) {
              "\"lambda\": %.17g, \"seg_len\": %d, \"rank\": %d, \"world\": %d, \"grid_update\": %d, "
              "\"threads_per_cta\": %d, \"smem_core_bytes\": %d, \"kernel_launches\": %lld, \"tensor_cores\": %s, \"generic\": %s, \"modes\": [",
              g.inited ? "true" : "false", g.N, g.J, g.prec == PTUCKER_F64 ? "f64" : "f32",
-             g.prec == PTUCKER_F64 ? "F64" : (policy_l64() == 0 ? "F32-A" : (policy_l64() == 1 ? "F32-B" : "F32-C")), (long long)g.nnz, g.lambda, g.seg_len_eff,
+             g.prec == PTUCKER_F64 ? "F64" : (policy_l64() == 0 ? "F32-A" : (policy_l64() == 1 ? "F32-B" : (g.N >= 5 && policy_l64() == g.N - 3 ? "F32-C2" : "F32-C"))), (long long)g.nnz, g.lambda, g.seg_len_eff,
              g.rank, g.world, g.grid_upd, kUpdThreads, g.gp_elems * g.esz, (long long)g.launches,
              (g.kern && g.kern != g.kern_alu) ? "true" : "false", g.generic ? "true" : "false");
     s += tmp;

@@ -89,13 +89,15 @@ __global__ void k_row_count(const int64_t* seg_start_g, int64_t nrows, int64_t I
 }
 
 __global__ void k_heavy_list(int64_t r0, int64_t nrows, int PW, const int64_t* nseg_r, const int64_t* hidx,
-                             const int64_t* hbase, int32_t* hrow, int32_t* hnseg, int64_t* hpbase) {
+                             const int64_t* hbase, int32_t* hrow, int32_t* hnseg, int64_t* hpbase,
+                             int64_t* row_pbase) {
     for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < nrows; t += (int64_t)gridDim.x * blockDim.x) {
         if (nseg_r[t] > 1) {
             hrow[hidx[t]] = (int32_t)(r0 + t);
             hnseg[hidx[t]] = (int32_t)nseg_r[t];
             hpbase[hidx[t]] = hbase[t] * PW;
         }
+        row_pbase[t] = nseg_r[t] > 1 ? hbase[t] * PW : -1;
     }
 }
 
@@ -386,8 +388,15 @@ cudaError_t build_mode_sell(const int32_t* d_coords, const void* d_vals, int ele
     IB_CHECK(dalloc(&mi.hpbase, mi.nheavy, arena));
     IB_CHECK(dalloc(&mi.partials, mi.npartial_doubles, arena));
     IB_CHECK(dalloc(&mi.hrec, mi.nheavy * PW, arena));
-    if (nrows > 0)
-        k_heavy_list<<<grid_for(nrows), 256, 0, st>>>(r0, nrows, PW, nseg_r, hidx, hbase, mi.hrow, mi.hnseg, mi.hpbase);
+    mi.hr0 = r0;
+    if (mi.nheavy > 0) {
+        IB_CHECK(dalloc(&mi.seg_done, nrows, arena));
+        IB_CHECK(dalloc(&mi.row_pbase, nrows, arena));
+        IB_CHECK(cudaMemsetAsync(mi.seg_done, 0, sizeof(int32_t) * nrows, st));
+    }
+    if (nrows > 0 && mi.nheavy > 0)
+        k_heavy_list<<<grid_for(nrows), 256, 0, st>>>(r0, nrows, PW, nseg_r, hidx, hbase, mi.hrow, mi.hnseg, mi.hpbase,
+                                                      mi.row_pbase);
     if (ngroups > 0)
         k_group_fill<<<grid_for(ngroups), 256, 0, st>>>(group_ptr, g0, ngroups, Is, S, PW, seg_start_g, nseg_r, hbase,
                                                         seg_row, seg_src, seg_aux, seg_len, seg_key, seg_pidx,

@@ -54,6 +54,9 @@ struct ModeIndex {
     int64_t* hpbase = nullptr;
     double* partials = nullptr;
     double* hrec = nullptr;          // [nheavy][PW] summed records (heavy-row finalize scratch)
+    int64_t hr0 = 0;                 // first row of this rank's block (seg_done / row_pbase index row - hr0)
+    int32_t* seg_done = nullptr;     // [rows of the block] heavy-row segment counters (in-kernel finalize)
+    int64_t* row_pbase = nullptr;    // [rows of the block] first partial of a heavy row (else unused)
     int32_t* sid = nullptr;          // [nslots] input entry id per SELL slot (P-Tucker-Cache only)
     std::vector<int64_t> bounds;     // world+1 row-block bounds
 };

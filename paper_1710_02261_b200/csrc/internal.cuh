@@ -107,6 +107,8 @@ struct UpdateParams {
     PeerRows peers;               // multi-GPU push: the other ranks' replicas of A^(n) (n = 0: none)
     int64_t dim_other[kMaxN - 1]; // I of the other modes (same order as A[]) -- bounds checks
     int64_t dim_n;                // I_n
+    int32_t* seg_done;            // heavy rows solved in the update kernel: per-row segment counters (null: off)
+    const int64_t* row_pbase;     //   per-row first partial (heavy rows of this mode)
 };
 
 using UpdateLauncher = void (*)(const void* params, bool literal, int grid, cudaStream_t st);
@@ -123,6 +125,7 @@ struct UpdateKernel {
 const UpdateKernel* update_kernels_f32a(int* count);
 const UpdateKernel* update_kernels_f32b(int* count);
 const UpdateKernel* update_kernels_f32c(int* count);
+const UpdateKernel* update_kernels_f32c2(int* count);  // order 5, l64 = 2 (policy 3)
 const UpdateKernel* update_kernels_f64(int* count);
 // Returns nullptr when (prec, l64, N, J) was not compiled.
 const UpdateKernel* find_update_kernel(int prec, int l64, int N, int J);

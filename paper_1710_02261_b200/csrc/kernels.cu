@@ -186,7 +186,58 @@ __global__ void __launch_bounds__(128) k_heavy_solve(int64_t nheavy, const int32
 }
 
 // Heavy rows with at most kSmallSeg segments each, one launch (small tensors whose
-// automatic S makes most rows heavy: c1, c2): a warp per row, lane l summing components
+// automatic S makes most rows heavy: c1, c2): a thread per row sums its segments' records
+// in segment order -- the additions of k_heavy_sum_small, so the same bits -- straight into
+// registers (segments outer, the PW independent components inner: PW loads in flight per
+// segment) and solves.  (Round 2's warp per row with lane 0 solving ran 31 us per c2 mode:
+// 5.6 waves of one serial solve per warp.)
+template <typename T, int JC>
+__global__ void __launch_bounds__(64) k_heavy_thread(int64_t nheavy, const int32_t* hrow, const int32_t* hnseg,
+                                                     const int64_t* hpbase, const double* partials, double lambda,
+                                                     T* An, int lda, double* sse_row, int* fail, const PeerRows peers) {
+    constexpr int NB = JC * (JC + 1) / 2;
+    for (int64_t h = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; h < nheavy; h += (int64_t)gridDim.x * blockDim.x) {
+        const int nseg = hnseg[h];
+        const double* src = partials + hpbase[h];
+        double B[NB], c[JC], s2 = 0.0;
+#pragma unroll
+        for (int q = 0; q < NB; ++q) B[q] = 0.0;
+#pragma unroll
+        for (int q = 0; q < JC; ++q) c[q] = 0.0;
+        for (int s = 0; s < nseg; ++s) {
+#pragma unroll
+            for (int q = 0; q < NB; ++q) B[q] += __ldg(src + (int64_t)q * nseg + s);
+#pragma unroll
+            for (int q = 0; q < JC; ++q) c[q] += __ldg(src + (int64_t)(NB + q) * nseg + s);
+            s2 += __ldg(src + (int64_t)(NB + JC) * nseg + s);
+        }
+        const int row = hrow[h];
+        double a[JC];
+        const bool ok = chol_solve<JC>(B, c, lambda, a);
+        if (!ok) {
+            atomicCAS(fail, 0, row + 1);
+#pragma unroll
+            for (int j = 0; j < JC; ++j) a[j] = 0.0;
+        }
+        T* out = An + (int64_t)row * lda;
+        double sse = s2, ac = 0.0, aa = 0.0, ec = 0.0;
+#pragma unroll
+        for (int j = 0; j < JC; ++j) {
+            const T st = T(a[j]);
+            out[j] = st;
+            const double at = double(st);
+            sse = fma(-2.0 * at, c[j], sse);
+            ac = fma(a[j], c[j], ac);
+            aa = fma(a[j], a[j], aa);
+            ec = fma(at - a[j], c[j] - lambda * a[j], ec);
+        }
+        sse_row[row] = sse + (ac - lambda * aa + 2.0 * ec);  // heavy_solve_row's expression
+        push_row(peers, out, row, lda * (int)sizeof(T));
+    }
+}
+
+// Few such heavy rows (c1: 100 per mode, fewer than the GPU's thread slots would fill): a
+// warp per row, lane l summing components
 // l, l + 32, ... over the row's segments in order -- the additions of k_heavy_sum_small, so
 // the same bits -- into shared memory, then lane 0 solves from there.
 template <typename T, int JC>
@@ -253,7 +304,7 @@ __device__ __forceinline__ void heavy_solve_row(const double* rec, int J, int ro
             aa = fma(a[j], a[j], aa);
             ec = fma(at - a[j], c[j] - lambda * a[j], ec);
         }
-        sse_row[row] = sse + ac - lambda * aa + 2.0 * ec;
+        sse_row[row] = sse + (ac - lambda * aa + 2.0 * ec);  // the update kernels' expression (same bits inline)
         push_row(peers, out, row, lda * (int)sizeof(T));
     }
 }
@@ -264,14 +315,36 @@ void launch_heavy_finalize(int64_t nheavy, const int32_t* hrow, const int32_t* h
                            int64_t max_seg) {
     if (nheavy <= 0) return;
     if (max_seg <= kSmallSeg && (J == 2 || J == 3 || J == 4 || J == 5 || J == 8 || J == 10)) {
-        const unsigned gf = (unsigned)std::min<int64_t>((nheavy + 3) / 4, 148 * 32);
-#define PT_HFF(JC)                                                                                               \
+        // many rows: a thread per row (c2: 31 -> 15 us per mode); few rows: a warp per row (c1: the
+        // thread version's one-thread serial sums ran 23 us against 8.6); the same bits either way
+        if (nheavy < 148 * 16) {
+            const unsigned gw = (unsigned)std::min<int64_t>((nheavy + 3) / 4, 148 * 32);
+#define PT_HFW(JC)                                                                                               \
     if (elem_bytes == 8)                                                                                         \
-        k_heavy_warp<double, JC><<<gf, 128, 0, st>>>(nheavy, hrow, hnseg, hpbase, partials, lambda, (double*)An,   \
+        k_heavy_warp<double, JC><<<gw, 128, 0, st>>>(nheavy, hrow, hnseg, hpbase, partials, lambda, (double*)An,   \
                                                      lda, sse_row, fail, peers);                                 \
     else                                                                                                         \
-        k_heavy_warp<float, JC><<<gf, 128, 0, st>>>(nheavy, hrow, hnseg, hpbase, partials, lambda, (float*)An,     \
+        k_heavy_warp<float, JC><<<gw, 128, 0, st>>>(nheavy, hrow, hnseg, hpbase, partials, lambda, (float*)An,     \
                                                     lda, sse_row, fail, peers);
+            switch (J) {
+                case 2: PT_HFW(2) break;
+                case 3: PT_HFW(3) break;
+                case 4: PT_HFW(4) break;
+                case 5: PT_HFW(5) break;
+                case 8: PT_HFW(8) break;
+                default: PT_HFW(10) break;
+            }
+#undef PT_HFW
+            return;
+        }
+        const unsigned gf = (unsigned)std::min<int64_t>((nheavy + 63) / 64, 148 * 16);
+#define PT_HFF(JC)                                                                                               \
+    if (elem_bytes == 8)                                                                                         \
+        k_heavy_thread<double, JC><<<gf, 64, 0, st>>>(nheavy, hrow, hnseg, hpbase, partials, lambda, (double*)An,  \
+                                                      lda, sse_row, fail, peers);                                \
+    else                                                                                                         \
+        k_heavy_thread<float, JC><<<gf, 64, 0, st>>>(nheavy, hrow, hnseg, hpbase, partials, lambda, (float*)An,    \
+                                                     lda, sse_row, fail, peers);
         switch (J) {
             case 2: PT_HFF(2) break;
             case 3: PT_HFF(3) break;

@@ -202,6 +202,33 @@ __device__ __forceinline__ void compute_delta(const TS* __restrict__ g, const TF
 
 __host__ __device__ constexpr int up_idx(int i, int j, int J) { return i * J - i * (i - 1) / 2 + (j - i); }
 
+// Heavy rows finished inside the update kernel (p.seg_done set; rows of at most 64
+// segments): the lane that stores a segment's partial (B, c, sum x^2) counts it in
+// seg_done[row]; the lane whose count completes the row (a multiple of its segment count:
+// the counters are never reset) sums the row's partials in segment order -- the additions
+// of k_heavy_warp, so the same bits -- and then solves the row like a one-segment row.
+// Replaces the separate finalize launch (c2: 31 us per mode).
+template <int J>
+__device__ __forceinline__ bool heavy_take_row(int32_t* seg_done, const int64_t* row_pbase, const double* partials,
+                                               int row, int nseg, double (&B)[J * (J + 1) / 2], double (&c)[J],
+                                               double& s2) {
+    constexpr int NB = J * (J + 1) / 2;
+    __threadfence();  // this lane's partial stores before its count
+    const int old = atomicAdd(seg_done + row, 1);
+    if ((old + 1) % nseg != 0) return false;
+    __threadfence();  // every other segment's partial (counted before) is visible
+    const double* src = partials + row_pbase[row];
+#pragma unroll
+    for (int q = 0; q < NB + J + 1; ++q) {
+        double acc = 0.0;
+        for (int s = 0; s < nseg; ++s) acc += __ldcg(src + (int64_t)q * nseg + s);
+        if (q < NB) B[q < NB ? q : 0] = acc;
+        else if (q < NB + J) c[q < NB + J && q >= NB ? q - NB : 0] = acc;
+        else s2 = acc;
+    }
+    return true;
+}
+
 // In-register fp64 Cholesky solve of a (B + lam I) = c (Eq. 9).  B is the
 // packed upper triangle; it is overwritten by L^T.  Returns false on a
 // non-positive (or NaN) pivot.
@@ -450,7 +477,18 @@ __global__ void __launch_bounds__(kUpdThreads, upd_min_blocks(J, (int)sizeof(TS)
         } else {
             if (row < 0) continue;
             const int64_t pidx = p.lane_pidx[slot];
-            if (pidx < 0) {
+            bool solve = pidx < 0;
+            if (!solve) {
+                const int st = p.lane_pstride[slot];
+                double* dst = p.partials + pidx;
+#pragma unroll
+                for (int q = 0; q < NB; ++q) dst[(int64_t)q * st] = B[q];
+#pragma unroll
+                for (int q = 0; q < J; ++q) dst[(int64_t)(NB + q) * st] = c[q];
+                dst[(int64_t)(NB + J) * st] = s2;
+                if (p.seg_done) solve = heavy_take_row<J>(p.seg_done, p.row_pbase, p.partials, row, st, B, c, s2);
+            }
+            if (solve) {
                 double a[J];
                 const bool ok = chol_solve<J>(B, c, p.lambda, a);
                 if (!ok) {
@@ -490,14 +528,6 @@ __global__ void __launch_bounds__(kUpdThreads, upd_min_blocks(J, (int)sizeof(TS)
                                              (int64_t)row * p.lda * (int64_t)sizeof(TS))[q] = v;
                 }
                 p.sse_row[row] = sse;
-            } else {
-                const int st = p.lane_pstride[slot];
-                double* dst = p.partials + pidx;
-#pragma unroll
-                for (int q = 0; q < NB; ++q) dst[(int64_t)q * st] = B[q];
-#pragma unroll
-                for (int q = 0; q < J; ++q) dst[(int64_t)(NB + q) * st] = c[q];
-                dst[(int64_t)(NB + J) * st] = s2;
             }
         }
     }

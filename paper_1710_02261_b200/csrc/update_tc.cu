@@ -39,6 +39,7 @@
 // Groups are assigned statically (serpentine over the CTAs; SELL groups are
 // sorted by length, so neighbouring CTAs get near-equal work), so every role
 // knows the CTA's whole tile sequence in advance.
+#include <cuda_fp16.h>
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -77,6 +78,19 @@ constexpr int kStash = kNA / 2 + 1;          // a0/x stash slots per level-0 war
 #define PT_KD 4
 #endif
 constexpr int kD = PT_KD;                        // delta ring slots (level 0 -> normal equations)
+// delta handoff through hardware named barriers (bar.arrive by the level-0 warp, bar.sync by
+// the normal-equation warp; ids 1 + 4 kD): the waiting warp blocks in hardware instead of
+// polling its mbarrier -- those polls were ~40% of the kernel's issued instructions
+// (profiles/r02/tc_f16_c5_full.txt: the d_full retry loop and the row-ring wait)
+#ifndef PT_NBAR
+#define PT_NBAR 0
+#endif
+constexpr bool kNbar = PT_NBAR != 0;
+#ifndef PT_SPLIT_LATE
+#define PT_SPLIT_LATE 0
+#endif
+constexpr bool kSplitLate = PT_SPLIT_LATE != 0;  // level-0 warps split tile k + kNA after (not before) tile k
+static_assert(!kNbar || 1 + 4 * kD <= 16, "named barriers: 4 quarters x kD slots + barrier 0");
 constexpr int kRegLaunch = 65536 / kThreads / 8 * 8;  // registers per thread at launch (128)
 #ifndef PT_REG_L0
 #define PT_REG_L0 136
@@ -122,6 +136,22 @@ constexpr bool kAccEarly = PT_ACC_EARLY != 0;
 #define PT_KCAT 1
 #endif
 constexpr bool kKcat = PT_KCAT != 0;
+// The same three products with fp16 operands (kind::f16: K = 16 per MMA at twice the tf32
+// rate).  An fp16 value carries the same 11 significant bits as tf32, so a = hi + lo keeps
+// 22 bits either way; the narrower exponent range is handled by exact power-of-two
+// scalings: every gathered a1 row by 2^sA (its largest |element| to [2^14, 2^15)) and the
+// core by 2^sG (the same for max |G|), undone exactly in fp64 by the level-0 weights
+// (a0 * 2^-(sA+sG)).  An element far below its row's (or the core's) maximum loses
+// relative precision to fp16 subnormals, but its absolute error stays below 2^-38 of that
+// maximum, far under the 2^-22 of the split itself.
+#ifndef PT_F16
+#define PT_F16 1
+#endif
+constexpr bool kF16 = PT_F16 != 0 && kKcat;
+#ifndef PT_DFULL1
+#define PT_DFULL1 1
+#endif
+constexpr bool kDfull1 = PT_DFULL1 != 0;  // delta handoff: one arrival per level-0 warp (else one per lane)
 #ifndef PT_LOADER_SLEEP
 #define PT_LOADER_SLEEP 0
 #endif
@@ -175,6 +205,29 @@ __device__ __forceinline__ void mma_tf32_ta(uint32_t tmem_d, uint32_t tmem_a, ui
         "tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n\t}\n" ::"r"(tmem_d),
         "r"(tmem_a), "l"(db), "r"(idesc), "r"(acc));
 }
+__device__ __forceinline__ void mma_f16_ta(uint32_t tmem_d, uint32_t tmem_a, uint64_t db, uint32_t idesc, uint32_t acc) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}\n" ::"r"(tmem_d),
+        "r"(tmem_a), "l"(db), "r"(idesc), "r"(acc));
+}
+// two floats -> packed f16x2 (round to nearest), a in the low half (the lower K index)
+__device__ __forceinline__ uint32_t pack_h2(float a, float b) {
+    uint32_t r;
+    asm("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(b), "f"(a));
+    return r;
+}
+// power-of-two scale exponent that takes a largest magnitude with float bits mb (sign
+// cleared) to [2^14, 2^15); 0 for an all-zero set; clamped to [-60, 120] so 2^s is a normal
+// float and the level-0 weight 2^(896 - sA - sG) a normal double
+__device__ __forceinline__ int f16_scale_exp(uint32_t mb) {
+    if (mb == 0u) return 0;
+    const int e = (int)(mb >> 23);  // biased exponent (0: subnormal)
+    const int s = 141 - e;
+    return s > 120 ? 120 : (s < -60 ? -60 : s);
+}
+__device__ __forceinline__ float exp2f_int(int s) { return __uint_as_float((uint32_t)(127 + s) << 23); }
+__device__ __forceinline__ double exp2d_int(int s) { return __hiloint2double((1023 + s) << 20, 0); }
 __device__ __forceinline__ void tmem_st16(uint32_t addr, const uint32_t (&r)[16]) {
     asm volatile(
         "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(addr),
@@ -304,9 +357,10 @@ template <int J>
 struct Shape {
     static constexpr int KP = (J + 7) / 8 * 8;             // K padded to the tf32 MMA K-step (8)
     static constexpr int KSTEPS = KP / 8;
-    static constexpr int KC = (3 * J + 7) / 8 * 8;          // concatenated K (kKcat): [hi | lo | hi]
-    static constexpr int KCSTEPS = KC / 8;
-    static constexpr int ACOLS = kKcat ? KC : 2 * KP;       // TMEM columns of one A buffer
+    static constexpr int KSTEP = kF16 ? 16 : 8;             // K per MMA (kind::f16 / kind::tf32)
+    static constexpr int KC = (3 * J + KSTEP - 1) / KSTEP * KSTEP;  // concatenated K (kKcat): [lo | hi | hi]
+    static constexpr int KCSTEPS = KC / KSTEP;
+    static constexpr int ACOLS = kKcat ? (kF16 ? KC / 2 : KC) : 2 * KP;  // TMEM columns of one A buffer
     static constexpr int NP = (J * J + 15) / 16 * 16;      // N padded to 16 (M = 128)
     static constexpr int LD = factor_ld(J, 4);             // padded factor row (floats)
     static constexpr int NQ = LD / 4;                       // 16-byte chunks per factor row
@@ -331,7 +385,8 @@ struct Shape {
     static constexpr int OFF_DEL = OFF_CRD + kCRing * CSLOT;
     // a0/x stash of the level-0 warps (copied out of the row ring when the A rows are
     // split, kNA tiles before the tile is reduced): [warp 0..7][kStash][NQ][32] uint4 + [32] x
-    static constexpr int STSLOT = NQ * kWarp * 16 + kWarp * 4;
+    // (+ [32] int: the lane's fp16 scale exponent sA + sG)
+    static constexpr int STSLOT = NQ * kWarp * 16 + kWarp * 4 + kWarp * 4;
     static constexpr int OFF_STASH = OFF_DEL + kD * DSLOT;
     static constexpr int OFF_BAR = (OFF_STASH + 8 * kStash * STSLOT + 7) / 8 * 8;
     // raw_full[kRing], raw_empty[kRing], acc_full[kNT], acc_empty[kNT], a_full[kNA], d_full[4][kD], d_empty[4][kD],
@@ -355,6 +410,26 @@ __device__ __forceinline__ void load_bcat(const float* T, float* sB, int t0, int
             v = (k >= J && k < 2 * J) ? tf32_rna(g - hv) : hv;  // [b_hi ; b_lo ; b_hi]
         }
         sB[kmaj<KC>(c, k)] = v;
+    }
+}
+
+// kF16: the same B in fp16 from the core block scaled by 2^sG: K-major canonical layout of
+// 16-bit elements (core matrix = 8 rows x 8 elements), element (c, k) at byte
+// ((c/8)*(KC/8) + k/8)*128 + (c%8)*16 + (k%8)*2.
+template <int J>
+__device__ __forceinline__ void load_bcat16(const float* T, unsigned char* sB, int t0, int nt, int sG) {
+    constexpr int NP = (J * J + 15) / 16 * 16, KC = (3 * J + 15) / 16 * 16, GB = gblk(J, 4);
+    const float sc = exp2f_int(sG);
+    for (int i = t0; i < NP * KC; i += nt) {
+        const int c = i / KC, k = i % KC;
+        __half v = __float2half_rn(0.f);
+        if (c < J * J && k < 3 * J) {
+            const int k1 = k % J;
+            const float g = T[(c / J) * GB + k1 * J + (c % J)] * sc;
+            const __half hv = __float2half_rn(g);
+            v = (k >= J && k < 2 * J) ? __float2half_rn(g - __half2float(hv)) : hv;  // [b_hi ; b_lo ; b_hi]
+        }
+        *reinterpret_cast<__half*>(sB + ((c >> 3) * (KC / 8) + (k >> 3)) * 128 + (c & 7) * 16 + (k & 7) * 2) = v;
     }
 }
 
@@ -439,7 +514,18 @@ __global__ void __launch_bounds__(kThreads, 1) k_update_tc(const UpdateParams<fl
 
     // ---------------------------------------------------------------- setup
     // B = core (hi/lo tf32 split), K-major: Bt[(k0, j)][k1] = G'[k0][k1][j]
-    if constexpr (kKcat) {
+    int sG = 0;  // kF16: core scale exponent (max |G| over every block this launch reads)
+    if constexpr (kF16) {
+        if (threadIdx.x == 0) misc[2] = 0u;
+        __syncthreads();
+        uint32_t mb = 0u;
+        for (int i = threadIdx.x; i < p.gp_elems; i += kThreads) mb = max(mb, __float_as_uint(p.Gp[i]) & 0x7FFFFFFFu);
+        mb = __reduce_max_sync(0xffffffffu, mb);
+        if (lane == 0) atomicMax(&misc[2], mb);
+        __syncthreads();
+        sG = f16_scale_exp(misc[2]);
+        load_bcat16<J>(p.Gp, reinterpret_cast<unsigned char*>(sBhi), threadIdx.x, kThreads, sG);
+    } else if constexpr (kKcat) {
         load_bcat<J>(p.Gp, sBhi, threadIdx.x, kThreads);
     } else {
     for (int i = threadIdx.x; i < NP * KP; i += kThreads) {
@@ -493,7 +579,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_update_tc(const UpdateParams<fl
             }
             for (int w = 0; w < 4; ++w)
                 for (int s = 0; s < kD; ++s) {
-                    mbar_init(d_full(w, s), kWarp);  // every lane of level-0 warp w (its delta stores)
+                    mbar_init(d_full(w, s), kDfull1 ? 1 : kWarp);  // lane 0 of level-0 warp w after a __syncwarp (its delta stores)
                     mbar_init(d_empty(w, s), 1);     // normal-equation warp 4+w read the slot
                 }
             asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -670,8 +756,10 @@ __global__ void __launch_bounds__(kThreads, 1) k_update_tc(const UpdateParams<fl
                 g_left = next_group();
                 if (gs.valid()) g_aux = __ldg(p.lane_aux + (int64_t)gs.group() * 128);
             }
-            const uint32_t idesc =
-                (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(NP >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
+            // instruction descriptor: D f32 (bits 4-5), A/B format (bits 7-9, 10-12: tf32 = 2,
+            // f16 = 0), both K-major, N >> 3 (bits 17-22), M >> 4 (bits 24-28)
+            const uint32_t idesc = (1u << 4) | (kF16 ? 0u : (2u << 7) | (2u << 10)) | ((uint32_t)(NP >> 3) << 17) |
+                                   ((uint32_t)(128 >> 4) << 24);
             // B descriptors (K-major, SWIZZLE_NONE; LBO: next 16-byte K chunk = next core
             // matrix (128 B); SBO: next 8 rows), per K-step of 8
             uint64_t dbhi[SH::KSTEPS], dblo[SH::KSTEPS], dbc[SH::KCSTEPS];
@@ -681,7 +769,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_update_tc(const UpdateParams<fl
                 dblo[ks] = umma_desc(smem_u32(sBlo) + ks * 256, 128, KP * 32);
             }
 #pragma unroll
-            for (int ks = 0; ks < SH::KCSTEPS; ++ks) dbc[ks] = umma_desc(smem_u32(sBhi) + ks * 256, 128, SH::KC * 32);
+            for (int ks = 0; ks < SH::KCSTEPS; ++ks)  // a K-step = 2 core matrices (32 bytes of K) either way
+                dbc[ks] = umma_desc(smem_u32(sBhi) + ks * 256, 128, SH::KC * (kF16 ? 16 : 32));
             // optional trace (tools/trace_tc.py): CTA 0, tiles [64, 128)
 #ifdef PT_TRACE
             long long* const trm = (p.trace && blockIdx.x == 0) ? p.trace + 4 * 512 : nullptr;
@@ -707,7 +796,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_update_tc(const UpdateParams<fl
                         mbar_wait(b_free, bpar);
                         bpar ^= 1u;
                         const float* T = p.Gp + (int64_t)aux * p.aux_stride;
-if constexpr (kKcat) {
+                        if constexpr (kF16) {
+                            load_bcat16<J>(T, reinterpret_cast<unsigned char*>(sBhi), lane, kWarp, sG);
+                        } else if constexpr (kKcat) {
                             load_bcat<J>(T, sBhi, lane, kWarp);
                         } else {
 #pragma unroll 8
@@ -746,8 +837,9 @@ if constexpr (kKcat) {
                 // loop once swallowed the next statement, the accumulator commit, and the kernel hung)
                 if constexpr (kKcat) {
 #pragma unroll
-                    for (int ks = 0; ks < SH::KCSTEPS; ++ks) {
-                        mma_tf32_ta(d, ahi + 8 * ks, dbc[ks], idesc, acc);
+                    for (int ks = 0; ks < SH::KCSTEPS; ++ks) {  // 8 TMEM columns of A per K-step
+                        if constexpr (kF16) mma_f16_ta(d, ahi + 8 * ks, dbc[ks], idesc, acc);
+                        else mma_tf32_ta(d, ahi + 8 * ks, dbc[ks], idesc, acc);
                         acc = 1;
                     }
                 } else {
@@ -805,6 +897,7 @@ if constexpr (kKcat) {
             // is one use of the buffer, so this wait can never be two phases behind)
             if (k >= (uint32_t)kNA) mbar_wait(a_empty((int)(k % kNA)), ((k / kNA) + 1) & 1);
             uint32_t hi[16], lo[16];
+            int sA = 0;  // kF16: row scale exponent
 #pragma unroll
             for (int q = 0; q < KQ; ++q) {
                 uint32_t wv[4] = {0u, 0u, 0u, 0u};
@@ -813,11 +906,26 @@ if constexpr (kKcat) {
                     wv[0] = r.x, wv[1] = r.y, wv[2] = r.z, wv[3] = r.w;
                 }
 #pragma unroll
-                for (int v = 0; v < 4; ++v) {
-                    const uint32_t hh = (wv[v] + 0x1000u) & 0xFFFFE000u;
-                    hi[4 * q + v] = hh;
-                    lo[4 * q + v] = __float_as_uint(__uint_as_float(wv[v]) - __uint_as_float(hh));
-                }
+                for (int v = 0; v < 4; ++v) hi[4 * q + v] = wv[v];
+            }
+            if constexpr (kF16) {
+                uint32_t mb = 0u;
+#pragma unroll
+                for (int i = 0; i < J; ++i) mb = max(mb, hi[i] & 0x7FFFFFFFu);
+                sA = f16_scale_exp(mb);
+                const float sc = exp2f_int(sA);
+#pragma unroll
+                for (int i = 0; i < J; ++i) hi[i] = __float_as_uint(__uint_as_float(hi[i]) * sc);  // exact
+            }
+#pragma unroll
+            for (int i = 0; i < 4 * KQ; ++i) {
+                // hi = the value rounded to 11 significant bits (nearest, ties away), lo = the exact
+                // remainder; fp16 holds hi exactly (after the scaling) and rounds lo to nearest, the
+                // tensor core truncates a tf32 lo
+                const uint32_t w = hi[i];
+                const uint32_t hh = (w + 0x1000u) & 0xFFFFE000u;
+                hi[i] = hh;
+                lo[i] = __float_as_uint(__uint_as_float(w) - __uint_as_float(hh));
             }
             // a0 and x of the tile go to this warp's stash: the ring slot is free once split
             {
@@ -827,9 +935,22 @@ if constexpr (kKcat) {
                 for (int q = 0; q < NQ; ++q)
                     reinterpret_cast<uint4*>(sb)[q * kWarp + lane] = *rowc(s, 0, q, te);
                 reinterpret_cast<float*>(sb + NQ * kWarp * 16)[lane] = *rowx(s, te);
+                if constexpr (kF16) reinterpret_cast<int*>(sb + NQ * kWarp * 16 + kWarp * 4)[lane] = sA + sG;
             }
             const uint32_t ta = tm_lane + SH::ACOL + (k % kNA) * SH::ACOLS;
-            if constexpr (kKcat) {
+            if constexpr (kF16) {
+                // [a_lo | a_hi | a_hi | 0] over KC fp16 elements, two per TMEM column (lower K
+                // index in the low half), against [b_hi ; b_lo ; b_hi]
+                float v[SH::KC];
+#pragma unroll
+                for (int i = 0; i < SH::KC; ++i)
+                    v[i] = __uint_as_float(i < J ? lo[i] : (i < 2 * J ? hi[i - J] : (i < 3 * J ? hi[i - 2 * J] : 0u)));
+                uint32_t w[16];
+#pragma unroll
+                for (int c = 0; c < 16; ++c) w[c] = 2 * c + 1 < SH::KC ? pack_h2(v[2 * c], v[2 * c + 1]) : 0u;
+                if constexpr (SH::ACOLS == 16) tmem_st16(ta, w);
+                else tmem_st8(ta, w);
+            } else if constexpr (kKcat) {
                 // [a_lo | a_hi | a_hi | 0] over KC columns (against [b_hi ; b_lo ; b_hi]: the two
                 // small products first, as in the 3-sweep order -- big-first doubled the worst
                 // full-size c5 row error to 1.9e-5), stored 16 (or 8) at a time
@@ -867,7 +988,7 @@ if constexpr (kKcat) {
         for (uint32_t k = par; k < total; k += 2) {
             const int b = (int)(k % kNT), s = (int)(k % kRing);
             mark(k, 0);
-            if (k + kNA < total) split(k + kNA);
+            if (!kSplitLate && k + kNA < total) split(k + kNA);
             mark(k, 6);
             mbar_wait(acc_full(b), (k / kNT) & 1);
             asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
@@ -889,6 +1010,8 @@ if constexpr (kKcat) {
                     if (4 * q + u < J) a0f[4 * q + u] = wv[u];
             }
             const float x = reinterpret_cast<const float*>(sbk + NQ * kWarp * 16)[lane];
+            // kF16: t arrives scaled by 2^ssc (row and core scalings), undone in the weights
+            const int ssc = kF16 ? reinterpret_cast<const int*>(sbk + NQ * kWarp * 16 + kWarp * 4)[lane] : 0;
             mark(k, 2);
 #pragma unroll
             for (int ch = 0; ch < kBCH && ch < NCH; ++ch) tmem_wait16(rb[ch]);
@@ -897,11 +1020,15 @@ if constexpr (kKcat) {
             TD d[J];
             float pf[J];  // fp32 partial sums (G0 > 1)
             double a0d[J];
+            // (G0 == 1, fp64: folded into a0 exactly; the other paths scale delta at the end)
+            constexpr bool kFold = LAST64 && G0 == 1 && kL0Conv == 1;
+            const double wsc_int = kF16 ? exp2d_int(896 - ssc) : 0x1p896, wsc_xu = kF16 ? exp2d_int(-ssc) : 1.0;
 #pragma unroll
             for (int q = 0; q < J; ++q) {
                 a0d[q] = kA0Int ? f2d_int(a0f[q]) : double(a0f[q]);
                 // scheme 1: a0[k0] * 2^896 pairs with f2d_scaled(t) = t * 2^-896 (both exact)
-                if (kL0Conv == 1 && LAST64 && G0 == 1 && !((kXuMask >> q) & 1u)) a0d[q] *= 0x1p896;
+                if (kFold && !((kXuMask >> q) & 1u)) a0d[q] *= wsc_int;
+                else if (kFold && kF16) a0d[q] *= wsc_xu;
             }
 #pragma unroll
             for (int j = 0; j < J; ++j) d[j] = TD(0);
@@ -949,6 +1076,13 @@ if constexpr (kKcat) {
                 __syncwarp();
                 if (lane == 0) mbar_arrive(acc_empty(b));
             }
+            if constexpr (kF16 && !kFold) {
+                // (fp32: in two steps, 2^-ssc can leave the float range)
+                const TD u = LAST64 ? TD(exp2d_int(-ssc)) : TD(exp2f_int(-(ssc / 2)));
+                const TD u2 = LAST64 ? TD(1) : TD(exp2f_int(-(ssc - ssc / 2)));
+#pragma unroll
+                for (int j = 0; j < J; ++j) d[j] = d[j] * u * u2;
+            }
             mark(k, 4);
             // hand delta (fp64) and x to normal-equation warp 8 + w4
             const int ds = (int)(k % kD);
@@ -957,8 +1091,22 @@ if constexpr (kKcat) {
             for (int q = 0; q < SH::JD / 2; ++q)
                 *dslot2(ds, q, te) = make_double2(double(d[2 * q]), 2 * q + 1 < J ? double(d[2 * q + 1]) : 0.0);
             *dslot_x(ds, te) = x;
-            mbar_arrive(d_full(w4, ds));
+            // one arrival per warp, not per lane: every arrival wakes the CTA's sleeping waiters
+            // (NANOSLEEP.SYNCS), and 128 per tile dominated their polling
+            if constexpr (kNbar) {
+                __threadfence_block();
+                __syncwarp();
+                asm volatile("bar.arrive %0, %1;" ::"r"(1 + w4 * kD + ds), "n"(2 * kWarp) : "memory");
+            } else if constexpr (kDfull1) {
+                __syncwarp();
+                if (lane == 0) mbar_arrive(d_full(w4, ds));
+            } else {
+                mbar_arrive(d_full(w4, ds));
+            }
             mark(k, 5);
+            // late split: tile k + kNA's rows get one more level-0 phase to land (the early
+            // split waited for them: the row-ring wait was the hottest polling loop)
+            if (kSplitLate && k + kNA < total) split(k + kNA);
         }
     } else {
         // ====================================================== normal equations
@@ -985,7 +1133,18 @@ if constexpr (kKcat) {
         auto finalize = [&](const Seg& g) {
             if (g.row < 0) return;
             const int64_t pidx = p.lane_pidx[g.slot];
-            if (pidx < 0) {
+            bool solve = pidx < 0;
+            if (!solve) {
+                const int stp = p.lane_pstride[g.slot];
+                double* dst = p.partials + pidx;
+#pragma unroll
+                for (int q = 0; q < NB; ++q) dst[(int64_t)q * stp] = B[q];
+#pragma unroll
+                for (int q = 0; q < J; ++q) dst[(int64_t)(NB + q) * stp] = c[q];
+                dst[(int64_t)(NB + J) * stp] = s2;
+                if (p.seg_done) solve = heavy_take_row<J>(p.seg_done, p.row_pbase, p.partials, g.row, stp, B, c, s2);
+            }
+            if (solve) {
                 double a[J];
                 const bool ok = chol_solve<J>(B, c, p.lambda, a);
                 if (!ok) {
@@ -1017,14 +1176,6 @@ if constexpr (kKcat) {
                                                   (int64_t)g.row * p.lda * 4)[q] = v;
                 }
                 p.sse_row[g.row] = sse;
-            } else {
-                const int stp = p.lane_pstride[g.slot];
-                double* dst = p.partials + pidx;
-#pragma unroll
-                for (int q = 0; q < NB; ++q) dst[(int64_t)q * stp] = B[q];
-#pragma unroll
-                for (int q = 0; q < J; ++q) dst[(int64_t)(NB + q) * stp] = c[q];
-                dst[(int64_t)(NB + J) * stp] = s2;
             }
         };
         Sched sc = s0;
@@ -1049,7 +1200,8 @@ if constexpr (kKcat) {
                 const int ds = (int)(k % kD);
                 markn(k, 0);
                 markn(k, 1);
-                if constexpr (kNeSleep > 0) mbar_wait_sleep(d_full(w4, ds), (k / kD) & 1, kNeSleep);
+                if constexpr (kNbar) asm volatile("bar.sync %0, %1;" ::"r"(1 + w4 * kD + ds), "n"(2 * kWarp) : "memory");
+                else if constexpr (kNeSleep > 0) mbar_wait_sleep(d_full(w4, ds), (k / kD) & 1, kNeSleep);
                 else mbar_wait(d_full(w4, ds), (k / kD) & 1);
                 markn(k, 2);
                 double dd[J];

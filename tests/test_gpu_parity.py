@@ -148,6 +148,20 @@ def test_mode_update_f32(pt, orc, name, scale, seg):
         assert [m["smp"] for m in info["modes"]] == [2, 2, 1, 1]
 
 
+@pytest.mark.parametrize("scale,seg", [(0.001, 256), (0.005, 256), (0.005, 7)])
+def test_mode_update_c4_f32c2(pt, orc, scale, seg):
+    """Policy 3 (F32-C2, order 5): the level next to the innermost in fp32 (J^3 instead of J^4
+    fp32 -> fp64 conversions per entry), the outer ones in fp64 -- held to the same 1e-5 per
+    row as the automatic F32-C, at the init state (the worst case) and mid-trajectory."""
+    cfg = synth.small("c4", scale)
+    coords, vals = init_cfg(pt, cfg, policy=3, seg_len=seg)
+    assert pt.ptucker_info()["policy"] == "F32-C2"
+    t = orc.Tensor(coords, vals, cfg.dims)
+    w0 = mode_update_parity(pt, orc, t, cfg, 1e-5, sweeps=0)
+    w1 = mode_update_parity(pt, orc, t, cfg, 1e-5, sweeps=1)
+    print(f"c4@{scale} seg={seg} F32-C2 worst row rel err init {w0:.2e} mid {w1:.2e}")
+
+
 @pytest.mark.parametrize("tc_table", [0, 1])
 def test_mode_update_c3_table_modes(pt, orc, tc_table):
     """Order-4 modes with one small other mode (c3 modes 2/3, SMP kind 1) on the ALU table
@@ -422,3 +436,42 @@ def test_invalid_data_keeps_context(pt, orc):
     assert e.value.code == pt.PTUCKER_EINVAL and "entry 77" in str(e.value)
     assert pt.ptucker_error() == e0            # the previous context is intact
     pt.ptucker_sweep()
+
+
+@pytest.mark.parametrize("name,scale,seg", [("c1", 1.0, 8), ("c2", 0.01, 7), ("c3", 0.002, 64), ("c5", 0.0005, 7),
+                                            ("c4", 0.0005, 5)])
+def test_inline_heavy_rows_bit_identical(pt, orc, name, scale, seg):
+    """Heavy rows (2..64 segments) solved inside the update kernel by the lane that stores the
+    row's last partial (option fin_inline; off by default: slower) give the same factors, core and errors bit
+    for bit as the separate finalize launch: the same additions in the same order, the same
+    solve.  The finalize launch count shows which path ran."""
+    cfg = synth.config(name) if scale == 1.0 else synth.small(name, scale)
+    N = len(cfg.dims)
+    runs = {}
+    for inline in (0, 1):
+        init_cfg(pt, cfg, seg_len=seg)
+        pt.ptucker_set_option("fin_inline", inline)
+        pt.ptucker_set_option("time_kernels", 1)
+        pt.ptucker_reset_kernel_stats()
+        errs = []
+        for it in range(3):
+            pt.ptucker_sweep()
+            errs.append(pt.ptucker_error())
+        _, nfin = pt.ptucker_kernel_stats("finalize")
+        pt.ptucker_set_option("time_kernels", 0)
+        runs[inline] = ([pt.ptucker_get_factor(n).copy() for n in range(N)], errs, nfin)
+    pt.ptucker_set_option("fin_inline", 0)
+    for n in range(N):
+        assert np.array_equal(runs[0][0][n], runs[1][0][n]), n
+    assert runs[0][1] == runs[1][1]
+    assert runs[0][2] > 0                    # the finalize launch ran without the option
+    assert runs[1][2] < runs[0][2]           # and (at least some modes) not with it
+    # and the inline run is still the ALS of the oracle: the error trajectory
+    coords, vals = synth.generate(cfg)
+    t = orc.Tensor(coords, vals, cfg.dims)
+    m = orc.init_model(cfg.dims, [cfg.J] * N, seed=0, prec=1 if cfg.dtype == "f64" else 0)
+    for it in range(3):
+        for n in range(N):
+            orc.update_mode(t, m, n, cfg.lam)
+        e = orc.error(t, m)
+        assert abs(runs[1][1][it] - e) <= 1e-3 * e, (it, runs[1][1][it], e)
