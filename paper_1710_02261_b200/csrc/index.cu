@@ -15,7 +15,10 @@
 //      at slot slice_off[s] + e*32 + l, so a warp's loads are coalesced.
 #include <cub/cub.cuh>
 
+#include <chrono>
 #include <cstdint>
+#include <cstdio>
+#include <cstdlib>
 #include <vector>
 
 #include "index.cuh"
@@ -170,17 +173,34 @@ __global__ void k_sell_fill(int64_t nslices, const int64_t* slice_off, const int
         const int32_t len = lane_len[t];
         const int64_t src0 = lane_src[t];
         const int64_t dst0 = slice_off[t >> 5] + (t & 31);
-        for (int32_t e = 0; e < len; ++e) {
-            const int64_t src = perm[src0 + e];
-            const int64_t dst = dst0 + (int64_t)e * 32;
-            int l = 0;
-            for (int m = 0; m < N; ++m) {
-                if (m == n) continue;
-                sc[l][dst] = coords[src * N + m];
-                ++l;
+        // four entries at a time: their entry ids, then all their loads, then the stores (the
+        // stores could alias the loads as far as the compiler knows: one entry per iteration
+        // serialised two dependent DRAM latencies)
+        constexpr int U = 4;
+        for (int32_t e0 = 0; e0 < len; e0 += U) {
+            int64_t src[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) src[u] = e0 + u < len ? __ldg(perm + src0 + e0 + u) : -1;
+            int32_t cv[U][kMaxN];
+            TS xv[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                if (src[u] < 0) continue;
+                int l = 0;
+                for (int m = 0; m < N; ++m) {
+                    if (m == n) continue;
+                    cv[u][l++] = __ldg(coords + src[u] * N + m);
+                }
+                xv[u] = __ldg(vals + src[u]);
             }
-            sv[dst] = vals[src];
-            if (sid) sid[dst] = (int32_t)src;  // input entry id (P-Tucker-Cache: the row of Pres)
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                if (src[u] < 0) continue;
+                const int64_t dst = dst0 + (int64_t)(e0 + u) * 32;
+                for (int l = 0; l < N - 1; ++l) sc[l][dst] = cv[u][l];
+                sv[dst] = xv[u];
+                if (sid) sid[dst] = (int32_t)src[u];  // input entry id (P-Tucker-Cache: the row of Pres)
+            }
         }
     }
 }
@@ -312,6 +332,16 @@ cudaError_t build_mode_sell(const int32_t* d_coords, const void* d_vals, int ele
                             DeviceArena& scratch, cudaStream_t st, bool aux_groups, bool with_sid) {
     const int PW = rec_width(J);
     const int64_t nrows = r1 - r0;
+    // PTUCKER_DEBUG=2: phase times of this function on stderr (synchronising)
+    const bool dbg = getenv("PTUCKER_DEBUG") && getenv("PTUCKER_DEBUG")[0] == '2';
+    auto t_last = std::chrono::steady_clock::now();
+    auto lap = [&](const char* what) {
+        if (!dbg) return;
+        cudaStreamSynchronize(st);
+        const auto now = std::chrono::steady_clock::now();
+        fprintf(stderr, "[ptucker]   sell %-24s %8.2f ms\n", what, std::chrono::duration<double, std::milli>(now - t_last).count());
+        t_last = now;
+    };
     mi.r0 = r0;
     mi.r1 = r1;
     // ---- groups: rows, or (row, i_s) pairs for a small-mode table ----
@@ -339,6 +369,7 @@ cudaError_t build_mode_sell(const int32_t* d_coords, const void* d_vals, int ele
         group_ptr = gptr;
         perm = perm2;
     }
+    lap("groups (small-mode sort)");
     const int64_t g0 = r0 * Is, ngroups = nrows * Is;
     // ---- 3. segments ----
     int64_t *nseg_g = nullptr, *seg_start_g = nullptr, *nseg_r = nullptr, *hflag = nullptr, *hseg = nullptr,
@@ -369,6 +400,7 @@ cudaError_t build_mode_sell(const int32_t* d_coords, const void* d_vals, int ele
     mi.npartial_doubles = tot[2] * PW;
     mi.nsegments = nS;
 
+    lap("segment counts");
     int32_t *seg_row, *seg_aux, *seg_len, *seg_pstride;
     int64_t *seg_src, *seg_pidx;
     uint32_t *seg_key, *seg_key_sorted;
@@ -401,6 +433,7 @@ cudaError_t build_mode_sell(const int32_t* d_coords, const void* d_vals, int ele
         k_group_fill<<<grid_for(ngroups), 256, 0, st>>>(group_ptr, g0, ngroups, Is, S, PW, seg_start_g, nseg_r, hbase,
                                                         seg_row, seg_src, seg_aux, seg_len, seg_key, seg_pidx,
                                                         seg_pstride);
+    lap("segment fill + allocs");
     // ---- 4. stable sort of segments by length (descending); aux-major when requested ----
     aux_groups = aux_groups && smode >= 0;
     if (aux_groups && nS > 0) k_aux_key<<<grid_for(nS), 256, 0, st>>>(nS, seg_aux, seg_len, Is, S, seg_key);
@@ -417,6 +450,7 @@ cudaError_t build_mode_sell(const int32_t* d_coords, const void* d_vals, int ele
         IB_CHECK(cub::DeviceRadixSort::SortPairs(tmp, tb, seg_key, seg_key_sorted, seg_iota, order, (int)nS, 0, bits,
                                                  st));
     }
+    lap("segment sort");
     // padded class layout (aux_groups): counts -> host -> lane offsets
     const int nclass = (int)Is + 1;
     std::vector<int64_t> h_cnt(nclass, 0), h_cs(nclass + 1, 0), h_ps(nclass + 1, 0);
@@ -465,6 +499,7 @@ cudaError_t build_mode_sell(const int32_t* d_coords, const void* d_vals, int ele
     IB_CHECK(exclusive_sum(slice_slots, mi.slice_off, mi.nslices + 1, scratch, st));
     IB_CHECK(cudaMemcpyAsync(&mi.nslots, mi.slice_off + mi.nslices, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
     IB_CHECK(cudaStreamSynchronize(st));
+    lap("slices");
     // ---- 5. SELL scatter ----
     for (int k = 0; k < N - 1; ++k) {
         IB_CHECK(dalloc(&mi.sc[k], mi.nslots, arena));
@@ -490,8 +525,10 @@ cudaError_t build_mode_sell(const int32_t* d_coords, const void* d_vals, int ele
                                                                  d_sc, (float*)mi.sv, mi.sid);
     }
     IB_CHECK(cudaGetLastError());
+    lap("SELL scatter");
     IB_CHECK(cudaStreamSynchronize(st));
     scratch.release_all();
+    lap("scratch release");
     return cudaSuccess;
 }
 

@@ -12,14 +12,24 @@ namespace pt {
 // Device allocations owned by a context (freed together).
 struct DeviceArena {
     std::vector<void*> ptrs;
+    // pool_stream set: stream-ordered allocations from the device's default memory pool
+    // (cudaMallocAsync / cudaFreeAsync, no device-wide synchronisation; the pool keeps the
+    // memory for the next index build) -- the index-build scratch: its cudaFree calls were
+    // ~5 ms of every mode's build on c5.  Not for memory exported by CUDA IPC (the factors).
+    cudaStream_t pool_stream = nullptr;
+    bool pooled = false;
     cudaError_t alloc(void** p, size_t bytes) {
-        cudaError_t e = cudaMalloc(p, bytes > 0 ? bytes : 1);
+        cudaError_t e = pooled ? cudaMallocAsync(p, bytes > 0 ? bytes : 1, pool_stream)
+                               : cudaMalloc(p, bytes > 0 ? bytes : 1);
         if (e == cudaSuccess) ptrs.push_back(*p);
         else *p = nullptr;
         return e;
     }
     void release_all() {
-        for (void* p : ptrs) cudaFree(p);
+        for (void* p : ptrs) {
+            if (pooled) cudaFreeAsync(p, pool_stream);
+            else cudaFree(p);
+        }
         ptrs.clear();
     }
     ~DeviceArena() { release_all(); }
