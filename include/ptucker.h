@@ -111,9 +111,7 @@ int ptucker_set_stream(void* cuda_stream);
  * Copies the COO to the device, draws the init, builds every mode's slice
  * index Omega^(n)_{i_n} on the device (stable radix sort -> CSR ->
  * length-sorted segments) and this rank's row blocks.  Replaces any previous
- * context's data (the communicator is kept).  The index-build temporaries come from the
- * device's default stream-ordered memory pool (cudaMallocAsync), whose release threshold is
- * set to "never": the pool keeps that memory (c5: ~2 GB) for later inits of the process. */
+ * context's data (the communicator is kept). */
 int ptucker_init(const int32_t* coords, const void* vals, int32_t vals_dtype, int64_t nnz, int32_t order,
                  const int64_t* dims, const int32_t* core_dims, double lambda, uint64_t seed);
 

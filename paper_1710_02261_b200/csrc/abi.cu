@@ -528,6 +528,7 @@ void free_all() {
     g.d_barrier = nullptr;
     g.arena.release_all();
     g.scratch.release_all();
+    g.scratch.free_chunks();
     for (int n = 0; n < kMaxN; ++n) {
         g.mi[n] = ModeIndex();
         g.A[n] = nullptr;
@@ -988,16 +989,10 @@ int ptucker_init(const int32_t* coords, const void* vals, int32_t vals_dtype, in
             g.seg_len_eff = sl;
         }
     }
-    {   // index-build scratch from the stream-ordered pool, kept cached between the builds and
-        // across contexts (release threshold: never): c5 init 0.148 -> 0.098 s (trimming the pool
-        // after each init made the next one re-map it: 0.24-0.48 s)
-        cudaMemPool_t pool;
-        CK(cudaDeviceGetDefaultMemPool(&pool, g.device));
-        uint64_t keep = UINT64_MAX;
-        CK(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep));
-        g.scratch.pooled = true;
-        g.scratch.pool_stream = S();
-    }
+#ifndef PT_SCRATCH_BUMP
+#define PT_SCRATCH_BUMP 1
+#endif
+    g.scratch.bump = PT_SCRATCH_BUMP != 0;  // index-build temporaries: rewound chunks, freed after the builds
     for (int n = 0; n < order; ++n) {
         ModeIndex& m = g.mi[n];
         CK(build_mode_csr(d_coords, nnz, order, n, dims[n], m, g.arena, g.scratch, S()));
@@ -1046,6 +1041,9 @@ int ptucker_init(const int32_t* coords, const void* vals, int32_t vals_dtype, in
         pc.lap("SELL segments + scatter", S());
     }
     CK(A.alloc((void**)&g.lit_part, std::max<int64_t>(g.mi[0].nslices * 32, 1) * sizeof(double)));
+    CK(cudaStreamSynchronize(S()));
+    g.scratch.free_chunks();
+    pc.lap("scratch free");
 
     CK(cudaStreamSynchronize(S()));
     if (g.generic) {

@@ -12,27 +12,56 @@ namespace pt {
 // Device allocations owned by a context (freed together).
 struct DeviceArena {
     std::vector<void*> ptrs;
-    // pool_stream set: stream-ordered allocations from the device's default memory pool
-    // (cudaMallocAsync / cudaFreeAsync, no device-wide synchronisation; the pool keeps the
-    // memory for the next index build) -- the index-build scratch: its cudaFree calls were
-    // ~5 ms of every mode's build on c5.  Not for memory exported by CUDA IPC (the factors).
-    cudaStream_t pool_stream = nullptr;
-    bool pooled = false;
+    // bump mode (the index-build scratch): sub-allocations from a few large chunks that are
+    // kept between the builds (release_all only rewinds them; free_chunks returns them) --
+    // the per-temporary cudaMalloc / cudaFree of round 2 cost ~8 ms of each c5 mode's build
+    // (a stream-ordered pool was as fast in isolation but its first growth inside a process
+    // that had freed a previous context took 0.2-0.7 s on some boxes)
+    bool bump = false;
+    struct Chunk {
+        char* base;
+        size_t size, used;
+    };
+    std::vector<Chunk> chunks;
     cudaError_t alloc(void** p, size_t bytes) {
-        cudaError_t e = pooled ? cudaMallocAsync(p, bytes > 0 ? bytes : 1, pool_stream)
-                               : cudaMalloc(p, bytes > 0 ? bytes : 1);
+        if (bump) {
+            const size_t b = ((bytes > 0 ? bytes : 1) + 255) & ~(size_t)255;
+            for (Chunk& c : chunks)
+                if (c.size - c.used >= b) {
+                    *p = c.base + c.used;
+                    c.used += b;
+                    return cudaSuccess;
+                }
+            const size_t sz = b > ((size_t)1 << 30) ? b : ((size_t)1 << 30);
+            char* base = nullptr;
+            const cudaError_t e = cudaMalloc((void**)&base, sz);
+            if (e != cudaSuccess) {
+                *p = nullptr;
+                return e;
+            }
+            chunks.push_back({base, sz, b});
+            *p = base;
+            return cudaSuccess;
+        }
+        cudaError_t e = cudaMalloc(p, bytes > 0 ? bytes : 1);
         if (e == cudaSuccess) ptrs.push_back(*p);
         else *p = nullptr;
         return e;
     }
+    // the caller has synchronised the stream that used the memory
     void release_all() {
-        for (void* p : ptrs) {
-            if (pooled) cudaFreeAsync(p, pool_stream);
-            else cudaFree(p);
-        }
+        for (void* p : ptrs) cudaFree(p);
         ptrs.clear();
+        for (Chunk& c : chunks) c.used = 0;
     }
-    ~DeviceArena() { release_all(); }
+    void free_chunks() {
+        for (Chunk& c : chunks) cudaFree(c.base);
+        chunks.clear();
+    }
+    ~DeviceArena() {
+        release_all();
+        free_chunks();
+    }
 };
 
 struct ModeIndex {

@@ -32,9 +32,16 @@ namespace pt {
 // One copy per translation unit (static); filled by set_core_constant().
 static __constant__ __align__(16) unsigned char c_core[65536];
 
-template <typename TS, int N, int J>
+// L64 = N - 3 at order 5 (policy F32-C2): the core from shared memory (LDS broadcast) -- in the
+// constant bank nvcc addressed it through a per-thread register there (LDC R, c[0x3][R]) instead
+// of the uniform datapath, and every core read became a per-thread constant load
+#ifndef PT_C2_SMEM
+#define PT_C2_SMEM 1
+#endif
+template <typename TS, int N, int J, int L64 = -1>
 struct CoreInConst {
-    static constexpr bool value = (size_t)ipow(J, N - 2) * gblk(J, sizeof(TS)) * sizeof(TS) <= sizeof(c_core);
+    static constexpr bool value = (size_t)ipow(J, N - 2) * gblk(J, sizeof(TS)) * sizeof(TS) <= sizeof(c_core) &&
+                                  !(PT_C2_SMEM && N == 5 && L64 == N - 3);
 };
 
 // float -> double by integer operations (ALU pipe) instead of the quarter-rate XU
@@ -341,7 +348,7 @@ __global__ void __launch_bounds__(kUpdThreads, upd_min_blocks(J, (int)sizeof(TS)
     using V = typename Vec16<TS>::type;
     constexpr int VN = Vec16<TS>::n;
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    constexpr bool GC = CoreInConst<TS, N, J>::value && !TABLE;
+    constexpr bool GC = CoreInConst<TS, N, J, L64>::value && !TABLE;
     const TS* gs;
     if constexpr (GC) {
         gs = reinterpret_cast<const TS*>(c_core);
@@ -536,9 +543,9 @@ __global__ void __launch_bounds__(kUpdThreads, upd_min_blocks(J, (int)sizeof(TS)
 template <typename TS, typename TF, int N, int J, int L64>
 void launch_update(const void* params, bool literal, int grid, cudaStream_t st) {
     const UpdateParams<TS>& p = *reinterpret_cast<const UpdateParams<TS>*>(params);
-    const size_t smem = (CoreInConst<TS, N, J>::value ? 0 : gp_smem_bytes(p.gp_elems, sizeof(TS))) +
+    const size_t smem = (CoreInConst<TS, N, J, L64>::value ? 0 : gp_smem_bytes(p.gp_elems, sizeof(TS))) +
                         (kUpdThreads / kWarp) * Stage<TS, N, J>::BYTES_PER_WARP;
-    if (CoreInConst<TS, N, J>::value)
+    if (CoreInConst<TS, N, J, L64>::value)
         cudaMemcpyToSymbolAsync(c_core, p.Gp, (size_t)p.gp_elems * sizeof(TS), 0, cudaMemcpyDeviceToDevice, st);
     if (literal) {
         auto k = k_update<TS, TF, N, J, L64, true>;
@@ -553,7 +560,7 @@ void launch_update(const void* params, bool literal, int grid, cudaStream_t st) 
 
 template <typename TS, typename TF, int N, int J, int L64>
 int occupancy_update(bool literal, size_t gp_bytes) {
-    const size_t smem = (CoreInConst<TS, N, J>::value ? 0 : gp_bytes) + (kUpdThreads / kWarp) * Stage<TS, N, J>::BYTES_PER_WARP;
+    const size_t smem = (CoreInConst<TS, N, J, L64>::value ? 0 : gp_bytes) + (kUpdThreads / kWarp) * Stage<TS, N, J>::BYTES_PER_WARP;
     int nb = 0;
     if (literal) {
         auto k = k_update<TS, TF, N, J, L64, true>;
