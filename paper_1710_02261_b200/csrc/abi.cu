@@ -1033,10 +1033,18 @@ int ptucker_init(const int32_t* coords, const void* vals, int32_t vals_dtype, in
         CK(build_mode_sell(d_coords, d_vals, esz, nnz, order, n, g.Jv.j[n], S_n, m.bounds[g.rank],
                            m.bounds[g.rank + 1], smode, m, g.arena, g.scratch, S(), aux_groups, g.cache_on));
         {   // most segments of one of this rank's rows (the heavy-row finalize picks its kernels by it)
-            int64_t mx = 0;
-            for (int64_t r = m.bounds[g.rank]; r < m.bounds[g.rank + 1]; ++r)
-                mx = std::max<int64_t>(mx, m.h_row_ptr[r + 1] - m.h_row_ptr[r]);
-            m.hmaxseg = (mx + S_n - 1) / S_n;
+            // exact, from the index (a small-mode-grouped row has a segment per class it meets)
+            std::vector<int32_t> hn((size_t)m.nheavy);
+            if (m.nheavy > 0)
+                CK(cudaMemcpyAsync(hn.data(), m.hnseg, sizeof(int32_t) * m.nheavy, cudaMemcpyDeviceToHost, S()));
+            CK(cudaStreamSynchronize(S()));
+            int64_t mx = 1, mn = 0;
+            for (int32_t v : hn) {
+                mx = std::max<int64_t>(mx, v);
+                mn = mn == 0 ? v : std::min<int64_t>(mn, v);
+            }
+            m.hmaxseg = mx;
+            m.hminseg = mn;  // fewest segments of a heavy row (0: none)
         }
         pc.lap("SELL segments + scatter", S());
     }
@@ -1143,7 +1151,7 @@ int ptucker_update_mode(int32_t n) {
                 for (int r = 0; r < g.npeer; ++r) pr.base[r] = g.peer_A[n][r];
             }
             launch_heavy_finalize(m.nheavy, m.hrow, m.hnseg, m.hpbase, m.partials, m.hrec, g.Jv.j[n], g.lambda, g.A[n], g.esz,
-                                  g.lda, g.sse_row[n], g.d_fail, S(), pr, m.hmaxseg);
+                                  g.lda, g.sse_row[n], g.d_fail, S(), pr, m.hmaxseg, m.hminseg);
             g.launches += 3;
             CK(cudaGetLastError());
             return PTUCKER_OK;

@@ -87,6 +87,7 @@ struct ModeIndex {
     // heavy rows (more than one segment)
     int64_t nheavy = 0, npartial_doubles = 0;
     int64_t hmaxseg = 0;             // most segments of one row (host; set by ptucker_init)
+    int64_t hminseg = 0;             // fewest segments of a heavy row (host; 0: no heavy row)
     int seg_len = 0;                 // the segment length S of this mode's index
     int32_t* hrow = nullptr;
     int32_t* hnseg = nullptr;

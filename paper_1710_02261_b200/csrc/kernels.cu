@@ -156,16 +156,16 @@ __global__ void __launch_bounds__(256) k_heavy_sum(int64_t nheavy, int PW, const
         const int nseg = hnseg[h];
         if (nseg <= kSmallSeg) continue;
         const double* src = partials + hpbase[h] + (int64_t)p * nseg;
-        double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+        // eight interleaved accumulators (eight loads in flight per lane: the sum is latency-bound,
+        // c3's table-mode rows have ~7,800 segments), combined in a fixed order
+        double a[8] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
         int s = lane;
-        for (; s + 96 < nseg; s += 128) {
-            a0 += src[s];
-            a1 += src[s + 32];
-            a2 += src[s + 64];
-            a3 += src[s + 96];
+        for (; s + 224 < nseg; s += 256) {
+#pragma unroll
+            for (int u = 0; u < 8; ++u) a[u] += __ldcg(src + s + 32 * u);
         }
-        for (; s < nseg; s += 32) a0 += src[s];
-        double acc = (a0 + a1) + (a2 + a3);
+        for (; s < nseg; s += 32) a[0] += __ldcg(src + s);
+        double acc = ((a[0] + a[1]) + (a[2] + a[3])) + ((a[4] + a[5]) + (a[6] + a[7]));
         for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
         if (lane == 0) rec[w] = acc;
     }
@@ -312,7 +312,7 @@ __device__ __forceinline__ void heavy_solve_row(const double* rec, int J, int ro
 void launch_heavy_finalize(int64_t nheavy, const int32_t* hrow, const int32_t* hnseg, const int64_t* hpbase,
                            const double* partials, double* rec, int J, double lambda, void* An, int elem_bytes,
                            int lda, double* sse_row, int* fail, cudaStream_t st, const PeerRows& peers,
-                           int64_t max_seg) {
+                           int64_t max_seg, int64_t min_seg) {
     if (nheavy <= 0) return;
     if (max_seg <= kSmallSeg && (J == 2 || J == 3 || J == 4 || J == 5 || J == 8 || J == 10)) {
         // many rows: a thread per row (c2: 31 -> 15 us per mode); few rows: a warp per row (c1: the
@@ -359,7 +359,8 @@ void launch_heavy_finalize(int64_t nheavy, const int32_t* hrow, const int32_t* h
     const int PW = J * (J + 1) / 2 + J + 1;
     const int64_t nitems = nheavy * PW;
     const unsigned g0 = (unsigned)std::min<int64_t>((nitems + 255) / 256, 148 * 32);
-    k_heavy_sum_small<<<g0, 256, 0, st>>>(nheavy, PW, hnseg, hpbase, partials, rec);
+    if (min_seg <= kSmallSeg)  // (some heavy rows short enough for a thread per component)
+        k_heavy_sum_small<<<g0, 256, 0, st>>>(nheavy, PW, hnseg, hpbase, partials, rec);
     const unsigned g1 = (unsigned)std::min<int64_t>((nitems + 7) / 8, 148 * 32);
     k_heavy_sum<<<g1, 256, 0, st>>>(nheavy, PW, hnseg, hpbase, partials, rec);
     const unsigned g2 = (unsigned)std::min<int64_t>((nheavy + 127) / 128, 148 * 16);

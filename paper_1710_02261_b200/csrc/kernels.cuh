@@ -17,7 +17,7 @@ void launch_permute_core(const void* G, void* Gp, int elem_bytes, int N, int J, 
 void launch_heavy_finalize(int64_t nheavy, const int32_t* hrow, const int32_t* hnseg, const int64_t* hpbase,
                            const double* partials, double* rec, int J, double lambda, void* An, int elem_bytes,
                            int lda, double* sse_row, int* fail, cudaStream_t st, const PeerRows& peers,
-                           int64_t max_seg);  // max segments of a heavy row (<= 64: one fused launch)
+                           int64_t max_seg, int64_t min_seg = 0);  // max segments of a heavy row (<= 64: one fused launch)
 // ---- ptucker_init input validation on the device: bad[0] = first out-of-range coordinate
 // (entry * 16 + mode), bad[1] = first non-finite value (all bits set = none), part[grid] =
 // per-block sums of x^2 ----
