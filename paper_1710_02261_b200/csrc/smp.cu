@@ -65,8 +65,12 @@ __global__ void k_table2(const TS* __restrict__ G, const TS* __restrict__ As1, c
 #define PT_SMP_LIGHT 32
 #endif
 constexpr int kSmpLight = PT_SMP_LIGHT;  // hybrid: fp64 table only for single-segment rows this short
+#ifndef PT_SMP_THREADS
+#define PT_SMP_THREADS kUpdThreads
+#endif
+constexpr int kSmpThreads = PT_SMP_THREADS;  // one CTA per SM (the fp32 table fills shared memory)
 template <typename TS, int J, int MODE>
-__global__ void __launch_bounds__(kUpdThreads, 1) k_update_smp2(const UpdateParams<TS> p, const double* __restrict__ T64,
+__global__ void __launch_bounds__(kSmpThreads, 1) k_update_smp2(const UpdateParams<TS> p, const double* __restrict__ T64,
                                                                const TS* __restrict__ T32, int64_t tab_elems, int ir,
                                                                int is1, int is2, int I2) {
     constexpr int NB = J * (J + 1) / 2;
@@ -273,9 +277,9 @@ int launch_smp2(const UpdateParams<TS>& p, const double* T64, const TS* T32, int
     const size_t smem = MODE == 1 ? 0 : (size_t)tab_elems * sizeof(TS);
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     int nb = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k, kUpdThreads, smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k, kSmpThreads, smem);
     if (nb < 1) nb = 1;
-    k<<<nsm * nb, kUpdThreads, smem, st>>>(p, T64, T32, tab_elems, ir, is1, is2, I2);
+    k<<<nsm * nb, kSmpThreads, smem, st>>>(p, T64, T32, tab_elems, ir, is1, is2, I2);
     return 0;
 }
 
