@@ -80,8 +80,11 @@ def roofline(N, J, policy, info, l0_group, nsm, clk_mhz, entries, launch_s, dtyp
         # inner stage on tcgen05; level 0 (J^2) fp64 per term (l0_group 1) or fp32 partial sums
         # of l0_group terms added in fp64 (J*ceil(J/g) DADDs)
         g = l0_group if policy != "F32-A" else J
-        nparts = -(-J // g)
-        if g == 1:
+        nparts = -(-J // g) if g > 0 else 1
+        if g == 0:  # compensated fp32 level 0 (J^2 products on the FMA pipe), fp64 combine
+            w32, w64 = J * J, J + bc
+            xu = 2 * J + 1
+        elif g == 1:
             w32, w64 = 0, J * J + bc
             xu = J * J + J + 1
         else:
@@ -564,7 +567,7 @@ def main():
                          "default; 0 = leave the driver's setting)")
     ap.add_argument("--pack-gathers", type=int, default=0, choices=[0, 1],
                     help="J = 10 tensor-core gathers from packed 40-byte tables (less DRAM traffic, slower)")
-    ap.add_argument("--l0-group", type=int, default=1, choices=[1, 2, 5], help="tensor-core level-0 grouping (1 = fp64 per term, g = fp32 partial sums of g terms)")
+    ap.add_argument("--l0-group", type=int, default=1, choices=[0, 1, 2, 5], help="tensor-core level-0 grouping (1 = fp64 per term, g = fp32 partial sums of g terms, 0 = compensated fp32 pairs)")
     ap.add_argument("--exchange", default="push", choices=["push", "nccl"],
                     help="multi-GPU replica refresh: rows pushed by the kernels over NVLink, or NCCL all-gather-v")
     ap.add_argument("--dtype", default=None, choices=["f32", "f64"],

@@ -225,7 +225,9 @@ int ptucker_get_partition(int32_t n, int64_t* bounds);
  *                 (default).  Modes with longer rows, the SMP and the generic kernels always
  *                 use the finalize launch
  *  "l0_group"     tensor-core kernel, F32-B: level-0 terms summed in fp32 in runs of g before
- *                 the fp64 sum (1 = every term in fp64, default; 2; 5 fails the 1e-5 row bound)
+ *                 the fp64 sum (1 = every term in fp64, default; 2; 5 fails the 1e-5 row bound;
+ *                 0 = packed fp32 pairs with Kahan compensation, even J: worst full-size c5 row
+ *                 5.8e-6, no faster)
  *  "l2_persist_mb" L2 set-aside (MB) for the evict_last factor-row gathers: -1 = the device
  *                 maximum (default; applied at init, released by ptucker_finalize), 0 = leave
  *                 the driver default.  Side effect: cudaLimitPersistingL2CacheSize is a

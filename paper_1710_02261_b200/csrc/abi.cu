@@ -713,7 +713,7 @@ int ptucker_set_option(const char* key, int64_t value) {
         return PTUCKER_OK;
     }
     if (k == "l0_group") {
-        if (value != 1 && value != 2 && value != 5) return fail(PTUCKER_EINVAL, "l0_group must be 1, 2 or 5");
+        if (value != 0 && value != 1 && value != 2 && value != 5) return fail(PTUCKER_EINVAL, "l0_group must be 0, 1, 2 or 5");
         g.l0_group = (int)value;
         return PTUCKER_OK;
     }

@@ -205,6 +205,25 @@ __device__ __forceinline__ void mma_tf32_ta(uint32_t tmem_d, uint32_t tmem_a, ui
         "tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n\t}\n" ::"r"(tmem_d),
         "r"(tmem_a), "l"(db), "r"(idesc), "r"(acc));
 }
+// packed fp32 pairs (FFMA2 / FADD2): two level-0 columns per instruction
+__device__ __forceinline__ uint64_t fma_f32x2(uint64_t a, uint64_t b, uint64_t c) {
+    uint64_t d;
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+    return d;
+}
+__device__ __forceinline__ uint64_t add_f32x2(uint64_t a, uint64_t b) {
+    uint64_t d;
+    asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+    return d;
+}
+__device__ __forceinline__ uint64_t sub_f32x2(uint64_t a, uint64_t b) {
+    uint64_t d;
+    asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+    return d;
+}
+__device__ __forceinline__ uint64_t pack_f32x2(float lo, float hi) {
+    return (uint64_t)__float_as_uint(lo) | ((uint64_t)__float_as_uint(hi) << 32);
+}
 __device__ __forceinline__ void mma_f16_ta(uint32_t tmem_d, uint32_t tmem_a, uint64_t db, uint32_t idesc, uint32_t acc) {
     asm volatile(
         "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
@@ -1032,6 +1051,16 @@ __global__ void __launch_bounds__(kThreads, 1) k_update_tc(const UpdateParams<fl
             }
 #pragma unroll
             for (int j = 0; j < J; ++j) d[j] = TD(0);
+            // G0 == 0 (l0_group 0): level 0 in fp32 pairs (FFMA2 / FADD2, columns j, j + 1) with
+            // Kahan compensation: y = a0 t + cn (the product exact inside the FMA, one rounding),
+            // s' = s + y, cn = (s - s') + y; delta_j = s_j + cn_j in fp64 (exact widenings) --
+            // one rounding per product instead of none (fp64 level 0), and no growth with k0
+            static_assert(G0 != 0 || (LAST64 && J % 2 == 0), "compensated level 0: fp64 delta, even J");
+            uint64_t ks[G0 == 0 ? J / 2 : 1], kc[G0 == 0 ? J / 2 : 1];
+            if constexpr (G0 == 0) {
+#pragma unroll
+                for (int q = 0; q < J / 2; ++q) ks[q] = kc[q] = 0ull;
+            }
 #pragma unroll
             for (int cc = 0; cc < J * J; ++cc) {
                 const int k0 = cc / J, j = cc % J;
@@ -1050,6 +1079,19 @@ __global__ void __launch_bounds__(kThreads, 1) k_update_tc(const UpdateParams<fl
                     }
                 }
                 const float tv = __uint_as_float(rb[(cc / 16) % kBCH][cc % 16]);
+                if constexpr (G0 == 0) {
+                    if (j % 2 == 0) {
+                        const uint64_t aa = pack_f32x2(a0f[k0], a0f[k0]);
+                        const uint64_t tt = (uint64_t)rb[(cc / 16) % kBCH][cc % 16] |
+                                            ((uint64_t)rb[((cc + 1) / 16) % kBCH][(cc + 1) % 16] << 32);
+                        const int q = j / 2;
+                        const uint64_t y = fma_f32x2(aa, tt, kc[q]);
+                        const uint64_t s1 = add_f32x2(ks[q], y);
+                        kc[q] = add_f32x2(sub_f32x2(ks[q], s1), y);
+                        ks[q] = s1;
+                    }
+                    continue;
+                }
 #ifdef PT_EXP_NOL0  // experiment (wrong results): level-0 arithmetic reduced to one fp32 add per term
                 if (true) {
                     pf[j] = (k0 == 0 ? 0.f : pf[j]) + tv;
@@ -1075,6 +1117,13 @@ __global__ void __launch_bounds__(kThreads, 1) k_update_tc(const UpdateParams<fl
                 asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
                 __syncwarp();
                 if (lane == 0) mbar_arrive(acc_empty(b));
+            }
+            if constexpr (G0 == 0) {
+#pragma unroll
+                for (int q = 0; q < J / 2; ++q) {
+                    d[2 * q] = TD(__uint_as_float((uint32_t)ks[q])) + TD(__uint_as_float((uint32_t)kc[q]));
+                    d[2 * q + 1] = TD(__uint_as_float((uint32_t)(ks[q] >> 32))) + TD(__uint_as_float((uint32_t)(kc[q] >> 32)));
+                }
             }
             if constexpr (kF16 && !kFold) {
                 // (fp32: in two steps, 2^-ssc can leave the float range)
@@ -1279,6 +1328,10 @@ void launch_tc(const void* params, bool literal, int grid, cudaStream_t st) {
         if (p.aux_stride > 0) launch_tc_g<J, true, 1, true>(p, grid, st);  // table mode
         else if (p.l0_group == 1) launch_tc_g<J, true, 1>(p, grid, st);
         else if (p.l0_group == 2) launch_tc_g<J, true, 2>(p, grid, st);
+        else if (p.l0_group == 0) {
+            if constexpr (J % 2 == 0) launch_tc_g<J, true, 0>(p, grid, st);
+            else launch_tc_g<J, true, 1>(p, grid, st);  // (odd J: no column pairs; fp64 level 0)
+        }
         else launch_tc_g<J, true, 5>(p, grid, st);
     }
 }

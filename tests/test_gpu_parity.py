@@ -148,6 +148,21 @@ def test_mode_update_f32(pt, orc, name, scale, seg):
         assert [m["smp"] for m in info["modes"]] == [2, 2, 1, 1]
 
 
+@pytest.mark.parametrize("name,scale", [("c5", 0.001), ("c2", 0.01)])
+def test_mode_update_l0_kahan(pt, orc, name, scale):
+    """l0_group 0: level 0 in packed fp32 pairs with Kahan compensation (one rounding per
+    product), held to the same 1e-5 per row (full size, all 3x10^6 c5 rows: 5.8e-6,
+    profiles/r02/l0_group_row_errors_c5_full_kahan.txt)."""
+    cfg = synth.small(name, scale)
+    coords, vals = init_cfg(pt, cfg)
+    pt.ptucker_set_option("l0_group", 0)
+    t = orc.Tensor(coords, vals, cfg.dims)
+    w0 = mode_update_parity(pt, orc, t, cfg, 1e-5, sweeps=0)
+    w1 = mode_update_parity(pt, orc, t, cfg, 1e-5, sweeps=1)
+    pt.ptucker_set_option("l0_group", 1)
+    print(f"{name}@{scale} l0_group 0 worst row rel err init {w0:.2e} mid {w1:.2e}")
+
+
 @pytest.mark.parametrize("scale,seg", [(0.001, 256), (0.005, 256), (0.005, 7)])
 def test_mode_update_c4_f32c2(pt, orc, scale, seg):
     """Policy 3 (F32-C2, order 5): the level next to the innermost in fp32 (J^3 instead of J^4
