@@ -67,7 +67,7 @@ def roofline(N, J, policy, info, l0_group, nsm, clk_mhz, entries, launch_s, dtyp
     mp = measured_peaks()
     p32 = nsm * 128 * 2 * clk_mhz * 1e6 / 1e12
     p64 = nsm * 64 * 2 * clk_mhz * 1e6 / 1e12
-    ptc = 0.5 * mp.get("bf16_tflops", 1590.0)
+    ptc = mp.get("bf16_tflops", 1590.0)  # the inner stage runs kind::f16 (fp16 splits): the bf16 rate
     bw = mp.get("hbm_gbs", 6650.0)
     inner = J ** N
     levels = [J ** (L + 2) for L in range(N - 2)]
@@ -85,8 +85,10 @@ def roofline(N, J, policy, info, l0_group, nsm, clk_mhz, entries, launch_s, dtyp
             w32, w64 = J * J, J + bc
             xu = 2 * J + 1
         elif g == 1:
+            # fp32 -> fp64 widenings on the XU: the t of 3 of the J rows k0 (the others by three
+            # integer operations), the J weights a0 and x
             w32, w64 = 0, J * J + bc
-            xu = J * J + J + 1
+            xu = 3 * J + J + 1
         else:
             w32, w64 = J * J, J * nparts + bc
             xu = J * nparts + 1
@@ -100,12 +102,12 @@ def roofline(N, J, policy, info, l0_group, nsm, clk_mhz, entries, launch_s, dtyp
 
     def pipe_times(a32, a64, atc):
         return {"fp32": 2 * a32 * entries / (p32 * 1e12), "fp64": 2 * a64 * entries / (p64 * 1e12),
-                "tensor_tf32": 2 * atc * entries / (ptc * 1e12), "hbm": hbm_bytes / (bw * 1e9)}
+                "tensor_f16": 2 * atc * entries / (ptc * 1e12), "hbm": hbm_bytes / (bw * 1e9)}
 
     t = pipe_times(w32, w64, wtc)
     pipe = max(t, key=t.get)
-    peak = {"fp32": p32, "fp64": p64, "tensor_tf32": ptc, "hbm": bw}[pipe]
-    work = {"fp32": 2 * w32, "fp64": 2 * w64, "tensor_tf32": 2 * wtc}.get(pipe)
+    peak = {"fp32": p32, "fp64": p64, "tensor_f16": ptc, "hbm": bw}[pipe]
+    work = {"fp32": 2 * w32, "fp64": 2 * w64, "tensor_f16": 2 * wtc}.get(pipe)
     kinds = [m.get("smp", 0) for m in info.get("modes", [])]
     per_mode = None
     if mode_s and any(kinds) and policy != "F64":
@@ -123,21 +125,21 @@ def roofline(N, J, policy, info, l0_group, nsm, clk_mhz, entries, launch_s, dtyp
                              "roof_ms": tn[pn] * 1e3, "measured_ms": mode_s[n] * 1e3})
         frac_t = roof_sum / sum(mode_s)
         pipe = max(pipe_sum, key=pipe_sum.get)
-        peak = {"fp32": p32, "fp64": p64, "tensor_tf32": ptc, "hbm": bw}[pipe]
+        peak = {"fp32": p32, "fp64": p64, "tensor_f16": ptc, "hbm": bw}[pipe]
         achieved, unit = frac_t * peak, ("GB/s" if pipe == "hbm" else "TFLOP/s")
-        bound = "hbm" if pipe == "hbm" else ("tensor" if pipe == "tensor_tf32" else "alu")
+        bound = "hbm" if pipe == "hbm" else ("tensor" if pipe == "tensor_f16" else "alu")
     elif pipe == "hbm":
         achieved, unit, bound = hbm_bytes / launch_s / 1e9, "GB/s", "hbm"
     else:
         achieved, unit = work * entries / launch_s / 1e12, "TFLOP/s"
-        bound = "tensor" if pipe == "tensor_tf32" else "alu"
+        bound = "tensor" if pipe == "tensor_f16" else "alu"
     r = {"bound": bound, "achieved": achieved, "peak": peak, "unit": unit, "frac": achieved / peak,
          "traffic": load_traffic(cfg_name), "pipe": pipe,
          "kernel": "k_update_tc (tcgen05 3xTF32 inner stage + level 0 + fp64 normal equations + Cholesky)" if tc
          else "k_update (fused TTV + fp64 normal equations + Cholesky)",
          "peak_source": {"fp32": f"derived: {nsm} SMs x 128 FMA/clk x 2 x {clk_mhz:.0f} MHz",
                          "fp64": f"derived: {nsm} SMs x 64 FMA/clk x 2 x {clk_mhz:.0f} MHz (pipe_probe: 63.2/clk measured)",
-                         "tensor_tf32": "MEASURED_PEAKS bf16_tflops x 0.5 (nominal tf32/bf16)",
+                         "tensor_f16": "MEASURED_PEAKS bf16_tflops (fp16 operands run at the bf16 rate)",
                          "hbm": "MEASURED_PEAKS hbm_gbs"}[pipe],
          "work_per_entry": {"fp32_fma": w32, "fp64_fma": w64, "tc_mac": wtc, "hbm_bytes": 4 * (N - 1) + sv},
          "roof_ms_by_pipe": {k: v * 1e3 for k, v in t.items()}, "roof_ms": t[pipe] * 1e3}
@@ -150,9 +152,10 @@ def roofline(N, J, policy, info, l0_group, nsm, clk_mhz, entries, launch_s, dtyp
         r["xu_conversions_per_entry"] = xu
         r["xu_floor_ms"] = xu * entries / xu_peak * 1e3
     if tc:
-        kp, np_ = -(-J // 8) * 8, -(-(J * J) // 16) * 16
-        r["tc_executed_mac_per_entry"] = 3 * kp * np_
-        r["tc_executed_floor_ms"] = 2 * 3 * kp * np_ * entries / (ptc * 1e12) * 1e3
+        # one K sweep over [lo | hi | hi] padded to the f16 K-step of 16, N padded to 16
+        kc, np_ = -(-(3 * J) // 16) * 16, -(-(J * J) // 16) * 16
+        r["tc_executed_mac_per_entry"] = kc * np_
+        r["tc_executed_floor_ms"] = 2 * kc * np_ * entries / (ptc * 1e12) * 1e3
     return r
 
 
