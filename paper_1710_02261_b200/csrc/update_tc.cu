@@ -54,10 +54,18 @@ namespace tc {
 
 constexpr int kE = 128;                      // TMEM lanes = segments per group (4 slices)
 constexpr int kThreads = 16 * 32;            // 2 level-0 WGs, normal-equation WG, loader/MMA WG
+// PT_NOSTASH: the level-0 warps read a0, x and the scale exponent straight from the row-ring
+// slot when they reduce the tile (the slot is released then, not at the split), instead of a
+// copy into a per-warp stash at the split: 18 KB less shared-memory traffic per tile; the ring
+// holds kNA more tiles
+#ifndef PT_NOSTASH
+#define PT_NOSTASH 1
+#endif
 #ifndef PT_RING
-#define PT_RING 6
+#define PT_RING (PT_NOSTASH ? 10 : 6)
 #endif
 constexpr int kRing = PT_RING;                     // row ring slots (tiles between loader and level 0)
+constexpr bool kNoStash = PT_NOSTASH != 0;
 constexpr int kCPref = 7;                    // loader: coordinates fetched this many tiles ahead of the gathers
 #ifndef PT_LOADERS
 #define PT_LOADERS 3
@@ -392,13 +400,13 @@ struct Shape {
     static_assert(ACOL + kNA * ACOLS <= TCOLS, "TMEM columns");
     // shared memory map (bytes)
     static constexpr int B_BYTES = kKcat ? NP * KC * 4 / 2 : NP * KP * 4;  // one of B_hi / B_lo (kKcat: half of B)
-    static constexpr int RSLOT = 2 * NQ * kE * 16 + kE * 4; // row ring slot: rows a0, a1 (chunk-major), x
+    static constexpr int RSLOT = 2 * NQ * kE * 16 + kE * 4 + (kNoStash ? kE * 4 : 0);  // rows a0, a1 (chunk-major), x (, scale)
     static constexpr int CSLOT = 3 * kE * 4;                // coordinate ring slot: c0, c1, x
     static constexpr int JD = (J + 1) / 2 * 2;              // delta doubles per lane (even: 16-byte pairs)
     static constexpr int DSLOT = JD * kE * 8 + kE * 4;      // delta ring slot: delta[u][j] (fp64), x[u]
     static constexpr int OFF_BHI = 0;
     static constexpr int OFF_BLO = OFF_BHI + B_BYTES;
-    static constexpr int OFF_MISC = OFF_BLO + B_BYTES;      // tmem base, tiles
+    static constexpr int OFF_MISC = OFF_BLO + (kF16 ? 0 : B_BYTES);  // tmem base, tiles (fp16: B is one array)
     static constexpr int OFF_ROW = (OFF_MISC + 64 + 127) / 128 * 128;
     static constexpr int OFF_CRD = OFF_ROW + kRing * RSLOT;
     static constexpr int OFF_DEL = OFF_CRD + kCRing * CSLOT;
@@ -407,7 +415,7 @@ struct Shape {
     // (+ [32] int: the lane's fp16 scale exponent sA + sG)
     static constexpr int STSLOT = NQ * kWarp * 16 + kWarp * 4 + kWarp * 4;
     static constexpr int OFF_STASH = OFF_DEL + kD * DSLOT;
-    static constexpr int OFF_BAR = (OFF_STASH + 8 * kStash * STSLOT + 7) / 8 * 8;
+    static constexpr int OFF_BAR = (OFF_STASH + (kNoStash ? 0 : 8 * kStash * STSLOT) + 7) / 8 * 8;
     // raw_full[kRing], raw_empty[kRing], acc_full[kNT], acc_empty[kNT], a_full[kNA], d_full[4][kD], d_empty[4][kD],
     // a_empty[kNA]
     static constexpr int NBAR = 2 * kRing + 2 * kNT + 2 * kNA + 8 * kD + 1;  // + b_free (table mode)
@@ -513,6 +521,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_update_tc(const UpdateParams<fl
     };
     auto rowx = [&](int s, int u) -> float* {
         return reinterpret_cast<float*>(sm + SH::OFF_ROW + s * SH::RSLOT + 2 * NQ * kE * 16) + u;
+    };
+    auto rowscale = [&](int s, int u) -> int* {  // kNoStash: the lane's fp16 scale exponent (split -> level 0)
+        return reinterpret_cast<int*>(sm + SH::OFF_ROW + s * SH::RSLOT + 2 * NQ * kE * 16 + kE * 4) + u;
     };
     // coordinate ring slot s: c0, c1, x (a = 0, 1, 2) of segment u
     auto crd = [&](int s, int a, int u) -> uint32_t* {
@@ -947,7 +958,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_update_tc(const UpdateParams<fl
                 lo[i] = __float_as_uint(__uint_as_float(w) - __uint_as_float(hh));
             }
             // a0 and x of the tile go to this warp's stash: the ring slot is free once split
-            {
+            if constexpr (kNoStash) {
+                if constexpr (kF16) *rowscale(s, te) = sA + sG;
+            } else {
                 const int st = (int)((k >> 1) % kStash);
                 unsigned char* sb = stash + st * SH::STSLOT;
 #pragma unroll
@@ -997,7 +1010,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_update_tc(const UpdateParams<fl
             __syncwarp();
             if (lane == 0) {
                 mbar_arrive(a_full((int)(k % kNA)));
-                mbar_arrive(raw_empty(s));
+                if constexpr (!kNoStash) mbar_arrive(raw_empty(s));
             }
         };
         // this warp writes the A rows of its own tiles (kNA is even: tile k + kNA has
@@ -1017,20 +1030,37 @@ __global__ void __launch_bounds__(kThreads, 1) k_update_tc(const UpdateParams<fl
             const uint32_t taddr = tm_lane + b * NP;
 #pragma unroll
             for (int ch = 0; ch < kBCH && ch < NCH; ++ch) tmem_ld16(taddr + ch * 16, rb[ch]);
-            // a0 and x of tile k from this warp's stash (written by this thread in split(k))
+            // a0 and x of tile k from this warp's stash (written by this thread in split(k)), or
+            // (kNoStash) from the ring slot itself, which is released here
             const unsigned char* sbk = stash + (int)((k >> 1) % kStash) * SH::STSLOT;
             float a0f[J];
+            float x;
+            int ssc;  // kF16: t arrives scaled by 2^ssc (row and core scalings), undone in the weights
+            if constexpr (kNoStash) {
 #pragma unroll
-            for (int q = 0; q < NQ; ++q) {
-                const float4 v = reinterpret_cast<const float4*>(sbk)[q * kWarp + lane];
-                const float wv[4] = {v.x, v.y, v.z, v.w};
+                for (int q = 0; q < NQ; ++q) {
+                    const uint4 v = *rowc(s, 0, q, te);
+                    const uint32_t wv[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
-                for (int u = 0; u < 4; ++u)
-                    if (4 * q + u < J) a0f[4 * q + u] = wv[u];
+                    for (int u = 0; u < 4; ++u)
+                        if (4 * q + u < J) a0f[4 * q + u] = __uint_as_float(wv[u]);
+                }
+                x = *rowx(s, te);
+                ssc = kF16 ? *rowscale(s, te) : 0;
+                __syncwarp();
+                if (lane == 0) mbar_arrive(raw_empty(s));
+            } else {
+#pragma unroll
+                for (int q = 0; q < NQ; ++q) {
+                    const float4 v = reinterpret_cast<const float4*>(sbk)[q * kWarp + lane];
+                    const float wv[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+                    for (int u = 0; u < 4; ++u)
+                        if (4 * q + u < J) a0f[4 * q + u] = wv[u];
+                }
+                x = reinterpret_cast<const float*>(sbk + NQ * kWarp * 16)[lane];
+                ssc = kF16 ? reinterpret_cast<const int*>(sbk + NQ * kWarp * 16 + kWarp * 4)[lane] : 0;
             }
-            const float x = reinterpret_cast<const float*>(sbk + NQ * kWarp * 16)[lane];
-            // kF16: t arrives scaled by 2^ssc (row and core scalings), undone in the weights
-            const int ssc = kF16 ? reinterpret_cast<const int*>(sbk + NQ * kWarp * 16 + kWarp * 4)[lane] : 0;
             mark(k, 2);
 #pragma unroll
             for (int ch = 0; ch < kBCH && ch < NCH; ++ch) tmem_wait16(rb[ch]);
