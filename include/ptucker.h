@@ -214,6 +214,13 @@ int ptucker_get_partition(int32_t n, int64_t* bounds);
  *  "graph"        1 = ptucker_sweep records its launches once as a CUDA graph and replays it
  *                 (default); the graph is dropped by any option change, init, finalize,
  *                 QR and ptucker_open_peers; not used while time_kernels is on.  0 = direct
+ *  "pdl"          1 = programmatic dependent launch: the tensor-core update, the heavy-row
+ *                 finalize and the error-sum kernels are launched with programmatic stream
+ *                 serialization, so each one's CTAs start (TMEM allocation, barrier setup) on
+ *                 the SMs its predecessor vacates and wait in griddepcontrol.wait for the
+ *                 predecessor's results; bit-identical results, but measured slower under
+ *                 the sweep's CUDA graph (c2 0.26 -> 0.37 ms per iteration, c1 and c5
+ *                 unchanged).  Process-wide (all contexts).  0 = plain stream order (default)
  *  "seg_len"      segment length S of the index (before init): -1 = automatic (default: the
  *                 power of two >= |Omega| / (SMs x 128) in [8, 256]), else 1..2^20
  *  "time_kernels" 1 = bracket every kernel launch with CUDA events (ptucker_kernel_stats)

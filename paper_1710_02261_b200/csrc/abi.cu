@@ -330,9 +330,17 @@ int launch_update_kernel(int n, bool literal) {
     const int grid = literal ? g.grid_lit : g.grid_upd;
     g.inline_used = false;
     if (g.mi[n].nslices == 0) return PTUCKER_OK;
-    CK(cudaMemsetAsync(g.d_work, 0, sizeof(unsigned int), S()));
     const Ctx::Smp& sp = g.smp[n];
-    if (!literal && g.use_smp && sp.kind == 2 && !(g.prec == PTUCKER_F32 && g.smp_tab != 1 && sp.elems * 4 > 200 * 1024)) {
+    // the dynamic slice counter of the ALU / SMP kernels; the tensor-core kernel schedules
+    // statically, and without the memset between it and the previous kernel its launch keeps
+    // the programmatic (PDL) edge
+    const bool smp2 = !literal && g.use_smp && sp.kind == 2 &&
+                      !(g.prec == PTUCKER_F32 && g.smp_tab != 1 && sp.elems * 4 > 200 * 1024);
+    const bool tc_main = !literal && !g.generic && !(g.use_smp && sp.kind == 1) && !smp2 && g.kern != g.kern_alu;
+    const bool tc_table = !literal && !smp2 && g.use_smp && sp.kind == 1 && g.mi[n].aux_groups && g.use_tc &&
+                          g.prec != PTUCKER_F64 && find_update_kernel_tc(1, g.J) != nullptr;
+    if (!tc_main && !tc_table) CK(cudaMemsetAsync(g.d_work, 0, sizeof(unsigned int), S()));
+    if (smp2) {
         // small-mode precontraction: T from the (unchanged) small-mode factors, then J^2 per entry
         const int mode = g.prec == PTUCKER_F64 ? 1 : g.smp_tab;
         launch_smp_table2(g.G, g.A[sp.s1], g.A[sp.s2], g.lda, g.dims[sp.s1], g.dims[sp.s2], g.J, n, sp.r, sp.s1, sp.s2,
@@ -383,7 +391,6 @@ int launch_update_kernel(int n, bool literal) {
             UpdateParams<float> p = make_params<float>(n, false);
             fill(p);
             p.gmain[0] = p.gmain[1] = p.gtail[0] = p.gtail[1] = nullptr;
-            CK(cudaMemsetAsync(g.d_work, 0, sizeof(unsigned int), S()));
             g.inline_used = p.seg_done != nullptr;
             ktc->launch(&p, false, g.nsm, S());
             ok = true;
@@ -671,6 +678,11 @@ int ptucker_set_option(const char* key, int64_t value) {
     if (!key) return fail(PTUCKER_EINVAL, "null key");
     const std::string k = key;
     invalidate_graph();
+    if (k == "pdl") {
+        if (value != 0 && value != 1) return fail(PTUCKER_EINVAL, "pdl must be 0 or 1");
+        g_pdl = (int)value;
+        return PTUCKER_OK;
+    }
     if (k == "graph") {
         if (value != 0 && value != 1) return fail(PTUCKER_EINVAL, "graph must be 0 or 1");
         g.use_graph = (int)value;

@@ -58,6 +58,43 @@ struct PeerRows {
     int n = 0;                          // peers (world - 1), 0: no push
     void* base[kMaxPeers] = {nullptr};  // peer replica of A^(n), same row stride as the local one
 };
+// Programmatic dependent launch (PDL, option "pdl"): the kernels of a sweep (mode updates,
+// heavy-row finalize, error sums) are launched with programmatic stream serialization, so a
+// kernel's CTAs are placed on the SMs its predecessor's CTAs vacate and run their prologue
+// (TMEM allocation, barrier setup) while the predecessor's tail drains.  Every kernel launched
+// this way calls pdl_wait() before it reads anything a predecessor writes: griddepcontrol.wait
+// returns once the preceding grid has completed and its stores are visible (immediately when
+// the launch carried no programmatic dependency).  pdl_trigger() lets the next grid launch.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+// where a kernel lets its dependent launch: at its start (PT_PDL_LATE 0) or once its own
+// pdl_wait() has returned (PT_PDL_LATE 1, the default: see DESIGN.md §9 for the A/B)
+#ifndef PT_PDL_LATE
+#define PT_PDL_LATE 1
+#endif
+__device__ __forceinline__ void pdl_trigger_early() {
+    if constexpr (!PT_PDL_LATE) pdl_trigger();
+}
+__device__ __forceinline__ void pdl_wait_trigger() {
+    pdl_wait();
+    if constexpr (PT_PDL_LATE) pdl_trigger();
+}
+extern int g_pdl;  // option "pdl" (default 0)
+template <typename... KArgs, typename... Args>
+inline void launch_pdl(void (*k)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, Args... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = g_pdl ? 1 : 0;
+    cudaLaunchKernelEx(&cfg, k, static_cast<KArgs>(args)...);
+}
+
 // Copy the row just stored at `local` (row_bytes, a multiple of 16) into every peer
 // replica at the same row.  The reads return this thread's own stores.
 __device__ __forceinline__ void push_row(const PeerRows& pr, const void* local, int64_t row, int row_bytes) {

@@ -11,6 +11,8 @@
 
 namespace pt {
 
+int g_pdl = 0;  // option "pdl" (internal.cuh): off, measured slower under graph replay
+
 // ---------------------------------------------------------------------------
 // Init (Alg. 2 line 1; "random real values between 0 and 1").
 // Reading R2: z = mix64(seed*0x9E3779B97F4A7C15 + (stream+1)*0xD1B54A32D192ED03 + idx),
@@ -133,6 +135,8 @@ constexpr int kSmallSeg = 64;
 __global__ void __launch_bounds__(256) k_heavy_sum_small(int64_t nheavy, int PW, const int32_t* hnseg,
                                                          const int64_t* hpbase, const double* partials,
                                                          double* rec) {
+    pdl_trigger_early();
+    pdl_wait_trigger();
     for (int64_t w = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; w < nheavy * PW;
          w += (int64_t)gridDim.x * blockDim.x) {
         const int64_t h = w / PW;
@@ -148,6 +152,8 @@ __global__ void __launch_bounds__(256) k_heavy_sum_small(int64_t nheavy, int PW,
 
 __global__ void __launch_bounds__(256) k_heavy_sum(int64_t nheavy, int PW, const int32_t* hnseg,
                                                    const int64_t* hpbase, const double* partials, double* rec) {
+    pdl_trigger_early();
+    pdl_wait_trigger();
     const int lane = threadIdx.x & 31;
     const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
     for (int64_t w = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); w < nheavy * PW; w += nw) {
@@ -180,6 +186,8 @@ template <typename T, int JC>
 __global__ void __launch_bounds__(128) k_heavy_solve(int64_t nheavy, const int32_t* hrow, const double* recs, int J,
                                                      double lambda, T* An, int lda, double* sse_row, int* fail,
                                                      const PeerRows peers) {
+    pdl_trigger_early();
+    pdl_wait_trigger();
     const int PW = J * (J + 1) / 2 + J + 1;
     for (int64_t h = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; h < nheavy; h += (int64_t)gridDim.x * blockDim.x)
         heavy_solve_row<T, JC>(recs + h * PW, J, hrow[h], lambda, An, lda, sse_row, fail, peers);
@@ -195,6 +203,8 @@ template <typename T, int JC>
 __global__ void __launch_bounds__(64) k_heavy_thread(int64_t nheavy, const int32_t* hrow, const int32_t* hnseg,
                                                      const int64_t* hpbase, const double* partials, double lambda,
                                                      T* An, int lda, double* sse_row, int* fail, const PeerRows peers) {
+    pdl_trigger_early();
+    pdl_wait_trigger();
     constexpr int NB = JC * (JC + 1) / 2;
     for (int64_t h = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; h < nheavy; h += (int64_t)gridDim.x * blockDim.x) {
         const int nseg = hnseg[h];
@@ -244,6 +254,8 @@ template <typename T, int JC>
 __global__ void __launch_bounds__(128) k_heavy_warp(int64_t nheavy, const int32_t* hrow, const int32_t* hnseg,
                                                     const int64_t* hpbase, const double* partials, double lambda,
                                                     T* An, int lda, double* sse_row, int* fail, const PeerRows peers) {
+    pdl_trigger_early();
+    pdl_wait_trigger();
     constexpr int PW = JC * (JC + 1) / 2 + JC + 1;
     __shared__ double rec[4][PW];
     const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -321,10 +333,10 @@ void launch_heavy_finalize(int64_t nheavy, const int32_t* hrow, const int32_t* h
             const unsigned gw = (unsigned)std::min<int64_t>((nheavy + 3) / 4, 148 * 32);
 #define PT_HFW(JC)                                                                                               \
     if (elem_bytes == 8)                                                                                         \
-        k_heavy_warp<double, JC><<<gw, 128, 0, st>>>(nheavy, hrow, hnseg, hpbase, partials, lambda, (double*)An,   \
+        launch_pdl(k_heavy_warp<double, JC>, gw, 128, 0, st, nheavy, hrow, hnseg, hpbase, partials, lambda, (double*)An,   \
                                                      lda, sse_row, fail, peers);                                 \
     else                                                                                                         \
-        k_heavy_warp<float, JC><<<gw, 128, 0, st>>>(nheavy, hrow, hnseg, hpbase, partials, lambda, (float*)An,     \
+        launch_pdl(k_heavy_warp<float, JC>, gw, 128, 0, st, nheavy, hrow, hnseg, hpbase, partials, lambda, (float*)An,     \
                                                     lda, sse_row, fail, peers);
             switch (J) {
                 case 2: PT_HFW(2) break;
@@ -340,10 +352,10 @@ void launch_heavy_finalize(int64_t nheavy, const int32_t* hrow, const int32_t* h
         const unsigned gf = (unsigned)std::min<int64_t>((nheavy + 63) / 64, 148 * 16);
 #define PT_HFF(JC)                                                                                               \
     if (elem_bytes == 8)                                                                                         \
-        k_heavy_thread<double, JC><<<gf, 64, 0, st>>>(nheavy, hrow, hnseg, hpbase, partials, lambda, (double*)An,  \
+        launch_pdl(k_heavy_thread<double, JC>, gf, 64, 0, st, nheavy, hrow, hnseg, hpbase, partials, lambda, (double*)An,  \
                                                       lda, sse_row, fail, peers);                                \
     else                                                                                                         \
-        k_heavy_thread<float, JC><<<gf, 64, 0, st>>>(nheavy, hrow, hnseg, hpbase, partials, lambda, (float*)An,    \
+        launch_pdl(k_heavy_thread<float, JC>, gf, 64, 0, st, nheavy, hrow, hnseg, hpbase, partials, lambda, (float*)An,    \
                                                      lda, sse_row, fail, peers);
         switch (J) {
             case 2: PT_HFF(2) break;
@@ -360,15 +372,15 @@ void launch_heavy_finalize(int64_t nheavy, const int32_t* hrow, const int32_t* h
     const int64_t nitems = nheavy * PW;
     const unsigned g0 = (unsigned)std::min<int64_t>((nitems + 255) / 256, 148 * 32);
     if (min_seg <= kSmallSeg)  // (some heavy rows short enough for a thread per component)
-        k_heavy_sum_small<<<g0, 256, 0, st>>>(nheavy, PW, hnseg, hpbase, partials, rec);
+        launch_pdl(k_heavy_sum_small, g0, 256, 0, st, nheavy, PW, hnseg, hpbase, partials, rec);
     const unsigned g1 = (unsigned)std::min<int64_t>((nitems + 7) / 8, 148 * 32);
-    k_heavy_sum<<<g1, 256, 0, st>>>(nheavy, PW, hnseg, hpbase, partials, rec);
+    launch_pdl(k_heavy_sum, g1, 256, 0, st, nheavy, PW, hnseg, hpbase, partials, rec);
     const unsigned g2 = (unsigned)std::min<int64_t>((nheavy + 127) / 128, 148 * 16);
 #define PT_HF(JC)                                                                                                  \
     if (elem_bytes == 8)                                                                                           \
-        k_heavy_solve<double, JC><<<g2, 128, 0, st>>>(nheavy, hrow, rec, J, lambda, (double*)An, lda, sse_row, fail, peers); \
+        launch_pdl(k_heavy_solve<double, JC>, g2, 128, 0, st, nheavy, hrow, rec, J, lambda, (double*)An, lda, sse_row, fail, peers); \
     else                                                                                                           \
-        k_heavy_solve<float, JC><<<g2, 128, 0, st>>>(nheavy, hrow, rec, J, lambda, (float*)An, lda, sse_row, fail, peers);
+        launch_pdl(k_heavy_solve<float, JC>, g2, 128, 0, st, nheavy, hrow, rec, J, lambda, (float*)An, lda, sse_row, fail, peers);
     switch (J) {
         case 2: PT_HF(2) break;
         case 3: PT_HF(3) break;
@@ -396,6 +408,8 @@ __device__ __forceinline__ double block_tree_sum(double v, double* sm) {
 }
 
 __global__ void __launch_bounds__(256) k_sum_stage1(const double* x, int64_t n, double* part) {
+    pdl_trigger_early();
+    pdl_wait_trigger();
     __shared__ double sm[256];
     const int64_t chunk = (n + 255) / 256;
     const int64_t b0 = blockIdx.x * chunk;
@@ -407,14 +421,16 @@ __global__ void __launch_bounds__(256) k_sum_stage1(const double* x, int64_t n, 
 }
 
 __global__ void __launch_bounds__(256) k_sum_stage2(const double* part, double* out) {
+    pdl_trigger_early();
+    pdl_wait_trigger();
     __shared__ double sm[256];
     const double s = block_tree_sum(part[threadIdx.x], sm);
     if (threadIdx.x == 0) *out = s;
 }
 
 void launch_sum(const double* x, int64_t n, double* part256, double* out, cudaStream_t st) {
-    k_sum_stage1<<<256, 256, 0, st>>>(x, n, part256);
-    k_sum_stage2<<<1, 256, 0, st>>>(part256, out);
+    launch_pdl(k_sum_stage1, 256, 256, 0, st, x, n, part256);
+    launch_pdl(k_sum_stage2, 1, 256, 0, st, part256, out);
 }
 
 // ---------------------------------------------------------------------------

@@ -543,6 +543,47 @@ __global__ void __launch_bounds__(kThreads, 1) k_update_tc(const UpdateParams<fl
     const Sched s0{ngroups, 0, (int)gridDim.x, (int)blockIdx.x};
 
     // ---------------------------------------------------------------- setup
+    pdl_trigger_early();  // the next grid may be placed on the SMs this one vacates
+    if constexpr (NQ == 3) {
+        // packed J = 10 gathers write 8 of chunk 2's 16 bytes: the rest (row padding) stays zero
+        for (int i = threadIdx.x; i < kRing * 2 * kE; i += kThreads) {
+            const int sl = i / (2 * kE), k = (i / kE) % 2, u = i % kE;
+            float* c2 = reinterpret_cast<float*>(rowc(sl, k, 2, u));
+            c2[2] = 0.f;
+            c2[3] = 0.f;
+        }
+    }
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&misc[0])),
+                     "n"(SH::TCOLS));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    if (warp == 14) {
+        if (lane == 0) {
+            for (int s = 0; s < kRing; ++s) {
+                mbar_init(raw_full(s), 2 * kWarp);  // loader lanes: cp.async completion + plain arrive (x)
+                mbar_init(raw_empty(s), 4);         // the 4 level-0 warps of the tile (split: a1 to TMEM, a0/x to the stash)
+            }
+            for (int b = 0; b < kNT; ++b) {
+                mbar_init(acc_full(b), 1);   // tcgen05.commit
+                mbar_init(acc_empty(b), 4);  // level-0 warps done reading the accumulator
+            }
+            for (int a = 0; a < kNA; ++a) {
+                mbar_init(a_full(a), 4);   // the 4 level-0 warps of the tile wrote their A rows
+                mbar_init(a_empty(a), 1);  // tcgen05.commit: the MMAs reading A buffer a completed
+                if (a == 0) mbar_init(b_free, 1);  // table mode: tcgen05.commit before a core-block switch
+            }
+            for (int w = 0; w < 4; ++w)
+                for (int s = 0; s < kD; ++s) {
+                    mbar_init(d_full(w, s), kDfull1 ? 1 : kWarp);  // lane 0 of level-0 warp w after a __syncwarp (its delta stores)
+                    mbar_init(d_empty(w, s), 1);     // normal-equation warp 4+w read the slot
+                }
+            asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        }
+    }
+    // PDL: everything above touches only this CTA's shared memory and TMEM; the core, the
+    // index and the factors may have been written by the preceding grid
+    pdl_wait_trigger();
     // B = core (hi/lo tf32 split), K-major: Bt[(k0, j)][k1] = G'[k0][k1][j]
     int sG = 0;  // kF16: core scale exponent (max |G| over every block this launch reads)
     if constexpr (kF16) {
@@ -567,20 +608,6 @@ __global__ void __launch_bounds__(kThreads, 1) k_update_tc(const UpdateParams<fl
         sBlo[kmaj<KP>(c, k1)] = tf32_rna(v - hv);
     }
     }
-    if constexpr (NQ == 3) {
-        // packed J = 10 gathers write 8 of chunk 2's 16 bytes: the rest (row padding) stays zero
-        for (int i = threadIdx.x; i < kRing * 2 * kE; i += kThreads) {
-            const int sl = i / (2 * kE), k = (i / kE) % 2, u = i % kE;
-            float* c2 = reinterpret_cast<float*>(rowc(sl, k, 2, u));
-            c2[2] = 0.f;
-            c2[3] = 0.f;
-        }
-    }
-    if (warp == 0) {
-        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&misc[0])),
-                     "n"(SH::TCOLS));
-        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
-    }
     if (warp == 14) {
         // tiles of this CTA = sum of the iteration counts of its groups
         uint32_t n = 0;
@@ -592,28 +619,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_update_tc(const UpdateParams<fl
         }
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) n += __shfl_xor_sync(0xffffffffu, n, o);
-        if (lane == 0) {
-            misc[1] = n;
-            for (int s = 0; s < kRing; ++s) {
-                mbar_init(raw_full(s), 2 * kWarp);  // loader lanes: cp.async completion + plain arrive (x)
-                mbar_init(raw_empty(s), 4);         // the 4 level-0 warps of the tile (split: a1 to TMEM, a0/x to the stash)
-            }
-            for (int b = 0; b < kNT; ++b) {
-                mbar_init(acc_full(b), 1);   // tcgen05.commit
-                mbar_init(acc_empty(b), 4);  // level-0 warps done reading the accumulator
-            }
-            for (int a = 0; a < kNA; ++a) {
-                mbar_init(a_full(a), 4);   // the 4 level-0 warps of the tile wrote their A rows
-                mbar_init(a_empty(a), 1);  // tcgen05.commit: the MMAs reading A buffer a completed
-                if (a == 0) mbar_init(b_free, 1);  // table mode: tcgen05.commit before a core-block switch
-            }
-            for (int w = 0; w < 4; ++w)
-                for (int s = 0; s < kD; ++s) {
-                    mbar_init(d_full(w, s), kDfull1 ? 1 : kWarp);  // lane 0 of level-0 warp w after a __syncwarp (its delta stores)
-                    mbar_init(d_empty(w, s), 1);     // normal-equation warp 4+w read the slot
-                }
-            asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-        }
+        if (lane == 0) misc[1] = n;
     }
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -1345,7 +1351,7 @@ void launch_tc_g(const UpdateParams<float>& p, int grid, cudaStream_t st) {
     auto k = k_update_tc<J, LAST64, G0, TBL>;
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, Shape<J>::SMEM);
     cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
-    k<<<grid, kThreads, Shape<J>::SMEM, st>>>(p);
+    launch_pdl(k, grid, kThreads, Shape<J>::SMEM, st, p);
 }
 
 template <int J, bool LAST64>

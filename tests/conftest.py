@@ -27,7 +27,7 @@ def orc():
 _OPTION_DEFAULTS = [("policy", -1), ("tc", 1), ("l0_group", 1), ("pack_gathers", 0), ("rows_l1", -1),
                     ("tc_table", 1), ("smp", 1), ("smp_table", 2), ("seg_len", -1), ("exchange", 1),
                     ("graph", 1), ("sparse_core", -1), ("cache", 0), ("time_kernels", 0),
-                    ("emulate_world", 1), ("emulate_rank", 0), ("fin_inline", 0)]
+                    ("emulate_world", 1), ("emulate_rank", 0), ("fin_inline", 0), ("pdl", 0)]
 
 
 @pytest.fixture(autouse=True)

@@ -490,3 +490,35 @@ def test_inline_heavy_rows_bit_identical(pt, orc, name, scale, seg):
             orc.update_mode(t, m, n, cfg.lam)
         e = orc.error(t, m)
         assert abs(runs[1][1][it] - e) <= 1e-3 * e, (it, runs[1][1][it], e)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name,scale,seg", [("c2", 0.05, -1), ("c5", 0.0005, -1), ("c3", 0.002, -1), ("c1", 1.0, 8)])
+def test_pdl_bit_identical(pt, orc, name, scale, seg):
+    """Programmatic dependent launch (option pdl, off by default) only changes when the kernels of a
+    sweep start, not what they compute: three graph-replayed sweeps with the error read back give
+    the same factors and errors bit for bit with pdl = 0 and 1 (tensor-core kernel, table mode,
+    heavy-row finalize, error sums), and the trajectory is the oracle's."""
+    cfg = synth.config(name) if scale == 1.0 else synth.small(name, scale)
+    N = len(cfg.dims)
+    runs = {}
+    for pdl in (0, 1):
+        pt.ptucker_set_option("pdl", pdl)
+        init_cfg(pt, cfg, seg_len=seg)
+        errs = []
+        for it in range(3):
+            pt.ptucker_sweep()
+            errs.append(pt.ptucker_error())
+        runs[pdl] = ([pt.ptucker_get_factor(n).copy() for n in range(N)], errs)
+    pt.ptucker_set_option("pdl", 0)
+    for n in range(N):
+        assert np.array_equal(runs[0][0][n], runs[1][0][n]), n
+    assert runs[0][1] == runs[1][1]
+    coords, vals = synth.generate(cfg)
+    t = orc.Tensor(coords, vals, cfg.dims)
+    m = orc.init_model(cfg.dims, [cfg.J] * N, seed=0, prec=1 if cfg.dtype == "f64" else 0)
+    for it in range(3):
+        for n in range(N):
+            orc.update_mode(t, m, n, cfg.lam)
+        e = orc.error(t, m)
+        assert abs(runs[1][1][it] - e) <= 1e-3 * e, (it, runs[1][1][it], e)
