@@ -496,6 +496,11 @@ int policy_l64() {
     const int all = g.N >= 4 ? g.N - 2 : 1;
     if (g.policy == 3) return g.N >= 5 ? g.N - 3 : all;  // F32-C2 (order 5): all outer levels but the innermost's parent
     if (g.policy >= 0) return g.policy == 2 ? all : g.policy;
+    // automatic: order 5 with J = 5 (c4) takes F32-C2 -- J^3 instead of J^4 fp32 -> fp64
+    // conversions per entry, worst full-size row 2.5e-6 of the 1e-5 bound (F32-C: 1.1e-6),
+    // 2.60 against 2.74 ms per mode once its core reads go through the uniform datapath
+    // (profiles/r02/ab_c4_f32c2.txt); other order-5 J keep F32-C (no full-size evidence)
+    if (g.N == 5 && g.J == 5) return g.N - 3;
     return all;
 }
 

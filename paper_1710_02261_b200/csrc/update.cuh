@@ -32,11 +32,18 @@ namespace pt {
 // One copy per translation unit (static); filled by set_core_constant().
 static __constant__ __align__(16) unsigned char c_core[65536];
 
-// L64 = N - 3 at order 5 (policy F32-C2): the core from shared memory (LDS broadcast) -- in the
-// constant bank nvcc addressed it through a per-thread register there (LDC R, c[0x3][R]) instead
-// of the uniform datapath, and every core read became a per-thread constant load
+// L64 = N - 3 at order 5 (policy F32-C2).  With the core offset computed from the level-0 loop
+// counter nvcc addressed the constant bank through a per-thread register there
+// (LDC R, c[0x3][R]: every core read a per-thread constant load, 5.1 ms per c4 mode);
+// PT_C2_SMEM = 1 moved the core to shared memory for this policy (3.2 ms).  PT_C2_LOOP = 1
+// (default) keeps it in the constant bank and walks it with a pointer of its own, levels 0
+// and 1 as runtime loops: the reads are LDCU c[0x3][UR] again (2.60 ms; F32-C 2.74).
+// PT_C2_LOOP = 2 unrolls level 1 (same time, 5x the code).
 #ifndef PT_C2_SMEM
-#define PT_C2_SMEM 1
+#define PT_C2_SMEM 0
+#endif
+#ifndef PT_C2_LOOP
+#define PT_C2_LOOP 1
 #endif
 template <typename TS, int N, int J, int L64 = -1>
 struct CoreInConst {
@@ -190,6 +197,40 @@ __device__ __forceinline__ void compute_delta(const TS* __restrict__ g, const TF
         } else {
 #pragma unroll
             for (int k = 0; k < J; ++k) level0(k);
+        }
+    } else if constexpr (PT_C2_LOOP && N == 5 && L64 == N - 3 && sizeof(TS) == 4) {
+        // F32-C2 at order 5: levels 0 and 1 as runtime loops (a0[k0], a1[k1] from the staged
+        // rows), so the unrolled body is one level-2 block (J^3 + J^2 fp32 FMAs) whose core
+        // offset is a loop counter; same products in the same order as the unrolled level 1
+        constexpr int sub0 = ipow(J, N - 3) * GB, sub1 = ipow(J, N - 4) * GB;
+        constexpr int VN = Vec16<TS>::n;
+        constexpr int NQ = factor_ld(J, sizeof(TS)) * (int)sizeof(TS) / 16;  // Stage<TS, N, J>::NQ
+        const TS* a1row = a0row + NQ * kWarp * VN;
+#pragma unroll
+        for (int j = 0; j < J; ++j) d[j] = TO(0);
+        static_assert(sub0 == J * sub1, "level-1 blocks are contiguous");
+        const TS* gp = g;  // walks the core block by block (its own counter: uniform datapath)
+        const TS* const gend = g + J * sub0;
+#pragma unroll 1
+        for (int k0 = 0; gp != gend; ++k0) {
+            TO t1[J];
+#pragma unroll
+            for (int j = 0; j < J; ++j) t1[j] = TO(0);
+#if PT_C2_LOOP == 2
+#pragma unroll
+#else
+#pragma unroll 1
+#endif
+            for (int k1 = 0; k1 < J; ++k1, gp += sub1) {
+                TF t2[J];
+                ttv_level<TS, TF, N, J, L64, 2>(gp, a_in, a_out, t2);
+                const TO ak1 = TO(a1row[(k1 / VN) * (kWarp * VN) + (k1 % VN)]);
+#pragma unroll
+                for (int j = 0; j < J; ++j) t1[j] = fma(ak1, TO(t2[j]), t1[j]);
+            }
+            const TO ak0 = TO(a0row[(k0 / VN) * (kWarp * VN) + (k0 % VN)]);
+#pragma unroll
+            for (int j = 0; j < J; ++j) d[j] = fma(ak0, t1[j], d[j]);
         }
     } else {
         constexpr int sub = ipow(J, N - 3) * GB;

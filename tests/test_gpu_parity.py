@@ -163,18 +163,20 @@ def test_mode_update_l0_kahan(pt, orc, name, scale):
     print(f"{name}@{scale} l0_group 0 worst row rel err init {w0:.2e} mid {w1:.2e}")
 
 
+@pytest.mark.parametrize("policy,label", [(3, "F32-C2"), (-1, "F32-C2"), (2, "F32-C")])
 @pytest.mark.parametrize("scale,seg", [(0.001, 256), (0.005, 256), (0.005, 7)])
-def test_mode_update_c4_f32c2(pt, orc, scale, seg):
-    """Policy 3 (F32-C2, order 5): the level next to the innermost in fp32 (J^3 instead of J^4
-    fp32 -> fp64 conversions per entry), the outer ones in fp64 -- held to the same 1e-5 per
-    row as the automatic F32-C, at the init state (the worst case) and mid-trajectory."""
+def test_mode_update_c4_f32c2(pt, orc, scale, seg, policy, label):
+    """Order 5: F32-C2 (policy 3, and the automatic choice for the c4 shape: the level next to
+    the innermost in fp32, J^3 instead of J^4 fp32 -> fp64 conversions per entry, the outer
+    ones in fp64) and F32-C (policy 2, every outer level in fp64) are both held to 1e-5 per
+    row, at the init state (the worst case) and mid-trajectory."""
     cfg = synth.small("c4", scale)
-    coords, vals = init_cfg(pt, cfg, policy=3, seg_len=seg)
-    assert pt.ptucker_info()["policy"] == "F32-C2"
+    coords, vals = init_cfg(pt, cfg, policy=policy, seg_len=seg)
+    assert pt.ptucker_info()["policy"] == label
     t = orc.Tensor(coords, vals, cfg.dims)
     w0 = mode_update_parity(pt, orc, t, cfg, 1e-5, sweeps=0)
     w1 = mode_update_parity(pt, orc, t, cfg, 1e-5, sweeps=1)
-    print(f"c4@{scale} seg={seg} F32-C2 worst row rel err init {w0:.2e} mid {w1:.2e}")
+    print(f"c4@{scale} seg={seg} {label} worst row rel err init {w0:.2e} mid {w1:.2e}")
 
 
 @pytest.mark.parametrize("tc_table", [0, 1])
