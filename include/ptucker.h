@@ -185,7 +185,7 @@ int ptucker_get_partition(int32_t n, int64_t* bounds);
 
 /* Options (set after init unless noted):
  *  "policy"       precision of the fp32 contraction: -1 = automatic
- *                 (default: every outer TTV stage in fp64), 0 = F32-A (all fp32), 1 = F32-B
+ *                 (default: every outer TTV stage in fp64; F32-C2 for N = 5, J = 5), 0 = F32-A (all fp32), 1 = F32-B
  *                 (outermost stage fp64), 2 = F32-C (all outer stages fp64), 3 = F32-C2 (order 5:
  *                 every outer stage in fp64 but the innermost one's parent: J^3 instead of J^4
  *                 fp32 -> fp64 conversions per entry; other orders: as 2)
