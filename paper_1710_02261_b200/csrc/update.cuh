@@ -38,7 +38,8 @@ static __constant__ __align__(16) unsigned char c_core[65536];
 // PT_C2_SMEM = 1 moved the core to shared memory for this policy (3.2 ms).  PT_C2_LOOP = 1
 // (default) keeps it in the constant bank and walks it with a pointer of its own, levels 0
 // and 1 as runtime loops: the reads are LDCU c[0x3][UR] again (2.60 ms; F32-C 2.74).
-// PT_C2_LOOP = 2 unrolls level 1 (same time, 5x the code).
+// PT_C2_LOOP = 2 unrolls level 1 (same time, 5x the code); 3 unrolls levels 0 and 1 (LDCU.128
+// reads, but 124 KB of code and spills: 3.15 ms).
 #ifndef PT_C2_SMEM
 #define PT_C2_SMEM 0
 #endif
@@ -211,12 +212,16 @@ __device__ __forceinline__ void compute_delta(const TS* __restrict__ g, const TF
         static_assert(sub0 == J * sub1, "level-1 blocks are contiguous");
         const TS* gp = g;  // walks the core block by block (its own counter: uniform datapath)
         const TS* const gend = g + J * sub0;
+#if PT_C2_LOOP == 3
+#pragma unroll
+#else
 #pragma unroll 1
-        for (int k0 = 0; gp != gend; ++k0) {
+#endif
+        for (int k0 = 0; PT_C2_LOOP == 3 ? k0 < J : gp != gend; ++k0) {
             TO t1[J];
 #pragma unroll
             for (int j = 0; j < J; ++j) t1[j] = TO(0);
-#if PT_C2_LOOP == 2
+#if PT_C2_LOOP >= 2
 #pragma unroll
 #else
 #pragma unroll 1
